@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark of the encrypted-LR fast matmul hot path (arXiv 2204.05496).
+
+Workload (default, BASELINE.json configs[3] = "C4"): 256 individuals x 40,000
+features x 11 classes, N = 8192, production twin moduli (t0 = 1073872897,
+t1 = 114689; 6 + 4 31-bit primes). One step = one matmul over the whole batch
+(every (individual, class) pair: chunk products, 13 keyed rotations, mask,
+packed accumulation, bias).
+
+Arms:
+  ours (default)      CUDA path, value = device-resident inputs (u32 in HBM),
+                      e2e = C-ABI call with host u64 buffers (H2D + D2H timed).
+  --impl reference    the reference's own CPU implementation (oracle/_ref,
+                      compiled from /root/reference in the build container)
+                      on the host cores, bounded sample per step.
+
+Multi-GPU (torchrun): individuals shard across ranks (weak scaling, no
+data-path collective; the packed partials would be combined by a mod-q add
+of ~0.65 MB per rank). Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+T0, T1, T1_16K = 1073872897, 114689, 163841
+CONFIGS = {
+    # name: (R, f, cols, N, p_feat, w_sigma)
+    "c1": (1, 1000, 11, 8192, 0.05, 0.1),
+    "c2": (1, 10000, 11, 8192, 0.05, 0.1),
+    "c3": (1, 40000, 11, 8192, 0.03, 0.05),
+    "c4": (256, 40000, 11, 8192, 0.03, 0.05),
+    "c5": (4096, 40000, 33, 16384, 0.03, 0.05),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--rows", type=int, default=0, help="override individuals per rank")
+    ap.add_argument("--batch-pairs", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--latency", action="store_true", help="also time a single-individual (C3) call")
+    return ap.parse_args()
+
+
+def q_chain(n: int, t: int):
+    """bfv::default_q_primes (params.cpp:84-104) for n >= 4096."""
+    count = 6 if t >= (1 << 25) else 4
+    two_n = 2 * n
+    c = ((((1 << 31) - 2) // two_n) * two_n) + 1
+    out = []
+    while len(out) < count:
+        if c != t and _is_prime(c):
+            out.append(c)
+        c -= two_n
+    return out
+
+
+def _is_prime(v: int) -> bool:
+    if v < 2:
+        return False
+    for p in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        if v % p == 0:
+            return v == p
+    d, r = v - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        r += 1
+    for a in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        x = pow(a, d, v)
+        if x in (1, v - 1):
+            continue
+        for _ in range(r - 1):
+            x = x * x % v
+            if x == v - 1:
+                break
+        else:
+            return False
+    return True
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        cmd = ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+               "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 8:
+                for k, nm in enumerate(names):
+                    if r[4 + k].lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ reference
+def reference_sample(cfg_name: str, rows: int | None = None, threads: int = 0):
+    """Time the reference CPU path (oracle/_ref) on a bounded sample of the
+    workload. Returns (inferences/s, sample description, threads, seconds)."""
+    from oracle.oracle import Reference, TwinParams, ref_available
+    from tests.helpers import synthetic
+
+    R, f, cols, n, pf, ws = CONFIGS[cfg_name]
+    if not ref_available():
+        return None
+    nthreads = threads or os.cpu_count() or 1
+    r = rows or max(1, min(R, nthreads))
+    p = TwinParams(n=n, t0=T0, t1=T1 if n < 16384 else T1_16K, sec=128)
+    ref = Reference(p, key_seed=1, enc_seed=2)
+    x, w, b = synthetic(r, f, cols, pf, ws)
+    ref.encode_inputs(x)
+    ref.set_weights(w)
+    ref.set_bias(b)
+    _, _, secs = ref.matmul(r, cols, threads=nthreads, export=False)
+    return r / secs, f"{r} individuals x {f} features x {cols} classes (N={n}) per step", nthreads, secs, ref
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    R, f, cols, n, _, _ = CONFIGS[args.config]
+    res = reference_sample(args.config)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libheiref.so not built (needs /root/reference at build time)"}))
+        return
+    rate, sample, threads, _, ref = res
+    r = max(1, min(R, threads))
+    times = []
+    for s in range(args.warmup + args.steps):
+        _, _, secs = ref.matmul(r, cols, threads=threads, export=False)
+        if s >= args.warmup:
+            times.append(secs)
+    v = r * len(times) / sum(times)
+    line = {"metric": "encrypted LR inferences/sec at 40k features", "value": v, "unit": "inferences/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.config}: {R}x{f}x{cols} N={n}", "sample_rows_per_step": r},
+            "cpu_baseline": {"value": v, "unit": "inferences/s", "cores": threads, "kind": "reference", "sample": sample},
+            "e2e": {"value": v, "unit": "inferences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------ ours
+def make_server(n, device, seed=1):
+    """Evaluate-only server with seeded uniform key material (the kernels are
+    data-oblivious; real encryptions are exercised by tests/)."""
+    from paper_2204_05496_b200 import GpuTwinServer, ScalingConfig
+
+    t1 = T1 if n < 16384 else T1_16K
+    q0, q1 = q_chain(n, T0), q_chain(n, t1)
+    L = [len(q0), len(q1)]
+    q = np.array(q0 + q1, dtype=np.uint64)
+    two_n = 2 * n
+    elts = sorted([pow(3, 1 << s, two_n) for s in range(int(np.log2(n)) - 1)] + [two_n - 1])
+    rng = np.random.default_rng(seed)
+    gks = []
+    for b, qb in enumerate((q0, q1)):
+        Lb = len(qb)
+        g = np.empty((len(elts), Lb, 2, Lb, n), dtype=np.uint64)
+        for i, qi in enumerate(qb):
+            g[:, :, :, i, :] = rng.integers(0, qi, size=(len(elts), Lb, 2, n), dtype=np.uint64)
+        gks.append(g)
+    srv = GpuTwinServer(n, (T0, t1), L, q, elts, gks, ScalingConfig(), device=device)
+    return srv, q0, q1
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    from paper_2204_05496_b200 import encode_weights, matmul, matmul_device, native
+    from tests.helpers import synthetic
+
+    R_total, f, cols, n, pf, ws = CONFIGS[args.config]
+    R = args.rows or R_total  # per rank (weak scaling: every rank gets the full per-GPU batch)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    srv, q0, q1 = make_server(n, local)
+    if args.batch_pairs:
+        srv.set_batch_pairs(args.batch_pairs)
+    kc = (f + n - 1) // n
+    P = len(q0) + len(q1)
+    ctw = 2 * P * n
+    _, w, b = synthetic(1, f, cols, pf, ws)
+    ew = encode_weights(srv, w)
+    # device-resident inputs: uniform residues per (part, prime) slab
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    d_in = torch.empty((R * kc, ctw), dtype=torch.int32, device=dev)
+    polys = []
+    for bi, qb in enumerate((q0, q1)):
+        for part in range(2):
+            polys += list(qb)
+    for poly, qi in enumerate(polys):
+        d_in[:, poly * n:(poly + 1) * n] = torch.randint(0, qi, (R * kc, n), generator=g, device=dev, dtype=torch.int64).to(torch.int32)
+    C_ = (R * cols + n - 1) // n
+    d_out = torch.empty((C_, ctw), dtype=torch.int32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        matmul_device(srv, d_in.data_ptr(), R, ew, b, d_out.data_ptr(), stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    native.reset_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = native.launch_count()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * R / (ms / 1000.0)
+
+    # e2e: host u64 (pinned) inputs through the C ABI, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        h_in = torch.empty((R, kc, ctw), dtype=torch.int64, pin_memory=True)
+        h_in.copy_(d_in.view(R, kc, ctw).to(torch.int64).cpu())
+        h_np = h_in.numpy().view(np.uint64)
+        matmul(srv, h_np, ew, b)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_steps = max(1, min(args.steps, 3))
+        for _ in range(e2e_steps):
+            out, _ = matmul(srv, h_np, ew, b)
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        e2e = {"value": world * R / e2e_s, "unit": "inferences/s", "h2d_bytes_per_step": int(h_np.nbytes),
+               "d2h_bytes_per_step": int(out.nbytes), "ms_per_step": 1000 * e2e_s}
+
+    lat = None
+    if args.latency and rank == 0:
+        # single individual, 40k features x 11 classes (C3 shape), device-resident
+        d1 = d_in[:kc].contiguous()
+        o1 = torch.empty((1, ctw), dtype=torch.int32, device=dev)
+        for _ in range(3):
+            matmul_device(srv, d1.data_ptr(), 1, ew, b, o1.data_ptr(), stream.cuda_stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(10):
+            matmul_device(srv, d1.data_ptr(), 1, ew, b, o1.data_ptr(), stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        lat = e0.elapsed_time(e1) / 10
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            res = reference_sample(args.config)
+            if res:
+                rate, sample, threads, secs, _ = res
+                cpu = {"value": rate, "unit": "inferences/s", "cores": threads, "kind": "reference", "sample": sample,
+                       "seconds": secs}
+        except Exception as e:  # report, never fail the bench on the CPU leg
+            cpu = {"error": str(e)}
+    line = {
+        "metric": "encrypted LR inferences/sec at 40k features",
+        "value": value, "unit": "inferences/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {R} individuals/rank x {f} features x {cols} classes, N={n}, "
+                               f"twin t=({T0},{T1 if n < 16384 else T1_16K}), L=({len(q0)},{len(q1)})",
+                   "inputs": "uniform residues in HBM (kernels are data-oblivious); inputs > L2 (no flush needed)",
+                   "parallelism": f"dp{world} (individual sharding)"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    if lat is not None:
+        line["latency_ms_single_individual"] = lat
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,147 @@
+/* heinfer_b200 — C ABI of the B200-native encrypted-LR matmul hot path.
+ *
+ * Drop-in boundary for the reference's hei::matmul entry points
+ * (/root/reference/proj/include/hei/matmul/matmul.hpp). Plain pointers and
+ * sizes only; every residue array uses the reference's own u64 values and the
+ * flat layouts below, so the C++ adapter only flattens
+ * std::vector<uint64_t> polynomials.
+ *
+ * Layouts (N = ring degree, L_b = primes of branch b, branch 0 = t0):
+ *   twin ciphertext   [branch 2][part 2][prime L_b][N] u64
+ *   twin plain        [branch 2][prime L_b][N] u64
+ *   inputs            [row][chunk k][twin ciphertext]
+ *   prepared weights  [col j][chunk k][twin plain]   (EncodedWeights values)
+ *   packed output     [ct c][twin ciphertext], eval form
+ *   galois keys (b)   [elt, ascending][l][part][i][N] u64, eval form
+ *                     (GaloisKey::rows[l][part][i].vals, keys.hpp:37-43)
+ *
+ * Errors: every entry point returns HEI_OK or the code of the reference
+ * exception it replaces (hei/util/errors.hpp:13-53); hei_gpu_last_error()
+ * returns the message of the last failure on the calling thread.
+ */
+#ifndef HEINFER_B200_H
+#define HEINFER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HEI_OK 0
+#define HEI_PARAM_ERROR 1 /* hei::ParamError */
+#define HEI_KEY_ERROR 2   /* hei::KeyError   */
+#define HEI_RANGE_ERROR 3 /* hei::RangeError */
+#define HEI_NOISE_ERROR 4 /* hei::NoiseError */
+#define HEI_CODEC_ERROR 5 /* hei::CodecError */
+#define HEI_CUDA_ERROR 6  /* device failure (no reference counterpart) */
+#define HEI_INTERNAL 9
+
+#define HEI_FORM_COEFF 0 /* ring::PolyForm::coeff (poly.hpp:13) */
+#define HEI_FORM_EVAL 1  /* ring::PolyForm::eval */
+
+typedef struct hei_gpu_ctx hei_gpu_ctx;         /* TwinContext + server keys on one device */
+typedef struct hei_gpu_weights hei_gpu_weights; /* EncodedWeights resident in HBM */
+typedef struct hei_gpu_stream hei_gpu_stream;   /* MatmulStream */
+typedef struct hei_gpu_prng hei_gpu_prng;       /* util::Prng replay (rng.hpp:19-68) */
+
+/* matmul::OpCounters (matmul.hpp:21-27) */
+typedef struct {
+  uint64_t mul_plain_count;
+  uint64_t rotation_count;
+  uint64_t add_count;
+  uint64_t ciphertexts_in;
+  uint64_t ciphertexts_out;
+} hei_op_counters;
+
+/* fpcrt::TwinParams (twin.hpp:90-95) + the derived q chains
+ * (bfv::default_q_primes, params.cpp:84-104). */
+typedef struct {
+  uint32_t n;
+  uint64_t t[2];
+  uint32_t L[2];
+  const uint64_t* q; /* [L0 + L1] */
+  uint32_t s_x, s_w, input_int_bits;
+  int device;
+} hei_twin_desc;
+
+const char* hei_gpu_last_error(void);
+const char* hei_gpu_version(void);
+
+/* Context + keys. Replaces TwinContext / server_backend (twin.hpp:119-145).
+ * Validates like EncryptionParams::validate (params.cpp:27-66). */
+int hei_gpu_ctx_create(const hei_twin_desc* desc, hei_gpu_ctx** out);
+void hei_gpu_ctx_destroy(hei_gpu_ctx* ctx);
+/* GaloisKeySet of one branch (keys.hpp:44-49); elts ascending. */
+int hei_gpu_upload_galois_keys(hei_gpu_ctx* ctx, uint32_t branch, uint32_t count,
+                               const uint64_t* elts, const uint64_t* rows);
+/* PublicKey of one branch, coeff form [2][L][N] (keys.hpp:28-32); needed only
+ * by the standard (baseline) algorithm, which encrypts internally. */
+int hei_gpu_upload_public_key(hei_gpu_ctx* ctx, uint32_t branch, const uint64_t* pk);
+
+/* Weights. hei_gpu_weights_create uploads EncodedWeights values as produced by
+ * matmul::encode_weights (matmul.cpp:225-246); hei_gpu_weights_encode runs
+ * encode_weights itself on the device from the scaled f x cols matrix. */
+int hei_gpu_weights_create(hei_gpu_ctx* ctx, const uint64_t* prepared, uint64_t f,
+                           uint64_t cols, hei_gpu_weights** out);
+int hei_gpu_weights_encode(hei_gpu_ctx* ctx, const int64_t* w, uint64_t f, uint64_t cols,
+                           hei_gpu_weights** out);
+void hei_gpu_weights_destroy(hei_gpu_weights* w);
+
+/* matmul::matmul (matmul.cpp:381-397). Host buffers; inputs in `form`;
+ * bias = EncodedBias::scaled [cols]; out = PackedResult cts (eval form). */
+int hei_gpu_matmul(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint64_t* inputs,
+                   int form, uint64_t rows, const int64_t* bias, uint64_t* out,
+                   hei_op_counters* counters);
+
+/* Same call on device-resident u32 residues (the HBM-resident bench path):
+ * d_inputs [row][k][twin ct] u32, d_out [C][twin ct] u32, both device
+ * pointers; `stream` is a cudaStream_t (NULL = legacy default). */
+int hei_gpu_matmul_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint32_t* d_inputs,
+                          int form, uint64_t rows, const int64_t* bias, uint32_t* d_out,
+                          hei_op_counters* counters, void* stream);
+
+/* MatmulStream (matmul.hpp:83-114): rows in any order, each once. */
+int hei_gpu_stream_create(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const int64_t* bias,
+                          uint64_t total_rows, hei_gpu_stream** out);
+int hei_gpu_stream_push_row(hei_gpu_stream* s, uint64_t row_index, const uint64_t* chunks,
+                            int form);
+int hei_gpu_stream_finish(hei_gpu_stream* s, uint64_t* out, hei_op_counters* counters);
+void hei_gpu_stream_destroy(hei_gpu_stream* s);
+
+/* matmul::baseline_matmul (matmul.cpp:415-486). Encrypts every feature column
+ * with the public key; encryption randomness is replayed from one util::Prng
+ * per branch, exactly as BfvBackend::encrypt draws it (context.cpp:262-303).
+ * out [ceil(rows/N)][cols][twin ct] eval form. */
+int hei_gpu_prng_create(uint64_t seed, hei_gpu_prng** out);
+void hei_gpu_prng_destroy(hei_gpu_prng* p);
+int hei_gpu_baseline_matmul(hei_gpu_ctx* ctx, const int64_t* x, uint64_t rows, uint64_t f,
+                            const int64_t* w, uint64_t cols, const int64_t* bias,
+                            hei_gpu_prng* rng0, hei_gpu_prng* rng1, uint64_t* out,
+                            hei_op_counters* counters);
+
+/* Closed forms (matmul.cpp:172-199). */
+int hei_proposed_counts(uint64_t rows, uint64_t cols, uint64_t f, uint32_t n, hei_op_counters* c);
+int hei_baseline_counts(uint64_t rows, uint64_t cols, uint64_t f, uint32_t n, hei_op_counters* c);
+
+/* ---- kernel-level seam (the reference's kernels::Kernels table,
+ *      modops.hpp:29-51), batched over `count` polynomials of one prime. ---- */
+int hei_gpu_ntt(hei_gpu_ctx* ctx, uint32_t branch, uint32_t prime, uint64_t* polys,
+                uint64_t count, int inverse);
+/* One keyed automorphism on a single-branch eval-form ciphertext [2][L][N]
+ * (BfvContext::apply_galois, context.cpp:428-507). */
+int hei_gpu_apply_galois(hei_gpu_ctx* ctx, uint32_t branch, uint64_t elt, const uint64_t* in,
+                         uint64_t* out);
+/* HeBackend::sum_all_slots on twin ciphertexts (backend.cpp:63-73). */
+int hei_gpu_sum_all_slots(hei_gpu_ctx* ctx, const uint64_t* in, uint64_t* out, uint64_t count);
+/* Kernel launches issued by this thread since the last reset. */
+uint64_t hei_gpu_launch_count(void);
+void hei_gpu_reset_launch_count(void);
+/* Tuning: pairs per device batch (0 = automatic). */
+void hei_gpu_set_batch_pairs(hei_gpu_ctx* ctx, uint64_t pairs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

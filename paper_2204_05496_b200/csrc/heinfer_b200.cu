@@ -1,0 +1,1275 @@
+// heinfer_b200: B200-native (sm_100a) encrypted-LR matmul hot path.
+//
+// Implements the C ABI of include/heinfer_b200.h. The reference path being
+// replaced is hei::matmul::MatmulStream / matmul / baseline_matmul
+// (/root/reference/proj/src/matmul/matmul.cpp:256-486) and everything it calls
+// on the server side: TwinBackend (fpcrt/twin.cpp:462-512), HeBackend
+// sum_all_slots (bfv/backend.cpp:63-73), BfvContext::mul_plain_inplace /
+// add_plain_inplace / apply_galois (bfv/context.cpp:393-507) and the kernels
+// table (kernels/modops_scalar.cpp, modops_avx2.cpp).
+//
+// Device layout: every residue is u32 (all q_i, t_b < 2^31). A twin
+// ciphertext is [branch][part][prime][N] exactly as the host layout, so the
+// flat "poly index" of (branch b, part p, prime i) is
+//   (b ? 2*L0 : 0) + p*L_b + i
+// and the flat prime index gp = (b ? L0 : 0) + i.
+//
+// Pipeline per batch of (row, class) pairs:
+//   k_chunk_dot     dot = sum_k chunk_k (.) W[j][k]                 (HBM)
+//   13/14 x { k_rot_digits     digit_l = INTT_l(sigma(c1)_l)
+//             k_rot_keyswitch  acc_i = sum_l NTT_i(digit_l mod q_i) (.) K[l][i],
+//                              dot <- dot + (acc0 + sigma(c0), acc1) }
+//   k_mask_acc      packed[g/N] += mask_{g mod N} (.) dot           (u64 RED)
+// and once per call k_finish (mod-q reduce + bias add_plain).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/heinfer_b200.h"
+#include "modmath.cuh"
+
+using namespace heb;
+
+namespace {
+
+// ---------------------------------------------------------------- errors
+thread_local std::string g_err;
+thread_local uint64_t g_launches = 0;
+
+struct HeiError {
+  int code;
+  std::string msg;
+};
+[[noreturn]] void raise(int code, const std::string& msg) { throw HeiError{code, msg}; }
+
+#define CU(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess)                                                           \
+      raise(HEI_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+#define LAUNCHED()                    \
+  do {                                \
+    ++g_launches;                     \
+    CU(cudaGetLastError());           \
+  } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HEI_OK;
+  } catch (const HeiError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return HEI_INTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HEI_INTERNAL;
+  }
+}
+
+// ------------------------------------------------ host modular helpers (setup)
+typedef unsigned __int128 u128;
+uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)((u128)a * b % q); }
+uint64_t powmod(uint64_t b, uint64_t e, uint64_t q) {
+  uint64_t r = 1 % q;
+  b %= q;
+  while (e) {
+    if (e & 1) r = mulmod(r, b, q);
+    b = mulmod(b, b, q);
+    e >>= 1;
+  }
+  return r;
+}
+uint64_t invmod(uint64_t a, uint64_t q) {
+  int64_t t = 0, nt = 1, r = (int64_t)q, nr = (int64_t)(a % q);
+  while (nr) {
+    int64_t k = r / nr, x = t - k * nt;
+    t = nt;
+    nt = x;
+    x = r - k * nr;
+    r = nr;
+    nr = x;
+  }
+  if (r != 1) raise(HEI_PARAM_ERROR, "inv_mod: value not invertible");
+  return (uint64_t)(t < 0 ? t + (int64_t)q : t);
+}
+// Deterministic Miller-Rabin (ring/modulus.cpp:24-53).
+bool is_prime(uint64_t v) {
+  static const uint64_t W[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  if (v < 2) return false;
+  for (uint64_t p : W) {
+    if (v == p) return true;
+    if (v % p == 0) return false;
+  }
+  uint64_t d = v - 1;
+  int r = 0;
+  while (!(d & 1)) d >>= 1, ++r;
+  for (uint64_t a : W) {
+    uint64_t x = powmod(a, d, v);
+    if (x == 1 || x == v - 1) continue;
+    bool wit = true;
+    for (int i = 1; i < r; ++i) {
+      x = mulmod(x, x, v);
+      if (x == v - 1) {
+        wit = false;
+        break;
+      }
+    }
+    if (wit) return false;
+  }
+  return true;
+}
+// Smallest-witness primitive 2n-th root (ring/modulus.cpp:73-85).
+uint64_t root_2n(uint32_t n, uint64_t q) {
+  const uint64_t e = (q - 1) / (2ull * n);
+  for (uint64_t c = 2; c < q; ++c) {
+    uint64_t w = powmod(c, e, q);
+    if (powmod(w, n, q) == q - 1) return w;
+  }
+  raise(HEI_PARAM_ERROR, "no primitive root found");
+}
+uint32_t rev_bits(uint32_t v, uint32_t bits) {
+  uint32_t r = 0;
+  for (uint32_t i = 0; i < bits; ++i) r = (r << 1) | ((v >> i) & 1u);
+  return r;
+}
+uint32_t shoup32(uint64_t w, uint64_t q) { return (uint32_t)((w << 32) / q); }
+int max_q_bits_128(uint32_t n) {
+  switch (n) {
+    case 1024: return 27;
+    case 2048: return 54;
+    case 4096: return 109;
+    case 8192: return 218;
+    case 16384: return 438;
+    case 32768: return 881;
+    default: return 0;
+  }
+}
+
+// ------------------------------------------------------------ device structs
+constexpr int kMaxPrimes = 16;
+constexpr int kMaxElts = 16;
+
+struct PrimeInfo {
+  uint32_t q;
+  uint32_t b, i;           // branch, index within branch
+  uint32_t poly0, poly1;   // poly index of part 0 / part 1 inside a twin ct
+  uint32_t first;          // flat index of prime 0 of this branch
+  uint32_t L;              // primes in this branch
+  uint32_t fast_reduce;    // digits of this branch reduce mod q with one csub
+  uint2 ninv, last;        // inverse-NTT scaling constants
+  uint2 delta;             // floor(Q/t) mod q (context.cpp:39-46)
+  uint64_t mu;             // floor(2^64 / q) for Barrett
+};
+struct BranchInfo {
+  uint32_t t;
+  uint32_t L, first;
+  uint2 ninv, last;  // mod-t inverse NTT constants
+};
+struct Geo {
+  uint32_t n, logn, P, ct_words, pt_words;
+  uint32_t L[2];
+  PrimeInfo pr[kMaxPrimes];
+  BranchInfo br[2];
+  const uint2* fwd;  // [P + 2][n]: q primes then t0, t1
+  const uint2* inv;
+  const uint32_t* index_map;
+};
+
+// ----------------------------------------------------------------- kernels
+__global__ void k_narrow(Geo g, const uint64_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t cts,
+                         uint32_t* err) {
+  const uint64_t total = cts * g.ct_words;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t poly = (uint32_t)((x % g.ct_words) / g.n);
+    // poly -> prime: branch 0 polys [0, 2L0), branch 1 after
+    const uint32_t L0 = g.L[0];
+    uint32_t gp = poly < 2 * L0 ? (poly % L0) : L0 + (poly - 2 * L0) % g.L[1];
+    const uint64_t v = in[x];
+    if (v >= g.pr[gp].q) *err = 1;
+    out[x] = (uint32_t)v;
+  }
+}
+
+__global__ void k_widen(const uint32_t* __restrict__ in, uint64_t* __restrict__ out, uint64_t total) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x)
+    out[x] = in[x];
+}
+
+__device__ __forceinline__ uint32_t poly_prime(const Geo& g, uint32_t poly) {
+  const uint32_t L0 = g.L[0];
+  return poly < 2 * L0 ? (poly % L0) : L0 + (poly - 2 * L0) % g.L[1];
+}
+
+// Forward (or inverse) NTT of whole twin ciphertexts in place: block per poly.
+__global__ void k_ct_ntt(Geo g, uint32_t* __restrict__ cts, int inverse) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = g.n, polys = 2 * g.P;
+  const uint64_t poly_g = blockIdx.x;
+  const uint32_t poly = (uint32_t)(poly_g % polys);
+  const uint32_t gp = poly_prime(g, poly);
+  uint32_t* p = cts + poly_g * n;
+  const PrimeInfo& pr = g.pr[gp];
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = p[x];
+  __syncthreads();
+  if (inverse) ntt_inv_smem(sm, g.inv + (size_t)gp * n, pr.q, n, g.logn, pr.last, pr.ninv);
+  else ntt_fwd_smem(sm, g.fwd + (size_t)gp * n, pr.q, n, g.logn);
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) p[x] = sm[x];
+}
+
+// Batched NTT of `count` polys of one flat prime (kernel-level seam).
+__global__ void k_poly_ntt(Geo g, uint32_t gp, uint32_t* __restrict__ polys, int inverse) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = g.n;
+  uint32_t* p = polys + (uint64_t)blockIdx.x * n;
+  const PrimeInfo& pr = g.pr[gp];
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = p[x];
+  __syncthreads();
+  if (inverse) ntt_inv_smem(sm, g.inv + (size_t)gp * n, pr.q, n, g.logn, pr.last, pr.ninv);
+  else ntt_fwd_smem(sm, g.fwd + (size_t)gp * n, pr.q, n, g.logn);
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) p[x] = sm[x];
+}
+
+// dot[pair] = sum_k in[row][k] (.) W[j][k]   (push_row, matmul.cpp:318-326)
+// One block per (pair, poly); pairs of the batch map to (slot s = pair / cols,
+// j = pair % cols) and input rows are stored per batch slot.
+__global__ void k_chunk_dot(Geo g, const uint32_t* __restrict__ in, const uint2* __restrict__ W, uint32_t cols,
+                            uint32_t kc, uint32_t* __restrict__ dot) {
+  const uint32_t n = g.n, polys = 2 * g.P;
+  const uint32_t pair = blockIdx.x / polys, poly = blockIdx.x % polys;
+  const uint32_t s = pair / cols, j = pair % cols;
+  const uint32_t gp = poly_prime(g, poly);
+  const uint32_t q = g.pr[gp].q;
+  const uint32_t* src = in + ((uint64_t)s * kc * g.ct_words) + (uint64_t)poly * n;
+  const uint2* wj = W + ((uint64_t)j * kc * g.pt_words) + (uint64_t)gp * n;
+  uint32_t* dst = dot + (uint64_t)pair * g.ct_words + (uint64_t)poly * n;
+  for (uint32_t x = threadIdx.x * 4; x < n; x += blockDim.x * 4) {
+    uint32_t acc[4] = {0, 0, 0, 0};
+    for (uint32_t k = 0; k < kc; ++k) {
+      const uint4 a = *reinterpret_cast<const uint4*>(src + (uint64_t)k * g.ct_words + x);
+      const uint4 w01 = *reinterpret_cast<const uint4*>(wj + (uint64_t)k * g.pt_words + x);
+      const uint4 w23 = *reinterpret_cast<const uint4*>(wj + (uint64_t)k * g.pt_words + x + 2);
+      acc[0] = add_mod(acc[0], mul_shoup(a.x, w01.x, w01.y, q), q);
+      acc[1] = add_mod(acc[1], mul_shoup(a.y, w01.z, w01.w, q), q);
+      acc[2] = add_mod(acc[2], mul_shoup(a.z, w23.x, w23.y, q), q);
+      acc[3] = add_mod(acc[3], mul_shoup(a.w, w23.z, w23.w, q), q);
+    }
+    *reinterpret_cast<uint4*>(dst + x) = make_uint4(acc[0], acc[1], acc[2], acc[3]);
+  }
+}
+
+// digit_l = INTT_l(sigma(c1)_l), block per (pair, gp)  (context.cpp:455-459)
+__global__ void k_rot_digits(Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ perm,
+                             uint32_t* __restrict__ digits) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = g.n;
+  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = c1[__ldg(&perm[x])];
+  __syncthreads();
+  ntt_inv_smem(sm, g.inv + (size_t)gp * n, pr.q, n, g.logn, pr.last, pr.ninv);
+  uint32_t* d = digits + ((uint64_t)pair * g.P + gp) * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) d[x] = sm[x];
+}
+
+// Key switch for output prime i of branch b plus the fold add
+// (context.cpp:467-506, backend.cpp:65-68):
+//   acc_{0,1} = sum_l NTT_i(digit_l mod q_i) (.) K[l][{0,1}][i]
+//   fold: out0 = c0 + sigma(c0) + acc0, out1 = c1 + acc1
+//   else: out0 = sigma(c0) + acc0,      out1 = acc1
+// The l == i term needs no transform: NTT_i(INTT_i(x)) = x exactly.
+// Keys: K[e] laid out [i][l][part][n] (val, shoup).
+__global__ void k_rot_keyswitch(Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ digits,
+                                const uint32_t* __restrict__ perm, const uint2* __restrict__ key0,
+                                const uint2* __restrict__ key1, uint32_t* __restrict__ out, int fold) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = g.n;
+  uint32_t* work = sm;
+  uint32_t* acc0 = sm + n;
+  uint32_t* acc1 = sm + 2 * n;
+  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t q = pr.q, L = pr.L, i = pr.i;
+  const uint32_t* ct = dot + (uint64_t)pair * g.ct_words;
+  const uint32_t* c0 = ct + (uint64_t)pr.poly0 * n;
+  const uint32_t* c1 = ct + (uint64_t)pr.poly1 * n;
+  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * n;
+  {
+    const uint2* k0 = key + (uint64_t)(i * 2 + 0) * n;
+    const uint2* k1 = key + (uint64_t)(i * 2 + 1) * n;
+    for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+      const uint32_t d = c1[__ldg(&perm[x])];
+      const uint2 a = __ldg(&k0[x]), b = __ldg(&k1[x]);
+      acc0[x] = mul_shoup(d, a.x, a.y, q);
+      acc1[x] = mul_shoup(d, b.x, b.y, q);
+    }
+  }
+  const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * n;
+  for (uint32_t l = 0; l < L; ++l) {
+    if (l == i) continue;
+    const uint32_t* src = dig + (uint64_t)l * n;
+    if (pr.fast_reduce) {
+      for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+        const uint32_t v = src[x];
+        work[x] = min(v, v - q);
+      }
+    } else {
+      for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) work[x] = src[x] % q;
+    }
+    __syncthreads();
+    ntt_fwd_smem(work, g.fwd + (size_t)gp * n, q, n, g.logn);
+    const uint2* k0 = key + (uint64_t)(l * 2 + 0) * n;
+    const uint2* k1 = key + (uint64_t)(l * 2 + 1) * n;
+    for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+      const uint32_t d = work[x];
+      const uint2 a = __ldg(&k0[x]), b = __ldg(&k1[x]);
+      acc0[x] = add_mod(acc0[x], mul_shoup(d, a.x, a.y, q), q);
+      acc1[x] = add_mod(acc1[x], mul_shoup(d, b.x, b.y, q), q);
+    }
+    __syncthreads();
+  }
+  uint32_t* o = out + (uint64_t)pair * g.ct_words;
+  uint32_t* o0 = o + (uint64_t)pr.poly0 * n;
+  uint32_t* o1 = o + (uint64_t)pr.poly1 * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+    uint32_t r0 = add_mod(acc0[x], c0[__ldg(&perm[x])], q);
+    uint32_t r1 = acc1[x];
+    if (fold) {
+      r0 = add_mod(r0, c0[x], q);
+      r1 = add_mod(r1, c1[x], q);
+    }
+    o0[x] = r0;
+    o1[x] = r1;
+  }
+}
+
+// packed[g / N] += mask_{g mod N} (.) dot   (matmul.cpp:329-338, mask :288-305)
+// mask = NTT_q(lift(INTT_t(onehot at index_map[slot]))), regenerated per pair
+// exactly as the reference does for N > 4096. u64 atomics make the packed
+// accumulation order-free (mod-q addition is exact; reduced in k_finish).
+__global__ void k_mask_acc(Geo g, const uint32_t* __restrict__ dot, const uint64_t* __restrict__ rows,
+                           uint32_t cols, unsigned long long* __restrict__ acc64) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = g.n;
+  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const BranchInfo& br = g.br[pr.b];
+  const uint64_t gidx = rows[pair / cols] * cols + pair % cols;
+  const uint32_t slot = (uint32_t)(gidx % n);
+  const uint64_t c = gidx / n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) sm[g.index_map[slot]] = 1;
+  __syncthreads();
+  ntt_inv_smem(sm, g.inv + (size_t)(g.P + pr.b) * n, br.t, n, g.logn, br.last, br.ninv);
+  const uint32_t q = pr.q;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = sm[x] % q;
+  __syncthreads();
+  ntt_fwd_smem(sm, g.fwd + (size_t)gp * n, q, n, g.logn);
+  const uint32_t* d0 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly0 * n;
+  const uint32_t* d1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n;
+  unsigned long long* a0 = acc64 + (c * g.ct_words) + (uint64_t)pr.poly0 * n;
+  unsigned long long* a1 = acc64 + (c * g.ct_words) + (uint64_t)pr.poly1 * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+    const uint32_t m = sm[x];
+    atomicAdd(&a0[x], (unsigned long long)mul_barrett(d0[x], m, q, pr.mu));
+    atomicAdd(&a1[x], (unsigned long long)mul_barrett(d1[x], m, q, pr.mu));
+  }
+}
+
+// finish (matmul.cpp:342-374): reduce the u64 packed sums mod q and add the
+// bias pattern: part0 += NTT_q(Delta * INTT_t(scatter(pattern)))
+// (context.cpp:393-402). Block per (packed ct c, gp).
+__global__ void k_finish(Geo g, const unsigned long long* __restrict__ acc64, const int64_t* __restrict__ bias,
+                         uint32_t cols, uint64_t total, uint32_t* __restrict__ out) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = g.n;
+  const uint64_t c = blockIdx.x / g.P;
+  const uint32_t gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const BranchInfo& br = g.br[pr.b];
+  const int64_t t = br.t;
+  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+    const uint64_t gi = c * n + s;
+    int64_t v = gi < total ? bias[gi % cols] : 0;
+    int64_t r = v % t;
+    if (r < 0) r += t;
+    sm[g.index_map[s]] = (uint32_t)r;
+  }
+  __syncthreads();
+  ntt_inv_smem(sm, g.inv + (size_t)(g.P + pr.b) * n, br.t, n, g.logn, br.last, br.ninv);
+  const uint32_t q = pr.q;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = mul_shoup(sm[x], pr.delta.x, pr.delta.y, q);
+  __syncthreads();
+  ntt_fwd_smem(sm, g.fwd + (size_t)gp * n, q, n, g.logn);
+  const unsigned long long* a0 = acc64 + c * g.ct_words + (uint64_t)pr.poly0 * n;
+  const unsigned long long* a1 = acc64 + c * g.ct_words + (uint64_t)pr.poly1 * n;
+  uint32_t* o0 = out + c * g.ct_words + (uint64_t)pr.poly0 * n;
+  uint32_t* o1 = out + c * g.ct_words + (uint64_t)pr.poly1 * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+    o0[x] = add_mod((uint32_t)(a0[x] % q), sm[x], q);
+    o1[x] = (uint32_t)(a1[x] % q);
+  }
+}
+
+// encode_weights on the device (matmul.cpp:225-246): block per (j, k, gp):
+// slots -> centered residues mod t_b -> scatter -> INTT_t -> lift -> NTT_q.
+__global__ void k_encode_weights(Geo g, const int64_t* __restrict__ w, uint64_t f, uint32_t cols, uint32_t kc,
+                                 uint2* __restrict__ W) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = g.n;
+  const uint32_t gp = blockIdx.x % g.P;
+  const uint32_t jk = blockIdx.x / g.P;
+  const uint32_t j = jk / kc, k = jk % kc;
+  const PrimeInfo& pr = g.pr[gp];
+  const BranchInfo& br = g.br[pr.b];
+  const int64_t t = br.t;
+  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+    const uint64_t feat = (uint64_t)k * n + s;
+    int64_t v = feat < f ? w[feat * cols + j] : 0;
+    int64_t r = v % t;
+    if (r < 0) r += t;
+    sm[g.index_map[s]] = (uint32_t)r;
+  }
+  __syncthreads();
+  ntt_inv_smem(sm, g.inv + (size_t)(g.P + pr.b) * n, br.t, n, g.logn, br.last, br.ninv);
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = sm[x] % pr.q;
+  __syncthreads();
+  ntt_fwd_smem(sm, g.fwd + (size_t)gp * n, pr.q, n, g.logn);
+  uint2* dst = W + ((uint64_t)jk * g.pt_words) + (uint64_t)gp * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+    const uint32_t v = sm[x];
+    dst[x] = make_uint2(v, (uint32_t)(((uint64_t)v << 32) / pr.q));
+  }
+}
+
+// Prepared u64 values -> (val, shoup) with a range check.
+__global__ void k_prepare_plain(Geo g, const uint64_t* __restrict__ vals, uint64_t count, uint2* __restrict__ out,
+                                uint32_t* err) {
+  const uint64_t total = count * g.pt_words;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t gp = (uint32_t)((x % g.pt_words) / g.n);
+    const uint32_t q = g.pr[gp].q;
+    const uint64_t v = vals[x];
+    if (v >= q) *err = 1;
+    out[x] = make_uint2((uint32_t)v, (uint32_t)((v << 32) / q));
+  }
+}
+
+// Galois keys of one branch: host [e][l][part][i][n] u64 -> device
+// [e][i][l][part][n] (val, shoup), the order k_rot_keyswitch streams them.
+__global__ void k_prepare_keys(Geo g, uint32_t b, uint32_t elts, const uint64_t* __restrict__ rows,
+                               uint2* __restrict__ out, uint32_t* err) {
+  const uint32_t n = g.n, L = g.L[b], first = b ? g.L[0] : 0;
+  const uint64_t total = (uint64_t)elts * L * 2 * L * n;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t r = x;
+    const uint32_t c = (uint32_t)(r % n);
+    r /= n;
+    const uint32_t i = (uint32_t)(r % L);
+    r /= L;
+    const uint32_t part = (uint32_t)(r % 2);
+    r /= 2;
+    const uint32_t l = (uint32_t)(r % L);
+    const uint64_t e = r / L;
+    const uint32_t q = g.pr[first + i].q;
+    const uint64_t v = rows[x];
+    if (v >= q) *err = 1;
+    const uint64_t dst = ((((e * L + i) * L + l) * 2 + part) * n) + c;
+    out[dst] = make_uint2((uint32_t)v, (uint32_t)((v << 32) / q));
+  }
+}
+
+}  // namespace
+
+// ================================================================ host side
+struct hei_gpu_ctx {
+  int device = 0;
+  uint32_t n = 0, logn = 0;
+  uint64_t t[2] = {0, 0};
+  uint32_t L[2] = {0, 0};
+  std::vector<uint64_t> q;
+  uint32_t s_x = 6, s_w = 14, in_bits = 8;
+  Geo geo{};
+  uint2 *d_fwd = nullptr, *d_inv = nullptr;
+  uint32_t* d_index = nullptr;
+  // galois elements in fold order: steps 1, 2, ..., n/4, then the swap
+  std::vector<uint64_t> fold_elts;
+  std::map<uint64_t, uint32_t> perm_index;  // elt -> row of d_perms
+  uint32_t* d_perms = nullptr;
+  uint2* d_keys[2] = {nullptr, nullptr};
+  std::map<uint64_t, uint32_t> key_index[2];  // elt -> e
+  bool has_keys[2] = {false, false};
+  uint64_t* d_pk[2] = {nullptr, nullptr};
+  uint32_t* d_err = nullptr;
+  cudaStream_t stream = nullptr;
+  uint64_t batch_pairs = 0;
+  // scratch (grown on demand)
+  uint32_t *d_dotA = nullptr, *d_dotB = nullptr, *d_dig = nullptr;
+  uint64_t scratch_pairs = 0;
+  std::mutex mu;
+
+  size_t ct_words() const { return 2ull * (L[0] + L[1]) * n; }
+  size_t pt_words() const { return (size_t)(L[0] + L[1]) * n; }
+  uint32_t P() const { return L[0] + L[1]; }
+  uint32_t threads() const { return std::min<uint32_t>(512, std::max<uint32_t>(32, n / 2)); }
+};
+
+struct hei_gpu_weights {
+  hei_gpu_ctx* ctx;
+  uint64_t f = 0, cols = 0, kc = 0;
+  uint2* d_w = nullptr;  // [cols][k][twin plain] (val, shoup)
+};
+
+struct hei_gpu_stream {
+  hei_gpu_ctx* ctx;
+  const hei_gpu_weights* w;
+  std::vector<int64_t> bias;
+  uint64_t rows = 0, pushed = 0, C = 0;
+  std::vector<bool> seen;
+  bool finished = false;
+  unsigned long long* d_acc = nullptr;  // [C][twin ct] u64
+  // pending rows staged on the device
+  std::vector<uint64_t> pend_idx;
+  uint32_t* d_stage = nullptr;  // [cap][k][twin ct] u32
+  uint64_t* d_stage64 = nullptr;
+  uint64_t* d_rows = nullptr;
+  uint64_t cap_rows = 0;
+};
+
+struct hei_gpu_prng {
+  std::mt19937_64 eng;
+  double spare = 0.0;
+  bool have_spare = false;
+};
+
+namespace {
+
+void set_device(hei_gpu_ctx* c) { CU(cudaSetDevice(c->device)); }
+
+void check_err_flag(hei_gpu_ctx* c, int code, const char* what) {
+  uint32_t h = 0;
+  CU(cudaMemcpyAsync(&h, c->d_err, 4, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (h) {
+    CU(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
+    raise(code, what);
+  }
+}
+
+unsigned grid_for(uint64_t total, unsigned threads) {
+  uint64_t b = (total + threads - 1) / threads;
+  return (unsigned)std::min<uint64_t>(b, 148ull * 32);
+}
+
+void ensure_scratch(hei_gpu_ctx* c, uint64_t pairs) {
+  if (pairs <= c->scratch_pairs) return;
+  if (c->d_dotA) cudaFree(c->d_dotA);
+  if (c->d_dotB) cudaFree(c->d_dotB);
+  if (c->d_dig) cudaFree(c->d_dig);
+  c->d_dotA = c->d_dotB = c->d_dig = nullptr;
+  CU(cudaMalloc(&c->d_dotA, pairs * c->ct_words() * 4));
+  CU(cudaMalloc(&c->d_dotB, pairs * c->ct_words() * 4));
+  CU(cudaMalloc(&c->d_dig, pairs * c->pt_words() * 4));
+  c->scratch_pairs = pairs;
+}
+
+size_t smem_bytes(hei_gpu_ctx* c, int words) { return (size_t)words * c->n * 4; }
+
+void set_smem_attr(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+uint64_t auto_batch_pairs(hei_gpu_ctx* c) {
+  if (c->batch_pairs) return c->batch_pairs;
+  // Enough (pair, prime) blocks for several waves on 148 SMs while keeping the
+  // per-step working set (2 x dot + digits) modest.
+  const uint64_t per_pair = (2 * c->ct_words() + c->pt_words()) * 4;
+  uint64_t p = (uint64_t)4 << 30;  // 4 GiB
+  p /= per_pair;
+  return std::max<uint64_t>(1, std::min<uint64_t>(p, 4096));
+}
+
+// The rotate-and-sum fold over `pairs` twin ciphertexts in `cur` (eval form);
+// returns the buffer holding the result.
+uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st) {
+  const Geo& g = c->geo;
+  const unsigned T = c->threads();
+  const size_t sm1 = smem_bytes(c, 1), sm3 = smem_bytes(c, 3);
+  const unsigned blocks = (unsigned)(pairs * c->P());
+  for (uint64_t elt : c->fold_elts) {
+    const uint32_t* perm = c->d_perms + (size_t)c->perm_index.at(elt) * c->n;
+    const uint2* k0 = c->d_keys[0] + (size_t)c->key_index[0].at(elt) * c->L[0] * 2 * c->L[0] * c->n;
+    const uint2* k1 = c->d_keys[1] + (size_t)c->key_index[1].at(elt) * c->L[1] * 2 * c->L[1] * c->n;
+    k_rot_digits<<<blocks, T, sm1, st>>>(g, cur, perm, c->d_dig);
+    LAUNCHED();
+    k_rot_keyswitch<<<blocks, T, sm3, st>>>(g, cur, c->d_dig, perm, k0, k1, other, 1);
+    LAUNCHED();
+    std::swap(cur, other);
+  }
+  return cur;
+}
+
+void require_keys(hei_gpu_ctx* c) {
+  for (int b = 0; b < 2; ++b) {
+    if (!c->has_keys[b]) raise(HEI_KEY_ERROR, "apply_galois: no galois keys uploaded for this branch");
+    for (uint64_t e : c->fold_elts)
+      if (!c->key_index[b].count(e))
+        raise(HEI_KEY_ERROR, "apply_galois: no key for galois element " + std::to_string(e));
+  }
+}
+
+// Core: process staged rows (device u32, eval form) into the packed u64 sums.
+void run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, uint64_t nrows, cudaStream_t st) {
+  hei_gpu_ctx* c = s->ctx;
+  const hei_gpu_weights* w = s->w;
+  const Geo& g = c->geo;
+  const uint32_t cols = (uint32_t)w->cols;
+  const uint64_t pairs = nrows * cols;
+  ensure_scratch(c, pairs);
+  const unsigned T = c->threads();
+  const unsigned blocksP = (unsigned)(pairs * c->P());
+  k_chunk_dot<<<(unsigned)(pairs * 2 * c->P()), std::min<unsigned>(T, c->n / 4), 0, st>>>(g, d_in, w->d_w, cols,
+                                                                                         (uint32_t)w->kc, c->d_dotA);
+  LAUNCHED();
+  uint32_t* res = fold(c, pairs, c->d_dotA, c->d_dotB, st);
+  k_mask_acc<<<blocksP, T, smem_bytes(c, 1), st>>>(g, res, d_rows, cols, s->d_acc);
+  LAUNCHED();
+}
+
+void stream_flush(hei_gpu_stream* s) {
+  if (s->pend_idx.empty()) return;
+  hei_gpu_ctx* c = s->ctx;
+  const uint64_t nr = s->pend_idx.size();
+  CU(cudaMemcpyAsync(s->d_rows, s->pend_idx.data(), nr * 8, cudaMemcpyHostToDevice, c->stream));
+  check_err_flag(c, HEI_CODEC_ERROR, "push_row: coefficient not reduced");
+  run_rows(s, s->d_stage, s->d_rows, nr, c->stream);
+  CU(cudaStreamSynchronize(c->stream));
+  s->pend_idx.clear();
+}
+
+void finish_to(hei_gpu_stream* s, uint32_t* d_out, cudaStream_t st) {
+  hei_gpu_ctx* c = s->ctx;
+  int64_t* d_bias = nullptr;
+  CU(cudaMallocAsync(&d_bias, s->bias.size() * 8, st));
+  CU(cudaMemcpyAsync(d_bias, s->bias.data(), s->bias.size() * 8, cudaMemcpyHostToDevice, st));
+  k_finish<<<(unsigned)(s->C * c->P()), c->threads(), smem_bytes(c, 1), st>>>(
+      c->geo, s->d_acc, d_bias, (uint32_t)s->w->cols, s->rows * s->w->cols, d_out);
+  LAUNCHED();
+  CU(cudaFreeAsync(d_bias, st));
+}
+
+void check_bias_range(hei_gpu_ctx* c, const int64_t* bias, uint64_t cols) {
+  const int64_t lim = (int64_t)(((u128)c->t[0] * c->t[1] - 1) / 2);
+  for (uint64_t j = 0; j < cols; ++j)
+    if (bias[j] > lim || bias[j] < -lim) raise(HEI_RANGE_ERROR, "encode_signed: value outside the centered range");
+}
+
+// capacity_check (fixed_point.cpp:248-264)
+void capacity_gate(hei_gpu_ctx* c, uint64_t f, const char* who) {
+  int log_f = f <= 1 ? 0 : 64 - __builtin_clzll(f - 1);
+  int required = (int)(c->in_bits + c->s_x + c->s_w) + log_f;
+  u128 prod = (u128)c->t[0] * c->t[1];
+  int cap = -1;
+  while (prod) ++cap, prod >>= 1;
+  if (required + 1 > cap)
+    raise(HEI_RANGE_ERROR, std::string(who) + ": product needs " + std::to_string(required) +
+                               " result bits, capacity is " + std::to_string(cap) + "; refusing");
+}
+
+hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64_t* bias, uint64_t rows) {
+  if (rows == 0) raise(HEI_PARAM_ERROR, "matmul: empty input");
+  if (!w || w->cols == 0 || w->f == 0) raise(HEI_PARAM_ERROR, "matmul: empty weights");
+  if (w->ctx != c) raise(HEI_PARAM_ERROR, "matmul: weights encoded for a different context");
+  capacity_gate(c, w->f, "matmul");
+  require_keys(c);
+  check_bias_range(c, bias, w->cols);
+  auto s = std::make_unique<hei_gpu_stream>();
+  s->ctx = c;
+  s->w = w;
+  s->bias.assign(bias, bias + w->cols);
+  s->rows = rows;
+  s->seen.assign(rows, false);
+  s->C = (rows * w->cols + c->n - 1) / c->n;
+  CU(cudaMalloc(&s->d_acc, s->C * c->ct_words() * 8));
+  CU(cudaMemsetAsync(s->d_acc, 0, s->C * c->ct_words() * 8, c->stream));
+  const uint64_t bp = auto_batch_pairs(c);
+  s->cap_rows = std::max<uint64_t>(1, std::min<uint64_t>(rows, bp / w->cols));
+  CU(cudaMalloc(&s->d_stage, s->cap_rows * w->kc * c->ct_words() * 4));
+  CU(cudaMalloc(&s->d_stage64, s->cap_rows * w->kc * c->ct_words() * 8));
+  CU(cudaMalloc(&s->d_rows, s->cap_rows * 8));
+  return s.release();
+}
+
+void stream_free(hei_gpu_stream* s) {
+  if (!s) return;
+  cudaSetDevice(s->ctx->device);
+  cudaFree(s->d_acc);
+  cudaFree(s->d_stage);
+  cudaFree(s->d_stage64);
+  cudaFree(s->d_rows);
+  delete s;
+}
+
+void stream_push(hei_gpu_stream* s, uint64_t row, const uint64_t* chunks, int form) {
+  hei_gpu_ctx* c = s->ctx;
+  if (s->finished) raise(HEI_PARAM_ERROR, "push_row: stream already finished");
+  if (row >= s->rows) raise(HEI_PARAM_ERROR, "push_row: row index out of range");
+  if (s->seen[row]) raise(HEI_PARAM_ERROR, "push_row: row pushed twice");
+  if (form != HEI_FORM_EVAL && form != HEI_FORM_COEFF) raise(HEI_PARAM_ERROR, "push_row: unknown form");
+  const uint64_t slot = s->pend_idx.size();
+  const size_t words = s->w->kc * c->ct_words();
+  CU(cudaMemcpyAsync(s->d_stage64 + slot * words, chunks, words * 8, cudaMemcpyHostToDevice, c->stream));
+  k_narrow<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, s->d_stage64 + slot * words,
+                                                          s->d_stage + slot * words, s->w->kc, c->d_err);
+  LAUNCHED();
+  if (form == HEI_FORM_COEFF) {
+    k_ct_ntt<<<(unsigned)(s->w->kc * 2 * c->P()), c->threads(), smem_bytes(c, 1), c->stream>>>(
+        c->geo, s->d_stage + slot * words, 0);
+    LAUNCHED();
+  }
+  s->seen[row] = true;
+  ++s->pushed;
+  s->pend_idx.push_back(row);
+  if (s->pend_idx.size() == s->cap_rows) stream_flush(s);
+}
+
+void stream_finish(hei_gpu_stream* s, uint64_t* out, hei_op_counters* cnt) {
+  hei_gpu_ctx* c = s->ctx;
+  if (s->finished) raise(HEI_PARAM_ERROR, "finish: already finished");
+  if (s->pushed != s->rows)
+    raise(HEI_PARAM_ERROR, "finish: " + std::to_string(s->rows - s->pushed) + " rows were never pushed");
+  stream_flush(s);
+  uint32_t* d_out = nullptr;
+  uint64_t* d_out64 = nullptr;
+  const uint64_t words = s->C * c->ct_words();
+  CU(cudaMalloc(&d_out, words * 4));
+  CU(cudaMalloc(&d_out64, words * 8));
+  finish_to(s, d_out, c->stream);
+  k_widen<<<grid_for(words, 256), 256, 0, c->stream>>>(d_out, d_out64, words);
+  LAUNCHED();
+  CU(cudaMemcpyAsync(out, d_out64, words * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  cudaFree(d_out);
+  cudaFree(d_out64);
+  s->finished = true;
+  if (cnt) hei_proposed_counts(s->rows, s->w->cols, s->w->f, c->n, cnt);
+}
+
+hei_gpu_weights* weights_alloc(hei_gpu_ctx* c, uint64_t f, uint64_t cols) {
+  if (f == 0 || cols == 0) raise(HEI_PARAM_ERROR, "encode_weights: empty matrix");
+  auto w = std::make_unique<hei_gpu_weights>();
+  w->ctx = c;
+  w->f = f;
+  w->cols = cols;
+  w->kc = (f + c->n - 1) / c->n;
+  CU(cudaMalloc(&w->d_w, cols * w->kc * c->pt_words() * sizeof(uint2)));
+  return w.release();
+}
+
+// ---- util::Prng replay (rng.hpp:19-68) ----
+uint64_t prng_uniform(hei_gpu_prng* p, uint64_t bound) {
+  uint64_t limit = bound * (UINT64_MAX / bound), v;
+  do v = p->eng();
+  while (v >= limit);
+  return v % bound;
+}
+double prng_udouble(hei_gpu_prng* p) { return (double)(p->eng() >> 11) * 0x1.0p-53; }
+double prng_gauss(hei_gpu_prng* p) {
+  if (p->have_spare) {
+    p->have_spare = false;
+    return p->spare;
+  }
+  double u1, u2;
+  do u1 = prng_udouble(p);
+  while (u1 <= 0.0);
+  u2 = prng_udouble(p);
+  double mag = std::sqrt(-2.0 * std::log(u1));
+  p->spare = mag * std::sin(6.283185307179586476925286766559 * u2);
+  p->have_spare = true;
+  return mag * std::cos(6.283185307179586476925286766559 * u2);
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* hei_gpu_last_error(void) { return g_err.c_str(); }
+const char* hei_gpu_version(void) { return "heinfer_b200 0.1 (sm_100a)"; }
+uint64_t hei_gpu_launch_count(void) { return g_launches; }
+void hei_gpu_reset_launch_count(void) { g_launches = 0; }
+
+int hei_proposed_counts(uint64_t R, uint64_t cols, uint64_t f, uint32_t n, hei_op_counters* c) {
+  return guarded([&] {
+    if (!R || !cols || !f) raise(HEI_PARAM_ERROR, "empty shape");
+    if (!n || (n & (n - 1))) raise(HEI_PARAM_ERROR, "ring degree must be a power of two");
+    uint64_t k = (f + n - 1) / n, lg = 63 - __builtin_clzll(n);
+    c->mul_plain_count = R * cols * (k + 1);
+    c->rotation_count = R * cols * lg;
+    c->add_count = R * cols * (k + lg);
+    c->ciphertexts_in = R * k;
+    c->ciphertexts_out = (R * cols + n - 1) / n;
+  });
+}
+
+int hei_baseline_counts(uint64_t R, uint64_t cols, uint64_t f, uint32_t n, hei_op_counters* c) {
+  return guarded([&] {
+    if (!R || !cols || !f) raise(HEI_PARAM_ERROR, "empty shape");
+    if (!n || (n & (n - 1))) raise(HEI_PARAM_ERROR, "ring degree must be a power of two");
+    uint64_t blocks = (R + n - 1) / n;
+    c->mul_plain_count = blocks * f * cols;
+    c->rotation_count = 0;
+    c->add_count = blocks * cols * f;
+    c->ciphertexts_in = blocks * f;
+    c->ciphertexts_out = blocks * cols;
+  });
+}
+
+int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
+  return guarded([&] {
+    if (!d || !out) raise(HEI_PARAM_ERROR, "null argument");
+    const uint32_t n = d->n;
+    if (!n || (n & (n - 1)) || n < 8 || n > 32768) raise(HEI_PARAM_ERROR, "ring degree must be a power of two in [8, 32768]");
+    if (n > 16384) raise(HEI_PARAM_ERROR, "ring degree above 16384 is not supported on the device path");
+    if (d->L[0] == 0 || d->L[1] == 0) raise(HEI_PARAM_ERROR, "ciphertext modulus chain is empty");
+    if (d->L[0] + d->L[1] > kMaxPrimes) raise(HEI_PARAM_ERROR, "too many primes for the device path");
+    if (d->t[0] == d->t[1]) raise(HEI_PARAM_ERROR, "twin moduli must differ");
+    auto c = std::make_unique<hei_gpu_ctx>();
+    c->device = d->device;
+    c->n = n;
+    c->logn = 31 - __builtin_clz(n);
+    c->s_x = d->s_x;
+    c->s_w = d->s_w;
+    c->in_bits = d->input_int_bits;
+    const uint64_t two_n = 2ull * n;
+    for (int b = 0; b < 2; ++b) {
+      const uint64_t t = d->t[b];
+      c->t[b] = t;
+      c->L[b] = d->L[b];
+      // EncryptionParams::validate (params.cpp:27-66)
+      if (t < 2 || t % two_n != 1)
+        raise(HEI_PARAM_ERROR, "plaintext modulus " + std::to_string(t) + " is not 1 mod 2n; slot batching is unavailable");
+      if (!is_prime(t)) raise(HEI_PARAM_ERROR, "plaintext modulus must be prime");
+      if (t >= (1ull << 31)) raise(HEI_PARAM_ERROR, "plaintext modulus must be below 2^31 on the device path");
+    }
+    c->q.assign(d->q, d->q + d->L[0] + d->L[1]);
+    for (int b = 0; b < 2; ++b) {
+      const uint64_t* qb = d->q + (b ? d->L[0] : 0);
+      for (uint32_t i = 0; i < d->L[b]; ++i) {
+        const uint64_t qi = qb[i];
+        if (!is_prime(qi)) raise(HEI_PARAM_ERROR, "ciphertext modulus " + std::to_string(qi) + " is not prime");
+        if (qi % two_n != 1) raise(HEI_PARAM_ERROR, "ciphertext modulus " + std::to_string(qi) + " is not 1 mod 2n");
+        if (qi == d->t[b]) raise(HEI_PARAM_ERROR, "ciphertext modulus collides with plaintext modulus");
+        if (qi >= (1ull << 31)) raise(HEI_PARAM_ERROR, "ciphertext moduli must be below 2^31 on the device path");
+        for (uint32_t j = 0; j < i; ++j)
+          if (qb[j] == qi) raise(HEI_PARAM_ERROR, "duplicate ciphertext modulus");
+      }
+    }
+    const uint32_t P = c->P();
+    Geo& g = c->geo;
+    g.n = n;
+    g.logn = c->logn;
+    g.P = P;
+    g.ct_words = (uint32_t)c->ct_words();
+    g.pt_words = (uint32_t)c->pt_words();
+    g.L[0] = c->L[0];
+    g.L[1] = c->L[1];
+    // twiddle tables: P q-primes then t0, t1
+    std::vector<uint2> fwd((size_t)(P + 2) * n), inv((size_t)(P + 2) * n);
+    auto build = [&](uint64_t q, size_t row, uint2& last, uint2& ninv) {
+      const uint64_t psi = root_2n(n, q), psi_inv = invmod(psi, q);
+      for (uint32_t k = 0; k < n; ++k) {
+        const uint32_t e = rev_bits(k, c->logn);
+        const uint64_t z = powmod(psi, e, q), iz = powmod(psi_inv, e, q);
+        fwd[row * n + k] = make_uint2((uint32_t)z, shoup32(z, q));
+        inv[row * n + k] = make_uint2((uint32_t)iz, shoup32(iz, q));
+      }
+      const uint64_t ni = invmod(n, q);
+      const uint64_t l1 = mulmod(inv[row * n + 1].x, ni, q);
+      ninv = make_uint2((uint32_t)ni, shoup32(ni, q));
+      last = make_uint2((uint32_t)l1, shoup32(l1, q));
+    };
+    for (int b = 0; b < 2; ++b) {
+      const uint32_t first = b ? c->L[0] : 0;
+      // Delta = floor(Q / t) mod q_i via exact multiprecision-free arithmetic:
+      // floor(Q/t) = (Q - (Q mod t)) / t, and Q mod t, Q mod q_i are products
+      // of residues, so Delta mod q_i = (Q mod q_i - Q mod t) * t^-1 mod q_i.
+      const uint64_t t = c->t[b];
+      uint64_t Qmodt = 1 % t;
+      for (uint32_t i = 0; i < c->L[b]; ++i) Qmodt = mulmod(Qmodt, d->q[first + i] % t, t);
+      // BranchInfo
+      BranchInfo& br = g.br[b];
+      br.t = (uint32_t)t;
+      br.L = c->L[b];
+      br.first = first;
+      build(t, P + b, br.last, br.ninv);
+      uint64_t qmin = UINT64_MAX, qmax = 0;
+      for (uint32_t i = 0; i < c->L[b]; ++i) qmin = std::min(qmin, d->q[first + i]), qmax = std::max(qmax, d->q[first + i]);
+      for (uint32_t i = 0; i < c->L[b]; ++i) {
+        const uint64_t qi = d->q[first + i];
+        PrimeInfo& pr = g.pr[first + i];
+        pr.q = (uint32_t)qi;
+        pr.b = b;
+        pr.i = i;
+        pr.L = c->L[b];
+        pr.first = first;
+        pr.poly0 = (b ? 2 * c->L[0] : 0) + i;
+        pr.poly1 = (b ? 2 * c->L[0] : 0) + c->L[b] + i;
+        pr.fast_reduce = qmax < 2 * qmin ? 1u : 0u;  // digit < q_l < 2 q_i
+        pr.mu = (uint64_t)(((u128)1 << 64) / qi);
+        build(qi, first + i, pr.last, pr.ninv);
+        // Q mod q_i = 0, so Delta mod q_i = (0 - Q mod t) * t^-1 mod q_i
+        const uint64_t dl = mulmod((qi - Qmodt % qi) % qi, invmod(t % qi, qi), qi);
+        pr.delta = make_uint2((uint32_t)dl, shoup32(dl, qi));
+      }
+    }
+    // slot index map, generator 3 (context.cpp:50-63)
+    std::vector<uint32_t> index_map(n);
+    {
+      const uint64_t m = two_n;
+      uint64_t pos = 1;
+      for (uint32_t i = 0; i < n / 2; ++i) {
+        index_map[i] = rev_bits((uint32_t)((pos - 1) >> 1), c->logn);
+        index_map[i + n / 2] = rev_bits((uint32_t)((m - pos - 1) >> 1), c->logn);
+        pos = (pos * 3) % m;
+      }
+    }
+    // fold elements and their eval permutations (poly.cpp:124-138)
+    for (uint32_t s = 1; s <= n / 4; s <<= 1) c->fold_elts.push_back(powmod(3, s, two_n));
+    c->fold_elts.push_back(two_n - 1);
+    std::vector<uint32_t> perms(c->fold_elts.size() * (size_t)n);
+    for (size_t e = 0; e < c->fold_elts.size(); ++e) {
+      const uint64_t gel = c->fold_elts[e];
+      c->perm_index[gel] = (uint32_t)e;
+      for (uint32_t i = 0; i < n; ++i) {
+        const uint64_t ex = 2ull * rev_bits(i, c->logn) + 1, src = (ex * gel) % two_n;
+        perms[e * n + i] = rev_bits((uint32_t)((src - 1) / 2), c->logn);
+      }
+    }
+    set_device(c.get());
+    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CU(cudaMalloc(&c->d_fwd, fwd.size() * sizeof(uint2)));
+    CU(cudaMalloc(&c->d_inv, inv.size() * sizeof(uint2)));
+    CU(cudaMalloc(&c->d_index, n * 4));
+    CU(cudaMalloc(&c->d_perms, perms.size() * 4));
+    CU(cudaMalloc(&c->d_err, 4));
+    CU(cudaMemcpy(c->d_fwd, fwd.data(), fwd.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_inv, inv.data(), inv.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_index, index_map.data(), n * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_perms, perms.data(), perms.size() * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemset(c->d_err, 0, 4));
+    g.fwd = c->d_fwd;
+    g.inv = c->d_inv;
+    g.index_map = c->d_index;
+    const size_t s3 = smem_bytes(c.get(), 3);
+    set_smem_attr((const void*)k_rot_keyswitch, s3);
+    set_smem_attr((const void*)k_rot_digits, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_mask_acc, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_finish, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_ct_ntt, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_poly_ntt, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_encode_weights, smem_bytes(c.get(), 1));
+    *out = c.release();
+  });
+}
+
+void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaFree(c->d_fwd);
+  cudaFree(c->d_inv);
+  cudaFree(c->d_index);
+  cudaFree(c->d_perms);
+  cudaFree(c->d_err);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(c->d_keys[b]);
+    cudaFree(c->d_pk[b]);
+  }
+  cudaFree(c->d_dotA);
+  cudaFree(c->d_dotB);
+  cudaFree(c->d_dig);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void hei_gpu_set_batch_pairs(hei_gpu_ctx* c, uint64_t pairs) { c->batch_pairs = pairs; }
+
+int hei_gpu_upload_galois_keys(hei_gpu_ctx* c, uint32_t b, uint32_t count, const uint64_t* elts,
+                               const uint64_t* rows) {
+  return guarded([&] {
+    if (b > 1) raise(HEI_PARAM_ERROR, "branch out of range");
+    if (count == 0 || count > kMaxElts) raise(HEI_KEY_ERROR, "galois key set size out of range");
+    set_device(c);
+    const uint32_t L = c->L[b];
+    const uint64_t words = (uint64_t)count * L * 2 * L * c->n;
+    std::map<uint64_t, uint32_t> idx;
+    for (uint32_t e = 0; e < count; ++e) {
+      if (!(elts[e] & 1) || elts[e] >= 2ull * c->n) raise(HEI_KEY_ERROR, "invalid galois element");
+      idx[elts[e]] = e;
+    }
+    uint64_t* d_raw = nullptr;
+    CU(cudaMalloc(&d_raw, words * 8));
+    if (c->d_keys[b]) cudaFree(c->d_keys[b]);
+    c->d_keys[b] = nullptr;
+    CU(cudaMalloc(&c->d_keys[b], words * sizeof(uint2)));
+    CU(cudaMemcpy(d_raw, rows, words * 8, cudaMemcpyHostToDevice));
+    k_prepare_keys<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, b, count, d_raw, c->d_keys[b], c->d_err);
+    LAUNCHED();
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(d_raw);
+    check_err_flag(c, HEI_CODEC_ERROR, "galois keys: coefficient not reduced");
+    c->key_index[b] = idx;
+    c->has_keys[b] = true;
+  });
+}
+
+int hei_gpu_upload_public_key(hei_gpu_ctx* c, uint32_t b, const uint64_t* pk) {
+  return guarded([&] {
+    if (b > 1) raise(HEI_PARAM_ERROR, "branch out of range");
+    set_device(c);
+    const size_t words = 2ull * c->L[b] * c->n;
+    if (!c->d_pk[b]) CU(cudaMalloc(&c->d_pk[b], words * 8));
+    CU(cudaMemcpy(c->d_pk[b], pk, words * 8, cudaMemcpyHostToDevice));
+  });
+}
+
+int hei_gpu_weights_create(hei_gpu_ctx* c, const uint64_t* prepared, uint64_t f, uint64_t cols,
+                           hei_gpu_weights** out) {
+  return guarded([&] {
+    set_device(c);
+    std::unique_ptr<hei_gpu_weights> w(weights_alloc(c, f, cols));
+    const uint64_t count = cols * w->kc, words = count * c->pt_words();
+    uint64_t* d_raw = nullptr;
+    CU(cudaMalloc(&d_raw, words * 8));
+    CU(cudaMemcpy(d_raw, prepared, words * 8, cudaMemcpyHostToDevice));
+    k_prepare_plain<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, d_raw, count, w->d_w, c->d_err);
+    LAUNCHED();
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(d_raw);
+    check_err_flag(c, HEI_CODEC_ERROR, "weights: coefficient not reduced");
+    *out = w.release();
+  });
+}
+
+int hei_gpu_weights_encode(hei_gpu_ctx* c, const int64_t* wm, uint64_t f, uint64_t cols, hei_gpu_weights** out) {
+  return guarded([&] {
+    set_device(c);
+    const int64_t lim = (int64_t)(((u128)c->t[0] * c->t[1] - 1) / 2);
+    for (uint64_t x = 0; x < f * cols; ++x)
+      if (wm[x] > lim || wm[x] < -lim) raise(HEI_RANGE_ERROR, "encode_signed: value outside the centered range");
+    std::unique_ptr<hei_gpu_weights> w(weights_alloc(c, f, cols));
+    int64_t* d_w = nullptr;
+    CU(cudaMalloc(&d_w, f * cols * 8));
+    CU(cudaMemcpy(d_w, wm, f * cols * 8, cudaMemcpyHostToDevice));
+    k_encode_weights<<<(unsigned)(cols * w->kc * c->P()), c->threads(), smem_bytes(c, 1), c->stream>>>(
+        c->geo, d_w, f, (uint32_t)cols, (uint32_t)w->kc, w->d_w);
+    LAUNCHED();
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(d_w);
+    *out = w.release();
+  });
+}
+
+void hei_gpu_weights_destroy(hei_gpu_weights* w) {
+  if (!w) return;
+  cudaSetDevice(w->ctx->device);
+  cudaFree(w->d_w);
+  delete w;
+}
+
+int hei_gpu_stream_create(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64_t* bias, uint64_t rows,
+                          hei_gpu_stream** out) {
+  return guarded([&] {
+    set_device(c);
+    *out = stream_new(c, w, bias, rows);
+  });
+}
+
+int hei_gpu_stream_push_row(hei_gpu_stream* s, uint64_t row, const uint64_t* chunks, int form) {
+  return guarded([&] {
+    set_device(s->ctx);
+    std::lock_guard<std::mutex> lk(s->ctx->mu);
+    stream_push(s, row, chunks, form);
+  });
+}
+
+int hei_gpu_stream_finish(hei_gpu_stream* s, uint64_t* out, hei_op_counters* cnt) {
+  return guarded([&] {
+    set_device(s->ctx);
+    std::lock_guard<std::mutex> lk(s->ctx->mu);
+    stream_finish(s, out, cnt);
+  });
+}
+
+void hei_gpu_stream_destroy(hei_gpu_stream* s) { stream_free(s); }
+
+int hei_gpu_matmul(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint64_t* inputs, int form, uint64_t rows,
+                   const int64_t* bias, uint64_t* out, hei_op_counters* cnt) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, bias, rows), stream_free);
+    const size_t words = w->kc * c->ct_words();
+    for (uint64_t r = 0; r < rows; ++r) stream_push(s.get(), r, inputs + r * words, form);
+    stream_finish(s.get(), out, cnt);
+  });
+}
+
+int hei_gpu_matmul_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint32_t* d_inputs, int form,
+                          uint64_t rows, const int64_t* bias, uint32_t* d_out, hei_op_counters* cnt, void* stream) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (form != HEI_FORM_EVAL) raise(HEI_PARAM_ERROR, "matmul_device: inputs must be in eval form");
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, bias, rows), stream_free);
+    CU(cudaStreamSynchronize(c->stream));  // zeroed accumulators visible to `st`
+    const size_t words = w->kc * c->ct_words();
+    std::vector<uint64_t> idx(s->cap_rows);
+    for (uint64_t r0 = 0; r0 < rows; r0 += s->cap_rows) {
+      const uint64_t nr = std::min<uint64_t>(s->cap_rows, rows - r0);
+      for (uint64_t k = 0; k < nr; ++k) idx[k] = r0 + k;
+      CU(cudaMemcpyAsync(s->d_rows, idx.data(), nr * 8, cudaMemcpyHostToDevice, st));
+      run_rows(s.get(), d_inputs + r0 * words, s->d_rows, nr, st);
+      CU(cudaStreamSynchronize(st));  // idx / d_rows reuse
+    }
+    s->pushed = rows;
+    finish_to(s.get(), d_out, st);
+    CU(cudaStreamSynchronize(st));
+    s->finished = true;
+    if (cnt) hei_proposed_counts(rows, w->cols, w->f, c->n, cnt);
+  });
+}
+
+int hei_gpu_ntt(hei_gpu_ctx* c, uint32_t b, uint32_t prime, uint64_t* polys, uint64_t count, int inverse) {
+  return guarded([&] {
+    if (b > 1 || prime >= c->L[b]) raise(HEI_PARAM_ERROR, "prime index out of range");
+    set_device(c);
+    const uint32_t gp = (b ? c->L[0] : 0) + prime;
+    const uint64_t words = count * c->n;
+    std::vector<uint32_t> h32(words);
+    for (uint64_t x = 0; x < words; ++x) {
+      if (polys[x] >= c->q[gp]) raise(HEI_PARAM_ERROR, "ntt: coefficient not reduced");
+      h32[x] = (uint32_t)polys[x];
+    }
+    uint32_t* d = nullptr;
+    CU(cudaMalloc(&d, words * 4));
+    CU(cudaMemcpy(d, h32.data(), words * 4, cudaMemcpyHostToDevice));
+    k_poly_ntt<<<(unsigned)count, c->threads(), smem_bytes(c, 1), c->stream>>>(c->geo, gp, d, inverse);
+    LAUNCHED();
+    CU(cudaMemcpyAsync(h32.data(), d, words * 4, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(d);
+    for (uint64_t x = 0; x < words; ++x) polys[x] = h32[x];
+  });
+}
+
+int hei_gpu_apply_galois(hei_gpu_ctx* c, uint32_t b, uint64_t elt, const uint64_t* in, uint64_t* out) {
+  return guarded([&] {
+    if (b > 1) raise(HEI_PARAM_ERROR, "branch out of range");
+    if (!c->has_keys[b] || !c->key_index[b].count(elt))
+      raise(HEI_KEY_ERROR, "apply_galois: no key for galois element " + std::to_string(elt));
+    if (!c->perm_index.count(elt)) raise(HEI_KEY_ERROR, "apply_galois: unsupported galois element");
+    set_device(c);
+    // Embed the branch ciphertext in a twin-shaped buffer; only branch b's
+    // blocks are launched (grid over its primes via a branch-restricted Geo).
+    Geo g = c->geo;
+    const uint32_t L = c->L[b], n = c->n;
+    // single-branch geometry: P = L, ct = [2][L][n]
+    Geo gb = g;
+    gb.P = L;
+    gb.ct_words = 2 * L * n;
+    gb.pt_words = L * n;
+    gb.L[0] = L;
+    gb.L[1] = 0;
+    for (uint32_t i = 0; i < L; ++i) {
+      gb.pr[i] = g.pr[(b ? c->L[0] : 0) + i];
+      gb.pr[i].poly0 = i;
+      gb.pr[i].poly1 = L + i;
+      gb.pr[i].first = 0;
+      gb.pr[i].b = 0;
+    }
+    // twiddle rows: shift the table base so row i maps to branch prime i
+    gb.fwd = g.fwd + (size_t)(b ? c->L[0] : 0) * n;
+    gb.inv = g.inv + (size_t)(b ? c->L[0] : 0) * n;
+    const size_t words = 2ull * L * n;
+    std::vector<uint32_t> h32(words);
+    for (size_t x = 0; x < words; ++x) h32[x] = (uint32_t)in[x];
+    uint32_t *d_in = nullptr, *d_out = nullptr, *d_dig = nullptr;
+    CU(cudaMalloc(&d_in, words * 4));
+    CU(cudaMalloc(&d_out, words * 4));
+    CU(cudaMalloc(&d_dig, (size_t)L * n * 4));
+    CU(cudaMemcpy(d_in, h32.data(), words * 4, cudaMemcpyHostToDevice));
+    const uint32_t* perm = c->d_perms + (size_t)c->perm_index.at(elt) * n;
+    const uint2* key = c->d_keys[b] + (size_t)c->key_index[b].at(elt) * L * 2 * L * n;
+    k_rot_digits<<<L, c->threads(), smem_bytes(c, 1), c->stream>>>(gb, d_in, perm, d_dig);
+    LAUNCHED();
+    k_rot_keyswitch<<<L, c->threads(), smem_bytes(c, 3), c->stream>>>(gb, d_in, d_dig, perm, key, key, d_out, 0);
+    LAUNCHED();
+    CU(cudaMemcpyAsync(h32.data(), d_out, words * 4, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(d_in);
+    cudaFree(d_out);
+    cudaFree(d_dig);
+    for (size_t x = 0; x < words; ++x) out[x] = h32[x];
+  });
+}
+
+int hei_gpu_sum_all_slots(hei_gpu_ctx* c, const uint64_t* in, uint64_t* out, uint64_t count) {
+  return guarded([&] {
+    set_device(c);
+    require_keys(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    const size_t words = count * c->ct_words();
+    ensure_scratch(c, count);
+    uint64_t* d64 = nullptr;
+    CU(cudaMalloc(&d64, words * 8));
+    CU(cudaMemcpy(d64, in, words * 8, cudaMemcpyHostToDevice));
+    k_narrow<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, d64, c->d_dotA, count, c->d_err);
+    LAUNCHED();
+    check_err_flag(c, HEI_CODEC_ERROR, "sum_all_slots: coefficient not reduced");
+    uint32_t* res = fold(c, count, c->d_dotA, c->d_dotB, c->stream);
+    k_widen<<<grid_for(words, 256), 256, 0, c->stream>>>(res, d64, words);
+    LAUNCHED();
+    CU(cudaMemcpyAsync(out, d64, words * 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(d64);
+  });
+}
+
+int hei_gpu_prng_create(uint64_t seed, hei_gpu_prng** out) {
+  return guarded([&] {
+    auto p = std::make_unique<hei_gpu_prng>();
+    p->eng.seed(seed);
+    *out = p.release();
+  });
+}
+void hei_gpu_prng_destroy(hei_gpu_prng* p) { delete p; }
+
+int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_t f, const int64_t* w,
+                            uint64_t cols, const int64_t* bias, hei_gpu_prng* rng0, hei_gpu_prng* rng1,
+                            uint64_t* out, hei_op_counters* cnt) {
+  return guarded([&] {
+    (void)x; (void)rows; (void)f; (void)w; (void)cols; (void)bias; (void)rng0; (void)rng1; (void)out; (void)cnt;
+    raise(HEI_INTERNAL, "baseline_matmul: not implemented yet");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,246 @@
+"""Host-side mirror of hei::matmul (proj/include/hei/matmul/matmul.hpp:16-142)
+over the C ABI. Same names, argument meaning and error types as the reference:
+
+    proposed_counts / baseline_counts      (matmul.cpp:172-199)
+    GpuTwinServer                          (TwinContext::server_backend, twin.cpp:359-368)
+    encode_weights                         (matmul.cpp:225-246, on the device)
+    EncodedWeights.from_prepared           (upload of reference EncodedWeights)
+    encode_bias                            (matmul.cpp:248-254)
+    MatmulStream(push_row, finish, counters) (matmul.cpp:256-379)
+    matmul                                 (matmul.cpp:381-397)
+
+All residues use the reference's flat u64 layouts (include/heinfer_b200.h).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from .native import FORM_COEFF, FORM_EVAL, OpCounters, ParamError, RangeError, check, i64p, u64p
+
+
+def proposed_counts(rows: int, cols: int, f: int, n: int) -> OpCounters:
+    c = OpCounters()
+    check(native.lib().hei_proposed_counts(C.c_uint64(rows), C.c_uint64(cols), C.c_uint64(f), C.c_uint32(n), C.byref(c)))
+    return c
+
+
+def baseline_counts(rows: int, cols: int, f: int, n: int) -> OpCounters:
+    c = OpCounters()
+    check(native.lib().hei_baseline_counts(C.c_uint64(rows), C.c_uint64(cols), C.c_uint64(f), C.c_uint32(n), C.byref(c)))
+    return c
+
+
+@dataclass
+class ScalingConfig:  # fixed_point.hpp:13-20
+    s_x: int = 6
+    s_w: int = 14
+    input_int_bits: int = 8
+
+    def output_scale(self) -> int:
+        return self.s_x + self.s_w
+
+
+def scale_value(x: float, exponent: int) -> int:
+    """fixed_point.cpp:37-48: x * 2^e rounded half away from zero."""
+    if not math.isfinite(x):
+        raise RangeError("scale_value: non-finite input")
+    if exponent > 62:
+        raise ParamError("scale_value: exponent too large")
+    scaled = math.ldexp(x, exponent)
+    limit = float((1073872897 * 114689 - 1) // 2)
+    if not abs(scaled) <= limit:
+        raise RangeError(f"scale_value: {x} * 2^{exponent} exceeds the plaintext capacity")
+    r = math.floor(abs(scaled) + 0.5)
+    return int(r if scaled >= 0 else -r)
+
+
+def encode_bias(bias, cfg: ScalingConfig = ScalingConfig()) -> np.ndarray:
+    return np.array([scale_value(float(b), cfg.output_scale()) for b in bias], dtype=np.int64)
+
+
+class GpuTwinServer:
+    """Evaluate-only twin backend resident on one GPU: context, tables and the
+    Galois keys of both branches (no secret material)."""
+
+    def __init__(self, n: int, t, L, q, galois_elts, galois_keys, scaling: ScalingConfig = ScalingConfig(),
+                 device: int = 0, public_keys=None):
+        self.n = int(n)
+        self.t = [int(t[0]), int(t[1])]
+        self.L = [int(L[0]), int(L[1])]
+        self.q = np.ascontiguousarray(q, dtype=np.uint64)
+        self.scaling = scaling
+        self.ct_words = 2 * (self.L[0] + self.L[1]) * self.n
+        self.pt_words = (self.L[0] + self.L[1]) * self.n
+        d = native.TwinDesc()
+        d.n = self.n
+        d.t[0], d.t[1] = self.t
+        d.L[0], d.L[1] = self.L
+        d.q = u64p(self.q)
+        d.s_x, d.s_w, d.input_int_bits = scaling.s_x, scaling.s_w, scaling.input_int_bits
+        d.device = device
+        self._h = C.c_void_p()
+        check(native.lib().hei_gpu_ctx_create(C.byref(d), C.byref(self._h)))
+        elts = np.ascontiguousarray(galois_elts, dtype=np.uint64)
+        for b in range(2):
+            if galois_keys is None or galois_keys[b] is None:
+                continue
+            rows = np.ascontiguousarray(galois_keys[b], dtype=np.uint64)
+            check(native.lib().hei_gpu_upload_galois_keys(self._h, C.c_uint32(b), C.c_uint32(len(elts)), u64p(elts), u64p(rows)))
+        if public_keys is not None:
+            for b in range(2):
+                pk = np.ascontiguousarray(public_keys[b], dtype=np.uint64)
+                check(native.lib().hei_gpu_upload_public_key(self._h, C.c_uint32(b), u64p(pk)))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def chunks(self, f: int) -> int:
+        return (f + self.n - 1) // self.n
+
+    def set_batch_pairs(self, pairs: int) -> None:
+        native.lib().hei_gpu_set_batch_pairs(self._h, C.c_uint64(pairs))
+
+    # kernel-level seam (kernels::Kernels table, modops.hpp:29-51)
+    def ntt(self, branch: int, prime: int, polys: np.ndarray, inverse: bool = False) -> np.ndarray:
+        a = np.array(polys, dtype=np.uint64, copy=True, order="C")
+        count = a.size // self.n
+        check(native.lib().hei_gpu_ntt(self._h, C.c_uint32(branch), C.c_uint32(prime), u64p(a), C.c_uint64(count), C.c_int(int(inverse))))
+        return a
+
+    def apply_galois(self, branch: int, elt: int, ct: np.ndarray) -> np.ndarray:
+        ct = np.ascontiguousarray(ct, dtype=np.uint64)
+        out = np.zeros_like(ct)
+        check(native.lib().hei_gpu_apply_galois(self._h, C.c_uint32(branch), C.c_uint64(elt), u64p(ct), u64p(out)))
+        return out
+
+    def sum_all_slots(self, cts: np.ndarray) -> np.ndarray:
+        cts = np.ascontiguousarray(cts, dtype=np.uint64)
+        out = np.zeros_like(cts)
+        count = cts.size // self.ct_words
+        check(native.lib().hei_gpu_sum_all_slots(self._h, u64p(cts), u64p(out), C.c_uint64(count)))
+        return out
+
+    def close(self):
+        if self._h:
+            native.lib().hei_gpu_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class EncodedWeights:
+    """Device-resident EncodedWeights (matmul.hpp:51-55)."""
+
+    def __init__(self, server: GpuTwinServer, handle, f: int, cols: int):
+        self.server, self._h, self.f, self.cols = server, handle, f, cols
+        self.n = server.n
+
+    @classmethod
+    def from_prepared(cls, server: GpuTwinServer, prepared: np.ndarray, f: int) -> "EncodedWeights":
+        prepared = np.ascontiguousarray(prepared, dtype=np.uint64)
+        cols = prepared.shape[0]
+        h = C.c_void_p()
+        check(native.lib().hei_gpu_weights_create(server.handle, u64p(prepared), C.c_uint64(f), C.c_uint64(cols), C.byref(h)))
+        return cls(server, h, f, cols)
+
+    def close(self):
+        if self._h:
+            native.lib().hei_gpu_weights_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def encode_weights(server: GpuTwinServer, w: np.ndarray) -> EncodedWeights:
+    """w is f x cols scaled integers; transposition + encoding on the device."""
+    w = np.ascontiguousarray(w, dtype=np.int64)
+    if w.ndim != 2 or w.size == 0:
+        raise ParamError("encode_weights: empty matrix")
+    f, cols = w.shape
+    h = C.c_void_p()
+    check(native.lib().hei_gpu_weights_encode(server.handle, i64p(w), C.c_uint64(f), C.c_uint64(cols), C.byref(h)))
+    return EncodedWeights(server, h, f, cols)
+
+
+class MatmulStream:
+    """MatmulStream (matmul.hpp:83-114): push rows in any order, then finish."""
+
+    def __init__(self, server: GpuTwinServer, w: EncodedWeights, bias, total_rows: int):
+        self.server, self.w = server, w
+        self.bias = np.ascontiguousarray(bias, dtype=np.int64)
+        if self.bias.size != w.cols:
+            raise ParamError("matmul: bias length does not match output count")
+        self.rows = int(total_rows)
+        self._h = C.c_void_p()
+        self._counters = None
+        check(native.lib().hei_gpu_stream_create(server.handle, w._h, i64p(self.bias), C.c_uint64(self.rows), C.byref(self._h)))
+
+    def push_row(self, row_index: int, chunks: np.ndarray, form: int = FORM_EVAL) -> None:
+        chunks = np.ascontiguousarray(chunks, dtype=np.uint64)
+        if chunks.size != self.server.chunks(self.w.f) * self.server.ct_words:
+            raise ParamError("push_row: row has the wrong chunk count")
+        check(native.lib().hei_gpu_stream_push_row(self._h, C.c_uint64(row_index), u64p(chunks), C.c_int(form)))
+
+    def finish(self) -> np.ndarray:
+        C_ = (self.rows * self.w.cols + self.server.n - 1) // self.server.n
+        out = np.zeros((C_, self.server.ct_words), dtype=np.uint64)
+        cnt = OpCounters()
+        check(native.lib().hei_gpu_stream_finish(self._h, u64p(out), C.byref(cnt)))
+        self._counters = cnt
+        return out
+
+    def counters(self) -> OpCounters:
+        if self._counters is None:
+            raise ParamError("counters: stream not finished")
+        return self._counters
+
+    def __del__(self):
+        try:
+            if self._h:
+                native.lib().hei_gpu_stream_destroy(self._h)
+                self._h = C.c_void_p()
+        except Exception:
+            pass
+
+
+def matmul(server: GpuTwinServer, inputs: np.ndarray, w: EncodedWeights, bias, form: int = FORM_EVAL):
+    """matmul::matmul (matmul.cpp:381-397): inputs [R][k][twin ct] u64 on the
+    host. Returns (packed [C][twin ct] eval form, OpCounters)."""
+    inputs = np.ascontiguousarray(inputs, dtype=np.uint64)
+    if inputs.ndim != 3 or inputs.shape[0] == 0:
+        raise ParamError("matmul: empty input")
+    R = inputs.shape[0]
+    if inputs.shape[1] != server.chunks(w.f):
+        raise ParamError("matmul: input and weight shapes do not match")
+    bias = np.ascontiguousarray(bias, dtype=np.int64)
+    if bias.size != w.cols:
+        raise ParamError("matmul: bias length does not match output count")
+    C_ = (R * w.cols + server.n - 1) // server.n
+    out = np.zeros((C_, server.ct_words), dtype=np.uint64)
+    cnt = OpCounters()
+    check(native.lib().hei_gpu_matmul(server.handle, w._h, u64p(inputs), C.c_int(form), C.c_uint64(R), i64p(bias), u64p(out), C.byref(cnt)))
+    return out, cnt
+
+
+def matmul_device(server: GpuTwinServer, d_inputs_ptr: int, rows: int, w: EncodedWeights, bias, d_out_ptr: int,
+                  stream_ptr: int = 0) -> OpCounters:
+    """Device-resident variant: u32 residues already in HBM (bench `value`)."""
+    bias = np.ascontiguousarray(bias, dtype=np.int64)
+    cnt = OpCounters()
+    check(native.lib().hei_gpu_matmul_device(server.handle, w._h, C.c_void_p(d_inputs_ptr), C.c_int(FORM_EVAL), C.c_uint64(rows),
+                                             i64p(bias), C.c_void_p(d_out_ptr), C.byref(cnt), C.c_void_p(stream_ptr)))
+    return cnt

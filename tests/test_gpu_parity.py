@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle, bit-exact.
+
+Every comparison is on identical keys and identical input ciphertexts; the
+bar is bit-for-bit equality of the output residues (integer work) and exact
+decrypted class scores (test_matmul.cpp:44-55 oracle).
+"""
+import numpy as np
+import pytest
+
+from tests.helpers import Oracle, TwinParams, gpu_server_from, oracle_matmul, production_params, random_mat, synthetic, tiny_params
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def prod():
+    o = Oracle(production_params(8192), key_seed=1, enc_seed=2)
+    s = gpu_server_from(o)
+    return o, s
+
+
+@pytest.fixture(scope="module")
+def tiny32():
+    o = Oracle(tiny_params(32), key_seed=72, enc_seed=73)
+    return o, gpu_server_from(o)
+
+
+def test_library_loads_and_reports_version():
+    from paper_2204_05496_b200 import native
+
+    assert b"sm_100a" in native.lib().hei_gpu_version()
+
+
+@pytest.mark.parametrize("n", [8, 32, 8192, 16384])
+def test_ntt_bit_exact_all_primes(n):
+    from oracle.oracle import oracle_lib, _u64p
+    import ctypes as C
+
+    p = production_params(n) if n >= 8192 else tiny_params(n)
+    o = Oracle(p, 3, 4)
+    s = gpu_server_from(o)
+    rng = np.random.default_rng(n)
+    lib = oracle_lib()
+    for b in range(2):
+        for i in range(o.L[b]):
+            q = o.q[(o.L[0] if b else 0) + i]
+            a = rng.integers(0, q, size=(3, n), dtype=np.uint64)
+            fwd = s.ntt(b, i, a)
+            want = a.copy()
+            for r in range(3):
+                row = np.ascontiguousarray(want[r])
+                assert lib.ho_ntt(C.c_uint32(n), C.c_uint64(q), _u64p(row), 0) == 0
+                want[r] = row
+            assert np.array_equal(fwd, want), (b, i)
+            back = s.ntt(b, i, fwd, inverse=True)
+            assert np.array_equal(back, a), (b, i)
+
+
+def _eval_ct(o, rng, b):
+    """A fresh eval-form single-branch ciphertext from the oracle client."""
+    x = rng.integers(-50, 50, size=(1, o.n), dtype=np.int64)
+    ct = o.encode_inputs(x)[0, 0]
+    n0 = 2 * o.L[0] * o.n
+    return ct[:n0] if b == 0 else ct[n0:]
+
+
+@pytest.mark.parametrize("which", ["tiny32", "prod"])
+def test_apply_galois_every_element(which, request):
+    o, s = request.getfixturevalue(which)
+    rng = np.random.default_rng(5)
+    for b in range(2):
+        ct = _eval_ct(o, rng, b)
+        for elt in o.elts():
+            got = s.apply_galois(b, int(elt), ct)
+            want = o.apply_galois(b, int(elt), ct)
+            assert np.array_equal(got, want), (b, int(elt))
+
+
+@pytest.mark.parametrize("which", ["tiny32", "prod"])
+def test_sum_all_slots_twin(which, request):
+    o, s = request.getfixturevalue(which)
+    rng = np.random.default_rng(6)
+    x = rng.integers(-9, 9, size=(2, o.n), dtype=np.int64)
+    cts = o.encode_inputs(x)[:, 0, :]
+    got = s.sum_all_slots(cts)
+    for r in range(2):
+        assert np.array_equal(got[r], o.sum_all_slots(cts[r])), r
+
+
+@pytest.mark.parametrize("n", [8, 32])
+def test_random_shapes_match_oracle_and_integers(n):
+    """test_matmul.cpp:172-205 restated: random shapes, bit-exact ciphertexts,
+    exact decrypted results and closed-form counters."""
+    from paper_2204_05496_b200 import EncodedWeights, matmul, proposed_counts
+
+    o = Oracle(tiny_params(n), 40 + n, 41 + n)
+    s = gpu_server_from(o)
+    rng = np.random.default_rng(100 + n)
+    for trial in range(12):
+        r = 1 + int(rng.integers(10))
+        c = 1 + int(rng.integers(5))
+        f = 1 + int(rng.integers(3 * n))
+        x = random_mat(rng, r, f, 32)
+        w = random_mat(rng, f, c, 8)
+        bias = rng.integers(-1000, 1001, size=c)
+        inputs = o.encode_inputs(x)
+        wp = o.encode_weights(w)
+        want_ct, want_cnt = o.fast_matmul(inputs, f, wp, bias)
+        ew = EncodedWeights.from_prepared(s, wp, f)
+        got_ct, cnt = matmul(s, inputs, ew, bias)
+        assert np.array_equal(got_ct, want_ct), trial
+        assert np.array_equal(o.unpack(got_ct, r, c), oracle_matmul(x, w, bias))
+        cf = proposed_counts(r, c, f, n)
+        assert cnt.as_tuple() == cf.as_tuple() == tuple(int(v) for v in want_cnt)
+
+
+def test_device_weight_encoding_matches_reference_encoding(prod):
+    from paper_2204_05496_b200 import encode_weights, matmul
+
+    o, s = prod
+    x, w, b = synthetic(1, 9000, 2, 0.05, 0.1, seed=11)
+    inputs = o.encode_inputs(x)
+    want, _ = o.fast_matmul(inputs, 9000, o.encode_weights(w), b)
+    got, _ = matmul(s, inputs, encode_weights(s, w), b)
+    assert np.array_equal(got, want)
+
+
+def test_production_c1_shape_bit_exact(prod):
+    """C1 restricted to 3 classes: N=8192, 1 x 1000 features."""
+    from paper_2204_05496_b200 import EncodedWeights, matmul
+
+    o, s = prod
+    x, w, b = synthetic(1, 1000, 3, 0.05, 0.1)
+    inputs = o.encode_inputs(x)
+    wp = o.encode_weights(w)
+    want, _ = o.fast_matmul(inputs, 1000, wp, b)
+    got, cnt = matmul(s, inputs, EncodedWeights.from_prepared(s, wp, 1000), b)
+    assert np.array_equal(got, want)
+    assert np.array_equal(o.unpack(got, 1, 3), oracle_matmul(x, w, b))
+    assert cnt.rotation_count == 3 * 13
+
+
+def test_production_multi_chunk_multi_row(prod):
+    """Two chunks per row (f > N) and several rows: 3 x 10000 x 2."""
+    from paper_2204_05496_b200 import EncodedWeights, matmul
+
+    o, s = prod
+    x, w, b = synthetic(3, 10000, 2, 0.05, 0.1, seed=3)
+    inputs = o.encode_inputs(x)
+    wp = o.encode_weights(w)
+    want, _ = o.fast_matmul(inputs, 10000, wp, b)
+    got, cnt = matmul(s, inputs, EncodedWeights.from_prepared(s, wp, 10000), b)
+    assert np.array_equal(got, want)
+    assert np.array_equal(o.unpack(got, 3, 2), oracle_matmul(x, w, b))
+    assert cnt.mul_plain_count == 3 * 2 * 3
+
+
+def test_coeff_form_inputs(tiny32):
+    """Server ingestion path: coefficient-form chunks are NTT'd on the device
+    (context.cpp:404-419)."""
+    from paper_2204_05496_b200 import FORM_COEFF, EncodedWeights, matmul
+
+    o, s = tiny32
+    rng = np.random.default_rng(9)
+    x = random_mat(rng, 3, 40, 20)
+    w = random_mat(rng, 40, 2, 5)
+    bias = np.array([3, -4])
+    inputs = o.encode_inputs(x)
+    # to coeff form with the GPU inverse NTT checked elsewhere; use the oracle
+    coeff = inputs.copy()
+    n = o.n
+    from oracle.oracle import oracle_lib, _u64p
+    import ctypes as C
+
+    lib = oracle_lib()
+    for r in range(coeff.shape[0]):
+        for k in range(coeff.shape[1]):
+            for poly in range(2 * (o.L[0] + o.L[1])):
+                b_ = 0 if poly < 2 * o.L[0] else 1
+                i = poly % o.L[0] if b_ == 0 else (poly - 2 * o.L[0]) % o.L[1]
+                q = o.q[(o.L[0] if b_ else 0) + i]
+                seg = np.ascontiguousarray(coeff[r, k, poly * n:(poly + 1) * n])
+                lib.ho_ntt(C.c_uint32(n), C.c_uint64(q), _u64p(seg), 1)
+                coeff[r, k, poly * n:(poly + 1) * n] = seg
+    wp = o.encode_weights(w)
+    want, _ = o.fast_matmul(coeff, 40, wp, bias, form=0)
+    got, _ = matmul(s, coeff, EncodedWeights.from_prepared(s, wp, 40), bias, form=FORM_COEFF)
+    assert np.array_equal(got, want)
+    assert np.array_equal(o.unpack(got, 3, 2), oracle_matmul(x, w, bias))
+
+
+def test_stream_any_order_and_misuse(tiny32):
+    """test_matmul.cpp:326-387 restated."""
+    from paper_2204_05496_b200 import EncodedWeights, MatmulStream, ParamError, matmul
+
+    o, s = tiny32
+    rng = np.random.default_rng(400)
+    x = random_mat(rng, 7, 10, 32)
+    w = random_mat(rng, 10, 3, 8)
+    bias = np.array([5, 6, 7])
+    inputs = o.encode_inputs(x)
+    ew = EncodedWeights.from_prepared(s, o.encode_weights(w), 10)
+    in_order, _ = matmul(s, inputs, ew, bias)
+    for seed in range(3):
+        order = np.random.default_rng(seed).permutation(7)
+        st = MatmulStream(s, ew, bias, 7)
+        for i in order:
+            st.push_row(int(i), inputs[i])
+        assert np.array_equal(st.finish(), in_order)
+
+    st = MatmulStream(s, ew, bias, 3)
+    st.push_row(0, inputs[0])
+    with pytest.raises(ParamError):
+        st.push_row(0, inputs[0])
+    with pytest.raises(ParamError):
+        st.push_row(3, inputs[1])
+    with pytest.raises(ParamError):
+        st.counters()
+    with pytest.raises(ParamError):
+        st.finish()
+    st.push_row(1, inputs[1])
+    st.push_row(2, inputs[2])
+    assert st.finish().shape[0] == 1
+    with pytest.raises(ParamError):
+        st.finish()
+    with pytest.raises(ParamError):
+        st.push_row(0, inputs[0])
+
+
+def test_errors_match_reference_types(tiny32):
+    """test_matmul.cpp:389-433: missing keys -> KeyError, capacity -> RangeError."""
+    from paper_2204_05496_b200 import EncodedWeights, GpuTwinServer, KeyError_, RangeError, ScalingConfig, matmul, native
+
+    o, s = tiny32
+    rng = np.random.default_rng(600)
+    x = random_mat(rng, 2, 4, 10)
+    w = random_mat(rng, 4, 2, 5)
+    inputs = o.encode_inputs(x)
+    wp = o.encode_weights(w)
+    norot = GpuTwinServer(o.n, (o.p.t0, o.p.t1), o.L, o.q, o.elts(), None, ScalingConfig(2, 3, 3))
+    with pytest.raises(KeyError_):
+        matmul(norot, inputs, EncodedWeights.from_prepared(norot, wp, 4), [1, 2])
+    wide = GpuTwinServer(o.n, (o.p.t0, o.p.t1), o.L, o.q, o.elts(), o.galois_keys()[1], ScalingConfig())
+    with pytest.raises(RangeError):
+        matmul(wide, inputs, EncodedWeights.from_prepared(wide, wp, 4), [0, 0])
+    bad = inputs.copy()
+    bad[0, 0, 0] = o.q[0]  # not reduced
+    with pytest.raises(native.CodecError):
+        matmul(s, bad, EncodedWeights.from_prepared(s, wp, 4), [0, 0])
