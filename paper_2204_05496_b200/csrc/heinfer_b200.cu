@@ -37,6 +37,7 @@
 
 #include "../../include/heinfer_b200.h"
 #include "modmath.cuh"
+#include "ntt_fast.cuh"
 
 using namespace heb;
 
@@ -187,6 +188,9 @@ struct Geo {
   BranchInfo br[2];
   const uint2* fwd;  // [P + 2][n]: q primes then t0, t1
   const uint2* inv;
+  const uint4* twc;  // pass-C twiddles, fast path only: [P + 2][KC][T]
+  const uint4* itwc;
+  uint32_t twc_stride;  // KC * T (uint4 per modulus)
   const uint32_t* index_map;
 };
 
@@ -491,9 +495,229 @@ __global__ void k_prepare_keys(Geo g, uint32_t b, uint32_t elts, const uint64_t*
     const uint32_t q = g.pr[first + i].q;
     const uint64_t v = rows[x];
     if (v >= q) *err = 1;
-    const uint64_t dst = ((((e * L + i) * L + l) * 2 + part) * n) + c;
+    // fast path (n >= 4096): pass-C transposed layout, slot x = 16 j + 2 c' + h
+    // stored at uint2 index (c' * (n / 16) + j) * 2 + h
+    uint32_t cpos = c;
+    if (n >= 4096) {
+      const uint32_t jj = c >> 4, rr = c & 15;
+      cpos = ((rr >> 1) * (n >> 4) + jj) * 2 + (rr & 1);
+    }
+    const uint64_t dst = ((((e * L + i) * L + l) * 2 + part) * n) + cpos;
     out[dst] = make_uint2((uint32_t)v, (uint32_t)((v << 32) / q));
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Register-blocked kernels (N = 2^LOGN, LOGN in 12..14, T = N/16 threads).
+// ---------------------------------------------------------------------------
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T) k_poly_ntt_f(Geo g, uint32_t gp, uint32_t* __restrict__ polys,
+                                                            int inverse) {
+  using NT = Ntt<LOGN>;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
+  uint32_t* p = polys + (uint64_t)blockIdx.x * NT::N;
+  const PrimeInfo& pr = g.pr[gp];
+  uint32_t e[16];
+  if (inverse) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = p[x0 + r];
+    NT::inv(e, sm, g.inv + (size_t)gp * NT::N, g.itwc + (size_t)gp * g.twc_stride, pr.q, pr.last, pr.ninv);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) p[NT::posA(j, r)] = e[r];
+  } else {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = p[NT::posA(j, r)];
+    NT::fwd(e, sm, g.fwd + (size_t)gp * NT::N, g.twc + (size_t)gp * g.twc_stride, pr.q);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) p[x0 + r] = e[r];
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T) k_ct_ntt_f(Geo g, uint32_t* __restrict__ cts) {
+  using NT = Ntt<LOGN>;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t polys = 2 * g.P;
+  const uint32_t poly = (uint32_t)(blockIdx.x % polys);
+  const uint32_t gp = poly_prime(g, poly);
+  uint32_t* p = cts + (uint64_t)blockIdx.x * NT::N;
+  const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
+  uint32_t e[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) e[r] = p[NT::posA(j, r)];
+  NT::fwd(e, sm, g.fwd + (size_t)gp * NT::N, g.twc + (size_t)gp * g.twc_stride, g.pr[gp].q);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) p[x0 + r] = e[r];
+}
+
+__device__ __forceinline__ void load16(const uint32_t* __restrict__ p, uint32_t (&v)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 a = *reinterpret_cast<const uint4*>(p + 4 * c);
+    v[4 * c] = a.x;
+    v[4 * c + 1] = a.y;
+    v[4 * c + 2] = a.z;
+    v[4 * c + 3] = a.w;
+  }
+}
+__device__ __forceinline__ void load16_ro(const uint32_t* __restrict__ p, uint32_t (&v)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(p + 4 * c));
+    v[4 * c] = a.x;
+    v[4 * c + 1] = a.y;
+    v[4 * c + 2] = a.z;
+    v[4 * c + 3] = a.w;
+  }
+}
+__device__ __forceinline__ void store16(uint32_t* __restrict__ p, const uint32_t (&v)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    *reinterpret_cast<uint4*>(p + 4 * c) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T) k_rot_digits_f(Geo g, const uint32_t* __restrict__ dot,
+                                                              const uint32_t* __restrict__ perm,
+                                                              uint32_t* __restrict__ digits) {
+  using NT = Ntt<LOGN>;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * NT::N;
+  const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
+  uint32_t pm[16], e[16];
+  load16_ro(perm + x0, pm);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) e[r] = c1[pm[r]];
+  NT::inv(e, sm, g.inv + (size_t)gp * NT::N, g.itwc + (size_t)gp * g.twc_stride, pr.q, pr.last, pr.ninv);
+  uint32_t* d = digits + ((uint64_t)pair * g.P + gp) * NT::N;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) d[NT::posA(j, r)] = e[r];
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T) k_rot_keyswitch_f(Geo g, const uint32_t* __restrict__ dot,
+                                                                 const uint32_t* __restrict__ digits,
+                                                                 const uint32_t* __restrict__ perm,
+                                                                 const uint2* __restrict__ key0,
+                                                                 const uint2* __restrict__ key1,
+                                                                 uint32_t* __restrict__ out, int fold) {
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t q = pr.q, L = pr.L, i = pr.i;
+  const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
+  const uint32_t* ct = dot + (uint64_t)pair * g.ct_words;
+  const uint32_t* c0 = ct + (uint64_t)pr.poly0 * N;
+  const uint32_t* c1 = ct + (uint64_t)pr.poly1 * N;
+  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * N;
+  uint32_t acc0[16], acc1[16], e[16];
+  {
+    uint32_t pm[16];
+    load16_ro(perm + x0, pm);
+    // keys in pass-C transposed layout: uint4 c of thread j at [c * T + j]
+    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * N) + j;
+    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * N) + j;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 a = __ldg(k0 + c * NT::T), b = __ldg(k1 + c * NT::T);
+      const uint32_t d0 = c1[pm[2 * c]], d1 = c1[pm[2 * c + 1]];
+      acc0[2 * c] = mul_shoup(d0, a.x, a.y, q);
+      acc0[2 * c + 1] = mul_shoup(d1, a.z, a.w, q);
+      acc1[2 * c] = mul_shoup(d0, b.x, b.y, q);
+      acc1[2 * c + 1] = mul_shoup(d1, b.z, b.w, q);
+    }
+  }
+  const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
+  const uint2* tw = g.fwd + (size_t)gp * N;
+  const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
+  for (uint32_t l = 0; l < L; ++l) {
+    if (l == i) continue;
+    const uint32_t* src = dig + (uint64_t)l * N;
+    if (pr.fast_reduce) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t v = src[NT::posA(j, r)];
+        e[r] = min(v, v - q);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
+    }
+    NT::fwd(e, sm, tw, twc, q);
+    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
+    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 a = __ldg(k0 + c * NT::T), b = __ldg(k1 + c * NT::T);
+      acc0[2 * c] = add_mod(acc0[2 * c], mul_shoup(e[2 * c], a.x, a.y, q), q);
+      acc0[2 * c + 1] = add_mod(acc0[2 * c + 1], mul_shoup(e[2 * c + 1], a.z, a.w, q), q);
+      acc1[2 * c] = add_mod(acc1[2 * c], mul_shoup(e[2 * c], b.x, b.y, q), q);
+      acc1[2 * c + 1] = add_mod(acc1[2 * c + 1], mul_shoup(e[2 * c + 1], b.z, b.w, q), q);
+    }
+  }
+  {
+    uint32_t pm[16];
+    load16_ro(perm + x0, pm);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) acc0[r] = add_mod(acc0[r], c0[pm[r]], q);
+  }
+  if (fold) {
+    load16(c0 + x0, e);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) acc0[r] = add_mod(acc0[r], e[r], q);
+    load16(c1 + x0, e);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) acc1[r] = add_mod(acc1[r], e[r], q);
+  }
+  uint32_t* o = out + (uint64_t)pair * g.ct_words;
+  store16(o + (uint64_t)pr.poly0 * N + x0, acc0);
+  store16(o + (uint64_t)pr.poly1 * N + x0, acc1);
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T) k_mask_acc_f(Geo g, const uint32_t* __restrict__ dot,
+                                                            const uint64_t* __restrict__ rows, uint32_t cols,
+                                                            unsigned long long* __restrict__ acc64) {
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const BranchInfo& br = g.br[pr.b];
+  const uint64_t gidx = rows[pair / cols] * cols + pair % cols;
+  const uint32_t slot = (uint32_t)(gidx % N);
+  const uint64_t c = gidx / N;
+  const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
+  const uint32_t hot = __ldg(&g.index_map[slot]);
+  uint32_t e[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) e[r] = (x0 + r == hot) ? 1u : 0u;
+  NT::inv(e, sm, g.inv + (size_t)(g.P + pr.b) * N, g.itwc + (size_t)(g.P + pr.b) * g.twc_stride, br.t, br.last, br.ninv);
+  const uint32_t q = pr.q;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) e[r] = e[r] % q;
+  NT::fwd(e, sm, g.fwd + (size_t)gp * N, g.twc + (size_t)gp * g.twc_stride, q);
+  uint32_t d[16];
+  const uint32_t* base = dot + (uint64_t)pair * g.ct_words;
+  unsigned long long* a0 = acc64 + c * g.ct_words + (uint64_t)pr.poly0 * N + x0;
+  unsigned long long* a1 = acc64 + c * g.ct_words + (uint64_t)pr.poly1 * N + x0;
+  load16(base + (uint64_t)pr.poly0 * N + x0, d);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) atomicAdd(&a0[r], (unsigned long long)mul_barrett(d[r], e[r], q, pr.mu));
+  load16(base + (uint64_t)pr.poly1 * N + x0, d);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) atomicAdd(&a1[r], (unsigned long long)mul_barrett(d[r], e[r], q, pr.mu));
 }
 
 }  // namespace
@@ -508,6 +732,7 @@ struct hei_gpu_ctx {
   uint32_t s_x = 6, s_w = 14, in_bits = 8;
   Geo geo{};
   uint2 *d_fwd = nullptr, *d_inv = nullptr;
+  uint4 *d_twc = nullptr, *d_itwc = nullptr;
   uint32_t* d_index = nullptr;
   // galois elements in fold order: steps 1, 2, ..., n/4, then the swap
   std::vector<uint64_t> fold_elts;
@@ -596,6 +821,59 @@ void set_smem_attr(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024) CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
+// ---- launch dispatch: register-blocked kernels for N in {4096, 8192, 16384},
+// ---- generic shared-memory kernels otherwise (small test rings).
+#define HEI_DISPATCH(LOGN_VAR, FAST, GENERIC)         \
+  switch (LOGN_VAR) {                                 \
+    case 12: { constexpr int LG = 12; FAST; } break;  \
+    case 13: { constexpr int LG = 13; FAST; } break;  \
+    case 14: { constexpr int LG = 14; FAST; } break;  \
+    default: { GENERIC; } break;                      \
+  }
+
+void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* perm,
+                       uint32_t* dig, cudaStream_t st) {
+  const size_t sm = smem_bytes(c, 1);
+  HEI_DISPATCH(c->logn, (k_rot_digits_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig)),
+               (k_rot_digits<<<blocks, c->threads(), sm, st>>>(g, cur, perm, dig)));
+  LAUNCHED();
+}
+void launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* dig,
+                          const uint32_t* perm, const uint2* k0, const uint2* k1, uint32_t* out, int fold,
+                          cudaStream_t st) {
+  HEI_DISPATCH(c->logn,
+               (k_rot_keyswitch_f<LG><<<blocks, Ntt<LG>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, out, fold)),
+               (k_rot_keyswitch<<<blocks, c->threads(), smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold)));
+  LAUNCHED();
+}
+void launch_mask_acc(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* res, const uint64_t* rows,
+                     uint32_t cols, unsigned long long* acc, cudaStream_t st) {
+  const size_t sm = smem_bytes(c, 1);
+  HEI_DISPATCH(c->logn, (k_mask_acc_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(g, res, rows, cols, acc)),
+               (k_mask_acc<<<blocks, c->threads(), sm, st>>>(g, res, rows, cols, acc)));
+  LAUNCHED();
+}
+void launch_ct_ntt(hei_gpu_ctx* c, unsigned blocks, uint32_t* cts, cudaStream_t st) {
+  const size_t sm = smem_bytes(c, 1);
+  HEI_DISPATCH(c->logn, (k_ct_ntt_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(c->geo, cts)),
+               (k_ct_ntt<<<blocks, c->threads(), sm, st>>>(c->geo, cts, 0)));
+  LAUNCHED();
+}
+void launch_poly_ntt(hei_gpu_ctx* c, unsigned blocks, uint32_t gp, uint32_t* polys, int inverse, cudaStream_t st) {
+  const size_t sm = smem_bytes(c, 1);
+  HEI_DISPATCH(c->logn, (k_poly_ntt_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(c->geo, gp, polys, inverse)),
+               (k_poly_ntt<<<blocks, c->threads(), sm, st>>>(c->geo, gp, polys, inverse)));
+  LAUNCHED();
+}
+template <int LG>
+void set_fast_attrs(size_t sm) {
+  set_smem_attr((const void*)k_rot_digits_f<LG>, sm);
+  set_smem_attr((const void*)k_rot_keyswitch_f<LG>, sm);
+  set_smem_attr((const void*)k_mask_acc_f<LG>, sm);
+  set_smem_attr((const void*)k_ct_ntt_f<LG>, sm);
+  set_smem_attr((const void*)k_poly_ntt_f<LG>, sm);
+}
+
 uint64_t auto_batch_pairs(hei_gpu_ctx* c) {
   if (c->batch_pairs) return c->batch_pairs;
   // Enough (pair, prime) blocks for several waves on 148 SMs while keeping the
@@ -610,17 +888,13 @@ uint64_t auto_batch_pairs(hei_gpu_ctx* c) {
 // returns the buffer holding the result.
 uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st) {
   const Geo& g = c->geo;
-  const unsigned T = c->threads();
-  const size_t sm1 = smem_bytes(c, 1), sm3 = smem_bytes(c, 3);
   const unsigned blocks = (unsigned)(pairs * c->P());
   for (uint64_t elt : c->fold_elts) {
     const uint32_t* perm = c->d_perms + (size_t)c->perm_index.at(elt) * c->n;
     const uint2* k0 = c->d_keys[0] + (size_t)c->key_index[0].at(elt) * c->L[0] * 2 * c->L[0] * c->n;
     const uint2* k1 = c->d_keys[1] + (size_t)c->key_index[1].at(elt) * c->L[1] * 2 * c->L[1] * c->n;
-    k_rot_digits<<<blocks, T, sm1, st>>>(g, cur, perm, c->d_dig);
-    LAUNCHED();
-    k_rot_keyswitch<<<blocks, T, sm3, st>>>(g, cur, c->d_dig, perm, k0, k1, other, 1);
-    LAUNCHED();
+    launch_rot_digits(c, g, blocks, cur, perm, c->d_dig, st);
+    launch_rot_keyswitch(c, g, blocks, cur, c->d_dig, perm, k0, k1, other, 1, st);
     std::swap(cur, other);
   }
   return cur;
@@ -649,8 +923,7 @@ void run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
                                                                                          (uint32_t)w->kc, c->d_dotA);
   LAUNCHED();
   uint32_t* res = fold(c, pairs, c->d_dotA, c->d_dotB, st);
-  k_mask_acc<<<blocksP, T, smem_bytes(c, 1), st>>>(g, res, d_rows, cols, s->d_acc);
-  LAUNCHED();
+  launch_mask_acc(c, g, blocksP, res, d_rows, cols, s->d_acc, st);
 }
 
 void stream_flush(hei_gpu_stream* s) {
@@ -693,7 +966,8 @@ void capacity_gate(hei_gpu_ctx* c, uint64_t f, const char* who) {
                                " result bits, capacity is " + std::to_string(cap) + "; refusing");
 }
 
-hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64_t* bias, uint64_t rows) {
+hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64_t* bias, uint64_t rows,
+                           bool host_staging = true) {
   if (rows == 0) raise(HEI_PARAM_ERROR, "matmul: empty input");
   if (!w || w->cols == 0 || w->f == 0) raise(HEI_PARAM_ERROR, "matmul: empty weights");
   if (w->ctx != c) raise(HEI_PARAM_ERROR, "matmul: weights encoded for a different context");
@@ -711,8 +985,10 @@ hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64
   CU(cudaMemsetAsync(s->d_acc, 0, s->C * c->ct_words() * 8, c->stream));
   const uint64_t bp = auto_batch_pairs(c);
   s->cap_rows = std::max<uint64_t>(1, std::min<uint64_t>(rows, bp / w->cols));
-  CU(cudaMalloc(&s->d_stage, s->cap_rows * w->kc * c->ct_words() * 4));
-  CU(cudaMalloc(&s->d_stage64, s->cap_rows * w->kc * c->ct_words() * 8));
+  if (host_staging) {
+    CU(cudaMalloc(&s->d_stage, s->cap_rows * w->kc * c->ct_words() * 4));
+    CU(cudaMalloc(&s->d_stage64, s->cap_rows * w->kc * c->ct_words() * 8));
+  }
   CU(cudaMalloc(&s->d_rows, s->cap_rows * 8));
   return s.release();
 }
@@ -740,9 +1016,7 @@ void stream_push(hei_gpu_stream* s, uint64_t row, const uint64_t* chunks, int fo
                                                           s->d_stage + slot * words, s->w->kc, c->d_err);
   LAUNCHED();
   if (form == HEI_FORM_COEFF) {
-    k_ct_ntt<<<(unsigned)(s->w->kc * 2 * c->P()), c->threads(), smem_bytes(c, 1), c->stream>>>(
-        c->geo, s->d_stage + slot * words, 0);
-    LAUNCHED();
+    launch_ct_ntt(c, (unsigned)(s->w->kc * 2 * c->P()), s->d_stage + slot * words, c->stream);
   }
   s->seen[row] = true;
   ++s->pushed;
@@ -963,8 +1237,40 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
         perms[e * n + i] = rev_bits((uint32_t)((src - 1) / 2), c->logn);
       }
     }
+    // pass-C twiddles for the register-blocked transforms (ntt_fast.cuh)
+    std::vector<uint4> twc, itwc;
+    if (c->logn >= 12 && c->logn <= 14) {
+      const uint32_t T = n / 16, XST = c->logn - 12, PAD = XST % 2 == 0 ? 1 : 0, KC = (PAD + XST + 16) / 2;
+      g.twc_stride = KC * T;
+      twc.resize((size_t)(P + 2) * KC * T);
+      itwc.resize(twc.size());
+      std::vector<uint32_t> idx(2 * KC);
+      for (uint32_t row = 0; row < P + 2; ++row)
+        for (uint32_t j = 0; j < T; ++j) {
+          const uint32_t x0 = 16 * j;
+          std::fill(idx.begin(), idx.end(), 0u);
+          uint32_t e = PAD;
+          for (uint32_t s = 0; s < XST; ++s) idx[e++] = (1u << (8 + s)) + (x0 >> (c->logn - 8 - s));
+          for (uint32_t s = 0; s < 4; ++s)
+            for (uint32_t b = 0; b < (1u << s); ++b) idx[e++] = (1u << (c->logn - 4 + s)) + (x0 >> (4 - s)) + b;
+          for (uint32_t k = 0; k < KC; ++k) {
+            const uint2 a = fwd[(size_t)row * n + idx[2 * k]], b = fwd[(size_t)row * n + idx[2 * k + 1]];
+            const uint2 ia = inv[(size_t)row * n + idx[2 * k]], ib = inv[(size_t)row * n + idx[2 * k + 1]];
+            twc[((size_t)row * KC + k) * T + j] = make_uint4(a.x, a.y, b.x, b.y);
+            itwc[((size_t)row * KC + k) * T + j] = make_uint4(ia.x, ia.y, ib.x, ib.y);
+          }
+        }
+    }
     set_device(c.get());
     CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    if (!twc.empty()) {
+      CU(cudaMalloc(&c->d_twc, twc.size() * sizeof(uint4)));
+      CU(cudaMalloc(&c->d_itwc, itwc.size() * sizeof(uint4)));
+      CU(cudaMemcpy(c->d_twc, twc.data(), twc.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(c->d_itwc, itwc.data(), itwc.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+      g.twc = c->d_twc;
+      g.itwc = c->d_itwc;
+    }
     CU(cudaMalloc(&c->d_fwd, fwd.size() * sizeof(uint2)));
     CU(cudaMalloc(&c->d_inv, inv.size() * sizeof(uint2)));
     CU(cudaMalloc(&c->d_index, n * 4));
@@ -986,6 +1292,9 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     set_smem_attr((const void*)k_ct_ntt, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_poly_ntt, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_encode_weights, smem_bytes(c.get(), 1));
+    if (c->logn == 12) set_fast_attrs<12>(smem_bytes(c.get(), 1));
+    if (c->logn == 13) set_fast_attrs<13>(smem_bytes(c.get(), 1));
+    if (c->logn == 14) set_fast_attrs<14>(smem_bytes(c.get(), 1));
     *out = c.release();
   });
 }
@@ -995,6 +1304,8 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaSetDevice(c->device);
   cudaFree(c->d_fwd);
   cudaFree(c->d_inv);
+  cudaFree(c->d_twc);
+  cudaFree(c->d_itwc);
   cudaFree(c->d_index);
   cudaFree(c->d_perms);
   cudaFree(c->d_err);
@@ -1139,7 +1450,7 @@ int hei_gpu_matmul_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint32
     std::lock_guard<std::mutex> lk(c->mu);
     if (form != HEI_FORM_EVAL) raise(HEI_PARAM_ERROR, "matmul_device: inputs must be in eval form");
     cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
-    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, bias, rows), stream_free);
+    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, bias, rows, false), stream_free);
     CU(cudaStreamSynchronize(c->stream));  // zeroed accumulators visible to `st`
     const size_t words = w->kc * c->ct_words();
     std::vector<uint64_t> idx(s->cap_rows);
@@ -1172,8 +1483,7 @@ int hei_gpu_ntt(hei_gpu_ctx* c, uint32_t b, uint32_t prime, uint64_t* polys, uin
     uint32_t* d = nullptr;
     CU(cudaMalloc(&d, words * 4));
     CU(cudaMemcpy(d, h32.data(), words * 4, cudaMemcpyHostToDevice));
-    k_poly_ntt<<<(unsigned)count, c->threads(), smem_bytes(c, 1), c->stream>>>(c->geo, gp, d, inverse);
-    LAUNCHED();
+    launch_poly_ntt(c, (unsigned)count, gp, d, inverse, c->stream);
     CU(cudaMemcpyAsync(h32.data(), d, words * 4, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     cudaFree(d);
@@ -1209,6 +1519,10 @@ int hei_gpu_apply_galois(hei_gpu_ctx* c, uint32_t b, uint64_t elt, const uint64_
     // twiddle rows: shift the table base so row i maps to branch prime i
     gb.fwd = g.fwd + (size_t)(b ? c->L[0] : 0) * n;
     gb.inv = g.inv + (size_t)(b ? c->L[0] : 0) * n;
+    if (g.twc) {
+      gb.twc = g.twc + (size_t)(b ? c->L[0] : 0) * g.twc_stride;
+      gb.itwc = g.itwc + (size_t)(b ? c->L[0] : 0) * g.twc_stride;
+    }
     const size_t words = 2ull * L * n;
     std::vector<uint32_t> h32(words);
     for (size_t x = 0; x < words; ++x) h32[x] = (uint32_t)in[x];
@@ -1219,10 +1533,8 @@ int hei_gpu_apply_galois(hei_gpu_ctx* c, uint32_t b, uint64_t elt, const uint64_
     CU(cudaMemcpy(d_in, h32.data(), words * 4, cudaMemcpyHostToDevice));
     const uint32_t* perm = c->d_perms + (size_t)c->perm_index.at(elt) * n;
     const uint2* key = c->d_keys[b] + (size_t)c->key_index[b].at(elt) * L * 2 * L * n;
-    k_rot_digits<<<L, c->threads(), smem_bytes(c, 1), c->stream>>>(gb, d_in, perm, d_dig);
-    LAUNCHED();
-    k_rot_keyswitch<<<L, c->threads(), smem_bytes(c, 3), c->stream>>>(gb, d_in, d_dig, perm, key, key, d_out, 0);
-    LAUNCHED();
+    launch_rot_digits(c, gb, L, d_in, perm, d_dig, c->stream);
+    launch_rot_keyswitch(c, gb, L, d_in, d_dig, perm, key, key, d_out, 0, c->stream);
     CU(cudaMemcpyAsync(h32.data(), d_out, words * 4, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     cudaFree(d_in);

@@ -1,0 +1,266 @@
+// Register-blocked negacyclic NTT for N = 2^LOGN, LOGN in {12, 13, 14}.
+//
+// One CTA of T = N/16 threads transforms one polynomial; every thread keeps
+// 16 residues in registers for the whole transform and the 13 (14) radix-2
+// stages run as three register passes with two shared-memory exchanges:
+//
+//   pass A  stages 0..3          thread j holds x = j + T*r          (r < 16)
+//   pass B  stages 4..7          x = blk*(N/16) + jj + (N/256)*r
+//   pass C  stages 8..LOGN-1     x = grp*G + 16*h + r, G = N/256; the first
+//                                LOGN-12 stages of pass C pair threads and
+//                                exchange through warp shuffles.
+//
+// The forward transform consumes pass-A order (natural coefficients, which
+// coalesce in global memory) and leaves pass-C order (16 contiguous eval
+// slots per thread); the inverse does the reverse. Shared memory is swizzled
+// (x ^ (((x >> 5) & 7) << 2)) so all three access patterns are free of bank
+// conflicts and pass C can use 128-bit accesses.
+//
+// The butterflies are the reference's (modops_scalar.cpp:45-81): forward
+// Cooley–Tukey with zetas[m + i] = psi^{bitrev(m + i)}, inverse
+// Gentleman–Sande with inv_zetas and a final n^-1 scaling folded into the
+// last stage. Values stay strictly reduced, so results are bit-identical.
+#pragma once
+#include "modmath.cuh"
+
+namespace heb {
+
+__device__ __forceinline__ uint32_t swz(uint32_t x) { return x ^ (((x >> 5) & 7u) << 2); }
+
+template <int LOGN>
+struct Ntt {
+  static constexpr uint32_t N = 1u << LOGN;
+  static constexpr uint32_t T = N / 16;          // threads per polynomial
+  static constexpr uint32_t G = N >> 8;          // pass-C block size
+  static constexpr uint32_t TPG = G / 16;        // threads per pass-C block
+  static constexpr int XST = LOGN - 12;          // cross-thread stages in pass C
+  // Pass-C twiddles are stored per thread, transposed for coalescing:
+  // tc[k * T + j] (uint4 = two (w, shoup) entries). Entry order:
+  // [pad][cross stages 0..XST-1][stage s0 (1)][s1 (2)][s2 (4)][s3 (8)],
+  // with one pad entry when XST is even so every s>=1 group starts even.
+  static constexpr int PAD = (XST % 2 == 0) ? 1 : 0;
+  static constexpr int B0 = PAD + XST;           // entry of register stage 0
+  static constexpr int KC = (PAD + XST + 15 + 1) / 2;  // uint4 per thread
+  static __device__ __forceinline__ uint2 lo(uint4 v) { return make_uint2(v.x, v.y); }
+  static __device__ __forceinline__ uint2 hi(uint4 v) { return make_uint2(v.z, v.w); }
+  static __device__ __forceinline__ uint2 entry(const uint4* __restrict__ tc, int e) {
+    const uint4 v = __ldg(tc + (e >> 1) * T);
+    return (e & 1) ? hi(v) : lo(v);
+  }
+
+  // pass-A position of register r
+  static __device__ __forceinline__ uint32_t posA(uint32_t j, uint32_t r) { return j + T * r; }
+  // pass-B position
+  static __device__ __forceinline__ uint32_t posB(uint32_t j, uint32_t r) {
+    const uint32_t blk = j >> (LOGN - 8), jj = j & ((N >> 8) - 1);
+    return blk * (N / 16) + jj + (N >> 8) * r;
+  }
+  // pass-C position (first of the 16 contiguous slots)
+  static __device__ __forceinline__ uint32_t posC0(uint32_t j) {
+    const uint32_t grp = j / TPG, h = j % TPG;
+    return grp * G + 16 * h;
+  }
+
+  static __device__ __forceinline__ void ct(uint32_t& u, uint32_t& v, uint2 w, uint32_t q) {
+    const uint32_t t = mul_shoup(v, w.x, w.y, q);
+    v = sub_mod(u, t, q);
+    u = add_mod(u, t, q);
+  }
+  static __device__ __forceinline__ void gs(uint32_t& u, uint32_t& v, uint2 w, uint32_t q) {
+    const uint32_t d = sub_mod(u, v, q);
+    u = add_mod(u, v, q);
+    v = mul_shoup(d, w.x, w.y, q);
+  }
+
+  static __device__ __forceinline__ void store_pos(uint32_t* sm, uint32_t x, uint32_t v) { sm[swz(x)] = v; }
+  static __device__ __forceinline__ void storeC(uint32_t* sm, uint32_t j, const uint32_t (&e)[16]) {
+    const uint32_t x0 = posC0(j);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      *reinterpret_cast<uint4*>(sm + swz(x0 + 4 * c)) = make_uint4(e[4 * c], e[4 * c + 1], e[4 * c + 2], e[4 * c + 3]);
+  }
+  static __device__ __forceinline__ void loadC(const uint32_t* sm, uint32_t j, uint32_t (&e)[16]) {
+    const uint32_t x0 = posC0(j);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 v = *reinterpret_cast<const uint4*>(sm + swz(x0 + 4 * c));
+      e[4 * c] = v.x;
+      e[4 * c + 1] = v.y;
+      e[4 * c + 2] = v.z;
+      e[4 * c + 3] = v.w;
+    }
+  }
+
+  // Forward: e in pass-A order -> e in pass-C order. Begins and ends with a
+  // barrier on the shared buffer (sm: N words).
+  static __device__ __forceinline__ void fwd(uint32_t (&e)[16], uint32_t* sm, const uint2* __restrict__ tw,
+                                             const uint4* __restrict__ twc, uint32_t q) {
+    const uint32_t j = threadIdx.x;
+    // ---- pass A: stages 0..3
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int half = 8 >> s;
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (!(r & half)) ct(e[r], e[r + half], __ldg(&tw[(1 << s) + (r >> (4 - s))]), q);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) store_pos(sm, posA(j, r), e[r]);
+    __syncthreads();
+    // ---- pass B: stages 4..7
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = sm[swz(posB(j, r))];
+    {
+      const uint32_t blk = j >> (LOGN - 8);
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const int half = 8 >> s;
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if (!(r & half)) ct(e[r], e[r + half], __ldg(&tw[(16u << s) + (blk << s) + (r >> (4 - s))]), q);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sm[swz(posB(j, r))] = e[r];
+    __syncthreads();
+    // ---- pass C: stages 8..LOGN-1
+    loadC(sm, j, e);
+    const uint32_t x0 = posC0(j);
+    const uint4* tc = twc + j;
+#pragma unroll
+    for (int s = 0; s < XST; ++s) {
+      // stage st = 8 + s, t = G >> (s + 1) >= 16: partner thread h ^ (t / 16)
+      const uint32_t t = G >> (s + 1);
+      const uint32_t lanebit = t / 16;
+      const bool upper = (x0 & t) != 0;
+      const uint2 w = entry(tc, PAD + s);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t mine = upper ? mul_shoup(e[r], w.x, w.y, q) : e[r];
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, mine, lanebit);
+        e[r] = upper ? sub_mod(other, mine, q) : add_mod(mine, other, q);
+      }
+    }
+    ct(e[0], e[8], entry(tc, B0), q);
+#pragma unroll
+    for (int r = 1; r < 8; ++r) ct(e[r], e[r + 8], entry(tc, B0), q);
+    {
+      const uint4 v = __ldg(tc + ((B0 + 1) >> 1) * T);
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (!(r & 4)) ct(e[r], e[r + 4], (r >> 3) ? hi(v) : lo(v), q);
+    }
+    {
+      const uint4 v0 = __ldg(tc + ((B0 + 3) >> 1) * T), v1 = __ldg(tc + ((B0 + 5) >> 1) * T);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if (r & 2) continue;
+        const int b = r >> 2;
+        const uint4 v = b < 2 ? v0 : v1;
+        ct(e[r], e[r + 2], (b & 1) ? hi(v) : lo(v), q);
+      }
+    }
+    {
+      uint4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = __ldg(tc + ((B0 + 7) / 2 + k) * T);
+#pragma unroll
+      for (int r = 0; r < 16; r += 2) {
+        const int b = r >> 1;
+        ct(e[r], e[r + 1], (b & 1) ? hi(v[b >> 1]) : lo(v[b >> 1]), q);
+      }
+    }
+  }
+
+  // Inverse: e in pass-C order (eval slots) -> e in pass-A order (natural
+  // coefficients), scaled by n^-1. Begins and ends with a barrier.
+  static __device__ __forceinline__ void inv(uint32_t (&e)[16], uint32_t* sm, const uint2* __restrict__ itw,
+                                             const uint4* __restrict__ itwc, uint32_t q, uint2 last, uint2 ninv) {
+    const uint32_t j = threadIdx.x;
+    const uint32_t x0 = posC0(j);
+    const uint4* tc = itwc + j;
+    // ---- pass C: stages LOGN-1 .. 8 (register stages first: t = 1, 2, 4, 8)
+    {
+      uint4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = __ldg(tc + ((B0 + 7) / 2 + k) * T);
+#pragma unroll
+      for (int r = 0; r < 16; r += 2) {
+        const int b = r >> 1;
+        gs(e[r], e[r + 1], (b & 1) ? hi(v[b >> 1]) : lo(v[b >> 1]), q);
+      }
+    }
+    {
+      const uint4 v0 = __ldg(tc + ((B0 + 3) >> 1) * T), v1 = __ldg(tc + ((B0 + 5) >> 1) * T);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if (r & 2) continue;
+        const int b = r >> 2;
+        const uint4 v = b < 2 ? v0 : v1;
+        gs(e[r], e[r + 2], (b & 1) ? hi(v) : lo(v), q);
+      }
+    }
+    {
+      const uint4 v = __ldg(tc + ((B0 + 1) >> 1) * T);
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (!(r & 4)) gs(e[r], e[r + 4], (r >> 3) ? hi(v) : lo(v), q);
+    }
+    {
+      const uint2 w = entry(tc, B0);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) gs(e[r], e[r + 8], w, q);
+    }
+#pragma unroll
+    for (int s = XST - 1; s >= 0; --s) {
+      const uint32_t t = G >> (s + 1);
+      const uint32_t lanebit = t / 16;
+      const bool upper = (x0 & t) != 0;
+      const uint2 w = entry(tc, PAD + s);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, e[r], lanebit);
+        // lower keeps u + v; upper keeps (u - v) * w
+        e[r] = upper ? mul_shoup(sub_mod(other, e[r], q), w.x, w.y, q) : add_mod(e[r], other, q);
+      }
+    }
+    __syncthreads();
+    storeC(sm, j, e);
+    __syncthreads();
+    // ---- pass B: stages 7..4
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = sm[swz(posB(j, r))];
+    {
+      const uint32_t blk = j >> (LOGN - 8);
+#pragma unroll
+      for (int s = 3; s >= 0; --s) {
+        const int half = 8 >> s;
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if (!(r & half)) gs(e[r], e[r + half], __ldg(&itw[(16u << s) + (blk << s) + (r >> (4 - s))]), q);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sm[swz(posB(j, r))] = e[r];
+    __syncthreads();
+    // ---- pass A: stages 3..1, then stage 0 fused with the n^-1 scaling
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = sm[swz(posA(j, r))];
+#pragma unroll
+    for (int s = 3; s >= 1; --s) {
+      const int half = 8 >> s;
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (!(r & half)) gs(e[r], e[r + half], __ldg(&itw[(1 << s) + (r >> (4 - s))]), q);
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint32_t u = e[r], v = e[r + 8];
+      e[r] = mul_shoup(add_mod(u, v, q), ninv.x, ninv.y, q);
+      e[r + 8] = mul_shoup(sub_mod(u, v, q), last.x, last.y, q);
+    }
+  }
+};
+
+}  // namespace heb
