@@ -684,6 +684,112 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T) k_rot_keyswitch_f(Geo g, const u
   store16(o + (uint64_t)pr.poly1 * N + x0, acc1);
 }
 
+
+// Same as k_rot_keyswitch_f but the two accumulators live in shared memory
+// (transposed [c][T] uint4, conflict-free), which keeps the kernel under 64
+// registers so two 512-thread CTAs share an SM (32 warps for latency hiding).
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_rot_keyswitch_s(Geo g, const uint32_t* __restrict__ dot,
+                                                                    const uint32_t* __restrict__ digits,
+                                                                    const uint32_t* __restrict__ perm,
+                                                                    const uint2* __restrict__ key0,
+                                                                    const uint2* __restrict__ key1,
+                                                                    uint32_t* __restrict__ out, int fold) {
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N, T = NT::T;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  uint4* a0s = smem4 + N / 4;
+  uint4* a1s = a0s + 4 * T;
+  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t q = pr.q, L = pr.L, i = pr.i;
+  const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
+  const uint32_t* ct = dot + (uint64_t)pair * g.ct_words;
+  const uint32_t* c0 = ct + (uint64_t)pr.poly0 * N;
+  const uint32_t* c1 = ct + (uint64_t)pr.poly1 * N;
+  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * N;
+  {
+    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * N) + j;
+    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * N) + j;
+    const uint4* pp = reinterpret_cast<const uint4*>(perm + x0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 pm = __ldg(pp + c);
+      const uint32_t d0 = c1[pm.x], d1 = c1[pm.y], d2 = c1[pm.z], d3 = c1[pm.w];
+      const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
+      const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
+      a0s[c * T + j] = make_uint4(mul_shoup(d0, a.x, a.y, q), mul_shoup(d1, a.z, a.w, q), mul_shoup(d2, b.x, b.y, q),
+                                  mul_shoup(d3, b.z, b.w, q));
+      a1s[c * T + j] = make_uint4(mul_shoup(d0, u.x, u.y, q), mul_shoup(d1, u.z, u.w, q), mul_shoup(d2, v.x, v.y, q),
+                                  mul_shoup(d3, v.z, v.w, q));
+    }
+  }
+  const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
+  const uint2* tw = g.fwd + (size_t)gp * N;
+  const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
+  uint32_t e[16];
+  for (uint32_t l = 0; l < L; ++l) {
+    if (l == i) continue;
+    const uint32_t* src = dig + (uint64_t)l * N;
+    if (pr.fast_reduce) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t v = src[NT::posA(j, r)];
+        e[r] = min(v, v - q);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
+    }
+    NT::fwd(e, sm, tw, twc, q);
+    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
+    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
+      uint4 A = a0s[c * T + j];
+      A.x = add_mod(A.x, mul_shoup(e[4 * c], a.x, a.y, q), q);
+      A.y = add_mod(A.y, mul_shoup(e[4 * c + 1], a.z, a.w, q), q);
+      A.z = add_mod(A.z, mul_shoup(e[4 * c + 2], b.x, b.y, q), q);
+      A.w = add_mod(A.w, mul_shoup(e[4 * c + 3], b.z, b.w, q), q);
+      a0s[c * T + j] = A;
+      const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
+      uint4 B = a1s[c * T + j];
+      B.x = add_mod(B.x, mul_shoup(e[4 * c], u.x, u.y, q), q);
+      B.y = add_mod(B.y, mul_shoup(e[4 * c + 1], u.z, u.w, q), q);
+      B.z = add_mod(B.z, mul_shoup(e[4 * c + 2], v.x, v.y, q), q);
+      B.w = add_mod(B.w, mul_shoup(e[4 * c + 3], v.z, v.w, q), q);
+      a1s[c * T + j] = B;
+    }
+  }
+  uint32_t* o = out + (uint64_t)pair * g.ct_words;
+  const uint4* pp = reinterpret_cast<const uint4*>(perm + x0);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 pm = __ldg(pp + c);
+    uint4 A = a0s[c * T + j], B = a1s[c * T + j];
+    A.x = add_mod(A.x, c0[pm.x], q);
+    A.y = add_mod(A.y, c0[pm.y], q);
+    A.z = add_mod(A.z, c0[pm.z], q);
+    A.w = add_mod(A.w, c0[pm.w], q);
+    if (fold) {
+      const uint4 u = *reinterpret_cast<const uint4*>(c0 + x0 + 4 * c);
+      const uint4 v = *reinterpret_cast<const uint4*>(c1 + x0 + 4 * c);
+      A.x = add_mod(A.x, u.x, q);
+      A.y = add_mod(A.y, u.y, q);
+      A.z = add_mod(A.z, u.z, q);
+      A.w = add_mod(A.w, u.w, q);
+      B.x = add_mod(B.x, v.x, q);
+      B.y = add_mod(B.y, v.y, q);
+      B.z = add_mod(B.z, v.z, q);
+      B.w = add_mod(B.w, v.w, q);
+    }
+    *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly0 * N + x0 + 4 * c) = A;
+    *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly1 * N + x0 + 4 * c) = B;
+  }
+}
+
 template <int LOGN>
 __global__ void __launch_bounds__(Ntt<LOGN>::T) k_mask_acc_f(Geo g, const uint32_t* __restrict__ dot,
                                                             const uint64_t* __restrict__ rows, uint32_t cols,
@@ -842,7 +948,8 @@ void launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const u
                           const uint32_t* perm, const uint2* k0, const uint2* k1, uint32_t* out, int fold,
                           cudaStream_t st) {
   HEI_DISPATCH(c->logn,
-               (k_rot_keyswitch_f<LG><<<blocks, Ntt<LG>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, out, fold)),
+               (LG <= 13 ? k_rot_keyswitch_s<LG><<<blocks, Ntt<LG>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold)
+                         : k_rot_keyswitch_f<LG><<<blocks, Ntt<LG>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, out, fold))),
                (k_rot_keyswitch<<<blocks, c->threads(), smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold)));
   LAUNCHED();
 }
@@ -869,6 +976,7 @@ template <int LG>
 void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_digits_f<LG>, sm);
   set_smem_attr((const void*)k_rot_keyswitch_f<LG>, sm);
+  set_smem_attr((const void*)k_rot_keyswitch_s<LG>, 3 * sm);
   set_smem_attr((const void*)k_mask_acc_f<LG>, sm);
   set_smem_attr((const void*)k_ct_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_poly_ntt_f<LG>, sm);
