@@ -947,10 +947,21 @@ void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint
 void launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* dig,
                           const uint32_t* perm, const uint2* k0, const uint2* k1, uint32_t* out, int fold,
                           cudaStream_t st) {
-  HEI_DISPATCH(c->logn,
-               (LG <= 13 ? k_rot_keyswitch_s<LG><<<blocks, Ntt<LG>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold)
-                         : k_rot_keyswitch_f<LG><<<blocks, Ntt<LG>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, out, fold))),
-               (k_rot_keyswitch<<<blocks, c->threads(), smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold)));
+  // N <= 8192: shared-memory accumulators, 2 CTAs/SM; N = 16384 (1024
+  // threads) keeps the accumulators in registers.
+  switch (c->logn) {
+    case 12:
+      k_rot_keyswitch_s<12><<<blocks, Ntt<12>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold);
+      break;
+    case 13:
+      k_rot_keyswitch_s<13><<<blocks, Ntt<13>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold);
+      break;
+    case 14:
+      k_rot_keyswitch_f<14><<<blocks, Ntt<14>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, out, fold);
+      break;
+    default:
+      k_rot_keyswitch<<<blocks, c->threads(), smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold);
+  }
   LAUNCHED();
 }
 void launch_mask_acc(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* res, const uint64_t* rows,
