@@ -116,6 +116,8 @@ void hei_gpu_stream_destroy(hei_gpu_stream* s);
  * out [ceil(rows/N)][cols][twin ct] eval form. */
 int hei_gpu_prng_create(uint64_t seed, hei_gpu_prng** out);
 void hei_gpu_prng_destroy(hei_gpu_prng* p);
+/* Draw raw mt19937_64 outputs (test seam: Prng::next, rng.hpp:37). */
+int hei_gpu_prng_draw(hei_gpu_prng* p, uint64_t count, uint64_t* out);
 int hei_gpu_baseline_matmul(hei_gpu_ctx* ctx, const int64_t* x, uint64_t rows, uint64_t f,
                             const int64_t* w, uint64_t cols, const int64_t* bias,
                             hei_gpu_prng* rng0, hei_gpu_prng* rng1, uint64_t* out,

@@ -21,6 +21,8 @@ from .matmul import (  # noqa: F401
     EncodedWeights,
     GpuTwinServer,
     MatmulStream,
+    Prng,
+    baseline_matmul,
     ScalingConfig,
     baseline_counts,
     encode_bias,

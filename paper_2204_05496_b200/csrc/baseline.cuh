@@ -1,0 +1,108 @@
+// Standard (sample-batched) comparator on the device:
+// hei::matmul::baseline_matmul (proj/src/matmul/matmul.cpp:415-486).
+//
+// Per feature k and sample block: the column x[:, k] is encrypted with the
+// public key (BfvContext::encrypt_parts, context.cpp:262-303) using the SAME
+// randomness stream as the reference's util::Prng (rng.hpp:19-68), then
+// multiplied by the all-slot constant w(k, j) for every class j and summed.
+//
+// Device pipeline per batch of F features:
+//   k_mt_generate   mt19937_64 replay, one CTA per branch (the stream is
+//                   sequential; the twist runs as two parallel phases)
+//   k_bl_noise      u = v mod 3 - 1, (e0, e1) = Box-Muller pairs, llround
+//   k_bl_encode     m = INTT_t(scatter(centered col residues))
+//   k_bl_encrypt    c0 = NTT(u).pk0 + NTT(e0 + Delta m), c1 = NTT(u).pk1 + NTT(e1)
+//   k_bl_accum      acc[blk][j] += sum_k c_k * w(k, j)      (u64, order-free)
+// then k_bl_finish reduces mod q and adds the bias plaintext.
+#pragma once
+
+namespace heb_baseline {
+
+constexpr uint64_t kMtUM = 0xFFFFFFFF80000000ULL, kMtLM = 0x7FFFFFFFULL, kMtA = 0xB5026F5AA96619E9ULL;
+
+__device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
+  x ^= (x >> 29) & 0x5555555555555555ULL;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+  x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+  x ^= (x >> 43);
+  return x;
+}
+
+// state: [2][313] (312 words + mti) for the two branches; block b advances
+// branch b by `count` draws into out[b * count ...].
+__global__ void __launch_bounds__(320) k_mt_generate(uint64_t* __restrict__ state, uint64_t* __restrict__ out,
+                                                     uint64_t count) {
+  __shared__ uint64_t mt[312];
+  const uint32_t b = blockIdx.x, t = threadIdx.x;
+  uint64_t* st = state + (uint64_t)b * 313;
+  uint64_t* o = out + (uint64_t)b * count;
+  for (uint32_t i = t; i < 312; i += blockDim.x) mt[i] = st[i];
+  uint32_t mti = (uint32_t)st[312];
+  __syncthreads();
+  uint64_t pos = 0;
+  while (pos < count) {
+    if (mti >= 312) {
+      uint64_t nv = 0;
+      if (t < 156) {
+        const uint64_t y = (mt[t] & kMtUM) | (mt[t + 1] & kMtLM);
+        nv = mt[t + 156] ^ (y >> 1) ^ ((y & 1) ? kMtA : 0);
+      }
+      __syncthreads();
+      if (t < 156) mt[t] = nv;
+      __syncthreads();
+      if (t >= 156 && t < 312) {
+        const uint64_t y = (mt[t] & kMtUM) | (mt[t == 311 ? 0 : t + 1] & kMtLM);
+        nv = mt[t - 156] ^ (y >> 1) ^ ((y & 1) ? kMtA : 0);
+      }
+      __syncthreads();
+      if (t >= 156 && t < 312) mt[t] = nv;
+      __syncthreads();
+      mti = 0;
+    }
+    const uint64_t avail = min((uint64_t)(312 - mti), count - pos);
+    if (t < avail) o[pos + t] = mt_temper(mt[mti + t]);
+    pos += avail;
+    mti += (uint32_t)avail;
+  }
+  __syncthreads();
+  for (uint32_t i = t; i < 312; i += blockDim.x) st[i] = mt[i];
+  if (t == 0) st[312] = mti;
+}
+
+// Noise of one encryption per (e, branch): raw draws [3][N] -> i8 [3][N]
+// (sample_ternary, sample_gaussian twice; sampling.cpp:16-34). The Box-Muller
+// pair (cos first, sin as the cached spare) follows Prng::gaussian. Any
+// rejection (v == 2^64 - 1 for the ternary draw, u1 == 0) would shift the
+// stream; it is flagged and the call fails rather than diverge.
+__global__ void k_bl_noise(const uint64_t* __restrict__ raw, uint64_t count, uint32_t n, uint32_t encs,
+                           int8_t* __restrict__ noise, uint32_t* err) {
+  const uint32_t e = blockIdx.x, b = blockIdx.y;
+  const uint64_t* d = raw + (uint64_t)b * count + (uint64_t)e * 3 * n;
+  int8_t* o = noise + ((uint64_t)e * 2 + b) * 3 * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+    const uint64_t v = d[x];
+    if (v == ~0ull) *err = 1;
+    o[x] = (int8_t)((int)(v % 3) - 1);
+  }
+  const double sigma = 3.2, bound = 6.0 * sigma, two_pi = 6.283185307179586476925286766559;
+  for (uint32_t s = 0; s < 2; ++s) {
+    const uint64_t* g = d + n + (uint64_t)s * n;
+    int8_t* og = o + n + s * n;
+    for (uint32_t k = threadIdx.x; k < n / 2; k += blockDim.x) {
+      const double u1 = (double)(g[2 * k] >> 11) * 0x1.0p-53;
+      const double u2 = (double)(g[2 * k + 1] >> 11) * 0x1.0p-53;
+      if (u1 <= 0.0) *err = 1;
+      const double mag = sqrt(-2.0 * log(u1));
+      double sn, cs;
+      sincos(two_pi * u2, &sn, &cs);
+      double x0 = mag * cs * sigma, x1 = mag * sn * sigma;
+      x0 = x0 > bound ? bound : (x0 < -bound ? -bound : x0);
+      x1 = x1 > bound ? bound : (x1 < -bound ? -bound : x1);
+      og[2 * k] = (int8_t)llround(x0);
+      og[2 * k + 1] = (int8_t)llround(x1);
+    }
+  }
+  (void)encs;
+}
+
+}  // namespace heb_baseline

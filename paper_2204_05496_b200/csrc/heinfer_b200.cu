@@ -38,6 +38,7 @@
 #include "../../include/heinfer_b200.h"
 #include "modmath.cuh"
 #include "ntt_fast.cuh"
+#include "baseline.cuh"
 
 using namespace heb;
 
@@ -826,6 +827,289 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T) k_mask_acc_f(Geo g, const uint32
   for (int r = 0; r < 16; ++r) atomicAdd(&a1[r], (unsigned long long)mul_barrett(d[r], e[r], q, pr.mu));
 }
 
+// ---------------------------------------------------------------------------
+// Standard algorithm (baseline_matmul) kernels; see baseline.cuh.
+// ---------------------------------------------------------------------------
+// m = INTT_t(scatter(centered residues of x[base + s][k])) per (encryption,
+// branch); encryption e = kk * B + blk (matmul.cpp:444-452 loop order).
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T) k_bl_encode(Geo g, const int64_t* __restrict__ x, uint64_t R,
+                                                           uint64_t f, uint64_t k0, uint32_t B,
+                                                           uint32_t* __restrict__ m_out) {
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t e = blockIdx.x, b = blockIdx.y;
+  const uint64_t k = k0 + e / B;
+  const uint64_t base = (uint64_t)(e % B) * N;
+  const uint64_t rows_b = min((uint64_t)N, R - base);
+  const BranchInfo& br = g.br[b];
+  const int64_t t = br.t;
+  for (uint32_t s = threadIdx.x; s < N; s += blockDim.x) {
+    int64_t r = 0;
+    if (s < rows_b) {
+      r = x[(base + s) * f + k] % t;
+      if (r < 0) r += t;
+    }
+    sm[swz(g.index_map[s])] = (uint32_t)r;
+  }
+  __syncthreads();
+  uint32_t v[16];
+  NT::loadC(sm, threadIdx.x, v);
+  NT::inv(v, sm, g.inv + (size_t)(g.P + b) * N, g.itwc + (size_t)(g.P + b) * g.twc_stride, br.t, br.last, br.ninv);
+  uint32_t* o = m_out + ((uint64_t)e * 2 + b) * N;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) o[NT::posA(threadIdx.x, r)] = v[r];
+}
+
+__device__ __forceinline__ uint32_t lift_small(int32_t v, uint32_t q) { return v >= 0 ? (uint32_t)v : q - (uint32_t)(-v); }
+
+// Public-key encryption in eval form, block per (encryption, gp)
+// (context.cpp:270-301): c0 = NTT(u) pk0 + NTT(e0 + Delta m),
+// c1 = NTT(u) pk1 + NTT(e1). pk is prepared [gp][part] in the pass-C
+// transposed layout.
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T) k_bl_encrypt(Geo g, const int8_t* __restrict__ noise,
+                                                            const uint32_t* __restrict__ m,
+                                                            const uint2* __restrict__ pkd,
+                                                            uint32_t* __restrict__ cts) {
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N, T = NT::T;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t e = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t q = pr.q, b = pr.b, j = threadIdx.x, x0 = NT::posC0(j);
+  const int8_t* nz = noise + ((uint64_t)e * 2 + b) * 3 * N;
+  const uint32_t* mm = m + ((uint64_t)e * 2 + b) * N;
+  const uint2* tw = g.fwd + (size_t)gp * N;
+  const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
+  uint32_t* ct = cts + (uint64_t)e * g.ct_words;
+  uint32_t* c0 = ct + (uint64_t)pr.poly0 * N + x0;
+  uint32_t* c1 = ct + (uint64_t)pr.poly1 * N + x0;
+  const uint4* p0 = reinterpret_cast<const uint4*>(pkd + (uint64_t)(2 * gp) * N) + j;
+  const uint4* p1 = reinterpret_cast<const uint4*>(pkd + (uint64_t)(2 * gp + 1) * N) + j;
+  uint32_t v[16], w[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = lift_small(nz[NT::posA(j, r)], q);
+  NT::fwd(v, sm, tw, twc, q);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 a = __ldg(p0 + c * T), bb = __ldg(p1 + c * T);
+    w[2 * c] = mul_shoup(v[2 * c], bb.x, bb.y, q);
+    w[2 * c + 1] = mul_shoup(v[2 * c + 1], bb.z, bb.w, q);
+    v[2 * c] = mul_shoup(v[2 * c], a.x, a.y, q);
+    v[2 * c + 1] = mul_shoup(v[2 * c + 1], a.z, a.w, q);
+  }
+  store16(c0, v);
+  store16(c1, w);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const uint32_t pa = NT::posA(j, r);
+    v[r] = add_mod(lift_small(nz[N + pa], q), mul_shoup(mm[pa], pr.delta.x, pr.delta.y, q), q);
+  }
+  NT::fwd(v, sm, tw, twc, q);
+  load16(c0, w);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) w[r] = add_mod(w[r], v[r], q);
+  store16(c0, w);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = lift_small(nz[2 * N + NT::posA(j, r)], q);
+  NT::fwd(v, sm, tw, twc, q);
+  load16(c1, w);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) w[r] = add_mod(w[r], v[r], q);
+  store16(c1, w);
+}
+
+// acc[blk][j] += sum_k ct[k, blk] * w(k, j) mod q, lazily in u64
+// (mul_plain + add_inplace of matmul.cpp:453-459). Thread per slot x of one
+// poly; weights of the batch for this branch sit in shared memory.
+constexpr int kBlJ = 12;
+__global__ void k_bl_accum(Geo g, const uint32_t* __restrict__ cts, uint32_t F, uint32_t B, uint32_t cols,
+                           uint32_t j0, const uint2* __restrict__ wc, unsigned long long* __restrict__ acc) {
+  extern __shared__ uint2 wsm[];  // [F][kBlJ]
+  const uint32_t n = g.n, polys = 2 * g.P;
+  const uint32_t tiles = n / blockDim.x;
+  const uint32_t tile = blockIdx.x % tiles;
+  const uint32_t poly = (blockIdx.x / tiles) % polys;
+  const uint32_t blk = blockIdx.x / (tiles * polys);
+  const uint32_t gp = poly_prime(g, poly);
+  const uint32_t q = g.pr[gp].q, b = g.pr[gp].b;
+  const uint32_t jn = min((uint32_t)kBlJ, cols - j0);
+  for (uint32_t x = threadIdx.x; x < F * kBlJ; x += blockDim.x) {
+    const uint32_t kk = x / kBlJ, jj = x % kBlJ;
+    wsm[x] = jj < jn ? wc[((uint64_t)kk * cols + j0 + jj) * g.P + gp] : make_uint2(0, 0);
+  }
+  __syncthreads();
+  const uint32_t xs = tile * blockDim.x + threadIdx.x;
+  unsigned long long a[kBlJ];
+#pragma unroll
+  for (int jj = 0; jj < kBlJ; ++jj) a[jj] = 0;
+  for (uint32_t kk = 0; kk < F; ++kk) {
+    const uint32_t v = cts[((uint64_t)kk * B + blk) * g.ct_words + (uint64_t)poly * n + xs];
+#pragma unroll
+    for (int jj = 0; jj < kBlJ; ++jj) {
+      const uint2 w = wsm[kk * kBlJ + jj];
+      const uint32_t qh = __umulhi(v, w.y);
+      a[jj] += (uint32_t)(v * w.x - qh * q);  // in [0, 2q): reduced at the end
+    }
+  }
+  (void)b;
+  for (uint32_t jj = 0; jj < jn; ++jj) {
+    unsigned long long* d = acc + (((uint64_t)blk * cols + j0 + jj) * g.ct_words) + (uint64_t)poly * n + xs;
+    *d += a[jj];
+  }
+}
+
+// finish of the baseline (matmul.cpp:464-476): reduce, then part0 +=
+// NTT(Delta * INTT_t(all slots = bias[j])). Block per ((blk, j), gp).
+__global__ void k_bl_finish(Geo g, const unsigned long long* __restrict__ acc, const int64_t* __restrict__ bias,
+                            uint32_t cols, uint32_t* __restrict__ out) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = g.n;
+  const uint64_t c = blockIdx.x / g.P;  // (blk * cols + j)
+  const uint32_t gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const BranchInfo& br = g.br[pr.b];
+  const int64_t t = br.t;
+  int64_t r = bias[c % cols] % t;
+  if (r < 0) r += t;
+  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) sm[g.index_map[s]] = (uint32_t)r;
+  __syncthreads();
+  ntt_inv_smem(sm, g.inv + (size_t)(g.P + pr.b) * n, br.t, n, g.logn, br.last, br.ninv);
+  const uint32_t q = pr.q;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = mul_shoup(sm[x], pr.delta.x, pr.delta.y, q);
+  __syncthreads();
+  ntt_fwd_smem(sm, g.fwd + (size_t)gp * n, q, n, g.logn);
+  const unsigned long long* a0 = acc + c * g.ct_words + (uint64_t)pr.poly0 * n;
+  const unsigned long long* a1 = acc + c * g.ct_words + (uint64_t)pr.poly1 * n;
+  uint32_t* o0 = out + c * g.ct_words + (uint64_t)pr.poly0 * n;
+  uint32_t* o1 = out + c * g.ct_words + (uint64_t)pr.poly1 * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+    o0[x] = add_mod((uint32_t)(a0[x] % q), sm[x], q);
+    o1[x] = (uint32_t)(a1[x] % q);
+  }
+}
+
+// Public key coeff [b][2][L][n] u64 -> eval-form prepared [gp][part] in the
+// pass-C transposed layout (prepare_public, context.cpp:175-187).
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T) k_prepare_pk(Geo g, const uint64_t* __restrict__ pk0,
+                                                            const uint64_t* __restrict__ pk1, uint2* __restrict__ out,
+                                                            uint32_t* err) {
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N, T = NT::T;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t gp = blockIdx.x / 2, part = blockIdx.x % 2;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint64_t* src = (pr.b ? pk1 : pk0) + ((uint64_t)part * pr.L + pr.i) * N;
+  const uint32_t j = threadIdx.x;
+  uint32_t v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const uint64_t a = src[NT::posA(j, r)];
+    if (a >= pr.q) *err = 1;
+    v[r] = (uint32_t)a;
+  }
+  NT::fwd(v, sm, g.fwd + (size_t)gp * N, g.twc + (size_t)gp * g.twc_stride, pr.q);
+  uint4* o = reinterpret_cast<uint4*>(out + (uint64_t)(2 * gp + part) * N) + j;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint32_t a = v[2 * c], bb = v[2 * c + 1];
+    o[c * T] = make_uint4(a, (uint32_t)(((uint64_t)a << 32) / pr.q), bb, (uint32_t)(((uint64_t)bb << 32) / pr.q));
+  }
+}
+
+// Generic (small-ring) versions of the baseline encoders, natural layouts.
+__global__ void k_bl_encode_g(Geo g, const int64_t* __restrict__ x, uint64_t R, uint64_t f, uint64_t k0, uint32_t B,
+                              uint32_t* __restrict__ m_out) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = g.n, e = blockIdx.x, b = blockIdx.y;
+  const uint64_t k = k0 + e / B, base = (uint64_t)(e % B) * n;
+  const uint64_t rows_b = min((uint64_t)n, R - base);
+  const BranchInfo& br = g.br[b];
+  const int64_t t = br.t;
+  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+    int64_t r = 0;
+    if (s < rows_b) {
+      r = x[(base + s) * f + k] % t;
+      if (r < 0) r += t;
+    }
+    sm[g.index_map[s]] = (uint32_t)r;
+  }
+  __syncthreads();
+  ntt_inv_smem(sm, g.inv + (size_t)(g.P + b) * n, br.t, n, g.logn, br.last, br.ninv);
+  uint32_t* o = m_out + ((uint64_t)e * 2 + b) * n;
+  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) o[s] = sm[s];
+}
+
+__global__ void k_bl_encrypt_g(Geo g, const int8_t* __restrict__ noise, const uint32_t* __restrict__ m,
+                               const uint2* __restrict__ pkd, uint32_t* __restrict__ cts) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = g.n, e = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t q = pr.q, b = pr.b;
+  const int8_t* nz = noise + ((uint64_t)e * 2 + b) * 3 * n;
+  const uint32_t* mm = m + ((uint64_t)e * 2 + b) * n;
+  const uint2* tw = g.fwd + (size_t)gp * n;
+  uint32_t* c0 = cts + (uint64_t)e * g.ct_words + (uint64_t)pr.poly0 * n;
+  uint32_t* c1 = cts + (uint64_t)e * g.ct_words + (uint64_t)pr.poly1 * n;
+  const uint2* p0 = pkd + (uint64_t)(2 * gp) * n;
+  const uint2* p1 = pkd + (uint64_t)(2 * gp + 1) * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = lift_small(nz[x], q);
+  __syncthreads();
+  ntt_fwd_smem(sm, tw, q, n, g.logn);
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+    c0[x] = mul_shoup(sm[x], p0[x].x, p0[x].y, q);
+    c1[x] = mul_shoup(sm[x], p1[x].x, p1[x].y, q);
+  }
+  __syncthreads();
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x)
+    sm[x] = add_mod(lift_small(nz[n + x], q), mul_shoup(mm[x], pr.delta.x, pr.delta.y, q), q);
+  __syncthreads();
+  ntt_fwd_smem(sm, tw, q, n, g.logn);
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) c0[x] = add_mod(c0[x], sm[x], q);
+  __syncthreads();
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = lift_small(nz[2 * n + x], q);
+  __syncthreads();
+  ntt_fwd_smem(sm, tw, q, n, g.logn);
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) c1[x] = add_mod(c1[x], sm[x], q);
+}
+
+__global__ void k_prepare_pk_g(Geo g, const uint64_t* __restrict__ pk0, const uint64_t* __restrict__ pk1,
+                               uint2* __restrict__ out, uint32_t* err) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = g.n, gp = blockIdx.x / 2, part = blockIdx.x % 2;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint64_t* src = (pr.b ? pk1 : pk0) + ((uint64_t)part * pr.L + pr.i) * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+    if (src[x] >= pr.q) *err = 1;
+    sm[x] = (uint32_t)src[x];
+  }
+  __syncthreads();
+  ntt_fwd_smem(sm, g.fwd + (size_t)gp * n, pr.q, n, g.logn);
+  uint2* o = out + (uint64_t)(2 * gp + part) * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x)
+    o[x] = make_uint2(sm[x], (uint32_t)(((uint64_t)sm[x] << 32) / pr.q));
+}
+
+// prepare_constant_signed (twin.cpp:424-436, context.cpp:120-137) for every
+// (feature, class): centered residue mod t_b with its Shoup constant mod q_i.
+__global__ void k_bl_weights(Geo g, const int64_t* __restrict__ w, uint64_t count, uint2* __restrict__ out) {
+  const uint64_t total = count * g.P;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t gp = (uint32_t)(x % g.P);
+    const PrimeInfo& pr = g.pr[gp];
+    const int64_t t = g.br[pr.b].t;
+    int64_t r = w[x / g.P] % t;
+    if (r < 0) r += t;
+    out[x] = make_uint2((uint32_t)r, (uint32_t)(((uint64_t)r << 32) / pr.q));
+  }
+}
+
 }  // namespace
 
 // ================================================================ host side
@@ -848,6 +1132,7 @@ struct hei_gpu_ctx {
   std::map<uint64_t, uint32_t> key_index[2];  // elt -> e
   bool has_keys[2] = {false, false};
   uint64_t* d_pk[2] = {nullptr, nullptr};
+  uint2* d_pkp = nullptr;  // prepared public key [gp][part] (baseline)
   uint32_t* d_err = nullptr;
   cudaStream_t stream = nullptr;
   uint64_t batch_pairs = 0;
@@ -884,8 +1169,11 @@ struct hei_gpu_stream {
   uint64_t cap_rows = 0;
 };
 
+// util::Prng (rng.hpp:19-68): mt19937_64 state kept explicitly so the
+// device generator (k_mt_generate) can continue the exact stream.
 struct hei_gpu_prng {
-  std::mt19937_64 eng;
+  uint64_t mt[312];
+  uint32_t mti = 312;
   double spare = 0.0;
   bool have_spare = false;
 };
@@ -991,6 +1279,9 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_mask_acc_f<LG>, sm);
   set_smem_attr((const void*)k_ct_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_poly_ntt_f<LG>, sm);
+  set_smem_attr((const void*)k_bl_encode<LG>, sm);
+  set_smem_attr((const void*)k_bl_encrypt<LG>, sm);
+  set_smem_attr((const void*)k_prepare_pk<LG>, sm);
 }
 
 uint64_t auto_batch_pairs(hei_gpu_ctx* c) {
@@ -1176,27 +1467,36 @@ hei_gpu_weights* weights_alloc(hei_gpu_ctx* c, uint64_t f, uint64_t cols) {
   return w.release();
 }
 
-// ---- util::Prng replay (rng.hpp:19-68) ----
-uint64_t prng_uniform(hei_gpu_prng* p, uint64_t bound) {
-  uint64_t limit = bound * (UINT64_MAX / bound), v;
-  do v = p->eng();
-  while (v >= limit);
-  return v % bound;
+// ---- util::Prng host side (rng.hpp:19-68) ----
+void prng_seed(hei_gpu_prng* p, uint64_t seed) {
+  p->mt[0] = seed;
+  for (int i = 1; i < 312; ++i) p->mt[i] = 6364136223846793005ULL * (p->mt[i - 1] ^ (p->mt[i - 1] >> 62)) + (uint64_t)i;
+  p->mti = 312;
+  p->have_spare = false;
 }
-double prng_udouble(hei_gpu_prng* p) { return (double)(p->eng() >> 11) * 0x1.0p-53; }
-double prng_gauss(hei_gpu_prng* p) {
-  if (p->have_spare) {
-    p->have_spare = false;
-    return p->spare;
+uint64_t prng_next(hei_gpu_prng* p) {
+  using namespace heb_baseline;
+  if (p->mti >= 312) {
+    int i;
+    uint64_t x;
+    for (i = 0; i < 156; ++i) {
+      x = (p->mt[i] & kMtUM) | (p->mt[i + 1] & kMtLM);
+      p->mt[i] = p->mt[i + 156] ^ (x >> 1) ^ ((x & 1) ? kMtA : 0);
+    }
+    for (; i < 311; ++i) {
+      x = (p->mt[i] & kMtUM) | (p->mt[i + 1] & kMtLM);
+      p->mt[i] = p->mt[i - 156] ^ (x >> 1) ^ ((x & 1) ? kMtA : 0);
+    }
+    x = (p->mt[311] & kMtUM) | (p->mt[0] & kMtLM);
+    p->mt[311] = p->mt[155] ^ (x >> 1) ^ ((x & 1) ? kMtA : 0);
+    p->mti = 0;
   }
-  double u1, u2;
-  do u1 = prng_udouble(p);
-  while (u1 <= 0.0);
-  u2 = prng_udouble(p);
-  double mag = std::sqrt(-2.0 * std::log(u1));
-  p->spare = mag * std::sin(6.283185307179586476925286766559 * u2);
-  p->have_spare = true;
-  return mag * std::cos(6.283185307179586476925286766559 * u2);
+  uint64_t x = p->mt[p->mti++];
+  x ^= (x >> 29) & 0x5555555555555555ULL;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+  x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+  x ^= (x >> 43);
+  return x;
 }
 
 }  // namespace
@@ -1411,6 +1711,10 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     set_smem_attr((const void*)k_ct_ntt, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_poly_ntt, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_encode_weights, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_bl_finish, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_bl_encode_g, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_bl_encrypt_g, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_prepare_pk_g, smem_bytes(c.get(), 1));
     if (c->logn == 12) set_fast_attrs<12>(smem_bytes(c.get(), 1));
     if (c->logn == 13) set_fast_attrs<13>(smem_bytes(c.get(), 1));
     if (c->logn == 14) set_fast_attrs<14>(smem_bytes(c.get(), 1));
@@ -1432,6 +1736,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
     cudaFree(c->d_keys[b]);
     cudaFree(c->d_pk[b]);
   }
+  cudaFree(c->d_pkp);
   cudaFree(c->d_dotA);
   cudaFree(c->d_dotB);
   cudaFree(c->d_dig);
@@ -1476,6 +1781,10 @@ int hei_gpu_upload_public_key(hei_gpu_ctx* c, uint32_t b, const uint64_t* pk) {
     set_device(c);
     const size_t words = 2ull * c->L[b] * c->n;
     if (!c->d_pk[b]) CU(cudaMalloc(&c->d_pk[b], words * 8));
+    if (c->d_pkp) {
+      cudaFree(c->d_pkp);
+      c->d_pkp = nullptr;
+    }
     CU(cudaMemcpy(c->d_pk[b], pk, words * 8, cudaMemcpyHostToDevice));
   });
 }
@@ -1688,18 +1997,136 @@ int hei_gpu_sum_all_slots(hei_gpu_ctx* c, const uint64_t* in, uint64_t* out, uin
 int hei_gpu_prng_create(uint64_t seed, hei_gpu_prng** out) {
   return guarded([&] {
     auto p = std::make_unique<hei_gpu_prng>();
-    p->eng.seed(seed);
+    prng_seed(p.get(), seed);
     *out = p.release();
   });
 }
 void hei_gpu_prng_destroy(hei_gpu_prng* p) { delete p; }
+int hei_gpu_prng_draw(hei_gpu_prng* p, uint64_t count, uint64_t* out) {
+  return guarded([&] {
+    for (uint64_t i = 0; i < count; ++i) out[i] = prng_next(p);
+  });
+}
 
 int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_t f, const int64_t* w,
                             uint64_t cols, const int64_t* bias, hei_gpu_prng* rng0, hei_gpu_prng* rng1,
                             uint64_t* out, hei_op_counters* cnt) {
   return guarded([&] {
-    (void)x; (void)rows; (void)f; (void)w; (void)cols; (void)bias; (void)rng0; (void)rng1; (void)out; (void)cnt;
-    raise(HEI_INTERNAL, "baseline_matmul: not implemented yet");
+    // matmul.cpp:418-434
+    if (rows == 0 || f == 0 || cols == 0) raise(HEI_PARAM_ERROR, "baseline: empty input");
+    capacity_gate(c, f, "baseline");
+    if (!c->d_pk[0] || !c->d_pk[1]) raise(HEI_KEY_ERROR, "encrypt: this backend holds no public key");
+    if (!rng0 || !rng1) raise(HEI_PARAM_ERROR, "baseline: encryption randomness required");
+    if (rng0->have_spare || rng1->have_spare)
+      raise(HEI_PARAM_ERROR, "baseline: rng holds a cached Box-Muller spare; cannot replay on the device");
+    const int64_t lim = (int64_t)(((u128)c->t[0] * c->t[1] - 1) / 2);
+    for (uint64_t i = 0; i < f * cols; ++i)
+      if (w[i] > lim || w[i] < -lim) raise(HEI_RANGE_ERROR, "prepare_constant_signed: value outside centered range");
+    for (uint64_t i = 0; i < rows * f; ++i)
+      if (x[i] > lim || x[i] < -lim) raise(HEI_RANGE_ERROR, "encode_signed: value outside the centered range");
+    check_bias_range(c, bias, cols);
+    for (int b = 0; b < 2; ++b)
+      for (uint32_t i = 0; i < c->L[b]; ++i)
+        if (c->t[b] >= c->q[(b ? c->L[0] : 0) + i])
+          raise(HEI_PARAM_ERROR, "baseline: plaintext modulus exceeds a ciphertext prime (unsupported)");
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = c->stream;
+    const Geo& g = c->geo;
+    const uint32_t n = c->n, P = c->P();
+    const uint64_t B = (rows + n - 1) / n;
+    const bool fast = c->logn >= 12 && c->logn <= 14;
+    // prepared public key [gp][part] (cached)
+    if (!c->d_pkp) {
+      CU(cudaMalloc(&c->d_pkp, 2ull * P * n * sizeof(uint2)));
+      const size_t sm = smem_bytes(c, 1);
+      HEI_DISPATCH(c->logn, (k_prepare_pk<LG><<<2 * P, Ntt<LG>::T, sm, st>>>(g, c->d_pk[0], c->d_pk[1], c->d_pkp, c->d_err)),
+                   (k_prepare_pk_g<<<2 * P, c->threads(), sm, st>>>(g, c->d_pk[0], c->d_pk[1], c->d_pkp, c->d_err)));
+      LAUNCHED();
+      check_err_flag(c, HEI_CODEC_ERROR, "public key: coefficient not reduced");
+    }
+    const uint64_t F = std::min<uint64_t>(f, std::max<uint64_t>(1, 256 / B));
+    const uint64_t Emax = F * B;
+    int64_t *d_x = nullptr, *d_w = nullptr, *d_bias = nullptr;
+    uint2* d_wc = nullptr;
+    unsigned long long* d_acc = nullptr;
+    uint64_t *d_raw = nullptr, *d_state = nullptr;
+    int8_t* d_noise = nullptr;
+    uint32_t *d_m = nullptr, *d_ct = nullptr, *d_out = nullptr;
+    uint64_t* d_out64 = nullptr;
+    struct Free {
+      std::vector<void*> p;
+      ~Free() {
+        for (void* x : p) cudaFree(x);
+      }
+    } fr;
+    auto alloc = [&](auto** ptr, size_t bytes) {
+      CU(cudaMalloc((void**)ptr, bytes));
+      fr.p.push_back((void*)*ptr);
+    };
+    const size_t outw = B * cols * c->ct_words();
+    alloc(&d_x, rows * f * 8);
+    alloc(&d_w, f * cols * 8);
+    alloc(&d_bias, cols * 8);
+    alloc(&d_wc, f * cols * P * sizeof(uint2));
+    alloc(&d_acc, outw * 8);
+    alloc(&d_raw, 2 * Emax * 3 * n * 8);
+    alloc(&d_state, 2 * 313 * 8);
+    alloc(&d_noise, Emax * 2 * 3 * n);
+    alloc(&d_m, Emax * 2 * n * 4);
+    alloc(&d_ct, Emax * c->ct_words() * 4);
+    alloc(&d_out, outw * 4);
+    alloc(&d_out64, outw * 8);
+    CU(cudaMemcpyAsync(d_x, x, rows * f * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d_w, w, f * cols * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d_bias, bias, cols * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(d_acc, 0, outw * 8, st));
+    uint64_t hstate[2][313];
+    for (int b = 0; b < 2; ++b) {
+      hei_gpu_prng* r = b ? rng1 : rng0;
+      std::memcpy(hstate[b], r->mt, 312 * 8);
+      hstate[b][312] = r->mti;
+    }
+    CU(cudaMemcpyAsync(d_state, hstate, sizeof(hstate), cudaMemcpyHostToDevice, st));
+    k_bl_weights<<<grid_for(f * cols * P, 256), 256, 0, st>>>(g, d_w, f * cols, d_wc);
+    LAUNCHED();
+    const size_t sm1 = smem_bytes(c, 1);
+    const unsigned at = std::min<uint32_t>(256, n);
+    for (uint64_t k0 = 0; k0 < f; k0 += F) {
+      const uint64_t Fb = std::min<uint64_t>(F, f - k0), E = Fb * B, draws = E * 3 * n;
+      heb_baseline::k_mt_generate<<<2, 320, 0, st>>>(d_state, d_raw, draws);
+      LAUNCHED();
+      heb_baseline::k_bl_noise<<<dim3((unsigned)E, 2), 256, 0, st>>>(d_raw, draws, n, (uint32_t)E, d_noise, c->d_err);
+      LAUNCHED();
+      HEI_DISPATCH(c->logn,
+                   (k_bl_encode<LG><<<dim3((unsigned)E, 2), Ntt<LG>::T, sm1, st>>>(g, d_x, rows, f, k0, (uint32_t)B, d_m)),
+                   (k_bl_encode_g<<<dim3((unsigned)E, 2), c->threads(), sm1, st>>>(g, d_x, rows, f, k0, (uint32_t)B, d_m)));
+      LAUNCHED();
+      HEI_DISPATCH(c->logn, (k_bl_encrypt<LG><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp, d_ct)),
+                   (k_bl_encrypt_g<<<(unsigned)(E * P), c->threads(), sm1, st>>>(g, d_noise, d_m, c->d_pkp, d_ct)));
+      LAUNCHED();
+      for (uint32_t j0 = 0; j0 < cols; j0 += kBlJ) {
+        const unsigned blocks = (unsigned)(B * 2 * P * (n / at));
+        k_bl_accum<<<blocks, at, Fb * kBlJ * sizeof(uint2), st>>>(g, d_ct, (uint32_t)Fb, (uint32_t)B, (uint32_t)cols, j0,
+                                                                  d_wc + k0 * cols * P, d_acc);
+        LAUNCHED();
+      }
+    }
+    (void)fast;
+    k_bl_finish<<<(unsigned)(B * cols * P), c->threads(), sm1, st>>>(g, d_acc, d_bias, (uint32_t)cols, d_out);
+    LAUNCHED();
+    k_widen<<<grid_for(outw, 256), 256, 0, st>>>(d_out, d_out64, outw);
+    LAUNCHED();
+    CU(cudaMemcpyAsync(out, d_out64, outw * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(hstate, d_state, sizeof(hstate), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int b = 0; b < 2; ++b) {
+      hei_gpu_prng* r = b ? rng1 : rng0;
+      std::memcpy(r->mt, hstate[b], 312 * 8);
+      r->mti = (uint32_t)hstate[b][312];
+    }
+    check_err_flag(c, HEI_INTERNAL, "baseline: rng rejection in the encryption stream (replay unsupported)");
+    if (cnt) hei_baseline_counts(rows, cols, f, n, cnt);
   });
 }
 

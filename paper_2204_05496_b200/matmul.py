@@ -244,3 +244,48 @@ def matmul_device(server: GpuTwinServer, d_inputs_ptr: int, rows: int, w: Encode
     check(native.lib().hei_gpu_matmul_device(server.handle, w._h, C.c_void_p(d_inputs_ptr), C.c_int(FORM_EVAL), C.c_uint64(rows),
                                              i64p(bias), C.c_void_p(d_out_ptr), C.byref(cnt), C.c_void_p(stream_ptr)))
     return cnt
+
+
+class Prng:
+    """util::Prng replay state (rng.hpp:19-68) for the standard algorithm's
+    encryption randomness; advances exactly like BfvBackend's rng_."""
+
+    def __init__(self, seed: int):
+        self._h = C.c_void_p()
+        check(native.lib().hei_gpu_prng_create(C.c_uint64(seed), C.byref(self._h)))
+
+    def draw(self, count: int) -> np.ndarray:
+        out = np.zeros(count, dtype=np.uint64)
+        check(native.lib().hei_gpu_prng_draw(self._h, C.c_uint64(count), u64p(out)))
+        return out
+
+    def __del__(self):
+        try:
+            if self._h:
+                native.lib().hei_gpu_prng_destroy(self._h)
+                self._h = C.c_void_p()
+        except Exception:
+            pass
+
+
+def baseline_matmul(server: GpuTwinServer, x: np.ndarray, w: np.ndarray, bias, rng0: Prng, rng1: Prng):
+    """matmul::baseline_matmul (matmul.cpp:415-486): x is R x f, w is f x cols
+    (scaled integers). Encrypts each feature column on the device with the
+    replayed randomness. Returns (blocks [ceil(R/N)][cols][twin ct], counters)."""
+    x = np.ascontiguousarray(x, dtype=np.int64)
+    w = np.ascontiguousarray(w, dtype=np.int64)
+    if x.ndim != 2 or w.ndim != 2 or x.size == 0 or w.shape[1] == 0:
+        raise ParamError("baseline: empty input")
+    R, f = x.shape
+    if w.shape[0] != f:
+        raise ParamError("baseline: input and weight shapes do not match")
+    cols = w.shape[1]
+    bias = np.ascontiguousarray(bias, dtype=np.int64)
+    if bias.size != cols:
+        raise ParamError("baseline: bias length does not match output count")
+    B = (R + server.n - 1) // server.n
+    out = np.zeros((B, cols, server.ct_words), dtype=np.uint64)
+    cnt = OpCounters()
+    check(native.lib().hei_gpu_baseline_matmul(server.handle, i64p(x), C.c_uint64(R), C.c_uint64(f), i64p(w), C.c_uint64(cols),
+                                               i64p(bias), rng0._h, rng1._h, u64p(out), C.byref(cnt)))
+    return out, cnt

@@ -93,7 +93,7 @@ EXPORTED = [
     "hei_gpu_upload_galois_keys", "hei_gpu_upload_public_key", "hei_gpu_weights_create",
     "hei_gpu_weights_encode", "hei_gpu_weights_destroy", "hei_gpu_matmul", "hei_gpu_matmul_device",
     "hei_gpu_stream_create", "hei_gpu_stream_push_row", "hei_gpu_stream_finish", "hei_gpu_stream_destroy",
-    "hei_gpu_prng_create", "hei_gpu_prng_destroy", "hei_gpu_baseline_matmul", "hei_proposed_counts",
+    "hei_gpu_prng_create", "hei_gpu_prng_destroy", "hei_gpu_prng_draw", "hei_gpu_baseline_matmul", "hei_proposed_counts",
     "hei_baseline_counts", "hei_gpu_ntt", "hei_gpu_apply_galois", "hei_gpu_sum_all_slots",
     "hei_gpu_launch_count", "hei_gpu_reset_launch_count", "hei_gpu_set_batch_pairs",
 ]

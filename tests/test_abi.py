@@ -89,3 +89,14 @@ def test_bench_q_chain_matches_reference_chain():
     assert bench.q_chain(8192, 1073872897) == g["chains"]["8192/1073872897/128"]
     assert bench.q_chain(8192, 114689) == g["chains"]["8192/114689/128"]
     assert bench.q_chain(16384, 163841) == g["chains"]["16384/163841/128"]
+
+
+def test_device_prng_replays_reference_stream():
+    """The product's util::Prng replay (host half) equals the reference stream."""
+    from oracle.oracle import prng_stream
+    from paper_2204_05496_b200 import Prng
+
+    raw, _, _ = prng_stream(2, 1000)
+    p = Prng(2)
+    assert np.array_equal(p.draw(400), raw[:400])
+    assert np.array_equal(p.draw(600), raw[400:])

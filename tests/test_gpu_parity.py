@@ -247,3 +247,52 @@ def test_errors_match_reference_types(tiny32):
     bad[0, 0, 0] = o.q[0]  # not reduced
     with pytest.raises(native.CodecError):
         matmul(s, bad, EncodedWeights.from_prepared(s, wp, 4), [0, 0])
+
+
+@pytest.mark.parametrize("n", [32, 8192])
+def test_baseline_bit_exact_and_rng_state(n):
+    """baseline_matmul (matmul.cpp:415-486): same keys, same replayed
+    randomness -> bit-identical blocks, exact decryption, closed-form counts;
+    the Prng state afterwards continues the reference stream."""
+    from paper_2204_05496_b200 import Prng, baseline_counts, baseline_matmul
+
+    if n == 32:
+        p, R, f, cols = tiny_params(32), 40, 9, 3  # two sample blocks
+    else:
+        p, R, f, cols = production_params(8192), 3, 24, 2
+    o = Oracle(p, key_seed=5, enc_seed=6)
+    s = gpu_server_from(o, with_pk=True)
+    rng = np.random.default_rng(n)
+    x = random_mat(rng, R, f, 20)
+    w = random_mat(rng, f, cols, 7)
+    b = rng.integers(-100, 101, size=cols)
+    r0, r1 = Prng(6), Prng(7)
+    got, cnt = baseline_matmul(s, x, w, b, r0, r1)
+    want, wcnt = o.baseline_matmul(x, w, b)
+    assert np.array_equal(got, want)
+    assert cnt.as_tuple() == tuple(int(v) for v in wcnt) == baseline_counts(R, cols, f, p.n).as_tuple()
+    assert np.array_equal(o.unpack_baseline(got, R, cols), oracle_matmul(x, w, b))
+    # the oracle's client RNG and ours continue identically
+    nxt = o.baseline_noise(1)
+    from oracle.oracle import prng_stream  # noqa: F401
+    r0b = Prng(6)
+    r0b.draw(int(np.ceil(R / p.n)) * f * 3 * p.n)
+    assert np.array_equal(r0.draw(4), r0b.draw(4))
+    assert nxt.shape[-1] == p.n
+
+
+def test_baseline_equals_fast_algorithm(tiny32):
+    """test_matmul.cpp:258-291: baseline == proposed == integer oracle."""
+    from paper_2204_05496_b200 import EncodedWeights, Prng, baseline_matmul, matmul
+
+    o, _ = tiny32
+    o2 = Oracle(tiny_params(32), key_seed=72, enc_seed=90)
+    s = gpu_server_from(o2, with_pk=True)
+    rng = np.random.default_rng(200)
+    x = random_mat(rng, 20, 30, 32)
+    w = random_mat(rng, 30, 3, 8)
+    b = rng.integers(-1000, 1001, size=3)
+    base, _ = baseline_matmul(s, x, w, b, Prng(90), Prng(91))
+    fast, _ = matmul(s, o2.encode_inputs(x), EncodedWeights.from_prepared(s, o2.encode_weights(w), 30), b)
+    assert np.array_equal(o2.unpack_baseline(base, 20, 3), o2.unpack(fast, 20, 3))
+    assert np.array_equal(o2.unpack(fast, 20, 3), oracle_matmul(x, w, b))
