@@ -56,7 +56,10 @@ def parse():
     ap.add_argument("--batch-pairs", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--latency", action="store_true", help="also time a single-individual (C3) call")
+    ap.add_argument("--latency", action="store_true", default=True, help="also time a single-individual (C3) call")
+    ap.add_argument("--no-latency", dest="latency", action="store_false")
+    ap.add_argument("--baseline", action="store_true", default=True, help="also time the standard algorithm at C3")
+    ap.add_argument("--no-baseline", dest="baseline", action="store_false")
     return ap.parse_args()
 
 
@@ -296,6 +299,74 @@ def run_ours(args, world, rank, local):
         e2e = {"value": world * R / e2e_s, "unit": "inferences/s", "h2d_bytes_per_step": int(h_np.nbytes),
                "d2h_bytes_per_step": int(out.nbytes), "ms_per_step": 1000 * e2e_s}
 
+    # ---- roofline of the dominant kernel (key switch), timed live with CUDA
+    # events on the launch stream inside the C ABI over one extra step.
+    roof = int_roof = None
+    if rank == 0:
+        native.kernel_timing(srv.handle, True)
+        step()
+        torch.cuda.synchronize()
+        ks_n, ks_ms = native.kernel_stats(srv.handle, 0)
+        dg_n, dg_ms = native.kernel_stats(srv.handle, 1)
+        native.kernel_timing(srv.handle, False)
+        L0, L1 = len(q0), len(q1)
+        pairs_per_launch = R * cols  # one batch holds every pair of the step
+        per_pair = sum(16 * n + 4 * n * (Lb - 1) for Lb in (L0, L1) for _ in range(Lb))
+        keys = sum(16 * Lb * n * Lb for Lb in (L0, L1))
+        alg_bytes = pairs_per_launch * per_pair + keys
+        avg_s = ks_ms / ks_n / 1000.0
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        traffic = None
+        try:
+            prof = json.load(open(os.path.join(ROOT, "profiles", "keyswitch_traffic.json")))
+            if prof.get("pairs_per_launch") == pairs_per_launch:
+                traffic = prof.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+        roof = {"kernel": "k_rot_keyswitch (fold step)", "bound": "hbm", "achieved": alg_bytes / avg_s / 1e9,
+                "peak": hbm, "unit": "GB/s", "frac": alg_bytes / avg_s / 1e9 / hbm, "traffic": traffic,
+                "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_s * 1e3, "launches": ks_n,
+                "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+                "share_of_fold": ks_ms / (ks_ms + dg_ms),
+                "digits_avg_launch_ms": dg_ms / max(1, dg_n)}
+        bfly = pairs_per_launch * sum(((Lb - 1) * (n // 2) * int(np.log2(n)) + 2 * Lb * n) for Lb in (L0, L1) for _ in range(Lb))
+        peak_b = native.butterfly_peak(local)
+        int_roof = {"kernel": "k_rot_keyswitch", "bound": "int32 pipes (CT butterfly = Shoup mulmod + add + sub)",
+                    "achieved": bfly / avg_s / 1e9, "peak": peak_b / 1e9, "unit": "Gbutterfly/s",
+                    "frac": (bfly / avg_s) / peak_b, "peak_source": "k_bfly_peak register microbenchmark, this run",
+                    "butterfly_equivalents_per_launch": bfly}
+
+    base = None
+    if args.baseline and rank == 0:
+        from paper_2204_05496_b200 import Prng, baseline_matmul
+
+        pk = []
+        rngk = np.random.default_rng(5)
+        for qb in (q0, q1):
+            a = np.empty((2, len(qb), n), dtype=np.uint64)
+            for i, qi in enumerate(qb):
+                a[:, i, :] = rngk.integers(0, qi, size=(2, n), dtype=np.uint64)
+            pk.append(a.reshape(-1))
+        from paper_2204_05496_b200 import native as _nat
+        import ctypes as _C
+
+        for bb in range(2):
+            _nat.check(_nat.lib().hei_gpu_upload_public_key(srv.handle, _C.c_uint32(bb), _nat.u64p(pk[bb])))
+        R3, f3, c3, _, pf3, ws3 = CONFIGS["c3"]
+        x3, w3, b3 = synthetic(R3, f3, c3, pf3, ws3)
+        baseline_matmul(srv, x3[:, :512], w3[:512], b3, Prng(2), Prng(3))  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, bc = baseline_matmul(srv, x3, w3, b3, Prng(2), Prng(3))
+        bs = time.perf_counter() - t0
+        base = {"algorithm": "standard (sample-batched, baseline_matmul)", "config": f"c3: {R3}x{f3}x{c3} N={n}",
+                "ms": bs * 1000.0, "mul_plain": int(bc.mul_plain_count), "note": "host call incl. H2D of x, w and D2H"}
+
     lat = None
     if args.latency and rank == 0:
         # single individual, 40k features x 11 classes (C3 shape), device-resident
@@ -338,8 +409,12 @@ def run_ours(args, world, rank, local):
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
+    line["roofline"] = roof
+    line["int_roofline"] = int_roof
     if lat is not None:
         line["latency_ms_single_individual"] = lat
+    if base is not None:
+        line["standard_algorithm"] = base
     print(json.dumps(line), flush=True)
 
 

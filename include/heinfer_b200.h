@@ -142,6 +142,12 @@ uint64_t hei_gpu_launch_count(void);
 void hei_gpu_reset_launch_count(void);
 /* Tuning: pairs per device batch (0 = automatic). */
 void hei_gpu_set_batch_pairs(hei_gpu_ctx* ctx, uint64_t pairs);
+/* Measurement hooks for bench.py: CUDA events around every fold kernel
+ * (which = 0 key switch, 1 digit INTT), and a register-only butterfly
+ * throughput microbenchmark (the integer roofline denominator). */
+int hei_gpu_kernel_timing(hei_gpu_ctx* ctx, int enable);
+int hei_gpu_kernel_stats(hei_gpu_ctx* ctx, int which, uint64_t* launches, double* total_ms);
+int hei_gpu_measure_butterfly_peak(int device, double* butterflies_per_s);
 
 #ifdef __cplusplus
 }

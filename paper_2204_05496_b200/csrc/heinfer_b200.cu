@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -1110,6 +1111,31 @@ __global__ void k_bl_weights(Geo g, const int64_t* __restrict__ w, uint64_t coun
   }
 }
 
+// Butterfly-throughput microbenchmark: the roofline denominator for the
+// integer-bound transforms. Each thread runs 8 independent
+// Cooley-Tukey butterfly chains (mul_shoup + add_mod + sub_mod) on registers.
+__global__ void __launch_bounds__(256) k_bfly_peak(uint32_t* __restrict__ sink, uint32_t iters, uint32_t q,
+                                                   uint32_t w, uint32_t ws) {
+  uint32_t u[8], v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    u[k] = (threadIdx.x * 7919u + k * 104729u) % q;
+    v[k] = (blockIdx.x * 31337u + k * 65537u) % q;
+  }
+  for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t t = mul_shoup(v[k], w, ws, q);
+      v[k] = sub_mod(u[k], t, q);
+      u[k] = add_mod(u[k], t, q);
+    }
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc ^= u[k] ^ v[k];
+  if (acc == 0xFFFFFFFFu) sink[blockIdx.x] = acc;
+}
+
 }  // namespace
 
 // ================================================================ host side
@@ -1140,6 +1166,9 @@ struct hei_gpu_ctx {
   uint32_t *d_dotA = nullptr, *d_dotB = nullptr, *d_dig = nullptr;
   uint64_t scratch_pairs = 0;
   std::mutex mu;
+  // optional per-kernel timing (bench.py roofline): events around the fold
+  bool timing = false;
+  std::vector<std::array<cudaEvent_t, 3>> fold_ev;  // digits: [0,1], key switch: [1,2]
 
   size_t ct_words() const { return 2ull * (L[0] + L[1]) * n; }
   size_t pt_words() const { return (size_t)(L[0] + L[1]) * n; }
@@ -1303,8 +1332,20 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
     const uint32_t* perm = c->d_perms + (size_t)c->perm_index.at(elt) * c->n;
     const uint2* k0 = c->d_keys[0] + (size_t)c->key_index[0].at(elt) * c->L[0] * 2 * c->L[0] * c->n;
     const uint2* k1 = c->d_keys[1] + (size_t)c->key_index[1].at(elt) * c->L[1] * 2 * c->L[1] * c->n;
+    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    if (c->timing) {
+      CU(cudaEventCreate(&e0));
+      CU(cudaEventCreate(&e1));
+      CU(cudaEventCreate(&e2));
+      CU(cudaEventRecord(e0, st));
+    }
     launch_rot_digits(c, g, blocks, cur, perm, c->d_dig, st);
+    if (c->timing) CU(cudaEventRecord(e1, st));
     launch_rot_keyswitch(c, g, blocks, cur, c->d_dig, perm, k0, k1, other, 1, st);
+    if (c->timing) {
+      CU(cudaEventRecord(e2, st));
+      c->fold_ev.push_back({e0, e1, e2});
+    }
     std::swap(cur, other);
   }
   return cur;
@@ -1740,11 +1781,72 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->d_dotA);
   cudaFree(c->d_dotB);
   cudaFree(c->d_dig);
+  for (auto& a : c->fold_ev)
+    for (auto e : a) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
 
 void hei_gpu_set_batch_pairs(hei_gpu_ctx* c, uint64_t pairs) { c->batch_pairs = pairs; }
+
+int hei_gpu_kernel_timing(hei_gpu_ctx* c, int enable) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    for (auto& a : c->fold_ev)
+      for (auto e : a) cudaEventDestroy(e);
+    c->fold_ev.clear();
+    c->timing = enable != 0;
+  });
+}
+
+// which: 0 = key switch, 1 = digits.
+int hei_gpu_kernel_stats(hei_gpu_ctx* c, int which, uint64_t* launches, double* total_ms) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaDeviceSynchronize());
+    double tot = 0;
+    for (const auto& a : c->fold_ev) {
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, which == 0 ? a[1] : a[0], which == 0 ? a[2] : a[1]));
+      tot += ms;
+    }
+    *launches = c->fold_ev.size();
+    *total_ms = tot;
+  });
+}
+
+int hei_gpu_measure_butterfly_peak(int device, double* bfly_per_s) {
+  return guarded([&] {
+    CU(cudaSetDevice(device));
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const uint32_t q = 2147352577u, w = 123456789u;
+    const uint32_t ws = (uint32_t)(((uint64_t)w << 32) / q);
+    const unsigned blocks = (unsigned)sms * 8, threads = 256;
+    const uint32_t iters = 4096;
+    uint32_t* sink = nullptr;
+    CU(cudaMalloc(&sink, blocks * 4));
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    k_bfly_peak<<<blocks, threads>>>(sink, 64, q, w, ws);  // warm-up
+    LAUNCHED();
+    CU(cudaEventRecord(a));
+    for (int r = 0; r < 5; ++r) k_bfly_peak<<<blocks, threads>>>(sink, iters, q, w, ws);
+    LAUNCHED();
+    CU(cudaEventRecord(b));
+    CU(cudaEventSynchronize(b));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    *bfly_per_s = 5.0 * blocks * threads * 8.0 * iters / (ms * 1e-3);
+  });
+}
 
 int hei_gpu_upload_galois_keys(hei_gpu_ctx* c, uint32_t b, uint32_t count, const uint64_t* elts,
                                const uint64_t* rows) {

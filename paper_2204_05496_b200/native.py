@@ -96,6 +96,7 @@ EXPORTED = [
     "hei_gpu_prng_create", "hei_gpu_prng_destroy", "hei_gpu_prng_draw", "hei_gpu_baseline_matmul", "hei_proposed_counts",
     "hei_baseline_counts", "hei_gpu_ntt", "hei_gpu_apply_galois", "hei_gpu_sum_all_slots",
     "hei_gpu_launch_count", "hei_gpu_reset_launch_count", "hei_gpu_set_batch_pairs",
+    "hei_gpu_kernel_timing", "hei_gpu_kernel_stats", "hei_gpu_measure_butterfly_peak",
 ]
 
 _lib = None
@@ -136,6 +137,25 @@ def u64p(a):
 
 def i64p(a):
     return a.ctypes.data_as(C.POINTER(C.c_int64)) if a is not None else None
+
+
+def kernel_timing(server_handle, enable: bool) -> None:
+    check(lib().hei_gpu_kernel_timing(server_handle, C.c_int(int(enable))))
+
+
+def kernel_stats(server_handle, which: int):
+    """(launches, total_ms) of the fold kernels timed with CUDA events:
+    which = 0 key switch, 1 digit INTT."""
+    n = C.c_uint64()
+    ms = C.c_double()
+    check(lib().hei_gpu_kernel_stats(server_handle, C.c_int(which), C.byref(n), C.byref(ms)))
+    return int(n.value), float(ms.value)
+
+
+def butterfly_peak(device: int = 0) -> float:
+    v = C.c_double()
+    check(lib().hei_gpu_measure_butterfly_peak(C.c_int(device), C.byref(v)))
+    return float(v.value)
 
 
 def launch_count() -> int:
