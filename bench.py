@@ -310,10 +310,15 @@ def run_ours(args, world, rank, local):
         dg_n, dg_ms = native.kernel_stats(srv.handle, 1)
         native.kernel_timing(srv.handle, False)
         L0, L1 = len(q0), len(q1)
-        pairs_per_launch = R * cols  # one batch holds every pair of the step
+        S = int(np.log2(n))  # fold steps per batch
+        batches = ks_n // S
+        # algorithmic bytes of one key-switch launch over P pairs: per pair
+        # and output prime, c0/c1 read + out0/out1 written (4 polys of 4N B)
+        # and L-1 digit polys read; the step's Galois key (2L polys of 8N B
+        # per prime) once per launch.
         per_pair = sum(16 * n + 4 * n * (Lb - 1) for Lb in (L0, L1) for _ in range(Lb))
         keys = sum(16 * Lb * n * Lb for Lb in (L0, L1))
-        alg_bytes = pairs_per_launch * per_pair + keys
+        tot_bytes = S * R * cols * per_pair + ks_n * keys
         avg_s = ks_ms / ks_n / 1000.0
         peaks = {}
         try:
@@ -324,22 +329,23 @@ def run_ours(args, world, rank, local):
         traffic = None
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "keyswitch_traffic.json")))
-            if prof.get("pairs_per_launch") == pairs_per_launch:
-                traffic = prof.get("dram_bytes_per_launch")
+            traffic = prof.get("dram_bytes_per_pair") * R * cols / batches
         except Exception:
             pass
-        roof = {"kernel": "k_rot_keyswitch (fold step)", "bound": "hbm", "achieved": alg_bytes / avg_s / 1e9,
-                "peak": hbm, "unit": "GB/s", "frac": alg_bytes / avg_s / 1e9 / hbm, "traffic": traffic,
-                "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_s * 1e3, "launches": ks_n,
-                "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
-                "share_of_fold": ks_ms / (ks_ms + dg_ms),
-                "digits_avg_launch_ms": dg_ms / max(1, dg_n)}
-        bfly = pairs_per_launch * sum(((Lb - 1) * (n // 2) * int(np.log2(n)) + 2 * Lb * n) for Lb in (L0, L1) for _ in range(Lb))
+        ach = tot_bytes / (ks_ms / 1000.0) / 1e9
+        roof = {"kernel": "k_rot_keyswitch_s<13> (fold key switch)", "bound": "hbm", "achieved": ach, "peak": hbm,
+                "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+                "algorithmic_bytes_per_launch": tot_bytes / ks_n, "avg_launch_ms": avg_s * 1e3, "launches": ks_n,
+                "batches": batches, "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+                "share_of_fold": ks_ms / (ks_ms + dg_ms), "digits_avg_launch_ms": dg_ms / max(1, dg_n)}
+        bfly_pair = sum(((Lb - 1) * (n // 2) * S + 2 * Lb * n) for Lb in (L0, L1) for _ in range(Lb))
+        tot_bfly = S * R * cols * bfly_pair
         peak_b = native.butterfly_peak(local)
-        int_roof = {"kernel": "k_rot_keyswitch", "bound": "int32 pipes (CT butterfly = Shoup mulmod + add + sub)",
-                    "achieved": bfly / avg_s / 1e9, "peak": peak_b / 1e9, "unit": "Gbutterfly/s",
-                    "frac": (bfly / avg_s) / peak_b, "peak_source": "k_bfly_peak register microbenchmark, this run",
-                    "butterfly_equivalents_per_launch": bfly}
+        int_roof = {"kernel": "k_rot_keyswitch_s<13>", "bound": "int32 pipes (CT butterfly = Shoup mulmod + add + sub)",
+                    "achieved": tot_bfly / (ks_ms / 1000.0) / 1e9, "peak": peak_b / 1e9, "unit": "Gbutterfly/s",
+                    "frac": tot_bfly / (ks_ms / 1000.0) / peak_b,
+                    "peak_source": "k_bfly_peak register microbenchmark, this run",
+                    "butterfly_equivalents_per_launch": tot_bfly / ks_n}
 
     base = None
     if args.baseline and rank == 0:

@@ -1318,9 +1318,9 @@ uint64_t auto_batch_pairs(hei_gpu_ctx* c) {
   // Enough (pair, prime) blocks for several waves on 148 SMs while keeping the
   // per-step working set (2 x dot + digits) modest.
   const uint64_t per_pair = (2 * c->ct_words() + c->pt_words()) * 4;
-  uint64_t p = (uint64_t)4 << 30;  // 4 GiB
+  uint64_t p = (uint64_t)16 << 30;  // 16 GiB of the 180 GB HBM
   p /= per_pair;
-  return std::max<uint64_t>(1, std::min<uint64_t>(p, 4096));
+  return std::max<uint64_t>(1, std::min<uint64_t>(p, 8192));
 }
 
 // The rotate-and-sum fold over `pairs` twin ciphertexts in `cur` (eval form);
