@@ -54,6 +54,8 @@ def build_oracle(verbose: bool = False) -> None:
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "all"], check=True)
     if os.path.isdir("/root/reference/proj/src"):
         subprocess.run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
+        if os.path.exists(LIB):  # drop-in parity binary: reference + C++ adapter + product
+            subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "dropin"], check=True)
 
 
 def build_all(force: bool = False, verbose: bool = False) -> None:

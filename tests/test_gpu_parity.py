@@ -296,3 +296,21 @@ def test_baseline_equals_fast_algorithm(tiny32):
     fast, _ = matmul(s, o2.encode_inputs(x), EncodedWeights.from_prepared(s, o2.encode_weights(w), 30), b)
     assert np.array_equal(o2.unpack_baseline(base, 20, 3), o2.unpack(fast, 20, 3))
     assert np.array_equal(o2.unpack(fast, 20, 3), oracle_matmul(x, w, b))
+
+
+def test_cpp_dropin_adapter_matches_unmodified_reference():
+    """The reference's own hei::matmul (compiled in place) and the product's
+    C++ drop-in adapter (paper_2204_05496_b200/dropin) on the same backend,
+    keys and input ciphertexts: every packed residue, the stream path, the
+    standard algorithm and the KeyError contract (oracle/dropin_test.cpp)."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_test not built (needs /root/reference at build time)")
+    r = subprocess.run([exe, "--production"], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "DROPIN OK" in r.stdout
+    assert r.stdout.count("bit-exact") == 6
