@@ -257,8 +257,27 @@ def run_ours(args, world, rank, local):
     d_out = torch.empty((C_, ctw), dtype=torch.int32, device=dev)
     stream = torch.cuda.Stream(device=dev)
 
-    def step():
-        matmul_device(srv, d_in.data_ptr(), R, ew, b, d_out.data_ptr(), stream.cuda_stream)
+    if world == 1:
+        def step():
+            matmul_device(srv, d_in.data_ptr(), R, ew, b, d_out.data_ptr(), stream.cuda_stream)
+    else:
+        # individual sharding: rank r holds rows [r*R, (r+1)*R) of a world*R
+        # batch; one int64 all-reduce of the packed partials (NCCL/NVLink),
+        # then the mod-q reduction + bias add on every rank.
+        from paper_2204_05496_b200.sharding import finish_packed_device, matmul_partial_device, packed_count
+
+        total_rows = world * R
+        Ct = packed_count(total_rows, cols, n)
+        acc = torch.zeros((Ct, ctw), dtype=torch.int64, device=dev)
+        d_out = torch.empty((Ct, ctw), dtype=torch.int32, device=dev)
+
+        def step():
+            with torch.cuda.stream(stream):
+                acc.zero_()
+            matmul_partial_device(srv, ew, d_in.data_ptr(), R, rank * R, total_rows, acc.data_ptr(), stream.cuda_stream)
+            with torch.cuda.stream(stream):
+                torch.distributed.all_reduce(acc)
+            finish_packed_device(srv, ew, acc.data_ptr(), b, total_rows, d_out.data_ptr(), stream.cuda_stream)
 
     for _ in range(args.warmup):
         with torch.cuda.stream(stream):

@@ -102,6 +102,19 @@ int hei_gpu_matmul_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint
                           int form, uint64_t rows, const int64_t* bias, uint32_t* d_out,
                           hei_op_counters* counters, void* stream);
 
+/* Sharded execution (one process per GPU). Each rank adds the
+ * masked class results of its rows [row_offset, row_offset + rows) of a
+ * total_rows batch into d_acc, an unreduced u64 packed accumulator
+ * [C][twin ct] (C = ceil(total_rows * cols / N), zeroed by the caller).
+ * Partial accumulators of all ranks sum exactly (no wrap below 2^63), so the
+ * exchange is one integer all-reduce; finish_packed then reduces mod q and
+ * adds the bias once (MatmulStream::finish, matmul.cpp:342-374). */
+int hei_gpu_matmul_partial_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint32_t* d_inputs,
+                                  uint64_t rows, uint64_t row_offset, uint64_t total_rows, uint64_t* d_acc,
+                                  void* stream);
+int hei_gpu_finish_packed_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint64_t* d_acc,
+                                 const int64_t* bias, uint64_t total_rows, uint32_t* d_out, void* stream);
+
 /* MatmulStream (matmul.hpp:83-114): rows in any order, each once. */
 int hei_gpu_stream_create(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const int64_t* bias,
                           uint64_t total_rows, hei_gpu_stream** out);

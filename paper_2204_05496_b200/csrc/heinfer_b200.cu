@@ -1190,6 +1190,7 @@ struct hei_gpu_stream {
   std::vector<bool> seen;
   bool finished = false;
   unsigned long long* d_acc = nullptr;  // [C][twin ct] u64
+  bool owns_acc = true;
   // pending rows staged on the device
   std::vector<uint64_t> pend_idx;
   uint32_t* d_stage = nullptr;  // [cap][k][twin ct] u32
@@ -1447,7 +1448,7 @@ hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64
 void stream_free(hei_gpu_stream* s) {
   if (!s) return;
   cudaSetDevice(s->ctx->device);
-  cudaFree(s->d_acc);
+  if (s->owns_acc) cudaFree(s->d_acc);
   cudaFree(s->d_stage);
   cudaFree(s->d_stage64);
   cudaFree(s->d_rows);
@@ -2229,6 +2230,54 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     }
     check_err_flag(c, HEI_INTERNAL, "baseline: rng rejection in the encryption stream (replay unsupported)");
     if (cnt) hei_baseline_counts(rows, cols, f, n, cnt);
+  });
+}
+
+
+// ---- sharded (multi-GPU) building blocks: partial packed sums + finish ----
+int hei_gpu_matmul_partial_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint32_t* d_inputs, uint64_t rows,
+                                  uint64_t row_offset, uint64_t total_rows, uint64_t* d_acc, void* stream) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (rows == 0 || row_offset + rows > total_rows) raise(HEI_PARAM_ERROR, "matmul: shard rows out of range");
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    std::vector<int64_t> zero_bias(w->cols, 0);
+    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, zero_bias.data(), total_rows, false),
+                                                                  stream_free);
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(s->d_acc);  // accumulate straight into the caller's buffer
+    s->d_acc = reinterpret_cast<unsigned long long*>(d_acc);
+    s->owns_acc = false;
+    const size_t words = w->kc * c->ct_words();
+    std::vector<uint64_t> idx(s->cap_rows);
+    for (uint64_t r0 = 0; r0 < rows; r0 += s->cap_rows) {
+      const uint64_t nr = std::min<uint64_t>(s->cap_rows, rows - r0);
+      for (uint64_t k = 0; k < nr; ++k) idx[k] = row_offset + r0 + k;
+      CU(cudaMemcpyAsync(s->d_rows, idx.data(), nr * 8, cudaMemcpyHostToDevice, st));
+      run_rows(s.get(), d_inputs + r0 * words, s->d_rows, nr, st);
+      CU(cudaStreamSynchronize(st));
+    }
+  });
+}
+
+int hei_gpu_finish_packed_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint64_t* d_acc, const int64_t* bias,
+                                 uint64_t total_rows, uint32_t* d_out, void* stream) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    check_bias_range(c, bias, w->cols);
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    hei_gpu_stream tmp{};
+    tmp.ctx = c;
+    tmp.w = w;
+    tmp.bias.assign(bias, bias + w->cols);
+    tmp.rows = total_rows;
+    tmp.C = (total_rows * w->cols + c->n - 1) / c->n;
+    tmp.d_acc = reinterpret_cast<unsigned long long*>(const_cast<uint64_t*>(d_acc));
+    tmp.owns_acc = false;
+    finish_to(&tmp, d_out, st);
+    CU(cudaStreamSynchronize(st));
   });
 }
 

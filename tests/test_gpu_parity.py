@@ -314,3 +314,38 @@ def test_cpp_dropin_adapter_matches_unmodified_reference():
     assert r.returncode == 0, r.stdout + r.stderr
     assert "DROPIN OK" in r.stdout
     assert r.stdout.count("bit-exact") == 6
+
+
+def test_sharded_partials_sum_to_single_gpu_result(prod):
+    """Three 'ranks' run back to back on one GPU (no cross-waiting kernels):
+    partial packed accumulators over disjoint row blocks, summed and finished,
+    equal the single-call result and the oracle bit for bit."""
+    import torch
+
+    from paper_2204_05496_b200 import EncodedWeights, matmul
+    from paper_2204_05496_b200.sharding import finish_packed_device, matmul_partial_device, packed_count, shard_rows
+
+    o, s = prod
+    R, f, cols = 5, 3000, 3
+    x, w, b = synthetic(R, f, cols, 0.05, 0.1, seed=21)
+    inputs = o.encode_inputs(x)
+    wp = o.encode_weights(w)
+    ew = EncodedWeights.from_prepared(s, wp, f)
+    want, _ = o.fast_matmul(inputs, f, wp, b)
+    single, _ = matmul(s, inputs, ew, b)
+    assert np.array_equal(single, want)
+    dev = torch.device("cuda", 0)
+    d_in = torch.from_numpy(inputs.astype(np.uint32).view(np.int32)).to(dev)
+    C_ = packed_count(R, cols, s.n)
+    total = torch.zeros((C_, s.ct_words), dtype=torch.int64, device=dev)
+    world = 3
+    for r in range(world):
+        lo, cnt = shard_rows(R, world, r)
+        acc = torch.zeros_like(total)
+        matmul_partial_device(s, ew, d_in[lo:].data_ptr(), cnt, lo, R, acc.data_ptr())
+        total += acc  # stands in for the NCCL all-reduce
+    out = torch.empty((C_, s.ct_words), dtype=torch.int32, device=dev)
+    finish_packed_device(s, ew, total.data_ptr(), b, R, out.data_ptr())
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert np.array_equal(got, want)
