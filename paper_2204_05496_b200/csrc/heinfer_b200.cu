@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T) k_rot_keyswitch_f(Geo g, const u
 #pragma unroll
       for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
     }
-    NT::fwd(e, sm, tw, twc, q);
+    NT::template fwd<true>(e, sm, tw, twc, q);
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
 #pragma unroll
@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_rot_keyswitch_s(Geo g, cons
 #pragma unroll
       for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
     }
-    NT::fwd(e, sm, tw, twc, q);
+    NT::template fwd<true>(e, sm, tw, twc, q);
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
 #pragma unroll
@@ -1166,6 +1166,14 @@ struct hei_gpu_ctx {
   uint32_t *d_dotA = nullptr, *d_dotB = nullptr, *d_dig = nullptr;
   uint64_t scratch_pairs = 0;
   std::mutex mu;
+  // grow-only device pools for the per-call buffers of the device-resident
+  // path (every C-ABI call synchronizes before returning, so reuse is safe)
+  unsigned long long* pool_acc = nullptr;
+  size_t pool_acc_bytes = 0;
+  uint64_t* pool_rows = nullptr;
+  size_t pool_rows_bytes = 0;
+  int64_t* pool_bias = nullptr;
+  size_t pool_bias_bytes = 0;
   // optional per-kernel timing (bench.py roofline): events around the fold
   bool timing = false;
   std::vector<std::array<cudaEvent_t, 3>> fold_ev;  // digits: [0,1], key switch: [1,2]
@@ -1190,7 +1198,7 @@ struct hei_gpu_stream {
   std::vector<bool> seen;
   bool finished = false;
   unsigned long long* d_acc = nullptr;  // [C][twin ct] u64
-  bool owns_acc = true;
+  bool owns_acc = true, owns_rows = true;
   // pending rows staged on the device
   std::vector<uint64_t> pend_idx;
   uint32_t* d_stage = nullptr;  // [cap][k][twin ct] u32
@@ -1225,6 +1233,17 @@ void check_err_flag(hei_gpu_ctx* c, int code, const char* what) {
 unsigned grid_for(uint64_t total, unsigned threads) {
   uint64_t b = (total + threads - 1) / threads;
   return (unsigned)std::min<uint64_t>(b, 148ull * 32);
+}
+
+template <typename T>
+T* pool_get(T*& p, size_t& cap, size_t bytes) {
+  if (bytes > cap) {
+    if (p) CU(cudaFree(p));
+    p = nullptr;
+    CU(cudaMalloc(&p, bytes));
+    cap = bytes;
+  }
+  return p;
 }
 
 void ensure_scratch(hei_gpu_ctx* c, uint64_t pairs) {
@@ -1391,13 +1410,11 @@ void stream_flush(hei_gpu_stream* s) {
 
 void finish_to(hei_gpu_stream* s, uint32_t* d_out, cudaStream_t st) {
   hei_gpu_ctx* c = s->ctx;
-  int64_t* d_bias = nullptr;
-  CU(cudaMallocAsync(&d_bias, s->bias.size() * 8, st));
+  int64_t* d_bias = pool_get(c->pool_bias, c->pool_bias_bytes, s->bias.size() * 8);
   CU(cudaMemcpyAsync(d_bias, s->bias.data(), s->bias.size() * 8, cudaMemcpyHostToDevice, st));
   k_finish<<<(unsigned)(s->C * c->P()), c->threads(), smem_bytes(c, 1), st>>>(
       c->geo, s->d_acc, d_bias, (uint32_t)s->w->cols, s->rows * s->w->cols, d_out);
   LAUNCHED();
-  CU(cudaFreeAsync(d_bias, st));
 }
 
 void check_bias_range(hei_gpu_ctx* c, const int64_t* bias, uint64_t cols) {
@@ -1433,15 +1450,21 @@ hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64
   s->rows = rows;
   s->seen.assign(rows, false);
   s->C = (rows * w->cols + c->n - 1) / c->n;
-  CU(cudaMalloc(&s->d_acc, s->C * c->ct_words() * 8));
-  CU(cudaMemsetAsync(s->d_acc, 0, s->C * c->ct_words() * 8, c->stream));
   const uint64_t bp = auto_batch_pairs(c);
   s->cap_rows = std::max<uint64_t>(1, std::min<uint64_t>(rows, bp / w->cols));
   if (host_staging) {
+    CU(cudaMalloc(&s->d_acc, s->C * c->ct_words() * 8));
     CU(cudaMalloc(&s->d_stage, s->cap_rows * w->kc * c->ct_words() * 4));
     CU(cudaMalloc(&s->d_stage64, s->cap_rows * w->kc * c->ct_words() * 8));
+    CU(cudaMalloc(&s->d_rows, s->cap_rows * 8));
+  } else {
+    // one-shot device-resident call: borrow the context pools
+    s->d_acc = pool_get(c->pool_acc, c->pool_acc_bytes, s->C * c->ct_words() * 8);
+    s->d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, s->cap_rows * 8);
+    s->owns_acc = false;
+    s->owns_rows = false;
   }
-  CU(cudaMalloc(&s->d_rows, s->cap_rows * 8));
+  CU(cudaMemsetAsync(s->d_acc, 0, s->C * c->ct_words() * 8, c->stream));
   return s.release();
 }
 
@@ -1449,9 +1472,9 @@ void stream_free(hei_gpu_stream* s) {
   if (!s) return;
   cudaSetDevice(s->ctx->device);
   if (s->owns_acc) cudaFree(s->d_acc);
-  cudaFree(s->d_stage);
-  cudaFree(s->d_stage64);
-  cudaFree(s->d_rows);
+  if (s->d_stage) cudaFree(s->d_stage);
+  if (s->d_stage64) cudaFree(s->d_stage64);
+  if (s->owns_rows) cudaFree(s->d_rows);
   delete s;
 }
 
@@ -1779,6 +1802,9 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
     cudaFree(c->d_pk[b]);
   }
   cudaFree(c->d_pkp);
+  cudaFree(c->pool_acc);
+  cudaFree(c->pool_rows);
+  cudaFree(c->pool_bias);
   cudaFree(c->d_dotA);
   cudaFree(c->d_dotB);
   cudaFree(c->d_dig);
@@ -2246,8 +2272,7 @@ int hei_gpu_matmul_partial_device(hei_gpu_ctx* c, const hei_gpu_weights* w, cons
     std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, zero_bias.data(), total_rows, false),
                                                                   stream_free);
     CU(cudaStreamSynchronize(c->stream));
-    cudaFree(s->d_acc);  // accumulate straight into the caller's buffer
-    s->d_acc = reinterpret_cast<unsigned long long*>(d_acc);
+    s->d_acc = reinterpret_cast<unsigned long long*>(d_acc);  // the caller's buffer
     s->owns_acc = false;
     const size_t words = w->kc * c->ct_words();
     std::vector<uint64_t> idx(s->cap_rows);

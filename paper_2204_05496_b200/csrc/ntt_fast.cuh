@@ -61,16 +61,29 @@ struct Ntt {
     return grp * G + 16 * h;
   }
 
-  static __device__ __forceinline__ void ct(uint32_t& u, uint32_t& v, uint2 w, uint32_t q) {
-    const uint32_t t = mul_shoup(v, w.x, w.y, q);
-    v = sub_mod(u, t, q);
-    u = add_mod(u, t, q);
+  // Cooley-Tukey butterfly with lazy outputs: u must be reduced (< q), v may
+  // be lazy (< 2q; Shoup accepts any x < 2^32). Each output is reduced only
+  // if the next stage uses it as a `u` (ru / rv); a lazy value is < 2q < 2^32.
+  // Every value stays congruent to the reference's, and each stage that
+  // feeds an add sees reduced operands, so the final result is identical.
+  static __device__ __forceinline__ void ct(uint32_t& u, uint32_t& v, uint2 w, uint32_t q, bool ru = true,
+                                            bool rv = true) {
+    const uint32_t t = mul_shoup(v, w.x, w.y, q);  // [0, q)
+    uint32_t a = u + t, b = u - t + q;             // [0, 2q), (0, 2q)
+    if (ru) a = min(a, a - q);
+    if (rv) b = min(b, b - q);
+    u = a;
+    v = b;
   }
+  // Gentleman-Sande: the difference feeds Shoup unreduced (u - v + q < 2q).
   static __device__ __forceinline__ void gs(uint32_t& u, uint32_t& v, uint2 w, uint32_t q) {
-    const uint32_t d = sub_mod(u, v, q);
+    const uint32_t d = u - v + q;
     u = add_mod(u, v, q);
     v = mul_shoup(d, w.x, w.y, q);
   }
+  // reduce output x of a stage whose butterfly half-distance is `half` iff
+  // the next stage (half / 2) uses it as the reduced operand u.
+  static __device__ __forceinline__ constexpr bool red(int x, int half) { return !(x & (half >> 1)); }
 
   static __device__ __forceinline__ void store_pos(uint32_t* sm, uint32_t x, uint32_t v) { sm[swz(x)] = v; }
   static __device__ __forceinline__ void storeC(uint32_t* sm, uint32_t j, const uint32_t (&e)[16]) {
@@ -93,6 +106,9 @@ struct Ntt {
 
   // Forward: e in pass-A order -> e in pass-C order. Begins and ends with a
   // barrier on the shared buffer (sm: N words).
+  // LAZY_OUT: leave the final stage's outputs in [0, 2q) (for consumers that
+  // only feed them to a Shoup multiply).
+  template <bool LAZY_OUT = false>
   static __device__ __forceinline__ void fwd(uint32_t (&e)[16], uint32_t* sm, const uint2* __restrict__ tw,
                                              const uint4* __restrict__ twc, uint32_t q) {
     const uint32_t j = threadIdx.x;
@@ -102,7 +118,7 @@ struct Ntt {
       const int half = 8 >> s;
 #pragma unroll
       for (int r = 0; r < 16; ++r)
-        if (!(r & half)) ct(e[r], e[r + half], __ldg(&tw[(1 << s) + (r >> (4 - s))]), q);
+        if (!(r & half)) ct(e[r], e[r + half], __ldg(&tw[(1 << s) + (r >> (4 - s))]), q, red(r, half), red(r + half, half));
     }
     __syncthreads();
 #pragma unroll
@@ -118,7 +134,8 @@ struct Ntt {
         const int half = 8 >> s;
 #pragma unroll
         for (int r = 0; r < 16; ++r)
-          if (!(r & half)) ct(e[r], e[r + half], __ldg(&tw[(16u << s) + (blk << s) + (r >> (4 - s))]), q);
+          if (!(r & half))
+            ct(e[r], e[r + half], __ldg(&tw[(16u << s) + (blk << s) + (r >> (4 - s))]), q, red(r, half), red(r + half, half));
       }
     }
 #pragma unroll
@@ -142,14 +159,16 @@ struct Ntt {
         e[r] = upper ? sub_mod(other, mine, q) : add_mod(mine, other, q);
       }
     }
-    ct(e[0], e[8], entry(tc, B0), q);
+    {
+      const uint2 w = entry(tc, B0);
 #pragma unroll
-    for (int r = 1; r < 8; ++r) ct(e[r], e[r + 8], entry(tc, B0), q);
+      for (int r = 0; r < 8; ++r) ct(e[r], e[r + 8], w, q, red(r, 8), red(r + 8, 8));
+    }
     {
       const uint4 v = __ldg(tc + ((B0 + 1) >> 1) * T);
 #pragma unroll
       for (int r = 0; r < 16; ++r)
-        if (!(r & 4)) ct(e[r], e[r + 4], (r >> 3) ? hi(v) : lo(v), q);
+        if (!(r & 4)) ct(e[r], e[r + 4], (r >> 3) ? hi(v) : lo(v), q, red(r, 4), red(r + 4, 4));
     }
     {
       const uint4 v0 = __ldg(tc + ((B0 + 3) >> 1) * T), v1 = __ldg(tc + ((B0 + 5) >> 1) * T);
@@ -158,7 +177,7 @@ struct Ntt {
         if (r & 2) continue;
         const int b = r >> 2;
         const uint4 v = b < 2 ? v0 : v1;
-        ct(e[r], e[r + 2], (b & 1) ? hi(v) : lo(v), q);
+        ct(e[r], e[r + 2], (b & 1) ? hi(v) : lo(v), q, red(r, 2), red(r + 2, 2));
       }
     }
     {
@@ -168,7 +187,7 @@ struct Ntt {
 #pragma unroll
       for (int r = 0; r < 16; r += 2) {
         const int b = r >> 1;
-        ct(e[r], e[r + 1], (b & 1) ? hi(v[b >> 1]) : lo(v[b >> 1]), q);
+        ct(e[r], e[r + 1], (b & 1) ? hi(v[b >> 1]) : lo(v[b >> 1]), q, !LAZY_OUT, !LAZY_OUT);
       }
     }
   }
@@ -257,8 +276,8 @@ struct Ntt {
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const uint32_t u = e[r], v = e[r + 8];
-      e[r] = mul_shoup(add_mod(u, v, q), ninv.x, ninv.y, q);
-      e[r + 8] = mul_shoup(sub_mod(u, v, q), last.x, last.y, q);
+      e[r] = mul_shoup(u + v, ninv.x, ninv.y, q);
+      e[r + 8] = mul_shoup(u - v + q, last.x, last.y, q);
     }
   }
 };
