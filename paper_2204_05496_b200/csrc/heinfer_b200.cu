@@ -1174,6 +1174,15 @@ struct hei_gpu_ctx {
   size_t pool_rows_bytes = 0;
   int64_t* pool_bias = nullptr;
   size_t pool_bias_bytes = 0;
+  uint64_t* pool_stage64 = nullptr;
+  size_t pool_stage64_bytes = 0;
+  uint32_t* pool_in32 = nullptr;
+  size_t pool_in32_bytes = 0;
+  uint32_t* pool_out = nullptr;
+  size_t pool_out_bytes = 0;
+  uint64_t* pool_out64 = nullptr;
+  size_t pool_out64_bytes = 0;
+  cudaStream_t copy_stream = nullptr;
   // optional per-kernel timing (bench.py roofline): events around the fold
   bool timing = false;
   std::vector<std::array<cudaEvent_t, 3>> fold_ev;  // digits: [0,1], key switch: [1,2]
@@ -1805,6 +1814,11 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->pool_acc);
   cudaFree(c->pool_rows);
   cudaFree(c->pool_bias);
+  cudaFree(c->pool_stage64);
+  cudaFree(c->pool_in32);
+  cudaFree(c->pool_out);
+  cudaFree(c->pool_out64);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   cudaFree(c->d_dotA);
   cudaFree(c->d_dotB);
   cudaFree(c->d_dig);
@@ -1990,13 +2004,64 @@ void hei_gpu_stream_destroy(hei_gpu_stream* s) { stream_free(s); }
 
 int hei_gpu_matmul(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint64_t* inputs, int form, uint64_t rows,
                    const int64_t* bias, uint64_t* out, hei_op_counters* cnt) {
+  // Host-buffer path: rows stream to the device in chunks on a copy stream
+  // (double-buffered u64 staging) while earlier chunks are narrowed and
+  // folded on the compute stream, so H2D overlaps the key switching.
   return guarded([&] {
     set_device(c);
     std::lock_guard<std::mutex> lk(c->mu);
-    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, bias, rows), stream_free);
+    if (form != HEI_FORM_EVAL && form != HEI_FORM_COEFF) raise(HEI_PARAM_ERROR, "matmul: unknown form");
+    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, bias, rows, false), stream_free);
+    cudaStream_t st = c->stream;
+    if (!c->copy_stream) CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    cudaStream_t cs = c->copy_stream;
     const size_t words = w->kc * c->ct_words();
-    for (uint64_t r = 0; r < rows; ++r) stream_push(s.get(), r, inputs + r * words, form);
-    stream_finish(s.get(), out, cnt);
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(s->cap_rows, (rows + 7) / 8));
+    const uint64_t nchunks = (rows + chunk - 1) / chunk;
+    uint64_t* stage64 = pool_get(c->pool_stage64, c->pool_stage64_bytes, 2 * chunk * words * 8);
+    uint32_t* in32 = pool_get(c->pool_in32, c->pool_in32_bytes, 2 * chunk * words * 4);
+    uint64_t* d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, rows * 8);
+    std::vector<uint64_t> idx(rows);
+    for (uint64_t r = 0; r < rows; ++r) idx[r] = r;
+    CU(cudaMemcpyAsync(d_rows, idx.data(), rows * 8, cudaMemcpyHostToDevice, st));
+    cudaEvent_t copied[2], narrowed[2];
+    for (int k = 0; k < 2; ++k) {
+      CU(cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&narrowed[k], cudaEventDisableTiming));
+      CU(cudaEventRecord(narrowed[k], st));
+    }
+    CU(cudaStreamSynchronize(st));  // zeroed accumulators + row ids in place
+    for (uint64_t b = 0; b < nchunks; ++b) {
+      const int slot = (int)(b % 2);
+      const uint64_t r0 = b * chunk, nr = std::min<uint64_t>(chunk, rows - r0);
+      uint64_t* s64 = stage64 + (size_t)slot * chunk * words;
+      uint32_t* s32 = in32 + (size_t)slot * chunk * words;
+      CU(cudaStreamWaitEvent(cs, narrowed[slot], 0));
+      CU(cudaMemcpyAsync(s64, inputs + r0 * words, nr * words * 8, cudaMemcpyHostToDevice, cs));
+      CU(cudaEventRecord(copied[slot], cs));
+      CU(cudaStreamWaitEvent(st, copied[slot], 0));
+      k_narrow<<<grid_for(nr * words, 256), 256, 0, st>>>(c->geo, s64, s32, nr * w->kc, c->d_err);
+      LAUNCHED();
+      CU(cudaEventRecord(narrowed[slot], st));
+      if (form == HEI_FORM_COEFF) launch_ct_ntt(c, (unsigned)(nr * w->kc * 2 * c->P()), s32, st);
+      run_rows(s.get(), s32, d_rows + r0, nr, st);
+    }
+    CU(cudaStreamSynchronize(st));
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(copied[k]);
+      cudaEventDestroy(narrowed[k]);
+    }
+    check_err_flag(c, HEI_CODEC_ERROR, "matmul: coefficient not reduced");
+    s->pushed = rows;
+    uint32_t* d_out = pool_get(c->pool_out, c->pool_out_bytes, s->C * c->ct_words() * 4);
+    uint64_t* d_out64 = pool_get(c->pool_out64, c->pool_out64_bytes, s->C * c->ct_words() * 8);
+    finish_to(s.get(), d_out, st);
+    k_widen<<<grid_for(s->C * c->ct_words(), 256), 256, 0, st>>>(d_out, d_out64, s->C * c->ct_words());
+    LAUNCHED();
+    CU(cudaMemcpyAsync(out, d_out64, s->C * c->ct_words() * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    s->finished = true;
+    if (cnt) hei_proposed_counts(rows, w->cols, w->f, c->n, cnt);
   });
 }
 
