@@ -182,6 +182,8 @@ struct BranchInfo {
   uint32_t t;
   uint32_t L, first;
   uint2 ninv, last;  // mod-t inverse NTT constants
+  uint32_t psi_inv;  // psi_t^-1 (inverse of the 2n-th root of the mod-t tables)
+  uint64_t mu;       // floor(2^64 / t)
 };
 struct Geo {
   uint32_t n, logn, P, ct_words, pt_words;
@@ -583,7 +585,7 @@ __device__ __forceinline__ void store16(uint32_t* __restrict__ p, const uint32_t
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(Ntt<LOGN>::T) k_rot_digits_f(Geo g, const uint32_t* __restrict__ dot,
+__global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digits_f(Geo g, const uint32_t* __restrict__ dot,
                                                               const uint32_t* __restrict__ perm,
                                                               uint32_t* __restrict__ digits) {
   using NT = Ntt<LOGN>;
@@ -792,8 +794,103 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_rot_keyswitch_s(Geo g, cons
   }
 }
 
+
+// Mask multiply + packed accumulation, G pairs per block (matmul.cpp:329-338).
+// The one-hot's INTT_t has a closed form: slot s sits at eval position
+// p = index_map[s], i.e. at psi^(2 brv(p) + 1), so its coefficients are
+// m_j = n^-1 * w^j (mod t) with w = psi^-(2 brv(p) + 1) — identical values to
+// the reference's INTT. Products accumulate mod q in shared memory across
+// the block's pairs and leave through one u64 atomic per slot and flush.
+__device__ __forceinline__ uint32_t pow_barrett(uint32_t b, uint32_t e, uint32_t t, uint64_t mu) {
+  uint32_t r = 1;
+  while (e) {
+    if (e & 1) r = mul_barrett(r, b, t, mu);
+    b = mul_barrett(b, b, t, mu);
+    e >>= 1;
+  }
+  return r;
+}
+
 template <int LOGN>
-__global__ void __launch_bounds__(Ntt<LOGN>::T) k_mask_acc_f(Geo g, const uint32_t* __restrict__ dot,
+__global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_mask_acc_g(Geo g, const uint32_t* __restrict__ dot,
+                                                               const uint64_t* __restrict__ rows, uint32_t cols,
+                                                               uint32_t npairs, uint32_t G,
+                                                               unsigned long long* __restrict__ acc64) {
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N, T = NT::T;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  uint4* a0s = smem4 + N / 4;
+  uint4* a1s = a0s + 4 * T;
+  const uint32_t gp = blockIdx.x % g.P;
+  const uint32_t p0 = (blockIdx.x / g.P) * G, p1 = min(npairs, p0 + G);
+  const PrimeInfo& pr = g.pr[gp];
+  const BranchInfo& br = g.br[pr.b];
+  const uint32_t q = pr.q, t = br.t, j = threadIdx.x, x0 = NT::posC0(j);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) a0s[c * T + j] = a1s[c * T + j] = make_uint4(0, 0, 0, 0);
+  uint64_t c_cur = ~0ull;
+  auto flush = [&](uint64_t cc) {
+    unsigned long long* d0 = acc64 + cc * g.ct_words + (uint64_t)pr.poly0 * N + x0;
+    unsigned long long* d1 = acc64 + cc * g.ct_words + (uint64_t)pr.poly1 * N + x0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint4 A = a0s[c * T + j], B = a1s[c * T + j];
+      atomicAdd(&d0[4 * c], (unsigned long long)A.x);
+      atomicAdd(&d0[4 * c + 1], (unsigned long long)A.y);
+      atomicAdd(&d0[4 * c + 2], (unsigned long long)A.z);
+      atomicAdd(&d0[4 * c + 3], (unsigned long long)A.w);
+      atomicAdd(&d1[4 * c], (unsigned long long)B.x);
+      atomicAdd(&d1[4 * c + 1], (unsigned long long)B.y);
+      atomicAdd(&d1[4 * c + 2], (unsigned long long)B.z);
+      atomicAdd(&d1[4 * c + 3], (unsigned long long)B.w);
+      a0s[c * T + j] = a1s[c * T + j] = make_uint4(0, 0, 0, 0);
+    }
+  };
+  for (uint32_t pair = p0; pair < p1; ++pair) {
+    const uint64_t gidx = rows[pair / cols] * cols + pair % cols;
+    const uint32_t slot = (uint32_t)(gidx % N);
+    const uint64_t c = gidx / N;
+    if (c != c_cur) {
+      if (c_cur != ~0ull) flush(c_cur);
+      c_cur = c;
+    }
+    // m at pass-A coefficient positions x = j + T r
+    const uint32_t pe = __brev(__ldg(&g.index_map[slot])) >> (32 - LOGN);
+    const uint32_t w = pow_barrett(br.psi_inv, 2 * pe + 1, t, br.mu);
+    const uint32_t wT = pow_barrett(w, T, t, br.mu);
+    uint32_t m = mul_barrett(br.ninv.x, pow_barrett(w, j, t, br.mu), t, br.mu);
+    uint32_t e[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      e[r] = m % q;
+      m = mul_barrett(m, wT, t, br.mu);
+    }
+    NT::fwd(e, sm, g.fwd + (size_t)gp * N, g.twc + (size_t)gp * g.twc_stride, q);
+    const uint32_t* base = dot + (uint64_t)pair * g.ct_words;
+    const uint4* d0 = reinterpret_cast<const uint4*>(base + (uint64_t)pr.poly0 * N + x0);
+    const uint4* d1 = reinterpret_cast<const uint4*>(base + (uint64_t)pr.poly1 * N + x0);
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4) {
+      const uint4 u = d0[c4], v = d1[c4];
+      uint4 A = a0s[c4 * T + j], B = a1s[c4 * T + j];
+      A.x = add_mod(A.x, mul_barrett(u.x, e[4 * c4], q, pr.mu), q);
+      A.y = add_mod(A.y, mul_barrett(u.y, e[4 * c4 + 1], q, pr.mu), q);
+      A.z = add_mod(A.z, mul_barrett(u.z, e[4 * c4 + 2], q, pr.mu), q);
+      A.w = add_mod(A.w, mul_barrett(u.w, e[4 * c4 + 3], q, pr.mu), q);
+      B.x = add_mod(B.x, mul_barrett(v.x, e[4 * c4], q, pr.mu), q);
+      B.y = add_mod(B.y, mul_barrett(v.y, e[4 * c4 + 1], q, pr.mu), q);
+      B.z = add_mod(B.z, mul_barrett(v.z, e[4 * c4 + 2], q, pr.mu), q);
+      B.w = add_mod(B.w, mul_barrett(v.w, e[4 * c4 + 3], q, pr.mu), q);
+      a0s[c4 * T + j] = A;
+      a1s[c4 * T + j] = B;
+    }
+  }
+  if (c_cur != ~0ull) flush(c_cur);
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_mask_acc_f(Geo g, const uint32_t* __restrict__ dot,
                                                             const uint64_t* __restrict__ rows, uint32_t cols,
                                                             unsigned long long* __restrict__ acc64) {
   using NT = Ntt<LOGN>;
@@ -1313,7 +1410,11 @@ void launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const u
 void launch_mask_acc(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* res, const uint64_t* rows,
                      uint32_t cols, unsigned long long* acc, cudaStream_t st) {
   const size_t sm = smem_bytes(c, 1);
-  HEI_DISPATCH(c->logn, (k_mask_acc_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(g, res, rows, cols, acc)),
+  const uint32_t npairs = blocks / g.P;
+  // enough blocks for every SM at small batches, up to 8 pairs per block
+  const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(8, npairs * g.P / (148 * 8)));
+  const unsigned gblocks = (unsigned)(((npairs + G - 1) / G) * g.P);
+  HEI_DISPATCH(c->logn, (k_mask_acc_g<LG><<<gblocks, Ntt<LG>::T, 3 * sm, st>>>(g, res, rows, cols, npairs, G, acc)),
                (k_mask_acc<<<blocks, c->threads(), sm, st>>>(g, res, rows, cols, acc)));
   LAUNCHED();
 }
@@ -1335,6 +1436,7 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_keyswitch_f<LG>, sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG>, 3 * sm);
   set_smem_attr((const void*)k_mask_acc_f<LG>, sm);
+  set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
   set_smem_attr((const void*)k_ct_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_poly_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_bl_encode<LG>, sm);
@@ -1687,6 +1789,8 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
       br.L = c->L[b];
       br.first = first;
       build(t, P + b, br.last, br.ninv);
+      br.psi_inv = (uint32_t)invmod(root_2n(n, t), t);
+      br.mu = (uint64_t)(((u128)1 << 64) / t);
       uint64_t qmin = UINT64_MAX, qmax = 0;
       for (uint32_t i = 0; i < c->L[b]; ++i) qmin = std::min(qmin, d->q[first + i]), qmax = std::max(qmax, d->q[first + i]);
       for (uint32_t i = 0; i < c->L[b]; ++i) {
