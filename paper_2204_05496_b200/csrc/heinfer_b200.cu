@@ -198,6 +198,13 @@ struct Geo {
   const uint32_t* index_map;
 };
 
+// Pass-A/B twiddles (indices 0..255) of every q prime, passed by value in the
+// kernel parameter space (CUDA >= 12.1 allows 32 KB of parameters).
+constexpr int kMaxAB = 12;
+struct TwAB {
+  uint2 w[kMaxAB][256];
+};
+
 // ----------------------------------------------------------------- kernels
 __global__ void k_narrow(Geo g, const uint64_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t cts,
                          uint32_t* err) {
@@ -587,7 +594,8 @@ __device__ __forceinline__ void store16(uint32_t* __restrict__ p, const uint32_t
 template <int LOGN>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digits_f(Geo g, const uint32_t* __restrict__ dot,
                                                               const uint32_t* __restrict__ perm,
-                                                              uint32_t* __restrict__ digits) {
+                                                              uint32_t* __restrict__ digits,
+                                                              const __grid_constant__ TwAB itab) {
   using NT = Ntt<LOGN>;
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
@@ -599,7 +607,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digi
   load16_ro(perm + x0, pm);
 #pragma unroll
   for (int r = 0; r < 16; ++r) e[r] = c1[pm[r]];
-  NT::inv(e, sm, g.inv + (size_t)gp * NT::N, g.itwc + (size_t)gp * g.twc_stride, pr.q, pr.last, pr.ninv);
+  NT::inv(e, sm, ParamTw{itab.w[gp]}, g.itwc + (size_t)gp * g.twc_stride, pr.q, pr.last, pr.ninv);
   uint32_t* d = digits + ((uint64_t)pair * g.P + gp) * NT::N;
 #pragma unroll
   for (int r = 0; r < 16; ++r) d[NT::posA(j, r)] = e[r];
@@ -698,7 +706,8 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_rot_keyswitch_s(Geo g, cons
                                                                     const uint32_t* __restrict__ perm,
                                                                     const uint2* __restrict__ key0,
                                                                     const uint2* __restrict__ key1,
-                                                                    uint32_t* __restrict__ out, int fold) {
+                                                                    uint32_t* __restrict__ out, int fold,
+                                                                    const __grid_constant__ TwAB tab) {
   using NT = Ntt<LOGN>;
   constexpr uint32_t N = NT::N, T = NT::T;
   extern __shared__ uint4 smem4[];
@@ -730,7 +739,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_rot_keyswitch_s(Geo g, cons
     }
   }
   const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
-  const uint2* tw = g.fwd + (size_t)gp * N;
+  const ParamTw tw{tab.w[gp]};
   const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
   uint32_t e[16];
   for (uint32_t l = 0; l < L; ++l) {
@@ -1245,6 +1254,7 @@ struct hei_gpu_ctx {
   uint32_t s_x = 6, s_w = 14, in_bits = 8;
   Geo geo{};
   uint2 *d_fwd = nullptr, *d_inv = nullptr;
+  std::vector<uint2> h_fwd, h_inv;  // host copies (pass-A/B rows go in kernel params)
   uint4 *d_twc = nullptr, *d_itwc = nullptr;
   uint32_t* d_index = nullptr;
   // galois elements in fold order: steps 1, 2, ..., n/4, then the swap
@@ -1380,10 +1390,23 @@ void set_smem_attr(const void* fn, size_t bytes) {
     default: { GENERIC; } break;                      \
   }
 
+// Host copy of the pass-A/B twiddle rows for the primes of `g` (its pr[]
+// order; a branch-restricted Geo from apply_galois is handled by matching q).
+const TwAB* tabs_of(hei_gpu_ctx* c, const Geo& g, int inverse) {
+  thread_local TwAB t;
+  for (uint32_t k = 0; k < g.P && k < (uint32_t)kMaxAB; ++k) {
+    uint32_t src = 0;
+    for (uint32_t m = 0; m < c->geo.P; ++m)
+      if (c->geo.pr[m].q == g.pr[k].q) src = m;
+    std::memcpy(t.w[k], (inverse ? c->h_inv : c->h_fwd).data() + (size_t)src * c->n, 256 * sizeof(uint2));
+  }
+  return &t;
+}
+
 void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* perm,
                        uint32_t* dig, cudaStream_t st) {
   const size_t sm = smem_bytes(c, 1);
-  HEI_DISPATCH(c->logn, (k_rot_digits_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig)),
+  HEI_DISPATCH(c->logn, (k_rot_digits_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1))),
                (k_rot_digits<<<blocks, c->threads(), sm, st>>>(g, cur, perm, dig)));
   LAUNCHED();
 }
@@ -1394,10 +1417,12 @@ void launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const u
   // threads) keeps the accumulators in registers.
   switch (c->logn) {
     case 12:
-      k_rot_keyswitch_s<12><<<blocks, Ntt<12>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold);
+      k_rot_keyswitch_s<12><<<blocks, Ntt<12>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                          *tabs_of(c, g, 0));
       break;
     case 13:
-      k_rot_keyswitch_s<13><<<blocks, Ntt<13>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold);
+      k_rot_keyswitch_s<13><<<blocks, Ntt<13>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                          *tabs_of(c, g, 0));
       break;
     case 14:
       k_rot_keyswitch_f<14><<<blocks, Ntt<14>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, out, fold);
@@ -1719,6 +1744,8 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (n > 16384) raise(HEI_PARAM_ERROR, "ring degree above 16384 is not supported on the device path");
     if (d->L[0] == 0 || d->L[1] == 0) raise(HEI_PARAM_ERROR, "ciphertext modulus chain is empty");
     if (d->L[0] + d->L[1] > kMaxPrimes) raise(HEI_PARAM_ERROR, "too many primes for the device path");
+    if (n >= 4096 && d->L[0] + d->L[1] > (uint32_t)kMaxAB)
+      raise(HEI_PARAM_ERROR, "at most 12 ciphertext primes in total for N >= 4096 on the device path");
     if (d->t[0] == d->t[1]) raise(HEI_PARAM_ERROR, "twin moduli must differ");
     auto c = std::make_unique<hei_gpu_ctx>();
     c->device = d->device;
@@ -1874,6 +1901,8 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     CU(cudaMalloc(&c->d_perms, perms.size() * 4));
     CU(cudaMalloc(&c->d_err, 4));
     CU(cudaMemcpy(c->d_fwd, fwd.data(), fwd.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    c->h_fwd = fwd;
+    c->h_inv = inv;
     CU(cudaMemcpy(c->d_inv, inv.data(), inv.size() * sizeof(uint2), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(c->d_index, index_map.data(), n * 4, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(c->d_perms, perms.data(), perms.size() * 4, cudaMemcpyHostToDevice));

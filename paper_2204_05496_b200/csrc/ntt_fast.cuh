@@ -27,6 +27,15 @@ namespace heb {
 
 __device__ __forceinline__ uint32_t swz(uint32_t x) { return x ^ (((x >> 5) & 7u) << 2); }
 
+// Twiddle sources for passes A/B (indices 1..255): read-only global loads,
+// or a table passed in the kernel's parameter space (constant bank), which
+// keeps these warp-uniform reads off the L1 data pipe.
+__device__ __forceinline__ uint2 load_tw(const uint2* __restrict__ p, uint32_t i) { return __ldg(p + i); }
+struct ParamTw {
+  const uint2* p;
+};
+__device__ __forceinline__ uint2 load_tw(ParamTw t, uint32_t i) { return t.p[i]; }
+
 template <int LOGN>
 struct Ntt {
   static constexpr uint32_t N = 1u << LOGN;
@@ -108,9 +117,9 @@ struct Ntt {
   // barrier on the shared buffer (sm: N words).
   // LAZY_OUT: leave the final stage's outputs in [0, 2q) (for consumers that
   // only feed them to a Shoup multiply).
-  template <bool LAZY_OUT = false>
-  static __device__ __forceinline__ void fwd(uint32_t (&e)[16], uint32_t* sm, const uint2* __restrict__ tw,
-                                             const uint4* __restrict__ twc, uint32_t q) {
+  template <bool LAZY_OUT = false, typename TW = const uint2*>
+  static __device__ __forceinline__ void fwd(uint32_t (&e)[16], uint32_t* sm, TW tw, const uint4* __restrict__ twc,
+                                             uint32_t q) {
     const uint32_t j = threadIdx.x;
     // ---- pass A: stages 0..3
 #pragma unroll
@@ -118,7 +127,7 @@ struct Ntt {
       const int half = 8 >> s;
 #pragma unroll
       for (int r = 0; r < 16; ++r)
-        if (!(r & half)) ct(e[r], e[r + half], __ldg(&tw[(1 << s) + (r >> (4 - s))]), q, red(r, half), red(r + half, half));
+        if (!(r & half)) ct(e[r], e[r + half], load_tw(tw, (1 << s) + (r >> (4 - s))), q, red(r, half), red(r + half, half));
     }
     __syncthreads();
 #pragma unroll
@@ -135,7 +144,7 @@ struct Ntt {
 #pragma unroll
         for (int r = 0; r < 16; ++r)
           if (!(r & half))
-            ct(e[r], e[r + half], __ldg(&tw[(16u << s) + (blk << s) + (r >> (4 - s))]), q, red(r, half), red(r + half, half));
+            ct(e[r], e[r + half], load_tw(tw, (16u << s) + (blk << s) + (r >> (4 - s))), q, red(r, half), red(r + half, half));
       }
     }
 #pragma unroll
@@ -194,8 +203,9 @@ struct Ntt {
 
   // Inverse: e in pass-C order (eval slots) -> e in pass-A order (natural
   // coefficients), scaled by n^-1. Begins and ends with a barrier.
-  static __device__ __forceinline__ void inv(uint32_t (&e)[16], uint32_t* sm, const uint2* __restrict__ itw,
-                                             const uint4* __restrict__ itwc, uint32_t q, uint2 last, uint2 ninv) {
+  template <typename TW = const uint2*>
+  static __device__ __forceinline__ void inv(uint32_t (&e)[16], uint32_t* sm, TW itw, const uint4* __restrict__ itwc,
+                                             uint32_t q, uint2 last, uint2 ninv) {
     const uint32_t j = threadIdx.x;
     const uint32_t x0 = posC0(j);
     const uint4* tc = itwc + j;
@@ -257,7 +267,7 @@ struct Ntt {
         const int half = 8 >> s;
 #pragma unroll
         for (int r = 0; r < 16; ++r)
-          if (!(r & half)) gs(e[r], e[r + half], __ldg(&itw[(16u << s) + (blk << s) + (r >> (4 - s))]), q);
+          if (!(r & half)) gs(e[r], e[r + half], load_tw(itw, (16u << s) + (blk << s) + (r >> (4 - s))), q);
       }
     }
 #pragma unroll
@@ -271,7 +281,7 @@ struct Ntt {
       const int half = 8 >> s;
 #pragma unroll
       for (int r = 0; r < 16; ++r)
-        if (!(r & half)) gs(e[r], e[r + half], __ldg(&itw[(1 << s) + (r >> (4 - s))]), q);
+        if (!(r & half)) gs(e[r], e[r + half], load_tw(itw, (1 << s) + (r >> (4 - s))), q);
     }
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
