@@ -27,6 +27,7 @@
 #include <array>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -701,7 +702,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T) k_rot_keyswitch_f(Geo g, const u
 // (transposed [c][T] uint4, conflict-free), which keeps the kernel under 64
 // registers so two 512-thread CTAs share an SM (32 warps for latency hiding).
 template <int LOGN>
-__global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_rot_keyswitch_s(Geo g, const uint32_t* __restrict__ dot,
+__global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keyswitch_s(Geo g, const uint32_t* __restrict__ dot,
                                                                     const uint32_t* __restrict__ digits,
                                                                     const uint32_t* __restrict__ perm,
                                                                     const uint2* __restrict__ key0,
@@ -1269,6 +1270,7 @@ struct hei_gpu_ctx {
   uint32_t* d_err = nullptr;
   cudaStream_t stream = nullptr;
   uint64_t batch_pairs = 0;
+  bool ks14_regs = false;  // N = 16384: register-accumulator key switch (HEI_KS14_REGS=1)
   // scratch (grown on demand)
   uint32_t *d_dotA = nullptr, *d_dotB = nullptr, *d_dig = nullptr;
   uint64_t scratch_pairs = 0;
@@ -1425,7 +1427,11 @@ void launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const u
                                                                           *tabs_of(c, g, 0));
       break;
     case 14:
-      k_rot_keyswitch_f<14><<<blocks, Ntt<14>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, out, fold);
+      if (c->ks14_regs)
+        k_rot_keyswitch_f<14><<<blocks, Ntt<14>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, out, fold);
+      else
+        k_rot_keyswitch_s<14><<<blocks, Ntt<14>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                            *tabs_of(c, g, 0));
       break;
     default:
       k_rot_keyswitch<<<blocks, c->threads(), smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold);
@@ -1749,6 +1755,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (d->t[0] == d->t[1]) raise(HEI_PARAM_ERROR, "twin moduli must differ");
     auto c = std::make_unique<hei_gpu_ctx>();
     c->device = d->device;
+    if (const char* v = std::getenv("HEI_KS14_REGS")) c->ks14_regs = std::atoi(v) != 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
