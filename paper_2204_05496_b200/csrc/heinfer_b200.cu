@@ -2404,7 +2404,7 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     alloc(&d_bias, cols * 8);
     alloc(&d_wc, f * cols * P * sizeof(uint2));
     alloc(&d_acc, outw * 8);
-    alloc(&d_raw, 2 * Emax * 3 * n * 8);
+    alloc(&d_raw, 2 * 2 * Emax * 3 * n * 8);  // [slot][branch][draws]
     alloc(&d_state, 2 * 313 * 8);
     alloc(&d_noise, Emax * 2 * 3 * n);
     alloc(&d_m, Emax * 2 * n * 4);
@@ -2426,12 +2426,35 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     LAUNCHED();
     const size_t sm1 = smem_bytes(c, 1);
     const unsigned at = std::min<uint32_t>(256, n);
-    for (uint64_t k0 = 0; k0 < f; k0 += F) {
+    // The mt19937_64 replay is sequential per branch (one CTA each), so the
+    // next batch's draws are generated on a side stream while the current
+    // batch is encrypted and accumulated (double-buffered raw draws).
+    if (!c->copy_stream) CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    cudaStream_t ms = c->copy_stream;
+    cudaEvent_t gen[2], used[2];
+    for (int k = 0; k < 2; ++k) {
+      CU(cudaEventCreateWithFlags(&gen[k], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&used[k], cudaEventDisableTiming));
+      CU(cudaEventRecord(used[k], st));
+    }
+    CU(cudaStreamSynchronize(st));  // state, x, w uploads visible to `ms`
+    auto generate = [&](uint64_t k0, int slot) {
+      const uint64_t Fb = std::min<uint64_t>(F, f - k0), draws = Fb * B * 3 * n;
+      CU(cudaStreamWaitEvent(ms, used[slot], 0));
+      heb_baseline::k_mt_generate<<<2, 320, 0, ms>>>(d_state, d_raw + (size_t)slot * 2 * Emax * 3 * n, draws);
+      LAUNCHED();
+      CU(cudaEventRecord(gen[slot], ms));
+    };
+    generate(0, 0);
+    int slot = 0;
+    for (uint64_t k0 = 0; k0 < f; k0 += F, slot ^= 1) {
       const uint64_t Fb = std::min<uint64_t>(F, f - k0), E = Fb * B, draws = E * 3 * n;
-      heb_baseline::k_mt_generate<<<2, 320, 0, st>>>(d_state, d_raw, draws);
+      if (k0 + F < f) generate(k0 + F, slot ^ 1);
+      CU(cudaStreamWaitEvent(st, gen[slot], 0));
+      heb_baseline::k_bl_noise<<<dim3((unsigned)E, 2), 256, 0, st>>>(d_raw + (size_t)slot * 2 * Emax * 3 * n, draws, n,
+                                                                    (uint32_t)E, d_noise, c->d_err);
       LAUNCHED();
-      heb_baseline::k_bl_noise<<<dim3((unsigned)E, 2), 256, 0, st>>>(d_raw, draws, n, (uint32_t)E, d_noise, c->d_err);
-      LAUNCHED();
+      CU(cudaEventRecord(used[slot], st));
       HEI_DISPATCH(c->logn,
                    (k_bl_encode<LG><<<dim3((unsigned)E, 2), Ntt<LG>::T, sm1, st>>>(g, d_x, rows, f, k0, (uint32_t)B, d_m)),
                    (k_bl_encode_g<<<dim3((unsigned)E, 2), c->threads(), sm1, st>>>(g, d_x, rows, f, k0, (uint32_t)B, d_m)));
@@ -2445,6 +2468,11 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
                                                                   d_wc + k0 * cols * P, d_acc);
         LAUNCHED();
       }
+    }
+    CU(cudaStreamSynchronize(ms));
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(gen[k]);
+      cudaEventDestroy(used[k]);
     }
     (void)fast;
     k_bl_finish<<<(unsigned)(B * cols * P), c->threads(), sm1, st>>>(g, d_acc, d_bias, (uint32_t)cols, d_out);
