@@ -29,43 +29,47 @@ __device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
 }
 
 // state: [2][313] (312 words + mti) for the two branches; block b advances
-// branch b by `count` draws into out[b * count ...].
+// branch b by `count` draws into out[b * count ...]. The twist runs as two
+// 156-wide phases on ping-pong buffers (2 barriers per 312 outputs); each
+// thread tempers and stores the word it produced.
 __global__ void __launch_bounds__(320) k_mt_generate(uint64_t* __restrict__ state, uint64_t* __restrict__ out,
                                                      uint64_t count) {
-  __shared__ uint64_t mt[312];
+  __shared__ uint64_t buf[2][312];
   const uint32_t b = blockIdx.x, t = threadIdx.x;
   uint64_t* st = state + (uint64_t)b * 313;
   uint64_t* o = out + (uint64_t)b * count;
-  for (uint32_t i = t; i < 312; i += blockDim.x) mt[i] = st[i];
+  for (uint32_t i = t; i < 312; i += blockDim.x) buf[0][i] = st[i];
   uint32_t mti = (uint32_t)st[312];
   __syncthreads();
-  uint64_t pos = 0;
+  // words of the current block not consumed yet
+  const uint64_t rem = min((uint64_t)(312 - mti), count);
+  if (t < rem) o[t] = mt_temper(buf[0][mti + t]);
+  uint64_t pos = rem;
+  mti += (uint32_t)rem;
+  int cur = 0;
   while (pos < count) {
-    if (mti >= 312) {
-      uint64_t nv = 0;
-      if (t < 156) {
-        const uint64_t y = (mt[t] & kMtUM) | (mt[t + 1] & kMtLM);
-        nv = mt[t + 156] ^ (y >> 1) ^ ((y & 1) ? kMtA : 0);
-      }
-      __syncthreads();
-      if (t < 156) mt[t] = nv;
-      __syncthreads();
-      if (t >= 156 && t < 312) {
-        const uint64_t y = (mt[t] & kMtUM) | (mt[t == 311 ? 0 : t + 1] & kMtLM);
-        nv = mt[t - 156] ^ (y >> 1) ^ ((y & 1) ? kMtA : 0);
-      }
-      __syncthreads();
-      if (t >= 156 && t < 312) mt[t] = nv;
-      __syncthreads();
-      mti = 0;
+    const uint64_t* A = buf[cur];
+    uint64_t* B = buf[cur ^ 1];
+    if (t < 156) {
+      const uint64_t y = (A[t] & kMtUM) | (A[t + 1] & kMtLM);
+      const uint64_t v = A[t + 156] ^ (y >> 1) ^ ((y & 1) ? kMtA : 0);
+      B[t] = v;
+      if (pos + t < count) o[pos + t] = mt_temper(v);
     }
-    const uint64_t avail = min((uint64_t)(312 - mti), count - pos);
-    if (t < avail) o[pos + t] = mt_temper(mt[mti + t]);
-    pos += avail;
-    mti += (uint32_t)avail;
+    __syncthreads();
+    if (t >= 156 && t < 312) {
+      const uint64_t y = (A[t] & kMtUM) | ((t == 311 ? B[0] : A[t + 1]) & kMtLM);
+      const uint64_t v = B[t - 156] ^ (y >> 1) ^ ((y & 1) ? kMtA : 0);
+      B[t] = v;
+      if (pos + t < count) o[pos + t] = mt_temper(v);
+    }
+    __syncthreads();
+    cur ^= 1;
+    const uint64_t nw = min((uint64_t)312, count - pos);
+    pos += nw;
+    mti = (uint32_t)nw;
   }
-  __syncthreads();
-  for (uint32_t i = t; i < 312; i += blockDim.x) st[i] = mt[i];
+  for (uint32_t i = t; i < 312; i += blockDim.x) st[i] = buf[cur][i];
   if (t == 0) st[312] = mti;
 }
 
