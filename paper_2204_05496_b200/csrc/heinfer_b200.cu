@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <array>
+#include <type_traits>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -205,6 +206,11 @@ constexpr int kMaxAB = 12;
 struct TwAB {
   uint2 w[kMaxAB][256];
 };
+struct TwNone {  // small launches: twiddles stay in global memory (tiny params)
+  int unused;
+};
+template <bool PTW>
+using TwArg = typename std::conditional<PTW, TwAB, TwNone>::type;
 
 // ----------------------------------------------------------------- kernels
 __global__ void k_narrow(Geo g, const uint64_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t cts,
@@ -219,6 +225,11 @@ __global__ void k_narrow(Geo g, const uint64_t* __restrict__ in, uint32_t* __res
     if (v >= g.pr[gp].q) *err = 1;
     out[x] = (uint32_t)v;
   }
+}
+
+__global__ void k_iota(uint64_t* __restrict__ out, uint64_t start, uint64_t n) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n; x += (uint64_t)gridDim.x * blockDim.x)
+    out[x] = start + x;
 }
 
 __global__ void k_widen(const uint32_t* __restrict__ in, uint64_t* __restrict__ out, uint64_t total) {
@@ -592,11 +603,11 @@ __device__ __forceinline__ void store16(uint32_t* __restrict__ p, const uint32_t
     *reinterpret_cast<uint4*>(p + 4 * c) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
 }
 
-template <int LOGN>
+template <int LOGN, bool PTW>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digits_f(Geo g, const uint32_t* __restrict__ dot,
                                                               const uint32_t* __restrict__ perm,
                                                               uint32_t* __restrict__ digits,
-                                                              const __grid_constant__ TwAB itab) {
+                                                              const __grid_constant__ TwArg<PTW> itab) {
   using NT = Ntt<LOGN>;
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
@@ -608,7 +619,10 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digi
   load16_ro(perm + x0, pm);
 #pragma unroll
   for (int r = 0; r < 16; ++r) e[r] = c1[pm[r]];
-  NT::inv(e, sm, ParamTw{itab.w[gp]}, g.itwc + (size_t)gp * g.twc_stride, pr.q, pr.last, pr.ninv);
+  if constexpr (PTW)
+    NT::inv(e, sm, ParamTw{itab.w[gp]}, g.itwc + (size_t)gp * g.twc_stride, pr.q, pr.last, pr.ninv);
+  else
+    NT::inv(e, sm, g.inv + (size_t)gp * NT::N, g.itwc + (size_t)gp * g.twc_stride, pr.q, pr.last, pr.ninv);
   uint32_t* d = digits + ((uint64_t)pair * g.P + gp) * NT::N;
 #pragma unroll
   for (int r = 0; r < 16; ++r) d[NT::posA(j, r)] = e[r];
@@ -701,14 +715,14 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T) k_rot_keyswitch_f(Geo g, const u
 // Same as k_rot_keyswitch_f but the two accumulators live in shared memory
 // (transposed [c][T] uint4, conflict-free), which keeps the kernel under 64
 // registers so two 512-thread CTAs share an SM (32 warps for latency hiding).
-template <int LOGN>
+template <int LOGN, bool PTW>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keyswitch_s(Geo g, const uint32_t* __restrict__ dot,
                                                                     const uint32_t* __restrict__ digits,
                                                                     const uint32_t* __restrict__ perm,
                                                                     const uint2* __restrict__ key0,
                                                                     const uint2* __restrict__ key1,
                                                                     uint32_t* __restrict__ out, int fold,
-                                                                    const __grid_constant__ TwAB tab) {
+                                                                    const __grid_constant__ TwArg<PTW> tab) {
   using NT = Ntt<LOGN>;
   constexpr uint32_t N = NT::N, T = NT::T;
   extern __shared__ uint4 smem4[];
@@ -740,7 +754,6 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
     }
   }
   const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
-  const ParamTw tw{tab.w[gp]};
   const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
   uint32_t e[16];
   for (uint32_t l = 0; l < L; ++l) {
@@ -756,7 +769,10 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
 #pragma unroll
       for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
     }
-    NT::template fwd<true>(e, sm, tw, twc, q);
+    if constexpr (PTW)
+      NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
+    else
+      NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
 #pragma unroll
@@ -819,6 +835,88 @@ __device__ __forceinline__ uint32_t pow_barrett(uint32_t b, uint32_t e, uint32_t
     e >>= 1;
   }
   return r;
+}
+
+
+// Small batches (latency): the key switch split over digits. Block per
+// (pair, prime, digit l) writes NTT_i(digit_l mod q_i) (.) K[l][i] (or the
+// untransformed l == i term); k_ks_reduce sums the L partials and adds the
+// fold terms. Same arithmetic as k_rot_keyswitch_s, L x more parallelism.
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_ks_part(Geo g, const uint32_t* __restrict__ dot,
+                                                            const uint32_t* __restrict__ digits,
+                                                            const uint32_t* __restrict__ perm,
+                                                            const uint2* __restrict__ key0,
+                                                            const uint2* __restrict__ key1,
+                                                            uint32_t* __restrict__ part, uint32_t Lmax,
+                                                            const __grid_constant__ TwAB tab) {
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N, T = NT::T;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t l = blockIdx.x % Lmax, pg = blockIdx.x / Lmax;
+  const uint32_t pair = pg / g.P, gp = pg % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  if (l >= pr.L) return;
+  const uint32_t q = pr.q, i = pr.i, j = threadIdx.x, x0 = NT::posC0(j);
+  uint32_t e[16];
+  if (l == i) {
+    const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * N;
+    uint32_t pm[16];
+    load16_ro(perm + x0, pm);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = c1[pm[r]];
+  } else {
+    const uint32_t* src = digits + ((uint64_t)pair * g.P + pr.first + l) * N;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint32_t v = src[NT::posA(j, r)];
+      e[r] = pr.fast_reduce ? min(v, v - q) : v % q;
+    }
+    NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, g.twc + (size_t)gp * g.twc_stride, q);
+  }
+  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * pr.L * 2 * N;
+  const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
+  const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
+  uint32_t* o = part + (uint64_t)blockIdx.x * 2 * N + x0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 a = __ldg(k0 + c * T), b = __ldg(k1 + c * T);
+    *reinterpret_cast<uint2*>(o + 2 * c) =
+        make_uint2(mul_shoup(e[2 * c], a.x, a.y, q), mul_shoup(e[2 * c + 1], a.z, a.w, q));
+    *reinterpret_cast<uint2*>(o + N + 2 * c) =
+        make_uint2(mul_shoup(e[2 * c], b.x, b.y, q), mul_shoup(e[2 * c + 1], b.z, b.w, q));
+  }
+}
+
+// grid (pair, prime, n / 1024 tiles), 256 threads x 4 slots (uint4 accesses)
+__global__ void __launch_bounds__(256) k_ks_reduce(Geo g, const uint32_t* __restrict__ dot,
+                                                   const uint32_t* __restrict__ part, const uint32_t* __restrict__ perm,
+                                                   uint32_t Lmax, uint32_t* __restrict__ out, int fold) {
+  const uint32_t n = g.n, tiles = n / 1024;
+  const uint32_t pg = blockIdx.x / tiles, tile = blockIdx.x % tiles;
+  const uint32_t pair = pg / g.P, gp = pg % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t q = pr.q, L = pr.L;
+  const uint32_t x = tile * 1024 + threadIdx.x * 4;
+  const uint32_t* c0 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly0 * n;
+  const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n;
+  const uint32_t* ps = part + (uint64_t)pg * Lmax * 2 * n + x;
+  const uint4 pm = __ldg(reinterpret_cast<const uint4*>(perm + x));
+  uint32_t a0[4] = {c0[pm.x], c0[pm.y], c0[pm.z], c0[pm.w]}, a1[4] = {0, 0, 0, 0};
+  for (uint32_t l = 0; l < L; ++l) {
+    const uint4 u = *reinterpret_cast<const uint4*>(ps + (uint64_t)l * 2 * n);
+    const uint4 v = *reinterpret_cast<const uint4*>(ps + (uint64_t)l * 2 * n + n);
+    a0[0] = add_mod(a0[0], u.x, q), a0[1] = add_mod(a0[1], u.y, q), a0[2] = add_mod(a0[2], u.z, q), a0[3] = add_mod(a0[3], u.w, q);
+    a1[0] = add_mod(a1[0], v.x, q), a1[1] = add_mod(a1[1], v.y, q), a1[2] = add_mod(a1[2], v.z, q), a1[3] = add_mod(a1[3], v.w, q);
+  }
+  if (fold) {
+    const uint4 u = *reinterpret_cast<const uint4*>(c0 + x), v = *reinterpret_cast<const uint4*>(c1 + x);
+    a0[0] = add_mod(a0[0], u.x, q), a0[1] = add_mod(a0[1], u.y, q), a0[2] = add_mod(a0[2], u.z, q), a0[3] = add_mod(a0[3], u.w, q);
+    a1[0] = add_mod(a1[0], v.x, q), a1[1] = add_mod(a1[1], v.y, q), a1[2] = add_mod(a1[2], v.z, q), a1[3] = add_mod(a1[3], v.w, q);
+  }
+  *reinterpret_cast<uint4*>(out + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly0 * n + x) = make_uint4(a0[0], a0[1], a0[2], a0[3]);
+  *reinterpret_cast<uint4*>(out + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n + x) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
 }
 
 template <int LOGN>
@@ -1292,6 +1390,22 @@ struct hei_gpu_ctx {
   uint64_t* pool_out64 = nullptr;
   size_t pool_out64_bytes = 0;
   cudaStream_t copy_stream = nullptr;
+  int64_t* pinned_bias = nullptr;  // pinned staging for the bias upload
+  size_t pinned_bias_bytes = 0;
+  uint32_t* pool_part = nullptr;  // split key-switch partials (small batches)
+  size_t pool_part_bytes = 0;
+  bool split = false;   // HEI_SPLIT=1: split the key switch over digits for small batches
+  bool graphs = true;   // HEI_NO_GRAPHS=1: launch the small-batch fold eagerly
+  struct FoldGraph {
+    uint64_t pairs;
+    uint32_t *cur, *other, *part;
+    uint64_t gen;
+    bool split;
+    cudaGraphExec_t exec;
+    uint64_t launches;
+  };
+  std::vector<FoldGraph> fold_graphs;
+  uint64_t graph_gen = 0;  // bumped when keys or scratch buffers change
   // optional per-kernel timing (bench.py roofline): events around the fold
   bool timing = false;
   std::vector<std::array<cudaEvent_t, 3>> fold_ev;  // digits: [0,1], key switch: [1,2]
@@ -1317,6 +1431,7 @@ struct hei_gpu_stream {
   bool finished = false;
   unsigned long long* d_acc = nullptr;  // [C][twin ct] u64
   bool owns_acc = true, owns_rows = true;
+  int64_t* d_bias = nullptr;  // staged bias (pool memory, not owned)
   // pending rows staged on the device
   std::vector<uint64_t> pend_idx;
   uint32_t* d_stage = nullptr;  // [cap][k][twin ct] u32
@@ -1374,6 +1489,7 @@ void ensure_scratch(hei_gpu_ctx* c, uint64_t pairs) {
   CU(cudaMalloc(&c->d_dotB, pairs * c->ct_words() * 4));
   CU(cudaMalloc(&c->d_dig, pairs * c->pt_words() * 4));
   c->scratch_pairs = pairs;
+  ++c->graph_gen;
 }
 
 size_t smem_bytes(hei_gpu_ctx* c, int words) { return (size_t)words * c->n * 4; }
@@ -1408,7 +1524,12 @@ const TwAB* tabs_of(hei_gpu_ctx* c, const Geo& g, int inverse) {
 void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* perm,
                        uint32_t* dig, cudaStream_t st) {
   const size_t sm = smem_bytes(c, 1);
-  HEI_DISPATCH(c->logn, (k_rot_digits_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1))),
+  // big launches take the pass-A/B twiddles as parameters (constant bank);
+  // small ones keep the 25 KB parameter block off the launch path
+  const bool ptw = blocks >= 2u * 148u;
+  HEI_DISPATCH(c->logn,
+               (ptw ? k_rot_digits_f<LG, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1))
+                    : k_rot_digits_f<LG, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig, TwNone{})),
                (k_rot_digits<<<blocks, c->threads(), sm, st>>>(g, cur, perm, dig)));
   LAUNCHED();
 }
@@ -1419,19 +1540,31 @@ void launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const u
   // threads) keeps the accumulators in registers.
   switch (c->logn) {
     case 12:
-      k_rot_keyswitch_s<12><<<blocks, Ntt<12>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                          *tabs_of(c, g, 0));
+      if (blocks >= 2u * 148u)
+        k_rot_keyswitch_s<12, true><<<blocks, Ntt<12>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                                *tabs_of(c, g, 0));
+      else
+        k_rot_keyswitch_s<12, false><<<blocks, Ntt<12>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                                 TwNone{});
       break;
     case 13:
-      k_rot_keyswitch_s<13><<<blocks, Ntt<13>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                          *tabs_of(c, g, 0));
+      if (blocks >= 2u * 148u)
+        k_rot_keyswitch_s<13, true><<<blocks, Ntt<13>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                                *tabs_of(c, g, 0));
+      else
+        k_rot_keyswitch_s<13, false><<<blocks, Ntt<13>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                                 TwNone{});
       break;
     case 14:
       if (c->ks14_regs)
         k_rot_keyswitch_f<14><<<blocks, Ntt<14>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, out, fold);
       else
-        k_rot_keyswitch_s<14><<<blocks, Ntt<14>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                            *tabs_of(c, g, 0));
+      if (blocks >= 2u * 148u)
+        k_rot_keyswitch_s<14, true><<<blocks, Ntt<14>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                                *tabs_of(c, g, 0));
+      else
+        k_rot_keyswitch_s<14, false><<<blocks, Ntt<14>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                                 TwNone{});
       break;
     default:
       k_rot_keyswitch<<<blocks, c->threads(), smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold);
@@ -1463,11 +1596,14 @@ void launch_poly_ntt(hei_gpu_ctx* c, unsigned blocks, uint32_t gp, uint32_t* pol
 }
 template <int LG>
 void set_fast_attrs(size_t sm) {
-  set_smem_attr((const void*)k_rot_digits_f<LG>, sm);
+  set_smem_attr((const void*)k_rot_digits_f<LG, true>, sm);
+  set_smem_attr((const void*)k_rot_digits_f<LG, false>, sm);
   set_smem_attr((const void*)k_rot_keyswitch_f<LG>, sm);
-  set_smem_attr((const void*)k_rot_keyswitch_s<LG>, 3 * sm);
+  set_smem_attr((const void*)k_rot_keyswitch_s<LG, true>, 3 * sm);
+  set_smem_attr((const void*)k_rot_keyswitch_s<LG, false>, 3 * sm);
   set_smem_attr((const void*)k_mask_acc_f<LG>, sm);
   set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
+  set_smem_attr((const void*)k_ks_part<LG>, sm);
   set_smem_attr((const void*)k_ct_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_poly_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_bl_encode<LG>, sm);
@@ -1487,9 +1623,11 @@ uint64_t auto_batch_pairs(hei_gpu_ctx* c) {
 
 // The rotate-and-sum fold over `pairs` twin ciphertexts in `cur` (eval form);
 // returns the buffer holding the result.
-uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st) {
+uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st, bool split,
+                    uint32_t* part) {
   const Geo& g = c->geo;
   const unsigned blocks = (unsigned)(pairs * c->P());
+  const uint32_t Lmax = std::max(c->L[0], c->L[1]);
   for (uint64_t elt : c->fold_elts) {
     const uint32_t* perm = c->d_perms + (size_t)c->perm_index.at(elt) * c->n;
     const uint2* k0 = c->d_keys[0] + (size_t)c->key_index[0].at(elt) * c->L[0] * 2 * c->L[0] * c->n;
@@ -1503,7 +1641,18 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
     }
     launch_rot_digits(c, g, blocks, cur, perm, c->d_dig, st);
     if (c->timing) CU(cudaEventRecord(e1, st));
-    launch_rot_keyswitch(c, g, blocks, cur, c->d_dig, perm, k0, k1, other, 1, st);
+    if (split) {
+      const unsigned pb = (unsigned)(blocks * Lmax);
+      HEI_DISPATCH(c->logn,
+                   (k_ks_part<LG><<<pb, Ntt<LG>::T, smem_bytes(c, 1), st>>>(g, cur, c->d_dig, perm, k0, k1, part, Lmax,
+                                                                          *tabs_of(c, g, 0))),
+                   (void)0);
+      LAUNCHED();
+      k_ks_reduce<<<blocks * (c->n / 1024), 256, 0, st>>>(g, cur, part, perm, Lmax, other, 1);
+      LAUNCHED();
+    } else {
+      launch_rot_keyswitch(c, g, blocks, cur, c->d_dig, perm, k0, k1, other, 1, st);
+    }
     if (c->timing) {
       CU(cudaEventRecord(e2, st));
       c->fold_ev.push_back({e0, e1, e2});
@@ -1511,6 +1660,40 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
     std::swap(cur, other);
   }
   return cur;
+}
+
+// Small batches (the single-individual latency path) replay the 26-28 fold
+// launches as one CUDA graph captured per (pairs, buffers), removing the
+// per-launch gaps that dominate when every launch covers < 2 blocks per SM.
+uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st) {
+  const unsigned blocks = (unsigned)(pairs * c->P());
+  const bool small = blocks < 2u * 148u;
+  // optionally split the key switch over digits for parallelism (HEI_SPLIT=1)
+  const bool split = c->logn >= 12 && c->logn <= 14 && small && c->split;
+  const uint32_t Lmax = std::max(c->L[0], c->L[1]);
+  uint32_t* part = split ? pool_get(c->pool_part, c->pool_part_bytes, (size_t)blocks * Lmax * 2 * c->n * 4) : nullptr;
+  uint32_t* result = (c->fold_elts.size() % 2) ? other : cur;
+  if (!small || c->timing || !c->graphs) return fold_impl(c, pairs, cur, other, st, split, part);
+  for (auto& fg : c->fold_graphs)
+    if (fg.pairs == pairs && fg.cur == cur && fg.other == other && fg.part == part && fg.gen == c->graph_gen &&
+        fg.split == split) {
+      CU(cudaGraphLaunch(fg.exec, st));
+      g_launches += fg.launches;
+      return result;
+    }
+  const uint64_t before = g_launches;
+  cudaGraph_t graph = nullptr;
+  CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  fold_impl(c, pairs, cur, other, st, split, part);
+  CU(cudaStreamEndCapture(st, &graph));
+  cudaGraphExec_t exec = nullptr;
+  CU(cudaGraphInstantiate(&exec, graph, 0));
+  cudaGraphDestroy(graph);
+  c->fold_graphs.push_back({pairs, cur, other, part, c->graph_gen, split, exec, g_launches - before});
+  g_launches = before;
+  CU(cudaGraphLaunch(exec, st));
+  g_launches += c->fold_graphs.back().launches;
+  return result;
 }
 
 void require_keys(hei_gpu_ctx* c) {
@@ -1552,8 +1735,11 @@ void stream_flush(hei_gpu_stream* s) {
 
 void finish_to(hei_gpu_stream* s, uint32_t* d_out, cudaStream_t st) {
   hei_gpu_ctx* c = s->ctx;
-  int64_t* d_bias = pool_get(c->pool_bias, c->pool_bias_bytes, s->bias.size() * 8);
-  CU(cudaMemcpyAsync(d_bias, s->bias.data(), s->bias.size() * 8, cudaMemcpyHostToDevice, st));
+  int64_t* d_bias = s->d_bias;
+  if (!d_bias) {  // streams created before the bias was staged (host API)
+    d_bias = pool_get(c->pool_bias, c->pool_bias_bytes, s->bias.size() * 8);
+    CU(cudaMemcpyAsync(d_bias, s->bias.data(), s->bias.size() * 8, cudaMemcpyHostToDevice, st));
+  }
   k_finish<<<(unsigned)(s->C * c->P()), c->threads(), smem_bytes(c, 1), st>>>(
       c->geo, s->d_acc, d_bias, (uint32_t)s->w->cols, s->rows * s->w->cols, d_out);
   LAUNCHED();
@@ -1578,7 +1764,7 @@ void capacity_gate(hei_gpu_ctx* c, uint64_t f, const char* who) {
 }
 
 hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64_t* bias, uint64_t rows,
-                           bool host_staging = true) {
+                           bool host_staging = true, cudaStream_t zero_on = nullptr) {
   if (rows == 0) raise(HEI_PARAM_ERROR, "matmul: empty input");
   if (!w || w->cols == 0 || w->f == 0) raise(HEI_PARAM_ERROR, "matmul: empty weights");
   if (w->ctx != c) raise(HEI_PARAM_ERROR, "matmul: weights encoded for a different context");
@@ -1606,7 +1792,20 @@ hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64
     s->owns_acc = false;
     s->owns_rows = false;
   }
-  CU(cudaMemsetAsync(s->d_acc, 0, s->C * c->ct_words() * 8, c->stream));
+  CU(cudaMemsetAsync(s->d_acc, 0, s->C * c->ct_words() * 8, zero_on ? zero_on : c->stream));
+  if (!host_staging) {
+    // stage the bias now (pinned, async): every earlier call has synchronised
+    const size_t bb = s->bias.size() * 8;
+    if (bb > c->pinned_bias_bytes) {
+      if (c->pinned_bias) cudaFreeHost(c->pinned_bias);
+      c->pinned_bias = nullptr;
+      CU(cudaMallocHost(&c->pinned_bias, bb));
+      c->pinned_bias_bytes = bb;
+    }
+    std::memcpy(c->pinned_bias, s->bias.data(), bb);
+    s->d_bias = pool_get(c->pool_bias, c->pool_bias_bytes, bb);
+    CU(cudaMemcpyAsync(s->d_bias, c->pinned_bias, bb, cudaMemcpyHostToDevice, zero_on ? zero_on : c->stream));
+  }
   return s.release();
 }
 
@@ -1756,6 +1955,8 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     auto c = std::make_unique<hei_gpu_ctx>();
     c->device = d->device;
     if (const char* v = std::getenv("HEI_KS14_REGS")) c->ks14_regs = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_SPLIT")) c->split = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_NO_GRAPHS")) c->graphs = std::atoi(v) == 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
@@ -1955,6 +2156,8 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->pool_rows);
   cudaFree(c->pool_bias);
   cudaFree(c->pool_stage64);
+  cudaFree(c->pool_part);
+  if (c->pinned_bias) cudaFreeHost(c->pinned_bias);
   cudaFree(c->pool_in32);
   cudaFree(c->pool_out);
   cudaFree(c->pool_out64);
@@ -1964,6 +2167,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->d_dig);
   for (auto& a : c->fold_ev)
     for (auto e : a) cudaEventDestroy(e);
+  for (auto& fg : c->fold_graphs) cudaGraphExecDestroy(fg.exec);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -2055,6 +2259,7 @@ int hei_gpu_upload_galois_keys(hei_gpu_ctx* c, uint32_t b, uint32_t count, const
     check_err_flag(c, HEI_CODEC_ERROR, "galois keys: coefficient not reduced");
     c->key_index[b] = idx;
     c->has_keys[b] = true;
+    ++c->graph_gen;
   });
 }
 
@@ -2207,21 +2412,22 @@ int hei_gpu_matmul(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint64_t* inp
 
 int hei_gpu_matmul_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint32_t* d_inputs, int form,
                           uint64_t rows, const int64_t* bias, uint32_t* d_out, hei_op_counters* cnt, void* stream) {
+  // Everything is enqueued on `st` with no host round trip until the final
+  // synchronisation (row ids come from a device iota, the bias from pinned
+  // staging), so small batches are not host-bound.
   return guarded([&] {
     set_device(c);
     std::lock_guard<std::mutex> lk(c->mu);
     if (form != HEI_FORM_EVAL) raise(HEI_PARAM_ERROR, "matmul_device: inputs must be in eval form");
     cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
-    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, bias, rows, false), stream_free);
-    CU(cudaStreamSynchronize(c->stream));  // zeroed accumulators visible to `st`
+    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, bias, rows, false, st), stream_free);
     const size_t words = w->kc * c->ct_words();
-    std::vector<uint64_t> idx(s->cap_rows);
+    uint64_t* d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, rows * 8);
+    k_iota<<<grid_for(rows, 256), 256, 0, st>>>(d_rows, 0, rows);
+    LAUNCHED();
     for (uint64_t r0 = 0; r0 < rows; r0 += s->cap_rows) {
       const uint64_t nr = std::min<uint64_t>(s->cap_rows, rows - r0);
-      for (uint64_t k = 0; k < nr; ++k) idx[k] = r0 + k;
-      CU(cudaMemcpyAsync(s->d_rows, idx.data(), nr * 8, cudaMemcpyHostToDevice, st));
-      run_rows(s.get(), d_inputs + r0 * words, s->d_rows, nr, st);
-      CU(cudaStreamSynchronize(st));  // idx / d_rows reuse
+      run_rows(s.get(), d_inputs + r0 * words, d_rows + r0, nr, st);
     }
     s->pushed = rows;
     finish_to(s.get(), d_out, st);
