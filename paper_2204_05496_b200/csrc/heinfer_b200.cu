@@ -1396,9 +1396,11 @@ struct hei_gpu_ctx {
   size_t pool_part_bytes = 0;
   bool split = false;   // HEI_SPLIT=1: split the key switch over digits for small batches
   bool graphs = true;   // HEI_NO_GRAPHS=1: launch the small-batch fold eagerly
+  bool two_streams = true;  // HEI_TWO_STREAMS=0: fold the batch on one stream only
+  cudaStream_t side_stream = nullptr;
   struct FoldGraph {
     uint64_t pairs;
-    uint32_t *cur, *other, *part;
+    uint32_t *cur, *other, *part, *dig;
     uint64_t gen;
     bool split;
     cudaGraphExec_t exec;
@@ -1624,7 +1626,7 @@ uint64_t auto_batch_pairs(hei_gpu_ctx* c) {
 // The rotate-and-sum fold over `pairs` twin ciphertexts in `cur` (eval form);
 // returns the buffer holding the result.
 uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st, bool split,
-                    uint32_t* part) {
+                    uint32_t* part, uint32_t* dig) {
   const Geo& g = c->geo;
   const unsigned blocks = (unsigned)(pairs * c->P());
   const uint32_t Lmax = std::max(c->L[0], c->L[1]);
@@ -1639,19 +1641,19 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
       CU(cudaEventCreate(&e2));
       CU(cudaEventRecord(e0, st));
     }
-    launch_rot_digits(c, g, blocks, cur, perm, c->d_dig, st);
+    launch_rot_digits(c, g, blocks, cur, perm, dig, st);
     if (c->timing) CU(cudaEventRecord(e1, st));
     if (split) {
       const unsigned pb = (unsigned)(blocks * Lmax);
       HEI_DISPATCH(c->logn,
-                   (k_ks_part<LG><<<pb, Ntt<LG>::T, smem_bytes(c, 1), st>>>(g, cur, c->d_dig, perm, k0, k1, part, Lmax,
+                   (k_ks_part<LG><<<pb, Ntt<LG>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, part, Lmax,
                                                                           *tabs_of(c, g, 0))),
                    (void)0);
       LAUNCHED();
       k_ks_reduce<<<blocks * (c->n / 1024), 256, 0, st>>>(g, cur, part, perm, Lmax, other, 1);
       LAUNCHED();
     } else {
-      launch_rot_keyswitch(c, g, blocks, cur, c->d_dig, perm, k0, k1, other, 1, st);
+      launch_rot_keyswitch(c, g, blocks, cur, dig, perm, k0, k1, other, 1, st);
     }
     if (c->timing) {
       CU(cudaEventRecord(e2, st));
@@ -1665,7 +1667,9 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
 // Small batches (the single-individual latency path) replay the 26-28 fold
 // launches as one CUDA graph captured per (pairs, buffers), removing the
 // per-launch gaps that dominate when every launch covers < 2 blocks per SM.
-uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st) {
+uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st,
+               uint32_t* dig = nullptr) {
+  if (!dig) dig = c->d_dig;
   const unsigned blocks = (unsigned)(pairs * c->P());
   const bool small = blocks < 2u * 148u;
   // optionally split the key switch over digits for parallelism (HEI_SPLIT=1)
@@ -1673,9 +1677,10 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
   const uint32_t Lmax = std::max(c->L[0], c->L[1]);
   uint32_t* part = split ? pool_get(c->pool_part, c->pool_part_bytes, (size_t)blocks * Lmax * 2 * c->n * 4) : nullptr;
   uint32_t* result = (c->fold_elts.size() % 2) ? other : cur;
-  if (!small || c->timing || !c->graphs) return fold_impl(c, pairs, cur, other, st, split, part);
+  if (!small || c->timing || !c->graphs) return fold_impl(c, pairs, cur, other, st, split, part, dig);
   for (auto& fg : c->fold_graphs)
-    if (fg.pairs == pairs && fg.cur == cur && fg.other == other && fg.part == part && fg.gen == c->graph_gen &&
+    if (fg.pairs == pairs && fg.cur == cur && fg.other == other && fg.part == part && fg.dig == dig &&
+        fg.gen == c->graph_gen &&
         fg.split == split) {
       CU(cudaGraphLaunch(fg.exec, st));
       g_launches += fg.launches;
@@ -1684,12 +1689,12 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
   const uint64_t before = g_launches;
   cudaGraph_t graph = nullptr;
   CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  fold_impl(c, pairs, cur, other, st, split, part);
+  fold_impl(c, pairs, cur, other, st, split, part, dig);
   CU(cudaStreamEndCapture(st, &graph));
   cudaGraphExec_t exec = nullptr;
   CU(cudaGraphInstantiate(&exec, graph, 0));
   cudaGraphDestroy(graph);
-  c->fold_graphs.push_back({pairs, cur, other, part, c->graph_gen, split, exec, g_launches - before});
+  c->fold_graphs.push_back({pairs, cur, other, part, dig, c->graph_gen, split, exec, g_launches - before});
   g_launches = before;
   CU(cudaGraphLaunch(exec, st));
   g_launches += c->fold_graphs.back().launches;
@@ -1715,6 +1720,34 @@ void run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
   ensure_scratch(c, pairs);
   const unsigned T = c->threads();
   const unsigned blocksP = (unsigned)(pairs * c->P());
+  if (c->two_streams && nrows >= 8) {
+    // two halves of the batch on two streams: one half's digit INTTs and
+    // key switches interleave with the other's, filling each launch's tail
+    if (!c->side_stream) CU(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+    cudaEvent_t fork, join;
+    CU(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    CU(cudaEventRecord(fork, st));
+    CU(cudaStreamWaitEvent(c->side_stream, fork, 0));
+    const uint64_t r1 = nrows / 2;
+    for (int h = 0; h < 2; ++h) {
+      cudaStream_t hs = h ? c->side_stream : st;
+      const uint64_t rr0 = h ? r1 : 0, nr = h ? nrows - r1 : r1, pp = nr * cols, off = rr0 * cols;
+      uint32_t* A = c->d_dotA + off * c->ct_words();
+      uint32_t* B = c->d_dotB + off * c->ct_words();
+      uint32_t* D = c->d_dig + off * c->pt_words();
+      k_chunk_dot<<<(unsigned)(pp * 2 * c->P()), std::min<unsigned>(T, c->n / 4), 0, hs>>>(
+          g, d_in + rr0 * w->kc * c->ct_words(), w->d_w, cols, (uint32_t)w->kc, A);
+      LAUNCHED();
+      uint32_t* res = fold(c, pp, A, B, hs, D);
+      launch_mask_acc(c, g, (unsigned)(pp * c->P()), res, d_rows + rr0, cols, s->d_acc, hs);
+    }
+    CU(cudaEventRecord(join, c->side_stream));
+    CU(cudaStreamWaitEvent(st, join, 0));
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    return;
+  }
   k_chunk_dot<<<(unsigned)(pairs * 2 * c->P()), std::min<unsigned>(T, c->n / 4), 0, st>>>(g, d_in, w->d_w, cols,
                                                                                          (uint32_t)w->kc, c->d_dotA);
   LAUNCHED();
@@ -1957,6 +1990,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_KS14_REGS")) c->ks14_regs = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_SPLIT")) c->split = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_NO_GRAPHS")) c->graphs = std::atoi(v) == 0;
+    if (const char* v = std::getenv("HEI_TWO_STREAMS")) c->two_streams = std::atoi(v) != 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
@@ -2168,6 +2202,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   for (auto& a : c->fold_ev)
     for (auto e : a) cudaEventDestroy(e);
   for (auto& fg : c->fold_graphs) cudaGraphExecDestroy(fg.exec);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
