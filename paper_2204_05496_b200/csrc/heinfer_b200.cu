@@ -1720,7 +1720,7 @@ void run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
   ensure_scratch(c, pairs);
   const unsigned T = c->threads();
   const unsigned blocksP = (unsigned)(pairs * c->P());
-  if (c->two_streams && nrows >= 8) {
+  if (c->two_streams && !c->timing && nrows >= 8) {
     // two halves of the batch on two streams: one half's digit INTTs and
     // key switches interleave with the other's, filling each launch's tail
     if (!c->side_stream) CU(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));

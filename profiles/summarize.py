@@ -54,9 +54,11 @@ def full(rep, out, pairs=None):
         js.append(d)
     open(out, "w").write("\n".join(lines) + "\n")
     ks = [d for d in js if "keyswitch" in d["kernel"]]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    unit = units[h.index("dram__bytes_read.sum")]
     if ks and pairs:
-        rd = float(ks[0]["dram__bytes_read.sum"]) * 1e9
-        wr = float(ks[0]["dram__bytes_write.sum"]) * 1e9
+        rd = float(ks[0]["dram__bytes_read.sum"]) * scale[unit]
+        wr = float(ks[0]["dram__bytes_write.sum"]) * scale[units[h.index("dram__bytes_write.sum")]]
         json.dump({"source": rep, "kernel": ks[0]["kernel"], "pairs_per_launch": pairs,
                    "dram_bytes_per_launch": rd + wr, "dram_bytes_per_pair": (rd + wr) / pairs},
                   open(out.rsplit("/", 1)[0] + "/keyswitch_traffic.json", "w"), indent=1)
