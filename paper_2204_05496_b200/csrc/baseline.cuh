@@ -109,4 +109,127 @@ __global__ void k_bl_noise(const uint64_t* __restrict__ raw, uint64_t count, uin
   (void)encs;
 }
 
+// ---- jump-ahead (parallel replay of one sequential stream) ----------------
+// A window state S_o = (W_o .. W_{o+311}) of the word recurrence
+// W_{k+312} = W_{k+156} ^ T(W_k, W_{k+1}) is exactly the generator array when
+// mti == 312. Advancing by J words is S -> p(A) S with p = x^J mod phi (phi
+// the characteristic polynomial of mt19937_64), and p(A) S is a sliding XOR
+// of the word sequence: (p(A) S)[k] = XOR_{i: p_i = 1} W_{o+k+i}.
+// One block per branch; writes the K chunk start windows (mti = 312) spaced
+// J words apart. smem: the 20249-word window sequence.
+constexpr int kMtDeg = 19937;
+constexpr int kMtSeq = kMtDeg + 312;  // words needed by one jump
+
+// One jump step is three launches so the XOR convolution runs on the whole
+// GPU: k_mt_wseq extends each branch's current window to the 20249-word
+// sequence (sequential twists, one block per branch), k_mt_xor computes
+// partial windows over slices of the polynomial (many blocks), and
+// k_mt_xor_reduce folds the partials into the next start window.
+__global__ void __launch_bounds__(320) k_mt_wseq(const uint64_t* __restrict__ cur, uint64_t* __restrict__ wseq,
+                                                 uint32_t wlen) {
+  __shared__ uint64_t buf[2][312];
+  const uint32_t b = blockIdx.x, t = threadIdx.x;
+  const uint64_t* st = cur + (uint64_t)b * 313;
+  uint64_t* W = wseq + (uint64_t)b * wlen;
+  for (uint32_t i = t; i < 312; i += blockDim.x) {
+    buf[0][i] = st[i];
+    W[i] = st[i];
+  }
+  __syncthreads();
+  int c = 0;
+  for (uint32_t blk = 1; 312 * blk < wlen; ++blk) {
+    const uint64_t* A = buf[c];
+    uint64_t* B = buf[c ^ 1];
+    if (t < 156) {
+      const uint64_t y = (A[t] & kMtUM) | (A[t + 1] & kMtLM);
+      B[t] = A[t + 156] ^ (y >> 1) ^ ((y & 1) ? kMtA : 0);
+      W[312 * blk + t] = B[t];
+    }
+    __syncthreads();
+    if (t >= 156 && t < 312) {
+      const uint64_t y = (A[t] & kMtUM) | ((t == 311 ? B[0] : A[t + 1]) & kMtLM);
+      B[t] = B[t - 156] ^ (y >> 1) ^ ((y & 1) ? kMtA : 0);
+      W[312 * blk + t] = B[t];
+    }
+    __syncthreads();
+    c ^= 1;
+  }
+}
+
+// partial[b][s][k] = XOR over set bits i of poly words [s*ws, (s+1)*ws) of W[k+i]
+__global__ void __launch_bounds__(320) k_mt_xor(const uint64_t* __restrict__ wseq, uint32_t wlen,
+                                                const uint64_t* __restrict__ poly, uint32_t ws,
+                                                uint64_t* __restrict__ partial) {
+  const uint32_t s = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
+  const uint32_t nw = (kMtDeg + 63) / 64;
+  const uint64_t* W = wseq + (uint64_t)b * wlen;
+  uint64_t acc = 0;
+  if (t < 312)
+    for (uint32_t wi = s * ws; wi < min(nw, (s + 1) * ws); ++wi) {
+      uint64_t bits = __ldg(&poly[wi]);
+      while (bits) {
+        const uint32_t i = wi * 64 + __ffsll((long long)bits) - 1;
+        acc ^= __ldg(&W[t + i]);
+        bits &= bits - 1;
+      }
+    }
+  if (t < 312) partial[((uint64_t)b * gridDim.x + s) * 312 + t] = acc;
+}
+
+__global__ void k_mt_xor_reduce(const uint64_t* __restrict__ partial, uint32_t S, uint64_t* __restrict__ cur,
+                                uint64_t* __restrict__ starts, uint32_t K, uint32_t m) {
+  const uint32_t b = blockIdx.x, t = threadIdx.x;
+  if (t >= 312) return;
+  uint64_t acc = 0;
+  for (uint32_t s = 0; s < S; ++s) acc ^= partial[((uint64_t)b * S + s) * 312 + t];
+  cur[(uint64_t)b * 313 + t] = acc;
+  starts[((uint64_t)b * K + m) * 313 + t] = acc;
+  if (t == 0) starts[((uint64_t)b * K + m) * 313 + 312] = 312;
+}
+
+// Chunk m of branch b generates draws [m*C, min((m+1)*C, total)) from its
+// start window; the last chunk's final state is written back to `state`.
+__global__ void __launch_bounds__(320) k_mt_chunks(uint64_t* __restrict__ starts, uint32_t K, uint64_t C,
+                                                   uint64_t total, uint64_t* __restrict__ out,
+                                                   uint64_t* __restrict__ state) {
+  __shared__ uint64_t buf[2][312];
+  const uint32_t m = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
+  const uint64_t* st = starts + ((uint64_t)b * K + m) * 313;
+  const uint64_t begin = (uint64_t)m * C;
+  const uint64_t count = min(C, total - begin);
+  uint64_t* o = out + (uint64_t)b * total + begin;
+  for (uint32_t i = t; i < 312; i += blockDim.x) buf[0][i] = st[i];
+  __syncthreads();
+  uint64_t pos = 0;
+  uint32_t mti = 312;
+  int cur = 0;
+  while (pos < count) {
+    const uint64_t* A = buf[cur];
+    uint64_t* B = buf[cur ^ 1];
+    if (t < 156) {
+      const uint64_t y = (A[t] & kMtUM) | (A[t + 1] & kMtLM);
+      const uint64_t v = A[t + 156] ^ (y >> 1) ^ ((y & 1) ? kMtA : 0);
+      B[t] = v;
+      if (pos + t < count) o[pos + t] = mt_temper(v);
+    }
+    __syncthreads();
+    if (t >= 156 && t < 312) {
+      const uint64_t y = (A[t] & kMtUM) | ((t == 311 ? B[0] : A[t + 1]) & kMtLM);
+      const uint64_t v = B[t - 156] ^ (y >> 1) ^ ((y & 1) ? kMtA : 0);
+      B[t] = v;
+      if (pos + t < count) o[pos + t] = mt_temper(v);
+    }
+    __syncthreads();
+    cur ^= 1;
+    const uint64_t nw = min((uint64_t)312, count - pos);
+    pos += nw;
+    mti = (uint32_t)nw;
+  }
+  if (m + 1 == K) {
+    uint64_t* fs = state + (uint64_t)b * 313;
+    for (uint32_t i = t; i < 312; i += blockDim.x) fs[i] = buf[cur][i];
+    if (t == 0) fs[312] = mti;
+  }
+}
+
 }  // namespace heb_baseline

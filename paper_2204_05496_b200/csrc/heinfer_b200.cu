@@ -1397,6 +1397,7 @@ struct hei_gpu_ctx {
   bool split = false;   // HEI_SPLIT=1: split the key switch over digits for small batches
   bool graphs = true;   // HEI_NO_GRAPHS=1: launch the small-batch fold eagerly
   bool two_streams = true;  // HEI_TWO_STREAMS=0: fold the batch on one stream only
+  bool mt_jump = true;      // HEI_MT_JUMP=0: sequential mt19937_64 replay only
   cudaStream_t side_stream = nullptr;
   struct FoldGraph {
     uint64_t pairs;
@@ -1938,6 +1939,135 @@ uint64_t prng_next(hei_gpu_prng* p) {
   return x;
 }
 
+
+// ---- mt19937_64 jump-ahead support (host, setup-time GF(2) algebra) ----
+// phi = characteristic polynomial of the generator (degree 19937), found
+// once by Berlekamp-Massey on bit 0 of the output stream; x^J mod phi by
+// square-and-shift. Both are seed-independent and cached.
+using Poly2 = std::vector<uint64_t>;  // bit i = coefficient of x^i
+
+uint64_t get64(const Poly2& a, uint64_t off) {
+  const uint64_t w = off >> 6, sh = off & 63;
+  const uint64_t lo = w < a.size() ? a[w] : 0, hi = w + 1 < a.size() ? a[w + 1] : 0;
+  return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+}
+
+const Poly2& mt_charpoly() {
+  static std::mutex mu;
+  static Poly2 phi;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!phi.empty()) return phi;
+  const int Lx = heb_baseline::kMtDeg, LEN = 2 * Lx + 64;
+  hei_gpu_prng g;
+  prng_seed(&g, 5489);
+  Poly2 srev((LEN + 63) / 64 + 2, 0);  // bit j = s[LEN - 1 - j]
+  std::vector<uint8_t> sbits(LEN);
+  for (int k = 0; k < LEN; ++k) sbits[k] = (uint8_t)(prng_next(&g) & 1);
+  for (int j = 0; j < LEN; ++j)
+    if (sbits[LEN - 1 - j]) srev[j >> 6] |= 1ull << (j & 63);
+  const size_t W = (Lx + 64) / 64 + 2;
+  Poly2 C(W, 0), B(W, 0), T;
+  C[0] = B[0] = 1;
+  int L = 0, m = 1;
+  for (int N = 0; N < LEN; ++N) {
+    const uint64_t base = (uint64_t)(LEN - 1 - N);
+    uint64_t acc = 0;
+    for (size_t w = 0; w * 64 <= (size_t)L; ++w) {
+      uint64_t cw = C[w];
+      if (w == 0) cw &= ~1ull;  // i >= 1
+      acc ^= cw & get64(srev, base + 64 * w);
+    }
+    const uint32_t d = sbits[N] ^ (uint32_t)(__builtin_popcountll(acc) & 1);
+    if (!d) {
+      ++m;
+      continue;
+    }
+    T = C;
+    // C ^= B << m
+    const size_t ws = m >> 6, bs = m & 63;
+    for (size_t w = W; w-- > ws;) {
+      uint64_t v = B[w - ws] << bs;
+      if (bs && w - ws >= 1) v |= B[w - ws - 1] >> (64 - bs);
+      C[w] ^= v;
+    }
+    if (2 * L <= N) {
+      L = N + 1 - L;
+      B = T;
+      m = 1;
+    } else {
+      ++m;
+    }
+  }
+  if (L != Lx) raise(HEI_INTERNAL, "mt19937_64 characteristic polynomial has unexpected degree");
+  // phi_k = c_{L-k}
+  Poly2 f((Lx + 64) / 64, 0);
+  for (int k = 0; k <= Lx; ++k)
+    if ((C[(Lx - k) >> 6] >> ((Lx - k) & 63)) & 1) f[k >> 6] |= 1ull << (k & 63);
+  phi = f;
+  return phi;
+}
+
+void poly_reduce(Poly2& a, const Poly2& phi) {
+  const int D = heb_baseline::kMtDeg;
+  const int64_t top = (int64_t)a.size() * 64 - 1;
+  for (int64_t k = top; k >= D; --k) {
+    if (!((a[k >> 6] >> (k & 63)) & 1)) continue;
+    const int64_t sh = k - D;  // a ^= phi << sh
+    const int64_t ws = sh >> 6, bs = sh & 63;
+    for (size_t w = 0; w < phi.size(); ++w) {
+      const uint64_t v = phi[w];
+      a[w + ws] ^= v << bs;
+      if (bs && w + ws + 1 < a.size()) a[w + ws + 1] ^= v >> (64 - bs);
+    }
+  }
+  a.resize((D + 63) / 64);
+}
+
+// x^J mod phi
+Poly2 mt_jump_poly(uint64_t J) {
+  static std::mutex mu;
+  static std::map<uint64_t, Poly2> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(J);
+  if (it != cache.end()) return it->second;
+  const Poly2& phi = mt_charpoly();
+  const size_t nw = (heb_baseline::kMtDeg + 63) / 64;
+  Poly2 r(nw, 0);
+  r[0] = 1;
+  for (int bit = 63; bit >= 0; --bit) {
+    if (!(J >> bit) && r[0] == 1) {
+      bool one = true;
+      for (size_t w = 1; w < nw; ++w) one = one && r[w] == 0;
+      if (one) continue;  // leading zeros of J
+    }
+    // square: spread bits
+    Poly2 sq(2 * nw + 1, 0);
+    for (size_t w = 0; w < nw; ++w) {
+      uint64_t x = r[w];
+      uint64_t lo = 0, hi = 0;
+      for (int i = 0; i < 32; ++i) {
+        lo |= ((x >> i) & 1ull) << (2 * i);
+        hi |= ((x >> (i + 32)) & 1ull) << (2 * i);
+      }
+      sq[2 * w] = lo;
+      sq[2 * w + 1] = hi;
+    }
+    poly_reduce(sq, phi);
+    r = sq;
+    if ((J >> bit) & 1) {  // r *= x
+      Poly2 sh(nw + 1, 0);
+      for (size_t w = 0; w < nw; ++w) {
+        sh[w] |= r[w] << 1;
+        sh[w + 1] |= r[w] >> 63;
+      }
+      poly_reduce(sh, phi);
+      r = sh;
+    }
+  }
+  cache[J] = r;
+  return r;
+}
+
 }  // namespace
 
 // ================================================================== C ABI
@@ -1991,6 +2121,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_SPLIT")) c->split = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_NO_GRAPHS")) c->graphs = std::atoi(v) == 0;
     if (const char* v = std::getenv("HEI_TWO_STREAMS")) c->two_streams = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_MT_JUMP")) c->mt_jump = std::atoi(v) != 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
@@ -2606,6 +2737,8 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
           raise(HEI_PARAM_ERROR, "baseline: plaintext modulus exceeds a ciphertext prime (unsupported)");
     set_device(c);
     std::lock_guard<std::mutex> lk(c->mu);
+    const hei_gpu_prng init0 = *rng0, init1 = *rng1;
+    for (bool force_seq = false;; force_seq = true) {
     cudaStream_t st = c->stream;
     const Geo& g = c->geo;
     const uint32_t n = c->n, P = c->P();
@@ -2665,6 +2798,46 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     CU(cudaMemcpyAsync(d_state, hstate, sizeof(hstate), cudaMemcpyHostToDevice, st));
     k_bl_weights<<<grid_for(f * cols * P, 256), 256, 0, st>>>(g, d_w, f * cols, d_wc);
     LAUNCHED();
+    // Jump-ahead replay: when both streams start block-aligned (mti == 312,
+    // e.g. fresh Prngs), the whole call's draws are produced by K chunk
+    // generators per branch whose start states come from x^C mod phi
+    // (k_mt_jumps), instead of one sequential generator per branch. A
+    // rejection anywhere would misalign the chunks; k_bl_noise flags it at
+    // its exact position and the call re-runs on the sequential path.
+    const uint64_t E_total = f * B, Dtot = E_total * 3 * n;
+    bool jump = c->mt_jump && !force_seq && hstate[0][312] == 312 && hstate[1][312] == 312 && E_total >= 64 &&
+                Dtot * 16 <= ((uint64_t)48 << 30);
+    uint64_t* d_rawall = nullptr;
+    if (jump) {
+      uint64_t K = std::min<uint64_t>(128, E_total / 8);
+      const uint64_t Cenc = (E_total + K - 1) / K;
+      K = (E_total + Cenc - 1) / Cenc;
+      const uint64_t C = Cenc * 3 * n;
+      const Poly2 poly = mt_jump_poly(C);
+      uint64_t *d_poly = nullptr, *d_starts = nullptr, *d_cur = nullptr, *d_wseq = nullptr, *d_part = nullptr;
+      const uint32_t wlen = 312 * 65, S = 64, wsl = (uint32_t)((poly.size() + S - 1) / S);
+      alloc(&d_poly, poly.size() * 8);
+      alloc(&d_starts, 2 * K * 313 * 8);
+      alloc(&d_cur, 2 * 313 * 8);
+      alloc(&d_wseq, 2ull * wlen * 8);
+      alloc(&d_part, 2ull * S * 312 * 8);
+      alloc(&d_rawall, 2 * Dtot * 8);
+      CU(cudaMemcpyAsync(d_poly, poly.data(), poly.size() * 8, cudaMemcpyHostToDevice, st));
+      // chunk 0 starts at the current (block-aligned) state
+      for (int bb = 0; bb < 2; ++bb) {
+        CU(cudaMemcpyAsync(d_starts + (uint64_t)bb * K * 313, d_state + bb * 313, 313 * 8, cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync(d_cur + bb * 313, d_state + bb * 313, 313 * 8, cudaMemcpyDeviceToDevice, st));
+      }
+      for (uint32_t m = 1; m < K; ++m) {
+        heb_baseline::k_mt_wseq<<<2, 320, 0, st>>>(d_cur, d_wseq, wlen);
+        heb_baseline::k_mt_xor<<<dim3(S, 2), 320, 0, st>>>(d_wseq, wlen, d_poly, wsl, d_part);
+        heb_baseline::k_mt_xor_reduce<<<2, 320, 0, st>>>(d_part, S, d_cur, d_starts, (uint32_t)K, m);
+        g_launches += 3;
+      }
+      CU(cudaGetLastError());
+      heb_baseline::k_mt_chunks<<<dim3((unsigned)K, 2), 320, 0, st>>>(d_starts, (uint32_t)K, C, Dtot, d_rawall, d_state);
+      LAUNCHED();
+    }
     const size_t sm1 = smem_bytes(c, 1);
     const unsigned at = std::min<uint32_t>(256, n);
     // The mt19937_64 replay is sequential per branch (one CTA each), so the
@@ -2680,6 +2853,7 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     }
     CU(cudaStreamSynchronize(st));  // state, x, w uploads visible to `ms`
     auto generate = [&](uint64_t k0, int slot) {
+      if (jump) return;
       const uint64_t Fb = std::min<uint64_t>(F, f - k0), draws = Fb * B * 3 * n;
       CU(cudaStreamWaitEvent(ms, used[slot], 0));
       heb_baseline::k_mt_generate<<<2, 320, 0, ms>>>(d_state, d_raw + (size_t)slot * 2 * Emax * 3 * n, draws);
@@ -2691,9 +2865,14 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     for (uint64_t k0 = 0; k0 < f; k0 += F, slot ^= 1) {
       const uint64_t Fb = std::min<uint64_t>(F, f - k0), E = Fb * B, draws = E * 3 * n;
       if (k0 + F < f) generate(k0 + F, slot ^ 1);
-      CU(cudaStreamWaitEvent(st, gen[slot], 0));
-      heb_baseline::k_bl_noise<<<dim3((unsigned)E, 2), 256, 0, st>>>(d_raw + (size_t)slot * 2 * Emax * 3 * n, draws, n,
-                                                                    (uint32_t)E, d_noise, c->d_err);
+      if (jump) {
+        heb_baseline::k_bl_noise<<<dim3((unsigned)E, 2), 256, 0, st>>>(d_rawall + k0 * B * 3 * n, Dtot, n, (uint32_t)E,
+                                                                      d_noise, c->d_err);
+      } else {
+        CU(cudaStreamWaitEvent(st, gen[slot], 0));
+        heb_baseline::k_bl_noise<<<dim3((unsigned)E, 2), 256, 0, st>>>(d_raw + (size_t)slot * 2 * Emax * 3 * n, draws,
+                                                                      n, (uint32_t)E, d_noise, c->d_err);
+      }
       LAUNCHED();
       CU(cudaEventRecord(used[slot], st));
       HEI_DISPATCH(c->logn,
@@ -2728,8 +2907,20 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
       std::memcpy(r->mt, hstate[b], 312 * 8);
       r->mti = (uint32_t)hstate[b][312];
     }
+    if (jump) {
+      uint32_t errh = 0;
+      CU(cudaMemcpy(&errh, c->d_err, 4, cudaMemcpyDeviceToHost));
+      if (errh) {  // a rejection misaligned the chunks: replay sequentially
+        CU(cudaMemset(c->d_err, 0, 4));
+        *rng0 = init0;
+        *rng1 = init1;
+        continue;
+      }
+    }
     check_err_flag(c, HEI_INTERNAL, "baseline: rng rejection in the encryption stream (replay unsupported)");
     if (cnt) hei_baseline_counts(rows, cols, f, n, cnt);
+    break;
+    }
   });
 }
 

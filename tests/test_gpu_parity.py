@@ -349,3 +349,27 @@ def test_sharded_partials_sum_to_single_gpu_result(prod):
     torch.cuda.synchronize()
     got = out.cpu().numpy().view(np.uint32).astype(np.uint64)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n,R,f,cols", [(32, 40, 100, 2), (8192, 2, 80, 2)])
+def test_baseline_jump_ahead_replay(n, R, f, cols):
+    """Enough encryptions (>= 64) for the jump-ahead mt19937_64 replay:
+    chunk generators seeded by x^C mod phi must reproduce the reference's
+    sequential stream exactly (ciphertexts, decryptions, final RNG state)."""
+    from paper_2204_05496_b200 import Prng, baseline_matmul
+
+    p = tiny_params(32) if n == 32 else production_params(8192)
+    o = Oracle(p, key_seed=11, enc_seed=20)
+    s = gpu_server_from(o, with_pk=True)
+    rng = np.random.default_rng(f)
+    x = random_mat(rng, R, f, 9)
+    w = random_mat(rng, f, cols, 5)
+    b = rng.integers(-50, 51, size=cols)
+    r0, r1 = Prng(20), Prng(21)
+    got, _ = baseline_matmul(s, x, w, b, r0, r1)
+    want, _ = o.baseline_matmul(x, w, b)
+    assert np.array_equal(got, want)
+    assert np.array_equal(o.unpack_baseline(got, R, cols), oracle_matmul(x, w, b))
+    ref0 = Prng(20)
+    ref0.draw(((R + p.n - 1) // p.n) * f * 3 * p.n)
+    assert np.array_equal(r0.draw(8), ref0.draw(8))
