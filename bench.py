@@ -384,7 +384,7 @@ def run_ours(args, world, rank, local):
             _nat.check(_nat.lib().hei_gpu_upload_public_key(srv.handle, _C.c_uint32(bb), _nat.u64p(pk[bb])))
         R3, f3, c3, _, pf3, ws3 = CONFIGS["c3"]
         x3, w3, b3 = synthetic(R3, f3, c3, pf3, ws3)
-        baseline_matmul(srv, x3[:, :512], w3[:512], b3, Prng(2), Prng(3))  # warm
+        baseline_matmul(srv, x3, w3, b3, Prng(2), Prng(3))  # warm (incl. the cached jump polynomial)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         _, bc = baseline_matmul(srv, x3, w3, b3, Prng(2), Prng(3))
