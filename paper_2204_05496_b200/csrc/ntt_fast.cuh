@@ -161,11 +161,17 @@ struct Ntt {
       const uint32_t lanebit = t / 16;
       const bool upper = (x0 & t) != 0;
       const uint2 w = entry(tc, PAD + s);
+      // Half exchange: the lower thread keeps pairs 0..7, the upper pairs
+      // 8..15; each does its 8 butterflies locally, then the outputs that
+      // belong to the partner go back (16 shuffles, no redundant products).
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const uint32_t mine = upper ? mul_shoup(e[r], w.x, w.y, q) : e[r];
-        const uint32_t other = __shfl_xor_sync(0xffffffffu, mine, lanebit);
-        e[r] = upper ? sub_mod(other, mine, q) : add_mod(mine, other, q);
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t recv = __shfl_xor_sync(0xffffffffu, upper ? e[k] : e[k + 8], lanebit);
+        uint32_t u = upper ? recv : e[k], v = upper ? e[k + 8] : recv;
+        ct(u, v, w, q);
+        const uint32_t back = __shfl_xor_sync(0xffffffffu, upper ? u : v, lanebit);
+        e[k] = upper ? back : u;
+        e[k + 8] = upper ? v : back;
       }
     }
     {
@@ -248,10 +254,13 @@ struct Ntt {
       const bool upper = (x0 & t) != 0;
       const uint2 w = entry(tc, PAD + s);
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const uint32_t other = __shfl_xor_sync(0xffffffffu, e[r], lanebit);
-        // lower keeps u + v; upper keeps (u - v) * w
-        e[r] = upper ? mul_shoup(sub_mod(other, e[r], q), w.x, w.y, q) : add_mod(e[r], other, q);
+      for (int k = 0; k < 8; ++k) {  // half exchange, as in the forward pass
+        const uint32_t recv = __shfl_xor_sync(0xffffffffu, upper ? e[k] : e[k + 8], lanebit);
+        uint32_t u = upper ? recv : e[k], v = upper ? e[k + 8] : recv;
+        gs(u, v, w, q);
+        const uint32_t back = __shfl_xor_sync(0xffffffffu, upper ? u : v, lanebit);
+        e[k] = upper ? back : u;
+        e[k + 8] = upper ? v : back;
       }
     }
     __syncthreads();
