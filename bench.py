@@ -391,6 +391,20 @@ def run_ours(args, world, rank, local):
         bs = time.perf_counter() - t0
         base = {"algorithm": "standard (sample-batched, baseline_matmul)", "config": f"c3: {R3}x{f3}x{c3} N={n}",
                 "ms": bs * 1000.0, "mul_plain": int(bc.mul_plain_count), "note": "host call incl. H2D of x, w and D2H"}
+        # client-side encryption of this step's inputs (encode_inputs,
+        # matmul.cpp:201-223), device path, R individuals x f features
+        from paper_2204_05496_b200 import encode_inputs_device
+
+        xe, _, _ = synthetic(R, f, cols, pf, ws)
+        d_enc = torch.empty((R * kc, ctw), dtype=torch.int32, device=dev)
+        encode_inputs_device(srv, xe, Prng(2), Prng(3), d_enc.data_ptr(), stream.cuda_stream)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        encode_inputs_device(srv, xe, Prng(2), Prng(3), d_enc.data_ptr(), stream.cuda_stream)
+        es = time.perf_counter() - t0
+        base["client_encrypt"] = {"config": f"{R} individuals x {f} features ({R * kc} twin encryptions)",
+                                  "ms": es * 1000.0, "individuals_per_s": R / es}
+        del d_enc
 
     lat = None
     if args.latency and rank == 0:

@@ -136,6 +136,17 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* ctx, const int64_t* x, uint64_t rows, u
                             hei_gpu_prng* rng0, hei_gpu_prng* rng1, uint64_t* out,
                             hei_op_counters* counters);
 
+/* Client-side encryption of inputs: matmul::encode_inputs
+ * (matmul.cpp:201-223) — ceil(f/N) slot chunks per row, encode_signed +
+ * encrypt in eval form, randomness replayed from the two branch Prngs exactly
+ * as BfvBackend::encrypt draws it. x is rows x f (scaled, row-major);
+ * out [row][k][twin ct] u64 (host) or u32 (device variant). */
+int hei_gpu_encode_inputs(hei_gpu_ctx* ctx, const int64_t* x, uint64_t rows, uint64_t f,
+                          hei_gpu_prng* rng0, hei_gpu_prng* rng1, uint64_t* out);
+int hei_gpu_encode_inputs_device(hei_gpu_ctx* ctx, const int64_t* x, uint64_t rows, uint64_t f,
+                                 hei_gpu_prng* rng0, hei_gpu_prng* rng1, uint32_t* d_out,
+                                 void* stream);
+
 /* Closed forms (matmul.cpp:172-199). */
 int hei_proposed_counts(uint64_t rows, uint64_t cols, uint64_t f, uint32_t n, hei_op_counters* c);
 int hei_baseline_counts(uint64_t rows, uint64_t cols, uint64_t f, uint32_t n, hei_op_counters* c);

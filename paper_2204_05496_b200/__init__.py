@@ -26,6 +26,8 @@ from .matmul import (  # noqa: F401
     ScalingConfig,
     baseline_counts,
     encode_bias,
+    encode_inputs,
+    encode_inputs_device,
     encode_weights,
     matmul,
     matmul_device,

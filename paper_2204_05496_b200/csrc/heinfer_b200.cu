@@ -1041,21 +1041,25 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_mask_acc_f(Geo g, const uin
 template <int LOGN>
 __global__ void __launch_bounds__(Ntt<LOGN>::T) k_bl_encode(Geo g, const int64_t* __restrict__ x, uint64_t R,
                                                            uint64_t f, uint64_t k0, uint32_t B,
-                                                           uint32_t* __restrict__ m_out) {
+                                                           uint32_t* __restrict__ m_out, int row_mode = 0) {
   using NT = Ntt<LOGN>;
   constexpr uint32_t N = NT::N;
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
   const uint32_t e = blockIdx.x, b = blockIdx.y;
-  const uint64_t k = k0 + e / B;
-  const uint64_t base = (uint64_t)(e % B) * N;
-  const uint64_t rows_b = min((uint64_t)N, R - base);
+  // column mode (baseline): slot s = row base + s of feature k.
+  // row mode (encode_inputs, matmul.cpp:201-211): encryption k0 + e is chunk
+  // (k0 + e) % B of row (k0 + e) / B (B = chunks per row), slot s = feature.
+  const uint64_t eg = k0 + e;
+  const uint64_t k = row_mode ? 0 : k0 + e / B;
+  const uint64_t base = row_mode ? (eg / B) * f + (eg % B) * N : (uint64_t)(e % B) * N;
+  const uint64_t lim = row_mode ? min((uint64_t)N, f - (eg % B) * N) : min((uint64_t)N, R - base);
   const BranchInfo& br = g.br[b];
   const int64_t t = br.t;
   for (uint32_t s = threadIdx.x; s < N; s += blockDim.x) {
     int64_t r = 0;
-    if (s < rows_b) {
-      r = x[(base + s) * f + k] % t;
+    if (s < lim) {
+      r = (row_mode ? x[base + s] : x[(base + s) * f + k]) % t;
       if (r < 0) r += t;
     }
     sm[swz(g.index_map[s])] = (uint32_t)r;
@@ -1231,17 +1235,19 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T) k_prepare_pk(Geo g, const uint64
 
 // Generic (small-ring) versions of the baseline encoders, natural layouts.
 __global__ void k_bl_encode_g(Geo g, const int64_t* __restrict__ x, uint64_t R, uint64_t f, uint64_t k0, uint32_t B,
-                              uint32_t* __restrict__ m_out) {
+                              uint32_t* __restrict__ m_out, int row_mode = 0) {
   extern __shared__ uint32_t sm[];
   const uint32_t n = g.n, e = blockIdx.x, b = blockIdx.y;
-  const uint64_t k = k0 + e / B, base = (uint64_t)(e % B) * n;
-  const uint64_t rows_b = min((uint64_t)n, R - base);
+  const uint64_t eg = k0 + e;
+  const uint64_t k = row_mode ? 0 : k0 + e / B;
+  const uint64_t base = row_mode ? (eg / B) * f + (eg % B) * n : (uint64_t)(e % B) * n;
+  const uint64_t lim = row_mode ? min((uint64_t)n, f - (eg % B) * n) : min((uint64_t)n, R - base);
   const BranchInfo& br = g.br[b];
   const int64_t t = br.t;
   for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
     int64_t r = 0;
-    if (s < rows_b) {
-      r = x[(base + s) * f + k] % t;
+    if (s < lim) {
+      r = (row_mode ? x[base + s] : x[(base + s) * f + k]) % t;
       if (r < 0) r += t;
     }
     sm[g.index_map[s]] = (uint32_t)r;
@@ -2066,6 +2072,139 @@ Poly2 mt_jump_poly(uint64_t J) {
   }
   cache[J] = r;
   return r;
+}
+
+
+// ---- client encryption: matmul::encode_inputs (matmul.cpp:201-223) --------
+// Every row is split into ceil(f / N) slot chunks, each encode_signed + encrypt
+// (eval form) with the branch's util::Prng stream, in (row, chunk) order — the
+// same draws BfvBackend::encrypt consumes (context.cpp:262-303).
+void encode_inputs_impl(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_t f, hei_gpu_prng* rng0,
+                        hei_gpu_prng* rng1, uint64_t* out_host, uint32_t* out_dev, cudaStream_t st) {
+  if (rows == 0 || f == 0) raise(HEI_PARAM_ERROR, "encode_inputs: empty matrix");
+  if (!c->d_pk[0] || !c->d_pk[1]) raise(HEI_KEY_ERROR, "encrypt: this backend holds no public key");
+  if (!rng0 || !rng1) raise(HEI_PARAM_ERROR, "encode_inputs: encryption randomness required");
+  if (rng0->have_spare || rng1->have_spare)
+    raise(HEI_PARAM_ERROR, "encode_inputs: rng holds a cached Box-Muller spare; cannot replay on the device");
+  const int64_t lim = (int64_t)(((u128)c->t[0] * c->t[1] - 1) / 2);
+  for (uint64_t i = 0; i < rows * f; ++i)
+    if (x[i] > lim || x[i] < -lim) raise(HEI_RANGE_ERROR, "encode_signed: value outside the centered range");
+  const Geo& g = c->geo;
+  const uint32_t n = c->n, P = c->P();
+  const uint64_t kc = (f + n - 1) / n, E_total = rows * kc, Dtot = E_total * 3 * n;
+  if (!c->d_pkp) {
+    CU(cudaMalloc(&c->d_pkp, 2ull * P * n * sizeof(uint2)));
+    const size_t sm = smem_bytes(c, 1);
+    HEI_DISPATCH(c->logn, (k_prepare_pk<LG><<<2 * P, Ntt<LG>::T, sm, st>>>(g, c->d_pk[0], c->d_pk[1], c->d_pkp, c->d_err)),
+                 (k_prepare_pk_g<<<2 * P, c->threads(), sm, st>>>(g, c->d_pk[0], c->d_pk[1], c->d_pkp, c->d_err)));
+    LAUNCHED();
+    check_err_flag(c, HEI_CODEC_ERROR, "public key: coefficient not reduced");
+  }
+  struct Free {
+    std::vector<void*> p;
+    ~Free() {
+      for (void* v : p) cudaFree(v);
+    }
+  } fr;
+  auto alloc = [&](auto** ptr, size_t bytes) {
+    CU(cudaMalloc((void**)ptr, bytes));
+    fr.p.push_back((void*)*ptr);
+  };
+  const uint64_t Eb = std::min<uint64_t>(E_total, 256);
+  int64_t* d_x = nullptr;
+  uint64_t *d_raw = nullptr, *d_state = nullptr, *d_out64 = nullptr;
+  int8_t* d_noise = nullptr;
+  uint32_t *d_m = nullptr, *d_ct = nullptr;
+  alloc(&d_x, rows * f * 8);
+  alloc(&d_raw, 2 * Dtot * 8);
+  alloc(&d_state, 2 * 313 * 8);
+  alloc(&d_noise, Eb * 2 * 3 * n);
+  alloc(&d_m, Eb * 2 * n * 4);
+  if (!out_dev) {
+    alloc(&d_ct, Eb * c->ct_words() * 4);
+    alloc(&d_out64, Eb * c->ct_words() * 8);
+  }
+  CU(cudaMemcpyAsync(d_x, x, rows * f * 8, cudaMemcpyHostToDevice, st));
+  const hei_gpu_prng init0 = *rng0, init1 = *rng1;
+  for (bool force_seq = false;; force_seq = true) {
+    uint64_t hstate[2][313];
+    for (int b = 0; b < 2; ++b) {
+      hei_gpu_prng* r = b ? rng1 : rng0;
+      std::memcpy(hstate[b], r->mt, 312 * 8);
+      hstate[b][312] = r->mti;
+    }
+    CU(cudaMemcpyAsync(d_state, hstate, sizeof(hstate), cudaMemcpyHostToDevice, st));
+    const bool jump = c->mt_jump && !force_seq && hstate[0][312] == 312 && hstate[1][312] == 312 && E_total >= 64;
+    if (jump) {
+      uint64_t K = std::min<uint64_t>(128, E_total / 8);
+      const uint64_t Cenc = (E_total + K - 1) / K;
+      K = (E_total + Cenc - 1) / Cenc;
+      const uint64_t C = Cenc * 3 * n;
+      const Poly2 poly = mt_jump_poly(C);
+      uint64_t *d_poly = nullptr, *d_starts = nullptr, *d_cur = nullptr, *d_wseq = nullptr, *d_part = nullptr;
+      const uint32_t wlen = 312 * 65, S = 64, wsl = (uint32_t)((poly.size() + S - 1) / S);
+      alloc(&d_poly, poly.size() * 8);
+      alloc(&d_starts, 2 * K * 313 * 8);
+      alloc(&d_cur, 2 * 313 * 8);
+      alloc(&d_wseq, 2ull * wlen * 8);
+      alloc(&d_part, 2ull * S * 312 * 8);
+      CU(cudaMemcpyAsync(d_poly, poly.data(), poly.size() * 8, cudaMemcpyHostToDevice, st));
+      for (int bb = 0; bb < 2; ++bb) {
+        CU(cudaMemcpyAsync(d_starts + (uint64_t)bb * K * 313, d_state + bb * 313, 313 * 8, cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync(d_cur + bb * 313, d_state + bb * 313, 313 * 8, cudaMemcpyDeviceToDevice, st));
+      }
+      for (uint32_t m = 1; m < K; ++m) {
+        heb_baseline::k_mt_wseq<<<2, 320, 0, st>>>(d_cur, d_wseq, wlen);
+        heb_baseline::k_mt_xor<<<dim3(S, 2), 320, 0, st>>>(d_wseq, wlen, d_poly, wsl, d_part);
+        heb_baseline::k_mt_xor_reduce<<<2, 320, 0, st>>>(d_part, S, d_cur, d_starts, (uint32_t)K, m);
+        g_launches += 3;
+      }
+      heb_baseline::k_mt_chunks<<<dim3((unsigned)K, 2), 320, 0, st>>>(d_starts, (uint32_t)K, C, Dtot, d_raw, d_state);
+      LAUNCHED();
+    } else {
+      heb_baseline::k_mt_generate<<<2, 320, 0, st>>>(d_state, d_raw, Dtot);
+      LAUNCHED();
+    }
+    const size_t sm1 = smem_bytes(c, 1);
+    for (uint64_t e0 = 0; e0 < E_total; e0 += Eb) {
+      const uint64_t E = std::min<uint64_t>(Eb, E_total - e0);
+      heb_baseline::k_bl_noise<<<dim3((unsigned)E, 2), 256, 0, st>>>(d_raw + e0 * 3 * n, Dtot, n, (uint32_t)E, d_noise,
+                                                                    c->d_err);
+      LAUNCHED();
+      HEI_DISPATCH(c->logn,
+                   (k_bl_encode<LG><<<dim3((unsigned)E, 2), Ntt<LG>::T, sm1, st>>>(g, d_x, rows, f, e0, (uint32_t)kc, d_m, 1)),
+                   (k_bl_encode_g<<<dim3((unsigned)E, 2), c->threads(), sm1, st>>>(g, d_x, rows, f, e0, (uint32_t)kc, d_m, 1)));
+      LAUNCHED();
+      uint32_t* ct = out_dev ? out_dev + e0 * c->ct_words() : d_ct;
+      HEI_DISPATCH(c->logn, (k_bl_encrypt<LG><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct)),
+                   (k_bl_encrypt_g<<<(unsigned)(E * P), c->threads(), sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct)));
+      LAUNCHED();
+      if (!out_dev) {
+        k_widen<<<grid_for(E * c->ct_words(), 256), 256, 0, st>>>(d_ct, d_out64, E * c->ct_words());
+        LAUNCHED();
+        CU(cudaMemcpyAsync(out_host + e0 * c->ct_words(), d_out64, E * c->ct_words() * 8, cudaMemcpyDeviceToHost, st));
+      }
+    }
+    CU(cudaMemcpyAsync(hstate, d_state, sizeof(hstate), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int b = 0; b < 2; ++b) {
+      hei_gpu_prng* r = b ? rng1 : rng0;
+      std::memcpy(r->mt, hstate[b], 312 * 8);
+      r->mti = (uint32_t)hstate[b][312];
+    }
+    if (jump) {
+      uint32_t errh = 0;
+      CU(cudaMemcpy(&errh, c->d_err, 4, cudaMemcpyDeviceToHost));
+      if (errh) {
+        CU(cudaMemset(c->d_err, 0, 4));
+        *rng0 = init0;
+        *rng1 = init1;
+        continue;
+      }
+    }
+    check_err_flag(c, HEI_INTERNAL, "encode_inputs: rng rejection in the encryption stream (replay unsupported)");
+    break;
+  }
 }
 
 }  // namespace
@@ -2968,6 +3107,25 @@ int hei_gpu_finish_packed_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const
     tmp.owns_acc = false;
     finish_to(&tmp, d_out, st);
     CU(cudaStreamSynchronize(st));
+  });
+}
+
+
+int hei_gpu_encode_inputs(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_t f, hei_gpu_prng* rng0,
+                          hei_gpu_prng* rng1, uint64_t* out) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    encode_inputs_impl(c, x, rows, f, rng0, rng1, out, nullptr, c->stream);
+  });
+}
+
+int hei_gpu_encode_inputs_device(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_t f, hei_gpu_prng* rng0,
+                                 hei_gpu_prng* rng1, uint32_t* d_out, void* stream) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    encode_inputs_impl(c, x, rows, f, rng0, rng1, nullptr, d_out, stream ? (cudaStream_t)stream : c->stream);
   });
 }
 

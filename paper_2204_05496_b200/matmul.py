@@ -289,3 +289,23 @@ def baseline_matmul(server: GpuTwinServer, x: np.ndarray, w: np.ndarray, bias, r
     check(native.lib().hei_gpu_baseline_matmul(server.handle, i64p(x), C.c_uint64(R), C.c_uint64(f), i64p(w), C.c_uint64(cols),
                                                i64p(bias), rng0._h, rng1._h, u64p(out), C.byref(cnt)))
     return out, cnt
+
+
+def encode_inputs(server: GpuTwinServer, x: np.ndarray, rng0: Prng, rng1: Prng) -> np.ndarray:
+    """matmul::encode_inputs (matmul.cpp:201-223) on the device: x is R x f
+    scaled integers; returns [R][ceil(f/N)][twin ct] u64 eval-form ciphertexts
+    drawn from the two branch Prng streams (needs the public keys)."""
+    x = np.ascontiguousarray(x, dtype=np.int64)
+    if x.ndim != 2 or x.size == 0:
+        raise ParamError("encode_inputs: empty matrix")
+    R, f = x.shape
+    out = np.zeros((R, server.chunks(f), server.ct_words), dtype=np.uint64)
+    check(native.lib().hei_gpu_encode_inputs(server.handle, i64p(x), C.c_uint64(R), C.c_uint64(f), rng0._h, rng1._h, u64p(out)))
+    return out
+
+
+def encode_inputs_device(server: GpuTwinServer, x: np.ndarray, rng0: Prng, rng1: Prng, d_out_ptr: int, stream_ptr: int = 0):
+    x = np.ascontiguousarray(x, dtype=np.int64)
+    R, f = x.shape
+    check(native.lib().hei_gpu_encode_inputs_device(server.handle, i64p(x), C.c_uint64(R), C.c_uint64(f), rng0._h, rng1._h,
+                                                    C.c_void_p(d_out_ptr), C.c_void_p(stream_ptr)))

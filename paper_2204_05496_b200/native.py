@@ -98,6 +98,7 @@ EXPORTED = [
     "hei_gpu_launch_count", "hei_gpu_reset_launch_count", "hei_gpu_set_batch_pairs",
     "hei_gpu_kernel_timing", "hei_gpu_kernel_stats", "hei_gpu_measure_butterfly_peak",
     "hei_gpu_matmul_partial_device", "hei_gpu_finish_packed_device",
+    "hei_gpu_encode_inputs", "hei_gpu_encode_inputs_device",
 ]
 
 _lib = None

@@ -373,3 +373,23 @@ def test_baseline_jump_ahead_replay(n, R, f, cols):
     ref0 = Prng(20)
     ref0.draw(((R + p.n - 1) // p.n) * f * 3 * p.n)
     assert np.array_equal(r0.draw(8), ref0.draw(8))
+
+
+@pytest.mark.parametrize("n,R,f", [(32, 3, 70), (8192, 2, 9000), (8192, 40, 9000)])
+def test_device_client_encryption_matches_reference(n, R, f):
+    """matmul::encode_inputs on the device (sequential and jump-ahead replay):
+    ciphertexts bit-identical to the reference client's, and they decrypt."""
+    from paper_2204_05496_b200 import Prng, encode_inputs
+
+    p = tiny_params(32) if n == 32 else production_params(8192)
+    o = Oracle(p, key_seed=3, enc_seed=30)
+    s = gpu_server_from(o, with_pk=True)
+    rng = np.random.default_rng(R + f)
+    x = random_mat(rng, R, f, 30)
+    got = encode_inputs(s, x, Prng(30), Prng(31))
+    want = o.encode_inputs(x)
+    assert np.array_equal(got, want)
+    vals, budget = o.decrypt_signed(got[-1, -1])
+    k = (f - 1) // p.n
+    tail = x[-1, k * p.n:]
+    assert np.array_equal(vals[: tail.size], tail) and budget > 0
