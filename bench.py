@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--rows", type=int, default=0, help="override individuals per rank")
     ap.add_argument("--batch-pairs", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-wire", dest="wire", action="store_false", help="skip the HECT wire-path e2e timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--latency", action="store_true", default=True, help="also time a single-individual (C3) call")
     ap.add_argument("--no-latency", dest="latency", action="store_false")
@@ -221,6 +222,40 @@ def make_server(n, device, seed=1):
     return srv, q0, q1
 
 
+def wire_e2e(srv, ew, b, h_np, R, kc, n, L0, L1, world, steps):
+    """Time hei_gpu_matmul_wire on the same residues laid out as the
+    request's HECT blobs (serialize.cpp:63-78; treated as coeff form)."""
+    import torch
+
+    from paper_2204_05496_b200 import matmul_wire
+
+    b0, b1 = srv.hect_bytes(0), srv.hect_bytes(1)
+    hdr = [np.frombuffer(b"HECT\x01\x00" + srv.params_hash(k).to_bytes(8, "little") + b"\x02\x00\x00\x00\x05", np.uint8)
+           for k in range(2)]
+    buf = torch.empty(R * kc * (b0 + b1), dtype=torch.uint8, pin_memory=True)
+    a = buf.numpy().reshape(R * kc, b0 + b1)
+    src = h_np.reshape(R * kc, -1)
+    off = 0
+    for k, L in enumerate((L0, L1)):
+        a[:, off:off + 19] = hdr[k]
+        polys = a[:, off + 19: off + 19 + 2 * L * (1 + 8 * n)].reshape(R * kc, 2 * L, 1 + 8 * n)
+        polys[:, :, 0] = 0
+        w0 = (2 * L0 * n) if k else 0
+        slab = np.ascontiguousarray(src[:, w0: w0 + 2 * L * n]).reshape(R * kc, 2 * L, n)
+        polys[:, :, 1:] = slab.view(np.uint8).reshape(R * kc, 2 * L, 8 * n)
+        off += (b0 if k == 0 else b1)
+    outs, _ = matmul_wire(srv, ew, a, R, b)  # warm
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        outs, _ = matmul_wire(srv, ew, a, R, b)
+    sec = (time.perf_counter() - t0) / steps
+    res = {"value": world * R / sec, "unit": "inferences/s", "h2d_bytes_per_step": int(a.nbytes),
+           "d2h_bytes_per_step": int(sum(len(o) for o in outs)), "ms_per_step": 1000 * sec,
+           "format": "HECT coeff-form blobs [row][chunk][branch] in, HECT blobs out (server.cpp:112-172)"}
+    del buf, a
+    return res
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -317,6 +352,11 @@ def run_ours(args, world, rank, local):
         e2e_s = (time.perf_counter() - t0) / e2e_steps
         e2e = {"value": world * R / e2e_s, "unit": "inferences/s", "h2d_bytes_per_step": int(h_np.nbytes),
                "d2h_bytes_per_step": int(out.nbytes), "ms_per_step": 1000 * e2e_s}
+        # the server's wire path (server.cpp:112-172): HECT coeff-form blobs
+        # in, HECT blobs out, parse/NTT/INTT/serialize on the device
+        if args.wire:
+            e2e["wire"] = wire_e2e(srv, ew, b, h_np, R, kc, n, len(q0), len(q1), world, e2e_steps)
+        del h_in, h_np
 
     # ---- roofline of the dominant kernel (key switch), timed live with CUDA
     # events on the launch stream inside the C ABI over one extra step.

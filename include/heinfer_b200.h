@@ -95,6 +95,23 @@ int hei_gpu_matmul(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint64_t* i
                    int form, uint64_t rows, const int64_t* bias, uint64_t* out,
                    hei_op_counters* counters);
 
+/* Server wire path (InferenceServer::do_infer, server.cpp:112-172): the
+ * request's HECT ciphertext blobs (bfv::load_ciphertext, serialize.cpp:80-91;
+ * coeff form) concatenated in request order [row][chunk][branch], each branch-b
+ * blob exactly hei_hect_ciphertext_bytes(N, L_b) bytes; the response blobs
+ * (bfv::save_ciphertext, serialize.cpp:63-78) are written to `out` in order
+ * [packed ct][branch]. Parsing, range checks, to_eval, the matmul, to_coeff
+ * and serialization all run on the device. params_hash[b] =
+ * BfvContext::hash() of branch b (hei_params_hash). Header errors raise
+ * HEI_CODEC_ERROR with the reference's messages. */
+uint64_t hei_hect_ciphertext_bytes(uint32_t n, uint32_t num_primes);
+uint64_t hei_params_hash(uint32_t n, uint64_t t, int security_level, const uint64_t* q,
+                         uint32_t num_primes);
+int hei_gpu_matmul_wire(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint64_t params_hash[2],
+                        const uint8_t* blobs, uint64_t blob_bytes, uint64_t rows, const int64_t* bias,
+                        uint8_t* out, uint64_t out_capacity, uint64_t* out_bytes,
+                        hei_op_counters* counters);
+
 /* Same call on device-resident u32 residues (the HBM-resident bench path):
  * d_inputs [row][k][twin ct] u32, d_out [C][twin ct] u32, both device
  * pointers; `stream` is a cudaStream_t (NULL = legacy default). */

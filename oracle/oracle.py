@@ -286,11 +286,38 @@ class Reference(_Twin):
     def set_weights(self, w):
         w = np.ascontiguousarray(w, np.int64)
         f, cols = w.shape
+        self._wcols = cols
         self._check(self.lib.ref_encode_weights(self._h, _i64p(w), C.c_uint64(f), C.c_uint64(cols), None))
 
     def set_bias(self, bias):
         bias = np.ascontiguousarray(bias, np.int64)
         self._check(self.lib.ref_set_bias(self._h, _i64p(bias), C.c_uint64(len(bias))))
+
+    def encode_weights(self, w: np.ndarray) -> np.ndarray:
+        self._wcols = np.asarray(w).shape[1]
+        return super().encode_weights(w)
+
+    def inputs_wire(self) -> bytes:
+        """The loaded/encoded inputs as the client's HECT blob list."""
+        n = C.c_uint64(0)
+        self._check(self.lib.ref_inputs_wire(self._h, None, C.c_uint64(0), C.byref(n)))
+        out = np.zeros(n.value, np.uint8)
+        self._check(self.lib.ref_inputs_wire(self._h, out.ctypes.data_as(C.POINTER(C.c_uint8)), C.c_uint64(out.size), C.byref(n)))
+        return out.tobytes()
+
+    def server_wire(self, blobs: bytes, rows: int, threads: int = 0):
+        """InferenceServer::do_infer's computation on a blob list; returns
+        (response bytes, seconds)."""
+        buf = np.frombuffer(blobs, np.uint8)
+        n = C.c_uint64(0)
+        secs = C.c_double(0)
+        C_ = (rows * self._wcols + self.n - 1) // self.n
+        cap = C_ * (8 * self.ct_words + 2 * (self.L[0] + self.L[1]) + 38)
+        out = np.zeros(cap, np.uint8)
+        self._check(self.lib.ref_server_wire(self._h, buf.ctypes.data_as(C.POINTER(C.c_uint8)), C.c_uint64(buf.size),
+                                             C.c_uint64(rows), C.c_uint(threads), out.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                             C.c_uint64(cap), C.byref(n), C.byref(secs)))
+        return out[: n.value].tobytes(), secs.value
 
     def matmul(self, R: int, cols: int, threads: int = 0, export: bool = True):
         C_ = (R * cols + self.n - 1) // self.n

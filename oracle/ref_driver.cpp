@@ -20,18 +20,21 @@
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "hei/bfv/backend.hpp"
 #include "hei/bfv/context.hpp"
 #include "hei/bfv/params.hpp"
+#include "hei/bfv/serialize.hpp"
 #include "hei/fpcrt/twin.hpp"
 #include "hei/kernels/modops.hpp"
 #include "hei/matmul/matmul.hpp"
 #include "hei/ring/ntt_tables.hpp"
 #include "hei/ring/poly.hpp"
 #include "hei/util/errors.hpp"
+#include "hei/util/parallel.hpp"
 #include "hei/util/rng.hpp"
 
 using namespace hei;
@@ -429,6 +432,85 @@ int ref_sum_all_slots(void* h, const uint64_t* in, uint64_t* out) {
   auto tc = read_twin(s, in, ring::PolyForm::eval);
   auto r = s.server->sum_all_slots(tc);
   write_twin(s, r, out);
+  return 0;
+  GUARD_END
+}
+
+// The session's inputs as the client sends them: one HECT blob per
+// (row, chunk, branch) from bfv::save_ciphertext (serialize.cpp:63-78),
+// concatenated in request order (client.cpp / server.cpp:145-147).
+int ref_inputs_wire(void* h, uint8_t* out, uint64_t cap, uint64_t* len) {
+  GUARD_BEGIN
+  auto& s = *static_cast<Session*>(h);
+  std::string all;
+  for (const auto& row : s.inputs.rows)
+    for (const auto& ch : row.chunks)
+      for (size_t b = 0; b < 2; ++b) {
+        std::ostringstream os(std::ios::binary);
+        bfv::save_ciphertext(os, std::get<bfv::Ciphertext>(ch.b[b].v), *s.ctx->branch(b));
+        all += os.str();
+      }
+  if (len) *len = all.size();
+  if (out) {
+    if (cap < all.size()) throw ParamError("ref_inputs_wire: buffer too small");
+    std::memcpy(out, all.data(), all.size());
+  }
+  return 0;
+  GUARD_END
+}
+
+// The computation of InferenceServer::do_infer (server.cpp:112-172) on a
+// concatenated blob list: load_ciphertext per blob, MatmulStream over rows
+// with parallel_for, finish, save_ciphertext per packed twin branch.
+int ref_server_wire(void* h, const uint8_t* blobs, uint64_t blob_bytes, uint64_t rows,
+                    unsigned threads, uint8_t* out, uint64_t cap, uint64_t* len,
+                    double* secs) {
+  GUARD_BEGIN
+  auto& s = *static_cast<Session*>(h);
+  const uint32_t n = s.params.n;
+  const uint64_t chunks = (s.weights.f + n - 1) / n;
+  uint64_t bsz[2];
+  for (size_t b = 0; b < 2; ++b) bsz[b] = 19 + 2ull * s.L[b] * (1 + 8ull * n);
+  const uint64_t per_row = chunks * (bsz[0] + bsz[1]);
+  if (rows == 0 || blob_bytes != rows * per_row)
+    throw ParamError("ciphertext count does not match rows x chunks");
+  auto t0 = std::chrono::steady_clock::now();
+  matmul::MatmulStream stream(*s.server, s.weights, s.bias, rows);
+  util::parallel_for(
+      rows,
+      [&](size_t lo, size_t hi) {
+        for (size_t i = lo; i < hi; ++i) {
+          matmul::EncodedInputRow row;
+          const uint8_t* p = blobs + i * per_row;
+          for (uint64_t c = 0; c < chunks; ++c) {
+            fpcrt::TwinCipher ct;
+            for (size_t b = 0; b < 2; ++b) {
+              std::istringstream is(std::string(reinterpret_cast<const char*>(p), bsz[b]),
+                                    std::ios::binary);
+              ct.b.push_back(bfv::HeCipher{bfv::load_ciphertext(is, *s.ctx->branch(b))});
+              p += bsz[b];
+            }
+            row.chunks.push_back(std::move(ct));
+          }
+          stream.push_row(i, row);
+        }
+      },
+      threads);
+  auto packed = stream.finish();
+  std::string all;
+  for (const auto& ct : packed.cts)
+    for (size_t b = 0; b < 2; ++b) {
+      std::ostringstream os(std::ios::binary);
+      bfv::save_ciphertext(os, std::get<bfv::Ciphertext>(ct.b[b].v), *s.ctx->branch(b));
+      all += os.str();
+    }
+  auto t1 = std::chrono::steady_clock::now();
+  if (secs) *secs = std::chrono::duration<double>(t1 - t0).count();
+  if (len) *len = all.size();
+  if (out) {
+    if (cap < all.size()) throw ParamError("ref_server_wire: buffer too small");
+    std::memcpy(out, all.data(), all.size());
+  }
   return 0;
   GUARD_END
 }

@@ -31,6 +31,7 @@ from .matmul import (  # noqa: F401
     encode_weights,
     matmul,
     matmul_device,
+    matmul_wire,
     proposed_counts,
     scale_value,
 )

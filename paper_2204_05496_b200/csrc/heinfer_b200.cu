@@ -242,6 +242,80 @@ __device__ __forceinline__ uint32_t poly_prime(const Geo& g, uint32_t poly) {
   return poly < 2 * L0 ? (poly % L0) : L0 + (poly - 2 * L0) % g.L[1];
 }
 
+// ---------------------------------------------------------------------------
+// HECT wire format (proj/include/hei/bfv/serialize.hpp:18-24,
+// proj/src/bfv/serialize.cpp:19-27,44-48,63-78): a ciphertext blob is
+//   "HECT" | version u16 | params_hash u64 | parts u32 (=2) | kind u8 (=5)
+// followed by 2·L polys [part][prime], each [form u8 | n x u64 LE], coeff form.
+// The 19-byte header makes every u64 unaligned, so the device reads/writes
+// them through aligned 32-bit words and funnel shifts.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kHectHeader = 19;
+
+struct WireGeo {
+  uint64_t blob[2];  // bytes of one branch blob
+  uint64_t hash[2];  // params_hash per branch
+};
+
+__device__ __forceinline__ uint64_t wire_offset(const Geo& g, const WireGeo& wg, uint64_t x, uint32_t& poly,
+                                                uint32_t& j) {
+  const uint64_t ct = x / g.ct_words;
+  const uint32_t w = (uint32_t)(x % g.ct_words);
+  poly = w / g.n;
+  j = w % g.n;
+  const uint32_t b = poly >= 2 * g.L[0];
+  const uint32_t lp = b ? poly - 2 * g.L[0] : poly;
+  return ct * (wg.blob[0] + wg.blob[1]) + (b ? wg.blob[0] : 0) + kHectHeader + (uint64_t)lp * (1 + 8ull * g.n) + 1 +
+         8ull * j;
+}
+
+// bytes (rows·kc twin blobs, padded by >= 8 bytes) -> u32 coeff residues.
+// err bit 1: coefficient >= q; bit 2: a poly's form byte is not coeff.
+__global__ void k_wire_parse(Geo g, WireGeo wg, const uint8_t* __restrict__ in, uint32_t* __restrict__ out,
+                             uint64_t cts, uint32_t* err) {
+  const uint64_t total = cts * g.ct_words;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t poly, j;
+    const uint64_t off = wire_offset(g, wg, x, poly, j);
+    const uint32_t* a = reinterpret_cast<const uint32_t*>(in + (off & ~3ull));
+    const uint32_t sh = (uint32_t)(off & 3) * 8;
+    const uint32_t w0 = __ldg(a), w1 = __ldg(a + 1), w2 = __ldg(a + 2);
+    const uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
+    if (hi != 0 || lo >= g.pr[poly_prime(g, poly)].q) atomicOr(err, 1u);
+    if (j == 0 && in[off - 1] != 0) atomicOr(err, 2u);
+    out[x] = lo;
+  }
+}
+
+// u32 coeff residues (cts twin ciphertexts) -> HECT bytes, headers included.
+__global__ void k_wire_emit(Geo g, WireGeo wg, const uint32_t* __restrict__ in, uint8_t* __restrict__ out,
+                            uint64_t cts) {
+  const uint64_t total = cts * g.ct_words;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t poly, j;
+    const uint64_t off = wire_offset(g, wg, x, poly, j);
+    const uint32_t v = in[x];
+    uint8_t* o = out + off;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = (uint8_t)(v >> (8 * k));
+#pragma unroll
+    for (int k = 4; k < 8; ++k) o[k] = 0;
+    if (j == 0) {
+      o[-1] = 0;  // PolyForm::coeff
+      const uint32_t b = poly >= 2 * g.L[0];
+      if (poly == (b ? 2 * g.L[0] : 0)) {  // first poly of a blob writes the header
+        uint8_t* h = o - 1 - kHectHeader;
+        h[0] = 'H'; h[1] = 'E'; h[2] = 'C'; h[3] = 'T';
+        h[4] = 1; h[5] = 0;  // version
+        for (int k = 0; k < 8; ++k) h[6 + k] = (uint8_t)(wg.hash[b] >> (8 * k));
+        h[14] = 2; h[15] = 0; h[16] = 0; h[17] = 0;  // parts
+        h[18] = 5;                                   // ObjectKind::ciphertext
+      }
+    }
+  }
+}
+
+
 // Forward (or inverse) NTT of whole twin ciphertexts in place: block per poly.
 __global__ void k_ct_ntt(Geo g, uint32_t* __restrict__ cts, int inverse) {
   extern __shared__ uint32_t sm[];
@@ -575,6 +649,26 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T) k_ct_ntt_f(Geo g, uint32_t* __re
   NT::fwd(e, sm, g.fwd + (size_t)gp * NT::N, g.twc + (size_t)gp * g.twc_stride, g.pr[gp].q);
 #pragma unroll
   for (int r = 0; r < 16; ++r) p[x0 + r] = e[r];
+}
+
+// to_coeff of whole twin ciphertexts (context.cpp to_coeff / serialize.cpp:67-71).
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T) k_ct_intt_f(Geo g, uint32_t* __restrict__ cts) {
+  using NT = Ntt<LOGN>;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t polys = 2 * g.P;
+  const uint32_t poly = (uint32_t)(blockIdx.x % polys);
+  const uint32_t gp = poly_prime(g, poly);
+  const PrimeInfo& pr = g.pr[gp];
+  uint32_t* p = cts + (uint64_t)blockIdx.x * NT::N;
+  const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
+  uint32_t e[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) e[r] = p[x0 + r];
+  NT::inv(e, sm, g.inv + (size_t)gp * NT::N, g.itwc + (size_t)gp * g.twc_stride, pr.q, pr.last, pr.ninv);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) p[NT::posA(j, r)] = e[r];
 }
 
 __device__ __forceinline__ void load16(const uint32_t* __restrict__ p, uint32_t (&v)[16]) {
@@ -1597,6 +1691,12 @@ void launch_ct_ntt(hei_gpu_ctx* c, unsigned blocks, uint32_t* cts, cudaStream_t 
                (k_ct_ntt<<<blocks, c->threads(), sm, st>>>(c->geo, cts, 0)));
   LAUNCHED();
 }
+void launch_ct_intt(hei_gpu_ctx* c, unsigned blocks, uint32_t* cts, cudaStream_t st) {
+  const size_t sm = smem_bytes(c, 1);
+  HEI_DISPATCH(c->logn, (k_ct_intt_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(c->geo, cts)),
+               (k_ct_ntt<<<blocks, c->threads(), sm, st>>>(c->geo, cts, 1)));
+  LAUNCHED();
+}
 void launch_poly_ntt(hei_gpu_ctx* c, unsigned blocks, uint32_t gp, uint32_t* polys, int inverse, cudaStream_t st) {
   const size_t sm = smem_bytes(c, 1);
   HEI_DISPATCH(c->logn, (k_poly_ntt_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(c->geo, gp, polys, inverse)),
@@ -1614,6 +1714,7 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
   set_smem_attr((const void*)k_ks_part<LG>, sm);
   set_smem_attr((const void*)k_ct_ntt_f<LG>, sm);
+  set_smem_attr((const void*)k_ct_intt_f<LG>, sm);
   set_smem_attr((const void*)k_poly_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_bl_encode<LG>, sm);
   set_smem_attr((const void*)k_bl_encrypt<LG>, sm);
@@ -2652,66 +2753,175 @@ int hei_gpu_stream_finish(hei_gpu_stream* s, uint64_t* out, hei_op_counters* cnt
 
 void hei_gpu_stream_destroy(hei_gpu_stream* s) { stream_free(s); }
 
+// Host-buffer matmul: rows stream to the device in chunks on a copy stream
+// (double-buffered staging) while earlier chunks are converted and folded on
+// the compute stream, so H2D overlaps the key switching. `wire` selects HECT
+// blobs (server.cpp:112-172) instead of flat u64 residues.
+struct HostIO {
+  const uint64_t* u64 = nullptr;  // flat [row][chunk][twin ct] residues
+  int form = HEI_FORM_EVAL;
+  const uint8_t* wire = nullptr;  // concatenated HECT blobs [row][chunk][branch]
+  WireGeo wg{};
+  uint64_t* out64 = nullptr;
+  uint8_t* out_wire = nullptr;
+};
+
+uint64_t hect_bytes(uint32_t n, uint32_t L) { return kHectHeader + 2ull * L * (1 + 8ull * n); }
+
+// Header checks in the reference's order (serialize.cpp:29-42, 82-84).
+void check_hect_header(const uint8_t* h, uint64_t hash) {
+  if (std::memcmp(h, "HECT", 4) != 0) raise(HEI_CODEC_ERROR, "not a scheme object (bad magic)");
+  uint16_t ver;
+  uint64_t hh;
+  uint32_t parts;
+  std::memcpy(&ver, h + 4, 2);
+  std::memcpy(&hh, h + 6, 8);
+  std::memcpy(&parts, h + 14, 4);
+  if (ver != 1) raise(HEI_CODEC_ERROR, "unsupported object version");
+  if (hh != hash) raise(HEI_CODEC_ERROR, "object was produced under different parameters");
+  if (h[18] != 5) raise(HEI_CODEC_ERROR, "object kind mismatch");
+  if (parts != 2) raise(HEI_CODEC_ERROR, "ciphertext must have two parts");
+}
+
+void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uint64_t rows, const int64_t* bias,
+                 hei_op_counters* cnt) {
+  set_device(c);
+  std::lock_guard<std::mutex> lk(c->mu);
+  std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, bias, rows, false), stream_free);
+  const bool wire = io.wire != nullptr;
+  if (wire)
+    for (uint64_t x = 0; x < rows * w->kc; ++x) {
+      const uint8_t* t = io.wire + x * (io.wg.blob[0] + io.wg.blob[1]);
+      check_hect_header(t, io.wg.hash[0]);
+      check_hect_header(t + io.wg.blob[0], io.wg.hash[1]);
+    }
+  cudaStream_t st = c->stream;
+  if (!c->copy_stream) CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = c->copy_stream;
+  const size_t words = w->kc * c->ct_words();
+  const size_t row_bytes = wire ? w->kc * (io.wg.blob[0] + io.wg.blob[1]) : words * 8;
+  const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(s->cap_rows, (rows + 7) / 8));
+  const uint64_t nchunks = (rows + chunk - 1) / chunk;
+  const size_t slot_bytes = (chunk * row_bytes + 64) & ~(size_t)15;  // + pad for the parser's 12-byte window
+  uint8_t* stage = reinterpret_cast<uint8_t*>(
+      pool_get(c->pool_stage64, c->pool_stage64_bytes, 2 * slot_bytes));
+  uint32_t* in32 = pool_get(c->pool_in32, c->pool_in32_bytes, 2 * chunk * words * 4);
+  uint64_t* d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, rows * 8);
+  k_iota<<<grid_for(rows, 256), 256, 0, st>>>(d_rows, 0, rows);
+  LAUNCHED();
+  cudaEvent_t copied[2], narrowed[2];
+  for (int k = 0; k < 2; ++k) {
+    CU(cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&narrowed[k], cudaEventDisableTiming));
+    CU(cudaEventRecord(narrowed[k], st));
+  }
+  const uint8_t* src = wire ? io.wire : reinterpret_cast<const uint8_t*>(io.u64);
+  for (uint64_t b = 0; b < nchunks; ++b) {
+    const int slot = (int)(b % 2);
+    const uint64_t r0 = b * chunk, nr = std::min<uint64_t>(chunk, rows - r0);
+    uint8_t* sb = stage + (size_t)slot * slot_bytes;
+    uint32_t* s32 = in32 + (size_t)slot * chunk * words;
+    CU(cudaStreamWaitEvent(cs, narrowed[slot], 0));
+    CU(cudaMemcpyAsync(sb, src + r0 * row_bytes, nr * row_bytes, cudaMemcpyHostToDevice, cs));
+    CU(cudaEventRecord(copied[slot], cs));
+    CU(cudaStreamWaitEvent(st, copied[slot], 0));
+    if (wire)
+      k_wire_parse<<<grid_for(nr * words, 256), 256, 0, st>>>(c->geo, io.wg, sb, s32, nr * w->kc, c->d_err);
+    else
+      k_narrow<<<grid_for(nr * words, 256), 256, 0, st>>>(c->geo, reinterpret_cast<const uint64_t*>(sb), s32,
+                                                          nr * w->kc, c->d_err);
+    LAUNCHED();
+    CU(cudaEventRecord(narrowed[slot], st));
+    if (wire || io.form == HEI_FORM_COEFF) launch_ct_ntt(c, (unsigned)(nr * w->kc * 2 * c->P()), s32, st);
+    run_rows(s.get(), s32, d_rows + r0, nr, st);
+  }
+  CU(cudaStreamSynchronize(st));
+  for (int k = 0; k < 2; ++k) {
+    cudaEventDestroy(copied[k]);
+    cudaEventDestroy(narrowed[k]);
+  }
+  {
+    uint32_t h = 0;
+    CU(cudaMemcpy(&h, c->d_err, 4, cudaMemcpyDeviceToHost));
+    if (h) {
+      CU(cudaMemset(c->d_err, 0, 4));
+      raise(HEI_CODEC_ERROR, (h & 2) ? "unexpected polynomial form" : "coefficient not reduced");
+    }
+  }
+  s->pushed = rows;
+  const size_t outw = s->C * c->ct_words();
+  uint32_t* d_out = pool_get(c->pool_out, c->pool_out_bytes, outw * 4);
+  const size_t out_bytes = wire ? s->C * (io.wg.blob[0] + io.wg.blob[1]) : outw * 8;
+  uint64_t* d_out64 = pool_get(c->pool_out64, c->pool_out64_bytes, out_bytes);
+  finish_to(s.get(), d_out, st);
+  if (wire) {
+    // save_ciphertext writes canonical coefficient form (serialize.cpp:67-71)
+    launch_ct_intt(c, (unsigned)(s->C * 2 * c->P()), d_out, st);
+    uint8_t* d_bytes = reinterpret_cast<uint8_t*>(d_out64);
+    k_wire_emit<<<grid_for(outw, 256), 256, 0, st>>>(c->geo, io.wg, d_out, d_bytes, s->C);
+    LAUNCHED();
+    CU(cudaMemcpyAsync(io.out_wire, d_bytes, out_bytes, cudaMemcpyDeviceToHost, st));
+  } else {
+    k_widen<<<grid_for(outw, 256), 256, 0, st>>>(d_out, d_out64, outw);
+    LAUNCHED();
+    CU(cudaMemcpyAsync(io.out64, d_out64, outw * 8, cudaMemcpyDeviceToHost, st));
+  }
+  CU(cudaStreamSynchronize(st));
+  s->finished = true;
+  if (cnt) hei_proposed_counts(rows, w->cols, w->f, c->n, cnt);
+}
+
 int hei_gpu_matmul(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint64_t* inputs, int form, uint64_t rows,
                    const int64_t* bias, uint64_t* out, hei_op_counters* cnt) {
-  // Host-buffer path: rows stream to the device in chunks on a copy stream
-  // (double-buffered u64 staging) while earlier chunks are narrowed and
-  // folded on the compute stream, so H2D overlaps the key switching.
   return guarded([&] {
-    set_device(c);
-    std::lock_guard<std::mutex> lk(c->mu);
     if (form != HEI_FORM_EVAL && form != HEI_FORM_COEFF) raise(HEI_PARAM_ERROR, "matmul: unknown form");
-    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, bias, rows, false), stream_free);
-    cudaStream_t st = c->stream;
-    if (!c->copy_stream) CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-    cudaStream_t cs = c->copy_stream;
-    const size_t words = w->kc * c->ct_words();
-    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(s->cap_rows, (rows + 7) / 8));
-    const uint64_t nchunks = (rows + chunk - 1) / chunk;
-    uint64_t* stage64 = pool_get(c->pool_stage64, c->pool_stage64_bytes, 2 * chunk * words * 8);
-    uint32_t* in32 = pool_get(c->pool_in32, c->pool_in32_bytes, 2 * chunk * words * 4);
-    uint64_t* d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, rows * 8);
-    std::vector<uint64_t> idx(rows);
-    for (uint64_t r = 0; r < rows; ++r) idx[r] = r;
-    CU(cudaMemcpyAsync(d_rows, idx.data(), rows * 8, cudaMemcpyHostToDevice, st));
-    cudaEvent_t copied[2], narrowed[2];
-    for (int k = 0; k < 2; ++k) {
-      CU(cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming));
-      CU(cudaEventCreateWithFlags(&narrowed[k], cudaEventDisableTiming));
-      CU(cudaEventRecord(narrowed[k], st));
+    HostIO io;
+    io.u64 = inputs;
+    io.form = form;
+    io.out64 = out;
+    matmul_host(c, w, io, rows, bias, cnt);
+  });
+}
+
+uint64_t hei_hect_ciphertext_bytes(uint32_t n, uint32_t num_primes) { return hect_bytes(n, num_primes); }
+
+uint64_t hei_params_hash(uint32_t n, uint64_t t, int security_level, const uint64_t* q, uint32_t num_primes) {
+  // FNV-1a over (n, t, security, q...) — EncryptionParams::hash (params.cpp:68-82)
+  uint64_t h = 0xcbf29ce484222325ull;
+  auto mix = [&h](uint64_t v) {
+    for (int i = 0; i < 8; ++i) {
+      h ^= (v >> (8 * i)) & 0xff;
+      h *= 0x100000001b3ull;
     }
-    CU(cudaStreamSynchronize(st));  // zeroed accumulators + row ids in place
-    for (uint64_t b = 0; b < nchunks; ++b) {
-      const int slot = (int)(b % 2);
-      const uint64_t r0 = b * chunk, nr = std::min<uint64_t>(chunk, rows - r0);
-      uint64_t* s64 = stage64 + (size_t)slot * chunk * words;
-      uint32_t* s32 = in32 + (size_t)slot * chunk * words;
-      CU(cudaStreamWaitEvent(cs, narrowed[slot], 0));
-      CU(cudaMemcpyAsync(s64, inputs + r0 * words, nr * words * 8, cudaMemcpyHostToDevice, cs));
-      CU(cudaEventRecord(copied[slot], cs));
-      CU(cudaStreamWaitEvent(st, copied[slot], 0));
-      k_narrow<<<grid_for(nr * words, 256), 256, 0, st>>>(c->geo, s64, s32, nr * w->kc, c->d_err);
-      LAUNCHED();
-      CU(cudaEventRecord(narrowed[slot], st));
-      if (form == HEI_FORM_COEFF) launch_ct_ntt(c, (unsigned)(nr * w->kc * 2 * c->P()), s32, st);
-      run_rows(s.get(), s32, d_rows + r0, nr, st);
-    }
-    CU(cudaStreamSynchronize(st));
-    for (int k = 0; k < 2; ++k) {
-      cudaEventDestroy(copied[k]);
-      cudaEventDestroy(narrowed[k]);
-    }
-    check_err_flag(c, HEI_CODEC_ERROR, "matmul: coefficient not reduced");
-    s->pushed = rows;
-    uint32_t* d_out = pool_get(c->pool_out, c->pool_out_bytes, s->C * c->ct_words() * 4);
-    uint64_t* d_out64 = pool_get(c->pool_out64, c->pool_out64_bytes, s->C * c->ct_words() * 8);
-    finish_to(s.get(), d_out, st);
-    k_widen<<<grid_for(s->C * c->ct_words(), 256), 256, 0, st>>>(d_out, d_out64, s->C * c->ct_words());
-    LAUNCHED();
-    CU(cudaMemcpyAsync(out, d_out64, s->C * c->ct_words() * 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    s->finished = true;
-    if (cnt) hei_proposed_counts(rows, w->cols, w->f, c->n, cnt);
+  };
+  mix(n);
+  mix(t);
+  mix((uint64_t)(int64_t)security_level);
+  for (uint32_t i = 0; i < num_primes; ++i) mix(q[i]);
+  return h;
+}
+
+int hei_gpu_matmul_wire(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint64_t params_hash[2],
+                        const uint8_t* blobs, uint64_t blob_bytes, uint64_t rows, const int64_t* bias,
+                        uint8_t* out, uint64_t out_capacity, uint64_t* out_bytes, hei_op_counters* cnt) {
+  return guarded([&] {
+    if (!w) raise(HEI_PARAM_ERROR, "matmul: empty weights");
+    if (rows == 0) raise(HEI_PARAM_ERROR, "request carries no rows");
+    HostIO io;
+    io.wg.blob[0] = hect_bytes(c->n, c->L[0]);
+    io.wg.blob[1] = hect_bytes(c->n, c->L[1]);
+    io.wg.hash[0] = params_hash[0];
+    io.wg.hash[1] = params_hash[1];
+    const uint64_t per = io.wg.blob[0] + io.wg.blob[1];
+    // server.cpp:131-136: the blob list must be exactly rows x chunks x branches
+    if (blob_bytes % (w->kc * per) != 0 || blob_bytes / (w->kc * per) != rows)
+      raise(HEI_PARAM_ERROR, "ciphertext count does not match rows x chunks");
+    const uint64_t C = (rows * w->cols + c->n - 1) / c->n;
+    if (out_bytes) *out_bytes = C * per;
+    if (out_capacity < C * per) raise(HEI_PARAM_ERROR, "matmul_wire: output buffer too small");
+    io.wire = blobs;
+    io.out_wire = out;
+    matmul_host(c, w, io, rows, bias, cnt);
   });
 }
 

@@ -68,8 +68,9 @@ class GpuTwinServer:
     Galois keys of both branches (no secret material)."""
 
     def __init__(self, n: int, t, L, q, galois_elts, galois_keys, scaling: ScalingConfig = ScalingConfig(),
-                 device: int = 0, public_keys=None):
+                 device: int = 0, public_keys=None, security_level: int = 128):
         self.n = int(n)
+        self.security_level = int(security_level)
         self.t = [int(t[0]), int(t[1])]
         self.L = [int(L[0]), int(L[1])]
         self.q = np.ascontiguousarray(q, dtype=np.uint64)
@@ -99,6 +100,16 @@ class GpuTwinServer:
     @property
     def handle(self):
         return self._h
+
+    def params_hash(self, branch: int) -> int:
+        """BfvContext::hash() of a branch (EncryptionParams::hash, params.cpp:68-82)."""
+        q0 = self.q[: self.L[0]] if branch == 0 else self.q[self.L[0]:]
+        q0 = np.ascontiguousarray(q0, dtype=np.uint64)
+        return int(native.lib().hei_params_hash(self.n, self.t[branch], self.security_level, u64p(q0), len(q0)))
+
+    def hect_bytes(self, branch: int) -> int:
+        """Size of one branch ciphertext blob (serialize.cpp:63-78)."""
+        return int(native.lib().hei_hect_ciphertext_bytes(self.n, self.L[branch]))
 
     def chunks(self, f: int) -> int:
         return (f + self.n - 1) // self.n
@@ -309,3 +320,33 @@ def encode_inputs_device(server: GpuTwinServer, x: np.ndarray, rng0: Prng, rng1:
     R, f = x.shape
     check(native.lib().hei_gpu_encode_inputs_device(server.handle, i64p(x), C.c_uint64(R), C.c_uint64(f), rng0._h, rng1._h,
                                                     C.c_void_p(d_out_ptr), C.c_void_p(stream_ptr)))
+
+
+
+def matmul_wire(server: GpuTwinServer, w: EncodedWeights, blobs, rows: int, bias):
+    """The server's computation on wire objects (InferenceServer::do_infer,
+    server.cpp:112-172): ``blobs`` is the request's HECT ciphertext list
+    concatenated in order [row][chunk][branch]. Returns (response blobs
+    [packed ct][branch] as a list of bytes — save_ciphertext, coeff form —,
+    OpCounters). Parsing, to_eval, the matmul, to_coeff and serialization run
+    on the GPU."""
+    buf = np.frombuffer(blobs, dtype=np.uint8) if isinstance(blobs, (bytes, bytearray)) else np.ascontiguousarray(blobs, np.uint8)
+    bias = np.ascontiguousarray(bias, dtype=np.int64)
+    if bias.size != w.cols:
+        raise ParamError("matmul: bias length does not match output count")
+    hashes = (C.c_uint64 * 2)(server.params_hash(0), server.params_hash(1))
+    b0, b1 = server.hect_bytes(0), server.hect_bytes(1)
+    C_ = (rows * w.cols + server.n - 1) // server.n
+    out = np.zeros(max(C_, 1) * (b0 + b1), np.uint8)
+    out_len = C.c_uint64(0)
+    cnt = OpCounters()
+    u8p = C.POINTER(C.c_uint8)
+    check(native.lib().hei_gpu_matmul_wire(server.handle, w._h, hashes, buf.ctypes.data_as(u8p), C.c_uint64(buf.size),
+                                           C.c_uint64(rows), i64p(bias), out.ctypes.data_as(u8p), C.c_uint64(out.size),
+                                           C.byref(out_len), C.byref(cnt)))
+    res = []
+    for c in range(C_):
+        base = c * (b0 + b1)
+        res.append(bytes(out[base: base + b0]))
+        res.append(bytes(out[base + b0: base + b0 + b1]))
+    return res, cnt

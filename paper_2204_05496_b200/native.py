@@ -99,6 +99,7 @@ EXPORTED = [
     "hei_gpu_kernel_timing", "hei_gpu_kernel_stats", "hei_gpu_measure_butterfly_peak",
     "hei_gpu_matmul_partial_device", "hei_gpu_finish_packed_device",
     "hei_gpu_encode_inputs", "hei_gpu_encode_inputs_device",
+    "hei_hect_ciphertext_bytes", "hei_params_hash", "hei_gpu_matmul_wire",
 ]
 
 _lib = None
@@ -123,6 +124,10 @@ def lib() -> C.CDLL:
         l.hei_gpu_reset_launch_count.restype = None
         l.hei_gpu_set_batch_pairs.restype = None
         l.hei_gpu_set_batch_pairs.argtypes = [C.c_void_p, C.c_uint64]
+        l.hei_hect_ciphertext_bytes.restype = C.c_uint64
+        l.hei_hect_ciphertext_bytes.argtypes = [C.c_uint32, C.c_uint32]
+        l.hei_params_hash.restype = C.c_uint64
+        l.hei_params_hash.argtypes = [C.c_uint32, C.c_uint64, C.c_int, C.POINTER(C.c_uint64), C.c_uint32]
         _lib = l
     return _lib
 

@@ -16,7 +16,8 @@ def gpu_server_from(o, device: int = 0, with_pk: bool = False):
         n0 = 2 * o.L[0] * o.n
         pks = [pk[:n0], pk[n0:]]
     return GpuTwinServer(o.n, (o.p.t0, o.p.t1), o.L, o.q, elts, gk,
-                         ScalingConfig(o.p.s_x, o.p.s_w, o.p.in_bits), device=device, public_keys=pks)
+                         ScalingConfig(o.p.s_x, o.p.s_w, o.p.in_bits), device=device, public_keys=pks,
+                         security_level=o.p.sec)
 
 
 def tiny_params(n: int) -> TwinParams:

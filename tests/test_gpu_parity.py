@@ -393,3 +393,74 @@ def test_device_client_encryption_matches_reference(n, R, f):
     k = (f - 1) // p.n
     tail = x[-1, k * p.n:]
     assert np.array_equal(vals[: tail.size], tail) and budget > 0
+
+
+@pytest.mark.parametrize("n,R,f,cols", [(32, 3, 70, 2), (8192, 3, 9000, 3), (8192, 1, 1000, 11)])
+def test_server_wire_path_byte_identical(n, R, f, cols):
+    """InferenceServer::do_infer (server.cpp:112-172) end to end on wire
+    objects: the request's HECT blobs in, the response blobs out, byte for
+    byte equal to the reference's load_ciphertext -> MatmulStream ->
+    save_ciphertext (serialize.cpp:63-91)."""
+    from oracle.oracle import Reference
+    from paper_2204_05496_b200 import EncodedWeights, matmul_wire
+
+    p = production_params(n) if n >= 8192 else tiny_params(n)
+    ref = Reference(p, key_seed=11, enc_seed=12)
+    s = gpu_server_from(ref)
+    if n >= 8192:
+        x, w, b = synthetic(R, f, cols, 0.05, 0.1, seed=n + R)
+    else:
+        rng = np.random.default_rng(5)
+        x, w, b = random_mat(rng, R, f, 3), random_mat(rng, f, cols, 4), np.arange(cols) - 1
+    ref.encode_inputs(x)
+    blobs = ref.inputs_wire()
+    assert len(blobs) == R * s.chunks(f) * (s.hect_bytes(0) + s.hect_bytes(1))
+    wp = ref.encode_weights(w)
+    ref.set_bias(b)
+    want, _ = ref.server_wire(blobs, R, threads=4)
+    got, cnt = matmul_wire(s, EncodedWeights.from_prepared(s, wp, f), blobs, R, b)
+    assert b"".join(got) == want
+    assert cnt.rotation_count == R * cols * (n.bit_length() - 1)
+
+
+def test_server_wire_errors_match_reference():
+    """serialize.cpp:29-42,50-60 CodecError conditions and the blob-count
+    check of server.cpp:131-136, raised before any result is produced."""
+    from oracle.oracle import OracleError, Reference
+    from paper_2204_05496_b200 import CodecError, EncodedWeights, ParamError, matmul_wire
+
+    p = tiny_params(32)
+    ref = Reference(p, key_seed=11, enc_seed=12)
+    s = gpu_server_from(ref)
+    rng = np.random.default_rng(6)
+    x, w = random_mat(rng, 2, 40, 3), random_mat(rng, 40, 2, 4)
+    b = np.array([1, 2])
+    ref.encode_inputs(x)
+    blobs = bytearray(ref.inputs_wire())
+    wp = ref.encode_weights(w)
+    ref.set_bias(b)
+    ew = EncodedWeights.from_prepared(s, wp, 40)
+    b0 = s.hect_bytes(0)
+
+    def both(buf, exc, msg):
+        with pytest.raises(exc, match=msg):
+            matmul_wire(s, ew, bytes(buf), 2, b)
+        with pytest.raises(OracleError, match=msg):
+            ref.server_wire(bytes(buf), 2)
+
+    bad = bytearray(blobs); bad[b0] = ord("X")  # second blob's magic
+    both(bad, CodecError, "bad magic")
+    bad = bytearray(blobs); bad[6] ^= 1  # params hash
+    both(bad, CodecError, "different parameters")
+    bad = bytearray(blobs); bad[18] = 4  # kind = plaintext
+    both(bad, CodecError, "kind mismatch")
+    q0 = int(ref.q[0])
+    bad = bytearray(blobs); bad[20:28] = q0.to_bytes(8, "little")  # first coefficient = q
+    both(bad, CodecError, "not reduced")
+    bad = bytearray(blobs); bad[19] = 1  # first poly claims eval form
+    both(bad, CodecError, "unexpected polynomial form")
+    both(blobs[:-1], ParamError, "does not match rows x chunks")
+    # the context recovers: a clean call still matches
+    want, _ = ref.server_wire(bytes(blobs), 2)
+    got, _ = matmul_wire(s, ew, bytes(blobs), 2, b)
+    assert b"".join(got) == want

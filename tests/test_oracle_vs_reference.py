@@ -80,3 +80,29 @@ def test_coeff_form_inputs_bit_exact():
     r.set_bias(b)
     rout, _, _ = r.matmul(2, 2)
     assert np.array_equal(out, rout)
+
+
+@pytest.mark.parametrize("n", [32, 8192, 16384])
+def test_wire_constants_match_reference(n):
+    """hei_params_hash == BfvContext::hash() (params.cpp:68-82) and the HECT
+    ciphertext size == save_ciphertext's output length (serialize.cpp:63-78);
+    host-only C-ABI helpers, no device work."""
+    import ctypes as C
+
+    from oracle.oracle import production_params
+    from paper_2204_05496_b200 import native
+    from tests.helpers import tiny_params
+
+    p = production_params(n) if n >= 8192 else tiny_params(n)
+    ref = Reference(p, 1, 2)
+    lib = native.lib()
+    for b, t in enumerate((p.t0, p.t1)):
+        q = np.ascontiguousarray(ref.q[: ref.L[0]] if b == 0 else ref.q[ref.L[0]:], np.uint64)
+        h = lib.hei_params_hash(n, t, p.sec, q.ctypes.data_as(C.POINTER(C.c_uint64)), len(q))
+        assert h == ref.hash[b]
+    x = np.zeros((2, 3), np.int64)
+    ref.encode_inputs(x)
+    blobs = ref.inputs_wire()
+    per = lib.hei_hect_ciphertext_bytes(n, ref.L[0]) + lib.hei_hect_ciphertext_bytes(n, ref.L[1])
+    assert len(blobs) == 2 * per
+    assert blobs[:4] == b"HECT" and blobs[18] == 5
