@@ -10,9 +10,11 @@
 #include <cstdio>
 #include <cstring>
 #include <random>
+#include <sstream>
 #include <string>
 #include <vector>
 
+#include "hei/bfv/serialize.hpp"
 #include "hei/matmul/matmul.hpp"
 #include "hei/util/errors.hpp"
 #include "hei/util/rng.hpp"
@@ -109,6 +111,52 @@ static void run(const fpcrt::TwinParams& p, size_t R, size_t f, size_t cols, con
     for (size_t j = 0; j < cols; ++j) s3 = s3 && same_ct(bref.blocks[blk][j], bgpu.blocks[blk][j]);
   CHECK(s3);
   std::printf("DROPIN %s baseline %s\n", name, s3 ? "bit-exact" : "MISMATCH");
+
+  // server wire path: client blobs (save_ciphertext) -> infer_wire -> blobs,
+  // against the reference's load_ciphertext -> MatmulStream -> save_ciphertext
+  {
+    std::vector<std::string> blobs;
+    for (const auto& row : ex.rows)
+      for (const auto& ch : row.chunks)
+        for (size_t b = 0; b < 2; ++b)
+          blobs.push_back(bfv::to_bytes(std::get<bfv::Ciphertext>(ch.b[b].v), *ctx.branch(b),
+                                        [](std::ostream& os, const bfv::Ciphertext& c, const bfv::BfvContext& cx) {
+                                          bfv::save_ciphertext(os, c, cx);
+                                        }));
+    matmul::MatmulStream rs(*server, ew, bias, R);
+    const size_t k = ex.rows[0].chunks.size();
+    for (size_t i = 0; i < R; ++i) {
+      matmul::EncodedInputRow row;
+      for (size_t c = 0; c < k; ++c) {
+        fpcrt::TwinCipher tc;
+        for (size_t b = 0; b < 2; ++b) {
+          std::istringstream is(blobs[(i * k + c) * 2 + b], std::ios::binary);
+          tc.b.push_back(bfv::HeCipher{bfv::load_ciphertext(is, *ctx.branch(b))});
+        }
+        row.chunks.push_back(std::move(tc));
+      }
+      rs.push_row(i, row);
+    }
+    auto rp = rs.finish();
+    std::vector<std::string> want;
+    for (const auto& ct : rp.cts)
+      for (size_t b = 0; b < 2; ++b) {
+        std::ostringstream os(std::ios::binary);
+        bfv::save_ciphertext(os, std::get<bfv::Ciphertext>(ct.b[b].v), *ctx.branch(b));
+        want.push_back(os.str());
+      }
+    auto got = matmul::gpu::infer_wire(*server, blobs, R, ew, bias);
+    CHECK(got == want);
+    blobs[1][0] = 'X';
+    bool codec = false;
+    try {
+      matmul::gpu::infer_wire(*server, blobs, R, ew, bias);
+    } catch (const CodecError&) {
+      codec = true;
+    }
+    CHECK(codec);
+    std::printf("DROPIN %s wire %s\n", name, got == want ? "byte-identical" : "MISMATCH");
+  }
 
   // error contract: no rotation keys -> KeyError (test_matmul.cpp:410-414)
   auto norot = ctx.client_backend(keys, 3, false);

@@ -278,3 +278,44 @@ BaselineResult baseline_matmul(fpcrt::TwinBackend& be, const std::vector<bfv::Pu
 }
 
 }  // namespace hei::matmul::gpu
+
+namespace hei::matmul::gpu {
+
+std::vector<std::string> infer_wire(fpcrt::TwinBackend& be, const std::vector<std::string>& ct_blobs, uint64_t rows,
+                                    const EncodedWeights& w, const EncodedBias& b, OpCounters* counters) {
+  auto& sess = DeviceSession::for_backend(be);
+  hei_gpu_weights* hw = sess.weights(w);
+  uint64_t hash[2], bytes[2];
+  for (size_t br = 0; br < 2; ++br) {
+    const auto& cx = bfv_branch(be, br).context();
+    hash[br] = cx.hash();
+    bytes[br] = hei_hect_ciphertext_bytes(cx.n(), (uint32_t)cx.num_primes());
+  }
+  // Concatenate. load_ciphertext reads exactly one object from each blob:
+  // a short blob fails with util::read_bytes's CodecError (io.hpp:26-30),
+  // trailing bytes are ignored.
+  std::string all;
+  all.reserve(ct_blobs.size() * (bytes[0] + bytes[1]) / 2);
+  for (size_t i = 0; i < ct_blobs.size(); ++i) {
+    if (ct_blobs[i].size() < bytes[i % 2]) throw CodecError("unexpected end of stream");
+    all.append(ct_blobs[i], 0, bytes[i % 2]);
+  }
+  const uint64_t cols = w.outputs.size();
+  const uint64_t C = rows ? (rows * cols + w.n - 1) / w.n : 0;
+  std::vector<uint8_t> out(std::max<uint64_t>(C, 1) * (bytes[0] + bytes[1]));
+  uint64_t out_len = 0;
+  hei_op_counters hc{};
+  check(hei_gpu_matmul_wire(sess.ctx(), hw, hash, reinterpret_cast<const uint8_t*>(all.data()), all.size(), rows,
+                            b.scaled.data(), out.data(), out.size(), &out_len, &hc));
+  std::vector<std::string> res;
+  const uint8_t* p = out.data();
+  for (uint64_t c = 0; c < C; ++c)
+    for (size_t br = 0; br < 2; ++br) {
+      res.emplace_back(reinterpret_cast<const char*>(p), bytes[br]);
+      p += bytes[br];
+    }
+  if (counters) *counters = to_counters(hc);
+  return res;
+}
+
+}  // namespace hei::matmul::gpu

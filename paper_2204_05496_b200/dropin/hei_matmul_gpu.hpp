@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <memory>
 #include <span>
+#include <string>
 #include <vector>
 
 #include "hei/bfv/keys.hpp"
@@ -77,5 +78,13 @@ class MatmulStream {
 BaselineResult baseline_matmul(fpcrt::TwinBackend& be, const std::vector<bfv::PublicKey>& pub, uint64_t rng_seed,
                                const util::IntMat& x, const util::IntMat& w, const EncodedBias& b,
                                OpCounters* counters = nullptr);
+
+// The computation of InferenceServer::do_infer (server.cpp:137-170) on wire
+// objects: `ct_blobs` = the request's HECT ciphertext blobs in request order
+// [row][chunk][branch] (InferRequestPayload::ct_blobs); returns the response
+// blobs [packed ct][branch] as bfv::save_ciphertext would write them.
+// load_ciphertext's CodecErrors and the blob-count check are preserved.
+std::vector<std::string> infer_wire(fpcrt::TwinBackend& be, const std::vector<std::string>& ct_blobs, uint64_t rows,
+                                    const EncodedWeights& w, const EncodedBias& b, OpCounters* counters = nullptr);
 
 }  // namespace hei::matmul::gpu
