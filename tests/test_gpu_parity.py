@@ -464,3 +464,20 @@ def test_server_wire_errors_match_reference():
     want, _ = ref.server_wire(bytes(blobs), 2)
     got, _ = matmul_wire(s, ew, bytes(blobs), 2, b)
     assert b"".join(got) == want
+
+
+def test_n16384_c5_shape_bit_exact():
+    """C5's ring (N = 16384, t1' = 163841, 14 rotations, 1024-thread NTTs)
+    on a small shape: 2 individuals x 20,000 features (2 chunks) x 3 classes."""
+    from paper_2204_05496_b200 import EncodedWeights, matmul
+
+    o = Oracle(production_params(16384), key_seed=1, enc_seed=2)
+    s = gpu_server_from(o)
+    x, w, b = synthetic(2, 20000, 3, 0.03, 0.05, seed=16)
+    inputs = o.encode_inputs(x)
+    wp = o.encode_weights(w)
+    want, _ = o.fast_matmul(inputs, 20000, wp, b)
+    got, cnt = matmul(s, inputs, EncodedWeights.from_prepared(s, wp, 20000), b)
+    assert np.array_equal(got, want)
+    assert np.array_equal(o.unpack(got, 2, 3), oracle_matmul(x, w, b))
+    assert cnt.rotation_count == 2 * 3 * 14
