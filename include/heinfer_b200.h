@@ -95,6 +95,25 @@ int hei_gpu_matmul(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint64_t* i
                    int form, uint64_t rows, const int64_t* bias, uint64_t* out,
                    hei_op_counters* counters);
 
+/* Client-side decryption on the device. The secret key
+ * of branch b is SecretKey::s (ternary int8 [N], keys.hpp). decrypt_core
+ * (context.cpp:316-370) with an exact multi-limb CRT per coefficient,
+ * decode_slots (context.cpp:95-102) and crt_recombine (fixed_point.cpp:89-106).
+ *   decrypt_signed: out [count][N] = TwinBackend::decrypt_signed per ct;
+ *                   HEI_NOISE_ERROR when a branch budget is exhausted.
+ *   noise_budget:   budgets [count] = TwinBackend::noise_budget (min of branches).
+ *   unpack_results: matmul::unpack_results (matmul.cpp:257-271), packed eval
+ *                   cts [count][twin ct] -> out [rows][cols].
+ *   unpack_baseline: matmul::unpack_baseline (matmul.cpp:346-358), blocks
+ *                   [ceil(rows/N)][cols][twin ct] -> out [rows][cols]. */
+int hei_gpu_upload_secret_key(hei_gpu_ctx* ctx, uint32_t branch, const int8_t* s);
+int hei_gpu_decrypt_signed(hei_gpu_ctx* ctx, const uint64_t* cts, int form, uint64_t count, int64_t* out);
+int hei_gpu_noise_budget(hei_gpu_ctx* ctx, const uint64_t* cts, int form, uint64_t count, int* budgets);
+int hei_gpu_unpack_results(hei_gpu_ctx* ctx, const uint64_t* packed, uint64_t count, uint64_t rows,
+                           uint64_t cols, int64_t* out);
+int hei_gpu_unpack_baseline(hei_gpu_ctx* ctx, const uint64_t* blocks, uint64_t rows, uint64_t cols,
+                            int64_t* out);
+
 /* Server wire path (InferenceServer::do_infer, server.cpp:112-172): the
  * request's HECT ciphertext blobs (bfv::load_ciphertext, serialize.cpp:80-91;
  * coeff form) concatenated in request order [row][chunk][branch], each branch-b

@@ -1441,6 +1441,8 @@ __global__ void __launch_bounds__(256) k_bfly_peak(uint32_t* __restrict__ sink, 
   if (acc == 0xFFFFFFFFu) sink[blockIdx.x] = acc;
 }
 
+#include "decrypt.cuh"
+
 }  // namespace
 
 // ================================================================ host side
@@ -1465,6 +1467,10 @@ struct hei_gpu_ctx {
   bool has_keys[2] = {false, false};
   uint64_t* d_pk[2] = {nullptr, nullptr};
   uint2* d_pkp = nullptr;  // prepared public key [gp][part] (baseline)
+  uint32_t* d_sk_hat = nullptr;  // NTT(lift(s)) per prime [P][n] (client decryption)
+  bool has_sk[2] = {false, false};
+  CrtInfo crt{};                 // exact CRT constants per branch (decrypt_core)
+  uint32_t t0inv = 0;            // t0^-1 mod t1 (crt_recombine)
   uint32_t* d_err = nullptr;
   cudaStream_t stream = nullptr;
   uint64_t batch_pairs = 0;
@@ -2462,6 +2468,46 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
         pos = (pos * 3) % m;
       }
     }
+    // exact CRT constants (context.cpp:35-48) in 8 x 32-bit limbs
+    for (uint32_t b = 0; b < 2; ++b) {
+      CrtBranch& cb = c->crt.b[b];
+      const uint32_t first = b ? c->L[0] : 0;
+      if (c->L[b] > (uint32_t)kMaxBranchPrimes) raise(HEI_PARAM_ERROR, "too many primes in one branch");
+      cb.L = c->L[b];
+      cb.t = (uint32_t)c->t[b];
+      auto mul_small = [](uint32_t (&a)[kLimbs], uint64_t m) {
+        uint64_t carry = 0;
+        for (int k = 0; k < kLimbs; ++k) {
+          const u128 v = (u128)a[k] * m + carry;
+          a[k] = (uint32_t)v;
+          carry = (uint64_t)(v >> 32);
+        }
+        if (carry) raise(HEI_PARAM_ERROR, "ciphertext modulus too wide for the device CRT");
+      };
+      std::fill(cb.Q, cb.Q + kLimbs, 0u);
+      cb.Q[0] = 1;
+      for (uint32_t i = 0; i < cb.L; ++i) mul_small(cb.Q, d->q[first + i]);
+      for (uint32_t i = 0; i < cb.L; ++i) {
+        cb.q[i] = (uint32_t)d->q[first + i];
+        std::fill(cb.Qp[i], cb.Qp[i] + kLimbs, 0u);
+        cb.Qp[i][0] = 1;
+        uint64_t pm = 1;
+        for (uint32_t k = 0; k < cb.L; ++k)
+          if (k != i) {
+            mul_small(cb.Qp[i], d->q[first + k]);
+            pm = mulmod(pm, d->q[first + k] % d->q[first + i], d->q[first + i]);
+          }
+        cb.y[i] = (uint32_t)invmod(pm, d->q[first + i]);
+      }
+      for (int k = 0; k < kLimbs; ++k) cb.Qh[k] = (cb.Q[k] >> 1) | (k + 1 < kLimbs ? (cb.Q[k + 1] << 31) : 0u);
+      cb.q_msb = -1;
+      for (int k = kLimbs - 1; k >= 0 && cb.q_msb < 0; --k)
+        if (cb.Q[k]) cb.q_msb = 32 * k + 31 - __builtin_clz(cb.Q[k]);
+      if (cb.q_msb > 32 * kLimbs - 34) raise(HEI_PARAM_ERROR, "ciphertext modulus too wide for the device CRT");
+      cb.Qd = 0.0;
+      for (int k = kLimbs - 1; k >= 0; --k) cb.Qd = cb.Qd * 4294967296.0 + (double)cb.Q[k];
+    }
+    c->t0inv = (uint32_t)invmod(c->t[0] % c->t[1], c->t[1]);
     // fold elements and their eval permutations (poly.cpp:124-138)
     for (uint32_t s = 1; s <= n / 4; s <<= 1) c->fold_elts.push_back(powmod(3, s, two_n));
     c->fold_elts.push_back(two_n - 1);
@@ -2535,6 +2581,9 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     set_smem_attr((const void*)k_bl_encode_g, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_bl_encrypt_g, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_prepare_pk_g, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_dec_phase, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_dec_decode, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_prepare_sk, smem_bytes(c.get(), 1));
     if (c->logn == 12) set_fast_attrs<12>(smem_bytes(c.get(), 1));
     if (c->logn == 13) set_fast_attrs<13>(smem_bytes(c.get(), 1));
     if (c->logn == 14) set_fast_attrs<14>(smem_bytes(c.get(), 1));
@@ -2557,6 +2606,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
     cudaFree(c->d_pk[b]);
   }
   cudaFree(c->d_pkp);
+  cudaFree(c->d_sk_hat);
   cudaFree(c->pool_acc);
   cudaFree(c->pool_rows);
   cudaFree(c->pool_bias);
@@ -2680,6 +2730,137 @@ int hei_gpu_upload_public_key(hei_gpu_ctx* c, uint32_t b, const uint64_t* pk) {
       c->d_pkp = nullptr;
     }
     CU(cudaMemcpy(c->d_pk[b], pk, words * 8, cudaMemcpyHostToDevice));
+  });
+}
+
+int hei_gpu_upload_secret_key(hei_gpu_ctx* c, uint32_t b, const int8_t* s) {
+  return guarded([&] {
+    if (b > 1) raise(HEI_PARAM_ERROR, "branch out of range");
+    for (uint32_t x = 0; x < c->n; ++x)
+      if (s[x] < -1 || s[x] > 1) raise(HEI_CODEC_ERROR, "secret key residue is not ternary");
+    set_device(c);
+    if (!c->d_sk_hat) CU(cudaMalloc(&c->d_sk_hat, (size_t)c->P() * c->n * 4));
+    int8_t* d_s = nullptr;
+    CU(cudaMalloc(&d_s, c->n));
+    CU(cudaMemcpy(d_s, s, c->n, cudaMemcpyHostToDevice));
+    k_prepare_sk<<<c->L[b], c->threads(), smem_bytes(c, 1), c->stream>>>(c->geo, b, d_s, c->d_sk_hat);
+    LAUNCHED();
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(d_s);
+    c->has_sk[b] = true;
+  });
+}
+
+// decrypt_core + decode_signed over `count` twin ciphertexts already on the
+// device (u32, eval form); budgets[ct][2] per branch; `out` on the device.
+void decrypt_device(hei_gpu_ctx* c, uint32_t* d_cts, uint64_t count, int mode, uint64_t rows, uint64_t cols,
+                    int64_t* d_out, std::vector<int>& budgets, cudaStream_t st) {
+  if (!c->has_sk[0] || !c->has_sk[1]) raise(HEI_KEY_ERROR, "decrypt: this backend holds no secret key");
+  const uint32_t n = c->n;
+  uint32_t *d_w = nullptr, *d_m = nullptr;
+  int* d_msb = nullptr;
+  CU(cudaMallocAsync(&d_w, count * c->P() * n * 4, st));
+  CU(cudaMallocAsync(&d_m, count * 2 * n * 4, st));
+  CU(cudaMallocAsync(&d_msb, count * 2 * sizeof(int), st));
+  CU(cudaMemsetAsync(d_msb, 0xff, count * 2 * sizeof(int), st));  // -1: all-zero residual
+  k_dec_phase<<<(unsigned)(count * c->P()), c->threads(), smem_bytes(c, 1), st>>>(c->geo, d_cts, c->d_sk_hat, d_w);
+  LAUNCHED();
+  k_dec_crt<<<grid_for(count * 2 * n, 256), 256, 0, st>>>(c->geo, c->crt, d_w, count, d_m, d_msb);
+  LAUNCHED();
+  k_dec_decode<<<(unsigned)(count * 2), c->threads(), smem_bytes(c, 1), st>>>(c->geo, d_m, d_w);
+  LAUNCHED();
+  std::vector<int> msb(count * 2);
+  CU(cudaMemcpyAsync(msb.data(), d_msb, count * 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  budgets.resize(count * 2);
+  for (uint64_t x = 0; x < count * 2; ++x) {
+    const int q_msb = c->crt.b[x % 2].q_msb;
+    int bud = msb[x] < 0 ? q_msb - 1 : q_msb - (msb[x] + 1);  // msb(max_r << 1)
+    budgets[x] = bud < 0 ? 0 : bud;
+  }
+  if (d_out) {
+    k_dec_recombine<<<grid_for(count * n, 256), 256, 0, st>>>(c->geo, d_w, count, rows, cols, mode, c->t0inv, d_out);
+    LAUNCHED();
+  }
+  CU(cudaFreeAsync(d_w, st));
+  CU(cudaFreeAsync(d_m, st));
+  CU(cudaFreeAsync(d_msb, st));
+}
+
+// Host twin ciphertexts (u64, `form`) -> device u32 eval form.
+uint32_t* stage_cts(hei_gpu_ctx* c, const uint64_t* cts, int form, uint64_t count, cudaStream_t st) {
+  if (form != HEI_FORM_EVAL && form != HEI_FORM_COEFF) raise(HEI_PARAM_ERROR, "decrypt: unknown form");
+  const size_t words = count * c->ct_words();
+  uint64_t* d64 = nullptr;
+  uint32_t* d32 = nullptr;
+  CU(cudaMallocAsync(&d64, words * 8, st));
+  CU(cudaMallocAsync(&d32, words * 4, st));
+  CU(cudaMemcpyAsync(d64, cts, words * 8, cudaMemcpyHostToDevice, st));
+  k_narrow<<<grid_for(words, 256), 256, 0, st>>>(c->geo, d64, d32, count, c->d_err);
+  LAUNCHED();
+  if (form == HEI_FORM_COEFF) launch_ct_ntt(c, (unsigned)(count * 2 * c->P()), d32, st);
+  CU(cudaFreeAsync(d64, st));
+  CU(cudaStreamSynchronize(st));
+  uint32_t h = 0;
+  CU(cudaMemcpy(&h, c->d_err, 4, cudaMemcpyDeviceToHost));
+  if (h) {
+    CU(cudaMemset(c->d_err, 0, 4));
+    cudaFree(d32);
+    raise(HEI_CODEC_ERROR, "decrypt: coefficient not reduced");
+  }
+  return d32;
+}
+
+void decrypt_host(hei_gpu_ctx* c, const uint64_t* cts, int form, uint64_t count, int mode, uint64_t rows,
+                  uint64_t cols, int64_t* out, size_t out_words, int* budgets, bool throw_noise) {
+  set_device(c);
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->has_sk[0] || !c->has_sk[1]) raise(HEI_KEY_ERROR, "decrypt: this backend holds no secret key");
+  cudaStream_t st = c->stream;
+  uint32_t* d32 = stage_cts(c, cts, form, count, st);
+  int64_t* d_out = nullptr;
+  if (out) CU(cudaMallocAsync(&d_out, out_words * 8, st));
+  std::vector<int> bud;
+  try {
+    decrypt_device(c, d32, count, mode, rows, cols, d_out, bud, st);
+  } catch (...) {
+    cudaFree(d32);
+    if (d_out) cudaFree(d_out);
+    throw;
+  }
+  if (out) CU(cudaMemcpyAsync(out, d_out, out_words * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  cudaFree(d32);
+  if (d_out) cudaFree(d_out);
+  if (budgets)
+    for (uint64_t x = 0; x < count; ++x) budgets[x] = std::min(bud[2 * x], bud[2 * x + 1]);
+  if (throw_noise)  // BfvContext::decrypt (context.cpp:372-377), branch 0 first
+    for (uint64_t x = 0; x < 2 * count; ++x)
+      if (bud[x] <= 0) raise(HEI_NOISE_ERROR, "decrypt: invariant noise budget exhausted");
+}
+
+int hei_gpu_decrypt_signed(hei_gpu_ctx* c, const uint64_t* cts, int form, uint64_t count, int64_t* out) {
+  return guarded([&] { decrypt_host(c, cts, form, count, 2, 0, 0, out, count * c->n, nullptr, true); });
+}
+
+int hei_gpu_noise_budget(hei_gpu_ctx* c, const uint64_t* cts, int form, uint64_t count, int* budgets) {
+  return guarded([&] { decrypt_host(c, cts, form, count, 2, 0, 0, nullptr, 0, budgets, false); });
+}
+
+int hei_gpu_unpack_results(hei_gpu_ctx* c, const uint64_t* packed, uint64_t count, uint64_t rows, uint64_t cols,
+                           int64_t* out) {
+  return guarded([&] {
+    if (rows == 0 || cols == 0) raise(HEI_PARAM_ERROR, "unpack: empty result");
+    if (count != (rows * cols + c->n - 1) / c->n) raise(HEI_PARAM_ERROR, "unpack: ciphertext count does not match layout");
+    decrypt_host(c, packed, HEI_FORM_EVAL, count, 0, rows, cols, out, rows * cols, nullptr, true);
+  });
+}
+
+int hei_gpu_unpack_baseline(hei_gpu_ctx* c, const uint64_t* blocks, uint64_t rows, uint64_t cols, int64_t* out) {
+  return guarded([&] {
+    if (rows == 0 || cols == 0) raise(HEI_PARAM_ERROR, "unpack: empty result");
+    const uint64_t nb = (rows + c->n - 1) / c->n;
+    decrypt_host(c, blocks, HEI_FORM_EVAL, nb * cols, 1, rows, cols, out, rows * cols, nullptr, true);
   });
 }
 

@@ -107,6 +107,43 @@ class GpuTwinServer:
         q0 = np.ascontiguousarray(q0, dtype=np.uint64)
         return int(native.lib().hei_params_hash(self.n, self.t[branch], self.security_level, u64p(q0), len(q0)))
 
+    # ---- client role (decryption), SURVEY §8(f) row 3 ----
+    def upload_secret_keys(self, sk) -> None:
+        """SecretKey::s of both branches, ternary int8 [2][N]."""
+        sk = np.ascontiguousarray(sk, dtype=np.int8).reshape(2, self.n)
+        for b in range(2):
+            check(native.lib().hei_gpu_upload_secret_key(self._h, C.c_uint32(b), sk[b].ctypes.data_as(C.POINTER(C.c_int8))))
+
+    def decrypt_signed(self, cts: np.ndarray, form: int = FORM_EVAL) -> np.ndarray:
+        """TwinBackend::decrypt_signed per twin ciphertext: [count][N] int64."""
+        cts = np.ascontiguousarray(cts, dtype=np.uint64).reshape(-1, self.ct_words)
+        out = np.zeros((cts.shape[0], self.n), np.int64)
+        check(native.lib().hei_gpu_decrypt_signed(self._h, u64p(cts), C.c_int(form), C.c_uint64(cts.shape[0]), i64p(out)))
+        return out
+
+    def noise_budget(self, cts: np.ndarray, form: int = FORM_EVAL) -> np.ndarray:
+        """TwinBackend::noise_budget per twin ciphertext."""
+        cts = np.ascontiguousarray(cts, dtype=np.uint64).reshape(-1, self.ct_words)
+        out = np.zeros(cts.shape[0], np.int32)
+        check(native.lib().hei_gpu_noise_budget(self._h, u64p(cts), C.c_int(form), C.c_uint64(cts.shape[0]),
+                                                out.ctypes.data_as(C.POINTER(C.c_int))))
+        return out
+
+    def unpack_results(self, packed: np.ndarray, rows: int, cols: int) -> np.ndarray:
+        """matmul::unpack_results (matmul.cpp:257-271)."""
+        packed = np.ascontiguousarray(packed, dtype=np.uint64).reshape(-1, self.ct_words)
+        out = np.zeros((rows, cols), np.int64)
+        check(native.lib().hei_gpu_unpack_results(self._h, u64p(packed), C.c_uint64(packed.shape[0]), C.c_uint64(rows),
+                                                  C.c_uint64(cols), i64p(out)))
+        return out
+
+    def unpack_baseline(self, blocks: np.ndarray, rows: int, cols: int) -> np.ndarray:
+        """matmul::unpack_baseline (matmul.cpp:346-358)."""
+        blocks = np.ascontiguousarray(blocks, dtype=np.uint64)
+        out = np.zeros((rows, cols), np.int64)
+        check(native.lib().hei_gpu_unpack_baseline(self._h, u64p(blocks), C.c_uint64(rows), C.c_uint64(cols), i64p(out)))
+        return out
+
     def hect_bytes(self, branch: int) -> int:
         """Size of one branch ciphertext blob (serialize.cpp:63-78)."""
         return int(native.lib().hei_hect_ciphertext_bytes(self.n, self.L[branch]))

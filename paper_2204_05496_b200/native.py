@@ -100,6 +100,8 @@ EXPORTED = [
     "hei_gpu_matmul_partial_device", "hei_gpu_finish_packed_device",
     "hei_gpu_encode_inputs", "hei_gpu_encode_inputs_device",
     "hei_hect_ciphertext_bytes", "hei_params_hash", "hei_gpu_matmul_wire",
+    "hei_gpu_upload_secret_key", "hei_gpu_decrypt_signed", "hei_gpu_noise_budget",
+    "hei_gpu_unpack_results", "hei_gpu_unpack_baseline",
 ]
 
 _lib = None

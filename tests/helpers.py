@@ -7,7 +7,7 @@ import numpy as np
 from oracle.oracle import T0, T1, Oracle, TwinParams, production_params  # noqa: F401
 
 
-def gpu_server_from(o, device: int = 0, with_pk: bool = False):
+def gpu_server_from(o, device: int = 0, with_pk: bool = False, with_sk: bool = False):
     from paper_2204_05496_b200 import GpuTwinServer, ScalingConfig
 
     elts, gk, sk, pk = o.galois_keys()
@@ -15,9 +15,12 @@ def gpu_server_from(o, device: int = 0, with_pk: bool = False):
     if with_pk:
         n0 = 2 * o.L[0] * o.n
         pks = [pk[:n0], pk[n0:]]
-    return GpuTwinServer(o.n, (o.p.t0, o.p.t1), o.L, o.q, elts, gk,
+    srv = GpuTwinServer(o.n, (o.p.t0, o.p.t1), o.L, o.q, elts, gk,
                          ScalingConfig(o.p.s_x, o.p.s_w, o.p.in_bits), device=device, public_keys=pks,
                          security_level=o.p.sec)
+    if with_sk:
+        srv.upload_secret_keys(sk)
+    return srv
 
 
 def tiny_params(n: int) -> TwinParams:

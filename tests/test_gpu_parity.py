@@ -481,3 +481,91 @@ def test_n16384_c5_shape_bit_exact():
     assert np.array_equal(got, want)
     assert np.array_equal(o.unpack(got, 2, 3), oracle_matmul(x, w, b))
     assert cnt.rotation_count == 2 * 3 * 14
+
+
+def _coeff_cts_from_wire(blob: bytes, count: int, n: int, L):
+    """Twin coeff-form u64 ciphertexts from concatenated HECT blobs."""
+    per = [19 + 2 * L[b] * (1 + 8 * n) for b in range(2)]
+    out = np.zeros((count, 2 * (L[0] + L[1]) * n), np.uint64)
+    off = 0
+    for c in range(count):
+        w = 0
+        for b in range(2):
+            body = np.frombuffer(blob[off + 19: off + per[b]], np.uint8).reshape(2 * L[b], 1 + 8 * n)
+            out[c, w: w + 2 * L[b] * n] = np.ascontiguousarray(body[:, 1:]).view("<u8").reshape(-1)
+            w += 2 * L[b] * n
+            off += per[b]
+    return out
+
+
+@pytest.mark.parametrize("n", [32, 8192, 16384])
+def test_device_decryption_matches_reference(n):
+    """decrypt_core (context.cpp:316-370, exact CRT + rounding + noise
+    residual), decode_slots and crt_recombine on the device: same slots and
+    same noise budget as the reference, eval and coeff form; an exhausted
+    budget raises NoiseError (context.cpp:372-377)."""
+    from oracle.oracle import OracleError, Reference
+    from paper_2204_05496_b200 import FORM_COEFF, NoiseError
+
+    p = production_params(n) if n >= 8192 else tiny_params(n)
+    ref = Reference(p, key_seed=21, enc_seed=22)
+    s = gpu_server_from(ref, with_sk=True)
+    rng = np.random.default_rng(n)
+    mag = 3 if n == 32 else 10 ** 6
+    x = random_mat(rng, 3, n, mag)
+    cts = ref.encode_inputs(x)[:, 0]
+    got = s.decrypt_signed(cts)
+    buds = s.noise_budget(cts)
+    for r in range(3):
+        want, bud = ref.decrypt_signed(cts[r])
+        assert np.array_equal(got[r], want)
+        assert np.array_equal(got[r], x[r])
+        assert buds[r] == bud
+    coeff = _coeff_cts_from_wire(ref.inputs_wire(), 3, n, ref.L)
+    gotc = s.decrypt_signed(coeff, form=FORM_COEFF)
+    for r in range(3):
+        want, bud = ref.decrypt_signed(coeff[r], form=0)
+        assert np.array_equal(gotc[r], want)
+        assert s.noise_budget(coeff[r:r + 1], form=FORM_COEFF)[0] == bud
+    # uniformly random "ciphertext": no noise budget left
+    junk = cts[:1].copy()
+    for poly in range(2 * (ref.L[0] + ref.L[1])):
+        b_ = 0 if poly < 2 * ref.L[0] else 1
+        i = poly % ref.L[0] if b_ == 0 else (poly - 2 * ref.L[0]) % ref.L[1]
+        q = int(ref.q[(ref.L[0] if b_ else 0) + i])
+        junk[0, poly * n:(poly + 1) * n] = rng.integers(0, q, size=n, dtype=np.uint64)
+    assert s.noise_budget(junk)[0] == 0
+    with pytest.raises(NoiseError):
+        s.decrypt_signed(junk)
+    with pytest.raises(OracleError, match="noise budget"):
+        ref.decrypt_signed(junk[0])
+
+
+@pytest.mark.parametrize("which", ["tiny32", "prod"])
+def test_device_unpack_results_and_baseline(which, request):
+    """unpack_results (matmul.cpp:257-271) of the packed matmul output and
+    unpack_baseline (:346-358) of the standard algorithm's blocks, decrypted
+    on the device, equal the integer product."""
+    from paper_2204_05496_b200 import EncodedWeights, KeyError_, Prng, baseline_matmul, matmul
+
+    o, _ = request.getfixturevalue(which)
+    s = gpu_server_from(o, with_pk=True, with_sk=True)
+    rng = np.random.default_rng(77)
+    if which == "tiny32":
+        R, f, cols, mag, wmag = 20, 30, 3, 8, 8
+    else:
+        R, f, cols, mag, wmag = 3, 9000, 11, 64, 3000
+    x = random_mat(rng, R, f, mag)
+    w = random_mat(rng, f, cols, wmag)
+    b = rng.integers(-1000, 1001, size=cols)
+    packed, _ = matmul(s, o.encode_inputs(x), EncodedWeights.from_prepared(s, o.encode_weights(w), f), b)
+    assert np.array_equal(s.unpack_results(packed, R, cols), oracle_matmul(x, w, b))
+    assert np.array_equal(s.unpack_results(packed, R, cols), o.unpack(packed, R, cols))
+    fb = min(f, 12)
+    blocks, _ = baseline_matmul(s, x[:, :fb], w[:fb], b, Prng(5), Prng(6))
+    # whatever randomness was used, decryption is exact
+    assert np.array_equal(s.unpack_baseline(blocks, R, cols), oracle_matmul(x[:, :fb], w[:fb], b))
+    assert np.array_equal(s.unpack_baseline(blocks, R, cols), o.unpack_baseline(blocks, R, cols))
+    s2 = gpu_server_from(o)  # no secret key: KeyError like BfvBackend::decrypt (backend.cpp:161-165)
+    with pytest.raises(KeyError_):
+        s2.unpack_results(packed, R, cols)
