@@ -114,6 +114,27 @@ int hei_gpu_unpack_results(hei_gpu_ctx* ctx, const uint64_t* packed, uint64_t co
 int hei_gpu_unpack_baseline(hei_gpu_ctx* ctx, const uint64_t* blocks, uint64_t rows, uint64_t cols,
                             int64_t* out);
 
+/* TwinContext::keygen (twin.cpp:41-48; BfvContext::keygen context.cpp:152-172
+ * and make_galois_keys :201-251 per branch) on the device, drawing from `rng`
+ * exactly as the reference draws from its util::Prng (the stream is replayed
+ * and rejection sampling resolved on the device; rng is advanced past every
+ * draw the reference would consume). Outputs (each may be NULL):
+ *   sk       [2][N] int8 (SecretKey::s per branch)
+ *   pk       [branch][part][prime][N] u64 coeff form (PublicKey p0, p1)
+ *   elts_out [log2(N)] galois elements, ascending
+ *   gk0/gk1  [elt ascending][l][part][i][N] u64 eval form (GaloisKey::rows)
+ * install != 0 also installs them in ctx (Galois keys for the server role,
+ * public and secret keys for the client role). */
+int hei_gpu_keygen(hei_gpu_ctx* ctx, hei_gpu_prng* rng, int install, int8_t* sk, uint64_t* pk,
+                   uint64_t* elts_out, uint64_t* gk0, uint64_t* gk1);
+
+/* Test seam (not a reference interface): the keygen draw planner on a given
+ * raw mt19937_64 stream; kinds 0 uniform_u64(bound) -> out32 (low 32 bits),
+ * 1 ternary -> out8, 2 gaussian (records the start in gpos). */
+int hei_gpu_debug_rejection_plan(hei_gpu_ctx* ctx, const uint64_t* raw, uint64_t avail, const uint32_t* kinds,
+                                 const uint32_t* counts, const uint64_t* bounds, uint32_t nseg,
+                                 uint32_t* out32, int8_t* out8, uint64_t* gpos, uint64_t* used);
+
 /* Server wire path (InferenceServer::do_infer, server.cpp:112-172): the
  * request's HECT ciphertext blobs (bfv::load_ciphertext, serialize.cpp:80-91;
  * coeff form) concatenated in request order [row][chunk][branch], each branch-b

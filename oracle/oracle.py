@@ -297,6 +297,12 @@ class Reference(_Twin):
         self._wcols = np.asarray(w).shape[1]
         return super().encode_weights(w)
 
+    def keygen_next(self, seed: int, count: int) -> np.ndarray:
+        """Raw draws following TwinContext::keygen(Prng(seed))."""
+        out = np.zeros(count, np.uint64)
+        self._check(self.lib.ref_keygen_next(self._h, C.c_uint64(seed), C.c_uint64(count), _u64p(out)))
+        return out
+
     def inputs_wire(self) -> bytes:
         """The loaded/encoded inputs as the client's HECT blob list."""
         n = C.c_uint64(0)

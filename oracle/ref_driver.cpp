@@ -515,6 +515,18 @@ int ref_server_wire(void* h, const uint8_t* blobs, uint64_t blob_bytes, uint64_t
   GUARD_END
 }
 
+// The draws that follow TwinContext::keygen(Prng(seed)) (twin.cpp:41-48):
+// pins where a keygen replay must leave the stream.
+int ref_keygen_next(void* h, uint64_t seed, uint64_t count, uint64_t* out) {
+  GUARD_BEGIN
+  auto& s = *static_cast<Session*>(h);
+  util::Prng rng(seed);
+  auto keys = s.ctx->keygen(rng);
+  for (uint64_t k = 0; k < count; ++k) out[k] = rng.next();
+  return 0;
+  GUARD_END
+}
+
 // Prng stream check (proj/include/hei/util/rng.hpp:19-68).
 int ref_prng(uint64_t seed, uint64_t count, uint64_t* raw, double* gauss,
              uint64_t* uni3) {

@@ -73,6 +73,25 @@ __global__ void __launch_bounds__(320) k_mt_generate(uint64_t* __restrict__ stat
   if (t == 0) st[312] = mti;
 }
 
+// One Prng::gaussian pair (rng.hpp:47-62: cos first, sin cached as the spare)
+// scaled by sigma = 3.2, clamped at 6 sigma and rounded with llround
+// (sample_gaussian, sampling.cpp:24-34). Returns false on the u1 == 0
+// rejection, which would shift the stream.
+__device__ __forceinline__ bool box_muller_pair(uint64_t r1, uint64_t r2, int8_t& a, int8_t& b) {
+  const double sigma = 3.2, bound = 6.0 * sigma, two_pi = 6.283185307179586476925286766559;
+  const double u1 = (double)(r1 >> 11) * 0x1.0p-53;
+  const double u2 = (double)(r2 >> 11) * 0x1.0p-53;
+  const double mag = sqrt(-2.0 * log(u1));
+  double sn, cs;
+  sincos(two_pi * u2, &sn, &cs);
+  double x0 = mag * cs * sigma, x1 = mag * sn * sigma;
+  x0 = x0 > bound ? bound : (x0 < -bound ? -bound : x0);
+  x1 = x1 > bound ? bound : (x1 < -bound ? -bound : x1);
+  a = (int8_t)llround(x0);
+  b = (int8_t)llround(x1);
+  return u1 > 0.0;
+}
+
 // Noise of one encryption per (e, branch): raw draws [3][N] -> i8 [3][N]
 // (sample_ternary, sample_gaussian twice; sampling.cpp:16-34). The Box-Muller
 // pair (cos first, sin as the cached spare) follows Prng::gaussian. Any
@@ -88,23 +107,11 @@ __global__ void k_bl_noise(const uint64_t* __restrict__ raw, uint64_t count, uin
     if (v == ~0ull) *err = 1;
     o[x] = (int8_t)((int)(v % 3) - 1);
   }
-  const double sigma = 3.2, bound = 6.0 * sigma, two_pi = 6.283185307179586476925286766559;
   for (uint32_t s = 0; s < 2; ++s) {
     const uint64_t* g = d + n + (uint64_t)s * n;
     int8_t* og = o + n + s * n;
-    for (uint32_t k = threadIdx.x; k < n / 2; k += blockDim.x) {
-      const double u1 = (double)(g[2 * k] >> 11) * 0x1.0p-53;
-      const double u2 = (double)(g[2 * k + 1] >> 11) * 0x1.0p-53;
-      if (u1 <= 0.0) *err = 1;
-      const double mag = sqrt(-2.0 * log(u1));
-      double sn, cs;
-      sincos(two_pi * u2, &sn, &cs);
-      double x0 = mag * cs * sigma, x1 = mag * sn * sigma;
-      x0 = x0 > bound ? bound : (x0 < -bound ? -bound : x0);
-      x1 = x1 > bound ? bound : (x1 < -bound ? -bound : x1);
-      og[2 * k] = (int8_t)llround(x0);
-      og[2 * k + 1] = (int8_t)llround(x1);
-    }
+    for (uint32_t k = threadIdx.x; k < n / 2; k += blockDim.x)
+      if (!box_muller_pair(g[2 * k], g[2 * k + 1], og[2 * k], og[2 * k + 1])) *err = 1;
   }
   (void)encs;
 }

@@ -1442,6 +1442,7 @@ __global__ void __launch_bounds__(256) k_bfly_peak(uint32_t* __restrict__ sink, 
 }
 
 #include "decrypt.cuh"
+#include "keygen.cuh"
 
 }  // namespace
 
@@ -2584,6 +2585,8 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     set_smem_attr((const void*)k_dec_phase, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_dec_decode, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_prepare_sk, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_kg_pk, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_kg_gk, smem_bytes(c.get(), 1));
     if (c->logn == 12) set_fast_attrs<12>(smem_bytes(c.get(), 1));
     if (c->logn == 13) set_fast_attrs<13>(smem_bytes(c.get(), 1));
     if (c->logn == 14) set_fast_attrs<14>(smem_bytes(c.get(), 1));
@@ -2689,33 +2692,257 @@ int hei_gpu_measure_butterfly_peak(int device, double* bfly_per_s) {
   });
 }
 
+// Galois key rows [elt][l][part][i][N] u64 already on the device -> the
+// key-switch layout (k_prepare_keys), installed as branch b's key set.
+void install_galois_keys(hei_gpu_ctx* c, uint32_t b, uint32_t count, const uint64_t* elts, const uint64_t* d_raw) {
+  if (b > 1) raise(HEI_PARAM_ERROR, "branch out of range");
+  if (count == 0 || count > kMaxElts) raise(HEI_KEY_ERROR, "galois key set size out of range");
+  const uint32_t L = c->L[b];
+  const uint64_t words = (uint64_t)count * L * 2 * L * c->n;
+  std::map<uint64_t, uint32_t> idx;
+  for (uint32_t e = 0; e < count; ++e) {
+    if (!(elts[e] & 1) || elts[e] >= 2ull * c->n) raise(HEI_KEY_ERROR, "invalid galois element");
+    idx[elts[e]] = e;
+  }
+  if (c->d_keys[b]) cudaFree(c->d_keys[b]);
+  c->d_keys[b] = nullptr;
+  CU(cudaMalloc(&c->d_keys[b], words * sizeof(uint2)));
+  k_prepare_keys<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, b, count, d_raw, c->d_keys[b], c->d_err);
+  LAUNCHED();
+  CU(cudaStreamSynchronize(c->stream));
+  check_err_flag(c, HEI_CODEC_ERROR, "galois keys: coefficient not reduced");
+  c->key_index[b] = idx;
+  c->has_keys[b] = true;
+  ++c->graph_gen;
+}
+
 int hei_gpu_upload_galois_keys(hei_gpu_ctx* c, uint32_t b, uint32_t count, const uint64_t* elts,
                                const uint64_t* rows) {
   return guarded([&] {
     if (b > 1) raise(HEI_PARAM_ERROR, "branch out of range");
     if (count == 0 || count > kMaxElts) raise(HEI_KEY_ERROR, "galois key set size out of range");
     set_device(c);
-    const uint32_t L = c->L[b];
-    const uint64_t words = (uint64_t)count * L * 2 * L * c->n;
-    std::map<uint64_t, uint32_t> idx;
-    for (uint32_t e = 0; e < count; ++e) {
-      if (!(elts[e] & 1) || elts[e] >= 2ull * c->n) raise(HEI_KEY_ERROR, "invalid galois element");
-      idx[elts[e]] = e;
-    }
+    const uint64_t words = (uint64_t)count * c->L[b] * 2 * c->L[b] * c->n;
     uint64_t* d_raw = nullptr;
     CU(cudaMalloc(&d_raw, words * 8));
-    if (c->d_keys[b]) cudaFree(c->d_keys[b]);
-    c->d_keys[b] = nullptr;
-    CU(cudaMalloc(&c->d_keys[b], words * sizeof(uint2)));
     CU(cudaMemcpy(d_raw, rows, words * 8, cudaMemcpyHostToDevice));
-    k_prepare_keys<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, b, count, d_raw, c->d_keys[b], c->d_err);
+    try {
+      install_galois_keys(c, b, count, elts, d_raw);
+    } catch (...) {
+      cudaFree(d_raw);
+      throw;
+    }
+    cudaFree(d_raw);
+  });
+}
+
+// Test seam for k_kg_plan: resolve uniform_u64 rejection sampling over a
+// given raw stream for a list of (kind, count, bound) segments (kind 0
+// uniform, 1 ternary, 2 gaussian start only). out32/out8 receive the values
+// in segment order; used = draws consumed; returns HEI_RANGE_ERROR if the
+// stream is too short.
+int hei_gpu_debug_rejection_plan(hei_gpu_ctx* c, const uint64_t* raw, uint64_t avail, const uint32_t* kinds,
+                                 const uint32_t* counts, const uint64_t* bounds, uint32_t nseg, uint32_t* out32,
+                                 int8_t* out8, uint64_t* gpos, uint64_t* used) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    std::vector<KgSeg> segs(nseg);
+    uint64_t o32 = 0, o8 = 0;
+    for (uint32_t i = 0; i < nseg; ++i) {
+      segs[i].kind = kinds[i];
+      segs[i].n = counts[i];
+      segs[i].bound = bounds[i];
+      segs[i].limit = bounds[i] ? bounds[i] * (UINT64_MAX / bounds[i]) : 0;
+      if (kinds[i] == 0) segs[i].out = o32, o32 += counts[i];
+      else segs[i].out = o8, o8 += counts[i];
+    }
+    KgSeg* d_segs;
+    uint64_t *d_raw, *d_gpos, *d_used;
+    uint32_t* d32;
+    int8_t* d8;
+    CU(cudaMalloc(&d_segs, nseg * sizeof(KgSeg) + 8));
+    CU(cudaMalloc(&d_raw, avail * 8 + 8));
+    CU(cudaMalloc(&d_gpos, nseg * 8 + 8));
+    CU(cudaMalloc(&d_used, 8));
+    CU(cudaMalloc(&d32, o32 * 4 + 4));
+    CU(cudaMalloc(&d8, o8 + 1));
+    CU(cudaMemcpy(d_segs, segs.data(), nseg * sizeof(KgSeg), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_raw, raw, avail * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemset(c->d_err, 0, 4));
+    k_kg_plan<<<1, 1024, 0, c->stream>>>(d_raw, avail, d_segs, nseg, d32, d8, d_gpos, d_used, c->d_err);
     LAUNCHED();
     CU(cudaStreamSynchronize(c->stream));
-    cudaFree(d_raw);
-    check_err_flag(c, HEI_CODEC_ERROR, "galois keys: coefficient not reduced");
-    c->key_index[b] = idx;
-    c->has_keys[b] = true;
-    ++c->graph_gen;
+    uint32_t err = 0;
+    CU(cudaMemcpy(&err, c->d_err, 4, cudaMemcpyDeviceToHost));
+    CU(cudaMemset(c->d_err, 0, 4));
+    CU(cudaMemcpy(used, d_used, 8, cudaMemcpyDeviceToHost));
+    if (out32 && o32) CU(cudaMemcpy(out32, d32, o32 * 4, cudaMemcpyDeviceToHost));
+    if (out8 && o8) CU(cudaMemcpy(out8, d8, o8, cudaMemcpyDeviceToHost));
+    if (gpos) CU(cudaMemcpy(gpos, d_gpos, nseg * 8, cudaMemcpyDeviceToHost));
+    for (void* v : {(void*)d_segs, (void*)d_raw, (void*)d_gpos, (void*)d_used, (void*)d32, (void*)d8}) cudaFree(v);
+    if (err & 4) raise(HEI_RANGE_ERROR, "rejection plan: raw stream too short");
+  });
+}
+
+// TwinContext::keygen (twin.cpp:41-48) on the device; see keygen.cuh.
+int hei_gpu_keygen(hei_gpu_ctx* c, hei_gpu_prng* rng, int install, int8_t* sk, uint64_t* pk, uint64_t* elts_out,
+                   uint64_t* gk0, uint64_t* gk1) {
+  return guarded([&] {
+    if (!rng) raise(HEI_PARAM_ERROR, "keygen: rng required");
+    if (rng->have_spare) raise(HEI_PARAM_ERROR, "keygen: rng holds a cached Box-Muller spare; cannot replay on the device");
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = c->stream;
+    const uint32_t n = c->n, P = c->P();
+    const std::vector<uint64_t>& gen = c->fold_elts;  // galois_steps() order, then the swap (context.cpp:179-212)
+    const uint32_t ne = (uint32_t)gen.size();
+    std::vector<uint64_t> asc(gen);
+    std::sort(asc.begin(), asc.end());
+    std::vector<uint32_t> slot(ne);
+    for (uint32_t e = 0; e < ne; ++e) slot[e] = (uint32_t)(std::lower_bound(asc.begin(), asc.end(), gen[e]) - asc.begin());
+    // draw plan, in the reference's order
+    std::vector<KgSeg> segs;
+    uint64_t off8 = 0, off32 = 0, D = 0;
+    uint64_t s8[2], e8[2], a32[2], ge8[2], ga32[2];
+    auto add = [&](uint32_t kind, uint64_t bound) {
+      KgSeg g{};
+      g.kind = kind;
+      g.n = n;
+      g.bound = bound;
+      g.limit = bound ? bound * (UINT64_MAX / bound) : 0;
+      if (kind == 0) g.out = off32, off32 += n;
+      else g.out = off8, off8 += n;
+      D += n;
+      segs.push_back(g);
+    };
+    for (uint32_t b = 0; b < 2; ++b) {
+      const uint32_t first = b ? c->L[0] : 0, L = c->L[b];
+      s8[b] = off8;
+      add(1, 3);  // sample_ternary
+      e8[b] = off8;
+      add(2, 0);  // sample_gaussian
+      a32[b] = off32;
+      for (uint32_t i = 0; i < L; ++i) add(0, c->q[first + i]);  // sample_uniform per prime
+      ge8[b] = off8;
+      ga32[b] = off32;
+      for (uint32_t e = 0; e < ne; ++e)
+        for (uint32_t l = 0; l < L; ++l) {
+          add(2, 0);
+          for (uint32_t i = 0; i < L; ++i) add(0, c->q[first + i]);
+        }
+    }
+    struct Free {
+      std::vector<void*> p;
+      ~Free() {
+        for (void* v : p) cudaFree(v);
+      }
+    } fr;
+    auto alloc = [&](auto** ptr, size_t bytes) {
+      CU(cudaMalloc((void**)ptr, bytes));
+      fr.p.push_back((void*)*ptr);
+    };
+    KgSeg* d_segs;
+    uint32_t* d_out32;
+    int8_t* d_out8;
+    uint64_t *d_gpos, *d_used, *d_state, *d_elts;
+    uint32_t *d_slot, *d_shat;
+    alloc(&d_segs, segs.size() * sizeof(KgSeg));
+    alloc(&d_out32, off32 * 4);
+    alloc(&d_out8, off8);
+    alloc(&d_gpos, segs.size() * 8);
+    alloc(&d_used, 8);
+    alloc(&d_state, 313 * 8);
+    alloc(&d_elts, ne * 8);
+    alloc(&d_slot, ne * 4);
+    alloc(&d_shat, (size_t)P * n * 4);
+    CU(cudaMemcpyAsync(d_segs, segs.data(), segs.size() * sizeof(KgSeg), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d_elts, gen.data(), ne * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d_slot, slot.data(), ne * 4, cudaMemcpyHostToDevice, st));
+    uint64_t hstate[313];
+    std::memcpy(hstate, rng->mt, 312 * 8);
+    hstate[312] = rng->mti;
+    // replay + plan; a rejected draw needs a longer stream (rare): retry
+    uint64_t avail = D, used = 0;
+    uint64_t* d_raw = nullptr;
+    for (int attempt = 0;; ++attempt) {
+      if (d_raw) cudaFree(d_raw);
+      CU(cudaMalloc(&d_raw, avail * 8));
+      CU(cudaMemcpyAsync(d_state, hstate, sizeof(hstate), cudaMemcpyHostToDevice, st));
+      heb_baseline::k_mt_generate<<<1, 320, 0, st>>>(d_state, d_raw, avail);
+      LAUNCHED();
+      CU(cudaMemsetAsync(c->d_err, 0, 4, st));
+      k_kg_plan<<<1, 1024, 0, st>>>(d_raw, avail, d_segs, (uint32_t)segs.size(), d_out32, d_out8, d_gpos, d_used,
+                                     c->d_err);
+      LAUNCHED();
+      uint32_t err = 0;
+      CU(cudaMemcpyAsync(&err, c->d_err, 4, cudaMemcpyDeviceToHost, st));
+      CU(cudaMemcpyAsync(&used, d_used, 8, cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      if (err & 2) {
+        CU(cudaMemset(c->d_err, 0, 4));
+        cudaFree(d_raw);
+        raise(HEI_INTERNAL, "keygen: Box-Muller u1 == 0 rejection (probability 2^-53) is not replayed on the device");
+      }
+      if (err & 4) {
+        if (attempt > 8) {
+          cudaFree(d_raw);
+          raise(HEI_INTERNAL, "keygen: rejection sampling ran past the replayed stream");
+        }
+        avail += 4096;
+        continue;
+      }
+      if (used != avail) {  // consumed fewer than generated: regenerate exactly `used` for the rng state
+        avail = used;
+        continue;
+      }
+      break;
+    }
+    fr.p.push_back(d_raw);
+    k_kg_gauss<<<(unsigned)segs.size(), 256, 0, st>>>(d_raw, d_segs, d_gpos, d_out8);
+    LAUNCHED();
+    const size_t sm1 = smem_bytes(c, 1);
+    uint64_t *d_pk, *d_gk[2];
+    alloc(&d_pk, c->ct_words() / 2 * 8 * 2);  // [branch][part][L_b][n]
+    for (uint32_t b = 0; b < 2; ++b) {
+      const uint32_t L = c->L[b];
+      alloc(&d_gk[b], (size_t)ne * L * 2 * L * n * 8);
+      k_prepare_sk<<<L, c->threads(), sm1, st>>>(c->geo, b, d_out8 + s8[b], d_shat);
+      LAUNCHED();
+      uint64_t* pkb = d_pk + (b ? 2ull * c->L[0] * n : 0);
+      k_kg_pk<<<L, c->threads(), sm1, st>>>(c->geo, b, d_out8 + e8[b], d_out32 + a32[b], d_shat, pkb);
+      LAUNCHED();
+      k_kg_gk<<<ne * L * L, c->threads(), sm1, st>>>(c->geo, b, d_elts, d_slot, d_out8 + s8[b], d_out8 + ge8[b],
+                                                     d_out32 + ga32[b], d_shat, d_gk[b]);
+      LAUNCHED();
+    }
+    CU(cudaMemcpyAsync(hstate, d_state, sizeof(hstate), cudaMemcpyDeviceToHost, st));
+    if (sk)
+      for (uint32_t b = 0; b < 2; ++b) CU(cudaMemcpyAsync(sk + (size_t)b * n, d_out8 + s8[b], n, cudaMemcpyDeviceToHost, st));
+    if (pk) CU(cudaMemcpyAsync(pk, d_pk, c->ct_words() * 8, cudaMemcpyDeviceToHost, st));
+    if (gk0) CU(cudaMemcpyAsync(gk0, d_gk[0], (size_t)ne * c->L[0] * 2 * c->L[0] * n * 8, cudaMemcpyDeviceToHost, st));
+    if (gk1) CU(cudaMemcpyAsync(gk1, d_gk[1], (size_t)ne * c->L[1] * 2 * c->L[1] * n * 8, cudaMemcpyDeviceToHost, st));
+    if (elts_out) std::memcpy(elts_out, asc.data(), ne * 8);
+    CU(cudaStreamSynchronize(st));
+    std::memcpy(rng->mt, hstate, 312 * 8);
+    rng->mti = (uint32_t)hstate[312];
+    if (install) {
+      for (uint32_t b = 0; b < 2; ++b) {
+        install_galois_keys(c, b, ne, asc.data(), d_gk[b]);
+        const size_t words = 2ull * c->L[b] * n;
+        if (!c->d_pk[b]) CU(cudaMalloc(&c->d_pk[b], words * 8));
+        CU(cudaMemcpy(c->d_pk[b], d_pk + (b ? 2ull * c->L[0] * n : 0), words * 8, cudaMemcpyDeviceToDevice));
+        if (!c->d_sk_hat) CU(cudaMalloc(&c->d_sk_hat, (size_t)P * n * 4));
+        k_prepare_sk<<<c->L[b], c->threads(), sm1, st>>>(c->geo, b, d_out8 + s8[b], c->d_sk_hat);
+        LAUNCHED();
+        c->has_sk[b] = true;
+      }
+      if (c->d_pkp) {
+        cudaFree(c->d_pkp);
+        c->d_pkp = nullptr;
+      }
+      CU(cudaStreamSynchronize(st));
+    }
   });
 }
 

@@ -107,6 +107,22 @@ class GpuTwinServer:
         q0 = np.ascontiguousarray(q0, dtype=np.uint64)
         return int(native.lib().hei_params_hash(self.n, self.t[branch], self.security_level, u64p(q0), len(q0)))
 
+    # ---- key generation, SURVEY §8(f) row 4 ----
+    def keygen(self, rng: "Prng", install: bool = True):
+        """TwinContext::keygen (twin.cpp:41-48) on the device from the replayed
+        util::Prng `rng` (advanced exactly as the reference's). Returns
+        (elts ascending, [gk0, gk1] [elt][l][part][i][N], sk [2][N] int8,
+        pk [branch][part][prime][N] coeff) — the layouts of the oracle's
+        galois_keys(). install=True also installs them in this context."""
+        ne = self.n.bit_length() - 1  # log2(N) - 1 power-of-two steps + the swap
+        elts = np.zeros(ne, np.uint64)
+        gk = [np.zeros((ne, self.L[b], 2, self.L[b], self.n), np.uint64) for b in range(2)]
+        sk = np.zeros((2, self.n), np.int8)
+        pk = np.zeros(self.ct_words, np.uint64)
+        check(native.lib().hei_gpu_keygen(self._h, rng._h, C.c_int(int(install)), sk.ctypes.data_as(C.POINTER(C.c_int8)),
+                                          u64p(pk), u64p(elts), u64p(gk[0]), u64p(gk[1])))
+        return elts, gk, sk, pk
+
     # ---- client role (decryption), SURVEY §8(f) row 3 ----
     def upload_secret_keys(self, sk) -> None:
         """SecretKey::s of both branches, ternary int8 [2][N]."""

@@ -101,7 +101,8 @@ EXPORTED = [
     "hei_gpu_encode_inputs", "hei_gpu_encode_inputs_device",
     "hei_hect_ciphertext_bytes", "hei_params_hash", "hei_gpu_matmul_wire",
     "hei_gpu_upload_secret_key", "hei_gpu_decrypt_signed", "hei_gpu_noise_budget",
-    "hei_gpu_unpack_results", "hei_gpu_unpack_baseline",
+    "hei_gpu_unpack_results", "hei_gpu_unpack_baseline", "hei_gpu_keygen",
+    "hei_gpu_debug_rejection_plan",
 ]
 
 _lib = None

@@ -569,3 +569,97 @@ def test_device_unpack_results_and_baseline(which, request):
     s2 = gpu_server_from(o)  # no secret key: KeyError like BfvBackend::decrypt (backend.cpp:161-165)
     with pytest.raises(KeyError_):
         s2.unpack_results(packed, R, cols)
+
+
+@pytest.mark.parametrize("n", [32, 8192, 16384])
+def test_device_keygen_matches_reference(n):
+    """TwinContext::keygen (twin.cpp:41-48) on the device from util::Prng(seed):
+    secret, public and Galois keys identical to the reference's, the Prng left
+    where the reference leaves it, and the installed keys usable end to end."""
+    from oracle.oracle import Reference
+    from paper_2204_05496_b200 import EncodedWeights, GpuTwinServer, Prng, ScalingConfig, matmul
+
+    p = production_params(n) if n >= 8192 else tiny_params(n)
+    ref = Reference(p, key_seed=31, enc_seed=32)
+    elts, gk, sk, pk = ref.galois_keys()
+    s = GpuTwinServer(ref.n, (p.t0, p.t1), ref.L, ref.q, [], None, ScalingConfig(p.s_x, p.s_w, p.in_bits),
+                      security_level=p.sec)
+    rng = Prng(31)
+    e2, gk2, sk2, pk2 = s.keygen(rng)
+    assert np.array_equal(e2, elts)
+    assert np.array_equal(sk2, sk)
+    assert np.array_equal(pk2, pk)
+    for b in range(2):
+        assert np.array_equal(gk2[b], gk[b]), b
+    # rng continues where the reference's keygen left it
+    assert np.array_equal(rng.draw(4), ref.keygen_next(31, 4))
+    # installed keys work: a small matmul + device decryption
+    rng_np = np.random.default_rng(3)
+    R, f, cols = 2, min(3 * n // 2, 700), 2
+    x = random_mat(rng_np, R, f, 3)
+    w = random_mat(rng_np, f, cols, 4)
+    b = np.array([5, -7])
+    inputs = ref.encode_inputs(x)
+    got, _ = matmul(s, inputs, EncodedWeights.from_prepared(s, ref.encode_weights(w), f), b)
+    assert np.array_equal(s.unpack_results(got, R, cols), oracle_matmul(x, w, b))
+
+
+def test_keygen_rejection_planner_exact():
+    """The device planner resolves uniform_u64's rejection loop (rng.hpp:31-40)
+    exactly: with bounds just above 2^63 about half the draws are rejected,
+    and every segment still starts where a sequential replay would."""
+    import ctypes as C
+
+    from paper_2204_05496_b200 import RangeError, native
+
+    o = Oracle(tiny_params(32), 1, 2)
+    s = gpu_server_from(o)
+    rng = np.random.default_rng(11)
+    raw = rng.integers(0, 2 ** 64, size=40000, dtype=np.uint64)
+    raw[5] = np.uint64(2 ** 64 - 1)  # rejected by the ternary bound too
+    kinds = np.array([1, 0, 2, 0, 0, 1, 2, 0], np.uint32)
+    counts = np.array([3000, 1500, 64, 2049, 5, 1025, 32, 3333], np.uint32)
+    big = 2 ** 63 + 12345
+    bounds = np.array([3, big, 0, 2147352577, big, 3, 0, big - 2], np.uint64)
+    # sequential reference replay (Prng::uniform_u64; a gaussian segment consumes n draws)
+    p, want32, want8, wpos = 0, [], [], []
+    for k, cnt, bd in zip(kinds, counts, bounds):
+        bd = int(bd)
+        if k == 2:
+            wpos.append(p)
+            p += int(cnt)
+            want8.extend([None] * int(cnt))  # gaussian values are not written by the planner
+            continue
+        wpos.append(0)
+        lim = bd * ((2 ** 64 - 1) // bd)
+        got = 0
+        while got < cnt:
+            v = int(raw[p])
+            p += 1
+            if v >= lim:
+                continue
+            got += 1
+            if k == 0:
+                want32.append((v % bd) & 0xFFFFFFFF)
+            else:
+                want8.append(v % 3 - 1)
+    out32 = np.zeros(len(want32), np.uint32)
+    out8 = np.zeros(len(want8), np.int8)  # ternary and gaussian segments share the i8 output
+    gpos = np.zeros(len(kinds), np.uint64)
+    used = C.c_uint64(0)
+    P = C.POINTER
+
+    def plan(avail):
+        return native.lib().hei_gpu_debug_rejection_plan(
+            s.handle, native.u64p(raw), C.c_uint64(avail), kinds.ctypes.data_as(P(C.c_uint32)),
+            counts.ctypes.data_as(P(C.c_uint32)), native.u64p(bounds), C.c_uint32(len(kinds)),
+            out32.ctypes.data_as(P(C.c_uint32)), out8.ctypes.data_as(P(C.c_int8)), native.u64p(gpos), C.byref(used))
+
+    native.check(plan(raw.size))
+    assert used.value == p
+    assert np.array_equal(out32, np.array(want32, np.uint32))
+    tern = np.array([v is not None for v in want8])
+    assert np.array_equal(out8[tern], np.array([v for v in want8 if v is not None], np.int8))
+    assert [int(gpos[i]) for i in range(len(kinds)) if kinds[i] == 2] == [wpos[i] for i in range(len(kinds)) if kinds[i] == 2]
+    with pytest.raises(RangeError):  # stream too short
+        native.check(plan(p - 1))
