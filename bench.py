@@ -200,26 +200,21 @@ def run_reference(args, world, rank):
 
 # ------------------------------------------------------------------------ ours
 def make_server(n, device, seed=1):
-    """Evaluate-only server with seeded uniform key material (the kernels are
-    data-oblivious; real encryptions are exercised by tests/)."""
-    from paper_2204_05496_b200 import GpuTwinServer, ScalingConfig
+    """Twin context with real keys: TwinContext::keygen from util::Prng(1) run
+    on the device (SURVEY §8d seeds), installed for both roles (server Galois
+    keys, client public/secret keys). Returns (server, q0, q1, keygen_ms)."""
+    from paper_2204_05496_b200 import GpuTwinServer, Prng, ScalingConfig
 
     t1 = T1 if n < 16384 else T1_16K
     q0, q1 = q_chain(n, T0), q_chain(n, t1)
     L = [len(q0), len(q1)]
     q = np.array(q0 + q1, dtype=np.uint64)
-    two_n = 2 * n
-    elts = sorted([pow(3, 1 << s, two_n) for s in range(int(np.log2(n)) - 1)] + [two_n - 1])
-    rng = np.random.default_rng(seed)
-    gks = []
-    for b, qb in enumerate((q0, q1)):
-        Lb = len(qb)
-        g = np.empty((len(elts), Lb, 2, Lb, n), dtype=np.uint64)
-        for i, qi in enumerate(qb):
-            g[:, :, :, i, :] = rng.integers(0, qi, size=(len(elts), Lb, 2, n), dtype=np.uint64)
-        gks.append(g)
-    srv = GpuTwinServer(n, (T0, t1), L, q, elts, gks, ScalingConfig(), device=device)
-    return srv, q0, q1
+    srv = GpuTwinServer(n, (T0, t1), L, q, [], None, ScalingConfig(), device=device)
+    srv.keygen(Prng(seed), install=True)  # warm (first-call allocations)
+    t0 = time.perf_counter()
+    srv.keygen(Prng(seed), install=True)
+    kg_ms = (time.perf_counter() - t0) * 1000.0
+    return srv, q0, q1, kg_ms
 
 
 def wire_e2e(srv, ew, b, h_np, R, kc, n, L0, L1, world, steps):
@@ -270,27 +265,29 @@ def run_ours(args, world, rank, local):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    srv, q0, q1 = make_server(n, local)
+    from paper_2204_05496_b200 import Prng, encode_inputs_device
+
+    srv, q0, q1, keygen_ms = make_server(n, local)
     if args.batch_pairs:
         srv.set_batch_pairs(args.batch_pairs)
     kc = (f + n - 1) // n
     P = len(q0) + len(q1)
     ctw = 2 * P * n
-    _, w, b = synthetic(1, f, cols, pf, ws)
+    # seeded synthetic individuals (rank r holds its own rows), weights, bias
+    x, _, _ = synthetic(R, f, cols, pf, ws, seed=7 + rank)
+    _, w, b = synthetic(1, f, cols, pf, ws)  # one model, shared by every rank
     ew = encode_weights(srv, w)
-    # device-resident inputs: uniform residues per (part, prime) slab
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
+    # device-resident inputs: the client's real encryptions of x
+    # (encode_inputs, matmul.cpp:201-223; Prng seeds 2, 3 as client_backend(keys, 2))
     d_in = torch.empty((R * kc, ctw), dtype=torch.int32, device=dev)
-    polys = []
-    for bi, qb in enumerate((q0, q1)):
-        for part in range(2):
-            polys += list(qb)
-    for poly, qi in enumerate(polys):
-        d_in[:, poly * n:(poly + 1) * n] = torch.randint(0, qi, (R * kc, n), generator=g, device=dev, dtype=torch.int64).to(torch.int32)
+    stream = torch.cuda.Stream(device=dev)
+    for _ in range(2):  # first call also builds the cached mt19937_64 jump polynomial
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        encode_inputs_device(srv, x, Prng(2 + 2 * rank), Prng(3 + 2 * rank), d_in.data_ptr(), stream.cuda_stream)
+        enc_ms = (time.perf_counter() - t0) * 1000.0
     C_ = (R * cols + n - 1) // n
     d_out = torch.empty((C_, ctw), dtype=torch.int32, device=dev)
-    stream = torch.cuda.Stream(device=dev)
 
     if world == 1:
         def step():
@@ -410,18 +407,6 @@ def run_ours(args, world, rank, local):
     if args.baseline and rank == 0:
         from paper_2204_05496_b200 import Prng, baseline_matmul
 
-        pk = []
-        rngk = np.random.default_rng(5)
-        for qb in (q0, q1):
-            a = np.empty((2, len(qb), n), dtype=np.uint64)
-            for i, qi in enumerate(qb):
-                a[:, i, :] = rngk.integers(0, qi, size=(2, n), dtype=np.uint64)
-            pk.append(a.reshape(-1))
-        from paper_2204_05496_b200 import native as _nat
-        import ctypes as _C
-
-        for bb in range(2):
-            _nat.check(_nat.lib().hei_gpu_upload_public_key(srv.handle, _C.c_uint32(bb), _nat.u64p(pk[bb])))
         R3, f3, c3, _, pf3, ws3 = CONFIGS["c3"]
         x3, w3, b3 = synthetic(R3, f3, c3, pf3, ws3)
         baseline_matmul(srv, x3, w3, b3, Prng(2), Prng(3))  # warm (incl. the cached jump polynomial)
@@ -431,20 +416,8 @@ def run_ours(args, world, rank, local):
         bs = time.perf_counter() - t0
         base = {"algorithm": "standard (sample-batched, baseline_matmul)", "config": f"c3: {R3}x{f3}x{c3} N={n}",
                 "ms": bs * 1000.0, "mul_plain": int(bc.mul_plain_count), "note": "host call incl. H2D of x, w and D2H"}
-        # client-side encryption of this step's inputs (encode_inputs,
-        # matmul.cpp:201-223), device path, R individuals x f features
-        from paper_2204_05496_b200 import encode_inputs_device
-
-        xe, _, _ = synthetic(R, f, cols, pf, ws)
-        d_enc = torch.empty((R * kc, ctw), dtype=torch.int32, device=dev)
-        encode_inputs_device(srv, xe, Prng(2), Prng(3), d_enc.data_ptr(), stream.cuda_stream)  # warm
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        encode_inputs_device(srv, xe, Prng(2), Prng(3), d_enc.data_ptr(), stream.cuda_stream)
-        es = time.perf_counter() - t0
         base["client_encrypt"] = {"config": f"{R} individuals x {f} features ({R * kc} twin encryptions)",
-                                  "ms": es * 1000.0, "individuals_per_s": R / es}
-        del d_enc
+                                  "ms": enc_ms, "individuals_per_s": R / (enc_ms / 1000.0)}
 
     lat = None
     if args.latency and rank == 0:
@@ -461,6 +434,19 @@ def run_ours(args, world, rank, local):
         e1.record(stream)
         torch.cuda.synchronize()
         lat = e0.elapsed_time(e1) / 10
+
+    # client side of the result: decrypt + CRT unpack on the device
+    # (unpack_results, matmul.cpp:257-271), checked against the exact product
+    check = None
+    if world == 1 and rank == 0:
+        packed = d_out.cpu().numpy().view(np.uint32).astype(np.uint64)
+        srv.unpack_results(packed, R, cols)  # warm
+        t0 = time.perf_counter()
+        got = srv.unpack_results(packed, R, cols)
+        dec_ms = (time.perf_counter() - t0) * 1000.0
+        want = np.rint(x.astype(np.float64) @ w.astype(np.float64)).astype(np.int64) + b  # exact: |partial sums| < 2^53
+        check = {"decrypted_equals_integer_product": bool(np.array_equal(got, want)), "client_decrypt_ms": dec_ms,
+                 "keygen_ms": keygen_ms, "client_encrypt_ms": enc_ms}
 
     if rank != 0:
         return
@@ -481,7 +467,8 @@ def run_ours(args, world, rank, local):
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {R} individuals/rank x {f} features x {cols} classes, N={n}, "
                                f"twin t=({T0},{T1 if n < 16384 else T1_16K}), L=({len(q0)},{len(q1)})",
-                   "inputs": "uniform residues in HBM (kernels are data-oblivious); inputs > L2 (no flush needed)",
+                   "inputs": "real encryptions (device keygen from Prng(1), client encryption with Prng(2),(3)) of "
+                             "seeded Bernoulli features, resident in HBM; inputs > L2 (no flush needed)",
                    "parallelism": f"dp{world} (individual sharding)"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -494,6 +481,8 @@ def run_ours(args, world, rank, local):
         line["latency_ms_single_individual"] = lat
     if base is not None:
         line["standard_algorithm"] = base
+    if check is not None:
+        line["client_roundtrip"] = check
     print(json.dumps(line), flush=True)
 
 
