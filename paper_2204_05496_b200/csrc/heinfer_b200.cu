@@ -3209,7 +3209,6 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
   const size_t words = w->kc * c->ct_words();
   const size_t row_bytes = wire ? w->kc * (io.wg.blob[0] + io.wg.blob[1]) : words * 8;
   const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(s->cap_rows, (rows + 7) / 8));
-  const uint64_t nchunks = (rows + chunk - 1) / chunk;
   const size_t slot_bytes = (chunk * row_bytes + 64) & ~(size_t)15;  // + pad for the parser's 12-byte window
   uint8_t* stage = reinterpret_cast<uint8_t*>(
       pool_get(c->pool_stage64, c->pool_stage64_bytes, 2 * slot_bytes));
@@ -3224,9 +3223,13 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
     CU(cudaEventRecord(narrowed[k], st));
   }
   const uint8_t* src = wire ? io.wire : reinterpret_cast<const uint8_t*>(io.u64);
-  for (uint64_t b = 0; b < nchunks; ++b) {
+  // chunk sizes ramp up (chunk/8, chunk/4, ..., chunk) so the first copy,
+  // the only one not hidden behind compute, is short
+  uint64_t nr_next = std::max<uint64_t>(1, chunk / 8);
+  for (uint64_t b = 0, r0 = 0; r0 < rows; ++b) {
     const int slot = (int)(b % 2);
-    const uint64_t r0 = b * chunk, nr = std::min<uint64_t>(chunk, rows - r0);
+    const uint64_t nr = std::min<uint64_t>(nr_next, rows - r0);
+    nr_next = std::min<uint64_t>(chunk, 2 * nr_next);
     uint8_t* sb = stage + (size_t)slot * slot_bytes;
     uint32_t* s32 = in32 + (size_t)slot * chunk * words;
     CU(cudaStreamWaitEvent(cs, narrowed[slot], 0));
@@ -3242,6 +3245,7 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
     CU(cudaEventRecord(narrowed[slot], st));
     if (wire || io.form == HEI_FORM_COEFF) launch_ct_ntt(c, (unsigned)(nr * w->kc * 2 * c->P()), s32, st);
     run_rows(s.get(), s32, d_rows + r0, nr, st);
+    r0 += nr;
   }
   CU(cudaStreamSynchronize(st));
   for (int k = 0; k < 2; ++k) {
