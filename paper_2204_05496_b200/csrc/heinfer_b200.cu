@@ -809,13 +809,15 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T) k_rot_keyswitch_f(Geo g, const u
 // Same as k_rot_keyswitch_f but the two accumulators live in shared memory
 // (transposed [c][T] uint4, conflict-free), which keeps the kernel under 64
 // registers so two 512-thread CTAs share an SM (32 warps for latency hiding).
-template <int LOGN, bool PTW>
+template <int LOGN, bool PTW, bool NEXT>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keyswitch_s(Geo g, const uint32_t* __restrict__ dot,
                                                                     const uint32_t* __restrict__ digits,
                                                                     const uint32_t* __restrict__ perm,
                                                                     const uint2* __restrict__ key0,
                                                                     const uint2* __restrict__ key1,
                                                                     uint32_t* __restrict__ out, int fold,
+                                                                    const uint32_t* __restrict__ perm_next,
+                                                                    uint32_t* __restrict__ dig_next,
                                                                     const __grid_constant__ TwArg<PTW> tab) {
   using NT = Ntt<LOGN>;
   constexpr uint32_t N = NT::N, T = NT::T;
@@ -889,6 +891,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
   }
   uint32_t* o = out + (uint64_t)pair * g.ct_words;
   const uint4* pp = reinterpret_cast<const uint4*>(perm + x0);
+  if constexpr (NEXT) __syncthreads();  // the last NTT's exchange reads of sm are done
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const uint4 pm = __ldg(pp + c);
@@ -911,6 +914,22 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
     }
     *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly0 * N + x0 + 4 * c) = A;
     *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly1 * N + x0 + 4 * c) = B;
+    if constexpr (NEXT) *reinterpret_cast<uint4*>(sm + x0 + 4 * c) = B;
+  }
+  if constexpr (NEXT) {
+    // Fused digit INTT of the NEXT rotation (apply_galois, context.cpp:445-470):
+    // this block owns prime i of the new c1, so it permutes it from shared
+    // memory and inverse-transforms it here instead of in k_rot_digits_f.
+    __syncthreads();
+    uint32_t pm[16];
+    load16_ro(perm_next + x0, pm);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = sm[pm[r]];
+    __syncthreads();
+    NT::inv(e, sm, g.inv + (size_t)gp * N, g.itwc + (size_t)gp * g.twc_stride, q, pr.last, pr.ninv);
+    uint32_t* d = dig_next + ((uint64_t)pair * g.P + gp) * N;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) d[NT::posA(j, r)] = e[r];
   }
 }
 
@@ -1477,7 +1496,8 @@ struct hei_gpu_ctx {
   uint64_t batch_pairs = 0;
   bool ks14_regs = false;  // N = 16384: register-accumulator key switch (HEI_KS14_REGS=1)
   // scratch (grown on demand)
-  uint32_t *d_dotA = nullptr, *d_dotB = nullptr, *d_dig = nullptr;
+  uint32_t *d_dotA = nullptr, *d_dotB = nullptr, *d_dig = nullptr, *d_dig2 = nullptr;
+  bool fuse_digits = true;  // HEI_FUSE_DIGITS=0: separate digit kernel every rotation (small batches)
   uint64_t scratch_pairs = 0;
   std::mutex mu;
   // grow-only device pools for the per-call buffers of the device-resident
@@ -1594,10 +1614,12 @@ void ensure_scratch(hei_gpu_ctx* c, uint64_t pairs) {
   if (c->d_dotA) cudaFree(c->d_dotA);
   if (c->d_dotB) cudaFree(c->d_dotB);
   if (c->d_dig) cudaFree(c->d_dig);
-  c->d_dotA = c->d_dotB = c->d_dig = nullptr;
+  if (c->d_dig2) cudaFree(c->d_dig2);
+  c->d_dotA = c->d_dotB = c->d_dig = c->d_dig2 = nullptr;
   CU(cudaMalloc(&c->d_dotA, pairs * c->ct_words() * 4));
   CU(cudaMalloc(&c->d_dotB, pairs * c->ct_words() * 4));
   CU(cudaMalloc(&c->d_dig, pairs * c->pt_words() * 4));
+  CU(cudaMalloc(&c->d_dig2, pairs * c->pt_words() * 4));
   c->scratch_pairs = pairs;
   ++c->graph_gen;
 }
@@ -1643,43 +1665,60 @@ void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint
                (k_rot_digits<<<blocks, c->threads(), sm, st>>>(g, cur, perm, dig)));
   LAUNCHED();
 }
-void launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* dig,
+// Returns true when the launched kernel also produced the next rotation's
+// digits (k_rot_keyswitch_s with dig_next != nullptr).
+template <int LG>
+void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* dig,
+                 const uint32_t* perm, const uint2* k0, const uint2* k1, uint32_t* out, int fold, cudaStream_t st,
+                 const uint32_t* perm_next, uint32_t* dig_next) {
+  const size_t sm = smem_bytes(c, 3);
+  const bool big = blocks >= 2u * 148u;
+  if (dig_next) {
+    if (big)
+      k_rot_keyswitch_s<LG, true, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, perm_next,
+                                                                        dig_next, *tabs_of(c, g, 0));
+    else
+      k_rot_keyswitch_s<LG, false, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                         perm_next, dig_next, TwNone{});
+  } else {
+    if (big)
+      k_rot_keyswitch_s<LG, true, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr,
+                                                                         nullptr, *tabs_of(c, g, 0));
+    else
+      k_rot_keyswitch_s<LG, false, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                          nullptr, nullptr, TwNone{});
+  }
+}
+
+// Returns true when the launched kernel also produced the next rotation's
+// digits (k_rot_keyswitch_s<.., NEXT = true>).
+bool launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* dig,
                           const uint32_t* perm, const uint2* k0, const uint2* k1, uint32_t* out, int fold,
-                          cudaStream_t st) {
+                          cudaStream_t st, const uint32_t* perm_next = nullptr, uint32_t* dig_next = nullptr) {
   // N <= 8192: shared-memory accumulators, 2 CTAs/SM; N = 16384 (1024
-  // threads) keeps the accumulators in registers.
+  // threads) keeps the accumulators in registers when HEI_KS14_REGS=1.
+  bool fused = dig_next != nullptr;
   switch (c->logn) {
     case 12:
-      if (blocks >= 2u * 148u)
-        k_rot_keyswitch_s<12, true><<<blocks, Ntt<12>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                                *tabs_of(c, g, 0));
-      else
-        k_rot_keyswitch_s<12, false><<<blocks, Ntt<12>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                                 TwNone{});
+      launch_ks_s<12>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, perm_next, dig_next);
       break;
     case 13:
-      if (blocks >= 2u * 148u)
-        k_rot_keyswitch_s<13, true><<<blocks, Ntt<13>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                                *tabs_of(c, g, 0));
-      else
-        k_rot_keyswitch_s<13, false><<<blocks, Ntt<13>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                                 TwNone{});
+      launch_ks_s<13>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, perm_next, dig_next);
       break;
     case 14:
-      if (c->ks14_regs)
+      if (c->ks14_regs) {
         k_rot_keyswitch_f<14><<<blocks, Ntt<14>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, out, fold);
-      else
-      if (blocks >= 2u * 148u)
-        k_rot_keyswitch_s<14, true><<<blocks, Ntt<14>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                                *tabs_of(c, g, 0));
-      else
-        k_rot_keyswitch_s<14, false><<<blocks, Ntt<14>::T, smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                                 TwNone{});
+        fused = false;
+      } else {
+        launch_ks_s<14>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, perm_next, dig_next);
+      }
       break;
     default:
       k_rot_keyswitch<<<blocks, c->threads(), smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold);
+      fused = false;
   }
   LAUNCHED();
+  return fused;
 }
 void launch_mask_acc(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* res, const uint64_t* rows,
                      uint32_t cols, unsigned long long* acc, cudaStream_t st) {
@@ -1715,8 +1754,10 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_digits_f<LG, true>, sm);
   set_smem_attr((const void*)k_rot_digits_f<LG, false>, sm);
   set_smem_attr((const void*)k_rot_keyswitch_f<LG>, sm);
-  set_smem_attr((const void*)k_rot_keyswitch_s<LG, true>, 3 * sm);
-  set_smem_attr((const void*)k_rot_keyswitch_s<LG, false>, 3 * sm);
+  set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, false>, 3 * sm);
+  set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, false>, 3 * sm);
+  set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
+  set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, true>, 3 * sm);
   set_smem_attr((const void*)k_mask_acc_f<LG>, sm);
   set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
   set_smem_attr((const void*)k_ks_part<LG>, sm);
@@ -1741,12 +1782,20 @@ uint64_t auto_batch_pairs(hei_gpu_ctx* c) {
 // The rotate-and-sum fold over `pairs` twin ciphertexts in `cur` (eval form);
 // returns the buffer holding the result.
 uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st, bool split,
-                    uint32_t* part, uint32_t* dig) {
+                    uint32_t* part, uint32_t* dig, uint32_t* dig2) {
   const Geo& g = c->geo;
   const unsigned blocks = (unsigned)(pairs * c->P());
   const uint32_t Lmax = std::max(c->L[0], c->L[1]);
-  for (uint64_t elt : c->fold_elts) {
+  bool have_digits = false;  // digits of this rotation already produced by the previous key switch
+  const size_t S = c->fold_elts.size();
+  for (size_t k = 0; k < S; ++k) {
+    const uint64_t elt = c->fold_elts[k];
     const uint32_t* perm = c->d_perms + (size_t)c->perm_index.at(elt) * c->n;
+    // fused digits pay off when launches are too small to fill the GPU
+    // (latency path); large batches keep the separate 3-CTA/SM digit kernel
+    const bool fuse = c->fuse_digits && blocks < 4u * 148u;
+    const uint32_t* perm_next =
+        (k + 1 < S && fuse) ? c->d_perms + (size_t)c->perm_index.at(c->fold_elts[k + 1]) * c->n : nullptr;
     const uint2* k0 = c->d_keys[0] + (size_t)c->key_index[0].at(elt) * c->L[0] * 2 * c->L[0] * c->n;
     const uint2* k1 = c->d_keys[1] + (size_t)c->key_index[1].at(elt) * c->L[1] * 2 * c->L[1] * c->n;
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
@@ -1756,8 +1805,9 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
       CU(cudaEventCreate(&e2));
       CU(cudaEventRecord(e0, st));
     }
-    launch_rot_digits(c, g, blocks, cur, perm, dig, st);
+    if (!have_digits) launch_rot_digits(c, g, blocks, cur, perm, dig, st);
     if (c->timing) CU(cudaEventRecord(e1, st));
+    have_digits = false;
     if (split) {
       const unsigned pb = (unsigned)(blocks * Lmax);
       HEI_DISPATCH(c->logn,
@@ -1768,7 +1818,9 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
       k_ks_reduce<<<blocks * (c->n / 1024), 256, 0, st>>>(g, cur, part, perm, Lmax, other, 1);
       LAUNCHED();
     } else {
-      launch_rot_keyswitch(c, g, blocks, cur, dig, perm, k0, k1, other, 1, st);
+      have_digits = launch_rot_keyswitch(c, g, blocks, cur, dig, perm, k0, k1, other, 1, st, perm_next,
+                                         perm_next ? dig2 : nullptr);
+      if (have_digits) std::swap(dig, dig2);
     }
     if (c->timing) {
       CU(cudaEventRecord(e2, st));
@@ -1785,6 +1837,7 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
 uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st,
                uint32_t* dig = nullptr) {
   if (!dig) dig = c->d_dig;
+  uint32_t* dig2 = c->d_dig2 + (dig - c->d_dig);  // second digit buffer of the same region
   const unsigned blocks = (unsigned)(pairs * c->P());
   const bool small = blocks < 2u * 148u;
   // optionally split the key switch over digits for parallelism (HEI_SPLIT=1)
@@ -1792,7 +1845,7 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
   const uint32_t Lmax = std::max(c->L[0], c->L[1]);
   uint32_t* part = split ? pool_get(c->pool_part, c->pool_part_bytes, (size_t)blocks * Lmax * 2 * c->n * 4) : nullptr;
   uint32_t* result = (c->fold_elts.size() % 2) ? other : cur;
-  if (!small || c->timing || !c->graphs) return fold_impl(c, pairs, cur, other, st, split, part, dig);
+  if (!small || c->timing || !c->graphs) return fold_impl(c, pairs, cur, other, st, split, part, dig, dig2);
   for (auto& fg : c->fold_graphs)
     if (fg.pairs == pairs && fg.cur == cur && fg.other == other && fg.part == part && fg.dig == dig &&
         fg.gen == c->graph_gen &&
@@ -1804,7 +1857,7 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
   const uint64_t before = g_launches;
   cudaGraph_t graph = nullptr;
   CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  fold_impl(c, pairs, cur, other, st, split, part, dig);
+  fold_impl(c, pairs, cur, other, st, split, part, dig, dig2);
   CU(cudaStreamEndCapture(st, &graph));
   cudaGraphExec_t exec = nullptr;
   CU(cudaGraphInstantiate(&exec, graph, 0));
@@ -2369,6 +2422,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_NO_GRAPHS")) c->graphs = std::atoi(v) == 0;
     if (const char* v = std::getenv("HEI_TWO_STREAMS")) c->two_streams = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MT_JUMP")) c->mt_jump = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_FUSE_DIGITS")) c->fuse_digits = std::atoi(v) != 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
@@ -2623,6 +2677,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->d_dotA);
   cudaFree(c->d_dotB);
   cudaFree(c->d_dig);
+  cudaFree(c->d_dig2);
   for (auto& a : c->fold_ev)
     for (auto e : a) cudaEventDestroy(e);
   for (auto& fg : c->fold_graphs) cudaGraphExecDestroy(fg.exec);
