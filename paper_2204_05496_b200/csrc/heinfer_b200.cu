@@ -20,7 +20,8 @@
 //             k_rot_keyswitch  acc_i = sum_l NTT_i(digit_l mod q_i) (.) K[l][i],
 //                              dot <- dot + (acc0 + sigma(c0), acc1) }
 //   k_mask_acc      packed[g/N] += mask_{g mod N} (.) dot           (u64 RED)
-// and once per call k_finish (mod-q reduce + bias add_plain).
+// and once per call k_bias_plain (side stream) + k_finish_add (mod-q reduce + bias add_plain).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -462,7 +463,7 @@ __global__ void k_rot_keyswitch(Geo g, const uint32_t* __restrict__ dot, const u
 // packed[g / N] += mask_{g mod N} (.) dot   (matmul.cpp:329-338, mask :288-305)
 // mask = NTT_q(lift(INTT_t(onehot at index_map[slot]))), regenerated per pair
 // exactly as the reference does for N > 4096. u64 atomics make the packed
-// accumulation order-free (mod-q addition is exact; reduced in k_finish).
+// accumulation order-free (mod-q addition is exact; reduced in k_finish_add).
 __global__ void k_mask_acc(Geo g, const uint32_t* __restrict__ dot, const uint64_t* __restrict__ rows,
                            uint32_t cols, unsigned long long* __restrict__ acc64) {
   extern __shared__ uint32_t sm[];
@@ -496,8 +497,12 @@ __global__ void k_mask_acc(Geo g, const uint32_t* __restrict__ dot, const uint64
 // finish (matmul.cpp:342-374): reduce the u64 packed sums mod q and add the
 // bias pattern: part0 += NTT_q(Delta * INTT_t(scatter(pattern)))
 // (context.cpp:393-402). Block per (packed ct c, gp).
-__global__ void k_finish(Geo g, const unsigned long long* __restrict__ acc64, const int64_t* __restrict__ bias,
-                         uint32_t cols, uint64_t total, uint32_t* __restrict__ out) {
+// Bias plaintext of every packed ciphertext (MatmulStream::finish,
+// matmul.cpp:342-374): slot s of ct c carries bias[(cN + s) mod |Y|] while
+// cN + s < R|Y|; encode_slots -> INTT_t -> Delta * lift -> NTT_q. One block
+// per (c, prime); independent of the fold, so it runs on a side stream.
+__global__ void k_bias_plain(Geo g, const int64_t* __restrict__ bias, uint32_t cols, uint64_t total,
+                             uint32_t* __restrict__ biasp) {
   extern __shared__ uint32_t sm[];
   const uint32_t n = g.n;
   const uint64_t c = blockIdx.x / g.P;
@@ -518,13 +523,22 @@ __global__ void k_finish(Geo g, const unsigned long long* __restrict__ acc64, co
   for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = mul_shoup(sm[x], pr.delta.x, pr.delta.y, q);
   __syncthreads();
   ntt_fwd_smem(sm, g.fwd + (size_t)gp * n, q, n, g.logn);
-  const unsigned long long* a0 = acc64 + c * g.ct_words + (uint64_t)pr.poly0 * n;
-  const unsigned long long* a1 = acc64 + c * g.ct_words + (uint64_t)pr.poly1 * n;
-  uint32_t* o0 = out + c * g.ct_words + (uint64_t)pr.poly0 * n;
-  uint32_t* o1 = out + c * g.ct_words + (uint64_t)pr.poly1 * n;
-  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
-    o0[x] = add_mod((uint32_t)(a0[x] % q), sm[x], q);
-    o1[x] = (uint32_t)(a1[x] % q);
+  uint32_t* o = biasp + blockIdx.x * (uint64_t)n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) o[x] = sm[x];
+}
+
+// Packed accumulators mod q plus the bias plaintext on part 0.
+__global__ void k_finish_add(Geo g, const unsigned long long* __restrict__ acc64, const uint32_t* __restrict__ biasp,
+                             uint64_t C, uint32_t* __restrict__ out) {
+  const uint64_t total = C * g.ct_words;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = x / g.ct_words;
+    const uint32_t w = (uint32_t)(x % g.ct_words), poly = w / g.n, k = w % g.n;
+    const uint32_t gp = poly_prime(g, poly);
+    const PrimeInfo& pr = g.pr[gp];
+    uint32_t v = (uint32_t)(acc64[x] % pr.q);
+    if (poly == pr.poly0) v = add_mod(v, biasp[(c * g.P + gp) * g.n + k], pr.q);
+    out[x] = v;
   }
 }
 
@@ -933,6 +947,299 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
   }
 }
 
+
+// Latency path: the key switch of one (pair, prime i) split over a 2-CTA
+// cluster. Rank 0 takes the i == l term and the first ceil((L-1)/2) digits,
+// rank 1 the rest; partial accumulators are summed through distributed
+// shared memory (each rank finalises half of the slots), and rank 1 also
+// runs the next rotation's digit INTT from the c1' it collects in its own
+// shared memory. Same arithmetic as k_rot_keyswitch_s (all sums exact mod q),
+// about half the serial transform chain per rotation.
+template <int LOGN, bool NEXT>
+__global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keyswitch_c2(
+    Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ digits, const uint32_t* __restrict__ perm,
+    const uint2* __restrict__ key0, const uint2* __restrict__ key1, uint32_t* __restrict__ out, int fold,
+    const uint32_t* __restrict__ perm_next, uint32_t* __restrict__ dig_next) {
+  namespace cg = cooperative_groups;
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N, T = NT::T;
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t rank = cl.block_rank();
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  uint4* a0s = smem4 + N / 4;
+  uint4* a1s = a0s + 4 * T;
+  const uint32_t cid = blockIdx.x / 2;
+  const uint32_t pair = cid / g.P, gp = cid % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t q = pr.q, L = pr.L, i = pr.i;
+  const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
+  const uint32_t* ct = dot + (uint64_t)pair * g.ct_words;
+  const uint32_t* c0 = ct + (uint64_t)pr.poly0 * N;
+  const uint32_t* c1 = ct + (uint64_t)pr.poly1 * N;
+  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * N;
+  if (rank == 0) {  // the l == i term needs no transform
+    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * N) + j;
+    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * N) + j;
+    const uint4* pp = reinterpret_cast<const uint4*>(perm + x0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 pm = __ldg(pp + c);
+      const uint32_t d0 = c1[pm.x], d1 = c1[pm.y], d2 = c1[pm.z], d3 = c1[pm.w];
+      const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
+      const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
+      a0s[c * T + j] = make_uint4(mul_shoup(d0, a.x, a.y, q), mul_shoup(d1, a.z, a.w, q), mul_shoup(d2, b.x, b.y, q),
+                                  mul_shoup(d3, b.z, b.w, q));
+      a1s[c * T + j] = make_uint4(mul_shoup(d0, u.x, u.y, q), mul_shoup(d1, u.z, u.w, q), mul_shoup(d2, v.x, v.y, q),
+                                  mul_shoup(d3, v.z, v.w, q));
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      a0s[c * T + j] = make_uint4(0, 0, 0, 0);
+      a1s[c * T + j] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
+  const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
+  const uint32_t half = L / 2;  // digits (l != i) with index < half go to rank 0
+  uint32_t e[16];
+  for (uint32_t l = 0, k = 0; l < L; ++l) {
+    if (l == i) continue;
+    const uint32_t mine = (k++ < half) ? 0u : 1u;
+    if (mine != rank) continue;
+    const uint32_t* src = dig + (uint64_t)l * N;
+    if (pr.fast_reduce) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t v = src[NT::posA(j, r)];
+        e[r] = min(v, v - q);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
+    }
+    NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
+    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
+    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
+      uint4 A = a0s[c * T + j];
+      A.x = add_mod(A.x, mul_shoup(e[4 * c], a.x, a.y, q), q);
+      A.y = add_mod(A.y, mul_shoup(e[4 * c + 1], a.z, a.w, q), q);
+      A.z = add_mod(A.z, mul_shoup(e[4 * c + 2], b.x, b.y, q), q);
+      A.w = add_mod(A.w, mul_shoup(e[4 * c + 3], b.z, b.w, q), q);
+      a0s[c * T + j] = A;
+      const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
+      uint4 B = a1s[c * T + j];
+      B.x = add_mod(B.x, mul_shoup(e[4 * c], u.x, u.y, q), q);
+      B.y = add_mod(B.y, mul_shoup(e[4 * c + 1], u.z, u.w, q), q);
+      B.z = add_mod(B.z, mul_shoup(e[4 * c + 2], v.x, v.y, q), q);
+      B.w = add_mod(B.w, mul_shoup(e[4 * c + 3], v.z, v.w, q), q);
+      a1s[c * T + j] = B;
+    }
+  }
+  cl.sync();  // both partial accumulators complete; every NTT's use of sm is over
+  const uint4* r0 = cl.map_shared_rank(a0s, rank ^ 1u);
+  const uint4* r1 = cl.map_shared_rank(a1s, rank ^ 1u);
+  uint32_t* sm1 = cl.map_shared_rank(sm, 1u);  // c1' gathers in rank 1 for the next digit INTT
+  uint32_t* o = out + (uint64_t)pair * g.ct_words;
+  // rank r finalises chunks c in {2r, 2r + 1} of every thread's 16 elements
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    const int c = 2 * (int)rank + cc;
+    const uint32_t xc = x0 + 4 * c;
+    const uint4 pm = __ldg(reinterpret_cast<const uint4*>(perm + xc));
+    uint4 A = a0s[c * T + j], B = a1s[c * T + j];
+    const uint4 RA = r0[c * T + j], RB = r1[c * T + j];
+    A.x = add_mod(A.x, RA.x, q);
+    A.y = add_mod(A.y, RA.y, q);
+    A.z = add_mod(A.z, RA.z, q);
+    A.w = add_mod(A.w, RA.w, q);
+    B.x = add_mod(B.x, RB.x, q);
+    B.y = add_mod(B.y, RB.y, q);
+    B.z = add_mod(B.z, RB.z, q);
+    B.w = add_mod(B.w, RB.w, q);
+    A.x = add_mod(A.x, c0[pm.x], q);
+    A.y = add_mod(A.y, c0[pm.y], q);
+    A.z = add_mod(A.z, c0[pm.z], q);
+    A.w = add_mod(A.w, c0[pm.w], q);
+    if (fold) {
+      const uint4 u = *reinterpret_cast<const uint4*>(c0 + xc);
+      const uint4 v = *reinterpret_cast<const uint4*>(c1 + xc);
+      A.x = add_mod(A.x, u.x, q);
+      A.y = add_mod(A.y, u.y, q);
+      A.z = add_mod(A.z, u.z, q);
+      A.w = add_mod(A.w, u.w, q);
+      B.x = add_mod(B.x, v.x, q);
+      B.y = add_mod(B.y, v.y, q);
+      B.z = add_mod(B.z, v.z, q);
+      B.w = add_mod(B.w, v.w, q);
+    }
+    *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly0 * N + xc) = A;
+    *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly1 * N + xc) = B;
+    if constexpr (NEXT) *reinterpret_cast<uint4*>(sm1 + xc) = B;
+  }
+  cl.sync();  // remote reads of the accumulators and the c1' stores are complete
+  if constexpr (NEXT) {
+    if (rank == 1) {  // next rotation's digit: INTT of sigma'(c1') mod q_i
+      uint32_t pm[16];
+      load16_ro(perm_next + x0, pm);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) e[r] = sm[pm[r]];
+      __syncthreads();
+      NT::inv(e, sm, g.inv + (size_t)gp * N, g.itwc + (size_t)gp * g.twc_stride, q, pr.last, pr.ninv);
+      uint32_t* d = dig_next + ((uint64_t)pair * g.P + gp) * N;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) d[NT::posA(j, r)] = e[r];
+    }
+  }
+}
+
+// Latency path, one CTA per (pair, prime i) with TWO 512-thread groups:
+// group 0 takes the l == i term and the first floor(L/2) digits, group 1 the
+// rest, each into its own shared accumulators (group barriers, 32 warps per
+// SM instead of 16); the groups then finalise half of the slots each and
+// group 1 runs the next rotation's digit INTT. Same arithmetic as
+// k_rot_keyswitch_s.
+template <int LOGN, bool NEXT>
+__global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
+    Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ digits, const uint32_t* __restrict__ perm,
+    const uint2* __restrict__ key0, const uint2* __restrict__ key1, uint32_t* __restrict__ out, int fold,
+    const uint32_t* __restrict__ perm_next, uint32_t* __restrict__ dig_next) {
+  using NT = Ntt<LOGN, 2>;
+  constexpr uint32_t N = NT::N, T = NT::T;
+  extern __shared__ uint4 smem4[];
+  const uint32_t grp = threadIdx.x / T;
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4 + grp * (3 * N / 4));
+  uint4* a0s = smem4 + grp * (3 * N / 4) + N / 4;
+  uint4* a1s = a0s + 4 * T;
+  uint4* o0s = smem4 + (grp ^ 1u) * (3 * N / 4) + N / 4;  // the other group's accumulators
+  uint4* o1s = o0s + 4 * T;
+  uint32_t* sm1 = reinterpret_cast<uint32_t*>(smem4 + 3 * N / 4);  // group 1's buffer
+  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t q = pr.q, L = pr.L, i = pr.i;
+  const uint32_t j = threadIdx.x % T, x0 = NT::posC0(j);
+  const uint32_t* ct = dot + (uint64_t)pair * g.ct_words;
+  const uint32_t* c0 = ct + (uint64_t)pr.poly0 * N;
+  const uint32_t* c1 = ct + (uint64_t)pr.poly1 * N;
+  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * N;
+  if (grp == 0) {  // the l == i term needs no transform
+    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * N) + j;
+    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * N) + j;
+    const uint4* pp = reinterpret_cast<const uint4*>(perm + x0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 pm = __ldg(pp + c);
+      const uint32_t d0 = c1[pm.x], d1 = c1[pm.y], d2 = c1[pm.z], d3 = c1[pm.w];
+      const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
+      const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
+      a0s[c * T + j] = make_uint4(mul_shoup(d0, a.x, a.y, q), mul_shoup(d1, a.z, a.w, q), mul_shoup(d2, b.x, b.y, q),
+                                  mul_shoup(d3, b.z, b.w, q));
+      a1s[c * T + j] = make_uint4(mul_shoup(d0, u.x, u.y, q), mul_shoup(d1, u.z, u.w, q), mul_shoup(d2, v.x, v.y, q),
+                                  mul_shoup(d3, v.z, v.w, q));
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      a0s[c * T + j] = make_uint4(0, 0, 0, 0);
+      a1s[c * T + j] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
+  const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
+  const uint32_t half = L / 2;  // digits (l != i) with index < half go to group 0
+  uint32_t e[16];
+  for (uint32_t l = 0, k = 0; l < L; ++l) {
+    if (l == i) continue;
+    const uint32_t mine = (k++ < half) ? 0u : 1u;
+    if (mine != grp) continue;
+    const uint32_t* src = dig + (uint64_t)l * N;
+    if (pr.fast_reduce) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t v = src[NT::posA(j, r)];
+        e[r] = min(v, v - q);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
+    }
+    NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
+    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
+    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
+      uint4 A = a0s[c * T + j];
+      A.x = add_mod(A.x, mul_shoup(e[4 * c], a.x, a.y, q), q);
+      A.y = add_mod(A.y, mul_shoup(e[4 * c + 1], a.z, a.w, q), q);
+      A.z = add_mod(A.z, mul_shoup(e[4 * c + 2], b.x, b.y, q), q);
+      A.w = add_mod(A.w, mul_shoup(e[4 * c + 3], b.z, b.w, q), q);
+      a0s[c * T + j] = A;
+      const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
+      uint4 B = a1s[c * T + j];
+      B.x = add_mod(B.x, mul_shoup(e[4 * c], u.x, u.y, q), q);
+      B.y = add_mod(B.y, mul_shoup(e[4 * c + 1], u.z, u.w, q), q);
+      B.z = add_mod(B.z, mul_shoup(e[4 * c + 2], v.x, v.y, q), q);
+      B.w = add_mod(B.w, mul_shoup(e[4 * c + 3], v.z, v.w, q), q);
+      a1s[c * T + j] = B;
+    }
+  }
+  __syncthreads();  // both groups' accumulators complete; all transforms done
+  uint32_t* o = out + (uint64_t)pair * g.ct_words;
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {  // group r finalises chunks {2r, 2r + 1}
+    const int c = 2 * (int)grp + cc;
+    const uint32_t xc = x0 + 4 * c;
+    const uint4 pm = __ldg(reinterpret_cast<const uint4*>(perm + xc));
+    uint4 A = a0s[c * T + j], B = a1s[c * T + j];
+    const uint4 RA = o0s[c * T + j], RB = o1s[c * T + j];
+    A.x = add_mod(A.x, RA.x, q);
+    A.y = add_mod(A.y, RA.y, q);
+    A.z = add_mod(A.z, RA.z, q);
+    A.w = add_mod(A.w, RA.w, q);
+    B.x = add_mod(B.x, RB.x, q);
+    B.y = add_mod(B.y, RB.y, q);
+    B.z = add_mod(B.z, RB.z, q);
+    B.w = add_mod(B.w, RB.w, q);
+    A.x = add_mod(A.x, c0[pm.x], q);
+    A.y = add_mod(A.y, c0[pm.y], q);
+    A.z = add_mod(A.z, c0[pm.z], q);
+    A.w = add_mod(A.w, c0[pm.w], q);
+    if (fold) {
+      const uint4 u = *reinterpret_cast<const uint4*>(c0 + xc);
+      const uint4 v = *reinterpret_cast<const uint4*>(c1 + xc);
+      A.x = add_mod(A.x, u.x, q);
+      A.y = add_mod(A.y, u.y, q);
+      A.z = add_mod(A.z, u.z, q);
+      A.w = add_mod(A.w, u.w, q);
+      B.x = add_mod(B.x, v.x, q);
+      B.y = add_mod(B.y, v.y, q);
+      B.z = add_mod(B.z, v.z, q);
+      B.w = add_mod(B.w, v.w, q);
+    }
+    *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly0 * N + xc) = A;
+    *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly1 * N + xc) = B;
+    if constexpr (NEXT) *reinterpret_cast<uint4*>(sm1 + xc) = B;
+  }
+  if constexpr (NEXT) {
+    __syncthreads();  // c1' complete in group 1's buffer
+    if (grp == 1) {   // next rotation's digit: INTT of sigma'(c1') mod q_i
+      uint32_t pm[16];
+      load16_ro(perm_next + x0, pm);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) e[r] = sm[pm[r]];
+      NT::sync();
+      NT::inv(e, sm, g.inv + (size_t)gp * N, g.itwc + (size_t)gp * g.twc_stride, q, pr.last, pr.ninv);
+      uint32_t* d = dig_next + ((uint64_t)pair * g.P + gp) * N;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) d[NT::posA(j, r)] = e[r];
+    }
+  }
+}
 
 // Mask multiply + packed accumulation, G pairs per block (matmul.cpp:329-338).
 // The one-hot's INTT_t has a closed form: slot s sits at eval position
@@ -1498,6 +1805,8 @@ struct hei_gpu_ctx {
   // scratch (grown on demand)
   uint32_t *d_dotA = nullptr, *d_dotB = nullptr, *d_dig = nullptr, *d_dig2 = nullptr;
   bool fuse_digits = true;  // HEI_FUSE_DIGITS=0: separate digit kernel every rotation (small batches)
+  bool cluster_ks = false;  // HEI_CLUSTER_KS=1: 2-CTA cluster key switch on the latency path
+  bool group_ks = true;     // HEI_GROUP_KS=0: no 2-group CTA key switch on the latency path
   uint64_t scratch_pairs = 0;
   std::mutex mu;
   // grow-only device pools for the per-call buffers of the device-resident
@@ -1526,6 +1835,9 @@ struct hei_gpu_ctx {
   bool two_streams = true;  // HEI_TWO_STREAMS=0: fold the batch on one stream only
   bool mt_jump = true;      // HEI_MT_JUMP=0: sequential mt19937_64 replay only
   cudaStream_t side_stream = nullptr;
+  cudaStream_t bias_stream = nullptr;  // bias plaintext encoding, overlapped with the fold
+  uint32_t* pool_biasp = nullptr;
+  size_t pool_biasp_bytes = 0;
   struct FoldGraph {
     uint64_t pairs;
     uint32_t *cur, *other, *part, *dig;
@@ -1562,6 +1874,8 @@ struct hei_gpu_stream {
   unsigned long long* d_acc = nullptr;  // [C][twin ct] u64
   bool owns_acc = true, owns_rows = true;
   int64_t* d_bias = nullptr;  // staged bias (pool memory, not owned)
+  uint32_t* d_biasp = nullptr;      // bias plaintext [C][P][N] (pool memory)
+  cudaEvent_t bias_ev = nullptr;    // recorded when d_biasp was produced on the side stream
   // pending rows staged on the device
   std::vector<uint64_t> pend_idx;
   uint32_t* d_stage = nullptr;  // [cap][k][twin ct] u32
@@ -1667,12 +1981,51 @@ void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint
 }
 // Returns true when the launched kernel also produced the next rotation's
 // digits (k_rot_keyswitch_s with dig_next != nullptr).
+template <int LG, bool NEXT>
+void launch_ks_c2(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* dig,
+                  const uint32_t* perm, const uint2* k0, const uint2* k1, uint32_t* out, int fold, cudaStream_t st,
+                  const uint32_t* perm_next, uint32_t* dig_next) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * blocks);
+  cfg.blockDim = dim3(Ntt<LG>::T);
+  cfg.dynamicSmemBytes = smem_bytes(c, 3);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&cfg, k_rot_keyswitch_c2<LG, NEXT>, g, cur, dig, perm, k0, k1, out, fold, perm_next, dig_next));
+}
+
 template <int LG>
 void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* dig,
                  const uint32_t* perm, const uint2* k0, const uint2* k1, uint32_t* out, int fold, cudaStream_t st,
                  const uint32_t* perm_next, uint32_t* dig_next) {
   const size_t sm = smem_bytes(c, 3);
   const bool big = blocks >= 2u * 148u;
+  if constexpr (LG <= 13) {
+    if (!big && c->group_ks && blocks <= 148u) {  // latency path: one 2-group CTA per SM
+      const size_t sm2 = smem_bytes(c, 6);
+      if (dig_next)
+        k_rot_keyswitch_w2<LG, true><<<blocks, 2 * Ntt<LG>::T, sm2, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                         perm_next, dig_next);
+      else
+        k_rot_keyswitch_w2<LG, false><<<blocks, 2 * Ntt<LG>::T, sm2, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                          nullptr, nullptr);
+      return;
+    }
+  }
+  constexpr unsigned per_sm = LG <= 13 ? 2u : 1u;  // resident CTAs per SM (shared memory)
+  if (!big && c->cluster_ks && 2 * blocks <= per_sm * 148u) {  // latency path: 2-CTA clusters, one wave
+    if (dig_next)
+      launch_ks_c2<LG, true>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, perm_next, dig_next);
+    else
+      launch_ks_c2<LG, false>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, nullptr, nullptr);
+    return;
+  }
   if (dig_next) {
     if (big)
       k_rot_keyswitch_s<LG, true, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, perm_next,
@@ -1758,6 +2111,12 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, false>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, true>, 3 * sm);
+  set_smem_attr((const void*)k_rot_keyswitch_c2<LG, true>, 3 * sm);
+  set_smem_attr((const void*)k_rot_keyswitch_c2<LG, false>, 3 * sm);
+  if constexpr (LG <= 13) {
+    set_smem_attr((const void*)k_rot_keyswitch_w2<LG, true>, 6 * sm);
+    set_smem_attr((const void*)k_rot_keyswitch_w2<LG, false>, 6 * sm);
+  }
   set_smem_attr((const void*)k_mask_acc_f<LG>, sm);
   set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
   set_smem_attr((const void*)k_ks_part<LG>, sm);
@@ -1934,15 +2293,27 @@ void stream_flush(hei_gpu_stream* s) {
   s->pend_idx.clear();
 }
 
+void launch_bias_plain(hei_gpu_stream* s, const int64_t* d_bias, cudaStream_t st) {
+  hei_gpu_ctx* c = s->ctx;
+  s->d_biasp = pool_get(c->pool_biasp, c->pool_biasp_bytes, s->C * c->pt_words() * 4);
+  k_bias_plain<<<(unsigned)(s->C * c->P()), c->threads(), smem_bytes(c, 1), st>>>(
+      c->geo, d_bias, (uint32_t)s->w->cols, s->rows * s->w->cols, s->d_biasp);
+  LAUNCHED();
+}
+
 void finish_to(hei_gpu_stream* s, uint32_t* d_out, cudaStream_t st) {
   hei_gpu_ctx* c = s->ctx;
-  int64_t* d_bias = s->d_bias;
-  if (!d_bias) {  // streams created before the bias was staged (host API)
-    d_bias = pool_get(c->pool_bias, c->pool_bias_bytes, s->bias.size() * 8);
-    CU(cudaMemcpyAsync(d_bias, s->bias.data(), s->bias.size() * 8, cudaMemcpyHostToDevice, st));
+  if (s->bias_ev) {
+    CU(cudaStreamWaitEvent(st, s->bias_ev, 0));
+  } else {
+    int64_t* d_bias = s->d_bias;
+    if (!d_bias) {  // streams created before the bias was staged (host API)
+      d_bias = pool_get(c->pool_bias, c->pool_bias_bytes, s->bias.size() * 8);
+      CU(cudaMemcpyAsync(d_bias, s->bias.data(), s->bias.size() * 8, cudaMemcpyHostToDevice, st));
+    }
+    launch_bias_plain(s, d_bias, st);
   }
-  k_finish<<<(unsigned)(s->C * c->P()), c->threads(), smem_bytes(c, 1), st>>>(
-      c->geo, s->d_acc, d_bias, (uint32_t)s->w->cols, s->rows * s->w->cols, d_out);
+  k_finish_add<<<grid_for(s->C * c->ct_words(), 256), 256, 0, st>>>(c->geo, s->d_acc, s->d_biasp, s->C, d_out);
   LAUNCHED();
 }
 
@@ -2005,7 +2376,18 @@ hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64
     }
     std::memcpy(c->pinned_bias, s->bias.data(), bb);
     s->d_bias = pool_get(c->pool_bias, c->pool_bias_bytes, bb);
-    CU(cudaMemcpyAsync(s->d_bias, c->pinned_bias, bb, cudaMemcpyHostToDevice, zero_on ? zero_on : c->stream));
+    cudaStream_t zs = zero_on ? zero_on : c->stream;
+    CU(cudaMemcpyAsync(s->d_bias, c->pinned_bias, bb, cudaMemcpyHostToDevice, zs));
+    // encode the bias plaintext off the critical path, overlapping the fold
+    if (!c->bias_stream) CU(cudaStreamCreateWithFlags(&c->bias_stream, cudaStreamNonBlocking));
+    cudaEvent_t staged;
+    CU(cudaEventCreateWithFlags(&staged, cudaEventDisableTiming));
+    CU(cudaEventRecord(staged, zs));
+    CU(cudaStreamWaitEvent(c->bias_stream, staged, 0));
+    cudaEventDestroy(staged);
+    launch_bias_plain(s.get(), s->d_bias, c->bias_stream);
+    CU(cudaEventCreateWithFlags(&s->bias_ev, cudaEventDisableTiming));
+    CU(cudaEventRecord(s->bias_ev, c->bias_stream));
   }
   return s.release();
 }
@@ -2017,6 +2399,7 @@ void stream_free(hei_gpu_stream* s) {
   if (s->d_stage) cudaFree(s->d_stage);
   if (s->d_stage64) cudaFree(s->d_stage64);
   if (s->owns_rows) cudaFree(s->d_rows);
+  if (s->bias_ev) cudaEventDestroy(s->bias_ev);
   delete s;
 }
 
@@ -2423,6 +2806,8 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_TWO_STREAMS")) c->two_streams = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MT_JUMP")) c->mt_jump = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_DIGITS")) c->fuse_digits = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_CLUSTER_KS")) c->cluster_ks = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_GROUP_KS")) c->group_ks = std::atoi(v) != 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
@@ -2628,7 +3013,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     set_smem_attr((const void*)k_rot_keyswitch, s3);
     set_smem_attr((const void*)k_rot_digits, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_mask_acc, smem_bytes(c.get(), 1));
-    set_smem_attr((const void*)k_finish, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_bias_plain, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_ct_ntt, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_poly_ntt, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_encode_weights, smem_bytes(c.get(), 1));
@@ -2673,6 +3058,8 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->pool_in32);
   cudaFree(c->pool_out);
   cudaFree(c->pool_out64);
+  cudaFree(c->pool_biasp);
+  if (c->bias_stream) cudaStreamDestroy(c->bias_stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   cudaFree(c->d_dotA);
   cudaFree(c->d_dotB);

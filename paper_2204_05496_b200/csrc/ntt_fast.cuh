@@ -36,10 +36,20 @@ struct ParamTw {
 };
 __device__ __forceinline__ uint2 load_tw(ParamTw t, uint32_t i) { return t.p[i]; }
 
-template <int LOGN>
+// NG > 1: the CTA holds NG independent thread groups of T threads, each
+// transforming its own polynomial in its own shared buffer; the group
+// barriers are named barriers 1..NG (barrier 0 stays __syncthreads).
+template <int LOGN, int NG = 1>
 struct Ntt {
   static constexpr uint32_t N = 1u << LOGN;
   static constexpr uint32_t T = N / 16;          // threads per polynomial
+  static __device__ __forceinline__ uint32_t tid() { return NG == 1 ? threadIdx.x : threadIdx.x % T; }
+  static __device__ __forceinline__ void sync() {
+    if constexpr (NG == 1)
+      __syncthreads();
+    else
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + threadIdx.x / T), "r"(T) : "memory");
+  }
   static constexpr uint32_t G = N >> 8;          // pass-C block size
   static constexpr uint32_t TPG = G / 16;        // threads per pass-C block
   static constexpr int XST = LOGN - 12;          // cross-thread stages in pass C
@@ -120,7 +130,7 @@ struct Ntt {
   template <bool LAZY_OUT = false, typename TW = const uint2*>
   static __device__ __forceinline__ void fwd(uint32_t (&e)[16], uint32_t* sm, TW tw, const uint4* __restrict__ twc,
                                              uint32_t q) {
-    const uint32_t j = threadIdx.x;
+    const uint32_t j = tid();
     // ---- pass A: stages 0..3
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
@@ -129,10 +139,10 @@ struct Ntt {
       for (int r = 0; r < 16; ++r)
         if (!(r & half)) ct(e[r], e[r + half], load_tw(tw, (1 << s) + (r >> (4 - s))), q, red(r, half), red(r + half, half));
     }
-    __syncthreads();
+    sync();
 #pragma unroll
     for (int r = 0; r < 16; ++r) store_pos(sm, posA(j, r), e[r]);
-    __syncthreads();
+    sync();
     // ---- pass B: stages 4..7
 #pragma unroll
     for (int r = 0; r < 16; ++r) e[r] = sm[swz(posB(j, r))];
@@ -149,7 +159,7 @@ struct Ntt {
     }
 #pragma unroll
     for (int r = 0; r < 16; ++r) sm[swz(posB(j, r))] = e[r];
-    __syncthreads();
+    sync();
     // ---- pass C: stages 8..LOGN-1
     loadC(sm, j, e);
     const uint32_t x0 = posC0(j);
@@ -212,7 +222,7 @@ struct Ntt {
   template <typename TW = const uint2*>
   static __device__ __forceinline__ void inv(uint32_t (&e)[16], uint32_t* sm, TW itw, const uint4* __restrict__ itwc,
                                              uint32_t q, uint2 last, uint2 ninv) {
-    const uint32_t j = threadIdx.x;
+    const uint32_t j = tid();
     const uint32_t x0 = posC0(j);
     const uint4* tc = itwc + j;
     // ---- pass C: stages LOGN-1 .. 8 (register stages first: t = 1, 2, 4, 8)
@@ -263,9 +273,9 @@ struct Ntt {
         e[k + 8] = upper ? v : back;
       }
     }
-    __syncthreads();
+    sync();
     storeC(sm, j, e);
-    __syncthreads();
+    sync();
     // ---- pass B: stages 7..4
 #pragma unroll
     for (int r = 0; r < 16; ++r) e[r] = sm[swz(posB(j, r))];
@@ -281,7 +291,7 @@ struct Ntt {
     }
 #pragma unroll
     for (int r = 0; r < 16; ++r) sm[swz(posB(j, r))] = e[r];
-    __syncthreads();
+    sync();
     // ---- pass A: stages 3..1, then stage 0 fused with the n^-1 scaling
 #pragma unroll
     for (int r = 0; r < 16; ++r) e[r] = sm[swz(posA(j, r))];
