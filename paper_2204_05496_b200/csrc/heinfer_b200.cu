@@ -1339,6 +1339,57 @@ __global__ void __launch_bounds__(256) k_ks_reduce(Geo g, const uint32_t* __rest
   *reinterpret_cast<uint4*>(out + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n + x) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
 }
 
+// Latency path, split in two: the one-hot mask plaintexts (same closed form
+// as k_mask_acc_g) depend only on the slot, so k_mask_prep computes them on a
+// side stream while the fold runs; k_mask_apply then multiplies and adds.
+// masks [pair][P][N] in eval order.
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T) k_mask_prep(Geo g, const uint64_t* __restrict__ rows, uint32_t cols,
+                                                           uint32_t* __restrict__ masks) {
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N, T = NT::T;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t gp = blockIdx.x % g.P, pair = blockIdx.x / g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const BranchInfo& br = g.br[pr.b];
+  const uint32_t q = pr.q, t = br.t, j = threadIdx.x, x0 = NT::posC0(j);
+  const uint64_t gidx = rows[pair / cols] * cols + pair % cols;
+  const uint32_t slot = (uint32_t)(gidx % N);
+  const uint32_t pe = __brev(__ldg(&g.index_map[slot])) >> (32 - LOGN);
+  const uint32_t w = pow_barrett(br.psi_inv, 2 * pe + 1, t, br.mu);
+  const uint32_t wT = pow_barrett(w, T, t, br.mu);
+  uint32_t m = mul_barrett(br.ninv.x, pow_barrett(w, j, t, br.mu), t, br.mu);
+  uint32_t e[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    e[r] = m % q;
+    m = mul_barrett(m, wT, t, br.mu);
+  }
+  NT::fwd(e, sm, g.fwd + (size_t)gp * N, g.twc + (size_t)gp * g.twc_stride, q);
+  uint4* o = reinterpret_cast<uint4*>(masks + (uint64_t)blockIdx.x * N + x0);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) o[c] = make_uint4(e[4 * c], e[4 * c + 1], e[4 * c + 2], e[4 * c + 3]);
+}
+
+__global__ void k_mask_apply(Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ masks,
+                             const uint64_t* __restrict__ rows, uint32_t cols, uint64_t npairs,
+                             unsigned long long* __restrict__ acc64) {
+  const uint64_t per = (uint64_t)g.P * g.n, total = npairs * per;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t pair = x / per;
+    const uint32_t gp = (uint32_t)((x % per) / g.n), k = (uint32_t)(x % g.n);
+    const PrimeInfo& pr = g.pr[gp];
+    const uint64_t gidx = rows[pair / cols] * cols + pair % cols, c = gidx / g.n;
+    const uint32_t m = masks[x];
+    const uint32_t* base = dot + pair * g.ct_words;
+    const uint32_t a = mul_barrett(base[(uint64_t)pr.poly0 * g.n + k], m, pr.q, pr.mu);
+    const uint32_t b = mul_barrett(base[(uint64_t)pr.poly1 * g.n + k], m, pr.q, pr.mu);
+    atomicAdd(&acc64[c * g.ct_words + (uint64_t)pr.poly0 * g.n + k], (unsigned long long)a);
+    atomicAdd(&acc64[c * g.ct_words + (uint64_t)pr.poly1 * g.n + k], (unsigned long long)b);
+  }
+}
+
 template <int LOGN>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_mask_acc_g(Geo g, const uint32_t* __restrict__ dot,
                                                                const uint64_t* __restrict__ rows, uint32_t cols,
@@ -1838,6 +1889,9 @@ struct hei_gpu_ctx {
   cudaStream_t bias_stream = nullptr;  // bias plaintext encoding, overlapped with the fold
   uint32_t* pool_biasp = nullptr;
   size_t pool_biasp_bytes = 0;
+  uint32_t* pool_masks = nullptr;  // latency path: precomputed mask plaintexts
+  size_t pool_masks_bytes = 0;
+  bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   struct FoldGraph {
     uint64_t pairs;
     uint32_t *cur, *other, *part, *dig;
@@ -2119,6 +2173,7 @@ void set_fast_attrs(size_t sm) {
   }
   set_smem_attr((const void*)k_mask_acc_f<LG>, sm);
   set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
+  set_smem_attr((const void*)k_mask_prep<LG>, sm);
   set_smem_attr((const void*)k_ks_part<LG>, sm);
   set_smem_attr((const void*)k_ct_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_ct_intt_f<LG>, sm);
@@ -2275,11 +2330,39 @@ void run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
     cudaEventDestroy(join);
     return;
   }
+  // latency path: the mask plaintexts are computed on a side stream while
+  // the fold runs (they depend only on the slot)
+  const bool premask = c->logn >= 12 && c->logn <= 14 && blocksP < 2u * 148u && c->premask;
+  cudaEvent_t mask_ev = nullptr;
+  uint32_t* masks = nullptr;
+  if (premask) {
+    masks = pool_get(c->pool_masks, c->pool_masks_bytes, (size_t)blocksP * c->n * 4);
+    if (!c->bias_stream) CU(cudaStreamCreateWithFlags(&c->bias_stream, cudaStreamNonBlocking));
+    cudaEvent_t fork;
+    CU(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CU(cudaEventRecord(fork, st));
+    CU(cudaStreamWaitEvent(c->bias_stream, fork, 0));
+    cudaEventDestroy(fork);
+    const size_t sm1 = smem_bytes(c, 1);
+    HEI_DISPATCH(c->logn, (k_mask_prep<LG><<<blocksP, Ntt<LG>::T, sm1, c->bias_stream>>>(g, d_rows, cols, masks)),
+                 (void)0);
+    LAUNCHED();
+    CU(cudaEventCreateWithFlags(&mask_ev, cudaEventDisableTiming));
+    CU(cudaEventRecord(mask_ev, c->bias_stream));
+  }
   k_chunk_dot<<<(unsigned)(pairs * 2 * c->P()), std::min<unsigned>(T, c->n / 4), 0, st>>>(g, d_in, w->d_w, cols,
                                                                                          (uint32_t)w->kc, c->d_dotA);
   LAUNCHED();
   uint32_t* res = fold(c, pairs, c->d_dotA, c->d_dotB, st);
-  launch_mask_acc(c, g, blocksP, res, d_rows, cols, s->d_acc, st);
+  if (premask) {
+    CU(cudaStreamWaitEvent(st, mask_ev, 0));
+    cudaEventDestroy(mask_ev);
+    k_mask_apply<<<grid_for((uint64_t)blocksP * c->n, 256), 256, 0, st>>>(g, res, masks, d_rows, cols, pairs,
+                                                                         s->d_acc);
+    LAUNCHED();
+  } else {
+    launch_mask_acc(c, g, blocksP, res, d_rows, cols, s->d_acc, st);
+  }
 }
 
 void stream_flush(hei_gpu_stream* s) {
@@ -2808,6 +2891,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_FUSE_DIGITS")) c->fuse_digits = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_CLUSTER_KS")) c->cluster_ks = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_GROUP_KS")) c->group_ks = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
@@ -3059,6 +3143,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->pool_out);
   cudaFree(c->pool_out64);
   cudaFree(c->pool_biasp);
+  cudaFree(c->pool_masks);
   if (c->bias_stream) cudaStreamDestroy(c->bias_stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   cudaFree(c->d_dotA);
