@@ -172,6 +172,22 @@ int hei_gpu_matmul_partial_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, co
 int hei_gpu_finish_packed_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint64_t* d_acc,
                                  const int64_t* bias, uint64_t total_rows, uint32_t* d_out, void* stream);
 
+/* Feature-block sharding (C5 "shard by feature block"): rank r
+ * holds chunks [chunk_lo, chunk_lo + chunk_count) of every row
+ * (d_inputs [rows][chunk_count][twin ct] u32) and adds its chunk products,
+ * each reduced mod q, into d_dot [rows * cols][twin ct] u64 (zeroed by the
+ * caller). The ranks' d_dot partials sum exactly (reduce-scatter by rows);
+ * fold_pack then reduces the summed dots of rows [row_lo, row_lo + row_count)
+ * mod q, runs sum_all_slots and the mask into the packed accumulator d_acc
+ * (as matmul_partial_device does), and finish_packed_device completes it.
+ * Bit-exact with the single-GPU result: the chunk sum is reduced before
+ * sum_all_slots, as MatmulStream::push_row does (matmul.cpp:318-326). */
+int hei_gpu_chunk_dot_partial_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint32_t* d_inputs,
+                                     uint64_t rows, uint64_t chunk_lo, uint64_t chunk_count, uint64_t* d_dot,
+                                     void* stream);
+int hei_gpu_fold_pack_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint64_t* d_dot, uint64_t row_lo,
+                             uint64_t row_count, uint64_t total_rows, uint64_t* d_acc, void* stream);
+
 /* MatmulStream (matmul.hpp:83-114): rows in any order, each once. */
 int hei_gpu_stream_create(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const int64_t* bias,
                           uint64_t total_rows, hei_gpu_stream** out);

@@ -374,6 +374,37 @@ __global__ void k_chunk_dot(Geo g, const uint32_t* __restrict__ in, const uint2*
   }
 }
 
+// Feature-block sharding: the chunk products of chunks
+// [k0, k0 + kn) of every pair, each reduced mod q, added into an unreduced
+// u64 dot accumulator (ranks' partials sum exactly; reduced by k_dot_reduce).
+__global__ void k_chunk_dot_part(Geo g, const uint32_t* __restrict__ in, const uint2* __restrict__ W, uint32_t cols,
+                                 uint32_t kc, uint32_t k0, uint32_t kn, unsigned long long* __restrict__ dot) {
+  const uint32_t n = g.n, polys = 2 * g.P;
+  const uint32_t pair = blockIdx.x / polys, poly = blockIdx.x % polys;
+  const uint32_t s = pair / cols, j = pair % cols;
+  const uint32_t gp = poly_prime(g, poly);
+  const uint32_t q = g.pr[gp].q;
+  const uint32_t* src = in + ((uint64_t)s * kn * g.ct_words) + (uint64_t)poly * n;
+  const uint2* wj = W + ((uint64_t)j * kc * g.pt_words) + (uint64_t)gp * n;
+  unsigned long long* dst = dot + (uint64_t)pair * g.ct_words + (uint64_t)poly * n;
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+    uint32_t acc = 0;
+    for (uint32_t k = 0; k < kn; ++k) {
+      const uint2 wv = wj[(uint64_t)(k0 + k) * g.pt_words + x];
+      acc = add_mod(acc, mul_shoup(src[(uint64_t)k * g.ct_words + x], wv.x, wv.y, q), q);
+    }
+    dst[x] += acc;
+  }
+}
+
+__global__ void k_dot_reduce(Geo g, const unsigned long long* __restrict__ in, uint64_t cts, uint32_t* __restrict__ out) {
+  const uint64_t total = cts * g.ct_words;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t poly = (uint32_t)((x % g.ct_words) / g.n);
+    out[x] = (uint32_t)(in[x] % g.pr[poly_prime(g, poly)].q);
+  }
+}
+
 // digit_l = INTT_l(sigma(c1)_l), block per (pair, gp)  (context.cpp:455-459)
 __global__ void k_rot_digits(Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ perm,
                              uint32_t* __restrict__ digits) {
@@ -2290,6 +2321,16 @@ void require_keys(hei_gpu_ctx* c) {
       if (!c->key_index[b].count(e))
         raise(HEI_KEY_ERROR, "apply_galois: no key for galois element " + std::to_string(e));
   }
+}
+
+// Fold + mask of `nrows` rows whose per-pair dot ciphertexts (u32, eval form)
+// are already in c->d_dotA (feature-block sharding path).
+void run_folded_dots(hei_gpu_stream* s, const uint64_t* d_rows, uint64_t nrows, cudaStream_t st) {
+  hei_gpu_ctx* c = s->ctx;
+  const uint32_t cols = (uint32_t)s->w->cols;
+  const uint64_t pairs = nrows * cols;
+  uint32_t* res = fold(c, pairs, c->d_dotA, c->d_dotB, st);
+  launch_mask_acc(c, c->geo, (unsigned)(pairs * c->P()), res, d_rows, cols, s->d_acc, st);
 }
 
 // Core: process staged rows (device u32, eval form) into the packed u64 sums.
@@ -4234,6 +4275,60 @@ int hei_gpu_matmul_partial_device(hei_gpu_ctx* c, const hei_gpu_weights* w, cons
       for (uint64_t k = 0; k < nr; ++k) idx[k] = row_offset + r0 + k;
       CU(cudaMemcpyAsync(s->d_rows, idx.data(), nr * 8, cudaMemcpyHostToDevice, st));
       run_rows(s.get(), d_inputs + r0 * words, s->d_rows, nr, st);
+      CU(cudaStreamSynchronize(st));
+    }
+  });
+}
+
+int hei_gpu_chunk_dot_partial_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint32_t* d_inputs,
+                                     uint64_t rows, uint64_t chunk_lo, uint64_t chunk_count, uint64_t* d_dot,
+                                     void* stream) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!w) raise(HEI_PARAM_ERROR, "matmul: empty weights");
+    if (rows == 0 || chunk_count == 0 || chunk_lo + chunk_count > w->kc)
+      raise(HEI_PARAM_ERROR, "matmul: feature block out of range");
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    const uint64_t pairs = rows * w->cols;
+    k_chunk_dot_part<<<(unsigned)(pairs * 2 * c->P()), std::min<unsigned>(c->threads(), 256u), 0, st>>>(
+        c->geo, d_inputs, w->d_w, (uint32_t)w->cols, (uint32_t)w->kc, (uint32_t)chunk_lo, (uint32_t)chunk_count,
+        reinterpret_cast<unsigned long long*>(d_dot));
+    LAUNCHED();
+    CU(cudaStreamSynchronize(st));
+  });
+}
+
+int hei_gpu_fold_pack_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint64_t* d_dot, uint64_t row_lo,
+                             uint64_t row_count, uint64_t total_rows, uint64_t* d_acc, void* stream) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!w) raise(HEI_PARAM_ERROR, "matmul: empty weights");
+    if (row_count == 0 || row_lo + row_count > total_rows) raise(HEI_PARAM_ERROR, "matmul: shard rows out of range");
+    capacity_gate(c, w->f, "matmul");
+    require_keys(c);
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    hei_gpu_stream tmp{};
+    tmp.ctx = c;
+    tmp.w = w;
+    tmp.rows = total_rows;
+    tmp.C = (total_rows * w->cols + c->n - 1) / c->n;
+    tmp.d_acc = reinterpret_cast<unsigned long long*>(d_acc);
+    tmp.owns_acc = false;
+    tmp.owns_rows = false;
+    const uint64_t cap = std::max<uint64_t>(1, auto_batch_pairs(c) / w->cols);
+    uint64_t* d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, std::min(cap, row_count) * 8);
+    for (uint64_t r0 = 0; r0 < row_count; r0 += cap) {
+      const uint64_t nr = std::min(cap, row_count - r0);
+      ensure_scratch(c, nr * w->cols);
+      k_iota<<<grid_for(nr, 256), 256, 0, st>>>(d_rows, row_lo + r0, nr);
+      LAUNCHED();
+      k_dot_reduce<<<grid_for(nr * w->cols * c->ct_words(), 256), 256, 0, st>>>(
+          c->geo, reinterpret_cast<const unsigned long long*>(d_dot) + r0 * w->cols * c->ct_words(), nr * w->cols,
+          c->d_dotA);
+      LAUNCHED();
+      run_folded_dots(&tmp, d_rows, nr, st);
       CU(cudaStreamSynchronize(st));
     }
   });

@@ -1,4 +1,6 @@
-"""Individual (row) sharding across GPUs — one process per GPU.
+"""Sharding across GPUs — one process per GPU.
+
+Individual (row) sharding is the default:
 
 Every (individual, class) pipeline is independent; rank r takes a
 contiguous row block and accumulates the masked class results of its rows into
@@ -8,6 +10,14 @@ integer all-reduce of C * 2 * (L0 + L1) * N words (0.65 M words, 5.2 MB at
 C4), followed by the mod-q reduction and a single bias add_plain
 (MatmulStream::finish, matmul.cpp:342-374). Order-free, hence bit-exact for
 any rank count.
+
+Feature-block sharding (C5's second mode): rank r holds only chunks
+shard_chunks(kc, world, r) of every row, computes the chunk products of those
+chunks into an unreduced u64 dot accumulator, the ranks reduce-scatter the
+dot partials by rows (each rank receives the summed dots of its row block),
+and every rank folds and masks its rows as in individual sharding. The dot
+exchange is rows * cols * 2 (L0 + L1) N words, so it is an option for
+feature-partitioned inputs, not the default.
 """
 from __future__ import annotations
 
@@ -61,3 +71,48 @@ def reduce_packed_mod_q(acc: np.ndarray, q_per_poly: np.ndarray) -> np.ndarray:
     """Host-side reference of the mod-q reduction k_finish applies (used by
     the CPU multi-rank tests): acc [C][polys][N] u64 -> residues."""
     return (acc % q_per_poly[None, :, None].astype(np.uint64)).astype(np.uint64)
+
+
+def shard_chunks(kc: int, world: int, rank: int):
+    """Contiguous feature block (chunk range) of `rank`: (chunk_lo, count)."""
+    return shard_rows(kc, world, rank)
+
+
+def chunk_dot_partial_device(server, w, d_inputs_ptr: int, rows: int, chunk_lo: int, chunk_count: int, d_dot_ptr: int,
+                             stream_ptr: int = 0) -> None:
+    check(native.lib().hei_gpu_chunk_dot_partial_device(server.handle, w._h, C.c_void_p(d_inputs_ptr), C.c_uint64(rows),
+                                                        C.c_uint64(chunk_lo), C.c_uint64(chunk_count),
+                                                        C.c_void_p(d_dot_ptr), C.c_void_p(stream_ptr)))
+
+
+def fold_pack_device(server, w, d_dot_ptr: int, row_lo: int, row_count: int, total_rows: int, d_acc_ptr: int,
+                     stream_ptr: int = 0) -> None:
+    check(native.lib().hei_gpu_fold_pack_device(server.handle, w._h, C.c_void_p(d_dot_ptr), C.c_uint64(row_lo),
+                                                C.c_uint64(row_count), C.c_uint64(total_rows), C.c_void_p(d_acc_ptr),
+                                                C.c_void_p(stream_ptr)))
+
+
+def reduce_scatter_dots(dot, total_rows: int, group=None):
+    """Sum the ranks' dot partials (torch int64 [total_rows * cols][ct]) and
+    return this rank's row block (shard_rows) of the sum. Uses
+    reduce_scatter_tensor over equal padded blocks (NCCL on GPUs, gloo on
+    CPU); world 1 returns the input."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return dot
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    per_row = dot.shape[0] // total_rows
+    block = (total_rows + world - 1) // world
+    padded = torch.zeros((block * world * per_row,) + tuple(dot.shape[1:]), dtype=dot.dtype, device=dot.device)
+    padded[: dot.shape[0]] = dot
+    out = torch.empty((block * per_row,) + tuple(dot.shape[1:]), dtype=dot.dtype, device=dot.device)
+    if dot.device.type == "cpu" and dist.get_backend(group) == "gloo":
+        # gloo has no reduce_scatter: all-reduce and slice
+        dist.all_reduce(padded, op=dist.ReduceOp.SUM, group=group)
+        out.copy_(padded[rank * block * per_row:(rank + 1) * block * per_row])
+    else:
+        dist.reduce_scatter_tensor(out, padded, op=dist.ReduceOp.SUM, group=group)
+    lo, cnt = shard_rows(total_rows, world, rank)
+    return out[: cnt * per_row]

@@ -663,3 +663,43 @@ def test_keygen_rejection_planner_exact():
     assert [int(gpos[i]) for i in range(len(kinds)) if kinds[i] == 2] == [wpos[i] for i in range(len(kinds)) if kinds[i] == 2]
     with pytest.raises(RangeError):  # stream too short
         native.check(plan(p - 1))
+
+
+def test_feature_block_sharding_bit_exact(prod):
+    """Feature-block sharding (C5's second mode), two ranks emulated one after
+    the other on one GPU (no rank waits on another): each rank's chunk
+    products of its feature block, the dot partials summed as the
+    reduce-scatter would, each rank folding its row block into the packed
+    accumulator — bit-identical to the single-GPU matmul."""
+    import torch
+
+    from paper_2204_05496_b200 import EncodedWeights, matmul
+    from paper_2204_05496_b200.sharding import (chunk_dot_partial_device, finish_packed_device, fold_pack_device,
+                                                packed_count, shard_chunks, shard_rows)
+
+    o, s = prod
+    R, f, cols, world = 3, 20000, 2, 2
+    x, w, b = synthetic(R, f, cols, 0.05, 0.1, seed=21)
+    inputs = o.encode_inputs(x)  # [R][kc][ct]
+    wp = o.encode_weights(w)
+    ew = EncodedWeights.from_prepared(s, wp, f)
+    want, _ = matmul(s, inputs, ew, b)
+    kc, ctw = inputs.shape[1], inputs.shape[2]
+    dot = torch.zeros((R * cols, ctw), dtype=torch.int64, device="cuda")
+    for r in range(world):  # each rank: its feature block of every row
+        k0, kn = shard_chunks(kc, world, r)
+        blk = torch.from_numpy(inputs[:, k0:k0 + kn].astype(np.int64)).to(torch.int32).cuda().contiguous()
+        part = torch.zeros_like(dot)
+        chunk_dot_partial_device(s, ew, blk.data_ptr(), R, k0, kn, part.data_ptr())
+        dot += part  # the reduce-scatter's sum
+    torch.cuda.synchronize()
+    C_ = packed_count(R, cols, s.n)
+    acc = torch.zeros((C_, ctw), dtype=torch.int64, device="cuda")
+    for r in range(world):  # each rank folds its row block
+        lo, cnt = shard_rows(R, world, r)
+        fold_pack_device(s, ew, dot[lo * cols:].data_ptr(), lo, cnt, R, acc.data_ptr())
+    out = torch.empty((C_, ctw), dtype=torch.int32, device="cuda")
+    finish_packed_device(s, ew, acc.data_ptr(), b, R, out.data_ptr())
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert np.array_equal(got, want)

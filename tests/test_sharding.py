@@ -65,3 +65,45 @@ def test_gloo_all_reduce_of_partials_is_exact(tmp_path):
     a = reduce_packed_mod_q(got, q)
     b = reduce_packed_mod_q(sum(reduce_packed_mod_q(p, q) for p in parts), q)
     assert np.array_equal(a, b)
+
+
+def _fb_worker(rank, world, port, total_rows, result_path):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_05496_b200.sharding import reduce_scatter_dots
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cols, ct = 3, 8
+    rng = np.random.default_rng(200 + rank)
+    part = rng.integers(0, 2 ** 31, size=(total_rows * cols, ct), dtype=np.int64)  # one rank's chunk products
+    got = reduce_scatter_dots(torch.from_numpy(part), total_rows)
+    np.save(result_path % rank, got.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total_rows", [5, 8])
+def test_gloo_feature_block_reduce_scatter_is_exact(tmp_path, total_rows):
+    """Feature-block sharding's exchange: every rank receives exactly the sum
+    of all ranks' dot partials for its own row block (shard_rows), ragged
+    row counts included."""
+    from paper_2204_05496_b200.sharding import shard_chunks, shard_rows
+
+    world, cols, ct = 2, 3, 8
+    path = str(tmp_path / "rs_%d.npy")
+    mp.spawn(_fb_worker, args=(world, _free_port(), total_rows, path), nprocs=world, join=True)
+    total = sum(np.random.default_rng(200 + r).integers(0, 2 ** 31, size=(total_rows * cols, ct), dtype=np.int64)
+                for r in range(world))
+    for r in range(world):
+        lo, cnt = shard_rows(total_rows, world, r)
+        assert np.array_equal(np.load(path % r), total[lo * cols:(lo + cnt) * cols])
+    # chunk blocks partition the chunks exactly once
+    for kc in (1, 3, 5):
+        seen = []
+        for r in range(world):
+            lo, cnt = shard_chunks(kc, world, r)
+            seen += list(range(lo, lo + cnt))
+        assert seen == list(range(kc))
