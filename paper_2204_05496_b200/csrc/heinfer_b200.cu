@@ -1920,6 +1920,8 @@ struct hei_gpu_ctx {
   cudaStream_t bias_stream = nullptr;  // bias plaintext encoding, overlapped with the fold
   uint32_t* pool_biasp = nullptr;
   size_t pool_biasp_bytes = 0;
+  void* named_pool[16] = {};       // grow-only scratch for the client-role calls (baseline, encryption)
+  size_t named_pool_bytes[16] = {};
   uint32_t* pool_masks = nullptr;  // latency path: precomputed mask plaintexts
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
@@ -2006,6 +2008,21 @@ T* pool_get(T*& p, size_t& cap, size_t bytes) {
     cap = bytes;
   }
   return p;
+}
+
+// Grow-only scratch slot `id` of the context (reused across calls; every
+// C-ABI call synchronises before returning).
+enum ScratchId { kScrRawAll = 0, kScrRaw, kScrNoise, kScrM, kScrCt, kScrWc, kScrAcc, kScrOut, kScrOut64, kScrX };
+template <typename T>
+T* scratch(hei_gpu_ctx* c, int id, size_t bytes) {
+  void*& p = c->named_pool[id];
+  if (bytes > c->named_pool_bytes[id]) {
+    if (p) CU(cudaFree(p));
+    p = nullptr;
+    CU(cudaMalloc(&p, bytes));
+    c->named_pool_bytes[id] = bytes;
+  }
+  return reinterpret_cast<T*>(p);
 }
 
 void ensure_scratch(hei_gpu_ctx* c, uint64_t pairs) {
@@ -3185,6 +3202,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->pool_out64);
   cudaFree(c->pool_biasp);
   cudaFree(c->pool_masks);
+  for (int k = 0; k < 16; ++k) cudaFree(c->named_pool[k]);
   if (c->bias_stream) cudaStreamDestroy(c->bias_stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   cudaFree(c->d_dotA);
@@ -4105,15 +4123,15 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     alloc(&d_x, rows * f * 8);
     alloc(&d_w, f * cols * 8);
     alloc(&d_bias, cols * 8);
-    alloc(&d_wc, f * cols * P * sizeof(uint2));
-    alloc(&d_acc, outw * 8);
-    alloc(&d_raw, 2 * 2 * Emax * 3 * n * 8);  // [slot][branch][draws]
+    d_wc = scratch<uint2>(c, kScrWc, f * cols * P * sizeof(uint2));
+    d_acc = scratch<unsigned long long>(c, kScrAcc, outw * 8);
+    d_raw = scratch<uint64_t>(c, kScrRaw, 2 * 2 * Emax * 3 * n * 8);  // [slot][branch][draws]
     alloc(&d_state, 2 * 313 * 8);
-    alloc(&d_noise, Emax * 2 * 3 * n);
-    alloc(&d_m, Emax * 2 * n * 4);
-    alloc(&d_ct, Emax * c->ct_words() * 4);
-    alloc(&d_out, outw * 4);
-    alloc(&d_out64, outw * 8);
+    d_noise = scratch<int8_t>(c, kScrNoise, Emax * 2 * 3 * n);
+    d_m = scratch<uint32_t>(c, kScrM, Emax * 2 * n * 4);
+    d_ct = scratch<uint32_t>(c, kScrCt, Emax * c->ct_words() * 4);
+    d_out = scratch<uint32_t>(c, kScrOut, outw * 4);
+    d_out64 = scratch<uint64_t>(c, kScrOut64, outw * 8);
     CU(cudaMemcpyAsync(d_x, x, rows * f * 8, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(d_w, w, f * cols * 8, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(d_bias, bias, cols * 8, cudaMemcpyHostToDevice, st));
@@ -4150,7 +4168,7 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
       alloc(&d_cur, 2 * 313 * 8);
       alloc(&d_wseq, 2ull * wlen * 8);
       alloc(&d_part, 2ull * S * 312 * 8);
-      alloc(&d_rawall, 2 * Dtot * 8);
+      d_rawall = scratch<uint64_t>(c, kScrRawAll, 2 * Dtot * 8);
       CU(cudaMemcpyAsync(d_poly, poly.data(), poly.size() * 8, cudaMemcpyHostToDevice, st));
       // chunk 0 starts at the current (block-aligned) state
       for (int bb = 0; bb < 2; ++bb) {
