@@ -1637,7 +1637,8 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T) k_bl_encrypt(Geo g, const int8_t
 
 // acc[blk][j] += sum_k ct[k, blk] * w(k, j) mod q, lazily in u64
 // (mul_plain + add_inplace of matmul.cpp:453-459). Thread per slot x of one
-// poly; weights of the batch for this branch sit in shared memory.
+// poly; weights of the batch for this branch sit in shared memory. The
+// feature loop is unrolled so several coalesced loads are in flight.
 constexpr int kBlJ = 12;
 __global__ void k_bl_accum(Geo g, const uint32_t* __restrict__ cts, uint32_t F, uint32_t B, uint32_t cols,
                            uint32_t j0, const uint2* __restrict__ wc, unsigned long long* __restrict__ acc) {
@@ -1648,7 +1649,7 @@ __global__ void k_bl_accum(Geo g, const uint32_t* __restrict__ cts, uint32_t F, 
   const uint32_t poly = (blockIdx.x / tiles) % polys;
   const uint32_t blk = blockIdx.x / (tiles * polys);
   const uint32_t gp = poly_prime(g, poly);
-  const uint32_t q = g.pr[gp].q, b = g.pr[gp].b;
+  const uint32_t q = g.pr[gp].q;
   const uint32_t jn = min((uint32_t)kBlJ, cols - j0);
   for (uint32_t x = threadIdx.x; x < F * kBlJ; x += blockDim.x) {
     const uint32_t kk = x / kBlJ, jj = x % kBlJ;
@@ -1656,11 +1657,14 @@ __global__ void k_bl_accum(Geo g, const uint32_t* __restrict__ cts, uint32_t F, 
   }
   __syncthreads();
   const uint32_t xs = tile * blockDim.x + threadIdx.x;
+  const uint32_t* src = cts + (uint64_t)blk * g.ct_words + (uint64_t)poly * n + xs;
+  const uint64_t stride = (uint64_t)B * g.ct_words;
   unsigned long long a[kBlJ];
 #pragma unroll
   for (int jj = 0; jj < kBlJ; ++jj) a[jj] = 0;
+#pragma unroll 4
   for (uint32_t kk = 0; kk < F; ++kk) {
-    const uint32_t v = cts[((uint64_t)kk * B + blk) * g.ct_words + (uint64_t)poly * n + xs];
+    const uint32_t v = src[kk * stride];
 #pragma unroll
     for (int jj = 0; jj < kBlJ; ++jj) {
       const uint2 w = wsm[kk * kBlJ + jj];
@@ -1668,10 +1672,12 @@ __global__ void k_bl_accum(Geo g, const uint32_t* __restrict__ cts, uint32_t F, 
       a[jj] += (uint32_t)(v * w.x - qh * q);  // in [0, 2q): reduced at the end
     }
   }
-  (void)b;
-  for (uint32_t jj = 0; jj < jn; ++jj) {
-    unsigned long long* d = acc + (((uint64_t)blk * cols + j0 + jj) * g.ct_words) + (uint64_t)poly * n + xs;
-    *d += a[jj];
+#pragma unroll
+  for (uint32_t jj = 0; jj < kBlJ; ++jj) {
+    if (jj < jn) {
+      unsigned long long* d = acc + (((uint64_t)blk * cols + j0 + jj) * g.ct_words) + (uint64_t)poly * n + xs;
+      *d += a[jj];
+    }
   }
 }
 
