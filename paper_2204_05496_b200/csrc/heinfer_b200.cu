@@ -1294,7 +1294,7 @@ __device__ __forceinline__ uint32_t pow_barrett(uint32_t b, uint32_t e, uint32_t
 // untransformed l == i term); k_ks_reduce sums the L partials and adds the
 // fold terms. Same arithmetic as k_rot_keyswitch_s, L x more parallelism.
 template <int LOGN>
-__global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_ks_part(Geo g, const uint32_t* __restrict__ dot,
+__global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_ks_part(Geo g, const uint32_t* __restrict__ dot,
                                                             const uint32_t* __restrict__ digits,
                                                             const uint32_t* __restrict__ perm,
                                                             const uint2* __restrict__ key0,
@@ -1422,7 +1422,7 @@ __global__ void k_mask_apply(Geo g, const uint32_t* __restrict__ dot, const uint
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_mask_acc_g(Geo g, const uint32_t* __restrict__ dot,
+__global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_mask_acc_g(Geo g, const uint32_t* __restrict__ dot,
                                                                const uint64_t* __restrict__ rows, uint32_t cols,
                                                                uint32_t npairs, uint32_t G,
                                                                unsigned long long* __restrict__ acc64) {
@@ -1499,41 +1499,6 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_mask_acc_g(Geo g, const uin
   if (c_cur != ~0ull) flush(c_cur);
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(Ntt<LOGN>::T, 2) k_mask_acc_f(Geo g, const uint32_t* __restrict__ dot,
-                                                            const uint64_t* __restrict__ rows, uint32_t cols,
-                                                            unsigned long long* __restrict__ acc64) {
-  using NT = Ntt<LOGN>;
-  constexpr uint32_t N = NT::N;
-  extern __shared__ uint4 smem4[];
-  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
-  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
-  const PrimeInfo& pr = g.pr[gp];
-  const BranchInfo& br = g.br[pr.b];
-  const uint64_t gidx = rows[pair / cols] * cols + pair % cols;
-  const uint32_t slot = (uint32_t)(gidx % N);
-  const uint64_t c = gidx / N;
-  const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
-  const uint32_t hot = __ldg(&g.index_map[slot]);
-  uint32_t e[16];
-#pragma unroll
-  for (int r = 0; r < 16; ++r) e[r] = (x0 + r == hot) ? 1u : 0u;
-  NT::inv(e, sm, g.inv + (size_t)(g.P + pr.b) * N, g.itwc + (size_t)(g.P + pr.b) * g.twc_stride, br.t, br.last, br.ninv);
-  const uint32_t q = pr.q;
-#pragma unroll
-  for (int r = 0; r < 16; ++r) e[r] = e[r] % q;
-  NT::fwd(e, sm, g.fwd + (size_t)gp * N, g.twc + (size_t)gp * g.twc_stride, q);
-  uint32_t d[16];
-  const uint32_t* base = dot + (uint64_t)pair * g.ct_words;
-  unsigned long long* a0 = acc64 + c * g.ct_words + (uint64_t)pr.poly0 * N + x0;
-  unsigned long long* a1 = acc64 + c * g.ct_words + (uint64_t)pr.poly1 * N + x0;
-  load16(base + (uint64_t)pr.poly0 * N + x0, d);
-#pragma unroll
-  for (int r = 0; r < 16; ++r) atomicAdd(&a0[r], (unsigned long long)mul_barrett(d[r], e[r], q, pr.mu));
-  load16(base + (uint64_t)pr.poly1 * N + x0, d);
-#pragma unroll
-  for (int r = 0; r < 16; ++r) atomicAdd(&a1[r], (unsigned long long)mul_barrett(d[r], e[r], q, pr.mu));
-}
 
 // ---------------------------------------------------------------------------
 // Standard algorithm (baseline_matmul) kernels; see baseline.cuh.
@@ -1582,10 +1547,12 @@ __device__ __forceinline__ uint32_t lift_small(int32_t v, uint32_t q) { return v
 // c1 = NTT(u) pk1 + NTT(e1). pk is prepared [gp][part] in the pass-C
 // transposed layout.
 template <int LOGN>
-__global__ void __launch_bounds__(Ntt<LOGN>::T) k_bl_encrypt(Geo g, const int8_t* __restrict__ noise,
+__global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_bl_encrypt(Geo g, const int8_t* __restrict__ noise,
                                                             const uint32_t* __restrict__ m,
                                                             const uint2* __restrict__ pkd,
                                                             uint32_t* __restrict__ cts) {
+  // c0 = NTT(u) pk0 + NTT(e0 + Delta m), c1 = NTT(u) pk1 + NTT(e1)
+  // (encrypt_parts, context.cpp:262-303); one transform live at a time.
   using NT = Ntt<LOGN>;
   constexpr uint32_t N = NT::N, T = NT::T;
   extern __shared__ uint4 smem4[];
@@ -1598,41 +1565,46 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T) k_bl_encrypt(Geo g, const int8_t
   const uint2* tw = g.fwd + (size_t)gp * N;
   const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
   uint32_t* ct = cts + (uint64_t)e * g.ct_words;
-  uint32_t* c0 = ct + (uint64_t)pr.poly0 * N + x0;
-  uint32_t* c1 = ct + (uint64_t)pr.poly1 * N + x0;
+  uint4* c0 = reinterpret_cast<uint4*>(ct + (uint64_t)pr.poly0 * N + x0);
+  uint4* c1 = reinterpret_cast<uint4*>(ct + (uint64_t)pr.poly1 * N + x0);
   const uint4* p0 = reinterpret_cast<const uint4*>(pkd + (uint64_t)(2 * gp) * N) + j;
   const uint4* p1 = reinterpret_cast<const uint4*>(pkd + (uint64_t)(2 * gp + 1) * N) + j;
-  uint32_t v[16], w[16];
+  uint32_t v[16];
+  // one transform instance (a rolled phase loop keeps the compiler from
+  // hoisting the shared twiddles of three inlined NTTs into registers)
+#pragma unroll 1
+  for (int ph = 0; ph < 3; ++ph) {
+    if (ph == 1) {
 #pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = lift_small(nz[NT::posA(j, r)], q);
-  NT::fwd(v, sm, tw, twc, q);
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t pa = NT::posA(j, r);
+        v[r] = add_mod(lift_small(nz[N + pa], q), mul_shoup(mm[pa], pr.delta.x, pr.delta.y, q), q);
+      }
+    } else {
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const uint4 a = __ldg(p0 + c * T), bb = __ldg(p1 + c * T);
-    w[2 * c] = mul_shoup(v[2 * c], bb.x, bb.y, q);
-    w[2 * c + 1] = mul_shoup(v[2 * c + 1], bb.z, bb.w, q);
-    v[2 * c] = mul_shoup(v[2 * c], a.x, a.y, q);
-    v[2 * c + 1] = mul_shoup(v[2 * c + 1], a.z, a.w, q);
+      for (int r = 0; r < 16; ++r) v[r] = lift_small(nz[(uint32_t)ph * N + NT::posA(j, r)], q);
+    }
+    NT::fwd(v, sm, tw, twc, q);
+    if (ph == 0) {  // NTT(u) pk0 -> c0, NTT(u) pk1 -> c1
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 a0 = __ldg(p0 + (2 * c) * T), a1 = __ldg(p0 + (2 * c + 1) * T);
+        const uint4 b0 = __ldg(p1 + (2 * c) * T), b1 = __ldg(p1 + (2 * c + 1) * T);
+        c1[c] = make_uint4(mul_shoup(v[4 * c], b0.x, b0.y, q), mul_shoup(v[4 * c + 1], b0.z, b0.w, q),
+                           mul_shoup(v[4 * c + 2], b1.x, b1.y, q), mul_shoup(v[4 * c + 3], b1.z, b1.w, q));
+        c0[c] = make_uint4(mul_shoup(v[4 * c], a0.x, a0.y, q), mul_shoup(v[4 * c + 1], a0.z, a0.w, q),
+                           mul_shoup(v[4 * c + 2], a1.x, a1.y, q), mul_shoup(v[4 * c + 3], a1.z, a1.w, q));
+      }
+    } else {  // c0 += NTT(e0 + Delta m), c1 += NTT(e1)
+      uint4* cp = ph == 1 ? c0 : c1;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 u = cp[c];
+        cp[c] = make_uint4(add_mod(u.x, v[4 * c], q), add_mod(u.y, v[4 * c + 1], q), add_mod(u.z, v[4 * c + 2], q),
+                           add_mod(u.w, v[4 * c + 3], q));
+      }
+    }
   }
-  store16(c0, v);
-  store16(c1, w);
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const uint32_t pa = NT::posA(j, r);
-    v[r] = add_mod(lift_small(nz[N + pa], q), mul_shoup(mm[pa], pr.delta.x, pr.delta.y, q), q);
-  }
-  NT::fwd(v, sm, tw, twc, q);
-  load16(c0, w);
-#pragma unroll
-  for (int r = 0; r < 16; ++r) w[r] = add_mod(w[r], v[r], q);
-  store16(c0, w);
-#pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = lift_small(nz[2 * N + NT::posA(j, r)], q);
-  NT::fwd(v, sm, tw, twc, q);
-  load16(c1, w);
-#pragma unroll
-  for (int r = 0; r < 16; ++r) w[r] = add_mod(w[r], v[r], q);
-  store16(c1, w);
 }
 
 // acc[blk][j] += sum_k ct[k, blk] * w(k, j) mod q, lazily in u64
@@ -2225,7 +2197,6 @@ void set_fast_attrs(size_t sm) {
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, true>, 6 * sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, false>, 6 * sm);
   }
-  set_smem_attr((const void*)k_mask_acc_f<LG>, sm);
   set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
   set_smem_attr((const void*)k_mask_prep<LG>, sm);
   set_smem_attr((const void*)k_ks_part<LG>, sm);
