@@ -318,6 +318,9 @@ def run_ours(args, world, rank, local):
     if world > 1:
         torch.distributed.barrier()
     native.reset_launch_count()
+    prof = os.environ.get("HEI_PROFILE_STEPS") == "1"  # ncu --profile-from-start off: timed steps only
+    if prof:
+        torch.cuda.cudart().cudaProfilerStart()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         torch.cuda.synchronize()
@@ -327,6 +330,8 @@ def run_ours(args, world, rank, local):
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = native.launch_count()
+    if prof:
+        torch.cuda.cudart().cudaProfilerStop()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)

@@ -2777,14 +2777,14 @@ void encode_inputs_impl(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_
   uint64_t *d_raw = nullptr, *d_state = nullptr, *d_out64 = nullptr;
   int8_t* d_noise = nullptr;
   uint32_t *d_m = nullptr, *d_ct = nullptr;
-  alloc(&d_x, rows * f * 8);
-  alloc(&d_raw, 2 * Dtot * 8);
+  d_x = scratch<int64_t>(c, kScrX, rows * f * 8);
+  d_raw = scratch<uint64_t>(c, kScrRawAll, 2 * Dtot * 8);
   alloc(&d_state, 2 * 313 * 8);
-  alloc(&d_noise, Eb * 2 * 3 * n);
-  alloc(&d_m, Eb * 2 * n * 4);
+  d_noise = scratch<int8_t>(c, kScrNoise, Eb * 2 * 3 * n);
+  d_m = scratch<uint32_t>(c, kScrM, Eb * 2 * n * 4);
   if (!out_dev) {
-    alloc(&d_ct, Eb * c->ct_words() * 4);
-    alloc(&d_out64, Eb * c->ct_words() * 8);
+    d_ct = scratch<uint32_t>(c, kScrCt, Eb * c->ct_words() * 4);
+    d_out64 = scratch<uint64_t>(c, kScrOut64, Eb * c->ct_words() * 8);
   }
   CU(cudaMemcpyAsync(d_x, x, rows * f * 8, cudaMemcpyHostToDevice, st));
   const hei_gpu_prng init0 = *rng0, init1 = *rng1;
