@@ -259,12 +259,20 @@ def run_ours(args, world, rank, local):
 
     R_total, f, cols, n, pf, ws = CONFIGS[args.config]
     R = args.rows or R_total  # per rank (weak scaling: every rank gets the full per-GPU batch)
+    # one process per GPU; the modulo only matters for the plumbing check below
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        # HEI_DIST_BACKEND=gloo: host-side exchange, used only to check the
+        # multi-rank plumbing on a single-GPU box (never for numbers)
+        backend = os.environ.get("HEI_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_2204_05496_b200 import Prng, encode_inputs_device
 
     srv, q0, q1, keygen_ms = make_server(n, local)
@@ -288,6 +296,7 @@ def run_ours(args, world, rank, local):
         enc_ms = (time.perf_counter() - t0) * 1000.0
     C_ = (R * cols + n - 1) // n
     d_out = torch.empty((C_, ctw), dtype=torch.int32, device=dev)
+    d_one = torch.empty((C_, ctw), dtype=torch.int32, device=dev)  # rank-local result (roofline step)
 
     if world == 1:
         def step():
@@ -365,7 +374,8 @@ def run_ours(args, world, rank, local):
     roof = int_roof = None
     if rank == 0:
         native.kernel_timing(srv.handle, True)
-        step()
+        # the rank's own fold work only: no collective, so rank 0 can time it alone
+        matmul_device(srv, d_in.data_ptr(), R, ew, b, d_one.data_ptr(), stream.cuda_stream)
         torch.cuda.synchronize()
         ks_n, ks_ms = native.kernel_stats(srv.handle, 0)
         dg_n, dg_ms = native.kernel_stats(srv.handle, 1)
@@ -498,6 +508,11 @@ def main():
         run_reference(args, world, rank)
         return
     run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

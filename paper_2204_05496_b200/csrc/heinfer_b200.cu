@@ -914,7 +914,7 @@ void capacity_gate(hei_gpu_ctx* c, uint64_t f, const char* who) {
 }
 
 hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64_t* bias, uint64_t rows,
-                           bool host_staging = true, cudaStream_t zero_on = nullptr) {
+                           bool host_staging = true, cudaStream_t zero_on = nullptr, bool encode_bias = true) {
   if (rows == 0) raise(HEI_PARAM_ERROR, "matmul: empty input");
   if (!w || w->cols == 0 || w->f == 0) raise(HEI_PARAM_ERROR, "matmul: empty weights");
   if (w->ctx != c) raise(HEI_PARAM_ERROR, "matmul: weights encoded for a different context");
@@ -943,7 +943,7 @@ hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64
     s->owns_rows = false;
   }
   CU(cudaMemsetAsync(s->d_acc, 0, s->C * c->ct_words() * 8, zero_on ? zero_on : c->stream));
-  if (!host_staging) {
+  if (!host_staging && encode_bias) {
     // stage the bias now (pinned, async): every earlier call has synchronised
     const size_t bb = s->bias.size() * 8;
     if (bb > c->pinned_bias_bytes) {
@@ -2712,26 +2712,27 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
 // ---- sharded (multi-GPU) building blocks: partial packed sums + finish ----
 int hei_gpu_matmul_partial_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint32_t* d_inputs, uint64_t rows,
                                   uint64_t row_offset, uint64_t total_rows, uint64_t* d_acc, void* stream) {
+  // Same enqueue-only structure as matmul_device (device row ids, no mid-call
+  // host round trips); the bias is added once by finish_packed_device.
   return guarded([&] {
     set_device(c);
     std::lock_guard<std::mutex> lk(c->mu);
     if (rows == 0 || row_offset + rows > total_rows) raise(HEI_PARAM_ERROR, "matmul: shard rows out of range");
     cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
-    std::vector<int64_t> zero_bias(w->cols, 0);
-    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, zero_bias.data(), total_rows, false),
-                                                                  stream_free);
-    CU(cudaStreamSynchronize(c->stream));
+    std::vector<int64_t> zero_bias(w ? w->cols : 1, 0);
+    std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(
+        stream_new(c, w, zero_bias.data(), total_rows, false, st, /*encode_bias=*/false), stream_free);
     s->d_acc = reinterpret_cast<unsigned long long*>(d_acc);  // the caller's buffer
     s->owns_acc = false;
     const size_t words = w->kc * c->ct_words();
-    std::vector<uint64_t> idx(s->cap_rows);
+    uint64_t* d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, rows * 8);
+    k_iota<<<grid_for(rows, 256), 256, 0, st>>>(d_rows, row_offset, rows);
+    LAUNCHED();
     for (uint64_t r0 = 0; r0 < rows; r0 += s->cap_rows) {
       const uint64_t nr = std::min<uint64_t>(s->cap_rows, rows - r0);
-      for (uint64_t k = 0; k < nr; ++k) idx[k] = row_offset + r0 + k;
-      CU(cudaMemcpyAsync(s->d_rows, idx.data(), nr * 8, cudaMemcpyHostToDevice, st));
-      run_rows(s.get(), d_inputs + r0 * words, s->d_rows, nr, st);
-      CU(cudaStreamSynchronize(st));
+      run_rows(s.get(), d_inputs + r0 * words, d_rows + r0, nr, st);
     }
+    CU(cudaStreamSynchronize(st));
   });
 }
 
