@@ -453,13 +453,18 @@ def run_ours(args, world, rank, local):
     # client side of the result: decrypt + CRT unpack on the device
     # (unpack_results, matmul.cpp:257-271), checked against the exact product
     check = None
-    if world == 1 and rank == 0:
+    if rank == 0:
+        # world > 1: d_out is the all-reduced result of every rank's rows
+        # (rank r encrypted synthetic(seed = 7 + r)); rank 0 regenerates them
+        rows_all = world * R
         packed = d_out.cpu().numpy().view(np.uint32).astype(np.uint64)
-        srv.unpack_results(packed, R, cols)  # warm
+        srv.unpack_results(packed, rows_all, cols)  # warm
         t0 = time.perf_counter()
-        got = srv.unpack_results(packed, R, cols)
+        got = srv.unpack_results(packed, rows_all, cols)
         dec_ms = (time.perf_counter() - t0) * 1000.0
-        want = np.rint(x.astype(np.float64) @ w.astype(np.float64)).astype(np.int64) + b  # exact: |partial sums| < 2^53
+        x_all = x if world == 1 else np.concatenate(
+            [synthetic(R, f, cols, pf, ws, seed=7 + r)[0] for r in range(world)], axis=0)
+        want = np.rint(x_all.astype(np.float64) @ w.astype(np.float64)).astype(np.int64) + b  # exact: |sums| < 2^53
         check = {"decrypted_equals_integer_product": bool(np.array_equal(got, want)), "client_decrypt_ms": dec_ms,
                  "keygen_ms": keygen_ms, "client_encrypt_ms": enc_ms}
 
