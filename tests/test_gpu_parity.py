@@ -395,7 +395,7 @@ def test_device_client_encryption_matches_reference(n, R, f):
     assert np.array_equal(vals[: tail.size], tail) and budget > 0
 
 
-@pytest.mark.parametrize("n,R,f,cols", [(32, 3, 70, 2), (8192, 3, 9000, 3), (8192, 1, 1000, 11)])
+@pytest.mark.parametrize("n,R,f,cols", [(32, 3, 70, 2), (32, 20, 64, 3), (8192, 3, 9000, 3), (8192, 1, 1000, 11)])
 def test_server_wire_path_byte_identical(n, R, f, cols):
     """InferenceServer::do_infer (server.cpp:112-172) end to end on wire
     objects: the request's HECT blobs in, the response blobs out, byte for
@@ -665,7 +665,8 @@ def test_keygen_rejection_planner_exact():
         native.check(plan(p - 1))
 
 
-def test_feature_block_sharding_bit_exact(prod):
+@pytest.mark.parametrize("R,f,world", [(3, 20000, 2), (5, 40000, 3)])
+def test_feature_block_sharding_bit_exact(prod, R, f, world):
     """Feature-block sharding (C5's second mode), two ranks emulated one after
     the other on one GPU (no rank waits on another): each rank's chunk
     products of its feature block, the dot partials summed as the
@@ -678,7 +679,7 @@ def test_feature_block_sharding_bit_exact(prod):
                                                 packed_count, shard_chunks, shard_rows)
 
     o, s = prod
-    R, f, cols, world = 3, 20000, 2, 2
+    cols = 2
     x, w, b = synthetic(R, f, cols, 0.05, 0.1, seed=21)
     inputs = o.encode_inputs(x)  # [R][kc][ct]
     wp = o.encode_weights(w)
@@ -688,6 +689,8 @@ def test_feature_block_sharding_bit_exact(prod):
     dot = torch.zeros((R * cols, ctw), dtype=torch.int64, device="cuda")
     for r in range(world):  # each rank: its feature block of every row
         k0, kn = shard_chunks(kc, world, r)
+        if kn == 0:
+            continue
         blk = torch.from_numpy(inputs[:, k0:k0 + kn].astype(np.int64)).to(torch.int32).cuda().contiguous()
         part = torch.zeros_like(dot)
         chunk_dot_partial_device(s, ew, blk.data_ptr(), R, k0, kn, part.data_ptr())
@@ -697,6 +700,8 @@ def test_feature_block_sharding_bit_exact(prod):
     acc = torch.zeros((C_, ctw), dtype=torch.int64, device="cuda")
     for r in range(world):  # each rank folds its row block
         lo, cnt = shard_rows(R, world, r)
+        if cnt == 0:
+            continue
         fold_pack_device(s, ew, dot[lo * cols:].data_ptr(), lo, cnt, R, acc.data_ptr())
     out = torch.empty((C_, ctw), dtype=torch.int32, device="cuda")
     finish_packed_device(s, ew, acc.data_ptr(), b, R, out.data_ptr())
