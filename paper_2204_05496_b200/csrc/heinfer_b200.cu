@@ -420,7 +420,10 @@ struct hei_gpu_prng {
 
 namespace {
 
-void set_device(hei_gpu_ctx* c) { CU(cudaSetDevice(c->device)); }
+void set_device(hei_gpu_ctx* c) {
+  if (!c) raise(HEI_PARAM_ERROR, "null context");
+  CU(cudaSetDevice(c->device));
+}
 
 void check_err_flag(hei_gpu_ctx* c, int code, const char* what) {
   uint32_t h = 0;

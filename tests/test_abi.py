@@ -100,3 +100,14 @@ def test_device_prng_replays_reference_stream():
     p = Prng(2)
     assert np.array_equal(p.draw(400), raw[:400])
     assert np.array_equal(p.draw(600), raw[400:])
+
+
+def test_null_context_is_a_param_error_not_a_crash():
+    """Every C entry point validates its context before any device work."""
+    import ctypes as C
+
+    lib = native.lib()
+    out = np.zeros(4, np.uint64)
+    assert lib.hei_gpu_matmul(None, None, None, 1, C.c_uint64(1), None, None, None) == native.HEI_PARAM_ERROR
+    assert lib.hei_gpu_upload_public_key(None, C.c_uint32(0), native.u64p(out)) in (native.HEI_PARAM_ERROR,)
+    assert b"null context" in lib.hei_gpu_last_error()
