@@ -363,6 +363,7 @@ struct hei_gpu_ctx {
   uint32_t* pool_masks = nullptr;  // latency path: precomputed mask plaintexts
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
+  uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   struct FoldGraph {
     uint64_t pairs;
     uint32_t *cur, *other, *part, *dig;
@@ -1390,6 +1391,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_CLUSTER_KS")) c->cluster_ks = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_GROUP_KS")) c->group_ks = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
@@ -2234,7 +2236,7 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
   cudaStream_t cs = c->copy_stream;
   const size_t words = w->kc * c->ct_words();
   const size_t row_bytes = wire ? w->kc * (io.wg.blob[0] + io.wg.blob[1]) : words * 8;
-  const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(s->cap_rows, (rows + 7) / 8));
+  const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(s->cap_rows, (rows + c->e2e_div - 1) / c->e2e_div));
   const size_t slot_bytes = (chunk * row_bytes + 64) & ~(size_t)15;  // + pad for the parser's 12-byte window
   uint8_t* stage = reinterpret_cast<uint8_t*>(
       pool_get(c->pool_stage64, c->pool_stage64_bytes, 2 * slot_bytes));
