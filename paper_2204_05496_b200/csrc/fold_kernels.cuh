@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
                                                                     const uint2* __restrict__ key1,
                                                                     uint32_t* __restrict__ out, int fold,
                                                                     const uint32_t* __restrict__ perm_next,
-                                                                    uint32_t* __restrict__ dig_next,
+                                                                    uint32_t* __restrict__ dig_next, int tma,
                                                                     const __grid_constant__ TwArg<PTW> tab) {
   using NT = Ntt<LOGN>;
   constexpr uint32_t N = NT::N, T = NT::T;
@@ -585,23 +585,56 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
   const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
   const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
   uint32_t e[16];
+  // tma: each digit polynomial (contiguous 4N bytes) arrives in `sm` through
+  // a TMA bulk copy issued while the previous digit's key products run.
+  __shared__ uint64_t bar;
+  uint32_t parity = 0;
+  if (tma) {
+    const uint32_t l0 = i == 0 ? 1u : 0u;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      bulk_load(sm, dig + (uint64_t)l0 * N, N * 4, &bar);
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+  }
   for (uint32_t l = 0; l < L; ++l) {
     if (l == i) continue;
-    const uint32_t* src = dig + (uint64_t)l * N;
-    if (pr.fast_reduce) {
+    if (tma) {
+      mbar_wait(&bar, parity);
+      parity ^= 1u;
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
-        const uint32_t v = src[NT::posA(j, r)];
-        e[r] = min(v, v - q);
+        const uint32_t v = sm[NT::posA(j, r)];
+        e[r] = pr.fast_reduce ? min(v, v - q) : v % q;
       }
     } else {
+      const uint32_t* src = dig + (uint64_t)l * N;
+      if (pr.fast_reduce) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
+        for (int r = 0; r < 16; ++r) {
+          const uint32_t v = src[NT::posA(j, r)];
+          e[r] = min(v, v - q);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
+      }
     }
     if constexpr (PTW)
       NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
     else
       NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
+    if (tma) {
+      uint32_t ln = l + 1;
+      if (ln == i) ++ln;
+      if (ln < L) {
+        __syncthreads();  // every thread's last read of sm in this transform is done
+        if (threadIdx.x == 0) {
+          fence_proxy_async_smem();
+          bulk_load(sm, dig + (uint64_t)ln * N, N * 4, &bar);
+        }
+      }
+    }
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
 #pragma unroll

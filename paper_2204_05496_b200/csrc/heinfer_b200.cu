@@ -26,6 +26,7 @@
 // the kernel namespace below):
 //   modmath.cuh        Shoup / Barrett arithmetic, shared-memory NTTs (small N)
 //   ntt_fast.cuh       register-blocked NTT (N = 4096..16384)
+//   bulk_copy.cuh      1-D TMA bulk copies (cp.async.bulk + mbarrier)
 //   wire.cuh           HECT ciphertext parse / emit kernels
 //   fold_kernels.cuh   fast algorithm: chunk products, digits, key switch,
 //                      mask + pack, bias / finish, weight and key preparation
@@ -55,6 +56,7 @@
 #include "../../include/heinfer_b200.h"
 #include "modmath.cuh"
 #include "ntt_fast.cuh"
+#include "bulk_copy.cuh"
 #include "baseline.cuh"
 
 using namespace heb;
@@ -364,6 +366,7 @@ struct hei_gpu_ctx {
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
+  int ks_tma = 0;        // HEI_KS_TMA=1: key switch prefetches digits with TMA bulk copies (measured 2 % slower)
   struct FoldGraph {
     uint64_t pairs;
     uint32_t *cur, *other, *part, *dig;
@@ -573,17 +576,17 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
   if (dig_next) {
     if (big)
       k_rot_keyswitch_s<LG, true, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, perm_next,
-                                                                        dig_next, *tabs_of(c, g, 0));
+                                                                        dig_next, c->ks_tma, *tabs_of(c, g, 0));
     else
       k_rot_keyswitch_s<LG, false, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                         perm_next, dig_next, TwNone{});
+                                                                         perm_next, dig_next, c->ks_tma, TwNone{});
   } else {
     if (big)
       k_rot_keyswitch_s<LG, true, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr,
-                                                                         nullptr, *tabs_of(c, g, 0));
+                                                                         nullptr, c->ks_tma, *tabs_of(c, g, 0));
     else
       k_rot_keyswitch_s<LG, false, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                          nullptr, nullptr, TwNone{});
+                                                                          nullptr, nullptr, c->ks_tma, TwNone{});
   }
 }
 
@@ -1392,6 +1395,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_GROUP_KS")) c->group_ks = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("HEI_KS_TMA")) c->ks_tma = std::atoi(v) != 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
