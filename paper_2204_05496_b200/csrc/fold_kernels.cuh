@@ -433,7 +433,7 @@ __device__ __forceinline__ void store16(uint32_t* __restrict__ p, const uint32_t
 template <int LOGN, bool PTW>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digits_f(Geo g, const uint32_t* __restrict__ dot,
                                                               const uint32_t* __restrict__ perm,
-                                                              uint32_t* __restrict__ digits,
+                                                              uint32_t* __restrict__ digits, int tma,
                                                               const __grid_constant__ TwArg<PTW> itab) {
   using NT = Ntt<LOGN>;
   extern __shared__ uint4 smem4[];
@@ -443,9 +443,25 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digi
   const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * NT::N;
   const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
   uint32_t pm[16], e[16];
-  load16_ro(perm + x0, pm);
+  if (tma) {
+    // the whole c1 polynomial lands in shared memory with one TMA bulk copy;
+    // the Galois gather then reads shared memory instead of scattered L1/L2
+    __shared__ uint64_t bar;
+    uint32_t* stg = sm + NT::N;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      bulk_load(stg, c1, NT::N * 4, &bar);
+    }
+    load16_ro(perm + x0, pm);
+    __syncthreads();
+    mbar_wait(&bar, 0);
 #pragma unroll
-  for (int r = 0; r < 16; ++r) e[r] = c1[pm[r]];
+    for (int r = 0; r < 16; ++r) e[r] = stg[pm[r]];
+  } else {
+    load16_ro(perm + x0, pm);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = c1[pm[r]];
+  }
   if constexpr (PTW)
     NT::inv(e, sm, ParamTw{itab.w[gp]}, g.itwc + (size_t)gp * g.twc_stride, pr.q, pr.last, pr.ninv);
   else

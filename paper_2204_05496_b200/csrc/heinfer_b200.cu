@@ -366,6 +366,7 @@ struct hei_gpu_ctx {
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
+  int dig_tma = 1;       // HEI_DIG_TMA=0: digit kernel gathers c1 from global memory
   int ks_tma = 0;        // HEI_KS_TMA=1: key switch prefetches digits with TMA bulk copies (measured 2 % slower)
   struct FoldGraph {
     uint64_t pairs;
@@ -516,13 +517,15 @@ const TwAB* tabs_of(hei_gpu_ctx* c, const Geo& g, int inverse) {
 
 void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* perm,
                        uint32_t* dig, cudaStream_t st) {
-  const size_t sm = smem_bytes(c, 1);
+  const size_t sm = smem_bytes(c, 1), smf = smem_bytes(c, c->dig_tma ? 2 : 1);
   // big launches take the pass-A/B twiddles as parameters (constant bank);
   // small ones keep the 25 KB parameter block off the launch path
   const bool ptw = blocks >= 2u * 148u;
   HEI_DISPATCH(c->logn,
-               (ptw ? k_rot_digits_f<LG, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1))
-                    : k_rot_digits_f<LG, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig, TwNone{})),
+               (ptw ? k_rot_digits_f<LG, true><<<blocks, Ntt<LG>::T, smf, st>>>(g, cur, perm, dig, c->dig_tma,
+                                                                                *tabs_of(c, g, 1))
+                    : k_rot_digits_f<LG, false><<<blocks, Ntt<LG>::T, smf, st>>>(g, cur, perm, dig, c->dig_tma,
+                                                                                 TwNone{})),
                (k_rot_digits<<<blocks, c->threads(), sm, st>>>(g, cur, perm, dig)));
   LAUNCHED();
 }
@@ -651,8 +654,8 @@ void launch_poly_ntt(hei_gpu_ctx* c, unsigned blocks, uint32_t gp, uint32_t* pol
 }
 template <int LG>
 void set_fast_attrs(size_t sm) {
-  set_smem_attr((const void*)k_rot_digits_f<LG, true>, sm);
-  set_smem_attr((const void*)k_rot_digits_f<LG, false>, sm);
+  set_smem_attr((const void*)k_rot_digits_f<LG, true>, 2 * sm);
+  set_smem_attr((const void*)k_rot_digits_f<LG, false>, 2 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_f<LG>, sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, false>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, false>, 3 * sm);
@@ -1396,6 +1399,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_KS_TMA")) c->ks_tma = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_DIG_TMA")) c->dig_tma = std::atoi(v) != 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
