@@ -875,7 +875,7 @@ template <int LOGN, bool NEXT>
 __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
     Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ digits, const uint32_t* __restrict__ perm,
     const uint2* __restrict__ key0, const uint2* __restrict__ key1, uint32_t* __restrict__ out, int fold,
-    const uint32_t* __restrict__ perm_next, uint32_t* __restrict__ dig_next) {
+    const uint32_t* __restrict__ perm_next, uint32_t* __restrict__ dig_next, int tma) {
   using NT = Ntt<LOGN, 2>;
   constexpr uint32_t N = NT::N, T = NT::T;
   extern __shared__ uint4 smem4[];
@@ -920,22 +920,52 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
   const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
   const uint32_t half = L / 2;  // digits (l != i) with index < half go to group 0
   uint32_t e[16];
+  // this group's digits, in order
+  uint32_t mine[8], cnt = 0;
   for (uint32_t l = 0, k = 0; l < L; ++l) {
     if (l == i) continue;
-    const uint32_t mine = (k++ < half) ? 0u : 1u;
-    if (mine != grp) continue;
-    const uint32_t* src = dig + (uint64_t)l * N;
-    if (pr.fast_reduce) {
+    if (((k++ < half) ? 0u : 1u) == grp) mine[cnt++] = l;
+  }
+  // tma: the next digit of the group arrives in its `sm` by a TMA bulk copy
+  // issued while the current digit's key products run
+  __shared__ uint64_t bars[2];
+  if (tma) {
+    if (j == 0) {
+      mbar_init(&bars[grp], 1);
+      if (cnt) bulk_load(sm, dig + (uint64_t)mine[0] * N, N * 4, &bars[grp]);
+    }
+    NT::sync();
+  }
+  for (uint32_t u = 0; u < cnt; ++u) {
+    const uint32_t l = mine[u];
+    if (tma) {
+      mbar_wait(&bars[grp], u & 1u);
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
-        const uint32_t v = src[NT::posA(j, r)];
-        e[r] = min(v, v - q);
+        const uint32_t v = sm[NT::posA(j, r)];
+        e[r] = pr.fast_reduce ? min(v, v - q) : v % q;
       }
     } else {
+      const uint32_t* src = dig + (uint64_t)l * N;
+      if (pr.fast_reduce) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
+        for (int r = 0; r < 16; ++r) {
+          const uint32_t v = src[NT::posA(j, r)];
+          e[r] = min(v, v - q);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
+      }
     }
     NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
+    if (tma && u + 1 < cnt) {
+      NT::sync();  // the group's last reads of sm in this transform are done
+      if (j == 0) {
+        fence_proxy_async_smem();
+        bulk_load(sm, dig + (uint64_t)mine[u + 1] * N, N * 4, &bars[grp]);
+      }
+    }
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
 #pragma unroll

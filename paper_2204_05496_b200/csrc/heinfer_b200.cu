@@ -367,6 +367,7 @@ struct hei_gpu_ctx {
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   int dig_tma = 1;       // HEI_DIG_TMA=0: digit kernel gathers c1 from global memory
+  int lat_tma = 0;       // HEI_LAT_TMA=1: latency-path key switch prefetches digits with TMA (measured slower)
   int ks_tma = 0;        // HEI_KS_TMA=1: key switch prefetches digits with TMA bulk copies (measured 2 % slower)
   struct FoldGraph {
     uint64_t pairs;
@@ -561,10 +562,10 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
       const size_t sm2 = smem_bytes(c, 6);
       if (dig_next)
         k_rot_keyswitch_w2<LG, true><<<blocks, 2 * Ntt<LG>::T, sm2, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                         perm_next, dig_next);
+                                                                         perm_next, dig_next, c->lat_tma);
       else
         k_rot_keyswitch_w2<LG, false><<<blocks, 2 * Ntt<LG>::T, sm2, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                          nullptr, nullptr);
+                                                                          nullptr, nullptr, c->lat_tma);
       return;
     }
   }
@@ -1400,6 +1401,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_KS_TMA")) c->ks_tma = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DIG_TMA")) c->dig_tma = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_LAT_TMA")) c->lat_tma = std::atoi(v) != 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
