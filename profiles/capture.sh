@@ -14,7 +14,7 @@ HEI_PROFILE_STEPS=1 ncu --profile-from-start off --metrics gpu__time_duration.su
     --log-file gpurun_out/launches_${TAG}_c4.csv $CMD > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_rot_keyswitch_s|k_rot_digits_f" -s 60 -c 2 \
     -o gpurun_out/full_${TAG}_c4 $CMD > gpurun_out/ncu_full.log 2>&1
-python tests/bench_latency_probe2.py > /dev/null 2>&1 || exit 3
+python profiles/probes/latency_probe2.py > /dev/null 2>&1 || exit 3
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_latency.csv \
-    env HEI_NO_GRAPHS=1 python tests/bench_latency_probe2.py > /dev/null 2>&1
+    env HEI_NO_GRAPHS=1 python profiles/probes/latency_probe2.py > /dev/null 2>&1
 echo done
