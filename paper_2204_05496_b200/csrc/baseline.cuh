@@ -132,12 +132,16 @@ constexpr int kMtSeq = kMtDeg + 312;  // words needed by one jump
 // sequence (sequential twists, one block per branch), k_mt_xor computes
 // partial windows over slices of the polynomial (many blocks), and
 // k_mt_xor_reduce folds the partials into the next start window.
-__global__ void __launch_bounds__(320) k_mt_wseq(const uint64_t* __restrict__ cur, uint64_t* __restrict__ wseq,
-                                                 uint32_t wlen) {
+// Tree-ordered jump-ahead: level k advances starts[m] by 2^k * C words into
+// starts[m + 2^k] for every m < min(2^k, K - 2^k) at once, so K chunk starts
+// cost ceil(log2 K) levels of three batched launches instead of K - 1
+// sequential jumps. grid.z (or .y) = job m; branch b = blockIdx.y (or .x).
+__global__ void __launch_bounds__(320) k_mt_wseq(const uint64_t* __restrict__ starts, uint32_t K,
+                                                 uint64_t* __restrict__ wseq, uint32_t wlen) {
   __shared__ uint64_t buf[2][312];
-  const uint32_t b = blockIdx.x, t = threadIdx.x;
-  const uint64_t* st = cur + (uint64_t)b * 313;
-  uint64_t* W = wseq + (uint64_t)b * wlen;
+  const uint32_t b = blockIdx.x, m = blockIdx.y, t = threadIdx.x;
+  const uint64_t* st = starts + ((uint64_t)b * K + m) * 313;
+  uint64_t* W = wseq + ((uint64_t)m * 2 + b) * wlen;
   for (uint32_t i = t; i < 312; i += blockDim.x) {
     buf[0][i] = st[i];
     W[i] = st[i];
@@ -163,13 +167,13 @@ __global__ void __launch_bounds__(320) k_mt_wseq(const uint64_t* __restrict__ cu
   }
 }
 
-// partial[b][s][k] = XOR over set bits i of poly words [s*ws, (s+1)*ws) of W[k+i]
+// partial[m][b][s][k] = XOR over set bits i of poly words [s*ws, (s+1)*ws) of W[k+i]
 __global__ void __launch_bounds__(320) k_mt_xor(const uint64_t* __restrict__ wseq, uint32_t wlen,
                                                 const uint64_t* __restrict__ poly, uint32_t ws,
                                                 uint64_t* __restrict__ partial) {
-  const uint32_t s = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
+  const uint32_t s = blockIdx.x, b = blockIdx.y, m = blockIdx.z, t = threadIdx.x;
   const uint32_t nw = (kMtDeg + 63) / 64;
-  const uint64_t* W = wseq + (uint64_t)b * wlen;
+  const uint64_t* W = wseq + ((uint64_t)m * 2 + b) * wlen;
   uint64_t acc = 0;
   if (t < 312)
     for (uint32_t wi = s * ws; wi < min(nw, (s + 1) * ws); ++wi) {
@@ -180,18 +184,18 @@ __global__ void __launch_bounds__(320) k_mt_xor(const uint64_t* __restrict__ wse
         bits &= bits - 1;
       }
     }
-  if (t < 312) partial[((uint64_t)b * gridDim.x + s) * 312 + t] = acc;
+  if (t < 312) partial[(((uint64_t)m * 2 + b) * gridDim.x + s) * 312 + t] = acc;
 }
 
-__global__ void k_mt_xor_reduce(const uint64_t* __restrict__ partial, uint32_t S, uint64_t* __restrict__ cur,
-                                uint64_t* __restrict__ starts, uint32_t K, uint32_t m) {
-  const uint32_t b = blockIdx.x, t = threadIdx.x;
+__global__ void k_mt_xor_reduce(const uint64_t* __restrict__ partial, uint32_t S, uint64_t* __restrict__ starts,
+                                uint32_t K, uint32_t step) {
+  const uint32_t b = blockIdx.x, m = blockIdx.y, t = threadIdx.x;
   if (t >= 312) return;
   uint64_t acc = 0;
-  for (uint32_t s = 0; s < S; ++s) acc ^= partial[((uint64_t)b * S + s) * 312 + t];
-  cur[(uint64_t)b * 313 + t] = acc;
-  starts[((uint64_t)b * K + m) * 313 + t] = acc;
-  if (t == 0) starts[((uint64_t)b * K + m) * 313 + 312] = 312;
+  for (uint32_t s = 0; s < S; ++s) acc ^= partial[(((uint64_t)m * 2 + b) * S + s) * 312 + t];
+  uint64_t* dst = starts + ((uint64_t)b * K + m + step) * 313;
+  dst[t] = acc;
+  if (t == 0) dst[312] = 312;
 }
 
 // Chunk m of branch b generates draws [m*C, min((m+1)*C, total)) from its

@@ -459,7 +459,10 @@ T* pool_get(T*& p, size_t& cap, size_t bytes) {
 
 // Grow-only scratch slot `id` of the context (reused across calls; every
 // C-ABI call synchronises before returning).
-enum ScratchId { kScrRawAll = 0, kScrRaw, kScrNoise, kScrM, kScrCt, kScrWc, kScrAcc, kScrOut, kScrOut64, kScrX };
+enum ScratchId {
+  kScrRawAll = 0, kScrRaw, kScrNoise, kScrM, kScrCt, kScrWc, kScrAcc, kScrOut, kScrOut64, kScrX,
+  kScrMtPoly, kScrMtWseq, kScrMtPart
+};
 template <typename T>
 T* scratch(hei_gpu_ctx* c, int id, size_t bytes) {
   void*& p = c->named_pool[id];
@@ -1208,6 +1211,71 @@ Poly2 mt_jump_poly(uint64_t J) {
 }
 
 
+// Jump polynomials of the tree levels for chunk size C: level k is
+// x^(2^k C) mod phi = (level k-1)^2 mod phi. Cached per C.
+const std::vector<Poly2>& mt_level_polys(uint64_t C, uint32_t levels) {
+  static std::mutex mu;
+  static std::map<uint64_t, std::vector<Poly2>> cache;
+  const Poly2 first = mt_jump_poly(C);
+  std::lock_guard<std::mutex> lk(mu);
+  auto& v = cache[C];
+  if (v.empty()) v.push_back(first);
+  const Poly2& phi = mt_charpoly();
+  const size_t nw = (heb_baseline::kMtDeg + 63) / 64;
+  while (v.size() < levels) {
+    const Poly2& r = v.back();
+    Poly2 sq(2 * nw + 1, 0);
+    for (size_t w = 0; w < nw; ++w) {
+      const uint64_t x = r[w];
+      uint64_t lo = 0, hi = 0;
+      for (int i = 0; i < 32; ++i) {
+        lo |= ((x >> i) & 1ull) << (2 * i);
+        hi |= ((x >> (i + 32)) & 1ull) << (2 * i);
+      }
+      sq[2 * w] = lo;
+      sq[2 * w + 1] = hi;
+    }
+    poly_reduce(sq, phi);
+    v.push_back(sq);
+  }
+  return v;
+}
+
+// Start windows of K chunk generators per branch, chunk m starting m * C
+// words after d_state (block-aligned, mti == 312): starts [2][K][313].
+void mt_chunk_starts(hei_gpu_ctx* c, const uint64_t* d_state, uint64_t K, uint64_t C, uint64_t* d_starts,
+                     cudaStream_t st) {
+  uint32_t levels = 0;
+  while ((1ull << levels) < K) ++levels;
+  if (levels == 0) {
+    for (int bb = 0; bb < 2; ++bb)
+      CU(cudaMemcpyAsync(d_starts + (uint64_t)bb * K * 313, d_state + bb * 313, 313 * 8, cudaMemcpyDeviceToDevice,
+                         st));
+    return;
+  }
+  const std::vector<Poly2>& polys = mt_level_polys(C, levels);
+  const uint32_t wlen = 312 * 65, S = 64;
+  const size_t pw = polys[0].size();
+  const uint64_t jobs_max = K / 2 + 1;
+  uint64_t* d_poly = scratch<uint64_t>(c, kScrMtPoly, levels * pw * 8);
+  uint64_t* d_wseq = scratch<uint64_t>(c, kScrMtWseq, jobs_max * 2 * wlen * 8);
+  uint64_t* d_part = scratch<uint64_t>(c, kScrMtPart, jobs_max * 2 * S * 312 * 8);
+  for (uint32_t k = 0; k < levels; ++k)
+    CU(cudaMemcpyAsync(d_poly + k * pw, polys[k].data(), pw * 8, cudaMemcpyHostToDevice, st));
+  for (int bb = 0; bb < 2; ++bb)
+    CU(cudaMemcpyAsync(d_starts + (uint64_t)bb * K * 313, d_state + bb * 313, 313 * 8, cudaMemcpyDeviceToDevice, st));
+  const uint32_t wsl = (uint32_t)((pw + S - 1) / S);
+  for (uint32_t k = 0; k < levels; ++k) {
+    const uint64_t step = 1ull << k, jobs = std::min<uint64_t>(step, K - step);
+    heb_baseline::k_mt_wseq<<<dim3(2, (unsigned)jobs), 320, 0, st>>>(d_starts, (uint32_t)K, d_wseq, wlen);
+    heb_baseline::k_mt_xor<<<dim3(S, 2, (unsigned)jobs), 320, 0, st>>>(d_wseq, wlen, d_poly + k * pw, wsl, d_part);
+    heb_baseline::k_mt_xor_reduce<<<dim3(2, (unsigned)jobs), 320, 0, st>>>(d_part, S, d_starts, (uint32_t)K,
+                                                                          (uint32_t)step);
+    g_launches += 3;
+  }
+  CU(cudaGetLastError());
+}
+
 // ---- client encryption: matmul::encode_inputs (matmul.cpp:201-223) --------
 // Every row is split into ceil(f / N) slot chunks, each encode_signed + encrypt
 // (eval form) with the branch's util::Prng stream, in (row, chunk) order — the
@@ -1273,25 +1341,9 @@ void encode_inputs_impl(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_
       const uint64_t Cenc = (E_total + K - 1) / K;
       K = (E_total + Cenc - 1) / Cenc;
       const uint64_t C = Cenc * 3 * n;
-      const Poly2 poly = mt_jump_poly(C);
-      uint64_t *d_poly = nullptr, *d_starts = nullptr, *d_cur = nullptr, *d_wseq = nullptr, *d_part = nullptr;
-      const uint32_t wlen = 312 * 65, S = 64, wsl = (uint32_t)((poly.size() + S - 1) / S);
-      alloc(&d_poly, poly.size() * 8);
+      uint64_t* d_starts = nullptr;
       alloc(&d_starts, 2 * K * 313 * 8);
-      alloc(&d_cur, 2 * 313 * 8);
-      alloc(&d_wseq, 2ull * wlen * 8);
-      alloc(&d_part, 2ull * S * 312 * 8);
-      CU(cudaMemcpyAsync(d_poly, poly.data(), poly.size() * 8, cudaMemcpyHostToDevice, st));
-      for (int bb = 0; bb < 2; ++bb) {
-        CU(cudaMemcpyAsync(d_starts + (uint64_t)bb * K * 313, d_state + bb * 313, 313 * 8, cudaMemcpyDeviceToDevice, st));
-        CU(cudaMemcpyAsync(d_cur + bb * 313, d_state + bb * 313, 313 * 8, cudaMemcpyDeviceToDevice, st));
-      }
-      for (uint32_t m = 1; m < K; ++m) {
-        heb_baseline::k_mt_wseq<<<2, 320, 0, st>>>(d_cur, d_wseq, wlen);
-        heb_baseline::k_mt_xor<<<dim3(S, 2), 320, 0, st>>>(d_wseq, wlen, d_poly, wsl, d_part);
-        heb_baseline::k_mt_xor_reduce<<<2, 320, 0, st>>>(d_part, S, d_cur, d_starts, (uint32_t)K, m);
-        g_launches += 3;
-      }
+      mt_chunk_starts(c, d_state, K, C, d_starts, st);
       heb_baseline::k_mt_chunks<<<dim3((unsigned)K, 2), 320, 0, st>>>(d_starts, (uint32_t)K, C, Dtot, d_raw, d_state);
       LAUNCHED();
     } else {
@@ -2612,28 +2664,10 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
       const uint64_t Cenc = (E_total + K - 1) / K;
       K = (E_total + Cenc - 1) / Cenc;
       const uint64_t C = Cenc * 3 * n;
-      const Poly2 poly = mt_jump_poly(C);
-      uint64_t *d_poly = nullptr, *d_starts = nullptr, *d_cur = nullptr, *d_wseq = nullptr, *d_part = nullptr;
-      const uint32_t wlen = 312 * 65, S = 64, wsl = (uint32_t)((poly.size() + S - 1) / S);
-      alloc(&d_poly, poly.size() * 8);
+      uint64_t* d_starts = nullptr;
       alloc(&d_starts, 2 * K * 313 * 8);
-      alloc(&d_cur, 2 * 313 * 8);
-      alloc(&d_wseq, 2ull * wlen * 8);
-      alloc(&d_part, 2ull * S * 312 * 8);
       d_rawall = scratch<uint64_t>(c, kScrRawAll, 2 * Dtot * 8);
-      CU(cudaMemcpyAsync(d_poly, poly.data(), poly.size() * 8, cudaMemcpyHostToDevice, st));
-      // chunk 0 starts at the current (block-aligned) state
-      for (int bb = 0; bb < 2; ++bb) {
-        CU(cudaMemcpyAsync(d_starts + (uint64_t)bb * K * 313, d_state + bb * 313, 313 * 8, cudaMemcpyDeviceToDevice, st));
-        CU(cudaMemcpyAsync(d_cur + bb * 313, d_state + bb * 313, 313 * 8, cudaMemcpyDeviceToDevice, st));
-      }
-      for (uint32_t m = 1; m < K; ++m) {
-        heb_baseline::k_mt_wseq<<<2, 320, 0, st>>>(d_cur, d_wseq, wlen);
-        heb_baseline::k_mt_xor<<<dim3(S, 2), 320, 0, st>>>(d_wseq, wlen, d_poly, wsl, d_part);
-        heb_baseline::k_mt_xor_reduce<<<2, 320, 0, st>>>(d_part, S, d_cur, d_starts, (uint32_t)K, m);
-        g_launches += 3;
-      }
-      CU(cudaGetLastError());
+      mt_chunk_starts(c, d_state, K, C, d_starts, st);  // chunk 0 = the current (block-aligned) state
       heb_baseline::k_mt_chunks<<<dim3((unsigned)K, 2), 320, 0, st>>>(d_starts, (uint32_t)K, C, Dtot, d_rawall, d_state);
       LAUNCHED();
     }
