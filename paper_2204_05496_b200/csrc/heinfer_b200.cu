@@ -369,6 +369,7 @@ struct hei_gpu_ctx {
   int dig_tma = 1;       // HEI_DIG_TMA=0: digit kernel gathers c1 from global memory
   int lat_tma = 0;       // HEI_LAT_TMA=1: latency-path key switch prefetches digits with TMA (measured slower)
   int ks_tma = 0;        // HEI_KS_TMA=1: key switch prefetches digits with TMA bulk copies (measured 2 % slower)
+  uint64_t mt_chunks_max = 128;   // HEI_MT_CHUNKS: parallel mt19937_64 generators per branch
   struct FoldGraph {
     uint64_t pairs;
     uint32_t *cur, *other, *part, *dig;
@@ -1337,7 +1338,7 @@ void encode_inputs_impl(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_
     CU(cudaMemcpyAsync(d_state, hstate, sizeof(hstate), cudaMemcpyHostToDevice, st));
     const bool jump = c->mt_jump && !force_seq && hstate[0][312] == 312 && hstate[1][312] == 312 && E_total >= 64;
     if (jump) {
-      uint64_t K = std::min<uint64_t>(128, E_total / 8);
+      uint64_t K = std::min<uint64_t>(c->mt_chunks_max, E_total / 8);
       const uint64_t Cenc = (E_total + K - 1) / K;
       K = (E_total + Cenc - 1) / Cenc;
       const uint64_t C = Cenc * 3 * n;
@@ -1452,6 +1453,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_KS_TMA")) c->ks_tma = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_DIG_TMA")) c->dig_tma = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_LAT_TMA")) c->lat_tma = std::atoi(v) != 0;
     c->n = n;
@@ -2660,7 +2662,7 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
                 Dtot * 16 <= ((uint64_t)48 << 30);
     uint64_t* d_rawall = nullptr;
     if (jump) {
-      uint64_t K = std::min<uint64_t>(128, E_total / 8);
+      uint64_t K = std::min<uint64_t>(c->mt_chunks_max, E_total / 8);
       const uint64_t Cenc = (E_total + K - 1) / K;
       K = (E_total + Cenc - 1) / Cenc;
       const uint64_t C = Cenc * 3 * n;
