@@ -360,8 +360,8 @@ struct hei_gpu_ctx {
   cudaStream_t bias_stream = nullptr;  // bias plaintext encoding, overlapped with the fold
   uint32_t* pool_biasp = nullptr;
   size_t pool_biasp_bytes = 0;
-  void* named_pool[16] = {};       // grow-only scratch for the client-role calls (baseline, encryption)
-  size_t named_pool_bytes[16] = {};
+  void* named_pool[24] = {};       // grow-only scratch for the client-role calls (baseline, encryption)
+  size_t named_pool_bytes[24] = {};
   uint32_t* pool_masks = nullptr;  // latency path: precomputed mask plaintexts
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
@@ -462,10 +462,11 @@ T* pool_get(T*& p, size_t& cap, size_t bytes) {
 // C-ABI call synchronises before returning).
 enum ScratchId {
   kScrRawAll = 0, kScrRaw, kScrNoise, kScrM, kScrCt, kScrWc, kScrAcc, kScrOut, kScrOut64, kScrX,
-  kScrMtPoly, kScrMtWseq, kScrMtPart
+  kScrMtPoly, kScrMtWseq, kScrMtPart, kScrW, kScrBias, kScrState, kScrStarts
 };
 template <typename T>
 T* scratch(hei_gpu_ctx* c, int id, size_t bytes) {
+  static_assert(kScrStarts < 24, "named scratch pool too small");
   void*& p = c->named_pool[id];
   if (bytes > c->named_pool_bytes[id]) {
     if (p) CU(cudaFree(p));
@@ -679,7 +680,8 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_ct_intt_f<LG>, sm);
   set_smem_attr((const void*)k_poly_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_bl_encode<LG>, sm);
-  set_smem_attr((const void*)k_bl_encrypt<LG>, sm);
+  set_smem_attr((const void*)k_bl_encrypt<LG, true>, sm);
+  set_smem_attr((const void*)k_bl_encrypt<LG, false>, sm);
   set_smem_attr((const void*)k_prepare_pk<LG>, sm);
 }
 
@@ -1319,7 +1321,7 @@ void encode_inputs_impl(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_
   uint32_t *d_m = nullptr, *d_ct = nullptr;
   d_x = scratch<int64_t>(c, kScrX, rows * f * 8);
   d_raw = scratch<uint64_t>(c, kScrRawAll, 2 * Dtot * 8);
-  alloc(&d_state, 2 * 313 * 8);
+  d_state = scratch<uint64_t>(c, kScrState, 2 * 313 * 8);
   d_noise = scratch<int8_t>(c, kScrNoise, Eb * 2 * 3 * n);
   d_m = scratch<uint32_t>(c, kScrM, Eb * 2 * n * 4);
   if (!out_dev) {
@@ -1343,7 +1345,7 @@ void encode_inputs_impl(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_
       K = (E_total + Cenc - 1) / Cenc;
       const uint64_t C = Cenc * 3 * n;
       uint64_t* d_starts = nullptr;
-      alloc(&d_starts, 2 * K * 313 * 8);
+      d_starts = scratch<uint64_t>(c, kScrStarts, 2 * K * 313 * 8);
       mt_chunk_starts(c, d_state, K, C, d_starts, st);
       heb_baseline::k_mt_chunks<<<dim3((unsigned)K, 2), 320, 0, st>>>(d_starts, (uint32_t)K, C, Dtot, d_raw, d_state);
       LAUNCHED();
@@ -1362,7 +1364,12 @@ void encode_inputs_impl(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_
                    (k_bl_encode_g<<<dim3((unsigned)E, 2), c->threads(), sm1, st>>>(g, d_x, rows, f, e0, (uint32_t)kc, d_m, 1)));
       LAUNCHED();
       uint32_t* ct = out_dev ? out_dev + e0 * c->ct_words() : d_ct;
-      HEI_DISPATCH(c->logn, (k_bl_encrypt<LG><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct)),
+      HEI_DISPATCH(c->logn,
+                   (E * P >= 2u * 148u
+                        ? k_bl_encrypt<LG, true><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp,
+                                                                                             ct, *tabs_of(c, g, 0))
+                        : k_bl_encrypt<LG, false><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp,
+                                                                                              ct, TwNone{})),
                    (k_bl_encrypt_g<<<(unsigned)(E * P), c->threads(), sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct)));
       LAUNCHED();
       if (!out_dev) {
@@ -1708,7 +1715,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->pool_out64);
   cudaFree(c->pool_biasp);
   cudaFree(c->pool_masks);
-  for (int k = 0; k < 16; ++k) cudaFree(c->named_pool[k]);
+  for (int k = 0; k < 24; ++k) cudaFree(c->named_pool[k]);
   if (c->bias_stream) cudaStreamDestroy(c->bias_stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   cudaFree(c->d_dotA);
@@ -2626,13 +2633,13 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
       fr.p.push_back((void*)*ptr);
     };
     const size_t outw = B * cols * c->ct_words();
-    alloc(&d_x, rows * f * 8);
-    alloc(&d_w, f * cols * 8);
-    alloc(&d_bias, cols * 8);
+    d_x = scratch<int64_t>(c, kScrX, rows * f * 8);
+    d_w = scratch<int64_t>(c, kScrW, f * cols * 8);
+    d_bias = scratch<int64_t>(c, kScrBias, cols * 8);
     d_wc = scratch<uint2>(c, kScrWc, f * cols * P * sizeof(uint2));
     d_acc = scratch<unsigned long long>(c, kScrAcc, outw * 8);
     d_raw = scratch<uint64_t>(c, kScrRaw, 2 * 2 * Emax * 3 * n * 8);  // [slot][branch][draws]
-    alloc(&d_state, 2 * 313 * 8);
+    d_state = scratch<uint64_t>(c, kScrState, 2 * 313 * 8);
     d_noise = scratch<int8_t>(c, kScrNoise, Emax * 2 * 3 * n);
     d_m = scratch<uint32_t>(c, kScrM, Emax * 2 * n * 4);
     d_ct = scratch<uint32_t>(c, kScrCt, Emax * c->ct_words() * 4);
@@ -2667,7 +2674,7 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
       K = (E_total + Cenc - 1) / Cenc;
       const uint64_t C = Cenc * 3 * n;
       uint64_t* d_starts = nullptr;
-      alloc(&d_starts, 2 * K * 313 * 8);
+      d_starts = scratch<uint64_t>(c, kScrStarts, 2 * K * 313 * 8);
       d_rawall = scratch<uint64_t>(c, kScrRawAll, 2 * Dtot * 8);
       mt_chunk_starts(c, d_state, K, C, d_starts, st);  // chunk 0 = the current (block-aligned) state
       heb_baseline::k_mt_chunks<<<dim3((unsigned)K, 2), 320, 0, st>>>(d_starts, (uint32_t)K, C, Dtot, d_rawall, d_state);
@@ -2714,7 +2721,12 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
                    (k_bl_encode<LG><<<dim3((unsigned)E, 2), Ntt<LG>::T, sm1, st>>>(g, d_x, rows, f, k0, (uint32_t)B, d_m)),
                    (k_bl_encode_g<<<dim3((unsigned)E, 2), c->threads(), sm1, st>>>(g, d_x, rows, f, k0, (uint32_t)B, d_m)));
       LAUNCHED();
-      HEI_DISPATCH(c->logn, (k_bl_encrypt<LG><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp, d_ct)),
+      HEI_DISPATCH(c->logn,
+                   (E * P >= 2u * 148u
+                        ? k_bl_encrypt<LG, true><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp,
+                                                                                             d_ct, *tabs_of(c, g, 0))
+                        : k_bl_encrypt<LG, false><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp,
+                                                                                              d_ct, TwNone{})),
                    (k_bl_encrypt_g<<<(unsigned)(E * P), c->threads(), sm1, st>>>(g, d_noise, d_m, c->d_pkp, d_ct)));
       LAUNCHED();
       for (uint32_t j0 = 0; j0 < cols; j0 += kBlJ) {

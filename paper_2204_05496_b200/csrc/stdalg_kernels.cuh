@@ -50,11 +50,12 @@ __device__ __forceinline__ uint32_t lift_small(int32_t v, uint32_t q) { return v
 // (context.cpp:270-301): c0 = NTT(u) pk0 + NTT(e0 + Delta m),
 // c1 = NTT(u) pk1 + NTT(e1). pk is prepared [gp][part] in the pass-C
 // transposed layout.
-template <int LOGN>
+template <int LOGN, bool PTW>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_bl_encrypt(Geo g, const int8_t* __restrict__ noise,
                                                             const uint32_t* __restrict__ m,
                                                             const uint2* __restrict__ pkd,
-                                                            uint32_t* __restrict__ cts) {
+                                                            uint32_t* __restrict__ cts,
+                                                            const __grid_constant__ TwArg<PTW> tab) {
   // c0 = NTT(u) pk0 + NTT(e0 + Delta m), c1 = NTT(u) pk1 + NTT(e1)
   // (encrypt_parts, context.cpp:262-303); one transform live at a time.
   using NT = Ntt<LOGN>;
@@ -88,7 +89,10 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_bl_encry
 #pragma unroll
       for (int r = 0; r < 16; ++r) v[r] = lift_small(nz[(uint32_t)ph * N + NT::posA(j, r)], q);
     }
-    NT::fwd(v, sm, tw, twc, q);
+    if constexpr (PTW)
+      NT::fwd(v, sm, ParamTw{tab.w[gp]}, twc, q);
+    else
+      NT::fwd(v, sm, tw, twc, q);
     if (ph == 0) {  // NTT(u) pk0 -> c0, NTT(u) pk1 -> c1
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
