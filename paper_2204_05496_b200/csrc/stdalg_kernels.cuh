@@ -142,7 +142,7 @@ __global__ void k_bl_accum(Geo g, const uint32_t* __restrict__ cts, uint32_t F, 
   unsigned long long a[kBlJ];
 #pragma unroll
   for (int jj = 0; jj < kBlJ; ++jj) a[jj] = 0;
-#pragma unroll 4
+#pragma unroll 8
   for (uint32_t kk = 0; kk < F; ++kk) {
     const uint32_t v = src[kk * stride];
 #pragma unroll
