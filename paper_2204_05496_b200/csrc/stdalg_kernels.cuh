@@ -142,14 +142,28 @@ __global__ void k_bl_accum(Geo g, const uint32_t* __restrict__ cts, uint32_t F, 
   unsigned long long a[kBlJ];
 #pragma unroll
   for (int jj = 0; jj < kBlJ; ++jj) a[jj] = 0;
+  if (g.br[g.pr[gp].b].t < (1u << 20)) {
+    // small plaintext modulus: the weight residues are < 2^20, so the exact
+    // products (< 2^51) accumulate with one IMAD.WIDE each; this batch's
+    // sums (< 2^59) are reduced mod q before they reach the accumulator
 #pragma unroll 8
-  for (uint32_t kk = 0; kk < F; ++kk) {
-    const uint32_t v = src[kk * stride];
+    for (uint32_t kk = 0; kk < F; ++kk) {
+      const uint64_t v = src[kk * stride];
 #pragma unroll
-    for (int jj = 0; jj < kBlJ; ++jj) {
-      const uint2 w = wsm[kk * kBlJ + jj];
-      const uint32_t qh = __umulhi(v, w.y);
-      a[jj] += (uint32_t)(v * w.x - qh * q);  // in [0, 2q): reduced at the end
+      for (int jj = 0; jj < kBlJ; ++jj) a[jj] += v * wsm[kk * kBlJ + jj].x;
+    }
+#pragma unroll
+    for (int jj = 0; jj < kBlJ; ++jj) a[jj] %= q;
+  } else {
+#pragma unroll 8
+    for (uint32_t kk = 0; kk < F; ++kk) {
+      const uint32_t v = src[kk * stride];
+#pragma unroll
+      for (int jj = 0; jj < kBlJ; ++jj) {
+        const uint2 w = wsm[kk * kBlJ + jj];
+        const uint32_t qh = __umulhi(v, w.y);
+        a[jj] += (uint32_t)(v * w.x - qh * q);  // in [0, 2q): reduced at the end
+      }
     }
   }
 #pragma unroll
