@@ -357,6 +357,8 @@ struct hei_gpu_ctx {
   bool two_streams = true;  // HEI_TWO_STREAMS=0: fold the batch on one stream only
   bool mt_jump = true;      // HEI_MT_JUMP=0: sequential mt19937_64 replay only
   cudaStream_t side_stream = nullptr;
+  std::vector<cudaStream_t> part_streams;  // fold slices 1.. of a batch
+  uint32_t fold_parts = 2;                 // HEI_FOLD_PARTS: concurrent fold slices per batch
   cudaStream_t bias_stream = nullptr;  // bias plaintext encoding, overlapped with the fold
   uint32_t* pool_biasp = nullptr;
   size_t pool_biasp_bytes = 0;
@@ -814,19 +816,23 @@ void run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
   ensure_scratch(c, pairs);
   const unsigned T = c->threads();
   const unsigned blocksP = (unsigned)(pairs * c->P());
-  if (c->two_streams && !c->timing && nrows >= 8) {
-    // two halves of the batch on two streams: one half's digit INTTs and
-    // key switches interleave with the other's, filling each launch's tail
-    if (!c->side_stream) CU(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
-    cudaEvent_t fork, join;
+  const uint32_t parts = std::min<uint64_t>(c->fold_parts, nrows / 4);
+  if (c->two_streams && !c->timing && parts >= 2) {
+    // the batch in `parts` slices on as many streams: one slice's digit INTTs
+    // and key switches interleave with the others', filling each launch's tail
+    while (c->part_streams.size() < parts - 1) {
+      cudaStream_t ps;
+      CU(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
+      c->part_streams.push_back(ps);
+    }
+    cudaEvent_t fork;
     CU(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    CU(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
     CU(cudaEventRecord(fork, st));
-    CU(cudaStreamWaitEvent(c->side_stream, fork, 0));
-    const uint64_t r1 = nrows / 2;
-    for (int h = 0; h < 2; ++h) {
-      cudaStream_t hs = h ? c->side_stream : st;
-      const uint64_t rr0 = h ? r1 : 0, nr = h ? nrows - r1 : r1, pp = nr * cols, off = rr0 * cols;
+    std::vector<cudaEvent_t> joins;
+    for (uint32_t h = 0; h < parts; ++h) {
+      cudaStream_t hs = h ? c->part_streams[h - 1] : st;
+      if (h) CU(cudaStreamWaitEvent(hs, fork, 0));
+      const uint64_t rr0 = nrows * h / parts, nr = nrows * (h + 1) / parts - rr0, pp = nr * cols, off = rr0 * cols;
       uint32_t* A = c->d_dotA + off * c->ct_words();
       uint32_t* B = c->d_dotB + off * c->ct_words();
       uint32_t* D = c->d_dig + off * c->pt_words();
@@ -835,11 +841,18 @@ void run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
       LAUNCHED();
       uint32_t* res = fold(c, pp, A, B, hs, D);
       launch_mask_acc(c, g, (unsigned)(pp * c->P()), res, d_rows + rr0, cols, s->d_acc, hs);
+      if (h) {
+        cudaEvent_t j;
+        CU(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+        CU(cudaEventRecord(j, hs));
+        joins.push_back(j);
+      }
     }
-    CU(cudaEventRecord(join, c->side_stream));
-    CU(cudaStreamWaitEvent(st, join, 0));
+    for (cudaEvent_t j : joins) {
+      CU(cudaStreamWaitEvent(st, j, 0));
+      cudaEventDestroy(j);
+    }
     cudaEventDestroy(fork);
-    cudaEventDestroy(join);
     return;
   }
   // latency path: the mask plaintexts are computed on a side stream while
@@ -1461,6 +1474,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_KS_TMA")) c->ks_tma = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("HEI_FOLD_PARTS")) c->fold_parts = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_DIG_TMA")) c->dig_tma = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_LAT_TMA")) c->lat_tma = std::atoi(v) != 0;
     c->n = n;
@@ -1718,6 +1732,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   for (int k = 0; k < 24; ++k) cudaFree(c->named_pool[k]);
   if (c->bias_stream) cudaStreamDestroy(c->bias_stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (cudaStream_t ps : c->part_streams) cudaStreamDestroy(ps);
   cudaFree(c->d_dotA);
   cudaFree(c->d_dotB);
   cudaFree(c->d_dig);
