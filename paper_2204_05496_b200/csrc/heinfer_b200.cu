@@ -359,6 +359,7 @@ struct hei_gpu_ctx {
   cudaStream_t side_stream = nullptr;
   std::vector<cudaStream_t> part_streams;  // fold slices 1.. of a batch
   uint32_t fold_parts = 2;                 // HEI_FOLD_PARTS: concurrent fold slices per batch
+  uint32_t mask_group = 8;                 // HEI_MASK_GROUP: max pairs per mask/pack block
   cudaStream_t bias_stream = nullptr;  // bias plaintext encoding, overlapped with the fold
   uint32_t* pool_biasp = nullptr;
   size_t pool_biasp_bytes = 0;
@@ -636,7 +637,7 @@ void launch_mask_acc(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32
   const size_t sm = smem_bytes(c, 1);
   const uint32_t npairs = blocks / g.P;
   // enough blocks for every SM at small batches, up to 8 pairs per block
-  const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(8, npairs * g.P / (148 * 8)));
+  const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(c->mask_group, npairs * g.P / (148 * 8)));
   const unsigned gblocks = (unsigned)(((npairs + G - 1) / G) * g.P);
   HEI_DISPATCH(c->logn, (k_mask_acc_g<LG><<<gblocks, Ntt<LG>::T, 3 * sm, st>>>(g, res, rows, cols, npairs, G, acc)),
                (k_mask_acc<<<blocks, c->threads(), sm, st>>>(g, res, rows, cols, acc)));
@@ -1475,6 +1476,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_KS_TMA")) c->ks_tma = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_FOLD_PARTS")) c->fold_parts = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("HEI_MASK_GROUP")) c->mask_group = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_DIG_TMA")) c->dig_tma = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_LAT_TMA")) c->lat_tma = std::atoi(v) != 0;
     c->n = n;
