@@ -76,8 +76,9 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* ctx);
 /* GaloisKeySet of one branch (keys.hpp:44-49); elts ascending. */
 int hei_gpu_upload_galois_keys(hei_gpu_ctx* ctx, uint32_t branch, uint32_t count,
                                const uint64_t* elts, const uint64_t* rows);
-/* PublicKey of one branch, coeff form [2][L][N] (keys.hpp:28-32); needed only
- * by the standard (baseline) algorithm, which encrypts internally. */
+/* PublicKey of one branch, coeff form [2][L][N] (keys.hpp:28-32); needed by
+ * the encrypting calls only: the standard (baseline) algorithm and client
+ * encryption (hei_gpu_encode_inputs). */
 int hei_gpu_upload_public_key(hei_gpu_ctx* ctx, uint32_t branch, const uint64_t* pk);
 
 /* Weights. hei_gpu_weights_create uploads EncodedWeights values as produced by
