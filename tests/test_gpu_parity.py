@@ -708,3 +708,44 @@ def test_feature_block_sharding_bit_exact(prod, R, f, world):
     torch.cuda.synchronize()
     got = out.cpu().numpy().view(np.uint32).astype(np.uint64)
     assert np.array_equal(got, want)
+
+
+def test_full_precision_range_roundtrip():
+    """test_matmul.cpp:227-256 restated: 44-bit products on the production
+    plaintext moduli pair at N = 8 (s_x = 0, s_w = 22, 22-bit inputs) survive
+    the encrypted matmul and the device decryption exactly."""
+    from paper_2204_05496_b200 import EncodedWeights, matmul
+
+    p = TwinParams(n=8, t0=1073872897, t1=114689, sec=0, s_x=0, s_w=22, in_bits=22)
+    o = Oracle(p, key_seed=5, enc_seed=6)
+    s = gpu_server_from(o, with_sk=True)
+
+    def run(xv, wv, bv):
+        x = np.array([[xv]], np.int64)
+        w = np.array([[wv]], np.int64)
+        got, _ = matmul(s, o.encode_inputs(x), EncodedWeights.from_prepared(s, o.encode_weights(w), 1), [bv])
+        v = s.unpack_results(got, 1, 1)[0, 0]
+        assert v == o.unpack(got, 1, 1)[0, 0]
+        return int(v)
+
+    assert run(1 << 21, 1 << 22, 0) == 1 << 43
+    assert run(-(1 << 21), 1 << 22, 0) == -(1 << 43)
+    assert run(1 << 21, 1 << 22, -1) == (1 << 43) - 1
+    assert run((1 << 21) - 1, -(1 << 22) + 1, 12345) == -((1 << 43) - (1 << 22) - (1 << 21) + 1) + 12345
+
+
+@pytest.mark.parametrize("f", [8192, 8193, 40960])
+def test_chunk_boundary_feature_counts(prod, f):
+    """Feature counts on chunk boundaries (exactly one full chunk, one value
+    spilling into a second, and the 40,960-feature maximum of test_fpcrt's
+    twin dot, test_fpcrt.cpp:171-218): bit-exact and exact after decryption."""
+    from paper_2204_05496_b200 import EncodedWeights, matmul
+
+    o, s = prod
+    x, w, b = synthetic(1, f, 2, 0.03, 0.05, seed=f)
+    inputs = o.encode_inputs(x)
+    wp = o.encode_weights(w)
+    want, _ = o.fast_matmul(inputs, f, wp, b)
+    got, _ = matmul(s, inputs, EncodedWeights.from_prepared(s, wp, f), b)
+    assert np.array_equal(got, want)
+    assert np.array_equal(o.unpack(got, 1, 2), oracle_matmul(x, w, b))
