@@ -749,3 +749,31 @@ def test_chunk_boundary_feature_counts(prod, f):
     got, _ = matmul(s, inputs, EncodedWeights.from_prepared(s, wp, f), b)
     assert np.array_equal(got, want)
     assert np.array_equal(o.unpack(got, 1, 2), oracle_matmul(x, w, b))
+
+
+@pytest.mark.parametrize("n", [32, 8192])
+def test_ntt_product_equals_negacyclic_schoolbook(n):
+    """test_ring.cpp:103-167 property restated on the device transforms:
+    INTT(NTT(a) * NTT(b)) is the negacyclic product a * b mod (x^n + 1, q)."""
+    p = production_params(n) if n >= 8192 else tiny_params(n)
+    o = Oracle(p, 3, 4)
+    s = gpu_server_from(o)
+    rng = np.random.default_rng(17 + n)
+    q = int(o.q[0])
+    a = rng.integers(0, q, size=n, dtype=np.uint64)
+    b = np.zeros(n, np.uint64)
+    b[rng.choice(n, 5, replace=False)] = rng.integers(0, q, size=5, dtype=np.uint64)  # sparse: cheap schoolbook
+    fa, fb = s.ntt(0, 0, a[None]), s.ntt(0, 0, b[None])
+    prod = ((fa.astype(object) * fb.astype(object)) % q).astype(np.uint64)
+    got = s.ntt(0, 0, prod, inverse=True)[0]
+    want = [0] * n
+    for j in np.nonzero(b)[0]:
+        bj = int(b[j])
+        for i in range(n):
+            k = i + int(j)
+            v = int(a[i]) * bj
+            if k >= n:
+                k -= n
+                v = -v
+            want[k] = (want[k] + v) % q
+    assert [int(v) for v in got] == want
