@@ -777,3 +777,23 @@ def test_ntt_product_equals_negacyclic_schoolbook(n):
                 v = -v
             want[k] = (want[k] + v) % q
     assert [int(v) for v in got] == want
+
+
+def test_device_pipeline_multi_ciphertext_output_exact():
+    """Everything on the device at a size the CPU oracle cannot check quickly:
+    keygen, client encryption of 800 individuals, the host-buffer matmul
+    (ramped chunk copies) with 800 x 11 = 8800 results spilling into a second
+    packed ciphertext, and decryption — equal to the exact integer product."""
+    from paper_2204_05496_b200 import GpuTwinServer, Prng, ScalingConfig, encode_inputs, encode_weights, matmul
+
+    p = production_params(8192)
+    o = Oracle(TwinParams(n=8192, t0=p.t0, t1=p.t1, sec=128), 1, 2)  # only for the q chain
+    s = GpuTwinServer(8192, (p.t0, p.t1), o.L, o.q, [], None, ScalingConfig(), security_level=128)
+    s.keygen(Prng(1))
+    R, f, cols = 800, 1000, 11
+    x, w, b = synthetic(R, f, cols, 0.05, 0.1, seed=99)
+    inputs = encode_inputs(s, x, Prng(2), Prng(3))
+    packed, cnt = matmul(s, inputs, encode_weights(s, w), b)
+    assert packed.shape[0] == 2
+    assert np.array_equal(s.unpack_results(packed, R, cols), oracle_matmul(x, w, b))
+    assert cnt.ciphertexts_out == 2
