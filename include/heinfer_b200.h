@@ -66,6 +66,11 @@ typedef struct {
   int device;
 } hei_twin_desc;
 
+/* bfv::default_q_primes (params.cpp:84-104): the ciphertext modulus chain
+ * make_params derives for (n, t) — the q[] a hei_twin_desc expects per
+ * branch. Host only. */
+int hei_default_q_primes(uint32_t n, uint64_t t, uint64_t* out, uint32_t capacity, uint32_t* count);
+
 const char* hei_gpu_last_error(void);
 const char* hei_gpu_version(void);
 

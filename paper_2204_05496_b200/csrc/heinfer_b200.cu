@@ -2411,6 +2411,37 @@ int hei_gpu_matmul(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint64_t* inp
   });
 }
 
+int hei_default_q_primes(uint32_t n, uint64_t t, uint64_t* out, uint32_t capacity, uint32_t* count) {
+  // bfv::default_q_primes (params.cpp:84-104) over ring::find_ntt_primes
+  // (modulus.cpp:54-71): descending candidates = 1 mod 2n below 2^bits.
+  return guarded([&] {
+    if (!n || (n & (n - 1))) raise(HEI_PARAM_ERROR, "n must be a power of two");
+    const int bits = n >= 4096 ? 31 : 30;
+    size_t want;
+    if (n >= 4096) {
+      want = t >= (1ull << 25) ? 6 : 4;
+    } else {
+      const int tb = 64 - __builtin_clzll(t);
+      want = (size_t)(7 * tb / 2 + 50 + 29) / 30;
+      if (want < 2) want = 2;
+    }
+    const uint64_t two_n = 2ull * n;
+    std::vector<uint64_t> found;
+    uint64_t c = ((((1ull << bits) - 2) / two_n) * two_n) + 1;
+    while (found.size() < want && c > (1ull << (bits - 1))) {
+      if (c != t && is_prime(c)) found.push_back(c);
+      if (c < two_n) break;
+      c -= two_n;
+    }
+    if (found.size() < want) raise(HEI_PARAM_ERROR, "not enough NTT-friendly primes of the requested size");
+    if (count) *count = (uint32_t)found.size();
+    if (out) {
+      if (capacity < found.size()) raise(HEI_PARAM_ERROR, "default_q_primes: output buffer too small");
+      std::memcpy(out, found.data(), found.size() * 8);
+    }
+  });
+}
+
 uint64_t hei_hect_ciphertext_bytes(uint32_t n, uint32_t num_primes) { return hect_bytes(n, num_primes); }
 
 uint64_t hei_params_hash(uint32_t n, uint64_t t, int security_level, const uint64_t* q, uint32_t num_primes) {

@@ -403,3 +403,11 @@ def matmul_wire(server: GpuTwinServer, w: EncodedWeights, blobs, rows: int, bias
         res.append(bytes(out[base: base + b0]))
         res.append(bytes(out[base + b0: base + b0 + b1]))
     return res, cnt
+
+
+def default_q_primes(n: int, t: int) -> list:
+    """bfv::default_q_primes (params.cpp:84-104): the q chain of one branch."""
+    out = np.zeros(16, np.uint64)
+    cnt = C.c_uint32(0)
+    check(native.lib().hei_default_q_primes(C.c_uint32(n), C.c_uint64(t), u64p(out), C.c_uint32(16), C.byref(cnt)))
+    return [int(v) for v in out[: cnt.value]]

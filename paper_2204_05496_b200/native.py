@@ -103,6 +103,7 @@ EXPORTED = [
     "hei_gpu_upload_secret_key", "hei_gpu_decrypt_signed", "hei_gpu_noise_budget",
     "hei_gpu_unpack_results", "hei_gpu_unpack_baseline", "hei_gpu_keygen",
     "hei_gpu_debug_rejection_plan", "hei_gpu_chunk_dot_partial_device", "hei_gpu_fold_pack_device",
+    "hei_default_q_primes",
 ]
 
 _lib = None

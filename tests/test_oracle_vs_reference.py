@@ -106,3 +106,25 @@ def test_wire_constants_match_reference(n):
     per = lib.hei_hect_ciphertext_bytes(n, ref.L[0]) + lib.hei_hect_ciphertext_bytes(n, ref.L[1])
     assert len(blobs) == 2 * per
     assert blobs[:4] == b"HECT" and blobs[18] == 5
+
+
+@pytest.mark.parametrize("n,t", [(8, 7681), (32, 12289), (8, 1073872897), (4096, 114689), (8192, 1073872897),
+                                 (8192, 114689), (16384, 1073872897), (16384, 163841)])
+def test_default_q_primes_match_make_params(n, t):
+    """hei_default_q_primes == bfv::make_params(n, t, .).q (params.cpp:84-114)."""
+    import ctypes as C
+
+    from paper_2204_05496_b200 import default_q_primes
+
+    lib = ref_lib_handle()
+    out = np.zeros(32, np.uint64)
+    cnt = C.c_uint32(0)
+    assert lib.ref_default_primes(C.c_uint32(n), C.c_uint64(t), C.c_int(0), out.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                  C.byref(cnt)) == 0
+    assert default_q_primes(n, t) == [int(v) for v in out[: cnt.value]]
+
+
+def ref_lib_handle():
+    from oracle.oracle import ref_lib
+
+    return ref_lib()
