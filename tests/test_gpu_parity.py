@@ -797,3 +797,41 @@ def test_device_pipeline_multi_ciphertext_output_exact():
     assert packed.shape[0] == 2
     assert np.array_equal(s.unpack_results(packed, R, cols), oracle_matmul(x, w, b))
     assert cnt.ciphertexts_out == 2
+
+
+def test_stream_concurrent_push_from_threads(tiny32):
+    """MatmulStream::push_row may be called concurrently from many threads,
+    rows in any order (matmul.hpp:79-82; test_matmul.cpp:326-356 order and
+    thread invariance): four host threads pushing interleaved rows give the
+    same packed ciphertexts as one call."""
+    import threading
+
+    from paper_2204_05496_b200 import EncodedWeights, MatmulStream, matmul
+
+    o, s = tiny32
+    rng = np.random.default_rng(31)
+    R = 24
+    x = random_mat(rng, R, 40, 20)
+    w = random_mat(rng, 40, 3, 5)
+    b = np.array([1, -2, 3])
+    inputs = o.encode_inputs(x)
+    ew = EncodedWeights.from_prepared(s, o.encode_weights(w), 40)
+    want, _ = matmul(s, inputs, ew, b)
+    st = MatmulStream(s, ew, b, R)
+    order = rng.permutation(R)
+    errors = []
+
+    def worker(k):
+        try:
+            for r in order[k::4]:
+                st.push_row(int(r), inputs[r])
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors
+    assert np.array_equal(st.finish(), want)
