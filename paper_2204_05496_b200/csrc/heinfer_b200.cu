@@ -2325,10 +2325,12 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
   const size_t words = w->kc * c->ct_words();
   const size_t row_bytes = wire ? w->kc * (io.wg.blob[0] + io.wg.blob[1]) : words * 8;
   const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(s->cap_rows, (rows + c->e2e_div - 1) / c->e2e_div));
-  const size_t slot_bytes = (chunk * row_bytes + 64) & ~(size_t)15;  // + pad for the parser's 12-byte window
+  // a slot holds up to 1.5 chunks so the final tail can be absorbed
+  const uint64_t slot_rows = std::min<uint64_t>(s->cap_rows, chunk + chunk / 2);
+  const size_t slot_bytes = (slot_rows * row_bytes + 64) & ~(size_t)15;  // + pad for the parser's 12-byte window
   uint8_t* stage = reinterpret_cast<uint8_t*>(
       pool_get(c->pool_stage64, c->pool_stage64_bytes, 2 * slot_bytes));
-  uint32_t* in32 = pool_get(c->pool_in32, c->pool_in32_bytes, 2 * chunk * words * 4);
+  uint32_t* in32 = pool_get(c->pool_in32, c->pool_in32_bytes, 2 * slot_rows * words * 4);
   uint64_t* d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, rows * 8);
   k_iota<<<grid_for(rows, 256), 256, 0, st>>>(d_rows, 0, rows);
   LAUNCHED();
@@ -2340,14 +2342,16 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
   }
   const uint8_t* src = wire ? io.wire : reinterpret_cast<const uint8_t*>(io.u64);
   // chunk sizes ramp up (chunk/8, chunk/4, ..., chunk) so the first copy,
-  // the only one not hidden behind compute, is short
+  // the only one not hidden behind compute, is short; a tail smaller than
+  // half the next chunk is absorbed (no small launches at the end)
   uint64_t nr_next = std::max<uint64_t>(1, chunk / 8);
   for (uint64_t b = 0, r0 = 0; r0 < rows; ++b) {
     const int slot = (int)(b % 2);
-    const uint64_t nr = std::min<uint64_t>(nr_next, rows - r0);
+    uint64_t nr = std::min<uint64_t>(nr_next, rows - r0);
+    if (rows - r0 - nr < std::min<uint64_t>(chunk, 2 * nr_next) / 2 && rows - r0 <= slot_rows) nr = rows - r0;
     nr_next = std::min<uint64_t>(chunk, 2 * nr_next);
     uint8_t* sb = stage + (size_t)slot * slot_bytes;
-    uint32_t* s32 = in32 + (size_t)slot * chunk * words;
+    uint32_t* s32 = in32 + (size_t)slot * slot_rows * words;
     CU(cudaStreamWaitEvent(cs, narrowed[slot], 0));
     CU(cudaMemcpyAsync(sb, src + r0 * row_bytes, nr * row_bytes, cudaMemcpyHostToDevice, cs));
     CU(cudaEventRecord(copied[slot], cs));
