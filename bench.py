@@ -365,7 +365,7 @@ def run_ours(args, world, rank, local):
                "d2h_bytes_per_step": int(out.nbytes), "ms_per_step": 1000 * e2e_s}
         # the server's wire path (server.cpp:112-172): HECT coeff-form blobs
         # in, HECT blobs out, parse/NTT/INTT/serialize on the device
-        if args.wire:
+        if args.wire and world == 1:  # the wire copy doubles pinned host memory; one rank only
             e2e["wire"] = wire_e2e(srv, ew, b, h_np, R, kc, n, len(q0), len(q1), world, e2e_steps)
         del h_in, h_np
 
