@@ -309,16 +309,41 @@ def run_ours(args, world, rank, local):
 
         total_rows = world * R
         Ct = packed_count(total_rows, cols, n)
-        acc = torch.zeros((Ct, ctw), dtype=torch.int64, device=dev)
         d_out = torch.empty((Ct, ctw), dtype=torch.int32, device=dev)
+        exchange = os.environ.get("HEI_EXCHANGE", "p2p")
+        peer = None
+        if exchange == "p2p":
+            # rank 0's accumulator mapped into every rank (CUDA IPC over
+            # NVLink): the mask/pack kernels add into it directly, so the
+            # exchange rides on the compute; host barriers order the phases
+            from paper_2204_05496_b200.sharding import PeerAccumulator
 
-        def step():
-            with torch.cuda.stream(stream):
-                acc.zero_()
-            matmul_partial_device(srv, ew, d_in.data_ptr(), R, rank * R, total_rows, acc.data_ptr(), stream.cuda_stream)
-            with torch.cuda.stream(stream):
-                torch.distributed.all_reduce(acc)
-            finish_packed_device(srv, ew, acc.data_ptr(), b, total_rows, d_out.data_ptr(), stream.cuda_stream)
+            try:
+                peer = PeerAccumulator(Ct * ctw * 8, local)
+            except Exception as e:  # no peer access: fall back to the collective
+                print(f"[bench] p2p exchange unavailable ({e}); using NCCL all_reduce", file=sys.stderr)
+                exchange = "nccl"
+        if exchange == "p2p":
+            def step():
+                if rank == 0:
+                    peer.zero(stream.cuda_stream)
+                    stream.synchronize()
+                torch.distributed.barrier()
+                matmul_partial_device(srv, ew, d_in.data_ptr(), R, rank * R, total_rows, peer.ptr, stream.cuda_stream)
+                torch.distributed.barrier()  # every rank's adds have landed
+                if rank == 0:
+                    finish_packed_device(srv, ew, peer.ptr, b, total_rows, d_out.data_ptr(), stream.cuda_stream)
+        else:
+            acc = torch.zeros((Ct, ctw), dtype=torch.int64, device=dev)
+
+            def step():
+                with torch.cuda.stream(stream):
+                    acc.zero_()
+                matmul_partial_device(srv, ew, d_in.data_ptr(), R, rank * R, total_rows, acc.data_ptr(),
+                                      stream.cuda_stream)
+                with torch.cuda.stream(stream):
+                    torch.distributed.all_reduce(acc)
+                finish_packed_device(srv, ew, acc.data_ptr(), b, total_rows, d_out.data_ptr(), stream.cuda_stream)
 
     for _ in range(args.warmup):
         with torch.cuda.stream(stream):
@@ -489,7 +514,8 @@ def run_ours(args, world, rank, local):
                                f"twin t=({T0},{T1 if n < 16384 else T1_16K}), L=({len(q0)},{len(q1)})",
                    "inputs": "real encryptions (device keygen from Prng(1), client encryption with Prng(2),(3)) of "
                              "seeded Bernoulli features, resident in HBM; inputs > L2 (no flush needed)",
-                   "parallelism": f"dp{world} (individual sharding)"},
+                   "parallelism": f"dp{world} (individual sharding)" + (
+                       f", exchange={exchange}" if world > 1 else "")},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": e2e,

@@ -2851,6 +2851,47 @@ int hei_gpu_matmul_partial_device(hei_gpu_ctx* c, const hei_gpu_weights* w, cons
   });
 }
 
+// Peer-memory exchange for sharded runs: a rank exports its packed
+// accumulator with CUDA IPC; the other ranks map it and their mask/pack
+// kernels add into it directly (u64 atomics over NVLink), so the partial-sum
+// exchange rides on the compute instead of a separate collective.
+// Plain device buffers (base allocations, as CUDA IPC requires).
+int hei_gpu_buffer_alloc(int device, uint64_t bytes, void** d_ptr) {
+  return guarded([&] {
+    if (!d_ptr) raise(HEI_PARAM_ERROR, "buffer: null argument");
+    CU(cudaSetDevice(device));
+    CU(cudaMalloc(d_ptr, bytes));
+  });
+}
+int hei_gpu_buffer_zero(void* d_ptr, uint64_t bytes, void* stream) {
+  return guarded([&] { CU(cudaMemsetAsync(d_ptr, 0, bytes, (cudaStream_t)stream)); });
+}
+void hei_gpu_buffer_free(void* d_ptr) { cudaFree(d_ptr); }
+
+int hei_gpu_ipc_handle(const void* d_ptr, uint8_t* handle64) {
+  return guarded([&] {
+    if (!d_ptr || !handle64) raise(HEI_PARAM_ERROR, "ipc: null argument");
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle64, &h, sizeof(h));
+  });
+}
+
+int hei_gpu_ipc_open(int device, const uint8_t* handle64, void** d_ptr) {
+  return guarded([&] {
+    if (!handle64 || !d_ptr) raise(HEI_PARAM_ERROR, "ipc: null argument");
+    CU(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    CU(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int hei_gpu_ipc_close(void* d_ptr) {
+  return guarded([&] { CU(cudaIpcCloseMemHandle(d_ptr)); });
+}
+
 int hei_gpu_chunk_dot_partial_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint32_t* d_inputs,
                                      uint64_t rows, uint64_t chunk_lo, uint64_t chunk_count, uint64_t* d_dot,
                                      void* stream) {

@@ -103,7 +103,8 @@ EXPORTED = [
     "hei_gpu_upload_secret_key", "hei_gpu_decrypt_signed", "hei_gpu_noise_budget",
     "hei_gpu_unpack_results", "hei_gpu_unpack_baseline", "hei_gpu_keygen",
     "hei_gpu_debug_rejection_plan", "hei_gpu_chunk_dot_partial_device", "hei_gpu_fold_pack_device",
-    "hei_default_q_primes",
+    "hei_default_q_primes", "hei_gpu_ipc_handle", "hei_gpu_ipc_open", "hei_gpu_ipc_close",
+    "hei_gpu_buffer_alloc", "hei_gpu_buffer_zero", "hei_gpu_buffer_free",
 ]
 
 _lib = None
@@ -128,6 +129,8 @@ def lib() -> C.CDLL:
         l.hei_gpu_reset_launch_count.restype = None
         l.hei_gpu_set_batch_pairs.restype = None
         l.hei_gpu_set_batch_pairs.argtypes = [C.c_void_p, C.c_uint64]
+        l.hei_gpu_buffer_free.restype = None
+        l.hei_gpu_buffer_free.argtypes = [C.c_void_p]
         l.hei_hect_ciphertext_bytes.restype = C.c_uint64
         l.hei_hect_ciphertext_bytes.argtypes = [C.c_uint32, C.c_uint32]
         l.hei_params_hash.restype = C.c_uint64

@@ -116,3 +116,49 @@ def reduce_scatter_dots(dot, total_rows: int, group=None):
         dist.reduce_scatter_tensor(out, padded, op=dist.ReduceOp.SUM, group=group)
     lo, cnt = shard_rows(total_rows, world, rank)
     return out[: cnt * per_row]
+
+
+class PeerAccumulator:
+    """The packed u64 accumulator of `owner` rank, mapped into every rank
+    (CUDA IPC; NVLink peer memory between GPUs): matmul_partial_device on any
+    rank adds into it directly with u64 atomics, so the exchange needs no
+    collective — only a barrier before the owner's finish. `ptr` is the
+    device pointer valid on this rank."""
+
+    def __init__(self, nbytes: int, device: int, owner: int = 0, group=None):
+        import torch.distributed as dist
+
+        self.owner, self.nbytes = owner, int(nbytes)
+        self.rank = dist.get_rank(group)
+        self._own = None
+        self._mapped = None
+        handle = [None]
+        if self.rank == owner:
+            p = C.c_void_p()
+            check(native.lib().hei_gpu_buffer_alloc(C.c_int(device), C.c_uint64(self.nbytes), C.byref(p)))
+            self._own = p
+            check(native.lib().hei_gpu_buffer_zero(p, C.c_uint64(self.nbytes), None))
+            h = (C.c_uint8 * 64)()
+            check(native.lib().hei_gpu_ipc_handle(p, h))
+            handle[0] = bytes(h)
+            self.ptr = p.value
+        dist.broadcast_object_list(handle, src=owner, group=group)
+        if self.rank != owner:
+            p = C.c_void_p()
+            hb = (C.c_uint8 * 64).from_buffer_copy(handle[0])
+            check(native.lib().hei_gpu_ipc_open(C.c_int(device), hb, C.byref(p)))
+            self._mapped = p
+            self.ptr = p.value
+
+    def zero(self, stream_ptr: int = 0) -> None:
+        """Owner only: clear before the ranks add (then barrier)."""
+        if self._own is not None:
+            check(native.lib().hei_gpu_buffer_zero(self._own, C.c_uint64(self.nbytes), C.c_void_p(stream_ptr)))
+
+    def close(self) -> None:
+        if self._mapped is not None:
+            check(native.lib().hei_gpu_ipc_close(self._mapped))
+            self._mapped = None
+        if self._own is not None:
+            native.lib().hei_gpu_buffer_free(self._own)
+            self._own = None
