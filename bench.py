@@ -311,31 +311,35 @@ def run_ours(args, world, rank, local):
         Ct = packed_count(total_rows, cols, n)
         d_out = torch.empty((Ct, ctw), dtype=torch.int32, device=dev)
         exchange = os.environ.get("HEI_EXCHANGE", "p2p")
-        peer = None
+        acc = torch.zeros((Ct, ctw), dtype=torch.int64, device=dev)
+        gather = None
         if exchange == "p2p":
-            # rank 0's accumulator mapped into every rank (CUDA IPC over
-            # NVLink): the mask/pack kernels add into it directly, so the
-            # exchange rides on the compute; host barriers order the phases
-            from paper_2204_05496_b200.sharding import PeerAccumulator
+            # each rank writes its packed accumulator into its slot of rank
+            # 0's receive buffer through a CUDA IPC mapping (an NVLink peer
+            # write); rank 0 sums the slots and finishes — no collective
+            from paper_2204_05496_b200.sharding import PeerGather
 
             try:
-                peer = PeerAccumulator(Ct * ctw * 8, local)
+                gather = PeerGather(Ct * ctw * 8, local)
             except Exception as e:  # no peer access: fall back to the collective
                 print(f"[bench] p2p exchange unavailable ({e}); using NCCL all_reduce", file=sys.stderr)
                 exchange = "nccl"
         if exchange == "p2p":
             def step():
+                with torch.cuda.stream(stream):
+                    acc.zero_()
+                matmul_partial_device(srv, ew, d_in.data_ptr(), R, rank * R, total_rows, acc.data_ptr(),
+                                      stream.cuda_stream)
+                stream.synchronize()
+                torch.distributed.barrier()  # the owner's previous reduce/finish is done with the slots
+                gather.push(acc.data_ptr(), stream.cuda_stream)
+                stream.synchronize()
+                torch.distributed.barrier()  # every slot written
                 if rank == 0:
-                    peer.zero(stream.cuda_stream)
-                    stream.synchronize()
-                torch.distributed.barrier()
-                matmul_partial_device(srv, ew, d_in.data_ptr(), R, rank * R, total_rows, peer.ptr, stream.cuda_stream)
-                torch.distributed.barrier()  # every rank's adds have landed
-                if rank == 0:
-                    finish_packed_device(srv, ew, peer.ptr, b, total_rows, d_out.data_ptr(), stream.cuda_stream)
+                    gather.reduce(stream.cuda_stream)
+                    finish_packed_device(srv, ew, gather.total_ptr, b, total_rows, d_out.data_ptr(),
+                                         stream.cuda_stream)
         else:
-            acc = torch.zeros((Ct, ctw), dtype=torch.int64, device=dev)
-
             def step():
                 with torch.cuda.stream(stream):
                     acc.zero_()

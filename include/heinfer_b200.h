@@ -178,13 +178,15 @@ int hei_gpu_matmul_partial_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, co
 int hei_gpu_finish_packed_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint64_t* d_acc,
                                  const int64_t* bias, uint64_t total_rows, uint32_t* d_out, void* stream);
 
-/* Peer-memory exchange: export a device buffer (the owner rank's
- * packed accumulator) as a 64-byte CUDA IPC handle; another rank opens it and
- * passes the mapped pointer as d_acc of hei_gpu_matmul_partial_device, so its
- * mask/pack kernel adds straight into the owner's memory over NVLink. */
+/* Peer-memory exchange: the owner rank exports a receive buffer
+ * (one slot per rank) as a 64-byte CUDA IPC handle; every rank maps it and
+ * writes its packed accumulator into its slot with a device-to-device copy
+ * (an NVLink peer write); the owner sums the slots (exact u64) and finishes. */
 int hei_gpu_buffer_alloc(int device, uint64_t bytes, void** d_ptr);
 int hei_gpu_buffer_zero(void* d_ptr, uint64_t bytes, void* stream);
 void hei_gpu_buffer_free(void* d_ptr);
+int hei_gpu_copy_async(void* dst, const void* src, uint64_t bytes, void* stream);
+int hei_gpu_sum_slots(void* d, uint64_t words, uint32_t count, void* stream);
 int hei_gpu_ipc_handle(const void* d_ptr, uint8_t* handle64);
 int hei_gpu_ipc_open(int device, const uint8_t* handle64, void** d_ptr);
 int hei_gpu_ipc_close(void* d_ptr);

@@ -2868,6 +2868,29 @@ int hei_gpu_buffer_zero(void* d_ptr, uint64_t bytes, void* stream) {
 }
 void hei_gpu_buffer_free(void* d_ptr) { cudaFree(d_ptr); }
 
+// Device-to-device copy on `stream`; with an IPC-mapped destination this is
+// a peer write over NVLink.
+int hei_gpu_copy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
+  return guarded([&] { CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream)); });
+}
+
+// slots[0] += slots[1] + ... + slots[count-1] over `words` u64 each (the
+// owner's reduction of gathered per-rank packed accumulators; exact).
+__global__ void k_sum_slots(unsigned long long* __restrict__ d, uint64_t words, uint32_t count) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < words; x += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long acc = d[x];
+    for (uint32_t k = 1; k < count; ++k) acc += d[(uint64_t)k * words + x];
+    d[x] = acc;
+  }
+}
+int hei_gpu_sum_slots(void* d, uint64_t words, uint32_t count, void* stream) {
+  return guarded([&] {
+    k_sum_slots<<<grid_for(words, 256), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<unsigned long long*>(d),
+                                                                      words, count);
+    LAUNCHED();
+  });
+}
+
 int hei_gpu_ipc_handle(const void* d_ptr, uint8_t* handle64) {
   return guarded([&] {
     if (!d_ptr || !handle64) raise(HEI_PARAM_ERROR, "ipc: null argument");

@@ -118,42 +118,49 @@ def reduce_scatter_dots(dot, total_rows: int, group=None):
     return out[: cnt * per_row]
 
 
-class PeerAccumulator:
-    """The packed u64 accumulator of `owner` rank, mapped into every rank
-    (CUDA IPC; NVLink peer memory between GPUs): matmul_partial_device on any
-    rank adds into it directly with u64 atomics, so the exchange needs no
-    collective — only a barrier before the owner's finish. `ptr` is the
-    device pointer valid on this rank."""
+class PeerGather:
+    """Exchange of the ranks' packed u64 accumulators over peer memory:
+    `owner` allocates a receive buffer with one slot per rank and exports it
+    with CUDA IPC; every rank maps it (an NVLink peer mapping between GPUs)
+    and `push` writes its accumulator into its slot with one device-to-device
+    copy. After a barrier the owner's `reduce` sums the slots (exact u64) into
+    slot 0, whose pointer is `total_ptr`. No collective library involved."""
 
     def __init__(self, nbytes: int, device: int, owner: int = 0, group=None):
         import torch.distributed as dist
 
         self.owner, self.nbytes = owner, int(nbytes)
-        self.rank = dist.get_rank(group)
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self._own = None
         self._mapped = None
         handle = [None]
         if self.rank == owner:
             p = C.c_void_p()
-            check(native.lib().hei_gpu_buffer_alloc(C.c_int(device), C.c_uint64(self.nbytes), C.byref(p)))
+            check(native.lib().hei_gpu_buffer_alloc(C.c_int(device), C.c_uint64(self.nbytes * self.world), C.byref(p)))
             self._own = p
-            check(native.lib().hei_gpu_buffer_zero(p, C.c_uint64(self.nbytes), None))
             h = (C.c_uint8 * 64)()
             check(native.lib().hei_gpu_ipc_handle(p, h))
             handle[0] = bytes(h)
-            self.ptr = p.value
+            self.base = p.value
         dist.broadcast_object_list(handle, src=owner, group=group)
         if self.rank != owner:
             p = C.c_void_p()
             hb = (C.c_uint8 * 64).from_buffer_copy(handle[0])
             check(native.lib().hei_gpu_ipc_open(C.c_int(device), hb, C.byref(p)))
             self._mapped = p
-            self.ptr = p.value
+            self.base = p.value
+        self.total_ptr = self.base
 
-    def zero(self, stream_ptr: int = 0) -> None:
-        """Owner only: clear before the ranks add (then barrier)."""
+    def push(self, local_ptr: int, stream_ptr: int = 0) -> None:
+        dst = self.base + self.rank * self.nbytes
+        check(native.lib().hei_gpu_copy_async(C.c_void_p(dst), C.c_void_p(local_ptr), C.c_uint64(self.nbytes),
+                                              C.c_void_p(stream_ptr)))
+
+    def reduce(self, stream_ptr: int = 0) -> None:
+        """Owner only, after every rank's push has completed (barrier)."""
         if self._own is not None:
-            check(native.lib().hei_gpu_buffer_zero(self._own, C.c_uint64(self.nbytes), C.c_void_p(stream_ptr)))
+            check(native.lib().hei_gpu_sum_slots(self._own, C.c_uint64(self.nbytes // 8), C.c_uint32(self.world),
+                                                 C.c_void_p(stream_ptr)))
 
     def close(self) -> None:
         if self._mapped is not None:

@@ -1,9 +1,9 @@
 """Multi-rank exchange over peer memory (CUDA IPC), two processes on one GPU.
 
-Each rank encrypts and processes its own rows; the mask/pack kernels of both
-ranks add straight into rank 0's packed accumulator through the IPC mapping
-(on a multi-GPU box this is NVLink peer memory), and rank 0 finishes and
-decrypts. The kernels of the two ranks never wait on each other — only host
+Each rank encrypts and processes its own rows into its own packed
+accumulator, writes it into its slot of rank 0's receive buffer through the
+IPC mapping (on a multi-GPU box: an NVLink peer write), and rank 0 sums the
+slots, finishes and decrypts. The kernels of the two ranks never wait on each other — only host
 barriers order the phases — so this checks the plumbing and the exactness of
 the exchange, not multi-GPU performance.
 """
@@ -32,7 +32,7 @@ def _worker(rank, world, port, rows_per_rank, result_path):
     from oracle.oracle import production_params
     from paper_2204_05496_b200 import (GpuTwinServer, Prng, ScalingConfig, default_q_primes, encode_inputs_device,
                                        encode_weights)
-    from paper_2204_05496_b200.sharding import PeerAccumulator, finish_packed_device, matmul_partial_device, packed_count
+    from paper_2204_05496_b200.sharding import PeerGather, finish_packed_device, matmul_partial_device, packed_count
     from tests.helpers import synthetic
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -51,19 +51,20 @@ def _worker(rank, world, port, rows_per_rank, result_path):
     encode_inputs_device(srv, x, Prng(2 + 2 * rank), Prng(3 + 2 * rank), d_in.data_ptr(), 0)
     ew = encode_weights(srv, w)
     Ct = packed_count(total, 11, 8192)
-    acc = PeerAccumulator(Ct * ctw * 8, 0)
+    gather = PeerGather(Ct * ctw * 8, 0)
+    acc = torch.zeros((Ct, ctw), dtype=torch.int64, device="cuda")
+    matmul_partial_device(srv, ew, d_in.data_ptr(), rows_per_rank, rank * rows_per_rank, total, acc.data_ptr())
+    gather.push(acc.data_ptr())
     torch.cuda.synchronize()
-    dist.barrier()
-    matmul_partial_device(srv, ew, d_in.data_ptr(), rows_per_rank, rank * rows_per_rank, total, acc.ptr)
-    torch.cuda.synchronize()
-    dist.barrier()  # every rank's adds have landed in rank 0's accumulator
+    dist.barrier()  # every rank's slot is written
     if rank == 0:
+        gather.reduce()
         out = torch.empty((Ct, ctw), dtype=torch.int32, device="cuda")
-        finish_packed_device(srv, ew, acc.ptr, b, total, out.data_ptr())
+        finish_packed_device(srv, ew, gather.total_ptr, b, total, out.data_ptr())
         packed = out.cpu().numpy().view(np.uint32).astype(np.uint64)
         np.save(result_path, srv.unpack_results(packed, total, 11))
     dist.barrier()
-    acc.close()
+    gather.close()
     dist.destroy_process_group()
 
 
