@@ -319,10 +319,15 @@ def run_ours(args, world, rank, local):
             # write); rank 0 sums the slots and finishes — no collective
             from paper_2204_05496_b200.sharding import PeerGather
 
+            ok = 1
             try:
                 gather = PeerGather(Ct * ctw * 8, local)
-            except Exception as e:  # no peer access: fall back to the collective
-                print(f"[bench] p2p exchange unavailable ({e}); using NCCL all_reduce", file=sys.stderr)
+            except Exception as e:  # no peer access on this rank
+                print(f"[bench] rank {rank}: p2p exchange unavailable ({e})", file=sys.stderr)
+                ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+            torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)  # every rank agrees
+            if int(flag.item()) == 0:
                 exchange = "nccl"
         if exchange == "p2p":
             def step():
