@@ -134,15 +134,24 @@ class PeerGather:
         self._own = None
         self._mapped = None
         handle = [None]
+        err = None
         if self.rank == owner:
-            p = C.c_void_p()
-            check(native.lib().hei_gpu_buffer_alloc(C.c_int(device), C.c_uint64(self.nbytes * self.world), C.byref(p)))
-            self._own = p
-            h = (C.c_uint8 * 64)()
-            check(native.lib().hei_gpu_ipc_handle(p, h))
-            handle[0] = bytes(h)
-            self.base = p.value
+            try:
+                p = C.c_void_p()
+                check(native.lib().hei_gpu_buffer_alloc(C.c_int(device), C.c_uint64(self.nbytes * self.world),
+                                                        C.byref(p)))
+                self._own = p
+                h = (C.c_uint8 * 64)()
+                check(native.lib().hei_gpu_ipc_handle(p, h))
+                handle[0] = bytes(h)
+                self.base = p.value
+            except Exception as e:  # still take part in the broadcast, then fail
+                err = e
         dist.broadcast_object_list(handle, src=owner, group=group)
+        if err is not None:
+            raise err
+        if handle[0] is None:
+            raise RuntimeError("peer gather: the owner could not export its buffer")
         if self.rank != owner:
             p = C.c_void_p()
             hb = (C.c_uint8 * 64).from_buffer_copy(handle[0])
