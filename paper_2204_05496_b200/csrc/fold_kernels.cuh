@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
                                                                     const uint2* __restrict__ key1,
                                                                     uint32_t* __restrict__ out, int fold,
                                                                     const uint32_t* __restrict__ perm_next,
-                                                                    uint32_t* __restrict__ dig_next, int tma,
+                                                                    uint32_t* __restrict__ dig_next,
                                                                     const __grid_constant__ TwArg<PTW> tab) {
   using NT = Ntt<LOGN>;
   constexpr uint32_t N = NT::N, T = NT::T;
@@ -582,6 +582,16 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
   const uint32_t* c0 = ct + (uint64_t)pr.poly0 * N;
   const uint32_t* c1 = ct + (uint64_t)pr.poly1 * N;
   const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * N;
+  // c1 (and, for the epilogue, c0) arrive in `sm` by one TMA bulk copy each;
+  // the Galois gathers then read shared memory instead of scattering 4-byte
+  // loads over L1/L2
+  __shared__ uint64_t gbar;
+  if (threadIdx.x == 0) {
+    mbar_init(&gbar, 1);
+    bulk_load(sm, c1, N * 4, &gbar);
+  }
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  mbar_wait(&gbar, 0);
   {
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * N) + j;
@@ -589,7 +599,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const uint4 pm = __ldg(pp + c);
-      const uint32_t d0 = c1[pm.x], d1 = c1[pm.y], d2 = c1[pm.z], d3 = c1[pm.w];
+      const uint32_t d0 = sm[pm.x], d1 = sm[pm.y], d2 = sm[pm.z], d3 = sm[pm.w];
       const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
       const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
       a0s[c * T + j] = make_uint4(mul_shoup(d0, a.x, a.y, q), mul_shoup(d1, a.z, a.w, q), mul_shoup(d2, b.x, b.y, q),
@@ -601,29 +611,9 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
   const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
   const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
   uint32_t e[16];
-  // tma: each digit polynomial (contiguous 4N bytes) arrives in `sm` through
-  // a TMA bulk copy issued while the previous digit's key products run.
-  __shared__ uint64_t bar;
-  uint32_t parity = 0;
-  if (tma) {
-    const uint32_t l0 = i == 0 ? 1u : 0u;
-    if (threadIdx.x == 0) {
-      mbar_init(&bar, 1);
-      bulk_load(sm, dig + (uint64_t)l0 * N, N * 4, &bar);
-    }
-    __syncthreads();  // the barrier is initialised before anyone waits on it
-  }
   for (uint32_t l = 0; l < L; ++l) {
     if (l == i) continue;
-    if (tma) {
-      mbar_wait(&bar, parity);
-      parity ^= 1u;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const uint32_t v = sm[NT::posA(j, r)];
-        e[r] = pr.fast_reduce ? min(v, v - q) : v % q;
-      }
-    } else {
+    {
       const uint32_t* src = dig + (uint64_t)l * N;
       if (pr.fast_reduce) {
 #pragma unroll
@@ -640,17 +630,6 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
       NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
     else
       NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
-    if (tma) {
-      uint32_t ln = l + 1;
-      if (ln == i) ++ln;
-      if (ln < L) {
-        __syncthreads();  // every thread's last read of sm in this transform is done
-        if (threadIdx.x == 0) {
-          fence_proxy_async_smem();
-          bulk_load(sm, dig + (uint64_t)ln * N, N * 4, &bar);
-        }
-      }
-    }
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
 #pragma unroll
@@ -673,17 +652,25 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
   }
   uint32_t* o = out + (uint64_t)pair * g.ct_words;
   const uint4* pp = reinterpret_cast<const uint4*>(perm + x0);
-  if constexpr (NEXT) __syncthreads();  // the last NTT's exchange reads of sm are done
+  __syncthreads();  // the last NTT's exchange reads of sm are done
+  if constexpr (!NEXT) {
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();
+      bulk_load(sm, c0, N * 4, &gbar);
+    }
+    mbar_wait(&gbar, 1);
+  }
+  const uint32_t* g0 = NEXT ? c0 : sm;  // NEXT reuses sm for the next digit
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const uint4 pm = __ldg(pp + c);
     uint4 A = a0s[c * T + j], B = a1s[c * T + j];
-    A.x = add_mod(A.x, c0[pm.x], q);
-    A.y = add_mod(A.y, c0[pm.y], q);
-    A.z = add_mod(A.z, c0[pm.z], q);
-    A.w = add_mod(A.w, c0[pm.w], q);
+    A.x = add_mod(A.x, g0[pm.x], q);
+    A.y = add_mod(A.y, g0[pm.y], q);
+    A.z = add_mod(A.z, g0[pm.z], q);
+    A.w = add_mod(A.w, g0[pm.w], q);
     if (fold) {
-      const uint4 u = *reinterpret_cast<const uint4*>(c0 + x0 + 4 * c);
+      const uint4 u = *reinterpret_cast<const uint4*>(g0 + x0 + 4 * c);
       const uint4 v = *reinterpret_cast<const uint4*>(c1 + x0 + 4 * c);
       A.x = add_mod(A.x, u.x, q);
       A.y = add_mod(A.y, u.y, q);

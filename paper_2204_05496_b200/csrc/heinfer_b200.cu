@@ -371,7 +371,6 @@ struct hei_gpu_ctx {
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   int dig_tma = 1;       // HEI_DIG_TMA=0: digit kernel gathers c1 from global memory
   int lat_tma = 0;       // HEI_LAT_TMA=1: latency-path key switch prefetches digits with TMA (measured slower)
-  int ks_tma = 0;        // HEI_KS_TMA=1: key switch prefetches digits with TMA bulk copies (measured 2 % slower)
   uint64_t mt_chunks_max = 128;   // HEI_MT_CHUNKS: parallel mt19937_64 generators per branch
   struct FoldGraph {
     uint64_t pairs;
@@ -588,17 +587,17 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
   if (dig_next) {
     if (big)
       k_rot_keyswitch_s<LG, true, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, perm_next,
-                                                                        dig_next, c->ks_tma, *tabs_of(c, g, 0));
+                                                                        dig_next, *tabs_of(c, g, 0));
     else
       k_rot_keyswitch_s<LG, false, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                         perm_next, dig_next, c->ks_tma, TwNone{});
+                                                                         perm_next, dig_next, TwNone{});
   } else {
     if (big)
       k_rot_keyswitch_s<LG, true, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr,
-                                                                         nullptr, c->ks_tma, *tabs_of(c, g, 0));
+                                                                         nullptr, *tabs_of(c, g, 0));
     else
       k_rot_keyswitch_s<LG, false, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                          nullptr, nullptr, c->ks_tma, TwNone{});
+                                                                          nullptr, nullptr, TwNone{});
   }
 }
 
@@ -1473,7 +1472,6 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_GROUP_KS")) c->group_ks = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
-    if (const char* v = std::getenv("HEI_KS_TMA")) c->ks_tma = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_FOLD_PARTS")) c->fold_parts = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_MASK_GROUP")) c->mask_group = std::max(1, std::atoi(v));
