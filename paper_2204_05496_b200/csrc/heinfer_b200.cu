@@ -1400,9 +1400,11 @@ void encode_inputs_impl(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_
     }
     if (jump) {
       uint32_t errh = 0;
-      CU(cudaMemcpy(&errh, c->d_err, 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpyAsync(&errh, c->d_err, 4, cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
       if (errh) {
-        CU(cudaMemset(c->d_err, 0, 4));
+        CU(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
         *rng0 = init0;
         *rng1 = init1;
         continue;
@@ -1658,8 +1660,10 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (!twc.empty()) {
       CU(cudaMalloc(&c->d_twc, twc.size() * sizeof(uint4)));
       CU(cudaMalloc(&c->d_itwc, itwc.size() * sizeof(uint4)));
-      CU(cudaMemcpy(c->d_twc, twc.data(), twc.size() * sizeof(uint4), cudaMemcpyHostToDevice));
-      CU(cudaMemcpy(c->d_itwc, itwc.data(), itwc.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+      CU(cudaMemcpyAsync(c->d_twc, twc.data(), twc.size() * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      CU(cudaMemcpyAsync(c->d_itwc, itwc.data(), itwc.size() * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
       g.twc = c->d_twc;
       g.itwc = c->d_itwc;
     }
@@ -1668,13 +1672,18 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     CU(cudaMalloc(&c->d_index, n * 4));
     CU(cudaMalloc(&c->d_perms, perms.size() * 4));
     CU(cudaMalloc(&c->d_err, 4));
-    CU(cudaMemcpy(c->d_fwd, fwd.data(), fwd.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(c->d_fwd, fwd.data(), fwd.size() * sizeof(uint2), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     c->h_fwd = fwd;
     c->h_inv = inv;
-    CU(cudaMemcpy(c->d_inv, inv.data(), inv.size() * sizeof(uint2), cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(c->d_index, index_map.data(), n * 4, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(c->d_perms, perms.data(), perms.size() * 4, cudaMemcpyHostToDevice));
-    CU(cudaMemset(c->d_err, 0, 4));
+    CU(cudaMemcpyAsync(c->d_inv, inv.data(), inv.size() * sizeof(uint2), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaMemcpyAsync(c->d_index, index_map.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaMemcpyAsync(c->d_perms, perms.data(), perms.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     g.fwd = c->d_fwd;
     g.inv = c->d_inv;
     g.index_map = c->d_index;
@@ -1839,7 +1848,8 @@ int hei_gpu_upload_galois_keys(hei_gpu_ctx* c, uint32_t b, uint32_t count, const
     const uint64_t words = (uint64_t)count * c->L[b] * 2 * c->L[b] * c->n;
     uint64_t* d_raw = nullptr;
     CU(cudaMalloc(&d_raw, words * 8));
-    CU(cudaMemcpy(d_raw, rows, words * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(d_raw, rows, words * 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     try {
       install_galois_keys(c, b, count, elts, d_raw);
     } catch (...) {
@@ -1881,16 +1891,22 @@ int hei_gpu_debug_rejection_plan(hei_gpu_ctx* c, const uint64_t* raw, uint64_t a
     CU(cudaMalloc(&d_used, 8));
     CU(cudaMalloc(&d32, o32 * 4 + 4));
     CU(cudaMalloc(&d8, o8 + 1));
-    CU(cudaMemcpy(d_segs, segs.data(), nseg * sizeof(KgSeg), cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(d_raw, raw, avail * 8, cudaMemcpyHostToDevice));
-    CU(cudaMemset(c->d_err, 0, 4));
+    CU(cudaMemcpyAsync(d_segs, segs.data(), nseg * sizeof(KgSeg), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaMemcpyAsync(d_raw, raw, avail * 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     k_kg_plan<<<1, 1024, 0, c->stream>>>(d_raw, avail, d_segs, nseg, d32, d8, d_gpos, d_used, c->d_err);
     LAUNCHED();
     CU(cudaStreamSynchronize(c->stream));
     uint32_t err = 0;
-    CU(cudaMemcpy(&err, c->d_err, 4, cudaMemcpyDeviceToHost));
-    CU(cudaMemset(c->d_err, 0, 4));
-    CU(cudaMemcpy(used, d_used, 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(&err, c->d_err, 4, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaMemcpyAsync(used, d_used, 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     if (out32 && o32) CU(cudaMemcpy(out32, d32, o32 * 4, cudaMemcpyDeviceToHost));
     if (out8 && o8) CU(cudaMemcpy(out8, d8, o8, cudaMemcpyDeviceToHost));
     if (gpos) CU(cudaMemcpy(gpos, d_gpos, nseg * 8, cudaMemcpyDeviceToHost));
@@ -1994,7 +2010,8 @@ int hei_gpu_keygen(hei_gpu_ctx* c, hei_gpu_prng* rng, int install, int8_t* sk, u
       CU(cudaMemcpyAsync(&used, d_used, 8, cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
       if (err & 2) {
-        CU(cudaMemset(c->d_err, 0, 4));
+        CU(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
         cudaFree(d_raw);
         raise(HEI_INTERNAL, "keygen: Box-Muller u1 == 0 rejection (probability 2^-53) is not replayed on the device");
       }
@@ -2045,7 +2062,8 @@ int hei_gpu_keygen(hei_gpu_ctx* c, hei_gpu_prng* rng, int install, int8_t* sk, u
         install_galois_keys(c, b, ne, asc.data(), d_gk[b]);
         const size_t words = 2ull * c->L[b] * n;
         if (!c->d_pk[b]) CU(cudaMalloc(&c->d_pk[b], words * 8));
-        CU(cudaMemcpy(c->d_pk[b], d_pk + (b ? 2ull * c->L[0] * n : 0), words * 8, cudaMemcpyDeviceToDevice));
+        CU(cudaMemcpyAsync(c->d_pk[b], d_pk + (b ? 2ull * c->L[0] * n : 0), words * 8, cudaMemcpyDeviceToDevice, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
         if (!c->d_sk_hat) CU(cudaMalloc(&c->d_sk_hat, (size_t)P * n * 4));
         k_prepare_sk<<<c->L[b], c->threads(), sm1, st>>>(c->geo, b, d_out8 + s8[b], c->d_sk_hat);
         LAUNCHED();
@@ -2070,7 +2088,8 @@ int hei_gpu_upload_public_key(hei_gpu_ctx* c, uint32_t b, const uint64_t* pk) {
       cudaFree(c->d_pkp);
       c->d_pkp = nullptr;
     }
-    CU(cudaMemcpy(c->d_pk[b], pk, words * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(c->d_pk[b], pk, words * 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
   });
 }
 
@@ -2083,7 +2102,8 @@ int hei_gpu_upload_secret_key(hei_gpu_ctx* c, uint32_t b, const int8_t* s) {
     if (!c->d_sk_hat) CU(cudaMalloc(&c->d_sk_hat, (size_t)c->P() * c->n * 4));
     int8_t* d_s = nullptr;
     CU(cudaMalloc(&d_s, c->n));
-    CU(cudaMemcpy(d_s, s, c->n, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(d_s, s, c->n, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     k_prepare_sk<<<c->L[b], c->threads(), smem_bytes(c, 1), c->stream>>>(c->geo, b, d_s, c->d_sk_hat);
     LAUNCHED();
     CU(cudaStreamSynchronize(c->stream));
@@ -2143,9 +2163,11 @@ uint32_t* stage_cts(hei_gpu_ctx* c, const uint64_t* cts, int form, uint64_t coun
   CU(cudaFreeAsync(d64, st));
   CU(cudaStreamSynchronize(st));
   uint32_t h = 0;
-  CU(cudaMemcpy(&h, c->d_err, 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpyAsync(&h, c->d_err, 4, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
   if (h) {
-    CU(cudaMemset(c->d_err, 0, 4));
+    CU(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     cudaFree(d32);
     raise(HEI_CODEC_ERROR, "decrypt: coefficient not reduced");
   }
@@ -2213,7 +2235,8 @@ int hei_gpu_weights_create(hei_gpu_ctx* c, const uint64_t* prepared, uint64_t f,
     const uint64_t count = cols * w->kc, words = count * c->pt_words();
     uint64_t* d_raw = nullptr;
     CU(cudaMalloc(&d_raw, words * 8));
-    CU(cudaMemcpy(d_raw, prepared, words * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(d_raw, prepared, words * 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     k_prepare_plain<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, d_raw, count, w->d_w, c->d_err);
     LAUNCHED();
     CU(cudaStreamSynchronize(c->stream));
@@ -2232,7 +2255,8 @@ int hei_gpu_weights_encode(hei_gpu_ctx* c, const int64_t* wm, uint64_t f, uint64
     std::unique_ptr<hei_gpu_weights> w(weights_alloc(c, f, cols));
     int64_t* d_w = nullptr;
     CU(cudaMalloc(&d_w, f * cols * 8));
-    CU(cudaMemcpy(d_w, wm, f * cols * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(d_w, wm, f * cols * 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     k_encode_weights<<<(unsigned)(cols * w->kc * c->P()), c->threads(), smem_bytes(c, 1), c->stream>>>(
         c->geo, d_w, f, (uint32_t)cols, (uint32_t)w->kc, w->d_w);
     LAUNCHED();
@@ -2372,9 +2396,11 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
   }
   {
     uint32_t h = 0;
-    CU(cudaMemcpy(&h, c->d_err, 4, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(&h, c->d_err, 4, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     if (h) {
-      CU(cudaMemset(c->d_err, 0, 4));
+      CU(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
       raise(HEI_CODEC_ERROR, (h & 2) ? "unexpected polynomial form" : "coefficient not reduced");
     }
   }
@@ -2526,7 +2552,8 @@ int hei_gpu_ntt(hei_gpu_ctx* c, uint32_t b, uint32_t prime, uint64_t* polys, uin
     }
     uint32_t* d = nullptr;
     CU(cudaMalloc(&d, words * 4));
-    CU(cudaMemcpy(d, h32.data(), words * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(d, h32.data(), words * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     launch_poly_ntt(c, (unsigned)count, gp, d, inverse, c->stream);
     CU(cudaMemcpyAsync(h32.data(), d, words * 4, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
@@ -2574,7 +2601,8 @@ int hei_gpu_apply_galois(hei_gpu_ctx* c, uint32_t b, uint64_t elt, const uint64_
     CU(cudaMalloc(&d_in, words * 4));
     CU(cudaMalloc(&d_out, words * 4));
     CU(cudaMalloc(&d_dig, (size_t)L * n * 4));
-    CU(cudaMemcpy(d_in, h32.data(), words * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(d_in, h32.data(), words * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     const uint32_t* perm = c->d_perms + (size_t)c->perm_index.at(elt) * n;
     const uint2* key = c->d_keys[b] + (size_t)c->key_index[b].at(elt) * L * 2 * L * n;
     launch_rot_digits(c, gb, L, d_in, perm, d_dig, c->stream);
@@ -2597,7 +2625,8 @@ int hei_gpu_sum_all_slots(hei_gpu_ctx* c, const uint64_t* in, uint64_t* out, uin
     ensure_scratch(c, count);
     uint64_t* d64 = nullptr;
     CU(cudaMalloc(&d64, words * 8));
-    CU(cudaMemcpy(d64, in, words * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(d64, in, words * 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     k_narrow<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, d64, c->d_dotA, count, c->d_err);
     LAUNCHED();
     check_err_flag(c, HEI_CODEC_ERROR, "sum_all_slots: coefficient not reduced");
@@ -2806,9 +2835,11 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     }
     if (jump) {
       uint32_t errh = 0;
-      CU(cudaMemcpy(&errh, c->d_err, 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpyAsync(&errh, c->d_err, 4, cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
       if (errh) {  // a rejection misaligned the chunks: replay sequentially
-        CU(cudaMemset(c->d_err, 0, 4));
+        CU(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
         *rng0 = init0;
         *rng1 = init1;
         continue;
