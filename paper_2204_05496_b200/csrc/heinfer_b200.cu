@@ -184,6 +184,7 @@ int max_q_bits_128(uint32_t n) {
 // ------------------------------------------------------------ device structs
 constexpr int kMaxPrimes = 16;
 constexpr int kMaxElts = 16;
+constexpr uint32_t kMaxFoldParts = 8;
 
 struct PrimeInfo {
   uint32_t q;
@@ -369,6 +370,8 @@ struct hei_gpu_ctx {
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
+  bool e2e_overlap = true;  // HEI_E2E_OVERLAP=0: host-buffer chunks run one after another
+  std::vector<cudaStream_t> chunk_streams;  // 2 x fold_parts streams: consecutive chunks overlap
   int dig_tma = 1;       // HEI_DIG_TMA=0: digit kernel gathers c1 from global memory
   int lat_tma = 0;       // HEI_LAT_TMA=1: latency-path key switch prefetches digits with TMA (measured slower)
   uint64_t mt_chunks_max = 128;   // HEI_MT_CHUNKS: parallel mt19937_64 generators per branch
@@ -806,17 +809,31 @@ void run_folded_dots(hei_gpu_stream* s, const uint64_t* d_rows, uint64_t nrows, 
   launch_mask_acc(c, c->geo, (unsigned)(pairs * c->P()), res, d_rows, cols, s->d_acc, st);
 }
 
+// Slice placement for a chunk that runs concurrently with its neighbours
+// (host-buffer matmul): the chunk's slices go to `streams` (not the caller's
+// stream), use the scratch region starting at pair `pair_off`, and the chunk
+// ends by recording `done` on streams[0] instead of joining the caller.
+struct ChunkSlot {
+  cudaStream_t streams[kMaxFoldParts];
+  uint64_t pair_off;
+  cudaEvent_t done;
+};
+
 // Core: process staged rows (device u32, eval form) into the packed u64 sums.
-void run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, uint64_t nrows, cudaStream_t st) {
+// Returns false when `cs` was given but the chunk is too small for slices (the
+// caller then runs it serialised on `st`).
+bool run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, uint64_t nrows, cudaStream_t st,
+              const ChunkSlot* cs = nullptr) {
   hei_gpu_ctx* c = s->ctx;
   const hei_gpu_weights* w = s->w;
   const Geo& g = c->geo;
   const uint32_t cols = (uint32_t)w->cols;
   const uint64_t pairs = nrows * cols;
-  ensure_scratch(c, pairs);
+  if (!cs) ensure_scratch(c, pairs);
   const unsigned T = c->threads();
   const unsigned blocksP = (unsigned)(pairs * c->P());
   const uint32_t parts = std::min<uint64_t>(c->fold_parts, nrows / 4);
+  if (cs && !(c->two_streams && !c->timing && parts >= 2)) return false;
   if (c->two_streams && !c->timing && parts >= 2) {
     // the batch in `parts` slices on as many streams: one slice's digit INTTs
     // and key switches interleave with the others', filling each launch's tail
@@ -829,10 +846,13 @@ void run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
     CU(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     CU(cudaEventRecord(fork, st));
     std::vector<cudaEvent_t> joins;
+    const uint64_t base = cs ? cs->pair_off : 0;
+    cudaStream_t head = cs ? cs->streams[0] : st;
     for (uint32_t h = 0; h < parts; ++h) {
-      cudaStream_t hs = h ? c->part_streams[h - 1] : st;
-      if (h) CU(cudaStreamWaitEvent(hs, fork, 0));
-      const uint64_t rr0 = nrows * h / parts, nr = nrows * (h + 1) / parts - rr0, pp = nr * cols, off = rr0 * cols;
+      cudaStream_t hs = cs ? cs->streams[h] : (h ? c->part_streams[h - 1] : st);
+      if (h || cs) CU(cudaStreamWaitEvent(hs, fork, 0));
+      const uint64_t rr0 = nrows * h / parts, nr = nrows * (h + 1) / parts - rr0, pp = nr * cols,
+                     off = base + rr0 * cols;
       uint32_t* A = c->d_dotA + off * c->ct_words();
       uint32_t* B = c->d_dotB + off * c->ct_words();
       uint32_t* D = c->d_dig + off * c->pt_words();
@@ -849,11 +869,12 @@ void run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
       }
     }
     for (cudaEvent_t j : joins) {
-      CU(cudaStreamWaitEvent(st, j, 0));
+      CU(cudaStreamWaitEvent(head, j, 0));
       cudaEventDestroy(j);
     }
+    if (cs) CU(cudaEventRecord(cs->done, head));
     cudaEventDestroy(fork);
-    return;
+    return true;
   }
   // latency path: the mask plaintexts are computed on a side stream while
   // the fold runs (they depend only on the slot)
@@ -888,6 +909,7 @@ void run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
   } else {
     launch_mask_acc(c, g, blocksP, res, d_rows, cols, s->d_acc, st);
   }
+  return true;
 }
 
 void stream_flush(hei_gpu_stream* s) {
@@ -1475,7 +1497,9 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
-    if (const char* v = std::getenv("HEI_FOLD_PARTS")) c->fold_parts = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("HEI_FOLD_PARTS"))
+      c->fold_parts = std::min<uint32_t>(kMaxFoldParts, std::max(1, std::atoi(v)));
+    if (const char* v = std::getenv("HEI_E2E_OVERLAP")) c->e2e_overlap = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_GROUP")) c->mask_group = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_DIG_TMA")) c->dig_tma = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_LAT_TMA")) c->lat_tma = std::atoi(v) != 0;
@@ -1742,6 +1766,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   if (c->bias_stream) cudaStreamDestroy(c->bias_stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (cudaStream_t ps : c->part_streams) cudaStreamDestroy(ps);
+  for (cudaStream_t ps : c->chunk_streams) cudaStreamDestroy(ps);
   cudaFree(c->d_dotA);
   cudaFree(c->d_dotB);
   cudaFree(c->d_dig);
@@ -2362,6 +2387,26 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
     CU(cudaEventCreateWithFlags(&narrowed[k], cudaEventDisableTiming));
     CU(cudaEventRecord(narrowed[k], st));
   }
+  // Consecutive chunks run concurrently on two stream sets, each with its own
+  // input slot and scratch region, so one chunk's launches fill the tails of
+  // the other's (packed sums are exact integer atomics: order-free).
+  const uint32_t fp = c->fold_parts;
+  const bool overlap = c->e2e_overlap && c->two_streams && !c->timing && fp >= 2;
+  ChunkSlot cslot[2] = {};
+  if (overlap) {
+    while (c->chunk_streams.size() < 2 * fp) {
+      cudaStream_t ps;
+      CU(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
+      c->chunk_streams.push_back(ps);
+    }
+    ensure_scratch(c, 2 * slot_rows * w->cols);
+    for (int k = 0; k < 2; ++k) {
+      for (uint32_t h = 0; h < fp; ++h) cslot[k].streams[h] = c->chunk_streams[k * fp + h];
+      cslot[k].pair_off = (uint64_t)k * slot_rows * w->cols;
+      CU(cudaEventCreateWithFlags(&cslot[k].done, cudaEventDisableTiming));
+      CU(cudaEventRecord(cslot[k].done, st));
+    }
+  }
   const uint8_t* src = wire ? io.wire : reinterpret_cast<const uint8_t*>(io.u64);
   // chunk sizes ramp up (chunk/8, chunk/4, ..., chunk) so the first copy,
   // the only one not hidden behind compute, is short; a tail smaller than
@@ -2378,6 +2423,7 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
     CU(cudaMemcpyAsync(sb, src + r0 * row_bytes, nr * row_bytes, cudaMemcpyHostToDevice, cs));
     CU(cudaEventRecord(copied[slot], cs));
     CU(cudaStreamWaitEvent(st, copied[slot], 0));
+    if (overlap) CU(cudaStreamWaitEvent(st, cslot[slot].done, 0));  // slot and scratch of chunk b-2 released
     if (wire)
       k_wire_parse<<<grid_for(nr * words, 256), 256, 0, st>>>(c->geo, io.wg, sb, s32, nr * w->kc, c->d_err);
     else
@@ -2386,13 +2432,21 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
     LAUNCHED();
     CU(cudaEventRecord(narrowed[slot], st));
     if (wire || io.form == HEI_FORM_COEFF) launch_ct_ntt(c, (unsigned)(nr * w->kc * 2 * c->P()), s32, st);
-    run_rows(s.get(), s32, d_rows + r0, nr, st);
+    if (!overlap || !run_rows(s.get(), s32, d_rows + r0, nr, st, &cslot[slot])) {
+      // serialised chunk (too small for slices): scratch from offset 0
+      if (overlap) CU(cudaStreamWaitEvent(st, cslot[1 - slot].done, 0));
+      run_rows(s.get(), s32, d_rows + r0, nr, st);
+      if (overlap) CU(cudaEventRecord(cslot[slot].done, st));
+    }
     r0 += nr;
   }
+  if (overlap)
+    for (int k = 0; k < 2; ++k) CU(cudaStreamWaitEvent(st, cslot[k].done, 0));
   CU(cudaStreamSynchronize(st));
   for (int k = 0; k < 2; ++k) {
     cudaEventDestroy(copied[k]);
     cudaEventDestroy(narrowed[k]);
+    if (cslot[k].done) cudaEventDestroy(cslot[k].done);
   }
   {
     uint32_t h = 0;
