@@ -262,6 +262,7 @@ __device__ __forceinline__ uint32_t poly_prime(const Geo& g, uint32_t poly) {
 #include "wire.cuh"
 
 #include "fold_kernels.cuh"
+#include "tmem_ks.cuh"
 
 #include "stdalg_kernels.cuh"
 
@@ -370,6 +371,7 @@ struct hei_gpu_ctx {
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
+  int ks_tmem = 4;  // HEI_KS_TMEM: full-batch key switch accumulates in TMEM (0 off; 2, 3 CTAs/SM; 4: 3 CTAs/SM, 4-slot rounds)
   bool e2e_overlap = true;  // HEI_E2E_OVERLAP=0: host-buffer chunks run one after another
   std::vector<cudaStream_t> chunk_streams;  // 2 x fold_parts streams: consecutive chunks overlap
   int dig_tma = 1;       // HEI_DIG_TMA=0: digit kernel gathers c1 from global memory
@@ -595,6 +597,21 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
       k_rot_keyswitch_s<LG, false, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
                                                                          perm_next, dig_next, TwNone{});
   } else {
+    if constexpr (LG == 13) {
+      if (big && c->ks_tmem) {  // accumulators in tensor memory
+        const size_t smt = smem_bytes(c, 1);
+        if (c->ks_tmem == 3)
+          k_rot_keyswitch_t<LG, true, 3><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                          *tabs_of(c, g, 0));
+        else if (c->ks_tmem == 4)  // 3 CTAs/SM, 4-slot TMEM rounds
+          k_rot_keyswitch_t<LG, true, 3, 4><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                             *tabs_of(c, g, 0));
+        else
+          k_rot_keyswitch_t<LG, true, 2><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                          *tabs_of(c, g, 0));
+        return;
+      }
+    }
     if (big)
       k_rot_keyswitch_s<LG, true, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr,
                                                                          nullptr, *tabs_of(c, g, 0));
@@ -1499,6 +1516,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_FOLD_PARTS"))
       c->fold_parts = std::min<uint32_t>(kMaxFoldParts, std::max(1, std::atoi(v)));
+    if (const char* v = std::getenv("HEI_KS_TMEM")) c->ks_tmem = std::atoi(v);
     if (const char* v = std::getenv("HEI_E2E_OVERLAP")) c->e2e_overlap = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_GROUP")) c->mask_group = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_DIG_TMA")) c->dig_tma = std::atoi(v) != 0;
