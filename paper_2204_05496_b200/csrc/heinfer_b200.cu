@@ -372,6 +372,7 @@ struct hei_gpu_ctx {
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   int ks_tmem = 4;  // HEI_KS_TMEM: full-batch key switch accumulates in TMEM (0 off; 2, 3 CTAs/SM; 4: 3 CTAs/SM, 4-slot rounds)
+  bool fuse_big = false;   // HEI_FUSE_BIG=1: full batches also fuse the next digit INTT into the TMEM key switch
   bool e2e_overlap = true;  // HEI_E2E_OVERLAP=0: host-buffer chunks run one after another
   std::vector<cudaStream_t> chunk_streams;  // 2 x fold_parts streams: consecutive chunks overlap
   int dig_tma = 1;       // HEI_DIG_TMA=0: digit kernel gathers c1 from global memory
@@ -590,6 +591,13 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
     return;
   }
   if (dig_next) {
+    if constexpr (LG == 13) {
+      if (big && c->ks_tmem) {  // TMEM accumulators + the next rotation's digit
+        k_rot_keyswitch_t<LG, true, 3, 4, true><<<blocks, Ntt<LG>::T, smem_bytes(c, 2), st>>>(
+            g, cur, dig, perm, k0, k1, out, fold, perm_next, dig_next, *tabs_of(c, g, 0));
+        return;
+      }
+    }
     if (big)
       k_rot_keyswitch_s<LG, true, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, perm_next,
                                                                         dig_next, *tabs_of(c, g, 0));
@@ -601,14 +609,14 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
       if (big && c->ks_tmem) {  // accumulators in tensor memory
         const size_t smt = smem_bytes(c, 1);
         if (c->ks_tmem == 3)
-          k_rot_keyswitch_t<LG, true, 3><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                          *tabs_of(c, g, 0));
+          k_rot_keyswitch_t<LG, true, 3><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr,
+                                                                          nullptr, *tabs_of(c, g, 0));
         else if (c->ks_tmem == 4)  // 3 CTAs/SM, 4-slot TMEM rounds
           k_rot_keyswitch_t<LG, true, 3, 4><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                             *tabs_of(c, g, 0));
+                                                                             nullptr, nullptr, *tabs_of(c, g, 0));
         else
-          k_rot_keyswitch_t<LG, true, 2><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                          *tabs_of(c, g, 0));
+          k_rot_keyswitch_t<LG, true, 2><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr,
+                                                                          nullptr, *tabs_of(c, g, 0));
         return;
       }
     }
@@ -688,6 +696,7 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, false>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, false>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
+  if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, true>, 2 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, true>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_c2<LG, true>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_c2<LG, false>, 3 * sm);
@@ -731,7 +740,7 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
     const uint32_t* perm = c->d_perms + (size_t)c->perm_index.at(elt) * c->n;
     // fused digits pay off when launches are too small to fill the GPU
     // (latency path); large batches keep the separate 3-CTA/SM digit kernel
-    const bool fuse = c->fuse_digits && blocks < 4u * 148u;
+    const bool fuse = c->fuse_digits && (blocks < 4u * 148u || (c->fuse_big && c->ks_tmem && c->logn == 13));
     const uint32_t* perm_next =
         (k + 1 < S && fuse) ? c->d_perms + (size_t)c->perm_index.at(c->fold_elts[k + 1]) * c->n : nullptr;
     const uint2* k0 = c->d_keys[0] + (size_t)c->key_index[0].at(elt) * c->L[0] * 2 * c->L[0] * c->n;
@@ -1517,6 +1526,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_FOLD_PARTS"))
       c->fold_parts = std::min<uint32_t>(kMaxFoldParts, std::max(1, std::atoi(v)));
     if (const char* v = std::getenv("HEI_KS_TMEM")) c->ks_tmem = std::atoi(v);
+    if (const char* v = std::getenv("HEI_FUSE_BIG")) c->fuse_big = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_OVERLAP")) c->e2e_overlap = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_GROUP")) c->mask_group = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_DIG_TMA")) c->dig_tma = std::atoi(v) != 0;

@@ -60,13 +60,18 @@ __device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::
 constexpr uint32_t kTmemCols = 128;
 
 // GS: accumulator slots per TMEM load/store round (8 or 4).
-template <int LOGN, bool PTW, int MINB, int GS = 8>
+// NEXT: also produce the next rotation's digit for prime i (as
+// k_rot_keyswitch_s<.., NEXT>): the new c1 lands in a second shared buffer,
+// is permuted by the next Galois element and inverse-transformed here.
+template <int LOGN, bool PTW, int MINB, int GS = 8, bool NEXT = false>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, const uint32_t* __restrict__ dot,
                                                                       const uint32_t* __restrict__ digits,
                                                                       const uint32_t* __restrict__ perm,
                                                                       const uint2* __restrict__ key0,
                                                                       const uint2* __restrict__ key1,
                                                                       uint32_t* __restrict__ out, int fold,
+                                                                      const uint32_t* __restrict__ perm_next,
+                                                                      uint32_t* __restrict__ dig_next,
                                                                       const __grid_constant__ TwArg<PTW> tab) {
   using NT = Ntt<LOGN>;
   static_assert(NT::T == 512, "TMEM layout assumes 16 warps (4 per lane quarter)");
@@ -211,7 +216,20 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
       }
       *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly0 * N + x0 + 4 * c) = make_uint4(A[k], A[k + 1], A[k + 2], A[k + 3]);
       *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly1 * N + x0 + 4 * c) = make_uint4(B[k], B[k + 1], B[k + 2], B[k + 3]);
+      if constexpr (NEXT) *reinterpret_cast<uint4*>(sm + N + x0 + 4 * c) = make_uint4(B[k], B[k + 1], B[k + 2], B[k + 3]);
     }
+  }
+  if constexpr (NEXT) {
+    // digit_i of the next rotation: INTT_i(sigma'(c1'_i)) (context.cpp:445-470)
+    __syncthreads();
+    uint32_t pm[16];
+    load16_ro(perm_next + x0, pm);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = sm[N + pm[r]];
+    NT::inv(e, sm, g.inv + (size_t)gp * N, g.itwc + (size_t)gp * g.twc_stride, q, pr.last, pr.ninv);
+    uint32_t* d = dig_next + ((uint64_t)pair * g.P + gp) * N;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) d[NT::posA(j, r)] = e[r];
   }
   tm_fence_before();
   __syncthreads();

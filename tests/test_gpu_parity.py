@@ -841,17 +841,18 @@ def test_full_batch_key_switch_variants_bit_exact(prod, monkeypatch):
     """sum_all_slots (backend.cpp:63-73) over 64 ciphertexts: 640 (pair, prime)
     blocks take the full-batch key switch (not the fused latency kernels).
     The TMEM-accumulator kernel at 3 and 2 CTAs/SM and the shared-memory
-    kernel give identical ciphertexts, equal to the oracle's."""
+    kernel give identical ciphertexts, equal to the oracle's; so does the TMEM
+    kernel that also produces the next rotation's digits (HEI_FUSE_BIG=1)."""
     o, _ = prod
     rng = np.random.default_rng(64)
     x = rng.integers(-9, 9, size=(64, o.n), dtype=np.int64)
     cts = o.encode_inputs(x)[:, 0, :]
     got = {}
-    for v in ("4", "3", "2", "0"):
-        monkeypatch.setenv("HEI_KS_TMEM", v)
+    for v in ("4", "3", "2", "0", "4f"):
+        monkeypatch.setenv("HEI_KS_TMEM", v[0])
+        monkeypatch.setenv("HEI_FUSE_BIG", "1" if v.endswith("f") else "0")
         got[v] = gpu_server_from(o).sum_all_slots(cts)
-    assert np.array_equal(got["3"], got["0"])
-    assert np.array_equal(got["2"], got["0"])
-    assert np.array_equal(got["4"], got["0"])
+    for v in ("4", "3", "2", "4f"):
+        assert np.array_equal(got[v], got["0"]), v
     for r in (0, 37, 63):
         assert np.array_equal(got["3"][r], o.sum_all_slots(cts[r])), r
