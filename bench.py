@@ -114,6 +114,10 @@ class Clocks:
             self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the sampler is live (first line read) before the timed region starts
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 3.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -438,7 +442,15 @@ def run_ours(args, world, rank, local):
         except Exception:
             pass
         ach = tot_bytes / (ks_ms / 1000.0) / 1e9
-        roof = {"kernel": "k_rot_keyswitch_s<13> (fold key switch)", "bound": "hbm", "achieved": ach, "peak": hbm,
+        logn = n.bit_length() - 1
+        blocks = R / batches * cols * (L0 + L1)  # (pair, prime) blocks per timed key-switch launch
+        if blocks <= 148:
+            ks_name = f"k_rot_keyswitch_w2<{logn}> (latency path: 2-group CTA, fused next digit)"
+        elif blocks < 296 or logn != 13 or os.environ.get("HEI_KS_TMEM", "4") == "0":
+            ks_name = f"k_rot_keyswitch_s<{logn}> (shared-memory accumulators)"
+        else:
+            ks_name = "k_rot_keyswitch_t<13> (TMEM accumulators, 3 CTAs/SM)"
+        roof = {"kernel": ks_name, "bound": "hbm", "achieved": ach, "peak": hbm,
                 "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
                 "algorithmic_bytes_per_launch": tot_bytes / ks_n, "avg_launch_ms": avg_s * 1e3, "launches": ks_n,
                 "batches": batches, "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
@@ -446,7 +458,7 @@ def run_ours(args, world, rank, local):
         bfly_pair = sum(((Lb - 1) * (n // 2) * S + 2 * Lb * n) for Lb in (L0, L1) for _ in range(Lb))
         tot_bfly = S * R * cols * bfly_pair
         peak_b = native.butterfly_peak(local)
-        int_roof = {"kernel": "k_rot_keyswitch_s<13>", "bound": "int32 pipes (CT butterfly = Shoup mulmod + add + sub)",
+        int_roof = {"kernel": ks_name, "bound": "int32 pipes (CT butterfly = Shoup mulmod + add + sub)",
                     "achieved": tot_bfly / (ks_ms / 1000.0) / 1e9, "peak": peak_b / 1e9, "unit": "Gbutterfly/s",
                     "frac": tot_bfly / (ks_ms / 1000.0) / peak_b,
                     "peak_source": "k_bfly_peak register microbenchmark, this run",

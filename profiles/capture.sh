@@ -12,7 +12,7 @@ CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-baseli
 $CMD > gpurun_out/plain.json 2>/dev/null || exit 2
 HEI_PROFILE_STEPS=1 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${TAG}_c4.csv $CMD > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_rot_keyswitch_s|k_rot_digits_f" -s 60 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:"k_rot_keyswitch_[st]|k_rot_digits_f" -s 60 -c 2 \
     -o gpurun_out/full_${TAG}_c4 $CMD > gpurun_out/ncu_full.log 2>&1
 python profiles/probes/latency_probe2.py > /dev/null 2>&1 || exit 3
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_latency.csv \
