@@ -352,6 +352,8 @@ struct hei_gpu_ctx {
   cudaStream_t copy_stream = nullptr;
   int64_t* pinned_bias = nullptr;  // pinned staging for the bias upload
   size_t pinned_bias_bytes = 0;
+  void* pinned_out = nullptr;  // pinned staging for result downloads to pageable memory
+  size_t pinned_out_bytes = 0;
   uint32_t* pool_part = nullptr;  // split key-switch partials (small batches)
   size_t pool_part_bytes = 0;
   bool split = false;   // HEI_SPLIT=1: split the key switch over digits for small batches
@@ -1785,6 +1787,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->pool_stage64);
   cudaFree(c->pool_part);
   if (c->pinned_bias) cudaFreeHost(c->pinned_bias);
+  if (c->pinned_out) cudaFreeHost(c->pinned_out);
   cudaFree(c->pool_in32);
   cudaFree(c->pool_out);
   cudaFree(c->pool_out64);
@@ -2382,6 +2385,29 @@ void check_hect_header(const uint8_t* h, uint64_t hash) {
   if (parts != 2) raise(HEI_CODEC_ERROR, "ciphertext must have two parts");
 }
 
+// Result download ending in a stream sync. A pageable destination goes
+// through a grow-only pinned staging buffer (one DMA at full PCIe rate, then
+// a host copy) instead of the driver's chunked pageable path.
+void d2h_result(hei_gpu_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  cudaPointerAttributes a{};
+  const bool pinned = cudaPointerGetAttributes(&a, dst) == cudaSuccess && a.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // clear a lookup failure on plain host memory
+  if (pinned || bytes > ((size_t)256 << 20)) {
+    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return;
+  }
+  if (bytes > c->pinned_out_bytes) {
+    if (c->pinned_out) cudaFreeHost(c->pinned_out);
+    c->pinned_out = nullptr;
+    CU(cudaMallocHost(&c->pinned_out, bytes));
+    c->pinned_out_bytes = bytes;
+  }
+  CU(cudaMemcpyAsync(c->pinned_out, src, bytes, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  std::memcpy(dst, c->pinned_out, bytes);
+}
+
 void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uint64_t rows, const int64_t* bias,
                  hei_op_counters* cnt) {
   set_device(c);
@@ -2498,13 +2524,12 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
     uint8_t* d_bytes = reinterpret_cast<uint8_t*>(d_out64);
     k_wire_emit<<<grid_for(outw, 256), 256, 0, st>>>(c->geo, io.wg, d_out, d_bytes, s->C);
     LAUNCHED();
-    CU(cudaMemcpyAsync(io.out_wire, d_bytes, out_bytes, cudaMemcpyDeviceToHost, st));
+    d2h_result(c, io.out_wire, d_bytes, out_bytes, st);
   } else {
     k_widen<<<grid_for(outw, 256), 256, 0, st>>>(d_out, d_out64, outw);
     LAUNCHED();
-    CU(cudaMemcpyAsync(io.out64, d_out64, outw * 8, cudaMemcpyDeviceToHost, st));
+    d2h_result(c, io.out64, d_out64, outw * 8, st);
   }
-  CU(cudaStreamSynchronize(st));
   s->finished = true;
   if (cnt) hei_proposed_counts(rows, w->cols, w->f, c->n, cnt);
 }

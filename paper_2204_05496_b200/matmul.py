@@ -294,7 +294,7 @@ def matmul(server: GpuTwinServer, inputs: np.ndarray, w: EncodedWeights, bias, f
     if bias.size != w.cols:
         raise ParamError("matmul: bias length does not match output count")
     C_ = (R * w.cols + server.n - 1) // server.n
-    out = np.zeros((C_, server.ct_words), dtype=np.uint64)
+    out = np.empty((C_, server.ct_words), dtype=np.uint64)  # every word is written
     cnt = OpCounters()
     check(native.lib().hei_gpu_matmul(server.handle, w._h, u64p(inputs), C.c_int(form), C.c_uint64(R), i64p(bias), u64p(out), C.byref(cnt)))
     return out, cnt
