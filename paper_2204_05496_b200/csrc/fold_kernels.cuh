@@ -308,7 +308,7 @@ __global__ void k_prepare_plain(Geo g, const uint64_t* __restrict__ vals, uint64
 // Galois keys of one branch: host [e][l][part][i][n] u64 -> device
 // [e][i][l][part][n] (val, shoup), the order k_rot_keyswitch streams them.
 __global__ void k_prepare_keys(Geo g, uint32_t b, uint32_t elts, const uint64_t* __restrict__ rows,
-                               uint2* __restrict__ out, uint32_t* err) {
+                               uint2* __restrict__ out, uint32_t* err, uint32_t V) {
   const uint32_t n = g.n, L = g.L[b], first = b ? g.L[0] : 0;
   const uint64_t total = (uint64_t)elts * L * 2 * L * n;
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
@@ -325,12 +325,12 @@ __global__ void k_prepare_keys(Geo g, uint32_t b, uint32_t elts, const uint64_t*
     const uint32_t q = g.pr[first + i].q;
     const uint64_t v = rows[x];
     if (v >= q) *err = 1;
-    // fast path (n >= 4096): pass-C transposed layout, slot x = 16 j + 2 c' + h
-    // stored at uint2 index (c' * (n / 16) + j) * 2 + h
+    // fast path (n >= 4096): pass-C transposed layout for V slots per thread,
+    // slot x = V j + 2 c' + h stored at uint2 index (c' * (n / V) + j) * 2 + h
     uint32_t cpos = c;
     if (n >= 4096) {
-      const uint32_t jj = c >> 4, rr = c & 15;
-      cpos = ((rr >> 1) * (n >> 4) + jj) * 2 + (rr & 1);
+      const uint32_t jj = c / V, rr = c % V;
+      cpos = ((rr >> 1) * (n / V) + jj) * 2 + (rr & 1);
     }
     const uint64_t dst = ((((e * L + i) * L + l) * 2 + part) * n) + cpos;
     out[dst] = make_uint2((uint32_t)v, (uint32_t)((v << 32) / q));

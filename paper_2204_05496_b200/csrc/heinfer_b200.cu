@@ -56,6 +56,7 @@
 #include "../../include/heinfer_b200.h"
 #include "modmath.cuh"
 #include "ntt_fast.cuh"
+#include "ntt32.cuh"
 #include "bulk_copy.cuh"
 #include "baseline.cuh"
 
@@ -214,6 +215,9 @@ struct Geo {
   const uint4* twc;  // pass-C twiddles, fast path only: [P + 2][KC][T]
   const uint4* itwc;
   uint32_t twc_stride;  // KC * T (uint4 per modulus)
+  const uint4* twc32;   // pass-C twiddles of the 32-residue NTT (ntt32.cuh): [P + 2][KC32][N/32]
+  const uint4* itwc32;
+  uint32_t twc32_stride;
   const uint32_t* index_map;
 };
 
@@ -263,6 +267,7 @@ __device__ __forceinline__ uint32_t poly_prime(const Geo& g, uint32_t poly) {
 
 #include "fold_kernels.cuh"
 #include "tmem_ks.cuh"
+#include "ks32.cuh"
 
 #include "stdalg_kernels.cuh"
 
@@ -308,6 +313,7 @@ struct hei_gpu_ctx {
   uint2 *d_fwd = nullptr, *d_inv = nullptr;
   std::vector<uint2> h_fwd, h_inv;  // host copies (pass-A/B rows go in kernel params)
   uint4 *d_twc = nullptr, *d_itwc = nullptr;
+  uint4 *d_twc32 = nullptr, *d_itwc32 = nullptr;
   uint32_t* d_index = nullptr;
   // galois elements in fold order: steps 1, 2, ..., n/4, then the swap
   std::vector<uint64_t> fold_elts;
@@ -326,6 +332,9 @@ struct hei_gpu_ctx {
   cudaStream_t stream = nullptr;
   uint64_t batch_pairs = 0;
   bool ks14_regs = false;  // N = 16384: register-accumulator key switch (HEI_KS14_REGS=1)
+  int ntt32 = 0;           // HEI_NTT32: 32-residue transforms (ntt32.cuh); 1 = N 16384 fold, 2 = also N 8192 full batches
+  uint2* d_keys32[2] = {nullptr, nullptr};  // Galois keys in the 32-slot-per-thread layout (ntt32 only)
+  uint64_t keys_words[2] = {0, 0};
   // scratch (grown on demand)
   uint32_t *d_dotA = nullptr, *d_dotB = nullptr, *d_dig = nullptr, *d_dig2 = nullptr;
   bool fuse_digits = true;  // HEI_FUSE_DIGITS=0: separate digit kernel every rotation (small batches)
@@ -531,12 +540,39 @@ const TwAB* tabs_of(hei_gpu_ctx* c, const Geo& g, int inverse) {
   return &t;
 }
 
+// The 32-residue transforms (ntt32.cuh) serve every N = 16384 fold when
+// HEI_NTT32 >= 1 and N = 8192 full batches when HEI_NTT32 = 2.
+bool use_ntt32(hei_gpu_ctx* c, unsigned blocks) {
+  if (c->logn == 14) return c->ntt32 >= 1;
+  if (c->logn == 13) return c->ntt32 >= 2 && blocks >= 4u * 148u;
+  return false;
+}
+const uint2* keys32_of(hei_gpu_ctx* c, const uint2* k) {
+  for (int b = 0; b < 2; ++b)
+    if (c->d_keys[b] && k >= c->d_keys[b] && k < c->d_keys[b] + c->keys_words[b]) {
+      if (!c->d_keys32[b]) raise(HEI_INTERNAL, "32-slot key layout not prepared (HEI_NTT32 set after key upload)");
+      return c->d_keys32[b] + (k - c->d_keys[b]);
+    }
+  raise(HEI_INTERNAL, "key pointer outside the uploaded key sets");
+}
+
 void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* perm,
                        uint32_t* dig, cudaStream_t st) {
   const size_t sm = smem_bytes(c, 1), smf = smem_bytes(c, c->dig_tma ? 2 : 1);
   // big launches take the pass-A/B twiddles as parameters (constant bank);
   // small ones keep the 25 KB parameter block off the launch path
   const bool ptw = blocks >= 2u * 148u;
+  if (use_ntt32(c, blocks)) {
+    if (c->logn == 14) {
+      if (ptw) k_rot_digits32<14, true><<<blocks, Ntt32<14>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1));
+      else k_rot_digits32<14, false><<<blocks, Ntt32<14>::T, sm, st>>>(g, cur, perm, dig, TwNone{});
+    } else {
+      if (ptw) k_rot_digits32<13, true><<<blocks, Ntt32<13>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1));
+      else k_rot_digits32<13, false><<<blocks, Ntt32<13>::T, sm, st>>>(g, cur, perm, dig, TwNone{});
+    }
+    LAUNCHED();
+    return;
+  }
   HEI_DISPATCH(c->logn,
                (ptw ? k_rot_digits_f<LG, true><<<blocks, Ntt<LG>::T, smf, st>>>(g, cur, perm, dig, c->dig_tma,
                                                                                 *tabs_of(c, g, 1))
@@ -638,6 +674,26 @@ bool launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const u
                           cudaStream_t st, const uint32_t* perm_next = nullptr, uint32_t* dig_next = nullptr) {
   // N <= 8192: shared-memory accumulators, 2 CTAs/SM; N = 16384 (1024
   // threads) keeps the accumulators in registers when HEI_KS14_REGS=1.
+  if (use_ntt32(c, blocks) && (c->logn == 14 || !dig_next)) {
+    // 32-residue transforms, TMEM accumulators; never fused with the next digit
+    const uint2* q0 = keys32_of(c, k0);
+    const uint2* q1 = keys32_of(c, k1);
+    const size_t smt = smem_bytes(c, 1);
+    const bool ptw = blocks >= 2u * 148u;
+    if (c->logn == 14) {
+      if (ptw)
+        k_rot_keyswitch_t32<14, true, 2><<<blocks, Ntt32<14>::T, smt, st>>>(g, cur, dig, perm, q0, q1, out, fold,
+                                                                             *tabs_of(c, g, 0));
+      else
+        k_rot_keyswitch_t32<14, false, 2><<<blocks, Ntt32<14>::T, smt, st>>>(g, cur, dig, perm, q0, q1, out, fold,
+                                                                              TwNone{});
+    } else {
+      k_rot_keyswitch_t32<13, true, 4><<<blocks, Ntt32<13>::T, smt, st>>>(g, cur, dig, perm, q0, q1, out, fold,
+                                                                           *tabs_of(c, g, 0));
+    }
+    LAUNCHED();
+    return false;
+  }
   bool fused = dig_next != nullptr;
   switch (c->logn) {
     case 12:
@@ -686,6 +742,12 @@ void launch_ct_intt(hei_gpu_ctx* c, unsigned blocks, uint32_t* cts, cudaStream_t
 }
 void launch_poly_ntt(hei_gpu_ctx* c, unsigned blocks, uint32_t gp, uint32_t* polys, int inverse, cudaStream_t st) {
   const size_t sm = smem_bytes(c, 1);
+  if (c->ntt32 && (c->logn == 13 || c->logn == 14)) {
+    if (c->logn == 14) k_poly_ntt32<14><<<blocks, Ntt32<14>::T, sm, st>>>(c->geo, gp, polys, inverse);
+    else k_poly_ntt32<13><<<blocks, Ntt32<13>::T, sm, st>>>(c->geo, gp, polys, inverse);
+    LAUNCHED();
+    return;
+  }
   HEI_DISPATCH(c->logn, (k_poly_ntt_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(c->geo, gp, polys, inverse)),
                (k_poly_ntt<<<blocks, c->threads(), sm, st>>>(c->geo, gp, polys, inverse)));
   LAUNCHED();
@@ -699,6 +761,13 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, false>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
   if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, true>, 2 * sm);
+  if constexpr (LG == 13 || LG == 14) {
+    set_smem_attr((const void*)k_poly_ntt32<LG>, sm);
+    set_smem_attr((const void*)k_rot_digits32<LG, true>, sm);
+    set_smem_attr((const void*)k_rot_digits32<LG, false>, sm);
+    set_smem_attr((const void*)k_rot_keyswitch_t32<LG, true, LG == 14 ? 2 : 4>, sm);
+    set_smem_attr((const void*)k_rot_keyswitch_t32<LG, false, LG == 14 ? 2 : 4>, sm);
+  }
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, true>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_c2<LG, true>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_c2<LG, false>, 3 * sm);
@@ -1515,6 +1584,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     auto c = std::make_unique<hei_gpu_ctx>();
     c->device = d->device;
     if (const char* v = std::getenv("HEI_KS14_REGS")) c->ks14_regs = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_NTT32")) c->ntt32 = std::atoi(v);
     if (const char* v = std::getenv("HEI_SPLIT")) c->split = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_NO_GRAPHS")) c->graphs = std::atoi(v) == 0;
     if (const char* v = std::getenv("HEI_TWO_STREAMS")) c->two_streams = std::atoi(v) != 0;
@@ -1709,8 +1779,40 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
           }
         }
     }
+    // pass-C twiddles of the 32-residue transforms (ntt32.cuh)
+    std::vector<uint4> twc32, itwc32;
+    if (c->logn == 13 || c->logn == 14) {
+      const uint32_t T = n / 32, NC = c->logn - 10, EC = c->logn == 14 ? 30 : 28, KC = EC / 2;
+      g.twc32_stride = KC * T;
+      twc32.resize((size_t)(P + 2) * KC * T);
+      itwc32.resize(twc32.size());
+      std::vector<uint32_t> idx(EC);
+      for (uint32_t row = 0; row < P + 2; ++row)
+        for (uint32_t j = 0; j < T; ++j) {
+          uint32_t e = 0;
+          for (uint32_t st = 10; st < 10 + NC; ++st) {
+            const uint32_t gsh = c->logn - st;  // log2 of the twiddle group size
+            for (uint32_t b = 0; b < (32u >> gsh); ++b) idx[e++] = (1u << st) + ((32u * j) >> gsh) + b;
+          }
+          for (uint32_t k = 0; k < KC; ++k) {
+            const uint2 a = fwd[(size_t)row * n + idx[2 * k]], b = fwd[(size_t)row * n + idx[2 * k + 1]];
+            const uint2 ia = inv[(size_t)row * n + idx[2 * k]], ib = inv[(size_t)row * n + idx[2 * k + 1]];
+            twc32[((size_t)row * KC + k) * T + j] = make_uint4(a.x, a.y, b.x, b.y);
+            itwc32[((size_t)row * KC + k) * T + j] = make_uint4(ia.x, ia.y, ib.x, ib.y);
+          }
+        }
+    }
     set_device(c.get());
     CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    if (!twc32.empty()) {
+      CU(cudaMalloc(&c->d_twc32, twc32.size() * sizeof(uint4)));
+      CU(cudaMalloc(&c->d_itwc32, itwc32.size() * sizeof(uint4)));
+      CU(cudaMemcpyAsync(c->d_twc32, twc32.data(), twc32.size() * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
+      CU(cudaMemcpyAsync(c->d_itwc32, itwc32.data(), itwc32.size() * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      g.twc32 = c->d_twc32;
+      g.itwc32 = c->d_itwc32;
+    }
     if (!twc.empty()) {
       CU(cudaMalloc(&c->d_twc, twc.size() * sizeof(uint4)));
       CU(cudaMalloc(&c->d_itwc, itwc.size() * sizeof(uint4)));
@@ -1772,11 +1874,14 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->d_inv);
   cudaFree(c->d_twc);
   cudaFree(c->d_itwc);
+  cudaFree(c->d_twc32);
+  cudaFree(c->d_itwc32);
   cudaFree(c->d_index);
   cudaFree(c->d_perms);
   cudaFree(c->d_err);
   for (int b = 0; b < 2; ++b) {
     cudaFree(c->d_keys[b]);
+    cudaFree(c->d_keys32[b]);
     cudaFree(c->d_pk[b]);
   }
   cudaFree(c->d_pkp);
@@ -1886,8 +1991,16 @@ void install_galois_keys(hei_gpu_ctx* c, uint32_t b, uint32_t count, const uint6
   if (c->d_keys[b]) cudaFree(c->d_keys[b]);
   c->d_keys[b] = nullptr;
   CU(cudaMalloc(&c->d_keys[b], words * sizeof(uint2)));
-  k_prepare_keys<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, b, count, d_raw, c->d_keys[b], c->d_err);
+  k_prepare_keys<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, b, count, d_raw, c->d_keys[b], c->d_err, 16);
   LAUNCHED();
+  c->keys_words[b] = words;
+  if (c->d_keys32[b]) cudaFree(c->d_keys32[b]);
+  c->d_keys32[b] = nullptr;
+  if (c->ntt32 && (c->logn == 13 || c->logn == 14)) {
+    CU(cudaMalloc(&c->d_keys32[b], words * sizeof(uint2)));
+    k_prepare_keys<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, b, count, d_raw, c->d_keys32[b], c->d_err, 32);
+    LAUNCHED();
+  }
   CU(cudaStreamSynchronize(c->stream));
   check_err_flag(c, HEI_CODEC_ERROR, "galois keys: coefficient not reduced");
   c->key_index[b] = idx;

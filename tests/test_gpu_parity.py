@@ -856,3 +856,31 @@ def test_full_batch_key_switch_variants_bit_exact(prod, monkeypatch):
         assert np.array_equal(got[v], got["0"]), v
     for r in (0, 37, 63):
         assert np.array_equal(got["3"][r], o.sum_all_slots(cts[r])), r
+
+
+@pytest.mark.parametrize("n", [8192, 16384])
+def test_ntt32_bit_exact_all_primes(n, monkeypatch):
+    """The 32-residue-per-thread transforms (ntt32.cuh, HEI_NTT32) equal the
+    oracle's NTT/INTT (ring/poly.cpp:36-50) on every prime."""
+    monkeypatch.setenv("HEI_NTT32", "1")
+    test_ntt_bit_exact_all_primes(n)
+
+
+def test_ntt32_fold_bit_exact(monkeypatch):
+    """Folds on the 32-residue transforms: every N = 16384 fold (C5's ring)
+    and, with HEI_NTT32=2, N = 8192 full batches (digit INTT + TMEM key
+    switch) give the oracle's ciphertexts."""
+    from paper_2204_05496_b200 import EncodedWeights, matmul
+
+    monkeypatch.setenv("HEI_NTT32", "2")
+    test_n16384_c5_shape_bit_exact()
+    o = Oracle(production_params(8192), key_seed=1, enc_seed=2)
+    rng = np.random.default_rng(65)
+    x = rng.integers(-9, 9, size=(64, o.n), dtype=np.int64)
+    cts = o.encode_inputs(x)[:, 0, :]
+    got = gpu_server_from(o).sum_all_slots(cts)
+    monkeypatch.setenv("HEI_NTT32", "0")
+    ref = gpu_server_from(o).sum_all_slots(cts)
+    assert np.array_equal(got, ref)
+    for r in (0, 63):
+        assert np.array_equal(got[r], o.sum_all_slots(cts[r])), r
