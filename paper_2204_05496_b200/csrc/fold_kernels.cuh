@@ -1252,3 +1252,83 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_mask_acc
   }
   if (c_cur != ~0ull) flush(c_cur);
 }
+
+// Mask plaintexts of every slot, once per context (MatmulStream::mask_for_slot,
+// matmul.cpp:146-163: one-hot slot -> INTT_t -> lift -> NTT_q). The reference
+// caches them only for N <= 4096 (host memory); with 180 GB of HBM the device
+// keeps all N of them (N = 8192: 2.7 GB, N = 16384: 10.7 GB), so the
+// per-pair mask step becomes a streaming multiply-accumulate.
+// masks [slot][P][N] in eval order; block = (slot, prime).
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T) k_mask_table(Geo g, uint32_t slot0, uint32_t* __restrict__ masks) {
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N, T = NT::T;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t gp = blockIdx.x % g.P, slot = slot0 + blockIdx.x / g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const BranchInfo& br = g.br[pr.b];
+  const uint32_t q = pr.q, t = br.t, j = threadIdx.x, x0 = NT::posC0(j);
+  const uint32_t pe = __brev(__ldg(&g.index_map[slot])) >> (32 - LOGN);
+  const uint32_t w = pow_barrett(br.psi_inv, 2 * pe + 1, t, br.mu);
+  const uint32_t wT = pow_barrett(w, T, t, br.mu);
+  uint32_t m = mul_barrett(br.ninv.x, pow_barrett(w, j, t, br.mu), t, br.mu);
+  uint32_t e[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    e[r] = m % q;
+    m = mul_barrett(m, wT, t, br.mu);
+  }
+  NT::fwd(e, sm, g.fwd + (size_t)gp * N, g.twc + (size_t)gp * g.twc_stride, q);
+  uint4* o = reinterpret_cast<uint4*>(masks + ((uint64_t)slot * g.P + gp) * N + x0);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) o[c] = make_uint4(e[4 * c], e[4 * c + 1], e[4 * c + 2], e[4 * c + 3]);
+}
+
+// Same accumulation as k_mask_acc_g with the masks read from the table:
+// block = (group of G consecutive pairs, prime, 1024-slot slice), 256 threads
+// x 4 slots, sums in registers, one u64 RED per slot and packed ciphertext.
+__global__ void __launch_bounds__(256) k_mask_acc_c(Geo g, const uint32_t* __restrict__ dot,
+                                                    const uint64_t* __restrict__ rows, uint32_t cols, uint32_t npairs,
+                                                    uint32_t G, const uint32_t* __restrict__ masks,
+                                                    unsigned long long* __restrict__ acc64) {
+  const uint32_t N = g.n, slices = N / 1024;
+  const uint32_t sl = blockIdx.x % slices, gp = (blockIdx.x / slices) % g.P;
+  const uint32_t p0 = (blockIdx.x / (slices * g.P)) * G, p1 = min(npairs, p0 + G);
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t q = pr.q, x0 = sl * 1024 + 4 * threadIdx.x;
+  uint32_t A[4] = {0, 0, 0, 0}, B[4] = {0, 0, 0, 0};
+  uint64_t c_cur = ~0ull;
+  auto flush = [&](uint64_t cc) {
+    unsigned long long* d0 = acc64 + cc * g.ct_words + (uint64_t)pr.poly0 * N + x0;
+    unsigned long long* d1 = acc64 + cc * g.ct_words + (uint64_t)pr.poly1 * N + x0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      atomicAdd(&d0[r], (unsigned long long)A[r]);
+      atomicAdd(&d1[r], (unsigned long long)B[r]);
+      A[r] = B[r] = 0;
+    }
+  };
+  for (uint32_t pair = p0; pair < p1; ++pair) {
+    const uint64_t gidx = rows[pair / cols] * cols + pair % cols;
+    const uint32_t slot = (uint32_t)(gidx % N);
+    const uint64_t c = gidx / N;
+    if (c != c_cur) {
+      if (c_cur != ~0ull) flush(c_cur);
+      c_cur = c;
+    }
+    const uint32_t* base = dot + (uint64_t)pair * g.ct_words;
+    const uint4 m = __ldg(reinterpret_cast<const uint4*>(masks + ((uint64_t)slot * g.P + gp) * N + x0));
+    const uint4 u = *reinterpret_cast<const uint4*>(base + (uint64_t)pr.poly0 * N + x0);
+    const uint4 v = *reinterpret_cast<const uint4*>(base + (uint64_t)pr.poly1 * N + x0);
+    A[0] = add_mod(A[0], mul_barrett(u.x, m.x, q, pr.mu), q);
+    A[1] = add_mod(A[1], mul_barrett(u.y, m.y, q, pr.mu), q);
+    A[2] = add_mod(A[2], mul_barrett(u.z, m.z, q, pr.mu), q);
+    A[3] = add_mod(A[3], mul_barrett(u.w, m.w, q, pr.mu), q);
+    B[0] = add_mod(B[0], mul_barrett(v.x, m.x, q, pr.mu), q);
+    B[1] = add_mod(B[1], mul_barrett(v.y, m.y, q, pr.mu), q);
+    B[2] = add_mod(B[2], mul_barrett(v.z, m.z, q, pr.mu), q);
+    B[3] = add_mod(B[3], mul_barrett(v.w, m.w, q, pr.mu), q);
+  }
+  if (c_cur != ~0ull) flush(c_cur);
+}

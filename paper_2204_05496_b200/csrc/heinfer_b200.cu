@@ -384,6 +384,8 @@ struct hei_gpu_ctx {
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   int ks_tmem = 4;  // HEI_KS_TMEM: full-batch key switch accumulates in TMEM (0 off; 2, 3 CTAs/SM; 4: 3 CTAs/SM, 4-slot rounds)
   bool fuse_big = false;   // HEI_FUSE_BIG=1: full batches also fuse the next digit INTT into the TMEM key switch
+  bool mask_cache = true;  // HEI_MASK_CACHE=0: regenerate each pair's mask (the reference's N > 4096 behaviour)
+  uint32_t* d_mask_table = nullptr;  // [slot][P][N] mask plaintexts, built on first full-batch use
   bool e2e_overlap = true;  // HEI_E2E_OVERLAP=0: host-buffer chunks run one after another
   std::vector<cudaStream_t> chunk_streams;  // 2 x fold_parts streams: consecutive chunks overlap
   int dig_tma = 1;       // HEI_DIG_TMA=0: digit kernel gathers c1 from global memory
@@ -717,6 +719,24 @@ bool launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const u
   LAUNCHED();
   return fused;
 }
+// All N mask plaintexts of the context, built once on first use (blocking,
+// on the context stream) and kept for its lifetime.
+const uint32_t* mask_table(hei_gpu_ctx* c) {
+  if (c->d_mask_table) return c->d_mask_table;
+  const Geo& g = c->geo;
+  CU(cudaMalloc(&c->d_mask_table, (size_t)c->n * g.P * c->n * 4));
+  const uint32_t per = 512;  // slots per launch
+  for (uint32_t s0 = 0; s0 < c->n; s0 += per) {
+    const unsigned blocks = std::min(per, c->n - s0) * g.P;
+    HEI_DISPATCH(c->logn,
+                 (k_mask_table<LG><<<blocks, Ntt<LG>::T, smem_bytes(c, 1), c->stream>>>(g, s0, c->d_mask_table)),
+                 raise(HEI_INTERNAL, "mask table: unsupported ring degree"));
+    LAUNCHED();
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return c->d_mask_table;
+}
+
 void launch_mask_acc(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* res, const uint64_t* rows,
                      uint32_t cols, unsigned long long* acc, cudaStream_t st) {
   const size_t sm = smem_bytes(c, 1);
@@ -724,6 +744,13 @@ void launch_mask_acc(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32
   // enough blocks for every SM at small batches, up to 8 pairs per block
   const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(c->mask_group, npairs * g.P / (148 * 8)));
   const unsigned gblocks = (unsigned)(((npairs + G - 1) / G) * g.P);
+  if (c->mask_cache && c->logn >= 12 && c->logn <= 14 && blocks >= 2u * 148u) {
+    const uint32_t* masks = mask_table(c);
+    const unsigned cb = (unsigned)(((npairs + G - 1) / G) * g.P * (c->n / 1024));
+    k_mask_acc_c<<<cb, 256, 0, st>>>(g, res, rows, cols, npairs, G, masks, acc);
+    LAUNCHED();
+    return;
+  }
   HEI_DISPATCH(c->logn, (k_mask_acc_g<LG><<<gblocks, Ntt<LG>::T, 3 * sm, st>>>(g, res, rows, cols, npairs, G, acc)),
                (k_mask_acc<<<blocks, c->threads(), sm, st>>>(g, res, rows, cols, acc)));
   LAUNCHED();
@@ -777,6 +804,7 @@ void set_fast_attrs(size_t sm) {
   }
   set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
   set_smem_attr((const void*)k_mask_prep<LG>, sm);
+  set_smem_attr((const void*)k_mask_table<LG>, sm);
   set_smem_attr((const void*)k_ks_part<LG>, sm);
   set_smem_attr((const void*)k_ct_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_ct_intt_f<LG>, sm);
@@ -1598,6 +1626,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_FOLD_PARTS"))
       c->fold_parts = std::min<uint32_t>(kMaxFoldParts, std::max(1, std::atoi(v)));
     if (const char* v = std::getenv("HEI_KS_TMEM")) c->ks_tmem = std::atoi(v);
+    if (const char* v = std::getenv("HEI_MASK_CACHE")) c->mask_cache = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_BIG")) c->fuse_big = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_OVERLAP")) c->e2e_overlap = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_GROUP")) c->mask_group = std::max(1, std::atoi(v));
@@ -1875,6 +1904,7 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->d_twc);
   cudaFree(c->d_itwc);
   cudaFree(c->d_twc32);
+  cudaFree(c->d_mask_table);
   cudaFree(c->d_itwc32);
   cudaFree(c->d_index);
   cudaFree(c->d_perms);

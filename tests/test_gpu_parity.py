@@ -884,3 +884,27 @@ def test_ntt32_fold_bit_exact(monkeypatch):
     assert np.array_equal(got, ref)
     for r in (0, 63):
         assert np.array_equal(got[r], o.sum_all_slots(cts[r])), r
+
+
+def test_mask_table_matches_per_pair_masks(prod, monkeypatch):
+    """Launches of >= 296 (pair, prime) blocks multiply by the context's table
+    of all N mask plaintexts (mask_for_slot, matmul.cpp:146-163, built once);
+    smaller ones regenerate each pair's mask as the reference does for
+    N > 4096. Same packed ciphertext either way, equal to the oracle's."""
+    from paper_2204_05496_b200 import EncodedWeights, MatmulStream
+
+    o, _ = prod
+    x, w, b = synthetic(7, 9000, 5, 0.05, 0.1, seed=24)  # 35 pairs = 350 blocks in one flush
+    inputs = o.encode_inputs(x)
+    wp = o.encode_weights(w)
+    got = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("HEI_MASK_CACHE", v)
+        s = gpu_server_from(o)
+        st = MatmulStream(s, EncodedWeights.from_prepared(s, wp, 9000), b, 7)
+        for r in range(7):
+            st.push_row(r, inputs[r])
+        got[v] = st.finish()
+    assert np.array_equal(got["1"], got["0"])
+    want, _ = o.fast_matmul(inputs, 9000, wp, b)
+    assert np.array_equal(got["1"], want)
