@@ -62,6 +62,45 @@ __global__ void k_chunk_dot(Geo g, const uint32_t* __restrict__ in, const uint2*
   }
 }
 
+// Same products for a batch of rows, organised so the weights are read once
+// per block instead of once per pair: block = (poly, 256-slot tile, group of
+// up to CG classes); each thread keeps its slot's weights for those classes
+// (CG x kc (value, Shoup) pairs) in registers and streams the rows. The
+// chunk sum is exact mod q, so the order of the adds does not matter.
+template <int CG, int KC>
+__global__ void __launch_bounds__(256) k_chunk_dot_rows(Geo g, const uint32_t* __restrict__ in,
+                                                       const uint2* __restrict__ W, uint32_t cols, uint32_t rows,
+                                                       uint32_t* __restrict__ dot) {
+  const uint32_t n = g.n, polys = 2 * g.P, tiles = n / 256, groups = (cols + CG - 1) / CG;
+  const uint32_t tile = blockIdx.x % tiles, poly = (blockIdx.x / tiles) % polys, cg = blockIdx.x / (tiles * polys);
+  if (cg >= groups) return;
+  const uint32_t x = tile * 256 + threadIdx.x;
+  const uint32_t gp = poly_prime(g, poly);
+  const uint32_t q = g.pr[gp].q;
+  const uint32_t j0 = cg * CG, nj = min((uint32_t)CG, cols - j0);
+  uint2 w[CG][KC];
+#pragma unroll
+  for (int jj = 0; jj < CG; ++jj)
+#pragma unroll
+    for (int k = 0; k < KC; ++k)
+      w[jj][k] = jj < (int)nj ? __ldg(W + ((uint64_t)(j0 + jj) * KC + k) * g.pt_words + (uint64_t)gp * n + x)
+                              : make_uint2(0, 0);
+  for (uint32_t s = 0; s < rows; ++s) {
+    const uint32_t* src = in + (uint64_t)s * KC * g.ct_words + (uint64_t)poly * n + x;
+    uint32_t a[KC];
+#pragma unroll
+    for (int k = 0; k < KC; ++k) a[k] = __ldg(src + (uint64_t)k * g.ct_words);
+#pragma unroll
+    for (int jj = 0; jj < CG; ++jj) {
+      if (jj >= (int)nj) break;
+      uint32_t acc = 0;
+#pragma unroll
+      for (int k = 0; k < KC; ++k) acc = add_mod(acc, mul_shoup(a[k], w[jj][k].x, w[jj][k].y, q), q);
+      dot[((uint64_t)s * cols + j0 + jj) * g.ct_words + (uint64_t)poly * n + x] = acc;
+    }
+  }
+}
+
 // Feature-block sharding: the chunk products of chunks
 // [k0, k0 + kn) of every pair, each reduced mod q, added into an unreduced
 // u64 dot accumulator (ranks' partials sum exactly; reduced by k_dot_reduce).

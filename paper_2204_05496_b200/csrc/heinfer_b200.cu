@@ -384,6 +384,7 @@ struct hei_gpu_ctx {
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   int ks_tmem = 4;  // HEI_KS_TMEM: full-batch key switch accumulates in TMEM (0 off; 2, 3 CTAs/SM; 4: 3 CTAs/SM, 4-slot rounds)
   bool fuse_big = false;   // HEI_FUSE_BIG=1: full batches also fuse the next digit INTT into the TMEM key switch
+  bool dot_rows = true;    // HEI_DOT_ROWS=0: per-pair chunk-product kernel for every batch
   bool mask_cache = true;  // HEI_MASK_CACHE=0: regenerate each pair's mask (the reference's N > 4096 behaviour)
   uint32_t* d_mask_table = nullptr;  // [slot][P][N] mask plaintexts, built on first full-batch use
   bool e2e_overlap = true;  // HEI_E2E_OVERLAP=0: host-buffer chunks run one after another
@@ -737,6 +738,30 @@ const uint32_t* mask_table(hei_gpu_ctx* c) {
   return c->d_mask_table;
 }
 
+// dot[pair] = sum_k chunk_k (.) W[j][k] for `rows` rows (push_row,
+// matmul.cpp:318-326): row-streaming kernel for the common chunk counts at
+// N >= 4096, the per-pair kernel otherwise.
+void launch_chunk_dot(hei_gpu_ctx* c, const uint32_t* in, const hei_gpu_weights* w, uint64_t rows, uint32_t* dot,
+                      cudaStream_t st) {
+  const Geo& g = c->geo;
+  const uint32_t cols = (uint32_t)w->cols, kc = (uint32_t)w->kc;
+  if (c->dot_rows && c->n >= 4096 && kc >= 1 && kc <= 5 && rows >= 8) {
+    constexpr uint32_t CG = 4;
+    const unsigned blocks = (unsigned)((c->n / 256) * 2 * c->P() * ((cols + CG - 1) / CG));
+    switch (kc) {
+      case 1: k_chunk_dot_rows<CG, 1><<<blocks, 256, 0, st>>>(g, in, w->d_w, cols, (uint32_t)rows, dot); break;
+      case 2: k_chunk_dot_rows<CG, 2><<<blocks, 256, 0, st>>>(g, in, w->d_w, cols, (uint32_t)rows, dot); break;
+      case 3: k_chunk_dot_rows<CG, 3><<<blocks, 256, 0, st>>>(g, in, w->d_w, cols, (uint32_t)rows, dot); break;
+      case 4: k_chunk_dot_rows<CG, 4><<<blocks, 256, 0, st>>>(g, in, w->d_w, cols, (uint32_t)rows, dot); break;
+      default: k_chunk_dot_rows<CG, 5><<<blocks, 256, 0, st>>>(g, in, w->d_w, cols, (uint32_t)rows, dot); break;
+    }
+  } else {
+    k_chunk_dot<<<(unsigned)(rows * cols * 2 * c->P()), std::min<unsigned>(c->threads(), c->n / 4), 0, st>>>(
+        g, in, w->d_w, cols, kc, dot);
+  }
+  LAUNCHED();
+}
+
 void launch_mask_acc(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* res, const uint64_t* rows,
                      uint32_t cols, unsigned long long* acc, cudaStream_t st) {
   const size_t sm = smem_bytes(c, 1);
@@ -981,9 +1006,7 @@ bool run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
       uint32_t* A = c->d_dotA + off * c->ct_words();
       uint32_t* B = c->d_dotB + off * c->ct_words();
       uint32_t* D = c->d_dig + off * c->pt_words();
-      k_chunk_dot<<<(unsigned)(pp * 2 * c->P()), std::min<unsigned>(T, c->n / 4), 0, hs>>>(
-          g, d_in + rr0 * w->kc * c->ct_words(), w->d_w, cols, (uint32_t)w->kc, A);
-      LAUNCHED();
+      launch_chunk_dot(c, d_in + rr0 * w->kc * c->ct_words(), w, nr, A, hs);
       uint32_t* res = fold(c, pp, A, B, hs, D);
       launch_mask_acc(c, g, (unsigned)(pp * c->P()), res, d_rows + rr0, cols, s->d_acc, hs);
       if (h) {
@@ -1021,9 +1044,7 @@ bool run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
     CU(cudaEventCreateWithFlags(&mask_ev, cudaEventDisableTiming));
     CU(cudaEventRecord(mask_ev, c->bias_stream));
   }
-  k_chunk_dot<<<(unsigned)(pairs * 2 * c->P()), std::min<unsigned>(T, c->n / 4), 0, st>>>(g, d_in, w->d_w, cols,
-                                                                                         (uint32_t)w->kc, c->d_dotA);
-  LAUNCHED();
+  launch_chunk_dot(c, d_in, w, nrows, c->d_dotA, st);
   uint32_t* res = fold(c, pairs, c->d_dotA, c->d_dotB, st);
   if (premask) {
     CU(cudaStreamWaitEvent(st, mask_ev, 0));
@@ -1626,6 +1647,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_FOLD_PARTS"))
       c->fold_parts = std::min<uint32_t>(kMaxFoldParts, std::max(1, std::atoi(v)));
     if (const char* v = std::getenv("HEI_KS_TMEM")) c->ks_tmem = std::atoi(v);
+    if (const char* v = std::getenv("HEI_DOT_ROWS")) c->dot_rows = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_CACHE")) c->mask_cache = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_BIG")) c->fuse_big = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_OVERLAP")) c->e2e_overlap = std::atoi(v) != 0;

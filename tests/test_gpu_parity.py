@@ -908,3 +908,26 @@ def test_mask_table_matches_per_pair_masks(prod, monkeypatch):
     assert np.array_equal(got["1"], got["0"])
     want, _ = o.fast_matmul(inputs, 9000, wp, b)
     assert np.array_equal(got["1"], want)
+
+
+def test_chunk_products_row_kernel(prod, monkeypatch):
+    """push_row's chunk products (matmul.cpp:318-326) for a batch of >= 8
+    rows take the row-streaming kernel (weights held in registers); same
+    packed ciphertext as the per-pair kernel and the oracle."""
+    from paper_2204_05496_b200 import EncodedWeights, MatmulStream
+
+    o, _ = prod
+    x, w, b = synthetic(9, 9000, 3, 0.05, 0.1, seed=25)
+    inputs = o.encode_inputs(x)
+    wp = o.encode_weights(w)
+    got = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("HEI_DOT_ROWS", v)
+        s = gpu_server_from(o)
+        st = MatmulStream(s, EncodedWeights.from_prepared(s, wp, 9000), b, 9)
+        for r in range(9):
+            st.push_row(r, inputs[r])
+        got[v] = st.finish()
+    assert np.array_equal(got["1"], got["0"])
+    want, _ = o.fast_matmul(inputs, 9000, wp, b)
+    assert np.array_equal(got["1"], want)
