@@ -1163,6 +1163,101 @@ __global__ void __launch_bounds__(256) k_ks_reduce(Geo g, const uint32_t* __rest
   *reinterpret_cast<uint4*>(out + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n + x) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
 }
 
+// Latency path, key switch split over its digits for parallelism (R = 1 has
+// only 110 (pair, prime) blocks for 148 SMs, and one block per (pair, prime)
+// is issue-bound on its SM). Block per (pair, prime i, digit l != i): one
+// forward NTT_i(digit_l mod q_i) and its two key products, 40 registers so
+// three blocks share an SM; the l == i term, the sum over l and the fold adds
+// happen in k_ks_reduce2. Same arithmetic as k_rot_keyswitch_t (exact sums).
+template <int LOGN>
+__global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_ks_part2(Geo g, const uint32_t* __restrict__ digits,
+                                                                             const uint2* __restrict__ key0,
+                                                                             const uint2* __restrict__ key1,
+                                                                             uint32_t* __restrict__ part, uint32_t Lm1) {
+  using NT = Ntt<LOGN>;
+  constexpr uint32_t N = NT::N, T = NT::T;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  const uint32_t lp = blockIdx.x % Lm1, pg = blockIdx.x / Lm1;
+  const uint32_t pair = pg / g.P, gp = pg % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  if (lp + 1 >= pr.L) return;
+  const uint32_t q = pr.q, i = pr.i, l = lp + (lp >= i ? 1u : 0u), j = threadIdx.x, x0 = NT::posC0(j);
+  uint32_t e[16];
+  const uint32_t* src = digits + ((uint64_t)pair * g.P + pr.first + l) * N;
+  if (pr.fast_reduce) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint32_t v = src[NT::posA(j, r)];
+      e[r] = min(v, v - q);
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
+  }
+  NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, g.twc + (size_t)gp * g.twc_stride, q);
+  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * pr.L * 2 * N;
+  const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
+  const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
+  uint32_t* o = part + (uint64_t)blockIdx.x * 2 * N + x0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
+    *reinterpret_cast<uint4*>(o + 4 * c) =
+        make_uint4(mul_shoup(e[4 * c], a.x, a.y, q), mul_shoup(e[4 * c + 1], a.z, a.w, q),
+                   mul_shoup(e[4 * c + 2], b.x, b.y, q), mul_shoup(e[4 * c + 3], b.z, b.w, q));
+    const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
+    *reinterpret_cast<uint4*>(o + N + 4 * c) =
+        make_uint4(mul_shoup(e[4 * c], u.x, u.y, q), mul_shoup(e[4 * c + 1], u.z, u.w, q),
+                   mul_shoup(e[4 * c + 2], v.x, v.y, q), mul_shoup(e[4 * c + 3], v.z, v.w, q));
+  }
+}
+
+// grid (pair, prime, n / 1024 tiles), 256 threads x 4 slots: out0 = sigma(c0)
+// + sigma(c1)_i (.) K[i][i][0] + sum_l part0 (+ c0), out1 = sigma(c1)_i (.)
+// K[i][i][1] + sum_l part1 (+ c1). Keys are in the pass-C transposed layout
+// (16 slots per NTT thread), so slots x..x+3 are two uint4 per part.
+__global__ void __launch_bounds__(256) k_ks_reduce2(Geo g, const uint32_t* __restrict__ dot,
+                                                    const uint32_t* __restrict__ part,
+                                                    const uint32_t* __restrict__ perm, const uint2* __restrict__ key0,
+                                                    const uint2* __restrict__ key1, uint32_t Lm1,
+                                                    uint32_t* __restrict__ out, int fold) {
+  const uint32_t n = g.n, tiles = n / 1024, T = n / 16;
+  const uint32_t pg = blockIdx.x / tiles, tile = blockIdx.x % tiles;
+  const uint32_t pair = pg / g.P, gp = pg % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t q = pr.q, L = pr.L, i = pr.i;
+  const uint32_t x = tile * 1024 + threadIdx.x * 4;
+  const uint32_t* c0 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly0 * n;
+  const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n;
+  const uint4 pm = __ldg(reinterpret_cast<const uint4*>(perm + x));
+  const uint32_t d[4] = {c1[pm.x], c1[pm.y], c1[pm.z], c1[pm.w]};
+  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * n;
+  const uint32_t jt = x >> 4, rr = x & 15;
+  const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * n) + jt;
+  const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * n) + jt;
+  const uint4 ka = __ldg(k0 + (rr >> 1) * T), kb = __ldg(k0 + ((rr >> 1) + 1) * T);
+  const uint4 ua = __ldg(k1 + (rr >> 1) * T), ub = __ldg(k1 + ((rr >> 1) + 1) * T);
+  uint32_t a0[4] = {add_mod(c0[pm.x], mul_shoup(d[0], ka.x, ka.y, q), q), add_mod(c0[pm.y], mul_shoup(d[1], ka.z, ka.w, q), q),
+                    add_mod(c0[pm.z], mul_shoup(d[2], kb.x, kb.y, q), q), add_mod(c0[pm.w], mul_shoup(d[3], kb.z, kb.w, q), q)};
+  uint32_t a1[4] = {mul_shoup(d[0], ua.x, ua.y, q), mul_shoup(d[1], ua.z, ua.w, q), mul_shoup(d[2], ub.x, ub.y, q),
+                    mul_shoup(d[3], ub.z, ub.w, q)};
+  const uint32_t* ps = part + (uint64_t)pg * Lm1 * 2 * n + x;
+  for (uint32_t l = 0; l + 1 < L; ++l) {
+    const uint4 u = *reinterpret_cast<const uint4*>(ps + (uint64_t)l * 2 * n);
+    const uint4 v = *reinterpret_cast<const uint4*>(ps + (uint64_t)l * 2 * n + n);
+    a0[0] = add_mod(a0[0], u.x, q), a0[1] = add_mod(a0[1], u.y, q), a0[2] = add_mod(a0[2], u.z, q), a0[3] = add_mod(a0[3], u.w, q);
+    a1[0] = add_mod(a1[0], v.x, q), a1[1] = add_mod(a1[1], v.y, q), a1[2] = add_mod(a1[2], v.z, q), a1[3] = add_mod(a1[3], v.w, q);
+  }
+  if (fold) {
+    const uint4 u = *reinterpret_cast<const uint4*>(c0 + x), v = *reinterpret_cast<const uint4*>(c1 + x);
+    a0[0] = add_mod(a0[0], u.x, q), a0[1] = add_mod(a0[1], u.y, q), a0[2] = add_mod(a0[2], u.z, q), a0[3] = add_mod(a0[3], u.w, q);
+    a1[0] = add_mod(a1[0], v.x, q), a1[1] = add_mod(a1[1], v.y, q), a1[2] = add_mod(a1[2], v.z, q), a1[3] = add_mod(a1[3], v.w, q);
+  }
+  *reinterpret_cast<uint4*>(out + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly0 * n + x) = make_uint4(a0[0], a0[1], a0[2], a0[3]);
+  *reinterpret_cast<uint4*>(out + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n + x) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
+}
+
 // Latency path, split in two: the one-hot mask plaintexts (same closed form
 // as k_mask_acc_g) depend only on the slot, so k_mask_prep computes them on a
 // side stream while the fold runs; k_mask_apply then multiplies and adds.

@@ -365,7 +365,7 @@ struct hei_gpu_ctx {
   size_t pinned_out_bytes = 0;
   uint32_t* pool_part = nullptr;  // split key-switch partials (small batches)
   size_t pool_part_bytes = 0;
-  bool split = false;   // HEI_SPLIT=1: split the key switch over digits for small batches
+  int split = 0;   // HEI_SPLIT: split the key switch over digits for small batches (1: per digit incl. l == i, 2: l != i only, 3 CTAs/SM)
   bool graphs = true;   // HEI_NO_GRAPHS=1: launch the small-batch fold eagerly
   bool two_streams = true;  // HEI_TWO_STREAMS=0: fold the batch on one stream only
   bool mt_jump = true;      // HEI_MT_JUMP=0: sequential mt19937_64 replay only
@@ -831,6 +831,7 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_mask_prep<LG>, sm);
   set_smem_attr((const void*)k_mask_table<LG>, sm);
   set_smem_attr((const void*)k_ks_part<LG>, sm);
+  set_smem_attr((const void*)k_ks_part2<LG>, sm);
   set_smem_attr((const void*)k_ct_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_ct_intt_f<LG>, sm);
   set_smem_attr((const void*)k_poly_ntt_f<LG>, sm);
@@ -879,7 +880,15 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
     if (!have_digits) launch_rot_digits(c, g, blocks, cur, perm, dig, st);
     if (c->timing) CU(cudaEventRecord(e1, st));
     have_digits = false;
-    if (split) {
+    if (split && c->split == 2) {
+      const uint32_t Lm1 = Lmax - 1;
+      HEI_DISPATCH(c->logn,
+                   (k_ks_part2<LG><<<(unsigned)(blocks * Lm1), Ntt<LG>::T, smem_bytes(c, 1), st>>>(g, dig, k0, k1, part, Lm1)),
+                   (void)0);
+      LAUNCHED();
+      k_ks_reduce2<<<blocks * (c->n / 1024), 256, 0, st>>>(g, cur, part, perm, k0, k1, Lm1, other, 1);
+      LAUNCHED();
+    } else if (split) {
       const unsigned pb = (unsigned)(blocks * Lmax);
       HEI_DISPATCH(c->logn,
                    (k_ks_part<LG><<<pb, Ntt<LG>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, part, Lmax,
@@ -1634,7 +1643,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     c->device = d->device;
     if (const char* v = std::getenv("HEI_KS14_REGS")) c->ks14_regs = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_NTT32")) c->ntt32 = std::atoi(v);
-    if (const char* v = std::getenv("HEI_SPLIT")) c->split = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_SPLIT")) c->split = std::atoi(v);
     if (const char* v = std::getenv("HEI_NO_GRAPHS")) c->graphs = std::atoi(v) == 0;
     if (const char* v = std::getenv("HEI_TWO_STREAMS")) c->two_streams = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MT_JUMP")) c->mt_jump = std::atoi(v) != 0;

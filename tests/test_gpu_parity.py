@@ -931,3 +931,24 @@ def test_chunk_products_row_kernel(prod, monkeypatch):
     assert np.array_equal(got["1"], got["0"])
     want, _ = o.fast_matmul(inputs, 9000, wp, b)
     assert np.array_equal(got["1"], want)
+
+
+def test_split_key_switch_latency_path(prod, monkeypatch):
+    """Single-individual folds with the key switch split over digits
+    (HEI_SPLIT=2: one block per (pair, prime, digit l != i), the l == i term
+    and the sums in the reduce kernel) match the default latency kernel and
+    the oracle (production C1 shape)."""
+    from paper_2204_05496_b200 import EncodedWeights, matmul
+
+    o, _ = prod
+    x, w, b = synthetic(1, 1000, 11, 0.05, 0.1, seed=26)
+    inputs = o.encode_inputs(x)
+    wp = o.encode_weights(w)
+    got = {}
+    for v in ("2", "0"):
+        monkeypatch.setenv("HEI_SPLIT", v)
+        s = gpu_server_from(o)
+        got[v], _ = matmul(s, inputs, EncodedWeights.from_prepared(s, wp, 1000), b)
+    assert np.array_equal(got["2"], got["0"])
+    want, _ = o.fast_matmul(inputs, 1000, wp, b)
+    assert np.array_equal(got["2"], want)
