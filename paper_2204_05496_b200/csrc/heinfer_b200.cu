@@ -655,6 +655,9 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
         else if (c->ks_tmem == 4)  // 3 CTAs/SM, 4-slot TMEM rounds
           k_rot_keyswitch_t<LG, true, 3, 4><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold,
                                                                              nullptr, nullptr, *tabs_of(c, g, 0));
+        else if (c->ks_tmem == 5)  // as 4, digits prefetched into shared memory by TMA
+          k_rot_keyswitch_t<LG, true, 3, 4, false, true><<<blocks, Ntt<LG>::T, 2 * smt, st>>>(
+              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
         else
           k_rot_keyswitch_t<LG, true, 2><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr,
                                                                           nullptr, *tabs_of(c, g, 0));
@@ -813,6 +816,7 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, false>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
   if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, true>, 2 * sm);
+  if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, false, true>, 2 * sm);
   if constexpr (LG == 13 || LG == 14) {
     set_smem_attr((const void*)k_poly_ntt32<LG>, sm);
     set_smem_attr((const void*)k_rot_digits32<LG, true>, sm);

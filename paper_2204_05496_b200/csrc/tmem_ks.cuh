@@ -63,7 +63,9 @@ constexpr uint32_t kTmemCols = 128;
 // NEXT: also produce the next rotation's digit for prime i (as
 // k_rot_keyswitch_s<.., NEXT>): the new c1 lands in a second shared buffer,
 // is permuted by the next Galois element and inverse-transformed here.
-template <int LOGN, bool PTW, int MINB, int GS = 8, bool NEXT = false>
+// PF: each digit arrives in a second shared buffer by a TMA bulk copy issued
+// as soon as the previous digit's transform has passed its barriers.
+template <int LOGN, bool PTW, int MINB, int GS = 8, bool NEXT = false, bool PF = false>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, const uint32_t* __restrict__ dot,
                                                                       const uint32_t* __restrict__ digits,
                                                                       const uint32_t* __restrict__ perm,
@@ -78,12 +80,14 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
   constexpr uint32_t N = NT::N, T = NT::T;
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
-  __shared__ uint64_t gbar;
+  __shared__ uint64_t gbar, dbar;
   __shared__ uint32_t tbase;
   const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t q = pr.q, L = pr.L, i = pr.i;
   const uint32_t j = threadIdx.x, x0 = NT::posC0(j), warp = j >> 5;
+  uint32_t* stg = sm + N;  // PF: digit staging buffer
+  const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
   const uint32_t* ct = dot + (uint64_t)pair * g.ct_words;
   const uint32_t* c0 = ct + (uint64_t)pr.poly0 * N;
   const uint32_t* c1 = ct + (uint64_t)pr.poly1 * N;
@@ -97,6 +101,10 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
   if (threadIdx.x == 32) {
     mbar_init(&gbar, 1);
     bulk_load(sm, c1, N * 4, &gbar);
+    if constexpr (PF) {
+      mbar_init(&dbar, 1);
+      if (L > 1) bulk_load(stg, dig + (uint64_t)(i == 0 ? 1 : 0) * N, N * 4, &dbar);
+    }
   }
   tm_fence_before();
   __syncthreads();
@@ -131,12 +139,20 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
       tm_st(ta + 16 + GS * h, B);
     }
   }
-  const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
   const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
   uint32_t e[16];
+  uint32_t dpar = 0;
   for (uint32_t l = 0; l < L; ++l) {
     if (l == i) continue;
-    {
+    if constexpr (PF) {
+      mbar_wait(&dbar, dpar);
+      dpar ^= 1u;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t v = stg[NT::posA(j, r)];
+        e[r] = pr.fast_reduce ? min(v, v - q) : v % q;
+      }
+    } else {
       const uint32_t* src = dig + (uint64_t)l * N;
       if (pr.fast_reduce) {
 #pragma unroll
@@ -153,6 +169,15 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
       NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
     else
       NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
+    if constexpr (PF) {
+      // every thread read the staged digit before the transform's barriers
+      uint32_t ln = l + 1;
+      if (ln == i) ++ln;
+      if (ln < L && threadIdx.x == 0) {
+        fence_proxy_async_smem();
+        bulk_load(stg, dig + (uint64_t)ln * N, N * 4, &dbar);
+      }
+    }
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
     tm_wait_st();  // the previous digit's accumulator stores have landed
