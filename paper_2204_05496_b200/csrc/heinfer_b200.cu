@@ -382,6 +382,7 @@ struct hei_gpu_ctx {
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
+  bool ks14_tmem = true;  // HEI_KS14_TMEM=0: N = 16384 full batches keep the shared-memory accumulators
   int ks_tmem = 4;  // HEI_KS_TMEM: full-batch key switch accumulates in TMEM (0 off; 2, 3 CTAs/SM; 4: 3 CTAs/SM, 4-slot rounds)
   bool fuse_big = false;   // HEI_FUSE_BIG=1: full batches also fuse the next digit INTT into the TMEM key switch
   bool dot_rows = true;    // HEI_DOT_ROWS=0: per-pair chunk-product kernel for every batch
@@ -631,6 +632,17 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
       launch_ks_c2<LG, false>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, nullptr, nullptr);
     return;
   }
+  if constexpr (LG == 14) {
+    if (c->ks14_tmem && !dig_next) {  // TMEM accumulators (256 columns), 1 CTA of 1024 threads per SM
+      if (big)
+        k_rot_keyswitch_t<LG, true, 1, 4><<<blocks, Ntt<LG>::T, smem_bytes(c, 1), st>>>(
+            g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
+      else
+        k_rot_keyswitch_t<LG, false, 1, 4><<<blocks, Ntt<LG>::T, smem_bytes(c, 1), st>>>(
+            g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, TwNone{});
+      return;
+    }
+  }
   if (dig_next) {
     if constexpr (LG == 13) {
       if (big && c->ks_tmem) {  // TMEM accumulators + the next rotation's digit
@@ -817,6 +829,10 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
   if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, true>, 2 * sm);
   if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, false, true>, 2 * sm);
+  if constexpr (LG == 14) {
+    set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 1, 4>, sm);
+    set_smem_attr((const void*)k_rot_keyswitch_t<LG, false, 1, 4>, sm);
+  }
   if constexpr (LG == 13 || LG == 14) {
     set_smem_attr((const void*)k_poly_ntt32<LG>, sm);
     set_smem_attr((const void*)k_rot_digits32<LG, true>, sm);
@@ -1660,6 +1676,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_FOLD_PARTS"))
       c->fold_parts = std::min<uint32_t>(kMaxFoldParts, std::max(1, std::atoi(v)));
     if (const char* v = std::getenv("HEI_KS_TMEM")) c->ks_tmem = std::atoi(v);
+    if (const char* v = std::getenv("HEI_KS14_TMEM")) c->ks14_tmem = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DOT_ROWS")) c->dot_rows = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_CACHE")) c->mask_cache = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_BIG")) c->fuse_big = std::atoi(v) != 0;

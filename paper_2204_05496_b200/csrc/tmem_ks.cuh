@@ -57,7 +57,6 @@ __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sy
 __device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-constexpr uint32_t kTmemCols = 128;
 
 // GS: accumulator slots per TMEM load/store round (8 or 4).
 // NEXT: also produce the next rotation's digit for prime i (as
@@ -76,7 +75,8 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
                                                                       uint32_t* __restrict__ dig_next,
                                                                       const __grid_constant__ TwArg<PTW> tab) {
   using NT = Ntt<LOGN>;
-  static_assert(NT::T == 512, "TMEM layout assumes 16 warps (4 per lane quarter)");
+  static_assert(NT::T == 512 || NT::T == 1024, "TMEM layout: 4 or 8 warps per lane quarter");
+  constexpr uint32_t kTmemCols = NT::T / 4;  // 32 columns per warp, warps of a lane quarter side by side
   constexpr uint32_t N = NT::N, T = NT::T;
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);

@@ -952,3 +952,19 @@ def test_split_key_switch_latency_path(prod, monkeypatch):
     assert np.array_equal(got["2"], got["0"])
     want, _ = o.fast_matmul(inputs, 1000, wp, b)
     assert np.array_equal(got["2"], want)
+
+
+def test_n16384_full_batch_tmem_key_switch(monkeypatch):
+    """C5's ring at full-batch launch sizes (60 ciphertexts = 600 blocks, not
+    fused): the TMEM-accumulator key switch (1024 threads, 256 TMEM columns)
+    equals the shared-memory kernel and the oracle."""
+    o = Oracle(production_params(16384), key_seed=5, enc_seed=6)
+    rng = np.random.default_rng(60)
+    x = rng.integers(-9, 9, size=(60, o.n), dtype=np.int64)
+    cts = o.encode_inputs(x)[:, 0, :]
+    got = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("HEI_KS14_TMEM", v)
+        got[v] = gpu_server_from(o).sum_all_slots(cts)
+    assert np.array_equal(got["1"], got["0"])
+    assert np.array_equal(got["1"][59], o.sum_all_slots(cts[59]))
