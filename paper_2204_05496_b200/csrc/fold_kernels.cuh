@@ -477,7 +477,8 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digi
   using NT = Ntt<LOGN>;
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
-  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  uint32_t pair, gp;
+  block_pair_prime(g, pair, gp);
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * NT::N;
   const uint32_t j = threadIdx.x, x0 = NT::posC0(j);

@@ -219,7 +219,22 @@ struct Geo {
   const uint4* itwc32;
   uint32_t twc32_stride;
   const uint32_t* index_map;
+  // block -> (pair, prime) order of the full-batch fold kernels: 0 pair-major
+  // (blockIdx = pair * P + prime), 1 prime-major (blockIdx = prime * pairs +
+  // pair: CTAs resident on one SM share a prime's twiddles and key lines)
+  uint32_t prime_major;
 };
+// (pair, prime) of this block, for grids of pairs * P blocks
+__device__ __forceinline__ void block_pair_prime(const Geo& g, uint32_t& pair, uint32_t& gp) {
+  if (g.prime_major) {
+    const uint32_t pairs = gridDim.x / g.P;
+    gp = blockIdx.x / pairs;
+    pair = blockIdx.x - gp * pairs;
+  } else {
+    pair = blockIdx.x / g.P;
+    gp = blockIdx.x % g.P;
+  }
+}
 
 // Pass-A/B twiddles (indices 0..255) of every q prime, passed by value in the
 // kernel parameter space (CUDA >= 12.1 allows 32 KB of parameters).
@@ -383,6 +398,7 @@ struct hei_gpu_ctx {
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   bool ks14_tmem = true;  // HEI_KS14_TMEM=0: N = 16384 full batches keep the shared-memory accumulators
+  bool prime_major = false;  // HEI_PRIME_MAJOR: full-batch fold kernels walk (pair, prime) blocks prime-major
   int ks_tmem = 4;  // HEI_KS_TMEM: full-batch key switch accumulates in TMEM (0 off; 2, 3 CTAs/SM; 4: 3 CTAs/SM, 4-slot rounds)
   bool fuse_big = false;   // HEI_FUSE_BIG=1: full batches also fuse the next digit INTT into the TMEM key switch
   bool dot_rows = true;    // HEI_DOT_ROWS=0: per-pair chunk-product kernel for every batch
@@ -667,6 +683,15 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
         else if (c->ks_tmem == 4)  // 3 CTAs/SM, 4-slot TMEM rounds
           k_rot_keyswitch_t<LG, true, 3, 4><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold,
                                                                              nullptr, nullptr, *tabs_of(c, g, 0));
+        else if (c->ks_tmem == 7)  // as 6, key loads free to move across the TMEM waits
+          k_rot_keyswitch_t<LG, true, 3, 4, false, false, true, true><<<blocks, Ntt<LG>::T, 2 * smt, st>>>(
+              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
+        else if (c->ks_tmem == 8)  // as 4, key loads free to move across the TMEM waits
+          k_rot_keyswitch_t<LG, true, 3, 4, false, false, false, true><<<blocks, Ntt<LG>::T, smt, st>>>(
+              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
+        else if (c->ks_tmem == 6)  // as 4, digit transforms alternate between two exchange buffers
+          k_rot_keyswitch_t<LG, true, 3, 4, false, false, true><<<blocks, Ntt<LG>::T, 2 * smt, st>>>(
+              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
         else if (c->ks_tmem == 5)  // as 4, digits prefetched into shared memory by TMA
           k_rot_keyswitch_t<LG, true, 3, 4, false, true><<<blocks, Ntt<LG>::T, 2 * smt, st>>>(
               g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
@@ -829,6 +854,8 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
   if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, true>, 2 * sm);
   if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, false, true>, 2 * sm);
+  if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, false, false, true>, 2 * sm);
+  if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, false, false, true, true>, 2 * sm);
   if constexpr (LG == 14) {
     set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 1, 4>, sm);
     set_smem_attr((const void*)k_rot_keyswitch_t<LG, false, 1, 4>, sm);
@@ -1676,6 +1703,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_FOLD_PARTS"))
       c->fold_parts = std::min<uint32_t>(kMaxFoldParts, std::max(1, std::atoi(v)));
     if (const char* v = std::getenv("HEI_KS_TMEM")) c->ks_tmem = std::atoi(v);
+    if (const char* v = std::getenv("HEI_PRIME_MAJOR")) c->prime_major = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_KS14_TMEM")) c->ks14_tmem = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DOT_ROWS")) c->dot_rows = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_CACHE")) c->mask_cache = std::atoi(v) != 0;
@@ -1924,6 +1952,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     g.fwd = c->d_fwd;
     g.inv = c->d_inv;
     g.index_map = c->d_index;
+    g.prime_major = c->prime_major ? 1u : 0u;
     const size_t s3 = smem_bytes(c.get(), 3);
     set_smem_attr((const void*)k_rot_keyswitch, s3);
     set_smem_attr((const void*)k_rot_digits, smem_bytes(c.get(), 1));

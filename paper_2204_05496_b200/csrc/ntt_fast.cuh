@@ -127,7 +127,10 @@ struct Ntt {
   // barrier on the shared buffer (sm: N words).
   // LAZY_OUT: leave the final stage's outputs in [0, 2q) (for consumers that
   // only feed them to a Shoup multiply).
-  template <bool LAZY_OUT = false, typename TW = const uint2*>
+  // LEAD_SYNC = false: the caller guarantees no thread still reads `sm`
+  // (e.g. consecutive transforms alternate between two buffers, so the
+  // previous reader of this one has since passed two barriers).
+  template <bool LAZY_OUT = false, typename TW = const uint2*, bool LEAD_SYNC = true>
   static __device__ __forceinline__ void fwd(uint32_t (&e)[16], uint32_t* sm, TW tw, const uint4* __restrict__ twc,
                                              uint32_t q) {
     const uint32_t j = tid();
@@ -139,7 +142,7 @@ struct Ntt {
       for (int r = 0; r < 16; ++r)
         if (!(r & half)) ct(e[r], e[r + half], load_tw(tw, (1 << s) + (r >> (4 - s))), q, red(r, half), red(r + half, half));
     }
-    sync();
+    if constexpr (LEAD_SYNC) sync();
 #pragma unroll
     for (int r = 0; r < 16; ++r) store_pos(sm, posA(j, r), e[r]);
     sync();

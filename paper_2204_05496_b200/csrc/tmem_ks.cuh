@@ -38,10 +38,15 @@ __device__ __forceinline__ void tm_st(uint32_t taddr, const uint32_t (&v)[X]) {
                  : "memory");
 }
 // wait::ld, threading the loaded registers through so no use is scheduled
-// before the wait
-template <int X>
+// before the wait. MEM = false drops the memory clobber: ordering against the
+// other tcgen05 instructions is kept (all are volatile asm), and read-only
+// global loads (the Galois key) may be scheduled across the wait.
+template <int X, bool MEM = true>
 __device__ __forceinline__ void tm_wait_ld(uint32_t (&a)[X], uint32_t (&b)[X]) {
-  if constexpr (X == 8)
+  if constexpr (!MEM && X == 4)
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]));
+  else if constexpr (X == 8)
     asm volatile("tcgen05.wait::ld.sync.aligned;"
                  : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
                    "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7])
@@ -64,7 +69,11 @@ __device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::
 // is permuted by the next Galois element and inverse-transformed here.
 // PF: each digit arrives in a second shared buffer by a TMA bulk copy issued
 // as soon as the previous digit's transform has passed its barriers.
-template <int LOGN, bool PTW, int MINB, int GS = 8, bool NEXT = false, bool PF = false>
+// PP: consecutive digit transforms alternate between two exchange buffers
+// (sm + N first, then sm, ...), so each transform skips its leading barrier.
+// HOIST: the digit loop's TMEM wait carries no memory clobber (see tm_wait_ld).
+template <int LOGN, bool PTW, int MINB, int GS = 8, bool NEXT = false, bool PF = false, bool PP = false,
+          bool HOIST = false>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, const uint32_t* __restrict__ dot,
                                                                       const uint32_t* __restrict__ digits,
                                                                       const uint32_t* __restrict__ perm,
@@ -76,13 +85,15 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
                                                                       const __grid_constant__ TwArg<PTW> tab) {
   using NT = Ntt<LOGN>;
   static_assert(NT::T == 512 || NT::T == 1024, "TMEM layout: 4 or 8 warps per lane quarter");
+  static_assert(!(PP && (PF || NEXT)), "PP uses sm + N as its second exchange buffer");
   constexpr uint32_t kTmemCols = NT::T / 4;  // 32 columns per warp, warps of a lane quarter side by side
   constexpr uint32_t N = NT::N, T = NT::T;
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
   __shared__ uint64_t gbar, dbar;
   __shared__ uint32_t tbase;
-  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  uint32_t pair, gp;
+  block_pair_prime(g, pair, gp);
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t q = pr.q, L = pr.L, i = pr.i;
   const uint32_t j = threadIdx.x, x0 = NT::posC0(j), warp = j >> 5;
@@ -141,7 +152,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
   }
   const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
   uint32_t e[16];
-  uint32_t dpar = 0;
+  uint32_t dpar = 0, nt = 0;
   for (uint32_t l = 0; l < L; ++l) {
     if (l == i) continue;
     if constexpr (PF) {
@@ -165,7 +176,13 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
         for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
       }
     }
-    if constexpr (PTW)
+    if constexpr (PP) {
+      uint32_t* xb = sm + ((nt++ & 1u) ? 0u : N);
+      if constexpr (PTW)
+        NT::template fwd<true, ParamTw, false>(e, xb, ParamTw{tab.w[gp]}, twc, q);
+      else
+        NT::template fwd<true, const uint2*, false>(e, xb, g.fwd + (size_t)gp * N, twc, q);
+    } else if constexpr (PTW)
       NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
     else
       NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
@@ -186,7 +203,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
       uint32_t A[GS], B[GS];
       tm_ld(ta + GS * h, A);
       tm_ld(ta + 16 + GS * h, B);
-      tm_wait_ld(A, B);
+      tm_wait_ld<GS, !HOIST>(A, B);
 #pragma unroll
       for (int c = h * GS / 4; c < (h + 1) * GS / 4; ++c) {
         const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
