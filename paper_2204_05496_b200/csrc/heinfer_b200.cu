@@ -683,6 +683,12 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
         else if (c->ks_tmem == 4)  // 3 CTAs/SM, 4-slot TMEM rounds
           k_rot_keyswitch_t<LG, true, 3, 4><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold,
                                                                              nullptr, nullptr, *tabs_of(c, g, 0));
+        else if (c->ks_tmem == 10)  // as 4, next digit (then c0) bulk-prefetched into L2
+          k_rot_keyswitch_t<LG, true, 3, 4, false, false, false, false, false, true><<<blocks, Ntt<LG>::T, smt, st>>>(
+              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
+        else if (c->ks_tmem == 9)  // as 4, Galois keys bypass L1 (L1::no_allocate)
+          k_rot_keyswitch_t<LG, true, 3, 4, false, false, false, false, true><<<blocks, Ntt<LG>::T, smt, st>>>(
+              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
         else if (c->ks_tmem == 7)  // as 6, key loads free to move across the TMEM waits
           k_rot_keyswitch_t<LG, true, 3, 4, false, false, true, true><<<blocks, Ntt<LG>::T, 2 * smt, st>>>(
               g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));

@@ -58,6 +58,20 @@ __device__ __forceinline__ void tm_wait_ld(uint32_t (&a)[X], uint32_t (&b)[X]) {
                  :
                  : "memory");
 }
+// Galois-key read: NA = true streams it past L1 (L1::no_allocate), leaving
+// L1 to the pass-C twiddles that every digit transform of the CTA re-reads.
+template <bool NA>
+__device__ __forceinline__ uint4 ldg_key(const uint4* p) {
+  if constexpr (NA) {
+    uint4 v;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "l"(p));
+    return v;
+  } else {
+    return __ldg(p);
+  }
+}
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -72,8 +86,11 @@ __device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::
 // PP: consecutive digit transforms alternate between two exchange buffers
 // (sm + N first, then sm, ...), so each transform skips its leading barrier.
 // HOIST: the digit loop's TMEM wait carries no memory clobber (see tm_wait_ld).
+// NA: Galois keys read with L1::no_allocate (ldg_key).
+// L2PF: one thread prefetches the next digit (and, at the last digit, c0)
+// into L2 with a bulk prefetch, so the digit loads hit L2 instead of HBM.
 template <int LOGN, bool PTW, int MINB, int GS = 8, bool NEXT = false, bool PF = false, bool PP = false,
-          bool HOIST = false>
+          bool HOIST = false, bool NA = false, bool L2PF = false>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, const uint32_t* __restrict__ dot,
                                                                       const uint32_t* __restrict__ digits,
                                                                       const uint32_t* __restrict__ perm,
@@ -112,6 +129,9 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
   if (threadIdx.x == 32) {
     mbar_init(&gbar, 1);
     bulk_load(sm, c1, N * 4, &gbar);
+    if constexpr (L2PF) {
+      if (L > 1) bulk_prefetch_l2(dig + (uint64_t)(i == 0 ? 1 : 0) * N, N * 4);
+    }
     if constexpr (PF) {
       mbar_init(&dbar, 1);
       if (L > 1) bulk_load(stg, dig + (uint64_t)(i == 0 ? 1 : 0) * N, N * 4, &dbar);
@@ -134,8 +154,8 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
       for (int c = h * GS / 4; c < (h + 1) * GS / 4; ++c) {
         const uint4 pm = __ldg(pp + c);
         const uint32_t d0 = sm[pm.x], d1 = sm[pm.y], d2 = sm[pm.z], d3 = sm[pm.w];
-        const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
-        const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
+        const uint4 a = ldg_key<NA>(k0 + (2 * c) * T), b = ldg_key<NA>(k0 + (2 * c + 1) * T);
+        const uint4 u = ldg_key<NA>(k1 + (2 * c) * T), v = ldg_key<NA>(k1 + (2 * c + 1) * T);
         const int o = 4 * c - GS * h;
         A[o] = mul_shoup(d0, a.x, a.y, q);
         A[o + 1] = mul_shoup(d1, a.z, a.w, q);
@@ -165,6 +185,13 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
       }
     } else {
       const uint32_t* src = dig + (uint64_t)l * N;
+      if constexpr (L2PF) {
+        if (threadIdx.x == 0) {
+          uint32_t ln = l + 1;
+          if (ln == i) ++ln;
+          bulk_prefetch_l2(ln < L ? dig + (uint64_t)ln * N : c0, N * 4);
+        }
+      }
       if (pr.fast_reduce) {
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
@@ -206,13 +233,13 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
       tm_wait_ld<GS, !HOIST>(A, B);
 #pragma unroll
       for (int c = h * GS / 4; c < (h + 1) * GS / 4; ++c) {
-        const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
+        const uint4 a = ldg_key<NA>(k0 + (2 * c) * T), b = ldg_key<NA>(k0 + (2 * c + 1) * T);
         const int o = 4 * c - GS * h;
         A[o] = add_mod(A[o], mul_shoup(e[4 * c], a.x, a.y, q), q);
         A[o + 1] = add_mod(A[o + 1], mul_shoup(e[4 * c + 1], a.z, a.w, q), q);
         A[o + 2] = add_mod(A[o + 2], mul_shoup(e[4 * c + 2], b.x, b.y, q), q);
         A[o + 3] = add_mod(A[o + 3], mul_shoup(e[4 * c + 3], b.z, b.w, q), q);
-        const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
+        const uint4 u = ldg_key<NA>(k1 + (2 * c) * T), v = ldg_key<NA>(k1 + (2 * c + 1) * T);
         B[o] = add_mod(B[o], mul_shoup(e[4 * c], u.x, u.y, q), q);
         B[o + 1] = add_mod(B[o + 1], mul_shoup(e[4 * c + 1], u.z, u.w, q), q);
         B[o + 2] = add_mod(B[o + 2], mul_shoup(e[4 * c + 2], v.x, v.y, q), q);

@@ -844,19 +844,20 @@ def test_full_batch_key_switch_variants_bit_exact(prod, monkeypatch):
     kernel give identical ciphertexts, equal to the oracle's; so does the TMEM
     kernel that also produces the next rotation's digits (HEI_FUSE_BIG=1), and
     the variants with TMA digit prefetch (5), two exchange buffers (6) and
-    key loads hoisted across the TMEM waits (7, 8), and prime-major block
-    order (4p)."""
+    key loads hoisted across the TMEM waits (7, 8), prime-major block
+    order (4p), keys read past L1 (9, 9p), and
+    L2 bulk prefetch of the next digit (10)."""
     o, _ = prod
     rng = np.random.default_rng(64)
     x = rng.integers(-9, 9, size=(64, o.n), dtype=np.int64)
     cts = o.encode_inputs(x)[:, 0, :]
     got = {}
-    for v in ("4", "3", "2", "0", "4f", "5", "6", "7", "8", "4p"):
-        monkeypatch.setenv("HEI_KS_TMEM", v[0])
+    for v in ("4", "3", "2", "0", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10"):
+        monkeypatch.setenv("HEI_KS_TMEM", v.rstrip("fp"))
         monkeypatch.setenv("HEI_FUSE_BIG", "1" if v.endswith("f") else "0")
         monkeypatch.setenv("HEI_PRIME_MAJOR", "1" if v.endswith("p") else "0")
         got[v] = gpu_server_from(o).sum_all_slots(cts)
-    for v in ("4", "3", "2", "4f", "5", "6", "7", "8", "4p"):
+    for v in ("4", "3", "2", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10"):
         assert np.array_equal(got[v], got["0"]), v
     for r in (0, 37, 63):
         assert np.array_equal(got["3"][r], o.sum_all_slots(cts[r])), r
