@@ -398,6 +398,9 @@ struct hei_gpu_ctx {
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   bool ks14_tmem = true;  // HEI_KS14_TMEM=0: N = 16384 full batches keep the shared-memory accumulators
+  int bl_split = 1;        // HEI_BL_SPLIT: feature slices per k_bl_accum_w launch (accumulator copies)
+  bool bl_accum_w = true;  // HEI_BL_ACCUM_W: standard-algorithm sums with exact 64-bit products (k_bl_accum_w)
+  int enc_minb = 3;  // HEI_ENC_MINB: resident CTAs/SM of the public-key encryption kernel (2 or 3)
   bool prime_major = false;  // HEI_PRIME_MAJOR: full-batch fold kernels walk (pair, prime) blocks prime-major
   int ks_tmem = 4;  // HEI_KS_TMEM: full-batch key switch accumulates in TMEM (0 off; 2, 3 CTAs/SM; 4: 3 CTAs/SM, 4-slot rounds)
   bool fuse_big = false;   // HEI_FUSE_BIG=1: full batches also fuse the next digit INTT into the TMEM key switch
@@ -576,6 +579,20 @@ const uint2* keys32_of(hei_gpu_ctx* c, const uint2* k) {
   raise(HEI_INTERNAL, "key pointer outside the uploaded key sets");
 }
 
+// Public-key encryption of E features/rows (E * P blocks); HEI_ENC_MINB=3
+// runs the fast kernel at 3 CTAs/SM (40 registers) instead of 2.
+void launch_bl_encrypt(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const int8_t* d_noise, const uint32_t* d_m,
+                       uint32_t* ct, size_t sm1, cudaStream_t st) {
+  const bool ptw = blocks >= 2u * 148u;
+  HEI_DISPATCH(c->logn,
+               (ptw ? (c->enc_minb == 3
+                           ? k_bl_encrypt<LG, true, (LG <= 13 ? 3 : 1)><<<blocks, Ntt<LG>::T, sm1, st>>>(
+                                 g, d_noise, d_m, c->d_pkp, ct, *tabs_of(c, g, 0))
+                           : k_bl_encrypt<LG, true><<<blocks, Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct,
+                                                                                     *tabs_of(c, g, 0)))
+                    : k_bl_encrypt<LG, false><<<blocks, Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct, TwNone{})),
+               (k_bl_encrypt_g<<<blocks, c->threads(), sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct)));
+}
 void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* perm,
                        uint32_t* dig, cudaStream_t st) {
   const size_t sm = smem_bytes(c, 1), smf = smem_bytes(c, c->dig_tma ? 2 : 1);
@@ -891,6 +908,7 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_bl_encode<LG>, sm);
   set_smem_attr((const void*)k_bl_encrypt<LG, true>, sm);
   set_smem_attr((const void*)k_bl_encrypt<LG, false>, sm);
+  set_smem_attr((const void*)k_bl_encrypt<LG, true, (LG <= 13 ? 3 : 1)>, sm);
   set_smem_attr((const void*)k_prepare_pk<LG>, sm);
 }
 
@@ -1607,13 +1625,7 @@ void encode_inputs_impl(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uint64_
                    (k_bl_encode_g<<<dim3((unsigned)E, 2), c->threads(), sm1, st>>>(g, d_x, rows, f, e0, (uint32_t)kc, d_m, 1)));
       LAUNCHED();
       uint32_t* ct = out_dev ? out_dev + e0 * c->ct_words() : d_ct;
-      HEI_DISPATCH(c->logn,
-                   (E * P >= 2u * 148u
-                        ? k_bl_encrypt<LG, true><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp,
-                                                                                             ct, *tabs_of(c, g, 0))
-                        : k_bl_encrypt<LG, false><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp,
-                                                                                              ct, TwNone{})),
-                   (k_bl_encrypt_g<<<(unsigned)(E * P), c->threads(), sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct)));
+      launch_bl_encrypt(c, g, (unsigned)(E * P), d_noise, d_m, ct, sm1, st);
       LAUNCHED();
       if (!out_dev) {
         k_widen<<<grid_for(E * c->ct_words(), 256), 256, 0, st>>>(d_ct, d_out64, E * c->ct_words());
@@ -1709,6 +1721,9 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_FOLD_PARTS"))
       c->fold_parts = std::min<uint32_t>(kMaxFoldParts, std::max(1, std::atoi(v)));
     if (const char* v = std::getenv("HEI_KS_TMEM")) c->ks_tmem = std::atoi(v);
+    if (const char* v = std::getenv("HEI_BL_SPLIT")) c->bl_split = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("HEI_BL_ACCUM_W")) c->bl_accum_w = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_ENC_MINB")) c->enc_minb = std::atoi(v);
     if (const char* v = std::getenv("HEI_PRIME_MAJOR")) c->prime_major = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_KS14_TMEM")) c->ks14_tmem = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DOT_ROWS")) c->dot_rows = std::atoi(v) != 0;
@@ -3053,7 +3068,8 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     d_w = scratch<int64_t>(c, kScrW, f * cols * 8);
     d_bias = scratch<int64_t>(c, kScrBias, cols * 8);
     d_wc = scratch<uint2>(c, kScrWc, f * cols * P * sizeof(uint2));
-    d_acc = scratch<unsigned long long>(c, kScrAcc, outw * 8);
+    const uint32_t S = c->bl_accum_w ? std::max(1, c->bl_split) : 1;  // accumulator copies (k_bl_accum_w slices)
+    d_acc = scratch<unsigned long long>(c, kScrAcc, outw * 8 * S);
     d_raw = scratch<uint64_t>(c, kScrRaw, 2 * 2 * Emax * 3 * n * 8);  // [slot][branch][draws]
     d_state = scratch<uint64_t>(c, kScrState, 2 * 313 * 8);
     d_noise = scratch<int8_t>(c, kScrNoise, Emax * 2 * 3 * n);
@@ -3064,7 +3080,7 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     CU(cudaMemcpyAsync(d_x, x, rows * f * 8, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(d_w, w, f * cols * 8, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(d_bias, bias, cols * 8, cudaMemcpyHostToDevice, st));
-    CU(cudaMemsetAsync(d_acc, 0, outw * 8, st));
+    CU(cudaMemsetAsync(d_acc, 0, outw * 8 * S, st));
     uint64_t hstate[2][313];
     for (int b = 0; b < 2; ++b) {
       hei_gpu_prng* r = b ? rng1 : rng0;
@@ -3137,18 +3153,16 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
                    (k_bl_encode<LG><<<dim3((unsigned)E, 2), Ntt<LG>::T, sm1, st>>>(g, d_x, rows, f, k0, (uint32_t)B, d_m)),
                    (k_bl_encode_g<<<dim3((unsigned)E, 2), c->threads(), sm1, st>>>(g, d_x, rows, f, k0, (uint32_t)B, d_m)));
       LAUNCHED();
-      HEI_DISPATCH(c->logn,
-                   (E * P >= 2u * 148u
-                        ? k_bl_encrypt<LG, true><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp,
-                                                                                             d_ct, *tabs_of(c, g, 0))
-                        : k_bl_encrypt<LG, false><<<(unsigned)(E * P), Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp,
-                                                                                              d_ct, TwNone{})),
-                   (k_bl_encrypt_g<<<(unsigned)(E * P), c->threads(), sm1, st>>>(g, d_noise, d_m, c->d_pkp, d_ct)));
+      launch_bl_encrypt(c, g, (unsigned)(E * P), d_noise, d_m, d_ct, sm1, st);
       LAUNCHED();
       for (uint32_t j0 = 0; j0 < cols; j0 += kBlJ) {
         const unsigned blocks = (unsigned)(B * 2 * P * (n / at));
-        k_bl_accum<<<blocks, at, Fb * kBlJ * sizeof(uint2), st>>>(g, d_ct, (uint32_t)Fb, (uint32_t)B, (uint32_t)cols, j0,
-                                                                  d_wc + k0 * cols * P, d_acc);
+        if (c->bl_accum_w)
+          k_bl_accum_w<<<dim3(blocks, S), at, Fb * kBlJ * sizeof(uint32_t), st>>>(
+              g, d_ct, (uint32_t)Fb, (uint32_t)B, (uint32_t)cols, j0, d_wc + k0 * cols * P, d_acc, outw);
+        else
+          k_bl_accum<<<blocks, at, Fb * kBlJ * sizeof(uint2), st>>>(g, d_ct, (uint32_t)Fb, (uint32_t)B, (uint32_t)cols,
+                                                                    j0, d_wc + k0 * cols * P, d_acc);
         LAUNCHED();
       }
     }
@@ -3158,7 +3172,7 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
       cudaEventDestroy(used[k]);
     }
     (void)fast;
-    k_bl_finish<<<(unsigned)(B * cols * P), c->threads(), sm1, st>>>(g, d_acc, d_bias, (uint32_t)cols, d_out);
+    k_bl_finish<<<(unsigned)(B * cols * P), c->threads(), sm1, st>>>(g, d_acc, d_bias, (uint32_t)cols, d_out, S, outw);
     LAUNCHED();
     k_widen<<<grid_for(outw, 256), 256, 0, st>>>(d_out, d_out64, outw);
     LAUNCHED();

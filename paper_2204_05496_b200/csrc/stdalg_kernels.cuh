@@ -50,8 +50,8 @@ __device__ __forceinline__ uint32_t lift_small(int32_t v, uint32_t q) { return v
 // (context.cpp:270-301): c0 = NTT(u) pk0 + NTT(e0 + Delta m),
 // c1 = NTT(u) pk1 + NTT(e1). pk is prepared [gp][part] in the pass-C
 // transposed layout.
-template <int LOGN, bool PTW>
-__global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_bl_encrypt(Geo g, const int8_t* __restrict__ noise,
+template <int LOGN, bool PTW, int MINB = (LOGN <= 13 ? 2 : 1)>
+__global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_bl_encrypt(Geo g, const int8_t* __restrict__ noise,
                                                             const uint32_t* __restrict__ m,
                                                             const uint2* __restrict__ pkd,
                                                             uint32_t* __restrict__ cts,
@@ -175,10 +175,83 @@ __global__ void k_bl_accum(Geo g, const uint32_t* __restrict__ cts, uint32_t F, 
   }
 }
 
+// Same sums with exact 64-bit products and no Shoup step: every weight
+// residue is < t < 2^31 and every ct residue < q < 2^31, so v * w < 2^62 and
+// one IMAD.WIDE.U32 accumulates it. The accumulator is folded every 3
+// features (a -> hi(a) * (2^32 mod q) + lo(a), congruent mod q): with k = 3
+// products of < 2^61 (t0 < 2^30) between folds the bound stays below
+// 3 * 2^62 + 2^33 < 2^64. For t < 2^20 (products < 2^51) no fold is needed
+// within a batch. The batch sum is reduced mod q before it reaches `acc`, so
+// the result equals k_bl_accum's mod q exactly. Weights (values only) are
+// read from shared memory as 3 x 128-bit per feature.
+//
+// The batch's features are split over S block slices (blockIdx.y); slice s
+// sums its feature range into its own accumulator copy acc + s * slice_words
+// (k_bl_finish adds the copies), so a launch has S times the blocks.
+__global__ void k_bl_accum_w(Geo g, const uint32_t* __restrict__ cts, uint32_t F, uint32_t B, uint32_t cols,
+                             uint32_t j0, const uint2* __restrict__ wc, unsigned long long* __restrict__ acc,
+                             uint64_t slice_words) {
+  static_assert(kBlJ == 12, "3 x uint4 of weights per feature");
+  extern __shared__ uint4 wsm4[];  // [F][3] = [F][kBlJ] u32
+  uint32_t* wsm = reinterpret_cast<uint32_t*>(wsm4);
+  const uint32_t n = g.n, polys = 2 * g.P;
+  const uint32_t tiles = n / blockDim.x;
+  const uint32_t tile = blockIdx.x % tiles;
+  const uint32_t poly = (blockIdx.x / tiles) % polys;
+  const uint32_t blk = blockIdx.x / (tiles * polys);
+  const uint32_t gp = poly_prime(g, poly);
+  const uint32_t q = g.pr[gp].q;
+  const uint32_t jn = min((uint32_t)kBlJ, cols - j0);
+  const uint32_t k_lo = (uint32_t)((uint64_t)F * blockIdx.y / gridDim.y);
+  F = (uint32_t)((uint64_t)F * (blockIdx.y + 1) / gridDim.y) - k_lo;
+  acc += blockIdx.y * slice_words;
+  for (uint32_t x = threadIdx.x; x < F * kBlJ; x += blockDim.x) {
+    const uint32_t kk = x / kBlJ, jj = x % kBlJ;
+    wsm[x] = jj < jn ? wc[((uint64_t)(k_lo + kk) * cols + j0 + jj) * g.P + gp].x : 0u;
+  }
+  __syncthreads();
+  const uint32_t xs = tile * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)B * g.ct_words;
+  const uint32_t* src = cts + (uint64_t)blk * g.ct_words + (uint64_t)poly * n + xs + k_lo * stride;
+  unsigned long long a[kBlJ];
+#pragma unroll
+  for (int jj = 0; jj < kBlJ; ++jj) a[jj] = 0;
+  auto mac = [&](uint32_t kk) {
+    const uint64_t v = src[kk * stride];
+    const uint4 w0 = wsm4[3 * kk], w1 = wsm4[3 * kk + 1], w2 = wsm4[3 * kk + 2];
+    const uint32_t w[kBlJ] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w, w2.x, w2.y, w2.z, w2.w};
+#pragma unroll
+    for (int jj = 0; jj < kBlJ; ++jj) a[jj] += v * w[jj];
+  };
+  if (g.br[g.pr[gp].b].t < (1u << 20)) {
+#pragma unroll 8
+    for (uint32_t kk = 0; kk < F; ++kk) mac(kk);
+  } else {
+    const uint64_t R = (uint64_t)((1ull << 32) % q);
+    uint32_t kk = 0;
+#pragma unroll 2
+    for (; kk + 3 <= F; kk += 3) {
+      mac(kk);
+      mac(kk + 1);
+      mac(kk + 2);
+#pragma unroll
+      for (int jj = 0; jj < kBlJ; ++jj) a[jj] = (a[jj] >> 32) * R + (a[jj] & 0xffffffffull);
+    }
+    for (; kk < F; ++kk) mac(kk);
+  }
+#pragma unroll
+  for (uint32_t jj = 0; jj < kBlJ; ++jj) {
+    if (jj < jn) {
+      unsigned long long* d = acc + (((uint64_t)blk * cols + j0 + jj) * g.ct_words) + (uint64_t)poly * n + xs;
+      *d += a[jj] % q;
+    }
+  }
+}
+
 // finish of the baseline (matmul.cpp:464-476): reduce, then part0 +=
 // NTT(Delta * INTT_t(all slots = bias[j])). Block per ((blk, j), gp).
 __global__ void k_bl_finish(Geo g, const unsigned long long* __restrict__ acc, const int64_t* __restrict__ bias,
-                            uint32_t cols, uint32_t* __restrict__ out) {
+                            uint32_t cols, uint32_t* __restrict__ out, uint32_t S = 1, uint64_t slice_words = 0) {
   extern __shared__ uint32_t sm[];
   const uint32_t n = g.n;
   const uint64_t c = blockIdx.x / g.P;  // (blk * cols + j)
@@ -200,8 +273,13 @@ __global__ void k_bl_finish(Geo g, const unsigned long long* __restrict__ acc, c
   uint32_t* o0 = out + c * g.ct_words + (uint64_t)pr.poly0 * n;
   uint32_t* o1 = out + c * g.ct_words + (uint64_t)pr.poly1 * n;
   for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
-    o0[x] = add_mod((uint32_t)(a0[x] % q), sm[x], q);
-    o1[x] = (uint32_t)(a1[x] % q);
+    unsigned long long s0 = a0[x], s1 = a1[x];  // each copy < 2^40: the sum cannot wrap
+    for (uint32_t k = 1; k < S; ++k) {
+      s0 += a0[x + k * slice_words];
+      s1 += a1[x + k * slice_words];
+    }
+    o0[x] = add_mod((uint32_t)(s0 % q), sm[x], q);
+    o1[x] = (uint32_t)(s1 % q);
   }
 }
 
