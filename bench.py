@@ -446,6 +446,8 @@ def run_ours(args, world, rank, local):
         blocks = R / batches * cols * (L0 + L1)  # (pair, prime) blocks per timed key-switch launch
         if blocks <= 148:
             ks_name = f"k_rot_keyswitch_w2<{logn}> (latency path: 2-group CTA, fused next digit)"
+        elif logn == 14 and os.environ.get("HEI_KS14_TMEM", "1") != "0":
+            ks_name = "k_rot_keyswitch_t<14> (TMEM accumulators, 1 CTA of 1024 threads/SM)"
         elif blocks < 296 or logn != 13 or os.environ.get("HEI_KS_TMEM", "4") == "0":
             ks_name = f"k_rot_keyswitch_s<{logn}> (shared-memory accumulators)"
         else:

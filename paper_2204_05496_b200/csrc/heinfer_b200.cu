@@ -223,6 +223,11 @@ struct Geo {
   // (blockIdx = pair * P + prime), 1 prime-major (blockIdx = prime * pairs +
   // pair: CTAs resident on one SM share a prime's twiddles and key lines)
   uint32_t prime_major;
+  // N = 16384 half-ring key switch (ks_half.cuh): per (prime, half) natural
+  // and pass-C tables of the half's N/2-point transform
+  const uint2* fwdh;    // [P][2][N/2]
+  const uint4* twch;    // [P][2][twch_stride]
+  uint32_t twch_stride;
 };
 // (pair, prime) of this block, for grids of pairs * P blocks
 __device__ __forceinline__ void block_pair_prime(const Geo& g, uint32_t& pair, uint32_t& gp) {
@@ -283,6 +288,7 @@ __device__ __forceinline__ uint32_t poly_prime(const Geo& g, uint32_t poly) {
 #include "fold_kernels.cuh"
 #include "tmem_ks.cuh"
 #include "ks32.cuh"
+#include "ks_half.cuh"
 
 #include "stdalg_kernels.cuh"
 
@@ -328,6 +334,9 @@ struct hei_gpu_ctx {
   uint2 *d_fwd = nullptr, *d_inv = nullptr;
   std::vector<uint2> h_fwd, h_inv;  // host copies (pass-A/B rows go in kernel params)
   uint4 *d_twc = nullptr, *d_itwc = nullptr;
+  uint2* d_fwdh = nullptr;  // N = 16384 half-ring tables (ks_half.cuh)
+  uint4* d_twch = nullptr;
+  std::vector<uint2> h_fwdh;
   uint4 *d_twc32 = nullptr, *d_itwc32 = nullptr;
   uint32_t* d_index = nullptr;
   // galois elements in fold order: steps 1, 2, ..., n/4, then the swap
@@ -397,6 +406,7 @@ struct hei_gpu_ctx {
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
+  bool ks14_half = true;  // HEI_KS14_HALF=0: N = 16384 full batches use the 1024-thread TMEM kernel
   bool ks14_tmem = true;  // HEI_KS14_TMEM=0: N = 16384 full batches keep the shared-memory accumulators
   int bl_split = 1;        // HEI_BL_SPLIT: feature slices per k_bl_accum_w launch (accumulator copies)
   bool bl_accum_w = true;  // HEI_BL_ACCUM_W: standard-algorithm sums with exact 64-bit products (k_bl_accum_w)
@@ -563,6 +573,18 @@ const TwAB* tabs_of(hei_gpu_ctx* c, const Geo& g, int inverse) {
   return &t;
 }
 
+// Pass-A/B rows of the N = 16384 half-ring tables (half h) for the primes of `g`.
+const TwAB* tabs_half(hei_gpu_ctx* c, const Geo& g, uint32_t h) {
+  thread_local TwAB t;
+  for (uint32_t k = 0; k < g.P && k < (uint32_t)kMaxAB; ++k) {
+    uint32_t src = 0;
+    for (uint32_t m = 0; m < c->geo.P; ++m)
+      if (c->geo.pr[m].q == g.pr[k].q) src = m;
+    std::memcpy(t.w[k], c->h_fwdh.data() + ((size_t)src * 2 + h) * (c->n / 2), 256 * sizeof(uint2));
+  }
+  return &t;
+}
+
 // The 32-residue transforms (ntt32.cuh) serve every N = 16384 fold when
 // HEI_NTT32 >= 1 and N = 8192 full batches when HEI_NTT32 = 2.
 bool use_ntt32(hei_gpu_ctx* c, unsigned blocks) {
@@ -666,6 +688,12 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
     return;
   }
   if constexpr (LG == 14) {
+    if (c->ks14_half && !dig_next && big && c->d_twch) {  // two 512-thread half-ring blocks, 3 CTAs/SM
+      for (uint32_t h = 0; h < 2; ++h)
+        k_rot_keyswitch_h<true><<<blocks, 512, 8192 * 4, st>>>(g, cur, dig, perm, k0, k1, out, fold, h,
+                                                                *tabs_half(c, g, h));
+      return;
+    }
     if (c->ks14_tmem && !dig_next) {  // TMEM accumulators (256 columns), 1 CTA of 1024 threads per SM
       if (big)
         k_rot_keyswitch_t<LG, true, 1, 4><<<blocks, Ntt<LG>::T, smem_bytes(c, 1), st>>>(
@@ -1726,6 +1754,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_ENC_MINB")) c->enc_minb = std::atoi(v);
     if (const char* v = std::getenv("HEI_PRIME_MAJOR")) c->prime_major = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_KS14_TMEM")) c->ks14_tmem = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_KS14_HALF")) c->ks14_half = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DOT_ROWS")) c->dot_rows = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_CACHE")) c->mask_cache = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_BIG")) c->fuse_big = std::atoi(v) != 0;
@@ -1909,6 +1938,35 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
           }
         }
     }
+    // N = 16384 half-ring tables (ks_half.cuh): half h's stage s' block i'
+    // uses zetas[2^(s'+1) + h 2^s' + i'], stored at local index 2^s' + i'
+    std::vector<uint4> twch;
+    if (c->logn == 14) {
+      const uint32_t nh = n / 2, T = nh / 16, KC = 8;  // Ntt<13>: XST = 1, PAD = 0
+      g.twch_stride = KC * T;
+      c->h_fwdh.assign((size_t)P * 2 * nh, make_uint2(0, 0));
+      twch.resize((size_t)P * 2 * KC * T);
+      std::vector<uint32_t> idx(2 * KC);
+      for (uint32_t row = 0; row < P; ++row)
+        for (uint32_t h = 0; h < 2; ++h) {
+          uint2* loc = c->h_fwdh.data() + ((size_t)row * 2 + h) * nh;
+          for (uint32_t k = 1; k < nh; ++k) {
+            const uint32_t m = 1u << (31 - __builtin_clz(k));
+            loc[k] = fwd[(size_t)row * n + 2 * m + h * m + (k - m)];
+          }
+          for (uint32_t j = 0; j < T; ++j) {
+            const uint32_t x0 = 16 * j;
+            uint32_t e = 0;
+            idx[e++] = (1u << 8) + (x0 >> 5);  // the cross-thread stage (logn 13)
+            for (uint32_t st = 0; st < 4; ++st)
+              for (uint32_t b2 = 0; b2 < (1u << st); ++b2) idx[e++] = (1u << (13 - 4 + st)) + (x0 >> (4 - st)) + b2;
+            for (uint32_t k = 0; k < KC; ++k) {
+              const uint2 a = loc[idx[2 * k]], b2 = loc[idx[2 * k + 1]];
+              twch[(((size_t)row * 2 + h) * KC + k) * T + j] = make_uint4(a.x, a.y, b2.x, b2.y);
+            }
+          }
+        }
+    }
     // pass-C twiddles of the 32-residue transforms (ntt32.cuh)
     std::vector<uint4> twc32, itwc32;
     if (c->logn == 13 || c->logn == 14) {
@@ -1942,6 +2000,16 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
       CU(cudaStreamSynchronize(c->stream));
       g.twc32 = c->d_twc32;
       g.itwc32 = c->d_itwc32;
+    }
+    if (!twch.empty()) {
+      CU(cudaMalloc(&c->d_twch, twch.size() * sizeof(uint4)));
+      CU(cudaMalloc(&c->d_fwdh, c->h_fwdh.size() * sizeof(uint2)));
+      CU(cudaMemcpyAsync(c->d_twch, twch.data(), twch.size() * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
+      CU(cudaMemcpyAsync(c->d_fwdh, c->h_fwdh.data(), c->h_fwdh.size() * sizeof(uint2), cudaMemcpyHostToDevice,
+                         c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      g.twch = c->d_twch;
+      g.fwdh = c->d_fwdh;
     }
     if (!twc.empty()) {
       CU(cudaMalloc(&c->d_twc, twc.size() * sizeof(uint4)));
@@ -2004,6 +2072,8 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->d_fwd);
   cudaFree(c->d_inv);
   cudaFree(c->d_twc);
+  cudaFree(c->d_twch);
+  cudaFree(c->d_fwdh);
   cudaFree(c->d_itwc);
   cudaFree(c->d_twc32);
   cudaFree(c->d_mask_table);
@@ -2945,6 +3015,10 @@ int hei_gpu_apply_galois(hei_gpu_ctx* c, uint32_t b, uint64_t elt, const uint64_
     if (g.twc) {
       gb.twc = g.twc + (size_t)(b ? c->L[0] : 0) * g.twc_stride;
       gb.itwc = g.itwc + (size_t)(b ? c->L[0] : 0) * g.twc_stride;
+    }
+    if (g.twch) {
+      gb.twch = g.twch + (size_t)(b ? c->L[0] : 0) * 2 * g.twch_stride;
+      gb.fwdh = g.fwdh + (size_t)(b ? c->L[0] : 0) * 2 * (n / 2);
     }
     const size_t words = 2ull * L * n;
     std::vector<uint32_t> h32(words);

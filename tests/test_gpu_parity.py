@@ -281,6 +281,31 @@ def test_baseline_bit_exact_and_rng_state(n):
     assert nxt.shape[-1] == p.n
 
 
+def test_baseline_gemv_variants_bit_exact(monkeypatch):
+    """baseline_matmul's feature sums (matmul.cpp:453-459) over 600 features
+    (three batches, a ragged last one) with weights of both signs, so the
+    branch-0 residues reach ~2^30: the Shoup GEMV (HEI_BL_ACCUM_W=0), the
+    exact-product GEMV (default) and its 3-slice split give the oracle's
+    blocks bit for bit."""
+    from paper_2204_05496_b200 import Prng, baseline_matmul
+
+    p, R, f, cols = production_params(8192), 1, 600, 3
+    o = Oracle(p, key_seed=15, enc_seed=16)
+    rng = np.random.default_rng(600)
+    x = random_mat(rng, R, f, 2)
+    w = rng.integers(-(1 << 14), 1 << 14, size=(f, cols), dtype=np.int64)
+    b = rng.integers(-100, 101, size=cols)
+    want, _ = o.baseline_matmul(x, w, b)
+    for env in ({"HEI_BL_ACCUM_W": "0"}, {"HEI_BL_ACCUM_W": "1", "HEI_BL_SPLIT": "1"},
+                {"HEI_BL_ACCUM_W": "1", "HEI_BL_SPLIT": "3"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s = gpu_server_from(o, with_pk=True)
+        got, _ = baseline_matmul(s, x, w, b, Prng(16), Prng(17))
+        assert np.array_equal(got, want), env
+    assert np.array_equal(o.unpack_baseline(want, R, cols), oracle_matmul(x, w, b))
+
+
 def test_baseline_equals_fast_algorithm(tiny32):
     """test_matmul.cpp:258-291: baseline == proposed == integer oracle."""
     from paper_2204_05496_b200 import EncodedWeights, Prng, baseline_matmul, matmul
@@ -961,15 +986,19 @@ def test_split_key_switch_latency_path(prod, monkeypatch):
 
 def test_n16384_full_batch_tmem_key_switch(monkeypatch):
     """C5's ring at full-batch launch sizes (60 ciphertexts = 600 blocks, not
-    fused): the TMEM-accumulator key switch (1024 threads, 256 TMEM columns)
-    equals the shared-memory kernel and the oracle."""
+    fused): the half-ring key switch (two 512-thread blocks per (pair, prime),
+    ks_half.cuh), the TMEM-accumulator kernel (1024 threads, 256 TMEM
+    columns) and the shared-memory kernel all equal the oracle."""
     o = Oracle(production_params(16384), key_seed=5, enc_seed=6)
     rng = np.random.default_rng(60)
     x = rng.integers(-9, 9, size=(60, o.n), dtype=np.int64)
     cts = o.encode_inputs(x)[:, 0, :]
     got = {}
-    for v in ("1", "0"):
-        monkeypatch.setenv("HEI_KS14_TMEM", v)
+    for v, env in (("half", ("1", "1")), ("1", ("0", "1")), ("0", ("0", "0"))):
+        monkeypatch.setenv("HEI_KS14_HALF", env[0])
+        monkeypatch.setenv("HEI_KS14_TMEM", env[1])
         got[v] = gpu_server_from(o).sum_all_slots(cts)
     assert np.array_equal(got["1"], got["0"])
-    assert np.array_equal(got["1"][59], o.sum_all_slots(cts[59]))
+    assert np.array_equal(got["half"], got["0"])
+    for r in (0, 59):
+        assert np.array_equal(got["half"][r], o.sum_all_slots(cts[r])), r
