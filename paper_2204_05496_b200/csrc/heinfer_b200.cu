@@ -228,6 +228,8 @@ struct Geo {
   const uint2* fwdh;    // [P][2][N/2]
   const uint4* twch;    // [P][2][twch_stride]
   uint32_t twch_stride;
+  const uint2* invh;    // inverse counterparts (k_rot_digits_h)
+  const uint4* itwch;
 };
 // (pair, prime) of this block, for grids of pairs * P blocks
 __device__ __forceinline__ void block_pair_prime(const Geo& g, uint32_t& pair, uint32_t& gp) {
@@ -337,6 +339,9 @@ struct hei_gpu_ctx {
   uint2* d_fwdh = nullptr;  // N = 16384 half-ring tables (ks_half.cuh)
   uint4* d_twch = nullptr;
   std::vector<uint2> h_fwdh;
+  uint2* d_invh = nullptr;
+  uint4* d_itwch = nullptr;
+  std::vector<uint2> h_invh;
   uint4 *d_twc32 = nullptr, *d_itwc32 = nullptr;
   uint32_t* d_index = nullptr;
   // galois elements in fold order: steps 1, 2, ..., n/4, then the swap
@@ -406,6 +411,7 @@ struct hei_gpu_ctx {
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
+  bool dig14_half = true;  // HEI_DIG14_HALF=0: N = 16384 full-batch digits use the 1024-thread kernel
   bool ks14_half = true;  // HEI_KS14_HALF=0: N = 16384 full batches use the 1024-thread TMEM kernel
   bool ks14_tmem = true;  // HEI_KS14_TMEM=0: N = 16384 full batches keep the shared-memory accumulators
   int bl_split = 1;        // HEI_BL_SPLIT: feature slices per k_bl_accum_w launch (accumulator copies)
@@ -574,13 +580,14 @@ const TwAB* tabs_of(hei_gpu_ctx* c, const Geo& g, int inverse) {
 }
 
 // Pass-A/B rows of the N = 16384 half-ring tables (half h) for the primes of `g`.
-const TwAB* tabs_half(hei_gpu_ctx* c, const Geo& g, uint32_t h) {
+const TwAB* tabs_half(hei_gpu_ctx* c, const Geo& g, uint32_t h, int inverse = 0) {
   thread_local TwAB t;
   for (uint32_t k = 0; k < g.P && k < (uint32_t)kMaxAB; ++k) {
     uint32_t src = 0;
     for (uint32_t m = 0; m < c->geo.P; ++m)
       if (c->geo.pr[m].q == g.pr[k].q) src = m;
-    std::memcpy(t.w[k], c->h_fwdh.data() + ((size_t)src * 2 + h) * (c->n / 2), 256 * sizeof(uint2));
+    std::memcpy(t.w[k], (inverse ? c->h_invh : c->h_fwdh).data() + ((size_t)src * 2 + h) * (c->n / 2),
+                256 * sizeof(uint2));
   }
   return &t;
 }
@@ -621,6 +628,16 @@ void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint
   // big launches take the pass-A/B twiddles as parameters (constant bank);
   // small ones keep the 25 KB parameter block off the launch path
   const bool ptw = blocks >= 2u * 148u;
+  if (c->logn == 14 && c->dig14_half && ptw && c->d_itwch && !use_ntt32(c, blocks)) {
+    // 2-CTA clusters, one per half of the eval slots (ks_half.cuh); the two
+    // halves of a launch need different pass-A/B rows, so both read them
+    // from global memory (PTW = false)
+    HEI_DISPATCH(c->logn,
+                 (k_rot_digits_h<false><<<2 * blocks, 512, 8192 * 4, st>>>(g, cur, perm, dig, TwNone{})),
+                 (void)0);
+    LAUNCHED();
+    return;
+  }
   if (use_ntt32(c, blocks)) {
     if (c->logn == 14) {
       if (ptw) k_rot_digits32<14, true><<<blocks, Ntt32<14>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1));
@@ -1755,6 +1772,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_PRIME_MAJOR")) c->prime_major = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_KS14_TMEM")) c->ks14_tmem = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_KS14_HALF")) c->ks14_half = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_DIG14_HALF")) c->dig14_half = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DOT_ROWS")) c->dot_rows = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_CACHE")) c->mask_cache = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_BIG")) c->fuse_big = std::atoi(v) != 0;
@@ -1940,19 +1958,23 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     }
     // N = 16384 half-ring tables (ks_half.cuh): half h's stage s' block i'
     // uses zetas[2^(s'+1) + h 2^s' + i'], stored at local index 2^s' + i'
-    std::vector<uint4> twch;
+    std::vector<uint4> twch, itwch;
     if (c->logn == 14) {
       const uint32_t nh = n / 2, T = nh / 16, KC = 8;  // Ntt<13>: XST = 1, PAD = 0
       g.twch_stride = KC * T;
       c->h_fwdh.assign((size_t)P * 2 * nh, make_uint2(0, 0));
+      c->h_invh.assign((size_t)P * 2 * nh, make_uint2(0, 0));
       twch.resize((size_t)P * 2 * KC * T);
+      itwch.resize(twch.size());
       std::vector<uint32_t> idx(2 * KC);
       for (uint32_t row = 0; row < P; ++row)
         for (uint32_t h = 0; h < 2; ++h) {
           uint2* loc = c->h_fwdh.data() + ((size_t)row * 2 + h) * nh;
+          uint2* iloc = c->h_invh.data() + ((size_t)row * 2 + h) * nh;
           for (uint32_t k = 1; k < nh; ++k) {
             const uint32_t m = 1u << (31 - __builtin_clz(k));
             loc[k] = fwd[(size_t)row * n + 2 * m + h * m + (k - m)];
+            iloc[k] = inv[(size_t)row * n + 2 * m + h * m + (k - m)];
           }
           for (uint32_t j = 0; j < T; ++j) {
             const uint32_t x0 = 16 * j;
@@ -1963,6 +1985,8 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
             for (uint32_t k = 0; k < KC; ++k) {
               const uint2 a = loc[idx[2 * k]], b2 = loc[idx[2 * k + 1]];
               twch[(((size_t)row * 2 + h) * KC + k) * T + j] = make_uint4(a.x, a.y, b2.x, b2.y);
+              const uint2 ia = iloc[idx[2 * k]], ib = iloc[idx[2 * k + 1]];
+              itwch[(((size_t)row * 2 + h) * KC + k) * T + j] = make_uint4(ia.x, ia.y, ib.x, ib.y);
             }
           }
         }
@@ -2010,6 +2034,14 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
       CU(cudaStreamSynchronize(c->stream));
       g.twch = c->d_twch;
       g.fwdh = c->d_fwdh;
+      CU(cudaMalloc(&c->d_itwch, itwch.size() * sizeof(uint4)));
+      CU(cudaMalloc(&c->d_invh, c->h_invh.size() * sizeof(uint2)));
+      CU(cudaMemcpyAsync(c->d_itwch, itwch.data(), itwch.size() * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
+      CU(cudaMemcpyAsync(c->d_invh, c->h_invh.data(), c->h_invh.size() * sizeof(uint2), cudaMemcpyHostToDevice,
+                         c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      g.itwch = c->d_itwch;
+      g.invh = c->d_invh;
     }
     if (!twc.empty()) {
       CU(cudaMalloc(&c->d_twc, twc.size() * sizeof(uint4)));
@@ -2074,6 +2106,8 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->d_twc);
   cudaFree(c->d_twch);
   cudaFree(c->d_fwdh);
+  cudaFree(c->d_itwch);
+  cudaFree(c->d_invh);
   cudaFree(c->d_itwc);
   cudaFree(c->d_twc32);
   cudaFree(c->d_mask_table);
@@ -3019,6 +3053,8 @@ int hei_gpu_apply_galois(hei_gpu_ctx* c, uint32_t b, uint64_t elt, const uint64_
     if (g.twch) {
       gb.twch = g.twch + (size_t)(b ? c->L[0] : 0) * 2 * g.twch_stride;
       gb.fwdh = g.fwdh + (size_t)(b ? c->L[0] : 0) * 2 * (n / 2);
+      gb.itwch = g.itwch + (size_t)(b ? c->L[0] : 0) * 2 * g.twch_stride;
+      gb.invh = g.invh + (size_t)(b ? c->L[0] : 0) * 2 * (n / 2);
     }
     const size_t words = 2ull * L * n;
     std::vector<uint32_t> h32(words);

@@ -165,3 +165,57 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_h(Geo g, const uint32_
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols) : "memory");
   }
 }
+
+// N = 16384 digit INTT as a 2-CTA cluster, one CTA per half of the eval
+// slots (the counterpart of k_rot_keyswitch_h; same arithmetic as
+// k_rot_digits_f, context.cpp:445-470). The inverse transform's stages with
+// m >= 2 blocks stay inside a half, with inv_zetas[2^(s'+1) + h 2^s' + i']
+// at local index 2^s' + i' (the half tables `itwh`); Ntt<13>::inv runs them
+// with its n^-1 fold replaced by 1. The last stage (m = 1) pairs local
+// coefficient x of both halves: each CTA publishes its half in shared
+// memory, reads its partner's through distributed shared memory, and writes
+// its own output half: (U + V) n^-1 for half 0, (U - V) inv_zetas[1] n^-1 for
+// half 1 — the digit comes out finished, exactly as k_rot_digits_f<14>'s.
+template <bool PTW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 3)
+    k_rot_digits_h(Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ perm,
+                   uint32_t* __restrict__ digits, const __grid_constant__ TwArg<PTW> itab) {
+  using NT = Ntt<13>;
+  constexpr uint32_t NF = 16384, NH = 8192;
+  extern __shared__ uint4 smem4[];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t h = cl.block_rank();
+  const uint32_t blk = blockIdx.x >> 1, pair = blk / g.P, gp = blk % g.P;
+  const PrimeInfo& pr = g.pr[gp];
+  const uint32_t q = pr.q, j = threadIdx.x;
+  const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * NF;
+  const uint32_t x0 = h * NH + NT::posC0(j);
+  uint32_t pm[16], e[16];
+  load16_ro(perm + x0, pm);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) e[r] = __ldg(c1 + pm[r]);
+  const uint2* itn = g.invh + ((size_t)gp * 2 + h) * NH;
+  const uint4* itc = g.itwch + ((size_t)gp * 2 + h) * g.twch_stride;
+  const uint2 lastH = __ldg(itn + 1);                               // local last stage: inv_zetas[2 + h]
+  const uint2 one = make_uint2(1u, (uint32_t)(0x100000000ull / q));  // Shoup constant of 1: a plain reduction
+  if constexpr (PTW)
+    NT::inv(e, sm, ParamTw{itab.w[gp]}, itc, q, lastH, one);
+  else
+    NT::inv(e, sm, itn, itc, q, lastH, one);
+  __syncthreads();  // the transform's last shared reads are done
+#pragma unroll
+  for (int r = 0; r < 16; ++r) sm[NT::posA(j, r)] = e[r];
+  cl.sync();
+  const uint32_t* peer = cl.map_shared_rank(sm, h ^ 1u);
+  uint32_t* d = digits + ((uint64_t)pair * g.P + gp) * NF + h * NH;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const uint32_t x = NT::posA(j, r);
+    const uint32_t o = peer[x];
+    // U = half 0's value, V = half 1's at local coefficient x
+    d[x] = h ? mul_shoup(o - e[r] + q, pr.last.x, pr.last.y, q) : mul_shoup(e[r] + o, pr.ninv.x, pr.ninv.y, q);
+  }
+  cl.sync();  // the partner has finished reading this CTA's shared memory
+}

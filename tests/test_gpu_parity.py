@@ -987,18 +987,20 @@ def test_split_key_switch_latency_path(prod, monkeypatch):
 def test_n16384_full_batch_tmem_key_switch(monkeypatch):
     """C5's ring at full-batch launch sizes (60 ciphertexts = 600 blocks, not
     fused): the half-ring key switch (two 512-thread blocks per (pair, prime),
-    ks_half.cuh), the TMEM-accumulator kernel (1024 threads, 256 TMEM
+    ks_half.cuh) with the 2-CTA-cluster digit INTT or the 1024-thread one,
+    the TMEM-accumulator kernel (1024 threads, 256 TMEM
     columns) and the shared-memory kernel all equal the oracle."""
     o = Oracle(production_params(16384), key_seed=5, enc_seed=6)
     rng = np.random.default_rng(60)
     x = rng.integers(-9, 9, size=(60, o.n), dtype=np.int64)
     cts = o.encode_inputs(x)[:, 0, :]
     got = {}
-    for v, env in (("half", ("1", "1")), ("1", ("0", "1")), ("0", ("0", "0"))):
+    for v, env in (("half", "111"), ("half_ks", "110"), ("1", "010"), ("0", "000")):
         monkeypatch.setenv("HEI_KS14_HALF", env[0])
         monkeypatch.setenv("HEI_KS14_TMEM", env[1])
+        monkeypatch.setenv("HEI_DIG14_HALF", env[2])
         got[v] = gpu_server_from(o).sum_all_slots(cts)
-    assert np.array_equal(got["1"], got["0"])
-    assert np.array_equal(got["half"], got["0"])
+    for v in ("1", "half", "half_ks"):
+        assert np.array_equal(got[v], got["0"]), v
     for r in (0, 59):
         assert np.array_equal(got["half"][r], o.sum_all_slots(cts[r])), r
