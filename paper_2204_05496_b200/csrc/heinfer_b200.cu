@@ -411,6 +411,7 @@ struct hei_gpu_ctx {
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
+  bool half13 = false;     // HEI_HALF13=1: N = 8192 full batches as 256-thread half-ring blocks (ks_half.cuh)
   bool dig14_half = true;  // HEI_DIG14_HALF=0: N = 16384 full-batch digits use the 1024-thread kernel
   bool ks14_half = true;  // HEI_KS14_HALF=0: N = 16384 full batches use the 1024-thread TMEM kernel
   bool ks14_tmem = true;  // HEI_KS14_TMEM=0: N = 16384 full batches keep the shared-memory accumulators
@@ -628,6 +629,13 @@ void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint
   // big launches take the pass-A/B twiddles as parameters (constant bank);
   // small ones keep the 25 KB parameter block off the launch path
   const bool ptw = blocks >= 2u * 148u;
+  if (c->logn == 13 && c->half13 && ptw && c->d_itwch && !use_ntt32(c, blocks)) {  // 256-thread halves
+    HEI_DISPATCH(c->logn,
+                 (k_rot_digits_h<false, 13><<<2 * blocks, 256, 4096 * 4, st>>>(g, cur, perm, dig, TwNone{})),
+                 (void)0);
+    LAUNCHED();
+    return;
+  }
   if (c->logn == 14 && c->dig14_half && ptw && c->d_itwch && !use_ntt32(c, blocks)) {
     // 2-CTA clusters, one per half of the eval slots (ks_half.cuh); the two
     // halves of a launch need different pass-A/B rows, so both read them
@@ -703,6 +711,14 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
     else
       launch_ks_c2<LG, false>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, nullptr, nullptr);
     return;
+  }
+  if constexpr (LG == 13) {
+    if (c->half13 && !dig_next && big && c->d_twch) {  // two 256-thread half-ring blocks, 6 CTAs/SM
+      for (uint32_t h = 0; h < 2; ++h)
+        k_rot_keyswitch_h<true, 13><<<blocks, 256, 4096 * 4, st>>>(g, cur, dig, perm, k0, k1, out, fold, h,
+                                                                    *tabs_half(c, g, h));
+      return;
+    }
   }
   if constexpr (LG == 14) {
     if (c->ks14_half && !dig_next && big && c->d_twch) {  // two 512-thread half-ring blocks, 3 CTAs/SM
@@ -1772,6 +1788,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_PRIME_MAJOR")) c->prime_major = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_KS14_TMEM")) c->ks14_tmem = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_KS14_HALF")) c->ks14_half = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_HALF13")) c->half13 = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DIG14_HALF")) c->dig14_half = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DOT_ROWS")) c->dot_rows = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_CACHE")) c->mask_cache = std::atoi(v) != 0;
@@ -1959,8 +1976,9 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     // N = 16384 half-ring tables (ks_half.cuh): half h's stage s' block i'
     // uses zetas[2^(s'+1) + h 2^s' + i'], stored at local index 2^s' + i'
     std::vector<uint4> twch, itwch;
-    if (c->logn == 14) {
-      const uint32_t nh = n / 2, T = nh / 16, KC = 8;  // Ntt<13>: XST = 1, PAD = 0
+    if (c->logn == 14 || c->logn == 13) {
+      const uint32_t hl = c->logn - 1, nh = n / 2, T = nh / 16, XST = hl - 12, PAD = XST % 2 == 0 ? 1 : 0,
+                     KC = (PAD + XST + 16) / 2;  // Ntt<hl>'s pass-C layout
       g.twch_stride = KC * T;
       c->h_fwdh.assign((size_t)P * 2 * nh, make_uint2(0, 0));
       c->h_invh.assign((size_t)P * 2 * nh, make_uint2(0, 0));
@@ -1978,10 +1996,11 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
           }
           for (uint32_t j = 0; j < T; ++j) {
             const uint32_t x0 = 16 * j;
-            uint32_t e = 0;
-            idx[e++] = (1u << 8) + (x0 >> 5);  // the cross-thread stage (logn 13)
+            std::fill(idx.begin(), idx.end(), 0u);
+            uint32_t e = PAD;
+            for (uint32_t st = 0; st < XST; ++st) idx[e++] = (1u << (8 + st)) + (x0 >> (hl - 8 - st));
             for (uint32_t st = 0; st < 4; ++st)
-              for (uint32_t b2 = 0; b2 < (1u << st); ++b2) idx[e++] = (1u << (13 - 4 + st)) + (x0 >> (4 - st)) + b2;
+              for (uint32_t b2 = 0; b2 < (1u << st); ++b2) idx[e++] = (1u << (hl - 4 + st)) + (x0 >> (4 - st)) + b2;
             for (uint32_t k = 0; k < KC; ++k) {
               const uint2 a = loc[idx[2 * k]], b2 = loc[idx[2 * k + 1]];
               twch[(((size_t)row * 2 + h) * KC + k) * T + j] = make_uint4(a.x, a.y, b2.x, b2.y);

@@ -22,16 +22,18 @@
 // Textually included by heinfer_b200.cu after tmem_ks.cuh.
 #pragma once
 
-template <bool PTW>
-__global__ void __launch_bounds__(512, 3) k_rot_keyswitch_h(Geo g, const uint32_t* __restrict__ dot,
+// LOGF = 14 (C5: 512-thread halves, 3 CTAs/SM) or 13 (256-thread halves,
+// 6 CTAs/SM; measured against the 512-thread full-ring kernel).
+template <bool PTW, int LOGF = 14>
+__global__ void __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6) k_rot_keyswitch_h(Geo g, const uint32_t* __restrict__ dot,
                                                            const uint32_t* __restrict__ digits,
                                                            const uint32_t* __restrict__ perm,
                                                            const uint2* __restrict__ key0,
                                                            const uint2* __restrict__ key1,
                                                            uint32_t* __restrict__ out, int fold, uint32_t h,
                                                            const __grid_constant__ TwArg<PTW> tab) {
-  using NT = Ntt<13>;
-  constexpr uint32_t NF = 16384, NH = 8192, T = 512, TF = 1024;
+  using NT = Ntt<LOGF - 1>;
+  constexpr uint32_t NF = 1u << LOGF, NH = NF / 2, T = NH / 16, TF = NF / 16;
   constexpr uint32_t kTmemCols = T / 4;
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
@@ -176,12 +178,12 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_h(Geo g, const uint32_
 // memory, reads its partner's through distributed shared memory, and writes
 // its own output half: (U + V) n^-1 for half 0, (U - V) inv_zetas[1] n^-1 for
 // half 1 — the digit comes out finished, exactly as k_rot_digits_f<14>'s.
-template <bool PTW>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 3)
+template <bool PTW, int LOGF = 14>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6)
     k_rot_digits_h(Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ perm,
                    uint32_t* __restrict__ digits, const __grid_constant__ TwArg<PTW> itab) {
-  using NT = Ntt<13>;
-  constexpr uint32_t NF = 16384, NH = 8192;
+  using NT = Ntt<LOGF - 1>;
+  constexpr uint32_t NF = 1u << LOGF, NH = NF / 2;
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
   namespace cg = cooperative_groups;
