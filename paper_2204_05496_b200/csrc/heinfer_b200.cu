@@ -413,7 +413,8 @@ struct hei_gpu_ctx {
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   bool half13 = false;     // HEI_HALF13=1: N = 8192 full batches as 256-thread half-ring blocks (ks_half.cuh)
   bool dig14_half = true;  // HEI_DIG14_HALF=0: N = 16384 full-batch digits use the 1024-thread kernel
-  bool ks14_half = true;  // HEI_KS14_HALF=0: N = 16384 full batches use the 1024-thread TMEM kernel
+  int ks14_half = 2;  // HEI_KS14_HALF: N = 16384 full-batch key switch as half-ring blocks (2: one launch per
+                     // branch with both halves side by side; 1: one launch per half; 0: the 1024-thread kernel)
   bool ks14_tmem = true;  // HEI_KS14_TMEM=0: N = 16384 full batches keep the shared-memory accumulators
   int bl_split = 1;        // HEI_BL_SPLIT: feature slices per k_bl_accum_w launch (accumulator copies)
   bool bl_accum_w = true;  // HEI_BL_ACCUM_W: standard-algorithm sums with exact 64-bit products (k_bl_accum_w)
@@ -593,6 +594,20 @@ const TwAB* tabs_half(hei_gpu_ctx* c, const Geo& g, uint32_t h, int inverse = 0)
   return &t;
 }
 
+// Rows [k][h] (k < np) of the half-ring forward tables for primes gp0.. of `g`.
+const TwAB* tabs_half_pairs(hei_gpu_ctx* c, const Geo& g, uint32_t gp0, uint32_t np) {
+  thread_local TwAB t;
+  if (2 * np > (uint32_t)kMaxAB) raise(HEI_INTERNAL, "half-ring parameter rows exceed the table");
+  for (uint32_t k = 0; k < np; ++k) {
+    uint32_t src = 0;
+    for (uint32_t m = 0; m < c->geo.P; ++m)
+      if (c->geo.pr[m].q == g.pr[gp0 + k].q) src = m;
+    for (uint32_t h = 0; h < 2; ++h)
+      std::memcpy(t.w[2 * k + h], c->h_fwdh.data() + ((size_t)src * 2 + h) * (c->n / 2), 256 * sizeof(uint2));
+  }
+  return &t;
+}
+
 // The 32-residue transforms (ntt32.cuh) serve every N = 16384 fold when
 // HEI_NTT32 >= 1 and N = 8192 full batches when HEI_NTT32 = 2.
 bool use_ntt32(hei_gpu_ctx* c, unsigned blocks) {
@@ -715,16 +730,25 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
   if constexpr (LG == 13) {
     if (c->half13 && !dig_next && big && c->d_twch) {  // two 256-thread half-ring blocks, 6 CTAs/SM
       for (uint32_t h = 0; h < 2; ++h)
-        k_rot_keyswitch_h<true, 13><<<blocks, 256, 4096 * 4, st>>>(g, cur, dig, perm, k0, k1, out, fold, h,
+        k_rot_keyswitch_h<true, 13><<<blocks, 256, 4096 * 4, st>>>(g, cur, dig, perm, k0, k1, out, fold, h, 0, 0,
                                                                     *tabs_half(c, g, h));
       return;
     }
   }
   if constexpr (LG == 14) {
     if (c->ks14_half && !dig_next && big && c->d_twch) {  // two 512-thread half-ring blocks, 3 CTAs/SM
-      for (uint32_t h = 0; h < 2; ++h)
-        k_rot_keyswitch_h<true><<<blocks, 512, 8192 * 4, st>>>(g, cur, dig, perm, k0, k1, out, fold, h,
-                                                                *tabs_half(c, g, h));
+      if (c->ks14_half == 2) {  // one launch per branch, the halves of a (pair, prime) adjacent
+        const uint32_t pairs = blocks / g.P;
+        for (uint32_t b = 0, gp0 = 0; b < 2; gp0 += g.L[b], ++b) {
+          if (!g.L[b]) continue;
+          k_rot_keyswitch_h<true><<<pairs * g.L[b] * 2, 512, 8192 * 4, st>>>(
+              g, cur, dig, perm, k0, k1, out, fold, 2, gp0, g.L[b], *tabs_half_pairs(c, g, gp0, g.L[b]));
+        }
+      } else {
+        for (uint32_t h = 0; h < 2; ++h)
+          k_rot_keyswitch_h<true><<<blocks, 512, 8192 * 4, st>>>(g, cur, dig, perm, k0, k1, out, fold, h, 0, 0,
+                                                                  *tabs_half(c, g, h));
+      }
       return;
     }
     if (c->ks14_tmem && !dig_next) {  // TMEM accumulators (256 columns), 1 CTA of 1024 threads per SM
@@ -1787,7 +1811,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_ENC_MINB")) c->enc_minb = std::atoi(v);
     if (const char* v = std::getenv("HEI_PRIME_MAJOR")) c->prime_major = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_KS14_TMEM")) c->ks14_tmem = std::atoi(v) != 0;
-    if (const char* v = std::getenv("HEI_KS14_HALF")) c->ks14_half = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_KS14_HALF")) c->ks14_half = std::atoi(v);
     if (const char* v = std::getenv("HEI_HALF13")) c->half13 = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DIG14_HALF")) c->dig14_half = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DOT_ROWS")) c->dot_rows = std::atoi(v) != 0;

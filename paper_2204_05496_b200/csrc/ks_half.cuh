@@ -30,7 +30,8 @@ __global__ void __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6) k_rot_k
                                                            const uint32_t* __restrict__ perm,
                                                            const uint2* __restrict__ key0,
                                                            const uint2* __restrict__ key1,
-                                                           uint32_t* __restrict__ out, int fold, uint32_t h,
+                                                           uint32_t* __restrict__ out, int fold, uint32_t hsel,
+                                                           uint32_t gp0, uint32_t np,
                                                            const __grid_constant__ TwArg<PTW> tab) {
   using NT = Ntt<LOGF - 1>;
   constexpr uint32_t NF = 1u << LOGF, NH = NF / 2, T = NH / 16, TF = NF / 16;
@@ -38,7 +39,24 @@ __global__ void __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6) k_rot_k
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
   __shared__ uint32_t tbase;
-  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  // hsel < 2: this launch covers half hsel of every (pair, prime), blockIdx =
+  // pair * P + prime. hsel == 2: both halves of primes [gp0, gp0 + np) with
+  // blockIdx = (pair * np + prime - gp0) * 2 + h, so the two halves of a
+  // (pair, prime) run side by side and the second digit read hits L2; the
+  // parameter rows are then [prime - gp0][h].
+  uint32_t pair, gp, h, row;
+  if (hsel < 2) {
+    pair = blockIdx.x / g.P;
+    gp = blockIdx.x % g.P;
+    h = hsel;
+    row = gp;
+  } else {
+    const uint32_t loc = blockIdx.x >> 1;
+    h = blockIdx.x & 1u;
+    pair = loc / np;
+    gp = gp0 + loc % np;
+    row = (loc % np) * 2 + h;
+  }
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t q = pr.q, L = pr.L, i = pr.i;
   const uint32_t j = threadIdx.x, warp = j >> 5;
@@ -106,7 +124,7 @@ __global__ void __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6) k_rot_k
       e[r] = h ? sub_mod(u, t, q) : add_mod(u, t, q);
     }
     if constexpr (PTW)
-      NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
+      NT::template fwd<true>(e, sm, ParamTw{tab.w[row]}, twc, q);
     else
       NT::template fwd<true>(e, sm, twn, twc, q);
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * NF) + jf;
