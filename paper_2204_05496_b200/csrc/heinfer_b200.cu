@@ -412,7 +412,8 @@ struct hei_gpu_ctx {
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   bool half13 = false;     // HEI_HALF13=1: N = 8192 full batches as 256-thread half-ring blocks (ks_half.cuh)
-  bool dig14_half = true;  // HEI_DIG14_HALF=0: N = 16384 full-batch digits use the 1024-thread kernel
+  int dig14_half = 1;  // HEI_DIG14_HALF: N = 16384 full-batch digits as 2-CTA clusters (2: c1 staged by TMA
+                      // across the cluster; 0: the 1024-thread kernel)
   int ks14_half = 2;  // HEI_KS14_HALF: N = 16384 full-batch key switch as half-ring blocks (2: one launch per
                      // branch with both halves side by side; 1: one launch per half; 0: the 1024-thread kernel)
   bool ks14_tmem = true;  // HEI_KS14_TMEM=0: N = 16384 full batches keep the shared-memory accumulators
@@ -646,7 +647,7 @@ void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint
   const bool ptw = blocks >= 2u * 148u;
   if (c->logn == 13 && c->half13 && ptw && c->d_itwch && !use_ntt32(c, blocks)) {  // 256-thread halves
     HEI_DISPATCH(c->logn,
-                 (k_rot_digits_h<false, 13><<<2 * blocks, 256, 4096 * 4, st>>>(g, cur, perm, dig, TwNone{})),
+                 (k_rot_digits_h<false, 13><<<2 * blocks, 256, 4096 * 4, st>>>(g, cur, perm, dig, 0, TwNone{})),
                  (void)0);
     LAUNCHED();
     return;
@@ -656,7 +657,8 @@ void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint
     // halves of a launch need different pass-A/B rows, so both read them
     // from global memory (PTW = false)
     HEI_DISPATCH(c->logn,
-                 (k_rot_digits_h<false><<<2 * blocks, 512, 8192 * 4, st>>>(g, cur, perm, dig, TwNone{})),
+                 (k_rot_digits_h<false><<<2 * blocks, 512, 8192 * 4, st>>>(g, cur, perm, dig, c->dig14_half == 2,
+                                                                           TwNone{})),
                  (void)0);
     LAUNCHED();
     return;
@@ -1813,7 +1815,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_KS14_TMEM")) c->ks14_tmem = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_KS14_HALF")) c->ks14_half = std::atoi(v);
     if (const char* v = std::getenv("HEI_HALF13")) c->half13 = std::atoi(v) != 0;
-    if (const char* v = std::getenv("HEI_DIG14_HALF")) c->dig14_half = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_DIG14_HALF")) c->dig14_half = std::atoi(v);
     if (const char* v = std::getenv("HEI_DOT_ROWS")) c->dot_rows = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_CACHE")) c->mask_cache = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_BIG")) c->fuse_big = std::atoi(v) != 0;

@@ -199,7 +199,7 @@ __global__ void __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6) k_rot_k
 template <bool PTW, int LOGF = 14>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6)
     k_rot_digits_h(Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ perm,
-                   uint32_t* __restrict__ digits, const __grid_constant__ TwArg<PTW> itab) {
+                   uint32_t* __restrict__ digits, int stage, const __grid_constant__ TwArg<PTW> itab) {
   using NT = Ntt<LOGF - 1>;
   constexpr uint32_t NF = 1u << LOGF, NH = NF / 2;
   extern __shared__ uint4 smem4[];
@@ -213,9 +213,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1u << LOGF) / 32, L
   const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * NF;
   const uint32_t x0 = h * NH + NT::posC0(j);
   uint32_t pm[16], e[16];
-  load16_ro(perm + x0, pm);
+  if (stage) {
+    // each CTA stages its half of c1 with one TMA bulk copy; the Galois
+    // gather then reads the cluster's shared memory (a thread's 16 sources
+    // lie in one aligned 16-slot group, so in one CTA's half)
+    __shared__ uint64_t bar;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      bulk_load(sm, c1 + h * NH, NH * 4, &bar);
+    }
+    load16_ro(perm + x0, pm);
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    cl.sync();  // both halves staged
+    const uint32_t* src = cl.map_shared_rank(sm, pm[0] / NH);
 #pragma unroll
-  for (int r = 0; r < 16; ++r) e[r] = __ldg(c1 + pm[r]);
+    for (int r = 0; r < 16; ++r) e[r] = src[pm[r] % NH];
+    cl.sync();  // every gather of this CTA's half is done before the transform reuses it
+  } else {
+    load16_ro(perm + x0, pm);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = __ldg(c1 + pm[r]);
+  }
   const uint2* itn = g.invh + ((size_t)gp * 2 + h) * NH;
   const uint4* itc = g.itwch + ((size_t)gp * 2 + h) * g.twch_stride;
   const uint2 lastH = __ldg(itn + 1);                               // local last stage: inv_zetas[2 + h]

@@ -997,12 +997,13 @@ def test_n16384_full_batch_tmem_key_switch(monkeypatch):
     x = rng.integers(-9, 9, size=(60, o.n), dtype=np.int64)
     cts = o.encode_inputs(x)[:, 0, :]
     got = {}
-    for v, env in (("half", "211"), ("half1", "111"), ("half_ks", "210"), ("1", "010"), ("0", "000")):
+    for v, env in (("half", "211"), ("half1", "111"), ("half_st", "212"), ("half_ks", "210"), ("1", "010"),
+                   ("0", "000")):
         monkeypatch.setenv("HEI_KS14_HALF", env[0])
         monkeypatch.setenv("HEI_KS14_TMEM", env[1])
         monkeypatch.setenv("HEI_DIG14_HALF", env[2])
         got[v] = gpu_server_from(o).sum_all_slots(cts)
-    for v in ("1", "half", "half1", "half_ks"):
+    for v in ("1", "half", "half1", "half_st", "half_ks"):
         assert np.array_equal(got[v], got["0"]), v
     for r in (0, 59):
         assert np.array_equal(got["half"][r], o.sum_all_slots(cts[r])), r
