@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digi
     // the whole c1 polynomial lands in shared memory with one TMA bulk copy;
     // the Galois gather then reads shared memory instead of scattered L1/L2
     __shared__ uint64_t bar;
-    uint32_t* stg = sm + NT::N;
+    uint32_t* stg = tma == 2 ? sm : sm + NT::N;  // 2: staged in the exchange buffer itself
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
       bulk_load(stg, c1, NT::N * 4, &bar);

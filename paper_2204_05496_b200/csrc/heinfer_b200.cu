@@ -428,7 +428,7 @@ struct hei_gpu_ctx {
   uint32_t* d_mask_table = nullptr;  // [slot][P][N] mask plaintexts, built on first full-batch use
   bool e2e_overlap = true;  // HEI_E2E_OVERLAP=0: host-buffer chunks run one after another
   std::vector<cudaStream_t> chunk_streams;  // 2 x fold_parts streams: consecutive chunks overlap
-  int dig_tma = 1;       // HEI_DIG_TMA=0: digit kernel gathers c1 from global memory
+  int dig_tma = 2;       // HEI_DIG_TMA: 2 c1 staged by TMA in the exchange buffer; 1 in a second buffer; 0 gathered from global
   int lat_tma = 0;       // HEI_LAT_TMA=1: latency-path key switch prefetches digits with TMA (measured slower)
   uint64_t mt_chunks_max = 128;   // HEI_MT_CHUNKS: parallel mt19937_64 generators per branch
   struct FoldGraph {
@@ -641,7 +641,9 @@ void launch_bl_encrypt(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const int8
 }
 void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* perm,
                        uint32_t* dig, cudaStream_t st) {
-  const size_t sm = smem_bytes(c, 1), smf = smem_bytes(c, c->dig_tma ? 2 : 1);
+  // dig_tma 2: the staged c1 shares the exchange buffer (the transform's
+  // first barrier orders every gather read before its first store)
+  const size_t sm = smem_bytes(c, 1), smf = smem_bytes(c, c->dig_tma == 1 ? 2 : 1);
   // big launches take the pass-A/B twiddles as parameters (constant bank);
   // small ones keep the 25 KB parameter block off the launch path
   const bool ptw = blocks >= 2u * 148u;
@@ -739,7 +741,8 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
   }
   if constexpr (LG == 14) {
     if (c->ks14_half && !dig_next && big && c->d_twch) {  // two 512-thread half-ring blocks, 3 CTAs/SM
-      if (c->ks14_half == 2) {  // one launch per branch, the halves of a (pair, prime) adjacent
+      if (c->ks14_half == 2 && 2 * std::max(g.L[0], g.L[1]) <= (uint32_t)kMaxAB) {
+        // one launch per branch, the halves of a (pair, prime) adjacent
         const uint32_t pairs = blocks / g.P;
         for (uint32_t b = 0, gp0 = 0; b < 2; gp0 += g.L[b], ++b) {
           if (!g.L[b]) continue;
@@ -1821,7 +1824,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_FUSE_BIG")) c->fuse_big = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_OVERLAP")) c->e2e_overlap = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_GROUP")) c->mask_group = std::max(1, std::atoi(v));
-    if (const char* v = std::getenv("HEI_DIG_TMA")) c->dig_tma = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_DIG_TMA")) c->dig_tma = std::atoi(v);
     if (const char* v = std::getenv("HEI_LAT_TMA")) c->lat_tma = std::atoi(v) != 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
