@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libheinfer_b200.so")
+# HEI_LIB_PATH: an alternative in-tree build of the same library (A/B timing of
+# two builds on one box); the default is the package's own lib/.
+LIB_PATH = os.environ.get("HEI_LIB_PATH") or os.path.join(HERE, "lib", "libheinfer_b200.so")
 
 HEI_OK = 0
 HEI_PARAM_ERROR = 1
