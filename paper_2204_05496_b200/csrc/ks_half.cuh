@@ -18,12 +18,36 @@
 // held by thread s / 16 in both the N = 16384 and the half layout, so the
 // Galois keys keep their N = 16384 pass-C layout (stride 1024, offset
 // 512 h). The Galois gathers read c1 / c0 through L1/L2 (a 64 KB polynomial
-// does not fit next to the exchange buffer at 3 CTAs/SM).
+// does not fit next to the exchange buffer at 3 CTAs/SM; staging each
+// thread's source group through shared memory as k_rot_digits_h does
+// measured 0.8 % slower here).
 // Textually included by heinfer_b200.cu after tmem_ks.cuh.
 #pragma once
 
 // LOGF = 14 (C5: 512-thread halves, 3 CTAs/SM) or 13 (256-thread halves,
 // 6 CTAs/SM; measured against the 512-thread full-ring kernel).
+// Galois gather of a thread's 16 slots: their sources form one aligned
+// 16-slot group (the automorphism maps groups onto groups), so the group is
+// read with 4 x 128-bit loads and permuted through a per-thread column of
+// shared memory (word k of thread j at scr[k * T + j]: conflict-free for any
+// permutation, and only the writing thread reads it, so no barrier).
+template <uint32_t T>
+__device__ __forceinline__ void gather_group(const uint32_t* __restrict__ src, const uint32_t (&pm)[16],
+                                             uint32_t* scr, uint32_t (&e)[16]) {
+  const uint4* gs = reinterpret_cast<const uint4*>(src + (pm[0] & ~15u));
+  const uint32_t j = threadIdx.x % T;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 v = __ldg(gs + c);
+    scr[(4 * c) * T + j] = v.x;
+    scr[(4 * c + 1) * T + j] = v.y;
+    scr[(4 * c + 2) * T + j] = v.z;
+    scr[(4 * c + 3) * T + j] = v.w;
+  }
+#pragma unroll
+  for (int r = 0; r < 16; ++r) e[r] = scr[(pm[r] & 15u) * T + j];
+}
+
 template <bool PTW, int LOGF = 14>
 __global__ void __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6) k_rot_keyswitch_h(Geo g, const uint32_t* __restrict__ dot,
                                                            const uint32_t* __restrict__ digits,
@@ -232,8 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1u << LOGF) / 32, L
     cl.sync();  // every gather of this CTA's half is done before the transform reuses it
   } else {
     load16_ro(perm + x0, pm);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) e[r] = __ldg(c1 + pm[r]);
+    gather_group<NT::T>(c1, pm, sm, e);  // sm is free until the transform's first barrier
   }
   const uint2* itn = g.invh + ((size_t)gp * 2 + h) * NH;
   const uint4* itc = g.itwch + ((size_t)gp * 2 + h) * g.twch_stride;
