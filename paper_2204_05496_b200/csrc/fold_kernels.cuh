@@ -483,7 +483,22 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digi
   const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * NT::N;
   const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
   uint32_t pm[16], e[16];
-  if (tma) {
+  if (tma == 3) {
+    // the 16 sources form one aligned group: 4 x 128-bit loads, permuted
+    // through a per-thread shared-memory column (conflict-free, no barrier)
+    load16_ro(perm + x0, pm);
+    const uint4* gs = reinterpret_cast<const uint4*>(c1 + (pm[0] & ~15u));
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 v = __ldg(gs + c);
+      sm[(4 * c) * NT::T + j] = v.x;
+      sm[(4 * c + 1) * NT::T + j] = v.y;
+      sm[(4 * c + 2) * NT::T + j] = v.z;
+      sm[(4 * c + 3) * NT::T + j] = v.w;
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = sm[(pm[r] & 15u) * NT::T + j];
+  } else if (tma) {
     // the whole c1 polynomial lands in shared memory with one TMA bulk copy;
     // the Galois gather then reads shared memory instead of scattered L1/L2
     __shared__ uint64_t bar;

@@ -428,7 +428,7 @@ struct hei_gpu_ctx {
   uint32_t* d_mask_table = nullptr;  // [slot][P][N] mask plaintexts, built on first full-batch use
   bool e2e_overlap = true;  // HEI_E2E_OVERLAP=0: host-buffer chunks run one after another
   std::vector<cudaStream_t> chunk_streams;  // 2 x fold_parts streams: consecutive chunks overlap
-  int dig_tma = 2;       // HEI_DIG_TMA: 2 c1 staged by TMA in the exchange buffer; 1 in a second buffer; 0 gathered from global
+  int dig_tma = 3;       // HEI_DIG_TMA: 3 c1 gathered by source group (4 x 128-bit loads, shared-memory column permute); 2 staged by TMA in the exchange buffer; 1 in a second buffer; 0 scalar global gathers
   int lat_tma = 0;       // HEI_LAT_TMA=1: latency-path key switch prefetches digits with TMA (measured slower)
   uint64_t mt_chunks_max = 128;   // HEI_MT_CHUNKS: parallel mt19937_64 generators per branch
   struct FoldGraph {

@@ -873,20 +873,21 @@ def test_full_batch_key_switch_variants_bit_exact(prod, monkeypatch):
     order (4p), keys read past L1 (9, 9p), and
     L2 bulk prefetch of the next digit (10), and the 256-thread half-ring
     key switch and 2-CTA-cluster digit INTT (4h, ks_half.cuh), and the digit
-    INTT staging c1 in its exchange buffer (4d)."""
+    INTT staging c1 in its exchange buffer (4d) or gathering it by source
+    group (4g)."""
     o, _ = prod
     rng = np.random.default_rng(64)
     x = rng.integers(-9, 9, size=(64, o.n), dtype=np.int64)
     cts = o.encode_inputs(x)[:, 0, :]
     got = {}
-    for v in ("4", "3", "2", "0", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10", "4h", "4d"):
-        monkeypatch.setenv("HEI_KS_TMEM", v.rstrip("fphd"))
-        monkeypatch.setenv("HEI_DIG_TMA", "2" if v.endswith("d") else "1")
+    for v in ("4", "3", "2", "0", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10", "4h", "4d", "4g"):
+        monkeypatch.setenv("HEI_KS_TMEM", v.rstrip("fphdg"))
+        monkeypatch.setenv("HEI_DIG_TMA", {"d": "2", "g": "3"}.get(v[-1], "1"))
         monkeypatch.setenv("HEI_HALF13", "1" if v.endswith("h") else "0")
         monkeypatch.setenv("HEI_FUSE_BIG", "1" if v.endswith("f") else "0")
         monkeypatch.setenv("HEI_PRIME_MAJOR", "1" if v.endswith("p") else "0")
         got[v] = gpu_server_from(o).sum_all_slots(cts)
-    for v in ("4", "3", "2", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10", "4h", "4d"):
+    for v in ("4", "3", "2", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10", "4h", "4d", "4g"):
         assert np.array_equal(got[v], got["0"]), v
     for r in (0, 37, 63):
         assert np.array_equal(got["3"][r], o.sum_all_slots(cts[r])), r
