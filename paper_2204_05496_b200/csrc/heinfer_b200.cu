@@ -790,6 +790,10 @@ void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* 
         else if (c->ks_tmem == 4)  // 3 CTAs/SM, 4-slot TMEM rounds
           k_rot_keyswitch_t<LG, true, 3, 4><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold,
                                                                              nullptr, nullptr, *tabs_of(c, g, 0));
+        else if (c->ks_tmem == 11)  // as 4, Galois gathers by source group instead of TMA-staged polynomials
+          k_rot_keyswitch_t<LG, true, 3, 4, false, false, false, false, false, false, true>
+              <<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr,
+                                                *tabs_of(c, g, 0));
         else if (c->ks_tmem == 10)  // as 4, next digit (then c0) bulk-prefetched into L2
           k_rot_keyswitch_t<LG, true, 3, 4, false, false, false, false, false, true><<<blocks, Ntt<LG>::T, smt, st>>>(
               g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));

@@ -89,8 +89,11 @@ __device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::
 // NA: Galois keys read with L1::no_allocate (ldg_key).
 // L2PF: one thread prefetches the next digit (and, at the last digit, c0)
 // into L2 with a bulk prefetch, so the digit loads hit L2 instead of HBM.
+// GG: the Galois gathers of c1 (l == i term) and c0 read each thread's one
+// aligned 16-slot source group with 4 x 128-bit loads, permuted through a
+// per-thread shared-memory column, instead of TMA-staging the polynomials.
 template <int LOGN, bool PTW, int MINB, int GS = 8, bool NEXT = false, bool PF = false, bool PP = false,
-          bool HOIST = false, bool NA = false, bool L2PF = false>
+          bool HOIST = false, bool NA = false, bool L2PF = false, bool GG = false>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, const uint32_t* __restrict__ dot,
                                                                       const uint32_t* __restrict__ digits,
                                                                       const uint32_t* __restrict__ perm,
@@ -126,9 +129,20 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  if (GG) {
+    const uint4* gs = reinterpret_cast<const uint4*>(c1 + (__ldg(perm + x0) & ~15u));
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 v = __ldg(gs + c);
+      sm[(4 * c) * T + j] = v.x;
+      sm[(4 * c + 1) * T + j] = v.y;
+      sm[(4 * c + 2) * T + j] = v.z;
+      sm[(4 * c + 3) * T + j] = v.w;
+    }
+  }
   if (threadIdx.x == 32) {
     mbar_init(&gbar, 1);
-    bulk_load(sm, c1, N * 4, &gbar);
+    if (!GG) bulk_load(sm, c1, N * 4, &gbar);
     if constexpr (L2PF) {
       if (L > 1) bulk_prefetch_l2(dig + (uint64_t)(i == 0 ? 1 : 0) * N, N * 4);
     }
@@ -141,7 +155,9 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
   __syncthreads();
   tm_fence_after();
   const uint32_t ta = tbase + ((32u * (warp & 3u)) << 16) + 32u * (warp >> 2);  // acc0 cols; acc1 at +16
-  mbar_wait(&gbar, 0);
+  if (!GG) mbar_wait(&gbar, 0);
+  // source of slot s of the permuted polynomial staged in sm
+  auto src_of = [&](uint32_t s) { return GG ? (s & 15u) * T + j : s; };
   const uint4* pp = reinterpret_cast<const uint4*>(perm + x0);
   {
     // l == i term: NTT_i(INTT_i(x)) = x, so sigma(c1)_i multiplies the key directly
@@ -153,7 +169,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
 #pragma unroll
       for (int c = h * GS / 4; c < (h + 1) * GS / 4; ++c) {
         const uint4 pm = __ldg(pp + c);
-        const uint32_t d0 = sm[pm.x], d1 = sm[pm.y], d2 = sm[pm.z], d3 = sm[pm.w];
+        const uint32_t d0 = sm[src_of(pm.x)], d1 = sm[src_of(pm.y)], d2 = sm[src_of(pm.z)], d3 = sm[src_of(pm.w)];
         const uint4 a = ldg_key<NA>(k0 + (2 * c) * T), b = ldg_key<NA>(k0 + (2 * c + 1) * T);
         const uint4 u = ldg_key<NA>(k1 + (2 * c) * T), v = ldg_key<NA>(k1 + (2 * c + 1) * T);
         const int o = 4 * c - GS * h;
@@ -251,12 +267,22 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
   }
   uint32_t* o = out + (uint64_t)pair * g.ct_words;
   __syncthreads();  // the last NTT's exchange reads of sm are done
-  if (threadIdx.x == 0) {
+  if (GG) {
+    const uint4* gs = reinterpret_cast<const uint4*>(c0 + (__ldg(perm + x0) & ~15u));
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 v = __ldg(gs + c);
+      sm[(4 * c) * T + j] = v.x;
+      sm[(4 * c + 1) * T + j] = v.y;
+      sm[(4 * c + 2) * T + j] = v.z;
+      sm[(4 * c + 3) * T + j] = v.w;
+    }
+  } else if (threadIdx.x == 0) {
     fence_proxy_async_smem();
     bulk_load(sm, c0, N * 4, &gbar);
   }
   tm_wait_st();
-  mbar_wait(&gbar, 1);
+  if (!GG) mbar_wait(&gbar, 1);
 #pragma unroll
   for (int h = 0; h < 16 / GS; ++h) {
     uint32_t A[GS], B[GS];
@@ -267,12 +293,13 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
     for (int c = h * GS / 4; c < (h + 1) * GS / 4; ++c) {
       const uint4 pm = __ldg(pp + c);
       const int k = 4 * c - GS * h;
-      A[k] = add_mod(A[k], sm[pm.x], q);
-      A[k + 1] = add_mod(A[k + 1], sm[pm.y], q);
-      A[k + 2] = add_mod(A[k + 2], sm[pm.z], q);
-      A[k + 3] = add_mod(A[k + 3], sm[pm.w], q);
+      A[k] = add_mod(A[k], sm[src_of(pm.x)], q);
+      A[k + 1] = add_mod(A[k + 1], sm[src_of(pm.y)], q);
+      A[k + 2] = add_mod(A[k + 2], sm[src_of(pm.z)], q);
+      A[k + 3] = add_mod(A[k + 3], sm[src_of(pm.w)], q);
       if (fold) {
-        const uint4 u = *reinterpret_cast<const uint4*>(sm + x0 + 4 * c);
+        const uint4 u = GG ? __ldg(reinterpret_cast<const uint4*>(c0 + x0) + c)
+                           : *reinterpret_cast<const uint4*>(sm + x0 + 4 * c);
         const uint4 v = *reinterpret_cast<const uint4*>(c1 + x0 + 4 * c);
         A[k] = add_mod(A[k], u.x, q);
         A[k + 1] = add_mod(A[k + 1], u.y, q);

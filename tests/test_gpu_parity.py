@@ -880,14 +880,14 @@ def test_full_batch_key_switch_variants_bit_exact(prod, monkeypatch):
     x = rng.integers(-9, 9, size=(64, o.n), dtype=np.int64)
     cts = o.encode_inputs(x)[:, 0, :]
     got = {}
-    for v in ("4", "3", "2", "0", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10", "4h", "4d", "4g"):
+    for v in ("4", "3", "2", "0", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10", "4h", "4d", "4g", "11"):
         monkeypatch.setenv("HEI_KS_TMEM", v.rstrip("fphdg"))
         monkeypatch.setenv("HEI_DIG_TMA", {"d": "2", "g": "3"}.get(v[-1], "1"))
         monkeypatch.setenv("HEI_HALF13", "1" if v.endswith("h") else "0")
         monkeypatch.setenv("HEI_FUSE_BIG", "1" if v.endswith("f") else "0")
         monkeypatch.setenv("HEI_PRIME_MAJOR", "1" if v.endswith("p") else "0")
         got[v] = gpu_server_from(o).sum_all_slots(cts)
-    for v in ("4", "3", "2", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10", "4h", "4d", "4g"):
+    for v in ("4", "3", "2", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10", "4h", "4d", "4g", "11"):
         assert np.array_equal(got[v], got["0"]), v
     for r in (0, 37, 63):
         assert np.array_equal(got["3"][r], o.sum_all_slots(cts[r])), r
