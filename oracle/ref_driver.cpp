@@ -345,7 +345,62 @@ int ref_matmul(void* h, unsigned threads, uint64_t* out_packed,
   GUARD_END
 }
 
-// unpack_results (matmul.cpp:399-413) on flat packed ciphertexts (eval form).
+// The reference bench's streaming shape (tools/heinfer.cpp:589-620): encrypt
+// `block` rows at a time with the client backend (encode_input_row, in row
+// order, so the Prng stream is the one encode_inputs would consume), push
+// them into one MatmulStream on the server backend with parallel_for, then
+// finish. Keeps paper-scale batches (C5: 4096 x 40000 at N = 16384, 32 GB of
+// u64 inputs) out of host memory. The weights and bias must be set.
+// *secs = the push_row + finish time only (the bench's "computation" phase).
+int ref_stream_matmul(void* h, const int64_t* x, uint64_t R, uint64_t f,
+                      uint64_t block, unsigned threads, uint64_t* out_packed,
+                      uint64_t* counters, double* secs) {
+  GUARD_BEGIN
+  auto& s = *static_cast<Session*>(h);
+  if (R == 0 || f != s.weights.f) throw ParamError("ref_stream_matmul: shape");
+  if (block == 0) block = 64;
+  matmul::MatmulStream stream(*s.server, s.weights, s.bias, R);
+  std::vector<matmul::EncodedInputRow> enc;
+  double comp = 0;
+  for (uint64_t base = 0; base < R; base += block) {
+    const uint64_t count = std::min<uint64_t>(block, R - base);
+    enc.clear();
+    for (uint64_t i = 0; i < count; ++i)
+      enc.push_back(matmul::encode_input_row(
+          *s.client, std::span<const int64_t>(x + (base + i) * f, f)));
+    auto t0 = std::chrono::steady_clock::now();
+    util::parallel_for(
+        count,
+        [&](size_t lo, size_t hi) {
+          for (size_t i = lo; i < hi; ++i) stream.push_row(base + i, enc[i]);
+        },
+        threads);
+    comp += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  auto packed = stream.finish();
+  comp += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (secs) *secs = comp;
+  if (out_packed) {
+    const size_t w = twin_ct_words(s);
+    for (const auto& ct : packed.cts) {
+      write_twin(s, ct, out_packed);
+      out_packed += w;
+    }
+  }
+  if (counters) {
+    const auto& ops = stream.counters();
+    counters[0] = ops.mul_plain_count;
+    counters[1] = ops.rotation_count;
+    counters[2] = ops.add_count;
+    counters[3] = ops.ciphertexts_in;
+    counters[4] = ops.ciphertexts_out;
+  }
+  return 0;
+  GUARD_END
+}
+
+// unpack_results (matmul.cpp:257-271) on flat packed ciphertexts (eval form).
 int ref_unpack(void* h, const uint64_t* packed, uint64_t R, uint64_t cols,
                int64_t* out) {
   GUARD_BEGIN

@@ -32,6 +32,7 @@ from .matmul import (  # noqa: F401
     matmul,
     matmul_device,
     matmul_wire,
+    save_ciphertexts,
     default_q_primes,
     proposed_counts,
     scale_value,

@@ -1091,6 +1091,22 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
   uint32_t* part = split ? pool_get(c->pool_part, c->pool_part_bytes, (size_t)blocks * Lmax * 2 * c->n * 4) : nullptr;
   uint32_t* result = (c->fold_elts.size() % 2) ? other : cur;
   if (!small || c->timing || !c->graphs) return fold_impl(c, pairs, cur, other, st, split, part, dig, dig2);
+  // drop graphs of an older key/scratch generation, and keep the cache
+  // bounded (a long-running server sees many small batch sizes); an
+  // executable graph still in flight is freed when it completes
+  for (size_t i = 0; i < c->fold_graphs.size();) {
+    if (c->fold_graphs[i].gen != c->graph_gen) {
+      cudaGraphExecDestroy(c->fold_graphs[i].exec);
+      c->fold_graphs.erase(c->fold_graphs.begin() + i);
+    } else {
+      ++i;
+    }
+  }
+  constexpr size_t kMaxFoldGraphs = 32;
+  if (c->fold_graphs.size() >= kMaxFoldGraphs) {
+    cudaGraphExecDestroy(c->fold_graphs.front().exec);
+    c->fold_graphs.erase(c->fold_graphs.begin());
+  }
   for (auto& fg : c->fold_graphs)
     if (fg.pairs == pairs && fg.cur == cur && fg.other == other && fg.part == part && fg.dig == dig &&
         fg.gen == c->graph_gen &&
@@ -1237,7 +1253,6 @@ void stream_flush(hei_gpu_stream* s) {
   hei_gpu_ctx* c = s->ctx;
   const uint64_t nr = s->pend_idx.size();
   CU(cudaMemcpyAsync(s->d_rows, s->pend_idx.data(), nr * 8, cudaMemcpyHostToDevice, c->stream));
-  check_err_flag(c, HEI_CODEC_ERROR, "push_row: coefficient not reduced");
   run_rows(s, s->d_stage, s->d_rows, nr, c->stream);
   CU(cudaStreamSynchronize(c->stream));
   s->pend_idx.clear();
@@ -1286,7 +1301,8 @@ void capacity_gate(hei_gpu_ctx* c, uint64_t f, const char* who) {
 }
 
 hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64_t* bias, uint64_t rows,
-                           bool host_staging = true, cudaStream_t zero_on = nullptr, bool encode_bias = true) {
+                           bool host_staging = true, cudaStream_t zero_on = nullptr, bool encode_bias = true,
+                           unsigned long long* ext_acc = nullptr) {
   if (rows == 0) raise(HEI_PARAM_ERROR, "matmul: empty input");
   if (!w || w->cols == 0 || w->f == 0) raise(HEI_PARAM_ERROR, "matmul: empty weights");
   if (w->ctx != c) raise(HEI_PARAM_ERROR, "matmul: weights encoded for a different context");
@@ -1308,13 +1324,14 @@ hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64
     CU(cudaMalloc(&s->d_stage64, s->cap_rows * w->kc * c->ct_words() * 8));
     CU(cudaMalloc(&s->d_rows, s->cap_rows * 8));
   } else {
-    // one-shot device-resident call: borrow the context pools
-    s->d_acc = pool_get(c->pool_acc, c->pool_acc_bytes, s->C * c->ct_words() * 8);
+    // one-shot device-resident call: borrow the context pools, or accumulate
+    // into the caller's (pre-zeroed) buffer
+    s->d_acc = ext_acc ? ext_acc : pool_get(c->pool_acc, c->pool_acc_bytes, s->C * c->ct_words() * 8);
     s->d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, s->cap_rows * 8);
     s->owns_acc = false;
     s->owns_rows = false;
   }
-  CU(cudaMemsetAsync(s->d_acc, 0, s->C * c->ct_words() * 8, zero_on ? zero_on : c->stream));
+  if (!ext_acc) CU(cudaMemsetAsync(s->d_acc, 0, s->C * c->ct_words() * 8, zero_on ? zero_on : c->stream));
   if (!host_staging && encode_bias) {
     // stage the bias now (pinned, async): every earlier call has synchronised
     const size_t bb = s->bias.size() * 8;
@@ -1365,6 +1382,11 @@ void stream_push(hei_gpu_stream* s, uint64_t row, const uint64_t* chunks, int fo
   k_narrow<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, s->d_stage64 + slot * words,
                                                           s->d_stage + slot * words, s->w->kc, c->d_err);
   LAUNCHED();
+  // a row with an unreduced residue is rejected before it is recorded (the
+  // reference's load_ciphertext throws before push_row sees it,
+  // serialize.cpp:80-90): its staging slot is reused by the next push and the
+  // caller may push the row again
+  check_err_flag(c, HEI_CODEC_ERROR, "push_row: coefficient not reduced");
   if (form == HEI_FORM_COEFF) {
     launch_ct_ntt(c, (unsigned)(s->w->kc * 2 * c->P()), s->d_stage + slot * words, c->stream);
   }
@@ -3378,9 +3400,9 @@ int hei_gpu_matmul_partial_device(hei_gpu_ctx* c, const hei_gpu_weights* w, cons
     cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
     std::vector<int64_t> zero_bias(w ? w->cols : 1, 0);
     std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(
-        stream_new(c, w, zero_bias.data(), total_rows, false, st, /*encode_bias=*/false), stream_free);
-    s->d_acc = reinterpret_cast<unsigned long long*>(d_acc);  // the caller's buffer
-    s->owns_acc = false;
+        stream_new(c, w, zero_bias.data(), total_rows, false, st, /*encode_bias=*/false,
+                   reinterpret_cast<unsigned long long*>(d_acc)),  // accumulate into the caller's buffer
+        stream_free);
     const size_t words = w->kc * c->ct_words();
     uint64_t* d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, rows * 8);
     k_iota<<<grid_for(rows, 256), 256, 0, st>>>(d_rows, row_offset, rows);

@@ -55,7 +55,13 @@ def scale_value(x: float, exponent: int) -> int:
     limit = float((1073872897 * 114689 - 1) // 2)
     if not abs(scaled) <= limit:
         raise RangeError(f"scale_value: {x} * 2^{exponent} exceeds the plaintext capacity")
-    r = math.floor(abs(scaled) + 0.5)
+    # std::llround: half away from zero, without the double rounding of
+    # floor(|s| + 0.5) (which gives 1 at 0.49999999999999994); a - floor(a)
+    # is exact for every |s| < 2^53 and the |s| >= 2^53 values are integers.
+    a = abs(scaled)
+    r = math.floor(a)
+    if a - r >= 0.5:
+        r += 1
     return int(r if scaled >= 0 else -r)
 
 
@@ -374,6 +380,39 @@ def encode_inputs_device(server: GpuTwinServer, x: np.ndarray, rng0: Prng, rng1:
     check(native.lib().hei_gpu_encode_inputs_device(server.handle, i64p(x), C.c_uint64(R), C.c_uint64(f), rng0._h, rng1._h,
                                                     C.c_void_p(d_out_ptr), C.c_void_p(stream_ptr)))
 
+
+
+def save_ciphertexts(server: GpuTwinServer, cts: np.ndarray, form: int = FORM_EVAL) -> bytes:
+    """bfv::save_ciphertext (serialize.cpp:63-78) of every branch of every
+    twin ciphertext in `cts` ([..][twin ct] u64), concatenated in order
+    [ct][branch] -- the client's request blob list (client.cpp /
+    server.cpp:145-147). Eval-form input is brought to coefficient form by
+    device inverse NTTs (to_coeff), then written as header (magic, version,
+    params hash, parts = 2, kind = ciphertext) + 2L polys of (form byte, N u64)."""
+    cts = np.ascontiguousarray(cts, dtype=np.uint64).reshape(-1, server.ct_words)
+    M, n = cts.shape[0], server.n
+    sizes = [server.hect_bytes(0), server.hect_bytes(1)]
+    out = np.zeros((M, sizes[0] + sizes[1]), np.uint8)
+    off_w, off_b = 0, 0
+    for b in range(2):
+        L = server.L[b]
+        hdr = np.frombuffer(b"HECT" + (1).to_bytes(2, "little") + server.params_hash(b).to_bytes(8, "little")
+                            + (2).to_bytes(4, "little") + bytes([5]), np.uint8)
+        blob = out[:, off_b: off_b + sizes[b]]
+        blob[:, :19] = hdr
+        polys = blob[:, 19:].reshape(M, 2 * L, 1 + 8 * n)
+        polys[:, :, 0] = FORM_COEFF
+        br = cts[:, off_w: off_w + 2 * L * n].reshape(M, 2, L, n)
+        for i in range(L):
+            v = np.ascontiguousarray(br[:, :, i, :]).reshape(2 * M, n)
+            if form == FORM_EVAL:
+                v = server.ntt(b, i, v, inverse=True)
+            v = v.reshape(M, 2, n)
+            for p in range(2):
+                polys[:, p * L + i, 1:] = v[:, p, :].view(np.uint8).reshape(M, 8 * n)
+        off_w += 2 * L * n
+        off_b += sizes[b]
+    return out.tobytes()
 
 
 def matmul_wire(server: GpuTwinServer, w: EncodedWeights, blobs, rows: int, bias):

@@ -74,6 +74,14 @@ def test_scale_value_matches_reference_rounding():
     assert scale_value(-0.5, 20) == -524288
     assert scale_value(0.0234375, 6) == 2
     assert scale_value(-0.0234375, 6) == -2
+    # std::llround is half away from zero with no double rounding: the largest
+    # double below 0.5 rounds to 0 (floor(|s| + 0.5) would give 1)
+    assert scale_value(0.49999999999999994, 0) == 0
+    assert scale_value(-0.49999999999999994, 0) == 0
+    assert scale_value(2.5, 0) == 3
+    assert scale_value(-2.5, 0) == -3
+    assert scale_value(0.5, 0) == 1 and scale_value(-0.5, 0) == -1
+    assert scale_value(1e13 + 0.5, 0) == 10000000000001 and scale_value(-(1e13 + 0.5), 0) == -10000000000001
     with pytest.raises(RangeError):
         scale_value(1e10, 20)
     with pytest.raises(RangeError):

@@ -249,6 +249,38 @@ def test_errors_match_reference_types(tiny32):
         matmul(s, bad, EncodedWeights.from_prepared(s, wp, 4), [0, 0])
 
 
+def test_stream_rejects_bad_row_and_keeps_going(tiny32):
+    """A push_row whose residues are not reduced raises CodecError and is not
+    recorded: the caller can catch it, push the corrected row (same index) and
+    the remaining rows, and finish() returns the oracle's result. (Earlier the
+    rejected row stayed counted and the next pushes overran the staging
+    buffer.)"""
+    from paper_2204_05496_b200 import EncodedWeights, MatmulStream, native
+
+    o, s = tiny32
+    rng = np.random.default_rng(601)
+    R, f, cols = 6, 40, 3
+    x = random_mat(rng, R, f, 10)
+    w = random_mat(rng, f, cols, 5)
+    bias = np.array([3, -1, 7], np.int64)
+    inputs = o.encode_inputs(x)
+    wp = o.encode_weights(w)
+    want, _ = o.fast_matmul(inputs, f, wp, bias)
+    ew = EncodedWeights.from_prepared(s, wp, f)
+    st = MatmulStream(s, ew, bias, R)
+    bad = inputs[2].copy()
+    bad[0, 5] = o.q[0] + 3
+    for r in (0, 1):
+        st.push_row(r, inputs[r])
+    for _ in range(3):  # repeated failures must not consume staging slots
+        with pytest.raises(native.CodecError):
+            st.push_row(2, bad)
+    for r in (2, 3, 4, 5):
+        st.push_row(r, inputs[r])
+    got = st.finish()
+    assert np.array_equal(got, want)
+
+
 @pytest.mark.parametrize("n", [32, 8192])
 def test_baseline_bit_exact_and_rng_state(n):
     """baseline_matmul (matmul.cpp:415-486): same keys, same replayed
