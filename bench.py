@@ -35,14 +35,29 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 T0, T1, T1_16K = 1073872897, 114689, 163841
-CONFIGS = {
-    # name: (R, f, cols, N, p_feat, w_sigma)
-    "c1": (1, 1000, 11, 8192, 0.05, 0.1),
-    "c2": (1, 10000, 11, 8192, 0.05, 0.1),
-    "c3": (1, 40000, 11, 8192, 0.03, 0.05),
-    "c4": (256, 40000, 11, 8192, 0.03, 0.05),
-    "c5": (4096, 40000, 33, 16384, 0.03, 0.05),
-}
+GOLDEN = os.path.join(ROOT, "tests", "golden", "configs")
+
+
+def _configs():
+    from paper_2204_05496_b200.workload import CONFIGS  # (R, f, cols, N, p_feat, w_sigma)
+
+    return CONFIGS
+
+
+def golden(case: str):
+    """Reference-written digests (tests/golden/make_golden_configs.py)."""
+    try:
+        return json.load(open(os.path.join(GOLDEN, case + ".json")))
+    except Exception:
+        return None
+
+
+def sha(a) -> str:
+    import hashlib
+
+    if isinstance(a, (bytes, bytearray)):
+        return hashlib.sha256(a).hexdigest()
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
 def parse():
@@ -51,7 +66,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--rows", type=int, default=0, help="override individuals per rank")
     ap.add_argument("--batch-pairs", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -155,21 +170,52 @@ def dist_setup(args):
     return world, rank, local
 
 
-# ------------------------------------------------------------------ reference
-def reference_sample(cfg_name: str, rows: int | None = None, threads: int = 0):
-    """Time the reference CPU path (oracle/_ref) on a bounded sample of the
-    workload. Returns (inferences/s, sample description, threads, seconds)."""
-    from oracle.oracle import Reference, TwinParams, ref_available
-    from tests.helpers import synthetic
+# ------------------------------------------------------------------ roofline model
+def algorithmic_counts(R: int, f: int, cols: int, n: int, L=(6, 4)):
+    """algorithmic HBM bytes and modular multiplies per
+    inference of the fast algorithm (one HBM pass per HE op, u32 residues,
+    the reference's pass structure; weights, keys and packed output amortised
+    over the batch)."""
+    P = 4 * n
+    k = (f + n - 1) // n
+    S = n.bit_length() - 1
+    Cb = [2 * Lb * P for Lb in L]
+    per = sum(k * Cb[i] + cols * (2 * S + 2) * Cb[i] + cols * L[i] * P for i in range(2))
+    shared = sum(cols * k * L[i] * P + S * 2 * L[i] ** 2 * P + ((R * cols + n - 1) // n) * Cb[i] for i in range(2))
+    bytes_inf = per + shared / R
+    M = cols * S * sum(Lb ** 2 for Lb in L) * n * (S / 2 + 2) + cols * (k + 1) * sum(2 * Lb * n for Lb in L)
+    return bytes_inf, M
 
-    R, f, cols, n, pf, ws = CONFIGS[cfg_name]
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "MEASURED_PEAKS.json"
+    except Exception:
+        return {"hbm_gbs": 7672.0}, "B200_PROFILING.md fallback"
+
+
+# ------------------------------------------------------------------ reference
+def _ref_session(cfg: str, rows: int | None = None):
+    from oracle.oracle import Reference, production_params
+    from paper_2204_05496_b200.workload import config_workload
+
+    R, f, cols, n, pf, ws = _configs()[cfg]
+    r = rows or R
+    x, w, b = config_workload(cfg, rows=r)
+    ref = Reference(production_params(n), key_seed=1, enc_seed=2)
+    return ref, x, w, b, r, f, cols, n
+
+
+def reference_sample(cfg_name: str, rows: int | None = None, threads: int = 0):
+    """The reference CPU path (oracle/_ref = the unmodified reference compiled
+    in place) on `rows` individuals of the workload, all host threads.
+    Returns (inferences/s, sample description, threads, seconds, session)."""
+    from oracle.oracle import ref_available
+
     if not ref_available():
         return None
+    ref, x, w, b, r, f, cols, n = _ref_session(cfg_name, rows)
     nthreads = threads or os.cpu_count() or 1
-    r = rows or max(1, min(R, nthreads))
-    p = TwinParams(n=n, t0=T0, t1=T1 if n < 16384 else T1_16K, sec=128)
-    ref = Reference(p, key_seed=1, enc_seed=2)
-    x, w, b = synthetic(r, f, cols, pf, ws)
     ref.encode_inputs(x)
     ref.set_weights(w)
     ref.set_bias(b)
@@ -177,26 +223,54 @@ def reference_sample(cfg_name: str, rows: int | None = None, threads: int = 0):
     return r / secs, f"{r} individuals x {f} features x {cols} classes (N={n}) per step", nthreads, secs, ref
 
 
+def reference_latency(threads: int = 0):
+    """Reference single-individual latency at C3 (matmul.cpp:239-255: rows are
+    the only parallel axis, so R = 1 runs on one thread whatever `threads`)."""
+    res = reference_sample("c3", threads=threads)
+    if res is None:
+        return None
+    _, _, nthreads, secs, ref = res
+    ref.close()
+    return {"value_ms": secs * 1000.0, "cores": 1, "threads_offered": nthreads, "kind": "reference",
+            "sample": "c3: 1 individual x 40000 features x 11 classes (N=8192), one full call"}
+
+
+def reference_standard(prefix: int = 400):
+    """Reference baseline_matmul (matmul.cpp:273-344, single-threaded, constant
+    cost per feature: 1 encryption + |Y| ct x pt per feature) timed on the
+    first `prefix` features of C3 and extrapolated to 40,000."""
+    from oracle.oracle import ref_available
+
+    if not ref_available():
+        return None
+    ref, x, w, b, r, f, cols, n = _ref_session("c3")
+    _, _, secs = ref.baseline_matmul(x[:, :prefix], w[:prefix], b, export=False)
+    ref.close()
+    return {"value_ms": secs / prefix * f * 1000.0, "cores": 1, "kind": "reference",
+            "sample": f"c3 baseline_matmul on the first {prefix} of {f} features ({secs:.2f} s), "
+                      f"extrapolated linearly (constant per-feature cost, matmul.cpp:301-320)"}
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    R, f, cols, n, _, _ = CONFIGS[args.config]
-    res = reference_sample(args.config)
+    R, f, cols, n, _, _ = _configs()[args.config]
+    res = reference_sample(args.config, rows=R)  # the full batch: same config as our arm
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libheiref.so not built (needs /root/reference at build time)"}))
         return
-    rate, sample, threads, _, ref = res
-    r = max(1, min(R, threads))
+    _, sample, threads, first, ref = res
     times = []
     for s in range(args.warmup + args.steps):
-        _, _, secs = ref.matmul(r, cols, threads=threads, export=False)
+        _, _, secs = ref.matmul(R, cols, threads=threads, export=False)
         if s >= args.warmup:
             times.append(secs)
-    v = r * len(times) / sum(times)
+    v = R * len(times) / sum(times)
     line = {"metric": "encrypted LR inferences/sec at 40k features", "value": v, "unit": "inferences/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config}: {R}x{f}x{cols} N={n}", "sample_rows_per_step": r},
+            "config": {"workload": f"{args.config}: {R} individuals x {f} features x {cols} classes, N={n}",
+                       "rows_per_step": R, "same_config_as_ours": True},
             "cpu_baseline": {"value": v, "unit": "inferences/s", "cores": threads, "kind": "reference", "sample": sample},
             "e2e": {"value": v, "unit": "inferences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -221,47 +295,78 @@ def make_server(n, device, seed=1):
     return srv, q0, q1, kg_ms
 
 
-def wire_e2e(srv, ew, b, h_np, R, kc, n, L0, L1, world, steps):
-    """Time hei_gpu_matmul_wire on the same residues laid out as the
-    request's HECT blobs (serialize.cpp:63-78; treated as coeff form)."""
+def wire_e2e(srv, ew, b, h_np, R, world, steps, g):
+    """Time hei_gpu_matmul_wire on the client's request: the same ciphertexts
+    serialised as HECT coeff-form blobs (save_ciphertext, serialize.cpp:63-78),
+    and compare the response bytes with the reference server's."""
+    from paper_2204_05496_b200 import matmul_wire, save_ciphertexts
+
     import torch
 
-    from paper_2204_05496_b200 import matmul_wire
-
-    b0, b1 = srv.hect_bytes(0), srv.hect_bytes(1)
-    hdr = [np.frombuffer(b"HECT\x01\x00" + srv.params_hash(k).to_bytes(8, "little") + b"\x02\x00\x00\x00\x05", np.uint8)
-           for k in range(2)]
-    buf = torch.empty(R * kc * (b0 + b1), dtype=torch.uint8, pin_memory=True)
-    a = buf.numpy().reshape(R * kc, b0 + b1)
-    src = h_np.reshape(R * kc, -1)
-    off = 0
-    for k, L in enumerate((L0, L1)):
-        a[:, off:off + 19] = hdr[k]
-        polys = a[:, off + 19: off + 19 + 2 * L * (1 + 8 * n)].reshape(R * kc, 2 * L, 1 + 8 * n)
-        polys[:, :, 0] = 0
-        w0 = (2 * L0 * n) if k else 0
-        slab = np.ascontiguousarray(src[:, w0: w0 + 2 * L * n]).reshape(R * kc, 2 * L, n)
-        polys[:, :, 1:] = slab.view(np.uint8).reshape(R * kc, 2 * L, 8 * n)
-        off += (b0 if k == 0 else b1)
-    outs, _ = matmul_wire(srv, ew, a, R, b)  # warm
+    raw = save_ciphertexts(srv, h_np)
+    pinned = torch.empty(len(raw), dtype=torch.uint8, pin_memory=True)  # as the e2e path's inputs
+    blobs = pinned.numpy()
+    blobs[:] = np.frombuffer(raw, np.uint8)
+    del raw
+    outs, _ = matmul_wire(srv, ew, blobs, R, b)  # warm
     t0 = time.perf_counter()
     for _ in range(steps):
-        outs, _ = matmul_wire(srv, ew, a, R, b)
+        outs, _ = matmul_wire(srv, ew, blobs, R, b)
     sec = (time.perf_counter() - t0) / steps
-    res = {"value": world * R / sec, "unit": "inferences/s", "h2d_bytes_per_step": int(a.nbytes),
-           "d2h_bytes_per_step": int(sum(len(o) for o in outs)), "ms_per_step": 1000 * sec,
+    resp = b"".join(outs)
+    res = {"value": world * R / sec, "unit": "inferences/s", "h2d_bytes_per_step": int(blobs.nbytes),
+           "d2h_bytes_per_step": len(resp), "ms_per_step": 1000 * sec,
            "format": "HECT coeff-form blobs [row][chunk][branch] in, HECT blobs out (server.cpp:112-172)"}
-    del buf, a
+    if g and "wire_request_sha256" in g:
+        res["request_equals_reference_client"] = sha(blobs) == g["wire_request_sha256"]
+        res["response_equals_reference_server"] = sha(resp) == g["wire_response_sha256"]
     return res
+
+
+def standard_algorithm(srv, bfly_peak):
+    """The standard algorithm (baseline_matmul, matmul.cpp:273-344) at C3:
+    40,000 column encryptions from the reference's Prng stream, summed over
+    features for 11 classes. Checked against the reference's bytes
+    (tests/golden/configs/base_c3.json) and decrypted."""
+    from paper_2204_05496_b200 import Prng, baseline_matmul
+    from paper_2204_05496_b200.workload import config_workload
+
+    R3, f3, c3, n3, _, _ = _configs()["c3"]
+    x3, w3, b3 = config_workload("c3")
+    baseline_matmul(srv, x3, w3, b3, Prng(2), Prng(3))  # warm (incl. the cached jump polynomial)
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        blocks, bc = baseline_matmul(srv, x3, w3, b3, Prng(2), Prng(3))
+        times.append(time.perf_counter() - t0)
+    ms = 1000 * statistics.median(times)
+    g = golden("base_c3")
+    dec = srv.unpack_baseline(blocks, R3, c3)
+    # the reference algorithm's own work (SURVEY §8d): per feature one twin
+    # encryption (3 sum(L) NTTs + 2 sum(L) N products) and |Y| ct x pt
+    # products over 2 sum(L) N residues, at the measured butterfly peak
+    L = (6, 4)
+    S = n3.bit_length() - 1
+    per_feat = 3 * sum(L) * (n3 // 2) * S + 2 * sum(L) * n3 + c3 * 2 * sum(L) * n3
+    floor_ms = per_feat * f3 / bfly_peak * 1000.0
+    return {"algorithm": "standard (sample-batched, baseline_matmul)", "config": f"c3: {R3}x{f3}x{c3} N={n3}",
+            "ms": ms, "mul_plain": int(bc.mul_plain_count), "note": "host call incl. H2D of x, w and D2H of the blocks",
+            "bit_exact_vs_reference": bool(g is not None and sha(blocks) == g["blocks_sha256"]),
+            "decrypted_equals_integer_product": bool(np.array_equal(dec, x3 @ w3 + b3)),
+            "reference_algorithm_int_floor_ms": floor_ms,
+            "reference_algorithm_int_floor_note": "the reference's per-feature transform + product count at the "
+                                                  "measured butterfly peak; the device computes the same residues by "
+                                                  "linearity (coefficient-domain sums, DESIGN.md §4), so it can run "
+                                                  "below this floor"}
 
 
 def run_ours(args, world, rank, local):
     import torch
 
     from paper_2204_05496_b200 import encode_weights, matmul, matmul_device, native
-    from tests.helpers import synthetic
+    from paper_2204_05496_b200.workload import workload
 
-    R_total, f, cols, n, pf, ws = CONFIGS[args.config]
+    R_total, f, cols, n, pf, ws = _configs()[args.config]
     R = args.rows or R_total  # per rank (weak scaling: every rank gets the full per-GPU batch)
     # one process per GPU; the modulo only matters for the plumbing check below
     local = local % max(1, torch.cuda.device_count())
@@ -285,12 +390,13 @@ def run_ours(args, world, rank, local):
     kc = (f + n - 1) // n
     P = len(q0) + len(q1)
     ctw = 2 * P * n
-    # seeded synthetic individuals (rank r holds its own rows), weights, bias
-    x, _, _ = synthetic(R, f, cols, pf, ws, seed=7 + rank)
-    _, w, b = synthetic(1, f, cols, pf, ws)  # one model, shared by every rank
+    # seeded workload from util::Prng(7): one X of world*R rows
+    # (rank r holds rows [rR, (r+1)R)), then the shared model W, bias
+    rows_all = world * R
+    x, w, b = workload(rows_all, f, cols, pf, ws, row_lo=rank * R, row_hi=(rank + 1) * R)
     ew = encode_weights(srv, w)
     # device-resident inputs: the client's real encryptions of x
-    # (encode_inputs, matmul.cpp:201-223; Prng seeds 2, 3 as client_backend(keys, 2))
+    # (encode_inputs, matmul.cpp:59-81; Prng seeds 2, 3 as client_backend(keys, 2))
     d_in = torch.empty((R * kc, ctw), dtype=torch.int32, device=dev)
     stream = torch.cuda.Stream(device=dev)
     for _ in range(2):  # first call also builds the cached mt19937_64 jump polynomial
@@ -301,14 +407,15 @@ def run_ours(args, world, rank, local):
     C_ = (R * cols + n - 1) // n
     d_out = torch.empty((C_, ctw), dtype=torch.int32, device=dev)
     d_one = torch.empty((C_, ctw), dtype=torch.int32, device=dev)  # rank-local result (roofline step)
+    exchange = None
 
     if world == 1:
         def step():
             matmul_device(srv, d_in.data_ptr(), R, ew, b, d_out.data_ptr(), stream.cuda_stream)
     else:
         # individual sharding: rank r holds rows [r*R, (r+1)*R) of a world*R
-        # batch; one int64 all-reduce of the packed partials (NCCL/NVLink),
-        # then the mod-q reduction + bias add on every rank.
+        # batch; one exchange of the packed partials, then the mod-q
+        # reduction + bias add.
         from paper_2204_05496_b200.sharding import finish_packed_device, matmul_partial_device, packed_count
 
         total_rows = world * R
@@ -386,6 +493,19 @@ def run_ours(args, world, rank, local):
         ms = float(t.item())
     value = world * R / (ms / 1000.0)
 
+    # bit-exactness of the timed path against the reference (single rank:
+    # the golden digests cover exactly this workload, keys and encryption)
+    g = None
+    if world == 1 and rank == 0:
+        g = golden("stream_c5") if args.config == "c5" else golden(f"fast_{args.config}")
+        if g is not None and g.get("rows") != R:
+            g = None
+    packed_dev = d_out.cpu().numpy().view(np.uint32).astype(np.uint64) if rank == 0 else None
+    parity = None
+    if g is not None:
+        parity = {"golden": os.path.relpath(os.path.join(GOLDEN, g["case"] + ".json"), ROOT),
+                  "device_packed_equals_reference": sha(packed_dev) == g["packed_sha256"]}
+
     # e2e: host u64 (pinned) inputs through the C ABI, copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -401,15 +521,24 @@ def run_ours(args, world, rank, local):
         e2e_s = (time.perf_counter() - t0) / e2e_steps
         e2e = {"value": world * R / e2e_s, "unit": "inferences/s", "h2d_bytes_per_step": int(h_np.nbytes),
                "d2h_bytes_per_step": int(out.nbytes), "ms_per_step": 1000 * e2e_s}
+        if parity is not None:
+            parity["inputs_equal_reference_client"] = sha(h_np) == g.get("inputs_sha256", "")
+            parity["e2e_packed_equals_reference"] = sha(out) == g["packed_sha256"]
         # the server's wire path (server.cpp:112-172): HECT coeff-form blobs
         # in, HECT blobs out, parse/NTT/INTT/serialize on the device
         if args.wire and world == 1:  # the wire copy doubles pinned host memory; one rank only
-            e2e["wire"] = wire_e2e(srv, ew, b, h_np, R, kc, n, len(q0), len(q1), world, e2e_steps)
+            e2e["wire"] = wire_e2e(srv, ew, b, h_np, R, world, e2e_steps, g)
+            if parity is not None and "response_equals_reference_server" in e2e["wire"]:
+                parity["wire_response_equals_reference"] = e2e["wire"]["response_equals_reference_server"]
         del h_in, h_np
 
-    # ---- roofline of the dominant kernel (key switch), timed live with CUDA
-    # events on the launch stream inside the C ABI over one extra step.
-    roof = int_roof = None
+    # ---- rooflines, timed live with CUDA events on the launch stream inside
+    # the C ABI over one extra (serialised) step
+    roof = int_roof = step_roof = None
+    peaks, peak_src = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 7672.0))
+    bfly_peak = native.butterfly_peak(local) if rank == 0 else None
+    L0, L1 = len(q0), len(q1)
     if rank == 0:
         native.kernel_timing(srv.handle, True)
         # the rank's own fold work only: no collective, so rank 0 can time it alone
@@ -418,114 +547,121 @@ def run_ours(args, world, rank, local):
         ks_n, ks_ms = native.kernel_stats(srv.handle, 0)
         dg_n, dg_ms = native.kernel_stats(srv.handle, 1)
         native.kernel_timing(srv.handle, False)
-        L0, L1 = len(q0), len(q1)
         S = int(np.log2(n))  # fold steps per batch
         batches = ks_n // S
-        # algorithmic bytes of one key-switch launch over P pairs: per pair
-        # and output prime, c0/c1 read + out0/out1 written (4 polys of 4N B)
-        # and L-1 digit polys read; the step's Galois key (2L polys of 8N B
-        # per prime) once per launch.
-        per_pair = sum(16 * n + 4 * n * (Lb - 1) for Lb in (L0, L1) for _ in range(Lb))
-        keys = sum(16 * Lb * n * Lb for Lb in (L0, L1))
-        tot_bytes = S * R * cols * per_pair + ks_n * keys
+        pairs_per_launch = R * cols / batches
+        # per pair-rotation the twin ciphertext is read and
+        # written once (2 sum_b C_b, C_b = 2 L_b 4N bytes); the step's Galois
+        # key (2 L_b^2 polys of value + Shoup u32 per branch) once per launch
+        pair_bytes = 2 * sum(2 * Lb * 4 * n for Lb in (L0, L1))
+        key_bytes = sum(2 * Lb * Lb * 4 * n * 2 for Lb in (L0, L1))
+        launch_bytes = pairs_per_launch * pair_bytes + key_bytes
         avg_s = ks_ms / ks_n / 1000.0
-        peaks = {}
-        try:
-            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        except Exception:
-            pass
-        hbm = float(peaks.get("hbm_gbs", 6650.0))
         traffic = None
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "keyswitch_traffic.json")))
-            traffic = prof.get("dram_bytes_per_pair") * R * cols / batches
+            traffic = prof.get("dram_bytes_per_pair") * pairs_per_launch
         except Exception:
             pass
-        ach = tot_bytes / (ks_ms / 1000.0) / 1e9
         logn = n.bit_length() - 1
-        blocks = R / batches * cols * (L0 + L1)  # (pair, prime) blocks per timed key-switch launch
+        blocks = pairs_per_launch * (L0 + L1)  # (pair, prime) blocks per timed key-switch launch
         if blocks <= 148:
-            ks_name = f"k_rot_keyswitch_w2<{logn}> (latency path: 2-group CTA, fused next digit)"
-        elif logn == 14 and os.environ.get("HEI_KS14_TMEM", "1") != "0":
-            ks_name = "k_rot_keyswitch_t<14> (TMEM accumulators, 1 CTA of 1024 threads/SM)"
-        elif blocks < 296 or logn != 13 or os.environ.get("HEI_KS_TMEM", "4") == "0":
+            ks_name = f"k_rot_keyswitch_w2<{logn}> (latency path)"
+        elif logn == 14:
+            ks_name = "k_rot_keyswitch_h (half-ring blocks, TMEM accumulators)"
+        elif blocks < 296:
             ks_name = f"k_rot_keyswitch_s<{logn}> (shared-memory accumulators)"
         else:
             ks_name = "k_rot_keyswitch_t<13> (TMEM accumulators, 3 CTAs/SM)"
-        roof = {"kernel": ks_name, "bound": "hbm", "achieved": ach, "peak": hbm,
-                "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
-                "algorithmic_bytes_per_launch": tot_bytes / ks_n, "avg_launch_ms": avg_s * 1e3, "launches": ks_n,
-                "batches": batches, "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
-                "share_of_fold": ks_ms / (ks_ms + dg_ms), "digits_avg_launch_ms": dg_ms / max(1, dg_n)}
+        ach = launch_bytes / avg_s / 1e9
+        roof = {"kernel": ks_name, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": traffic, "binding": "int32 pipes (see int_roofline)",
+                "algorithmic_bytes_per_launch": launch_bytes, "bytes_model": "SURVEY 8(d): pairs x 2 sum_b C_b + key",
+                "avg_launch_ms": avg_s * 1e3, "launches": ks_n, "pairs_per_launch": pairs_per_launch,
+                "peak_source": peak_src, "share_of_fold": ks_ms / (ks_ms + dg_ms),
+                "digits_avg_launch_ms": dg_ms / max(1, dg_n)}
         bfly_pair = sum(((Lb - 1) * (n // 2) * S + 2 * Lb * n) for Lb in (L0, L1) for _ in range(Lb))
-        tot_bfly = S * R * cols * bfly_pair
-        peak_b = native.butterfly_peak(local)
+        tot_bfly = pairs_per_launch * bfly_pair
         int_roof = {"kernel": ks_name, "bound": "int32 pipes (CT butterfly = Shoup mulmod + add + sub)",
-                    "achieved": tot_bfly / (ks_ms / 1000.0) / 1e9, "peak": peak_b / 1e9, "unit": "Gbutterfly/s",
-                    "frac": tot_bfly / (ks_ms / 1000.0) / peak_b,
+                    "achieved": tot_bfly / avg_s / 1e9, "peak": bfly_peak / 1e9, "unit": "Gbutterfly/s",
+                    "frac": tot_bfly / avg_s / bfly_peak, "binding": True,
                     "peak_source": "k_bfly_peak register microbenchmark, this run",
-                    "butterfly_equivalents_per_launch": tot_bfly / ks_n}
+                    "butterfly_equivalents_per_launch": tot_bfly}
+        bi, M = algorithmic_counts(R, f, cols, n, (L0, L1))
+        t_int = R * M / bfly_peak
+        t_hbm = R * bi / (hbm * 1e9)
+        step_roof = {"model": "SURVEY 8(d) per inference: bytes and modular multiplies of the fast algorithm",
+                     "bytes_per_inference": bi, "modmul_per_inference": M,
+                     "hbm_frac": t_hbm / (ms / 1000.0), "int_frac": t_int / (ms / 1000.0),
+                     "binding": "int" if t_int > t_hbm else "hbm",
+                     "roofline_inferences_per_s": world * R / max(t_int, t_hbm)}
 
     base = None
     if args.baseline and rank == 0:
-        from paper_2204_05496_b200 import Prng, baseline_matmul
-
-        R3, f3, c3, _, pf3, ws3 = CONFIGS["c3"]
-        x3, w3, b3 = synthetic(R3, f3, c3, pf3, ws3)
-        baseline_matmul(srv, x3, w3, b3, Prng(2), Prng(3))  # warm (incl. the cached jump polynomial)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        _, bc = baseline_matmul(srv, x3, w3, b3, Prng(2), Prng(3))
-        bs = time.perf_counter() - t0
-        base = {"algorithm": "standard (sample-batched, baseline_matmul)", "config": f"c3: {R3}x{f3}x{c3} N={n}",
-                "ms": bs * 1000.0, "mul_plain": int(bc.mul_plain_count), "note": "host call incl. H2D of x, w and D2H"}
+        base = standard_algorithm(srv, bfly_peak)
         base["client_encrypt"] = {"config": f"{R} individuals x {f} features ({R * kc} twin encryptions)",
                                   "ms": enc_ms, "individuals_per_s": R / (enc_ms / 1000.0)}
 
     lat = None
     if args.latency and rank == 0:
-        # single individual, 40k features x 11 classes (C3 shape), device-resident
-        d1 = d_in[:kc].contiguous()
+        # single individual, C3 (40,000 features x 11 classes): its own seeded
+        # workload, encrypted with Prng(2)/(3), device-resident; the output is
+        # compared with the reference's (tests/golden/configs/fast_c3.json)
+        from paper_2204_05496_b200.workload import config_workload
+
+        x3, w3, b3 = config_workload("c3")
+        ew3 = encode_weights(srv, w3)
+        d1 = torch.empty((kc, ctw), dtype=torch.int32, device=dev)
+        encode_inputs_device(srv, x3, Prng(2), Prng(3), d1.data_ptr(), stream.cuda_stream)
         o1 = torch.empty((1, ctw), dtype=torch.int32, device=dev)
         for _ in range(3):
-            matmul_device(srv, d1.data_ptr(), 1, ew, b, o1.data_ptr(), stream.cuda_stream)
+            matmul_device(srv, d1.data_ptr(), 1, ew3, b3, o1.data_ptr(), stream.cuda_stream)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(10):
-            matmul_device(srv, d1.data_ptr(), 1, ew, b, o1.data_ptr(), stream.cuda_stream)
+        for _ in range(20):
+            matmul_device(srv, d1.data_ptr(), 1, ew3, b3, o1.data_ptr(), stream.cuda_stream)
         e1.record(stream)
         torch.cuda.synchronize()
-        lat = e0.elapsed_time(e1) / 10
+        lat_ms = e0.elapsed_time(e1) / 20
+        g3 = golden("fast_c3")
+        bi3, M3 = algorithmic_counts(1, 40000, 11, n, (L0, L1))
+        lat = {"ms": lat_ms, "config": "c3: 1 individual x 40000 features x 11 classes, device-resident",
+               "bit_exact_vs_reference": bool(g3 is not None and n == 8192 and
+                                              sha(o1.cpu().numpy().view(np.uint32).astype(np.uint64)) == g3["packed_sha256"]),
+               "roofline": {"int_frac": M3 / bfly_peak * 1000.0 / lat_ms, "hbm_frac": bi3 / (hbm * 1e9) * 1000.0 / lat_ms,
+                            "model": "SURVEY 8(d) per-inference bytes and modmuls at R = 1"}}
+        del d1, ew3
 
     # client side of the result: decrypt + CRT unpack on the device
     # (unpack_results, matmul.cpp:257-271), checked against the exact product
     check = None
     if rank == 0:
-        # world > 1: d_out is the all-reduced result of every rank's rows
-        # (rank r encrypted synthetic(seed = 7 + r)); rank 0 regenerates them
-        rows_all = world * R
-        packed = d_out.cpu().numpy().view(np.uint32).astype(np.uint64)
-        srv.unpack_results(packed, rows_all, cols)  # warm
+        # world > 1: d_out is the reduced result of every rank's rows
+        srv.unpack_results(packed_dev, rows_all, cols)  # warm
         t0 = time.perf_counter()
-        got = srv.unpack_results(packed, rows_all, cols)
+        got = srv.unpack_results(packed_dev, rows_all, cols)
         dec_ms = (time.perf_counter() - t0) * 1000.0
-        x_all = x if world == 1 else np.concatenate(
-            [synthetic(R, f, cols, pf, ws, seed=7 + r)[0] for r in range(world)], axis=0)
+        x_all = x if world == 1 else workload(rows_all, f, cols, pf, ws)[0]
         want = np.rint(x_all.astype(np.float64) @ w.astype(np.float64)).astype(np.int64) + b  # exact: |sums| < 2^53
         check = {"decrypted_equals_integer_product": bool(np.array_equal(got, want)), "client_decrypt_ms": dec_ms,
                  "keygen_ms": keygen_ms, "client_encrypt_ms": enc_ms}
 
     if rank != 0:
         return
-    cpu = None
+    cpu = cpu_lat = cpu_std = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            res = reference_sample(args.config)
+            res = reference_sample(args.config, rows=min(R, 32))
             if res:
-                rate, sample, threads, secs, _ = res
+                rate, sample, threads, secs, ref = res
+                ref.close()
                 cpu = {"value": rate, "unit": "inferences/s", "cores": threads, "kind": "reference", "sample": sample,
                        "seconds": secs}
+            if args.latency:
+                cpu_lat = reference_latency()
+            if args.baseline:
+                cpu_std = reference_standard()
         except Exception as e:  # report, never fail the bench on the CPU leg
             cpu = {"error": str(e)}
     line = {
@@ -535,21 +671,30 @@ def run_ours(args, world, rank, local):
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {R} individuals/rank x {f} features x {cols} classes, N={n}, "
                                f"twin t=({T0},{T1 if n < 16384 else T1_16K}), L=({len(q0)},{len(q1)})",
-                   "inputs": "real encryptions (device keygen from Prng(1), client encryption with Prng(2),(3)) of "
-                             "seeded Bernoulli features, resident in HBM; inputs > L2 (no flush needed)",
+                   "inputs": "seeded util::Prng(7) workload (SURVEY 8d), real encryptions (device keygen from "
+                             "Prng(1), client encryption with Prng(2),(3)), resident in HBM; inputs > L2 (no flush "
+                             "needed)",
                    "parallelism": f"dp{world} (individual sharding)" + (
                        f", exchange={exchange}" if world > 1 else "")},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "bit_exact_vs_reference": None if parity is None else all(v for k, v in parity.items() if k != "golden"),
+        "parity": parity,
     }
     line["roofline"] = roof
     line["int_roofline"] = int_roof
+    line["step_roofline"] = step_roof
     if lat is not None:
-        line["latency_ms_single_individual"] = lat
+        line["latency_single_individual"] = lat
+        line["latency_ms_single_individual"] = lat["ms"]
+        if cpu_lat is not None:
+            lat["cpu_baseline"] = cpu_lat
     if base is not None:
         line["standard_algorithm"] = base
+        if cpu_std is not None:
+            base["cpu_baseline"] = cpu_std
     if check is not None:
         line["client_roundtrip"] = check
     print(json.dumps(line), flush=True)

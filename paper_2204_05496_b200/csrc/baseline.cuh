@@ -1,19 +1,18 @@
 // Standard (sample-batched) comparator on the device:
-// hei::matmul::baseline_matmul (proj/src/matmul/matmul.cpp:415-486).
+// hei::matmul::baseline_matmul (proj/src/matmul/matmul.cpp:273-344).
 //
-// Per feature k and sample block: the column x[:, k] is encrypted with the
-// public key (BfvContext::encrypt_parts, context.cpp:262-303) using the SAME
-// randomness stream as the reference's util::Prng (rng.hpp:19-68), then
-// multiplied by the all-slot constant w(k, j) for every class j and summed.
-//
-// Device pipeline per batch of F features:
-//   k_mt_generate   mt19937_64 replay, one CTA per branch (the stream is
-//                   sequential; the twist runs as two parallel phases)
-//   k_bl_noise      u = v mod 3 - 1, (e0, e1) = Box-Muller pairs, llround
-//   k_bl_encode     m = INTT_t(scatter(centered col residues))
-//   k_bl_encrypt    c0 = NTT(u).pk0 + NTT(e0 + Delta m), c1 = NTT(u).pk1 + NTT(e1)
-//   k_bl_accum      acc[blk][j] += sum_k c_k * w(k, j)      (u64, order-free)
-// then k_bl_finish reduces mod q and adds the bias plaintext.
+// Per feature k and sample block the reference encrypts the column x[:, k]
+// with the public key (BfvContext::encrypt_parts, context.cpp:262-303) using
+// its util::Prng stream (rng.hpp:19-68), multiplies it by the all-slot
+// constant w(k, j) for every class j and sums. The device draws the SAME
+// stream and sums by linearity (stdalg_kernels.cuh):
+//   k_mt_chunks /   mt19937_64 replay: jump-ahead chunk generators, or one
+//   k_mt_generate   sequential CTA per branch
+//   k_bl_noise_p    u = v mod 3 - 1, (e0, e1) = Box-Muller pairs, llround
+//   k_bl_encode     m = INTT_t(scatter(centered column residues))
+//   k_bl_sums       exact int64 sums over features of w' u, w' e0, w' e1, w' m
+//   k_bl_fold_sums  -> residues mod every q_i
+//   k_bl_finish_lin c0 = NTT(A) pk0 + NTT(B) + bias, c1 = NTT(A) pk1 + NTT(C)
 #pragma once
 
 namespace heb_baseline {

@@ -417,8 +417,6 @@ struct hei_gpu_ctx {
   int ks14_half = 2;  // HEI_KS14_HALF: N = 16384 full-batch key switch as half-ring blocks (2: one launch per
                      // branch with both halves side by side; 1: one launch per half; 0: the 1024-thread kernel)
   bool ks14_tmem = true;  // HEI_KS14_TMEM=0: N = 16384 full batches keep the shared-memory accumulators
-  int bl_split = 1;        // HEI_BL_SPLIT: feature slices per k_bl_accum_w launch (accumulator copies)
-  bool bl_accum_w = true;  // HEI_BL_ACCUM_W: standard-algorithm sums with exact 64-bit products (k_bl_accum_w)
   int enc_minb = 3;  // HEI_ENC_MINB: resident CTAs/SM of the public-key encryption kernel (2 or 3)
   bool prime_major = false;  // HEI_PRIME_MAJOR: full-batch fold kernels walk (pair, prime) blocks prime-major
   int ks_tmem = 4;  // HEI_KS_TMEM: full-batch key switch accumulates in TMEM (0 off; 2, 3 CTAs/SM; 4: 3 CTAs/SM, 4-slot rounds)
@@ -1837,8 +1835,6 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_FOLD_PARTS"))
       c->fold_parts = std::min<uint32_t>(kMaxFoldParts, std::max(1, std::atoi(v)));
     if (const char* v = std::getenv("HEI_KS_TMEM")) c->ks_tmem = std::atoi(v);
-    if (const char* v = std::getenv("HEI_BL_SPLIT")) c->bl_split = std::max(1, std::atoi(v));
-    if (const char* v = std::getenv("HEI_BL_ACCUM_W")) c->bl_accum_w = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_ENC_MINB")) c->enc_minb = std::atoi(v);
     if (const char* v = std::getenv("HEI_PRIME_MAJOR")) c->prime_major = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_KS14_TMEM")) c->ks14_tmem = std::atoi(v) != 0;
@@ -2156,7 +2152,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     set_smem_attr((const void*)k_ct_ntt, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_poly_ntt, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_encode_weights, smem_bytes(c.get(), 1));
-    set_smem_attr((const void*)k_bl_finish, smem_bytes(c.get(), 1));
+    set_smem_attr((const void*)k_bl_finish_lin, 3 * (size_t)c->n * 4);
     set_smem_attr((const void*)k_bl_encode_g, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_bl_encrypt_g, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_prepare_pk_g, smem_bytes(c.get(), 1));
@@ -3228,43 +3224,39 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
       LAUNCHED();
       check_err_flag(c, HEI_CODEC_ERROR, "public key: coefficient not reduced");
     }
-    const uint64_t F = std::min<uint64_t>(f, std::max<uint64_t>(1, 256 / B));
+    // features per batch (one noise/encode/sum round); every batch's draws
+    // are the next F*B encryptions of both branch streams
+    const uint64_t F = std::min<uint64_t>(f, std::max<uint64_t>(1, 1024 / B));
     const uint64_t Emax = F * B;
     int64_t *d_x = nullptr, *d_w = nullptr, *d_bias = nullptr;
     uint2* d_wc = nullptr;
-    unsigned long long* d_acc = nullptr;
     uint64_t *d_raw = nullptr, *d_state = nullptr;
-    int8_t* d_noise = nullptr;
-    uint32_t *d_m = nullptr, *d_ct = nullptr, *d_out = nullptr;
+    uint32_t *d_noisep = nullptr, *d_m = nullptr, *d_res = nullptr, *d_out = nullptr;
+    long long* d_sums = nullptr;
     uint64_t* d_out64 = nullptr;
-    struct Free {
-      std::vector<void*> p;
-      ~Free() {
-        for (void* x : p) cudaFree(x);
-      }
-    } fr;
-    auto alloc = [&](auto** ptr, size_t bytes) {
-      CU(cudaMalloc((void**)ptr, bytes));
-      fr.p.push_back((void*)*ptr);
-    };
     const size_t outw = B * cols * c->ct_words();
+    // feature slices per k_bl_sums launch: enough blocks to fill the GPU
+    const uint32_t tiles = std::max<uint32_t>(1, n / 128), grp = (uint32_t)((cols + kBlSumJ - 1) / kBlSumJ);
+    const uint64_t base_blocks = (uint64_t)tiles * grp * B * 2;
+    const uint32_t S = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>({8, F, (2048 + base_blocks - 1) / base_blocks}));
+    const size_t sums_words = (size_t)S * B * cols * 2 * 5 * n;
     d_x = scratch<int64_t>(c, kScrX, rows * f * 8);
     d_w = scratch<int64_t>(c, kScrW, f * cols * 8);
     d_bias = scratch<int64_t>(c, kScrBias, cols * 8);
     d_wc = scratch<uint2>(c, kScrWc, f * cols * P * sizeof(uint2));
-    const uint32_t S = c->bl_accum_w ? std::max(1, c->bl_split) : 1;  // accumulator copies (k_bl_accum_w slices)
-    d_acc = scratch<unsigned long long>(c, kScrAcc, outw * 8 * S);
+    d_sums = scratch<long long>(c, kScrAcc, sums_words * 8);
+    d_res = scratch<uint32_t>(c, kScrCt, (size_t)B * cols * P * 3 * n * 4);
     d_raw = scratch<uint64_t>(c, kScrRaw, 2 * 2 * Emax * 3 * n * 8);  // [slot][branch][draws]
     d_state = scratch<uint64_t>(c, kScrState, 2 * 313 * 8);
-    d_noise = scratch<int8_t>(c, kScrNoise, Emax * 2 * 3 * n);
+    d_noisep = scratch<uint32_t>(c, kScrNoise, Emax * 2 * n * 4);
     d_m = scratch<uint32_t>(c, kScrM, Emax * 2 * n * 4);
-    d_ct = scratch<uint32_t>(c, kScrCt, Emax * c->ct_words() * 4);
     d_out = scratch<uint32_t>(c, kScrOut, outw * 4);
     d_out64 = scratch<uint64_t>(c, kScrOut64, outw * 8);
     CU(cudaMemcpyAsync(d_x, x, rows * f * 8, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(d_w, w, f * cols * 8, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(d_bias, bias, cols * 8, cudaMemcpyHostToDevice, st));
-    CU(cudaMemsetAsync(d_acc, 0, outw * 8 * S, st));
+    CU(cudaMemsetAsync(d_sums, 0, sums_words * 8, st));
+    CU(cudaMemsetAsync(d_res, 0, (size_t)B * cols * P * 3 * n * 4, st));
     uint64_t hstate[2][313];
     for (int b = 0; b < 2; ++b) {
       hei_gpu_prng* r = b ? rng1 : rng0;
@@ -3278,8 +3270,8 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     // e.g. fresh Prngs), the whole call's draws are produced by K chunk
     // generators per branch whose start states come from x^C mod phi
     // (k_mt_jumps), instead of one sequential generator per branch. A
-    // rejection anywhere would misalign the chunks; k_bl_noise flags it at
-    // its exact position and the call re-runs on the sequential path.
+    // rejection anywhere would misalign the chunks; the noise kernel flags it
+    // at its exact position and the call re-runs on the sequential path.
     const uint64_t E_total = f * B, Dtot = E_total * 3 * n;
     bool jump = c->mt_jump && !force_seq && hstate[0][312] == 312 && hstate[1][312] == 312 && E_total >= 64 &&
                 Dtot * 16 <= ((uint64_t)48 << 30);
@@ -3297,10 +3289,9 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
       LAUNCHED();
     }
     const size_t sm1 = smem_bytes(c, 1);
-    const unsigned at = std::min<uint32_t>(256, n);
     // The mt19937_64 replay is sequential per branch (one CTA each), so the
     // next batch's draws are generated on a side stream while the current
-    // batch is encrypted and accumulated (double-buffered raw draws).
+    // batch is summed (double-buffered raw draws).
     if (!c->copy_stream) CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     cudaStream_t ms = c->copy_stream;
     cudaEvent_t gen[2], used[2];
@@ -3318,18 +3309,24 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
       LAUNCHED();
       CU(cudaEventRecord(gen[slot], ms));
     };
+    auto fold_sums = [&]() {
+      k_bl_fold_sums<<<grid_for((uint64_t)B * cols * P * n, 256), 256, 0, st>>>(g, d_sums, S, (uint32_t)B,
+                                                                                (uint32_t)cols, d_res);
+      LAUNCHED();
+      CU(cudaMemsetAsync(d_sums, 0, sums_words * 8, st));
+    };
     generate(0, 0);
     int slot = 0;
+    uint64_t since_fold = 0;
     for (uint64_t k0 = 0; k0 < f; k0 += F, slot ^= 1) {
       const uint64_t Fb = std::min<uint64_t>(F, f - k0), E = Fb * B, draws = E * 3 * n;
       if (k0 + F < f) generate(k0 + F, slot ^ 1);
       if (jump) {
-        heb_baseline::k_bl_noise<<<dim3((unsigned)E, 2), 256, 0, st>>>(d_rawall + k0 * B * 3 * n, Dtot, n, (uint32_t)E,
-                                                                      d_noise, c->d_err);
+        k_bl_noise_p<<<dim3((unsigned)E, 2), 256, 0, st>>>(d_rawall + k0 * B * 3 * n, Dtot, n, d_noisep, c->d_err);
       } else {
         CU(cudaStreamWaitEvent(st, gen[slot], 0));
-        heb_baseline::k_bl_noise<<<dim3((unsigned)E, 2), 256, 0, st>>>(d_raw + (size_t)slot * 2 * Emax * 3 * n, draws,
-                                                                      n, (uint32_t)E, d_noise, c->d_err);
+        k_bl_noise_p<<<dim3((unsigned)E, 2), 256, 0, st>>>(d_raw + (size_t)slot * 2 * Emax * 3 * n, draws, n,
+                                                           d_noisep, c->d_err);
       }
       LAUNCHED();
       CU(cudaEventRecord(used[slot], st));
@@ -3337,26 +3334,25 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
                    (k_bl_encode<LG><<<dim3((unsigned)E, 2), Ntt<LG>::T, sm1, st>>>(g, d_x, rows, f, k0, (uint32_t)B, d_m)),
                    (k_bl_encode_g<<<dim3((unsigned)E, 2), c->threads(), sm1, st>>>(g, d_x, rows, f, k0, (uint32_t)B, d_m)));
       LAUNCHED();
-      launch_bl_encrypt(c, g, (unsigned)(E * P), d_noise, d_m, d_ct, sm1, st);
+      const uint32_t Sb = (uint32_t)std::min<uint64_t>(S, Fb);
+      k_bl_sums<<<dim3(tiles * grp, Sb, (unsigned)(B * 2)), std::min<uint32_t>(128, n), 0, st>>>(
+          g, d_noisep, d_m, (uint32_t)Fb, (uint32_t)B, (uint32_t)cols, d_wc + k0 * cols * P, d_sums);
       LAUNCHED();
-      for (uint32_t j0 = 0; j0 < cols; j0 += kBlJ) {
-        const unsigned blocks = (unsigned)(B * 2 * P * (n / at));
-        if (c->bl_accum_w)
-          k_bl_accum_w<<<dim3(blocks, S), at, Fb * kBlJ * sizeof(uint32_t), st>>>(
-              g, d_ct, (uint32_t)Fb, (uint32_t)B, (uint32_t)cols, j0, d_wc + k0 * cols * P, d_acc, outw);
-        else
-          k_bl_accum<<<blocks, at, Fb * kBlJ * sizeof(uint2), st>>>(g, d_ct, (uint32_t)Fb, (uint32_t)B, (uint32_t)cols,
-                                                                    j0, d_wc + k0 * cols * P, d_acc);
-        LAUNCHED();
+      since_fold += Fb;
+      if (since_fold + F > (1u << 17)) {  // keep every int64 sum below 2^63
+        fold_sums();
+        since_fold = 0;
       }
     }
+    if (since_fold) fold_sums();
     CU(cudaStreamSynchronize(ms));
     for (int k = 0; k < 2; ++k) {
       cudaEventDestroy(gen[k]);
       cudaEventDestroy(used[k]);
     }
     (void)fast;
-    k_bl_finish<<<(unsigned)(B * cols * P), c->threads(), sm1, st>>>(g, d_acc, d_bias, (uint32_t)cols, d_out, S, outw);
+    k_bl_finish_lin<<<(unsigned)(B * cols * P), c->threads(), 3 * n * 4, st>>>(g, d_res, c->d_pk[0], c->d_pk[1],
+                                                                                d_bias, (uint32_t)cols, d_out);
     LAUNCHED();
     k_widen<<<grid_for(outw, 256), 256, 0, st>>>(d_out, d_out64, outw);
     LAUNCHED();

@@ -115,171 +115,186 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_bl_encrypt(Geo g, const 
   }
 }
 
-// acc[blk][j] += sum_k ct[k, blk] * w(k, j) mod q, lazily in u64
-// (mul_plain + add_inplace of matmul.cpp:453-459). Thread per slot x of one
-// poly; weights of the batch for this branch sit in shared memory. The
-// feature loop is unrolled so several coalesced loads are in flight.
-constexpr int kBlJ = 12;
-__global__ void k_bl_accum(Geo g, const uint32_t* __restrict__ cts, uint32_t F, uint32_t B, uint32_t cols,
-                           uint32_t j0, const uint2* __restrict__ wc, unsigned long long* __restrict__ acc) {
-  extern __shared__ uint2 wsm[];  // [F][kBlJ]
-  const uint32_t n = g.n, polys = 2 * g.P;
-  const uint32_t tiles = n / blockDim.x;
-  const uint32_t tile = blockIdx.x % tiles;
-  const uint32_t poly = (blockIdx.x / tiles) % polys;
-  const uint32_t blk = blockIdx.x / (tiles * polys);
-  const uint32_t gp = poly_prime(g, poly);
-  const uint32_t q = g.pr[gp].q;
-  const uint32_t jn = min((uint32_t)kBlJ, cols - j0);
-  for (uint32_t x = threadIdx.x; x < F * kBlJ; x += blockDim.x) {
-    const uint32_t kk = x / kBlJ, jj = x % kBlJ;
-    wsm[x] = jj < jn ? wc[((uint64_t)kk * cols + j0 + jj) * g.P + gp] : make_uint2(0, 0);
-  }
-  __syncthreads();
-  const uint32_t xs = tile * blockDim.x + threadIdx.x;
-  const uint32_t* src = cts + (uint64_t)blk * g.ct_words + (uint64_t)poly * n + xs;
-  const uint64_t stride = (uint64_t)B * g.ct_words;
-  unsigned long long a[kBlJ];
-#pragma unroll
-  for (int jj = 0; jj < kBlJ; ++jj) a[jj] = 0;
-  if (g.br[g.pr[gp].b].t < (1u << 20)) {
-    // small plaintext modulus: the weight residues are < 2^20, so the exact
-    // products (< 2^51) accumulate with one IMAD.WIDE each; this batch's
-    // sums (< 2^59) are reduced mod q before they reach the accumulator
-#pragma unroll 8
-    for (uint32_t kk = 0; kk < F; ++kk) {
-      const uint64_t v = src[kk * stride];
-#pragma unroll
-      for (int jj = 0; jj < kBlJ; ++jj) a[jj] += v * wsm[kk * kBlJ + jj].x;
-    }
-#pragma unroll
-    for (int jj = 0; jj < kBlJ; ++jj) a[jj] %= q;
-  } else {
-#pragma unroll 8
-    for (uint32_t kk = 0; kk < F; ++kk) {
-      const uint32_t v = src[kk * stride];
-#pragma unroll
-      for (int jj = 0; jj < kBlJ; ++jj) {
-        const uint2 w = wsm[kk * kBlJ + jj];
-        const uint32_t qh = __umulhi(v, w.y);
-        a[jj] += (uint32_t)(v * w.x - qh * q);  // in [0, 2q): reduced at the end
-      }
-    }
-  }
-#pragma unroll
-  for (uint32_t jj = 0; jj < kBlJ; ++jj) {
-    if (jj < jn) {
-      unsigned long long* d = acc + (((uint64_t)blk * cols + j0 + jj) * g.ct_words) + (uint64_t)poly * n + xs;
-      *d += a[jj];
-    }
-  }
-}
-
-// Same sums with exact 64-bit products and no Shoup step: every weight
-// residue is < t < 2^31 and every ct residue < q < 2^31, so v * w < 2^62 and
-// one IMAD.WIDE.U32 accumulates it. The accumulator is folded every 3
-// features (a -> hi(a) * (2^32 mod q) + lo(a), congruent mod q): with k = 3
-// products of < 2^61 (t0 < 2^30) between folds the bound stays below
-// 3 * 2^62 + 2^33 < 2^64. For t < 2^20 (products < 2^51) no fold is needed
-// within a batch. The batch sum is reduced mod q before it reaches `acc`, so
-// the result equals k_bl_accum's mod q exactly. Weights (values only) are
-// read from shared memory as 3 x 128-bit per feature.
+// ---------------------------------------------------------------------------
+// Standard algorithm by linearity (the path hei_gpu_baseline_matmul runs).
 //
-// The batch's features are split over S block slices (blockIdx.y); slice s
-// sums its feature range into its own accumulator copy acc + s * slice_words
-// (k_bl_finish adds the copies), so a launch has S times the blocks.
-__global__ void k_bl_accum_w(Geo g, const uint32_t* __restrict__ cts, uint32_t F, uint32_t B, uint32_t cols,
-                             uint32_t j0, const uint2* __restrict__ wc, unsigned long long* __restrict__ acc,
-                             uint64_t slice_words) {
-  static_assert(kBlJ == 12, "3 x uint4 of weights per feature");
-  extern __shared__ uint4 wsm4[];  // [F][3] = [F][kBlJ] u32
-  uint32_t* wsm = reinterpret_cast<uint32_t*>(wsm4);
-  const uint32_t n = g.n, polys = 2 * g.P;
-  const uint32_t tiles = n / blockDim.x;
-  const uint32_t tile = blockIdx.x % tiles;
-  const uint32_t poly = (blockIdx.x / tiles) % polys;
-  const uint32_t blk = blockIdx.x / (tiles * polys);
-  const uint32_t gp = poly_prime(g, poly);
-  const uint32_t q = g.pr[gp].q;
-  const uint32_t jn = min((uint32_t)kBlJ, cols - j0);
-  const uint32_t k_lo = (uint32_t)((uint64_t)F * blockIdx.y / gridDim.y);
-  F = (uint32_t)((uint64_t)F * (blockIdx.y + 1) / gridDim.y) - k_lo;
-  acc += blockIdx.y * slice_words;
-  for (uint32_t x = threadIdx.x; x < F * kBlJ; x += blockDim.x) {
-    const uint32_t kk = x / kBlJ, jj = x % kBlJ;
-    wsm[x] = jj < jn ? wc[((uint64_t)(k_lo + kk) * cols + j0 + jj) * g.P + gp].x : 0u;
-  }
-  __syncthreads();
-  const uint32_t xs = tile * blockDim.x + threadIdx.x;
-  const uint64_t stride = (uint64_t)B * g.ct_words;
-  const uint32_t* src = cts + (uint64_t)blk * g.ct_words + (uint64_t)poly * n + xs + k_lo * stride;
-  unsigned long long a[kBlJ];
-#pragma unroll
-  for (int jj = 0; jj < kBlJ; ++jj) a[jj] = 0;
-  auto mac = [&](uint32_t kk) {
-    const uint64_t v = src[kk * stride];
-    const uint4 w0 = wsm4[3 * kk], w1 = wsm4[3 * kk + 1], w2 = wsm4[3 * kk + 2];
-    const uint32_t w[kBlJ] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w, w2.x, w2.y, w2.z, w2.w};
-#pragma unroll
-    for (int jj = 0; jj < kBlJ; ++jj) a[jj] += v * w[jj];
-  };
-  if (g.br[g.pr[gp].b].t < (1u << 20)) {
-#pragma unroll 8
-    for (uint32_t kk = 0; kk < F; ++kk) mac(kk);
-  } else {
-    const uint64_t R = (uint64_t)((1ull << 32) % q);
-    uint32_t kk = 0;
-#pragma unroll 2
-    for (; kk + 3 <= F; kk += 3) {
-      mac(kk);
-      mac(kk + 1);
-      mac(kk + 2);
-#pragma unroll
-      for (int jj = 0; jj < kBlJ; ++jj) a[jj] = (a[jj] >> 32) * R + (a[jj] & 0xffffffffull);
-    }
-    for (; kk < F; ++kk) mac(kk);
-  }
-#pragma unroll
-  for (uint32_t jj = 0; jj < kBlJ; ++jj) {
-    if (jj < jn) {
-      unsigned long long* d = acc + (((uint64_t)blk * cols + j0 + jj) * g.ct_words) + (uint64_t)poly * n + xs;
-      *d += a[jj] % q;
-    }
+// The reference accumulates, per output (row block blk, class j) and prime
+// q_i, acc = sum_k ct_k (x) w'_kj with ct_k = Enc(m_k; u_k, e0_k, e1_k) and
+// w'_kj = [w_kj]_t the constant plaintext (prepare_constant_signed,
+// twin.cpp:131-143; context.cpp:120-137), i.e. in eval form
+//   acc.c0 = sum_k w'_kj (NTT(u_k) pk0 + NTT(e0_k + Delta m_k))
+//   acc.c1 = sum_k w'_kj (NTT(u_k) pk1 + NTT(e1_k))          mod q_i
+// (encrypt_parts, context.cpp:262-303; mul_plain + add_inplace,
+// matmul.cpp:303-320). Every step is exact arithmetic mod q_i and the NTT is
+// linear, so the same residues are
+//   acc.c0 = NTT([sum_k w' u_k]) pk0 + NTT([sum_k w' e0_k] + Delta [sum_k w' m_k])
+//   acc.c1 = NTT([sum_k w' u_k]) pk1 + NTT([sum_k w' e1_k])
+// -- three transforms per (blk, j, prime) instead of 3 + 2 per (feature,
+// prime). The sums over features are exact integer sums of the SAME sampled
+// noise (the full util::Prng stream is still drawn and consumed in order) and
+// the same encoded columns m_k = INTT_t(column k), reduced mod q_i at the end.
+// ---------------------------------------------------------------------------
+
+// Noise of one encryption per (e, branch), packed: raw draws [3][N] ->
+// u32 [N] with byte 0 = u + 1, byte 1 = e0, byte 2 = e1 (sample_ternary,
+// sample_gaussian twice; sampling.cpp:16-34). A thread takes coefficient pair
+// (2k, 2k+1): the Box-Muller pair of Prng::gaussian (cos first, sin as the
+// cached spare, rng.hpp:47-62). A rejection would shift the stream: flagged.
+__global__ void k_bl_noise_p(const uint64_t* __restrict__ raw, uint64_t count, uint32_t n,
+                             uint32_t* __restrict__ noisep, uint32_t* err) {
+  const uint32_t e = blockIdx.x, b = blockIdx.y;
+  const uint64_t* d = raw + (uint64_t)b * count + (uint64_t)e * 3 * n;
+  uint2* o = reinterpret_cast<uint2*>(noisep + ((uint64_t)e * 2 + b) * n);
+  for (uint32_t k = threadIdx.x; k < n / 2; k += blockDim.x) {
+    const uint64_t v0 = d[2 * k], v1 = d[2 * k + 1];
+    if (v0 == ~0ull || v1 == ~0ull) *err = 1;
+    int8_t a0, a1, c0, c1;
+    bool ok = heb_baseline::box_muller_pair(d[n + 2 * k], d[n + 2 * k + 1], a0, a1);
+    ok &= heb_baseline::box_muller_pair(d[2 * n + 2 * k], d[2 * n + 2 * k + 1], c0, c1);
+    if (!ok) *err = 1;
+    const uint32_t u0 = (uint32_t)(v0 % 3), u1 = (uint32_t)(v1 % 3);  // u + 1
+    o[k] = make_uint2(u0 | ((uint32_t)(uint8_t)a0 << 8) | ((uint32_t)(uint8_t)c0 << 16),
+                      u1 | ((uint32_t)(uint8_t)a1 << 8) | ((uint32_t)(uint8_t)c1 << 16));
   }
 }
 
-// finish of the baseline (matmul.cpp:464-476): reduce, then part0 +=
-// NTT(Delta * INTT_t(all slots = bias[j])). Block per ((blk, j), gp).
-__global__ void k_bl_finish(Geo g, const unsigned long long* __restrict__ acc, const int64_t* __restrict__ bias,
-                            uint32_t cols, uint32_t* __restrict__ out, uint32_t S = 1, uint64_t slice_words = 0) {
-  extern __shared__ uint32_t sm[];
+// Feature sums of one batch: thread per coefficient x, block per (x tile,
+// class group of J, feature slice s, row block, branch). Five exact int64
+// sums per class: su = sum w' u, se0 = sum w' e0, se1 = sum w' e1 and the
+// column sum sum w' m split as w' = wh 2^15 + wl (m < t < 2^31, so every
+// product is < 2^46 and 2^17 features stay below 2^63). sums layout
+// [s][blk][j][b][5][n]; each element has one owner per launch (plain RMW).
+constexpr int kBlSumJ = 4;
+__global__ void __launch_bounds__(128) k_bl_sums(Geo g, const uint32_t* __restrict__ noisep,
+                                                 const uint32_t* __restrict__ m, uint32_t Fb, uint32_t B,
+                                                 uint32_t cols, const uint2* __restrict__ wc,
+                                                 long long* __restrict__ sums) {
+  constexpr int J = kBlSumJ;
+  __shared__ uint32_t wsm[1024 * J];
+  const uint32_t n = g.n, G = (cols + J - 1) / J;
+  const uint32_t tile = blockIdx.x / G, grp = blockIdx.x - tile * G;
+  const uint32_t x = tile * blockDim.x + threadIdx.x;
+  const uint32_t blk = blockIdx.z >> 1, b = blockIdx.z & 1, S = gridDim.y, s = blockIdx.y;
+  const uint32_t k_lo = (uint32_t)((uint64_t)Fb * s / S), k_hi = (uint32_t)((uint64_t)Fb * (s + 1) / S);
+  const uint32_t j0 = grp * J, jn = min((uint32_t)J, cols - j0);
+  const uint32_t gp0 = b ? g.L[0] : 0;  // w' = [w]_t is the same value for every prime of the branch
+  for (uint32_t i = threadIdx.x; i < (k_hi - k_lo) * J; i += blockDim.x) {
+    const uint32_t kk = i / J, jj = i - kk * J;
+    wsm[i] = jj < jn ? wc[((uint64_t)(k_lo + kk) * cols + j0 + jj) * g.P + gp0].x : 0u;
+  }
+  __syncthreads();
+  long long su[J], s0[J], s1[J];
+  unsigned long long ml[J], mh[J];
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) su[jj] = s0[jj] = s1[jj] = 0, ml[jj] = mh[jj] = 0;
+  const uint64_t estride = (uint64_t)B * 2 * n;
+  const uint32_t* np = noisep + ((uint64_t)(k_lo * B + blk) * 2 + b) * n + x;
+  const uint32_t* mp = m + ((uint64_t)(k_lo * B + blk) * 2 + b) * n + x;
+#pragma unroll 4
+  for (uint32_t kk = 0; kk < k_hi - k_lo; ++kk) {
+    const uint32_t pk = __ldg(np + kk * estride);
+    const uint32_t mv = __ldg(mp + kk * estride);
+    const int u = (int)(pk & 0xff) - 1, e0 = (int8_t)(pk >> 8), e1 = (int8_t)(pk >> 16);
+    const uint4 w4 = *reinterpret_cast<const uint4*>(wsm + kk * J);
+    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+      const int wi = (int)w[jj];  // w' < t < 2^31
+      su[jj] += (long long)wi * u;
+      s0[jj] += (long long)wi * e0;
+      s1[jj] += (long long)wi * e1;
+      ml[jj] += (unsigned long long)mv * (w[jj] & 0x7fffu);
+      mh[jj] += (unsigned long long)mv * (w[jj] >> 15);
+    }
+  }
+  if (x >= n) return;
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    if ((uint32_t)jj >= jn) break;
+    long long* o = sums + ((((uint64_t)s * B + blk) * cols + j0 + jj) * 2 + b) * 5 * n + x;
+    o[0] += su[jj];
+    o[n] += s0[jj];
+    o[2 * (uint64_t)n] += s1[jj];
+    o[3 * (uint64_t)n] += (long long)ml[jj];
+    o[4 * (uint64_t)n] += (long long)mh[jj];
+  }
+}
+
+// Fold the int64 feature sums (all S slices) into residues mod every prime
+// of the branch: res [blk*cols + j][gp][3][n] u32, accumulated mod q:
+// [su], [se0 + Delta (ml + mh 2^15)], [se1]. Run at least every 2^17
+// features and at the end; the caller zeroes `sums` afterwards.
+__global__ void k_bl_fold_sums(Geo g, const long long* __restrict__ sums, uint32_t S, uint32_t B, uint32_t cols,
+                               uint32_t* __restrict__ res) {
   const uint32_t n = g.n;
-  const uint64_t c = blockIdx.x / g.P;  // (blk * cols + j)
+  const uint64_t total = (uint64_t)B * cols * g.P * n;
+  for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = (uint32_t)(idx % n);
+    const uint64_t cg = idx / n;
+    const uint32_t gp = (uint32_t)(cg % g.P);
+    const uint64_t c = cg / g.P;  // blk * cols + j
+    const PrimeInfo& pr = g.pr[gp];
+    const uint32_t q = pr.q;
+    long long a[5] = {0, 0, 0, 0, 0};
+    for (uint32_t s = 0; s < S; ++s) {
+      const long long* p = sums + (((uint64_t)s * B * cols + c) * 2 + pr.b) * 5 * n + x;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) a[k] += p[(uint64_t)k * n];
+    }
+    auto smod = [q](long long v) -> uint32_t {
+      long long r = v % (long long)q;
+      return (uint32_t)(r < 0 ? r + q : r);
+    };
+    const uint32_t ml = (uint32_t)((unsigned long long)a[3] % q), mh = (uint32_t)((unsigned long long)a[4] % q);
+    const uint32_t mm = (uint32_t)(((uint64_t)mh << 15) % q);
+    const uint32_t msum = add_mod(ml, mm, q);
+    uint32_t* r = res + (c * g.P + gp) * 3 * n + x;
+    r[0] = add_mod(r[0], smod(a[0]), q);
+    r[n] = add_mod(r[n], add_mod(smod(a[1]), mul_shoup(msum, pr.delta.x, pr.delta.y, q), q), q);
+    r[2 * n] = add_mod(r[2 * n], smod(a[2]), q);
+  }
+}
+
+// Finish per ((blk, j), prime): c0 = NTT(A) NTT(pk0) + NTT(Bv) + [Delta r_j],
+// c1 = NTT(A) NTT(pk1) + NTT(Cv), with (A, Bv, Cv) the folded residues and
+// r_j = [bias_j]_t: the bias plaintext (all slots r_j) is the constant
+// polynomial r_j, so NTT(Delta r_j) is Delta r_j in every slot
+// (add_plain_inplace, context.cpp:393-402; matmul.cpp:328-335).
+// pk is the coefficient-form public key [b][part][prime][n] u64.
+__global__ void k_bl_finish_lin(Geo g, const uint32_t* __restrict__ res, const uint64_t* __restrict__ pk0,
+                                const uint64_t* __restrict__ pk1, const int64_t* __restrict__ bias, uint32_t cols,
+                                uint32_t* __restrict__ out) {
+  extern __shared__ uint32_t smf[];
+  const uint32_t n = g.n;
+  uint32_t *S1 = smf, *S2 = smf + n, *S3 = smf + 2 * n;
+  const uint64_t c = blockIdx.x / g.P;
   const uint32_t gp = blockIdx.x % g.P;
   const PrimeInfo& pr = g.pr[gp];
-  const BranchInfo& br = g.br[pr.b];
-  const int64_t t = br.t;
-  int64_t r = bias[c % cols] % t;
-  if (r < 0) r += t;
-  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) sm[g.index_map[s]] = (uint32_t)r;
-  __syncthreads();
-  ntt_inv_smem(sm, g.inv + (size_t)(g.P + pr.b) * n, br.t, n, g.logn, br.last, br.ninv);
   const uint32_t q = pr.q;
-  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) sm[x] = mul_shoup(sm[x], pr.delta.x, pr.delta.y, q);
+  const uint2* tw = g.fwd + (size_t)gp * n;
+  const uint32_t* r = res + (c * g.P + gp) * 3 * n;
+  const uint64_t* pk = (pr.b ? pk1 : pk0);
+  int64_t bt = bias[c % cols] % (int64_t)g.br[pr.b].t;
+  if (bt < 0) bt += g.br[pr.b].t;
+  const uint32_t bd = mul_shoup((uint32_t)bt, pr.delta.x, pr.delta.y, q);
+  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) S1[x] = r[x];
   __syncthreads();
-  ntt_fwd_smem(sm, g.fwd + (size_t)gp * n, q, n, g.logn);
-  const unsigned long long* a0 = acc + c * g.ct_words + (uint64_t)pr.poly0 * n;
-  const unsigned long long* a1 = acc + c * g.ct_words + (uint64_t)pr.poly1 * n;
-  uint32_t* o0 = out + c * g.ct_words + (uint64_t)pr.poly0 * n;
-  uint32_t* o1 = out + c * g.ct_words + (uint64_t)pr.poly1 * n;
-  for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
-    unsigned long long s0 = a0[x], s1 = a1[x];  // each copy < 2^40: the sum cannot wrap
-    for (uint32_t k = 1; k < S; ++k) {
-      s0 += a0[x + k * slice_words];
-      s1 += a1[x + k * slice_words];
+  ntt_fwd_smem(S1, tw, q, n, g.logn);
+  for (int part = 0; part < 2; ++part) {
+    for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+      S2[x] = (uint32_t)pk[((uint64_t)part * pr.L + pr.i) * n + x];
+      S3[x] = r[(uint64_t)(1 + part) * n + x];
     }
-    o0[x] = add_mod((uint32_t)(s0 % q), sm[x], q);
-    o1[x] = (uint32_t)(s1 % q);
+    __syncthreads();
+    ntt_fwd_smem(S2, tw, q, n, g.logn);
+    ntt_fwd_smem(S3, tw, q, n, g.logn);
+    uint32_t* o = out + c * g.ct_words + (uint64_t)(part ? pr.poly1 : pr.poly0) * n;
+    for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) {
+      uint32_t v = add_mod(mul_barrett(S1[x], S2[x], q, pr.mu), S3[x], q);
+      o[x] = part ? v : add_mod(v, bd, q);
+    }
+    __syncthreads();
   }
 }
 
