@@ -1,6 +1,6 @@
-// Fast-algorithm kernels (MatmulStream::push_row / finish, matmul.cpp:256-379):
-// ciphertext NTTs, chunk products, digit INTTs, key switching (full-batch,
-// latency and split variants), mask + packed accumulation, bias and finish,
+// Fast-algorithm kernels (MatmulStream::push_row / finish, matmul.cpp:165-232):
+// ciphertext NTTs, chunk products, digit INTTs, key switching (small-batch
+// and latency kernels), mask + packed accumulation, bias and finish,
 // weight/key preparation. Textually included by heinfer_b200.cu inside its
 // kernel namespace (uses Geo, PrimeInfo, BranchInfo, Ntt, modmath).
 #pragma once
@@ -347,7 +347,8 @@ __global__ void k_prepare_plain(Geo g, const uint64_t* __restrict__ vals, uint64
 // Galois keys of one branch: host [e][l][part][i][n] u64 -> device
 // [e][i][l][part][n] (val, shoup), the order k_rot_keyswitch streams them.
 __global__ void k_prepare_keys(Geo g, uint32_t b, uint32_t elts, const uint64_t* __restrict__ rows,
-                               uint2* __restrict__ out, uint32_t* err, uint32_t V) {
+                               uint2* __restrict__ out, uint32_t* err) {
+  constexpr uint32_t V = 16;  // slots per thread of the register-blocked transforms
   const uint32_t n = g.n, L = g.L[b], first = b ? g.L[0] : 0;
   const uint64_t total = (uint64_t)elts * L * 2 * L * n;
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
@@ -364,10 +365,11 @@ __global__ void k_prepare_keys(Geo g, uint32_t b, uint32_t elts, const uint64_t*
     const uint32_t q = g.pr[first + i].q;
     const uint64_t v = rows[x];
     if (v >= q) *err = 1;
-    // fast path (n >= 4096): pass-C transposed layout for V slots per thread,
-    // slot x = V j + 2 c' + h stored at uint2 index (c' * (n / V) + j) * 2 + h
+    // register-blocked rings (n >= 8192): pass-C transposed layout for V slots
+    // per thread, slot x = V j + 2 c' + h stored at uint2 index
+    // (c' * (n / V) + j) * 2 + h
     uint32_t cpos = c;
-    if (n >= 4096) {
+    if (n >= 8192) {
       const uint32_t jj = c / V, rr = c % V;
       cpos = ((rr >> 1) * (n / V) + jj) * 2 + (rr & 1);
     }
@@ -378,7 +380,7 @@ __global__ void k_prepare_keys(Geo g, uint32_t b, uint32_t elts, const uint64_t*
 
 
 // ---------------------------------------------------------------------------
-// Register-blocked kernels (N = 2^LOGN, LOGN in 12..14, T = N/16 threads).
+// Register-blocked kernels (N = 2^LOGN, LOGN in 13..14, T = N/16 threads).
 // ---------------------------------------------------------------------------
 template <int LOGN>
 __global__ void __launch_bounds__(Ntt<LOGN>::T) k_poly_ntt_f(Geo g, uint32_t gp, uint32_t* __restrict__ polys,
@@ -469,10 +471,14 @@ __device__ __forceinline__ void store16(uint32_t* __restrict__ p, const uint32_t
     *reinterpret_cast<uint4*>(p + 4 * c) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
 }
 
+// digit_l = INTT_l(sigma(c1)_l), block per (pair, gp) (context.cpp:455-459).
+// A thread's 16 sources form one aligned 16-slot group (the automorphism maps
+// groups onto groups): 4 x 128-bit loads, permuted through a per-thread
+// shared-memory column (conflict-free, no barrier before the transform's own).
 template <int LOGN, bool PTW>
 __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digits_f(Geo g, const uint32_t* __restrict__ dot,
                                                               const uint32_t* __restrict__ perm,
-                                                              uint32_t* __restrict__ digits, int tma,
+                                                              uint32_t* __restrict__ digits,
                                                               const __grid_constant__ TwArg<PTW> itab) {
   using NT = Ntt<LOGN>;
   extern __shared__ uint4 smem4[];
@@ -483,10 +489,8 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digi
   const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * NT::N;
   const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
   uint32_t pm[16], e[16];
-  if (tma == 3) {
-    // the 16 sources form one aligned group: 4 x 128-bit loads, permuted
-    // through a per-thread shared-memory column (conflict-free, no barrier)
-    load16_ro(perm + x0, pm);
+  load16_ro(perm + x0, pm);
+  {
     const uint4* gs = reinterpret_cast<const uint4*>(c1 + (pm[0] & ~15u));
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -498,24 +502,6 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digi
     }
 #pragma unroll
     for (int r = 0; r < 16; ++r) e[r] = sm[(pm[r] & 15u) * NT::T + j];
-  } else if (tma) {
-    // the whole c1 polynomial lands in shared memory with one TMA bulk copy;
-    // the Galois gather then reads shared memory instead of scattered L1/L2
-    __shared__ uint64_t bar;
-    uint32_t* stg = tma == 2 ? sm : sm + NT::N;  // 2: staged in the exchange buffer itself
-    if (threadIdx.x == 0) {
-      mbar_init(&bar, 1);
-      bulk_load(stg, c1, NT::N * 4, &bar);
-    }
-    load16_ro(perm + x0, pm);
-    __syncthreads();
-    mbar_wait(&bar, 0);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) e[r] = stg[pm[r]];
-  } else {
-    load16_ro(perm + x0, pm);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) e[r] = c1[pm[r]];
   }
   if constexpr (PTW)
     NT::inv(e, sm, ParamTw{itab.w[gp]}, g.itwc + (size_t)gp * g.twc_stride, pr.q, pr.last, pr.ninv);
@@ -526,91 +512,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_rot_digi
   for (int r = 0; r < 16; ++r) d[NT::posA(j, r)] = e[r];
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(Ntt<LOGN>::T) k_rot_keyswitch_f(Geo g, const uint32_t* __restrict__ dot,
-                                                                 const uint32_t* __restrict__ digits,
-                                                                 const uint32_t* __restrict__ perm,
-                                                                 const uint2* __restrict__ key0,
-                                                                 const uint2* __restrict__ key1,
-                                                                 uint32_t* __restrict__ out, int fold) {
-  using NT = Ntt<LOGN>;
-  constexpr uint32_t N = NT::N;
-  extern __shared__ uint4 smem4[];
-  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
-  const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
-  const PrimeInfo& pr = g.pr[gp];
-  const uint32_t q = pr.q, L = pr.L, i = pr.i;
-  const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
-  const uint32_t* ct = dot + (uint64_t)pair * g.ct_words;
-  const uint32_t* c0 = ct + (uint64_t)pr.poly0 * N;
-  const uint32_t* c1 = ct + (uint64_t)pr.poly1 * N;
-  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * N;
-  uint32_t acc0[16], acc1[16], e[16];
-  {
-    uint32_t pm[16];
-    load16_ro(perm + x0, pm);
-    // keys in pass-C transposed layout: uint4 c of thread j at [c * T + j]
-    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * N) + j;
-    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * N) + j;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint4 a = __ldg(k0 + c * NT::T), b = __ldg(k1 + c * NT::T);
-      const uint32_t d0 = c1[pm[2 * c]], d1 = c1[pm[2 * c + 1]];
-      acc0[2 * c] = mul_shoup(d0, a.x, a.y, q);
-      acc0[2 * c + 1] = mul_shoup(d1, a.z, a.w, q);
-      acc1[2 * c] = mul_shoup(d0, b.x, b.y, q);
-      acc1[2 * c + 1] = mul_shoup(d1, b.z, b.w, q);
-    }
-  }
-  const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
-  const uint2* tw = g.fwd + (size_t)gp * N;
-  const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
-  for (uint32_t l = 0; l < L; ++l) {
-    if (l == i) continue;
-    const uint32_t* src = dig + (uint64_t)l * N;
-    if (pr.fast_reduce) {
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const uint32_t v = src[NT::posA(j, r)];
-        e[r] = min(v, v - q);
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
-    }
-    NT::template fwd<true>(e, sm, tw, twc, q);
-    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
-    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint4 a = __ldg(k0 + c * NT::T), b = __ldg(k1 + c * NT::T);
-      acc0[2 * c] = add_mod(acc0[2 * c], mul_shoup(e[2 * c], a.x, a.y, q), q);
-      acc0[2 * c + 1] = add_mod(acc0[2 * c + 1], mul_shoup(e[2 * c + 1], a.z, a.w, q), q);
-      acc1[2 * c] = add_mod(acc1[2 * c], mul_shoup(e[2 * c], b.x, b.y, q), q);
-      acc1[2 * c + 1] = add_mod(acc1[2 * c + 1], mul_shoup(e[2 * c + 1], b.z, b.w, q), q);
-    }
-  }
-  {
-    uint32_t pm[16];
-    load16_ro(perm + x0, pm);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) acc0[r] = add_mod(acc0[r], c0[pm[r]], q);
-  }
-  if (fold) {
-    load16(c0 + x0, e);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) acc0[r] = add_mod(acc0[r], e[r], q);
-    load16(c1 + x0, e);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) acc1[r] = add_mod(acc1[r], e[r], q);
-  }
-  uint32_t* o = out + (uint64_t)pair * g.ct_words;
-  store16(o + (uint64_t)pr.poly0 * N + x0, acc0);
-  store16(o + (uint64_t)pr.poly1 * N + x0, acc1);
-}
-
-
-// Same as k_rot_keyswitch_f but the two accumulators live in shared memory
+// Key switch with the two accumulators in shared memory
 // (transposed [c][T] uint4, conflict-free), which keeps the kernel under 64
 // registers so two 512-thread CTAs share an SM (32 warps for latency hiding).
 template <int LOGN, bool PTW, bool NEXT>
@@ -758,155 +660,6 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
 }
 
 
-// Latency path: the key switch of one (pair, prime i) split over a 2-CTA
-// cluster. Rank 0 takes the i == l term and the first ceil((L-1)/2) digits,
-// rank 1 the rest; partial accumulators are summed through distributed
-// shared memory (each rank finalises half of the slots), and rank 1 also
-// runs the next rotation's digit INTT from the c1' it collects in its own
-// shared memory. Same arithmetic as k_rot_keyswitch_s (all sums exact mod q),
-// about half the serial transform chain per rotation.
-template <int LOGN, bool NEXT>
-__global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keyswitch_c2(
-    Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ digits, const uint32_t* __restrict__ perm,
-    const uint2* __restrict__ key0, const uint2* __restrict__ key1, uint32_t* __restrict__ out, int fold,
-    const uint32_t* __restrict__ perm_next, uint32_t* __restrict__ dig_next) {
-  namespace cg = cooperative_groups;
-  using NT = Ntt<LOGN>;
-  constexpr uint32_t N = NT::N, T = NT::T;
-  cg::cluster_group cl = cg::this_cluster();
-  const uint32_t rank = cl.block_rank();
-  extern __shared__ uint4 smem4[];
-  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
-  uint4* a0s = smem4 + N / 4;
-  uint4* a1s = a0s + 4 * T;
-  const uint32_t cid = blockIdx.x / 2;
-  const uint32_t pair = cid / g.P, gp = cid % g.P;
-  const PrimeInfo& pr = g.pr[gp];
-  const uint32_t q = pr.q, L = pr.L, i = pr.i;
-  const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
-  const uint32_t* ct = dot + (uint64_t)pair * g.ct_words;
-  const uint32_t* c0 = ct + (uint64_t)pr.poly0 * N;
-  const uint32_t* c1 = ct + (uint64_t)pr.poly1 * N;
-  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * N;
-  if (rank == 0) {  // the l == i term needs no transform
-    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * N) + j;
-    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * N) + j;
-    const uint4* pp = reinterpret_cast<const uint4*>(perm + x0);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint4 pm = __ldg(pp + c);
-      const uint32_t d0 = c1[pm.x], d1 = c1[pm.y], d2 = c1[pm.z], d3 = c1[pm.w];
-      const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
-      const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
-      a0s[c * T + j] = make_uint4(mul_shoup(d0, a.x, a.y, q), mul_shoup(d1, a.z, a.w, q), mul_shoup(d2, b.x, b.y, q),
-                                  mul_shoup(d3, b.z, b.w, q));
-      a1s[c * T + j] = make_uint4(mul_shoup(d0, u.x, u.y, q), mul_shoup(d1, u.z, u.w, q), mul_shoup(d2, v.x, v.y, q),
-                                  mul_shoup(d3, v.z, v.w, q));
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      a0s[c * T + j] = make_uint4(0, 0, 0, 0);
-      a1s[c * T + j] = make_uint4(0, 0, 0, 0);
-    }
-  }
-  const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
-  const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
-  const uint32_t half = L / 2;  // digits (l != i) with index < half go to rank 0
-  uint32_t e[16];
-  for (uint32_t l = 0, k = 0; l < L; ++l) {
-    if (l == i) continue;
-    const uint32_t mine = (k++ < half) ? 0u : 1u;
-    if (mine != rank) continue;
-    const uint32_t* src = dig + (uint64_t)l * N;
-    if (pr.fast_reduce) {
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const uint32_t v = src[NT::posA(j, r)];
-        e[r] = min(v, v - q);
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
-    }
-    NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
-    const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
-    const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
-      uint4 A = a0s[c * T + j];
-      A.x = add_mod(A.x, mul_shoup(e[4 * c], a.x, a.y, q), q);
-      A.y = add_mod(A.y, mul_shoup(e[4 * c + 1], a.z, a.w, q), q);
-      A.z = add_mod(A.z, mul_shoup(e[4 * c + 2], b.x, b.y, q), q);
-      A.w = add_mod(A.w, mul_shoup(e[4 * c + 3], b.z, b.w, q), q);
-      a0s[c * T + j] = A;
-      const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
-      uint4 B = a1s[c * T + j];
-      B.x = add_mod(B.x, mul_shoup(e[4 * c], u.x, u.y, q), q);
-      B.y = add_mod(B.y, mul_shoup(e[4 * c + 1], u.z, u.w, q), q);
-      B.z = add_mod(B.z, mul_shoup(e[4 * c + 2], v.x, v.y, q), q);
-      B.w = add_mod(B.w, mul_shoup(e[4 * c + 3], v.z, v.w, q), q);
-      a1s[c * T + j] = B;
-    }
-  }
-  cl.sync();  // both partial accumulators complete; every NTT's use of sm is over
-  const uint4* r0 = cl.map_shared_rank(a0s, rank ^ 1u);
-  const uint4* r1 = cl.map_shared_rank(a1s, rank ^ 1u);
-  uint32_t* sm1 = cl.map_shared_rank(sm, 1u);  // c1' gathers in rank 1 for the next digit INTT
-  uint32_t* o = out + (uint64_t)pair * g.ct_words;
-  // rank r finalises chunks c in {2r, 2r + 1} of every thread's 16 elements
-#pragma unroll
-  for (int cc = 0; cc < 2; ++cc) {
-    const int c = 2 * (int)rank + cc;
-    const uint32_t xc = x0 + 4 * c;
-    const uint4 pm = __ldg(reinterpret_cast<const uint4*>(perm + xc));
-    uint4 A = a0s[c * T + j], B = a1s[c * T + j];
-    const uint4 RA = r0[c * T + j], RB = r1[c * T + j];
-    A.x = add_mod(A.x, RA.x, q);
-    A.y = add_mod(A.y, RA.y, q);
-    A.z = add_mod(A.z, RA.z, q);
-    A.w = add_mod(A.w, RA.w, q);
-    B.x = add_mod(B.x, RB.x, q);
-    B.y = add_mod(B.y, RB.y, q);
-    B.z = add_mod(B.z, RB.z, q);
-    B.w = add_mod(B.w, RB.w, q);
-    A.x = add_mod(A.x, c0[pm.x], q);
-    A.y = add_mod(A.y, c0[pm.y], q);
-    A.z = add_mod(A.z, c0[pm.z], q);
-    A.w = add_mod(A.w, c0[pm.w], q);
-    if (fold) {
-      const uint4 u = *reinterpret_cast<const uint4*>(c0 + xc);
-      const uint4 v = *reinterpret_cast<const uint4*>(c1 + xc);
-      A.x = add_mod(A.x, u.x, q);
-      A.y = add_mod(A.y, u.y, q);
-      A.z = add_mod(A.z, u.z, q);
-      A.w = add_mod(A.w, u.w, q);
-      B.x = add_mod(B.x, v.x, q);
-      B.y = add_mod(B.y, v.y, q);
-      B.z = add_mod(B.z, v.z, q);
-      B.w = add_mod(B.w, v.w, q);
-    }
-    *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly0 * N + xc) = A;
-    *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly1 * N + xc) = B;
-    if constexpr (NEXT) *reinterpret_cast<uint4*>(sm1 + xc) = B;
-  }
-  cl.sync();  // remote reads of the accumulators and the c1' stores are complete
-  if constexpr (NEXT) {
-    if (rank == 1) {  // next rotation's digit: INTT of sigma'(c1') mod q_i
-      uint32_t pm[16];
-      load16_ro(perm_next + x0, pm);
-#pragma unroll
-      for (int r = 0; r < 16; ++r) e[r] = sm[pm[r]];
-      __syncthreads();
-      NT::inv(e, sm, g.inv + (size_t)gp * N, g.itwc + (size_t)gp * g.twc_stride, q, pr.last, pr.ninv);
-      uint32_t* d = dig_next + ((uint64_t)pair * g.P + gp) * N;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) d[NT::posA(j, r)] = e[r];
-    }
-  }
-}
-
 // Latency path, one CTA per (pair, prime i) with TWO 512-thread groups:
 // group 0 takes the l == i term and the first floor(L/2) digits, group 1 the
 // rest, each into its own shared accumulators (group barriers, 32 warps per
@@ -917,7 +670,7 @@ template <int LOGN, bool NEXT>
 __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
     Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ digits, const uint32_t* __restrict__ perm,
     const uint2* __restrict__ key0, const uint2* __restrict__ key1, uint32_t* __restrict__ out, int fold,
-    const uint32_t* __restrict__ perm_next, uint32_t* __restrict__ dig_next, int tma) {
+    const uint32_t* __restrict__ perm_next, uint32_t* __restrict__ dig_next) {
   using NT = Ntt<LOGN, 2>;
   constexpr uint32_t N = NT::N, T = NT::T;
   extern __shared__ uint4 smem4[];
@@ -968,46 +721,20 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
     if (l == i) continue;
     if (((k++ < half) ? 0u : 1u) == grp) mine[cnt++] = l;
   }
-  // tma: the next digit of the group arrives in its `sm` by a TMA bulk copy
-  // issued while the current digit's key products run
-  __shared__ uint64_t bars[2];
-  if (tma) {
-    if (j == 0) {
-      mbar_init(&bars[grp], 1);
-      if (cnt) bulk_load(sm, dig + (uint64_t)mine[0] * N, N * 4, &bars[grp]);
-    }
-    NT::sync();
-  }
   for (uint32_t u = 0; u < cnt; ++u) {
     const uint32_t l = mine[u];
-    if (tma) {
-      mbar_wait(&bars[grp], u & 1u);
+    const uint32_t* src = dig + (uint64_t)l * N;
+    if (pr.fast_reduce) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
-        const uint32_t v = sm[NT::posA(j, r)];
-        e[r] = pr.fast_reduce ? min(v, v - q) : v % q;
+        const uint32_t v = src[NT::posA(j, r)];
+        e[r] = min(v, v - q);
       }
     } else {
-      const uint32_t* src = dig + (uint64_t)l * N;
-      if (pr.fast_reduce) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const uint32_t v = src[NT::posA(j, r)];
-          e[r] = min(v, v - q);
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
-      }
+      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
     }
     NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
-    if (tma && u + 1 < cnt) {
-      NT::sync();  // the group's last reads of sm in this transform are done
-      if (j == 0) {
-        fence_proxy_async_smem();
-        bulk_load(sm, dig + (uint64_t)mine[u + 1] * N, N * 4, &bars[grp]);
-      }
-    }
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
 #pragma unroll
@@ -1097,182 +824,6 @@ __device__ __forceinline__ uint32_t pow_barrett(uint32_t b, uint32_t e, uint32_t
   return r;
 }
 
-
-// Small batches (latency): the key switch split over digits. Block per
-// (pair, prime, digit l) writes NTT_i(digit_l mod q_i) (.) K[l][i] (or the
-// untransformed l == i term); k_ks_reduce sums the L partials and adds the
-// fold terms. Same arithmetic as k_rot_keyswitch_s, L x more parallelism.
-template <int LOGN>
-__global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_ks_part(Geo g, const uint32_t* __restrict__ dot,
-                                                            const uint32_t* __restrict__ digits,
-                                                            const uint32_t* __restrict__ perm,
-                                                            const uint2* __restrict__ key0,
-                                                            const uint2* __restrict__ key1,
-                                                            uint32_t* __restrict__ part, uint32_t Lmax,
-                                                            const __grid_constant__ TwAB tab) {
-  using NT = Ntt<LOGN>;
-  constexpr uint32_t N = NT::N, T = NT::T;
-  extern __shared__ uint4 smem4[];
-  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
-  const uint32_t l = blockIdx.x % Lmax, pg = blockIdx.x / Lmax;
-  const uint32_t pair = pg / g.P, gp = pg % g.P;
-  const PrimeInfo& pr = g.pr[gp];
-  if (l >= pr.L) return;
-  const uint32_t q = pr.q, i = pr.i, j = threadIdx.x, x0 = NT::posC0(j);
-  uint32_t e[16];
-  if (l == i) {
-    const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * N;
-    uint32_t pm[16];
-    load16_ro(perm + x0, pm);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) e[r] = c1[pm[r]];
-  } else {
-    const uint32_t* src = digits + ((uint64_t)pair * g.P + pr.first + l) * N;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const uint32_t v = src[NT::posA(j, r)];
-      e[r] = pr.fast_reduce ? min(v, v - q) : v % q;
-    }
-    NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, g.twc + (size_t)gp * g.twc_stride, q);
-  }
-  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * pr.L * 2 * N;
-  const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
-  const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
-  uint32_t* o = part + (uint64_t)blockIdx.x * 2 * N + x0;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const uint4 a = __ldg(k0 + c * T), b = __ldg(k1 + c * T);
-    *reinterpret_cast<uint2*>(o + 2 * c) =
-        make_uint2(mul_shoup(e[2 * c], a.x, a.y, q), mul_shoup(e[2 * c + 1], a.z, a.w, q));
-    *reinterpret_cast<uint2*>(o + N + 2 * c) =
-        make_uint2(mul_shoup(e[2 * c], b.x, b.y, q), mul_shoup(e[2 * c + 1], b.z, b.w, q));
-  }
-}
-
-// grid (pair, prime, n / 1024 tiles), 256 threads x 4 slots (uint4 accesses)
-__global__ void __launch_bounds__(256) k_ks_reduce(Geo g, const uint32_t* __restrict__ dot,
-                                                   const uint32_t* __restrict__ part, const uint32_t* __restrict__ perm,
-                                                   uint32_t Lmax, uint32_t* __restrict__ out, int fold) {
-  const uint32_t n = g.n, tiles = n / 1024;
-  const uint32_t pg = blockIdx.x / tiles, tile = blockIdx.x % tiles;
-  const uint32_t pair = pg / g.P, gp = pg % g.P;
-  const PrimeInfo& pr = g.pr[gp];
-  const uint32_t q = pr.q, L = pr.L;
-  const uint32_t x = tile * 1024 + threadIdx.x * 4;
-  const uint32_t* c0 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly0 * n;
-  const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n;
-  const uint32_t* ps = part + (uint64_t)pg * Lmax * 2 * n + x;
-  const uint4 pm = __ldg(reinterpret_cast<const uint4*>(perm + x));
-  uint32_t a0[4] = {c0[pm.x], c0[pm.y], c0[pm.z], c0[pm.w]}, a1[4] = {0, 0, 0, 0};
-  for (uint32_t l = 0; l < L; ++l) {
-    const uint4 u = *reinterpret_cast<const uint4*>(ps + (uint64_t)l * 2 * n);
-    const uint4 v = *reinterpret_cast<const uint4*>(ps + (uint64_t)l * 2 * n + n);
-    a0[0] = add_mod(a0[0], u.x, q), a0[1] = add_mod(a0[1], u.y, q), a0[2] = add_mod(a0[2], u.z, q), a0[3] = add_mod(a0[3], u.w, q);
-    a1[0] = add_mod(a1[0], v.x, q), a1[1] = add_mod(a1[1], v.y, q), a1[2] = add_mod(a1[2], v.z, q), a1[3] = add_mod(a1[3], v.w, q);
-  }
-  if (fold) {
-    const uint4 u = *reinterpret_cast<const uint4*>(c0 + x), v = *reinterpret_cast<const uint4*>(c1 + x);
-    a0[0] = add_mod(a0[0], u.x, q), a0[1] = add_mod(a0[1], u.y, q), a0[2] = add_mod(a0[2], u.z, q), a0[3] = add_mod(a0[3], u.w, q);
-    a1[0] = add_mod(a1[0], v.x, q), a1[1] = add_mod(a1[1], v.y, q), a1[2] = add_mod(a1[2], v.z, q), a1[3] = add_mod(a1[3], v.w, q);
-  }
-  *reinterpret_cast<uint4*>(out + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly0 * n + x) = make_uint4(a0[0], a0[1], a0[2], a0[3]);
-  *reinterpret_cast<uint4*>(out + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n + x) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
-}
-
-// Latency path, key switch split over its digits for parallelism (R = 1 has
-// only 110 (pair, prime) blocks for 148 SMs, and one block per (pair, prime)
-// is issue-bound on its SM). Block per (pair, prime i, digit l != i): one
-// forward NTT_i(digit_l mod q_i) and its two key products, 40 registers so
-// three blocks share an SM; the l == i term, the sum over l and the fold adds
-// happen in k_ks_reduce2. Same arithmetic as k_rot_keyswitch_t (exact sums).
-template <int LOGN>
-__global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 3 : 1)) k_ks_part2(Geo g, const uint32_t* __restrict__ digits,
-                                                                             const uint2* __restrict__ key0,
-                                                                             const uint2* __restrict__ key1,
-                                                                             uint32_t* __restrict__ part, uint32_t Lm1) {
-  using NT = Ntt<LOGN>;
-  constexpr uint32_t N = NT::N, T = NT::T;
-  extern __shared__ uint4 smem4[];
-  uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
-  const uint32_t lp = blockIdx.x % Lm1, pg = blockIdx.x / Lm1;
-  const uint32_t pair = pg / g.P, gp = pg % g.P;
-  const PrimeInfo& pr = g.pr[gp];
-  if (lp + 1 >= pr.L) return;
-  const uint32_t q = pr.q, i = pr.i, l = lp + (lp >= i ? 1u : 0u), j = threadIdx.x, x0 = NT::posC0(j);
-  uint32_t e[16];
-  const uint32_t* src = digits + ((uint64_t)pair * g.P + pr.first + l) * N;
-  if (pr.fast_reduce) {
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const uint32_t v = src[NT::posA(j, r)];
-      e[r] = min(v, v - q);
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
-  }
-  NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, g.twc + (size_t)gp * g.twc_stride, q);
-  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * pr.L * 2 * N;
-  const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
-  const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
-  uint32_t* o = part + (uint64_t)blockIdx.x * 2 * N + x0;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
-    *reinterpret_cast<uint4*>(o + 4 * c) =
-        make_uint4(mul_shoup(e[4 * c], a.x, a.y, q), mul_shoup(e[4 * c + 1], a.z, a.w, q),
-                   mul_shoup(e[4 * c + 2], b.x, b.y, q), mul_shoup(e[4 * c + 3], b.z, b.w, q));
-    const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
-    *reinterpret_cast<uint4*>(o + N + 4 * c) =
-        make_uint4(mul_shoup(e[4 * c], u.x, u.y, q), mul_shoup(e[4 * c + 1], u.z, u.w, q),
-                   mul_shoup(e[4 * c + 2], v.x, v.y, q), mul_shoup(e[4 * c + 3], v.z, v.w, q));
-  }
-}
-
-// grid (pair, prime, n / 1024 tiles), 256 threads x 4 slots: out0 = sigma(c0)
-// + sigma(c1)_i (.) K[i][i][0] + sum_l part0 (+ c0), out1 = sigma(c1)_i (.)
-// K[i][i][1] + sum_l part1 (+ c1). Keys are in the pass-C transposed layout
-// (16 slots per NTT thread), so slots x..x+3 are two uint4 per part.
-__global__ void __launch_bounds__(256) k_ks_reduce2(Geo g, const uint32_t* __restrict__ dot,
-                                                    const uint32_t* __restrict__ part,
-                                                    const uint32_t* __restrict__ perm, const uint2* __restrict__ key0,
-                                                    const uint2* __restrict__ key1, uint32_t Lm1,
-                                                    uint32_t* __restrict__ out, int fold) {
-  const uint32_t n = g.n, tiles = n / 1024, T = n / 16;
-  const uint32_t pg = blockIdx.x / tiles, tile = blockIdx.x % tiles;
-  const uint32_t pair = pg / g.P, gp = pg % g.P;
-  const PrimeInfo& pr = g.pr[gp];
-  const uint32_t q = pr.q, L = pr.L, i = pr.i;
-  const uint32_t x = tile * 1024 + threadIdx.x * 4;
-  const uint32_t* c0 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly0 * n;
-  const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n;
-  const uint4 pm = __ldg(reinterpret_cast<const uint4*>(perm + x));
-  const uint32_t d[4] = {c1[pm.x], c1[pm.y], c1[pm.z], c1[pm.w]};
-  const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * n;
-  const uint32_t jt = x >> 4, rr = x & 15;
-  const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * n) + jt;
-  const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * n) + jt;
-  const uint4 ka = __ldg(k0 + (rr >> 1) * T), kb = __ldg(k0 + ((rr >> 1) + 1) * T);
-  const uint4 ua = __ldg(k1 + (rr >> 1) * T), ub = __ldg(k1 + ((rr >> 1) + 1) * T);
-  uint32_t a0[4] = {add_mod(c0[pm.x], mul_shoup(d[0], ka.x, ka.y, q), q), add_mod(c0[pm.y], mul_shoup(d[1], ka.z, ka.w, q), q),
-                    add_mod(c0[pm.z], mul_shoup(d[2], kb.x, kb.y, q), q), add_mod(c0[pm.w], mul_shoup(d[3], kb.z, kb.w, q), q)};
-  uint32_t a1[4] = {mul_shoup(d[0], ua.x, ua.y, q), mul_shoup(d[1], ua.z, ua.w, q), mul_shoup(d[2], ub.x, ub.y, q),
-                    mul_shoup(d[3], ub.z, ub.w, q)};
-  const uint32_t* ps = part + (uint64_t)pg * Lm1 * 2 * n + x;
-  for (uint32_t l = 0; l + 1 < L; ++l) {
-    const uint4 u = *reinterpret_cast<const uint4*>(ps + (uint64_t)l * 2 * n);
-    const uint4 v = *reinterpret_cast<const uint4*>(ps + (uint64_t)l * 2 * n + n);
-    a0[0] = add_mod(a0[0], u.x, q), a0[1] = add_mod(a0[1], u.y, q), a0[2] = add_mod(a0[2], u.z, q), a0[3] = add_mod(a0[3], u.w, q);
-    a1[0] = add_mod(a1[0], v.x, q), a1[1] = add_mod(a1[1], v.y, q), a1[2] = add_mod(a1[2], v.z, q), a1[3] = add_mod(a1[3], v.w, q);
-  }
-  if (fold) {
-    const uint4 u = *reinterpret_cast<const uint4*>(c0 + x), v = *reinterpret_cast<const uint4*>(c1 + x);
-    a0[0] = add_mod(a0[0], u.x, q), a0[1] = add_mod(a0[1], u.y, q), a0[2] = add_mod(a0[2], u.z, q), a0[3] = add_mod(a0[3], u.w, q);
-    a1[0] = add_mod(a1[0], v.x, q), a1[1] = add_mod(a1[1], v.y, q), a1[2] = add_mod(a1[2], v.z, q), a1[3] = add_mod(a1[3], v.w, q);
-  }
-  *reinterpret_cast<uint4*>(out + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly0 * n + x) = make_uint4(a0[0], a0[1], a0[2], a0[3]);
-  *reinterpret_cast<uint4*>(out + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * n + x) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
-}
 
 // Latency path, split in two: the one-hot mask plaintexts (same closed form
 // as k_mask_acc_g) depend only on the slot, so k_mask_prep computes them on a

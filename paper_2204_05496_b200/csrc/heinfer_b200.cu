@@ -25,7 +25,7 @@
 // Source layout (one translation unit; the .cuh files are included inside
 // the kernel namespace below):
 //   modmath.cuh        Shoup / Barrett arithmetic, shared-memory NTTs (small N)
-//   ntt_fast.cuh       register-blocked NTT (N = 4096..16384)
+//   ntt_fast.cuh       register-blocked NTT (N = 8192, 16384)
 //   bulk_copy.cuh      1-D TMA bulk copies (cp.async.bulk + mbarrier)
 //   wire.cuh           HECT ciphertext parse / emit kernels
 //   fold_kernels.cuh   fast algorithm: chunk products, digits, key switch,
@@ -56,7 +56,6 @@
 #include "../../include/heinfer_b200.h"
 #include "modmath.cuh"
 #include "ntt_fast.cuh"
-#include "ntt32.cuh"
 #include "bulk_copy.cuh"
 #include "baseline.cuh"
 
@@ -215,14 +214,7 @@ struct Geo {
   const uint4* twc;  // pass-C twiddles, fast path only: [P + 2][KC][T]
   const uint4* itwc;
   uint32_t twc_stride;  // KC * T (uint4 per modulus)
-  const uint4* twc32;   // pass-C twiddles of the 32-residue NTT (ntt32.cuh): [P + 2][KC32][N/32]
-  const uint4* itwc32;
-  uint32_t twc32_stride;
   const uint32_t* index_map;
-  // block -> (pair, prime) order of the full-batch fold kernels: 0 pair-major
-  // (blockIdx = pair * P + prime), 1 prime-major (blockIdx = prime * pairs +
-  // pair: CTAs resident on one SM share a prime's twiddles and key lines)
-  uint32_t prime_major;
   // N = 16384 half-ring key switch (ks_half.cuh): per (prime, half) natural
   // and pass-C tables of the half's N/2-point transform
   const uint2* fwdh;    // [P][2][N/2]
@@ -231,16 +223,10 @@ struct Geo {
   const uint2* invh;    // inverse counterparts (k_rot_digits_h)
   const uint4* itwch;
 };
-// (pair, prime) of this block, for grids of pairs * P blocks
+// (pair, prime) of this block, for grids of pairs * P blocks (pair-major)
 __device__ __forceinline__ void block_pair_prime(const Geo& g, uint32_t& pair, uint32_t& gp) {
-  if (g.prime_major) {
-    const uint32_t pairs = gridDim.x / g.P;
-    gp = blockIdx.x / pairs;
-    pair = blockIdx.x - gp * pairs;
-  } else {
-    pair = blockIdx.x / g.P;
-    gp = blockIdx.x % g.P;
-  }
+  pair = blockIdx.x / g.P;
+  gp = blockIdx.x % g.P;
 }
 
 // Pass-A/B twiddles (indices 0..255) of every q prime, passed by value in the
@@ -289,7 +275,6 @@ __device__ __forceinline__ uint32_t poly_prime(const Geo& g, uint32_t poly) {
 
 #include "fold_kernels.cuh"
 #include "tmem_ks.cuh"
-#include "ks32.cuh"
 #include "ks_half.cuh"
 
 #include "stdalg_kernels.cuh"
@@ -342,7 +327,6 @@ struct hei_gpu_ctx {
   uint2* d_invh = nullptr;
   uint4* d_itwch = nullptr;
   std::vector<uint2> h_invh;
-  uint4 *d_twc32 = nullptr, *d_itwc32 = nullptr;
   uint32_t* d_index = nullptr;
   // galois elements in fold order: steps 1, 2, ..., n/4, then the swap
   std::vector<uint64_t> fold_elts;
@@ -360,15 +344,10 @@ struct hei_gpu_ctx {
   uint32_t* d_err = nullptr;
   cudaStream_t stream = nullptr;
   uint64_t batch_pairs = 0;
-  bool ks14_regs = false;  // N = 16384: register-accumulator key switch (HEI_KS14_REGS=1)
-  int ntt32 = 0;           // HEI_NTT32: 32-residue transforms (ntt32.cuh); 1 = N 16384 fold, 2 = also N 8192 full batches
-  uint2* d_keys32[2] = {nullptr, nullptr};  // Galois keys in the 32-slot-per-thread layout (ntt32 only)
   uint64_t keys_words[2] = {0, 0};
   // scratch (grown on demand)
   uint32_t *d_dotA = nullptr, *d_dotB = nullptr, *d_dig = nullptr, *d_dig2 = nullptr;
   bool fuse_digits = true;  // HEI_FUSE_DIGITS=0: separate digit kernel every rotation (small batches)
-  bool cluster_ks = false;  // HEI_CLUSTER_KS=1: 2-CTA cluster key switch on the latency path
-  bool group_ks = true;     // HEI_GROUP_KS=0: no 2-group CTA key switch on the latency path
   uint64_t scratch_pairs = 0;
   std::mutex mu;
   // grow-only device pools for the per-call buffers of the device-resident
@@ -392,9 +371,6 @@ struct hei_gpu_ctx {
   size_t pinned_bias_bytes = 0;
   void* pinned_out = nullptr;  // pinned staging for result downloads to pageable memory
   size_t pinned_out_bytes = 0;
-  uint32_t* pool_part = nullptr;  // split key-switch partials (small batches)
-  size_t pool_part_bytes = 0;
-  int split = 0;   // HEI_SPLIT: split the key switch over digits for small batches (1: per digit incl. l == i, 2: l != i only, 3 CTAs/SM)
   bool graphs = true;   // HEI_NO_GRAPHS=1: launch the small-batch fold eagerly
   bool two_streams = true;  // HEI_TWO_STREAMS=0: fold the batch on one stream only
   bool mt_jump = true;      // HEI_MT_JUMP=0: sequential mt19937_64 replay only
@@ -411,29 +387,16 @@ struct hei_gpu_ctx {
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
-  bool half13 = false;     // HEI_HALF13=1: N = 8192 full batches as 256-thread half-ring blocks (ks_half.cuh)
-  int dig14_half = 1;  // HEI_DIG14_HALF: N = 16384 full-batch digits as 2-CTA clusters (2: c1 staged by TMA
-                      // across the cluster; 0: the 1024-thread kernel)
-  int ks14_half = 2;  // HEI_KS14_HALF: N = 16384 full-batch key switch as half-ring blocks (2: one launch per
-                     // branch with both halves side by side; 1: one launch per half; 0: the 1024-thread kernel)
-  bool ks14_tmem = true;  // HEI_KS14_TMEM=0: N = 16384 full batches keep the shared-memory accumulators
-  int enc_minb = 3;  // HEI_ENC_MINB: resident CTAs/SM of the public-key encryption kernel (2 or 3)
-  bool prime_major = false;  // HEI_PRIME_MAJOR: full-batch fold kernels walk (pair, prime) blocks prime-major
-  int ks_tmem = 4;  // HEI_KS_TMEM: full-batch key switch accumulates in TMEM (0 off; 2, 3 CTAs/SM; 4: 3 CTAs/SM, 4-slot rounds)
-  bool fuse_big = false;   // HEI_FUSE_BIG=1: full batches also fuse the next digit INTT into the TMEM key switch
   bool dot_rows = true;    // HEI_DOT_ROWS=0: per-pair chunk-product kernel for every batch
   bool mask_cache = true;  // HEI_MASK_CACHE=0: regenerate each pair's mask (the reference's N > 4096 behaviour)
   uint32_t* d_mask_table = nullptr;  // [slot][P][N] mask plaintexts, built on first full-batch use
   bool e2e_overlap = true;  // HEI_E2E_OVERLAP=0: host-buffer chunks run one after another
   std::vector<cudaStream_t> chunk_streams;  // 2 x fold_parts streams: consecutive chunks overlap
-  int dig_tma = 3;       // HEI_DIG_TMA: 3 c1 gathered by source group (4 x 128-bit loads, shared-memory column permute); 2 staged by TMA in the exchange buffer; 1 in a second buffer; 0 scalar global gathers
-  int lat_tma = 0;       // HEI_LAT_TMA=1: latency-path key switch prefetches digits with TMA (measured slower)
   uint64_t mt_chunks_max = 128;   // HEI_MT_CHUNKS: parallel mt19937_64 generators per branch
   struct FoldGraph {
     uint64_t pairs;
-    uint32_t *cur, *other, *part, *dig;
+    uint32_t *cur, *other, *dig;
     uint64_t gen;
-    bool split;
     cudaGraphExec_t exec;
     uint64_t launches;
   };
@@ -557,11 +520,11 @@ void set_smem_attr(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024) CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
-// ---- launch dispatch: register-blocked kernels for N in {4096, 8192, 16384},
-// ---- generic shared-memory kernels otherwise (small test rings).
+// ---- launch dispatch: register-blocked kernels for the production rings
+// ---- N in {8192, 16384}; generic shared-memory kernels otherwise (the small
+// ---- rings of the reference's own tests).
 #define HEI_DISPATCH(LOGN_VAR, FAST, GENERIC)         \
   switch (LOGN_VAR) {                                 \
-    case 12: { constexpr int LG = 12; FAST; } break;  \
     case 13: { constexpr int LG = 13; FAST; } break;  \
     case 14: { constexpr int LG = 14; FAST; } break;  \
     default: { GENERIC; } break;                      \
@@ -580,20 +543,8 @@ const TwAB* tabs_of(hei_gpu_ctx* c, const Geo& g, int inverse) {
   return &t;
 }
 
-// Pass-A/B rows of the N = 16384 half-ring tables (half h) for the primes of `g`.
-const TwAB* tabs_half(hei_gpu_ctx* c, const Geo& g, uint32_t h, int inverse = 0) {
-  thread_local TwAB t;
-  for (uint32_t k = 0; k < g.P && k < (uint32_t)kMaxAB; ++k) {
-    uint32_t src = 0;
-    for (uint32_t m = 0; m < c->geo.P; ++m)
-      if (c->geo.pr[m].q == g.pr[k].q) src = m;
-    std::memcpy(t.w[k], (inverse ? c->h_invh : c->h_fwdh).data() + ((size_t)src * 2 + h) * (c->n / 2),
-                256 * sizeof(uint2));
-  }
-  return &t;
-}
-
-// Rows [k][h] (k < np) of the half-ring forward tables for primes gp0.. of `g`.
+// Rows [k][h] (k < np) of the N = 16384 half-ring forward tables for primes
+// gp0.. of `g`.
 const TwAB* tabs_half_pairs(hei_gpu_ctx* c, const Geo& g, uint32_t gp0, uint32_t np) {
   thread_local TwAB t;
   if (2 * np > (uint32_t)kMaxAB) raise(HEI_INTERNAL, "half-ring parameter rows exceed the table");
@@ -607,273 +558,101 @@ const TwAB* tabs_half_pairs(hei_gpu_ctx* c, const Geo& g, uint32_t gp0, uint32_t
   return &t;
 }
 
-// The 32-residue transforms (ntt32.cuh) serve every N = 16384 fold when
-// HEI_NTT32 >= 1 and N = 8192 full batches when HEI_NTT32 = 2.
-bool use_ntt32(hei_gpu_ctx* c, unsigned blocks) {
-  if (c->logn == 14) return c->ntt32 >= 1;
-  if (c->logn == 13) return c->ntt32 >= 2 && blocks >= 4u * 148u;
-  return false;
-}
-const uint2* keys32_of(hei_gpu_ctx* c, const uint2* k) {
-  for (int b = 0; b < 2; ++b)
-    if (c->d_keys[b] && k >= c->d_keys[b] && k < c->d_keys[b] + c->keys_words[b]) {
-      if (!c->d_keys32[b]) raise(HEI_INTERNAL, "32-slot key layout not prepared (HEI_NTT32 set after key upload)");
-      return c->d_keys32[b] + (k - c->d_keys[b]);
-    }
-  raise(HEI_INTERNAL, "key pointer outside the uploaded key sets");
-}
-
-// Public-key encryption of E features/rows (E * P blocks); HEI_ENC_MINB=3
-// runs the fast kernel at 3 CTAs/SM (40 registers) instead of 2.
+// Public-key encryption of E features/rows (E * P blocks); large launches run
+// the register kernel at 3 CTAs/SM (N = 8192) with parameter-space twiddles.
 void launch_bl_encrypt(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const int8_t* d_noise, const uint32_t* d_m,
                        uint32_t* ct, size_t sm1, cudaStream_t st) {
   const bool ptw = blocks >= 2u * 148u;
   HEI_DISPATCH(c->logn,
-               (ptw ? (c->enc_minb == 3
-                           ? k_bl_encrypt<LG, true, (LG <= 13 ? 3 : 1)><<<blocks, Ntt<LG>::T, sm1, st>>>(
-                                 g, d_noise, d_m, c->d_pkp, ct, *tabs_of(c, g, 0))
-                           : k_bl_encrypt<LG, true><<<blocks, Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct,
-                                                                                     *tabs_of(c, g, 0)))
+               (ptw ? k_bl_encrypt<LG, true, (LG <= 13 ? 3 : 1)><<<blocks, Ntt<LG>::T, sm1, st>>>(
+                          g, d_noise, d_m, c->d_pkp, ct, *tabs_of(c, g, 0))
                     : k_bl_encrypt<LG, false><<<blocks, Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct, TwNone{})),
                (k_bl_encrypt_g<<<blocks, c->threads(), sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct)));
 }
+
+// digit_l = INTT_l(sigma(c1)_l) for every (pair, prime) block.
 void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* perm,
                        uint32_t* dig, cudaStream_t st) {
-  // dig_tma 2: the staged c1 shares the exchange buffer (the transform's
-  // first barrier orders every gather read before its first store)
-  const size_t sm = smem_bytes(c, 1), smf = smem_bytes(c, c->dig_tma == 1 ? 2 : 1);
+  const size_t sm = smem_bytes(c, 1);
   // big launches take the pass-A/B twiddles as parameters (constant bank);
   // small ones keep the 25 KB parameter block off the launch path
   const bool ptw = blocks >= 2u * 148u;
-  if (c->logn == 13 && c->half13 && ptw && c->d_itwch && !use_ntt32(c, blocks)) {  // 256-thread halves
-    HEI_DISPATCH(c->logn,
-                 (k_rot_digits_h<false, 13><<<2 * blocks, 256, 4096 * 4, st>>>(g, cur, perm, dig, 0, TwNone{})),
-                 (void)0);
-    LAUNCHED();
-    return;
-  }
-  if (c->logn == 14 && c->dig14_half && ptw && c->d_itwch && !use_ntt32(c, blocks)) {
-    // 2-CTA clusters, one per half of the eval slots (ks_half.cuh); the two
-    // halves of a launch need different pass-A/B rows, so both read them
-    // from global memory (PTW = false)
-    HEI_DISPATCH(c->logn,
-                 (k_rot_digits_h<false><<<2 * blocks, 512, 8192 * 4, st>>>(g, cur, perm, dig, c->dig14_half == 2,
-                                                                           TwNone{})),
-                 (void)0);
-    LAUNCHED();
-    return;
-  }
-  if (use_ntt32(c, blocks)) {
-    if (c->logn == 14) {
-      if (ptw) k_rot_digits32<14, true><<<blocks, Ntt32<14>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1));
-      else k_rot_digits32<14, false><<<blocks, Ntt32<14>::T, sm, st>>>(g, cur, perm, dig, TwNone{});
-    } else {
-      if (ptw) k_rot_digits32<13, true><<<blocks, Ntt32<13>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1));
-      else k_rot_digits32<13, false><<<blocks, Ntt32<13>::T, sm, st>>>(g, cur, perm, dig, TwNone{});
-    }
+  if (c->logn == 14 && ptw) {
+    // N = 16384: 2-CTA clusters, one CTA per half of the eval slots (ks_half.cuh)
+    k_rot_digits_h<<<2 * blocks, 512, 8192 * 4, st>>>(g, cur, perm, dig);
     LAUNCHED();
     return;
   }
   HEI_DISPATCH(c->logn,
-               (ptw ? k_rot_digits_f<LG, true><<<blocks, Ntt<LG>::T, smf, st>>>(g, cur, perm, dig, c->dig_tma,
-                                                                                *tabs_of(c, g, 1))
-                    : k_rot_digits_f<LG, false><<<blocks, Ntt<LG>::T, smf, st>>>(g, cur, perm, dig, c->dig_tma,
-                                                                                 TwNone{})),
+               (ptw ? k_rot_digits_f<LG, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1))
+                    : k_rot_digits_f<LG, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig, TwNone{})),
                (k_rot_digits<<<blocks, c->threads(), sm, st>>>(g, cur, perm, dig)));
   LAUNCHED();
 }
-// Returns true when the launched kernel also produced the next rotation's
-// digits (k_rot_keyswitch_s with dig_next != nullptr).
-template <int LG, bool NEXT>
-void launch_ks_c2(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* dig,
-                  const uint32_t* perm, const uint2* k0, const uint2* k1, uint32_t* out, int fold, cudaStream_t st,
-                  const uint32_t* perm_next, uint32_t* dig_next) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * blocks);
-  cfg.blockDim = dim3(Ntt<LG>::T);
-  cfg.dynamicSmemBytes = smem_bytes(c, 3);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CU(cudaLaunchKernelEx(&cfg, k_rot_keyswitch_c2<LG, NEXT>, g, cur, dig, perm, k0, k1, out, fold, perm_next, dig_next));
-}
 
-template <int LG>
-void launch_ks_s(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* dig,
-                 const uint32_t* perm, const uint2* k0, const uint2* k1, uint32_t* out, int fold, cudaStream_t st,
-                 const uint32_t* perm_next, uint32_t* dig_next) {
-  const size_t sm = smem_bytes(c, 3);
-  const bool big = blocks >= 2u * 148u;
-  if constexpr (LG <= 13) {
-    if (!big && c->group_ks && blocks <= 148u) {  // latency path: one 2-group CTA per SM
-      const size_t sm2 = smem_bytes(c, 6);
-      if (dig_next)
-        k_rot_keyswitch_w2<LG, true><<<blocks, 2 * Ntt<LG>::T, sm2, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                         perm_next, dig_next, c->lat_tma);
-      else
-        k_rot_keyswitch_w2<LG, false><<<blocks, 2 * Ntt<LG>::T, sm2, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                          nullptr, nullptr, c->lat_tma);
-      return;
-    }
-  }
-  constexpr unsigned per_sm = LG <= 13 ? 2u : 1u;  // resident CTAs per SM (shared memory)
-  if (!big && c->cluster_ks && 2 * blocks <= per_sm * 148u) {  // latency path: 2-CTA clusters, one wave
-    if (dig_next)
-      launch_ks_c2<LG, true>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, perm_next, dig_next);
-    else
-      launch_ks_c2<LG, false>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, nullptr, nullptr);
-    return;
-  }
-  if constexpr (LG == 13) {
-    if (c->half13 && !dig_next && big && c->d_twch) {  // two 256-thread half-ring blocks, 6 CTAs/SM
-      for (uint32_t h = 0; h < 2; ++h)
-        k_rot_keyswitch_h<true, 13><<<blocks, 256, 4096 * 4, st>>>(g, cur, dig, perm, k0, k1, out, fold, h, 0, 0,
-                                                                    *tabs_half(c, g, h));
-      return;
-    }
-  }
-  if constexpr (LG == 14) {
-    if (c->ks14_half && !dig_next && big && c->d_twch) {  // two 512-thread half-ring blocks, 3 CTAs/SM
-      if (c->ks14_half == 2 && 2 * std::max(g.L[0], g.L[1]) <= (uint32_t)kMaxAB) {
-        // one launch per branch, the halves of a (pair, prime) adjacent
-        const uint32_t pairs = blocks / g.P;
-        for (uint32_t b = 0, gp0 = 0; b < 2; gp0 += g.L[b], ++b) {
-          if (!g.L[b]) continue;
-          k_rot_keyswitch_h<true><<<pairs * g.L[b] * 2, 512, 8192 * 4, st>>>(
-              g, cur, dig, perm, k0, k1, out, fold, 2, gp0, g.L[b], *tabs_half_pairs(c, g, gp0, g.L[b]));
-        }
-      } else {
-        for (uint32_t h = 0; h < 2; ++h)
-          k_rot_keyswitch_h<true><<<blocks, 512, 8192 * 4, st>>>(g, cur, dig, perm, k0, k1, out, fold, h, 0, 0,
-                                                                  *tabs_half(c, g, h));
-      }
-      return;
-    }
-    if (c->ks14_tmem && !dig_next) {  // TMEM accumulators (256 columns), 1 CTA of 1024 threads per SM
-      if (big)
-        k_rot_keyswitch_t<LG, true, 1, 4><<<blocks, Ntt<LG>::T, smem_bytes(c, 1), st>>>(
-            g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
-      else
-        k_rot_keyswitch_t<LG, false, 1, 4><<<blocks, Ntt<LG>::T, smem_bytes(c, 1), st>>>(
-            g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, TwNone{});
-      return;
-    }
-  }
-  if (dig_next) {
-    if constexpr (LG == 13) {
-      if (big && c->ks_tmem) {  // TMEM accumulators + the next rotation's digit
-        k_rot_keyswitch_t<LG, true, 3, 4, true><<<blocks, Ntt<LG>::T, smem_bytes(c, 2), st>>>(
-            g, cur, dig, perm, k0, k1, out, fold, perm_next, dig_next, *tabs_of(c, g, 0));
-        return;
-      }
-    }
-    if (big)
-      k_rot_keyswitch_s<LG, true, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, perm_next,
-                                                                        dig_next, *tabs_of(c, g, 0));
-    else
-      k_rot_keyswitch_s<LG, false, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                         perm_next, dig_next, TwNone{});
-  } else {
-    if constexpr (LG == 13) {
-      if (big && c->ks_tmem) {  // accumulators in tensor memory
-        const size_t smt = smem_bytes(c, 1);
-        if (c->ks_tmem == 3)
-          k_rot_keyswitch_t<LG, true, 3><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr,
-                                                                          nullptr, *tabs_of(c, g, 0));
-        else if (c->ks_tmem == 4)  // 3 CTAs/SM, 4-slot TMEM rounds
-          k_rot_keyswitch_t<LG, true, 3, 4><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                             nullptr, nullptr, *tabs_of(c, g, 0));
-        else if (c->ks_tmem == 11)  // as 4, Galois gathers by source group instead of TMA-staged polynomials
-          k_rot_keyswitch_t<LG, true, 3, 4, false, false, false, false, false, false, true>
-              <<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr,
-                                                *tabs_of(c, g, 0));
-        else if (c->ks_tmem == 10)  // as 4, next digit (then c0) bulk-prefetched into L2
-          k_rot_keyswitch_t<LG, true, 3, 4, false, false, false, false, false, true><<<blocks, Ntt<LG>::T, smt, st>>>(
-              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
-        else if (c->ks_tmem == 9)  // as 4, Galois keys bypass L1 (L1::no_allocate)
-          k_rot_keyswitch_t<LG, true, 3, 4, false, false, false, false, true><<<blocks, Ntt<LG>::T, smt, st>>>(
-              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
-        else if (c->ks_tmem == 7)  // as 6, key loads free to move across the TMEM waits
-          k_rot_keyswitch_t<LG, true, 3, 4, false, false, true, true><<<blocks, Ntt<LG>::T, 2 * smt, st>>>(
-              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
-        else if (c->ks_tmem == 8)  // as 4, key loads free to move across the TMEM waits
-          k_rot_keyswitch_t<LG, true, 3, 4, false, false, false, true><<<blocks, Ntt<LG>::T, smt, st>>>(
-              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
-        else if (c->ks_tmem == 6)  // as 4, digit transforms alternate between two exchange buffers
-          k_rot_keyswitch_t<LG, true, 3, 4, false, false, true><<<blocks, Ntt<LG>::T, 2 * smt, st>>>(
-              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
-        else if (c->ks_tmem == 5)  // as 4, digits prefetched into shared memory by TMA
-          k_rot_keyswitch_t<LG, true, 3, 4, false, true><<<blocks, Ntt<LG>::T, 2 * smt, st>>>(
-              g, cur, dig, perm, k0, k1, out, fold, nullptr, nullptr, *tabs_of(c, g, 0));
-        else
-          k_rot_keyswitch_t<LG, true, 2><<<blocks, Ntt<LG>::T, smt, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr,
-                                                                          nullptr, *tabs_of(c, g, 0));
-        return;
-      }
-    }
-    if (big)
-      k_rot_keyswitch_s<LG, true, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, nullptr,
-                                                                         nullptr, *tabs_of(c, g, 0));
-    else
-      k_rot_keyswitch_s<LG, false, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                          nullptr, nullptr, TwNone{});
-  }
-}
-
-// Returns true when the launched kernel also produced the next rotation's
-// digits (k_rot_keyswitch_s<.., NEXT = true>).
+// Key switch + fold add of one rotation (apply_galois, context.cpp:428-507;
+// backend.cpp:63-73). Returns true when the launched kernel also produced the
+// next rotation's digits (dig_next != nullptr; small batches only).
+//   N = 8192:  <= 148 blocks    k_rot_keyswitch_w2 (2-group CTA, latency)
+//              >= 296, unfused  k_rot_keyswitch_t  (TMEM accumulators, 3 CTAs/SM)
+//              otherwise        k_rot_keyswitch_s  (shared-memory accumulators)
+//   N = 16384: >= 296, unfused  k_rot_keyswitch_h  (half-ring blocks, TMEM)
+//              otherwise        k_rot_keyswitch_s
+//   other N:   k_rot_keyswitch (generic)
 bool launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* dig,
                           const uint32_t* perm, const uint2* k0, const uint2* k1, uint32_t* out, int fold,
                           cudaStream_t st, const uint32_t* perm_next = nullptr, uint32_t* dig_next = nullptr) {
-  // N <= 8192: shared-memory accumulators, 2 CTAs/SM; N = 16384 (1024
-  // threads) keeps the accumulators in registers when HEI_KS14_REGS=1.
-  if (use_ntt32(c, blocks) && (c->logn == 14 || !dig_next)) {
-    // 32-residue transforms, TMEM accumulators; never fused with the next digit
-    const uint2* q0 = keys32_of(c, k0);
-    const uint2* q1 = keys32_of(c, k1);
-    const size_t smt = smem_bytes(c, 1);
-    const bool ptw = blocks >= 2u * 148u;
-    if (c->logn == 14) {
-      if (ptw)
-        k_rot_keyswitch_t32<14, true, 2><<<blocks, Ntt32<14>::T, smt, st>>>(g, cur, dig, perm, q0, q1, out, fold,
-                                                                             *tabs_of(c, g, 0));
-      else
-        k_rot_keyswitch_t32<14, false, 2><<<blocks, Ntt32<14>::T, smt, st>>>(g, cur, dig, perm, q0, q1, out, fold,
-                                                                              TwNone{});
-    } else {
-      k_rot_keyswitch_t32<13, true, 4><<<blocks, Ntt32<13>::T, smt, st>>>(g, cur, dig, perm, q0, q1, out, fold,
-                                                                           *tabs_of(c, g, 0));
-    }
-    LAUNCHED();
-    return false;
-  }
-  bool fused = dig_next != nullptr;
+  const bool big = blocks >= 2u * 148u;
+  bool next = dig_next != nullptr;
+  const size_t sm = smem_bytes(c, 1);
   switch (c->logn) {
-    case 12:
-      launch_ks_s<12>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, perm_next, dig_next);
-      break;
     case 13:
-      launch_ks_s<13>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, perm_next, dig_next);
+      if (blocks <= 148u) {
+        if (next)
+          k_rot_keyswitch_w2<13, true><<<blocks, 2 * Ntt<13>::T, 6 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                              perm_next, dig_next);
+        else
+          k_rot_keyswitch_w2<13, false><<<blocks, 2 * Ntt<13>::T, 6 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                               nullptr, nullptr);
+      } else if (big && !next) {
+        k_rot_keyswitch_t<<<blocks, Ntt<13>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, *tabs_of(c, g, 0));
+      } else if (big) {
+        k_rot_keyswitch_s<13, true, true><<<blocks, Ntt<13>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                              perm_next, dig_next, *tabs_of(c, g, 0));
+      } else if (next) {
+        k_rot_keyswitch_s<13, false, true><<<blocks, Ntt<13>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                               perm_next, dig_next, TwNone{});
+      } else {
+        k_rot_keyswitch_s<13, false, false><<<blocks, Ntt<13>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                                nullptr, nullptr, TwNone{});
+      }
       break;
     case 14:
-      if (c->ks14_regs) {
-        k_rot_keyswitch_f<14><<<blocks, Ntt<14>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, out, fold);
-        fused = false;
+      if (big && !next) {
+        // one launch per branch, the two halves of a (pair, prime) adjacent
+        const uint32_t pairs = blocks / g.P;
+        for (uint32_t b = 0, gp0 = 0; b < 2; gp0 += g.L[b], ++b) {
+          k_rot_keyswitch_h<<<pairs * g.L[b] * 2, 512, 8192 * 4, st>>>(g, cur, dig, perm, k0, k1, out, fold, gp0,
+                                                                       g.L[b], *tabs_half_pairs(c, g, gp0, g.L[b]));
+          if (b == 0) LAUNCHED();
+        }
+      } else if (big) {
+        k_rot_keyswitch_s<14, true, true><<<blocks, Ntt<14>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                              perm_next, dig_next, *tabs_of(c, g, 0));
+      } else if (next) {
+        k_rot_keyswitch_s<14, false, true><<<blocks, Ntt<14>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                               perm_next, dig_next, TwNone{});
       } else {
-        launch_ks_s<14>(c, g, blocks, cur, dig, perm, k0, k1, out, fold, st, perm_next, dig_next);
+        k_rot_keyswitch_s<14, false, false><<<blocks, Ntt<14>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                                nullptr, nullptr, TwNone{});
       }
       break;
     default:
       k_rot_keyswitch<<<blocks, c->threads(), smem_bytes(c, 3), st>>>(g, cur, dig, perm, k0, k1, out, fold);
-      fused = false;
+      next = false;
   }
   LAUNCHED();
-  return fused;
+  return next;
 }
 // All N mask plaintexts of the context, built once on first use (blocking,
 // on the context stream) and kept for its lifetime.
@@ -924,7 +703,7 @@ void launch_mask_acc(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32
   // enough blocks for every SM at small batches, up to 8 pairs per block
   const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(c->mask_group, npairs * g.P / (148 * 8)));
   const unsigned gblocks = (unsigned)(((npairs + G - 1) / G) * g.P);
-  if (c->mask_cache && c->logn >= 12 && c->logn <= 14 && blocks >= 2u * 148u) {
+  if (c->mask_cache && c->logn >= 13 && c->logn <= 14 && blocks >= 2u * 148u) {
     const uint32_t* masks = mask_table(c);
     const unsigned cb = (unsigned)(((npairs + G - 1) / G) * g.P * (c->n / 1024));
     k_mask_acc_c<<<cb, 256, 0, st>>>(g, res, rows, cols, npairs, G, masks, acc);
@@ -949,56 +728,29 @@ void launch_ct_intt(hei_gpu_ctx* c, unsigned blocks, uint32_t* cts, cudaStream_t
 }
 void launch_poly_ntt(hei_gpu_ctx* c, unsigned blocks, uint32_t gp, uint32_t* polys, int inverse, cudaStream_t st) {
   const size_t sm = smem_bytes(c, 1);
-  if (c->ntt32 && (c->logn == 13 || c->logn == 14)) {
-    if (c->logn == 14) k_poly_ntt32<14><<<blocks, Ntt32<14>::T, sm, st>>>(c->geo, gp, polys, inverse);
-    else k_poly_ntt32<13><<<blocks, Ntt32<13>::T, sm, st>>>(c->geo, gp, polys, inverse);
-    LAUNCHED();
-    return;
-  }
   HEI_DISPATCH(c->logn, (k_poly_ntt_f<LG><<<blocks, Ntt<LG>::T, sm, st>>>(c->geo, gp, polys, inverse)),
                (k_poly_ntt<<<blocks, c->threads(), sm, st>>>(c->geo, gp, polys, inverse)));
   LAUNCHED();
 }
 template <int LG>
 void set_fast_attrs(size_t sm) {
-  set_smem_attr((const void*)k_rot_digits_f<LG, true>, 2 * sm);
-  set_smem_attr((const void*)k_rot_digits_f<LG, false>, 2 * sm);
-  set_smem_attr((const void*)k_rot_keyswitch_f<LG>, sm);
-  set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, false>, 3 * sm);
+  set_smem_attr((const void*)k_rot_digits_f<LG, true>, sm);
+  set_smem_attr((const void*)k_rot_digits_f<LG, false>, sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, false>, 3 * sm);
-  set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
-  if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, true>, 2 * sm);
-  if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, false, true>, 2 * sm);
-  if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, false, false, true>, 2 * sm);
-  if constexpr (LG == 13) set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 3, 4, false, false, true, true>, 2 * sm);
-  if constexpr (LG == 14) {
-    set_smem_attr((const void*)k_rot_keyswitch_t<LG, true, 1, 4>, sm);
-    set_smem_attr((const void*)k_rot_keyswitch_t<LG, false, 1, 4>, sm);
-  }
-  if constexpr (LG == 13 || LG == 14) {
-    set_smem_attr((const void*)k_poly_ntt32<LG>, sm);
-    set_smem_attr((const void*)k_rot_digits32<LG, true>, sm);
-    set_smem_attr((const void*)k_rot_digits32<LG, false>, sm);
-    set_smem_attr((const void*)k_rot_keyswitch_t32<LG, true, LG == 14 ? 2 : 4>, sm);
-    set_smem_attr((const void*)k_rot_keyswitch_t32<LG, false, LG == 14 ? 2 : 4>, sm);
-  }
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, true>, 3 * sm);
-  set_smem_attr((const void*)k_rot_keyswitch_c2<LG, true>, 3 * sm);
-  set_smem_attr((const void*)k_rot_keyswitch_c2<LG, false>, 3 * sm);
-  if constexpr (LG <= 13) {
+  set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
+  if constexpr (LG == 13) {
+    set_smem_attr((const void*)k_rot_keyswitch_t, sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, true>, 6 * sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, false>, 6 * sm);
   }
   set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
   set_smem_attr((const void*)k_mask_prep<LG>, sm);
   set_smem_attr((const void*)k_mask_table<LG>, sm);
-  set_smem_attr((const void*)k_ks_part<LG>, sm);
-  set_smem_attr((const void*)k_ks_part2<LG>, sm);
   set_smem_attr((const void*)k_ct_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_ct_intt_f<LG>, sm);
   set_smem_attr((const void*)k_poly_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_bl_encode<LG>, sm);
-  set_smem_attr((const void*)k_bl_encrypt<LG, true>, sm);
   set_smem_attr((const void*)k_bl_encrypt<LG, false>, sm);
   set_smem_attr((const void*)k_bl_encrypt<LG, true, (LG <= 13 ? 3 : 1)>, sm);
   set_smem_attr((const void*)k_prepare_pk<LG>, sm);
@@ -1016,11 +768,10 @@ uint64_t auto_batch_pairs(hei_gpu_ctx* c) {
 
 // The rotate-and-sum fold over `pairs` twin ciphertexts in `cur` (eval form);
 // returns the buffer holding the result.
-uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st, bool split,
-                    uint32_t* part, uint32_t* dig, uint32_t* dig2) {
+uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st, uint32_t* dig,
+                    uint32_t* dig2) {
   const Geo& g = c->geo;
   const unsigned blocks = (unsigned)(pairs * c->P());
-  const uint32_t Lmax = std::max(c->L[0], c->L[1]);
   bool have_digits = false;  // digits of this rotation already produced by the previous key switch
   const size_t S = c->fold_elts.size();
   for (size_t k = 0; k < S; ++k) {
@@ -1028,7 +779,7 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
     const uint32_t* perm = c->d_perms + (size_t)c->perm_index.at(elt) * c->n;
     // fused digits pay off when launches are too small to fill the GPU
     // (latency path); large batches keep the separate 3-CTA/SM digit kernel
-    const bool fuse = c->fuse_digits && (blocks < 4u * 148u || (c->fuse_big && c->ks_tmem && c->logn == 13));
+    const bool fuse = c->fuse_digits && blocks < 4u * 148u;
     const uint32_t* perm_next =
         (k + 1 < S && fuse) ? c->d_perms + (size_t)c->perm_index.at(c->fold_elts[k + 1]) * c->n : nullptr;
     const uint2* k0 = c->d_keys[0] + (size_t)c->key_index[0].at(elt) * c->L[0] * 2 * c->L[0] * c->n;
@@ -1042,29 +793,9 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
     }
     if (!have_digits) launch_rot_digits(c, g, blocks, cur, perm, dig, st);
     if (c->timing) CU(cudaEventRecord(e1, st));
-    have_digits = false;
-    if (split && c->split == 2) {
-      const uint32_t Lm1 = Lmax - 1;
-      HEI_DISPATCH(c->logn,
-                   (k_ks_part2<LG><<<(unsigned)(blocks * Lm1), Ntt<LG>::T, smem_bytes(c, 1), st>>>(g, dig, k0, k1, part, Lm1)),
-                   (void)0);
-      LAUNCHED();
-      k_ks_reduce2<<<blocks * (c->n / 1024), 256, 0, st>>>(g, cur, part, perm, k0, k1, Lm1, other, 1);
-      LAUNCHED();
-    } else if (split) {
-      const unsigned pb = (unsigned)(blocks * Lmax);
-      HEI_DISPATCH(c->logn,
-                   (k_ks_part<LG><<<pb, Ntt<LG>::T, smem_bytes(c, 1), st>>>(g, cur, dig, perm, k0, k1, part, Lmax,
-                                                                          *tabs_of(c, g, 0))),
-                   (void)0);
-      LAUNCHED();
-      k_ks_reduce<<<blocks * (c->n / 1024), 256, 0, st>>>(g, cur, part, perm, Lmax, other, 1);
-      LAUNCHED();
-    } else {
-      have_digits = launch_rot_keyswitch(c, g, blocks, cur, dig, perm, k0, k1, other, 1, st, perm_next,
-                                         perm_next ? dig2 : nullptr);
-      if (have_digits) std::swap(dig, dig2);
-    }
+    have_digits = launch_rot_keyswitch(c, g, blocks, cur, dig, perm, k0, k1, other, 1, st, perm_next,
+                                       perm_next ? dig2 : nullptr);
+    if (have_digits) std::swap(dig, dig2);
     if (c->timing) {
       CU(cudaEventRecord(e2, st));
       c->fold_ev.push_back({e0, e1, e2});
@@ -1083,12 +814,8 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
   uint32_t* dig2 = c->d_dig2 + (dig - c->d_dig);  // second digit buffer of the same region
   const unsigned blocks = (unsigned)(pairs * c->P());
   const bool small = blocks < 2u * 148u;
-  // optionally split the key switch over digits for parallelism (HEI_SPLIT=1)
-  const bool split = c->logn >= 12 && c->logn <= 14 && small && c->split;
-  const uint32_t Lmax = std::max(c->L[0], c->L[1]);
-  uint32_t* part = split ? pool_get(c->pool_part, c->pool_part_bytes, (size_t)blocks * Lmax * 2 * c->n * 4) : nullptr;
   uint32_t* result = (c->fold_elts.size() % 2) ? other : cur;
-  if (!small || c->timing || !c->graphs) return fold_impl(c, pairs, cur, other, st, split, part, dig, dig2);
+  if (!small || c->timing || !c->graphs) return fold_impl(c, pairs, cur, other, st, dig, dig2);
   // drop graphs of an older key/scratch generation, and keep the cache
   // bounded (a long-running server sees many small batch sizes); an
   // executable graph still in flight is freed when it completes
@@ -1106,9 +833,7 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
     c->fold_graphs.erase(c->fold_graphs.begin());
   }
   for (auto& fg : c->fold_graphs)
-    if (fg.pairs == pairs && fg.cur == cur && fg.other == other && fg.part == part && fg.dig == dig &&
-        fg.gen == c->graph_gen &&
-        fg.split == split) {
+    if (fg.pairs == pairs && fg.cur == cur && fg.other == other && fg.dig == dig && fg.gen == c->graph_gen) {
       CU(cudaGraphLaunch(fg.exec, st));
       g_launches += fg.launches;
       return result;
@@ -1116,12 +841,12 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
   const uint64_t before = g_launches;
   cudaGraph_t graph = nullptr;
   CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  fold_impl(c, pairs, cur, other, st, split, part, dig, dig2);
+  fold_impl(c, pairs, cur, other, st, dig, dig2);
   CU(cudaStreamEndCapture(st, &graph));
   cudaGraphExec_t exec = nullptr;
   CU(cudaGraphInstantiate(&exec, graph, 0));
   cudaGraphDestroy(graph);
-  c->fold_graphs.push_back({pairs, cur, other, part, dig, c->graph_gen, split, exec, g_launches - before});
+  c->fold_graphs.push_back({pairs, cur, other, dig, c->graph_gen, exec, g_launches - before});
   g_launches = before;
   CU(cudaGraphLaunch(exec, st));
   g_launches += c->fold_graphs.back().launches;
@@ -1214,7 +939,7 @@ bool run_rows(hei_gpu_stream* s, const uint32_t* d_in, const uint64_t* d_rows, u
   }
   // latency path: the mask plaintexts are computed on a side stream while
   // the fold runs (they depend only on the slot)
-  const bool premask = c->logn >= 12 && c->logn <= 14 && blocksP < 2u * 148u && c->premask;
+  const bool premask = c->logn >= 13 && c->logn <= 14 && blocksP < 2u * 148u && c->premask;
   cudaEvent_t mask_ev = nullptr;
   uint32_t* masks = nullptr;
   if (premask) {
@@ -1820,34 +1545,19 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (d->t[0] == d->t[1]) raise(HEI_PARAM_ERROR, "twin moduli must differ");
     auto c = std::make_unique<hei_gpu_ctx>();
     c->device = d->device;
-    if (const char* v = std::getenv("HEI_KS14_REGS")) c->ks14_regs = std::atoi(v) != 0;
-    if (const char* v = std::getenv("HEI_NTT32")) c->ntt32 = std::atoi(v);
-    if (const char* v = std::getenv("HEI_SPLIT")) c->split = std::atoi(v);
     if (const char* v = std::getenv("HEI_NO_GRAPHS")) c->graphs = std::atoi(v) == 0;
     if (const char* v = std::getenv("HEI_TWO_STREAMS")) c->two_streams = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MT_JUMP")) c->mt_jump = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_DIGITS")) c->fuse_digits = std::atoi(v) != 0;
-    if (const char* v = std::getenv("HEI_CLUSTER_KS")) c->cluster_ks = std::atoi(v) != 0;
-    if (const char* v = std::getenv("HEI_GROUP_KS")) c->group_ks = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_FOLD_PARTS"))
       c->fold_parts = std::min<uint32_t>(kMaxFoldParts, std::max(1, std::atoi(v)));
-    if (const char* v = std::getenv("HEI_KS_TMEM")) c->ks_tmem = std::atoi(v);
-    if (const char* v = std::getenv("HEI_ENC_MINB")) c->enc_minb = std::atoi(v);
-    if (const char* v = std::getenv("HEI_PRIME_MAJOR")) c->prime_major = std::atoi(v) != 0;
-    if (const char* v = std::getenv("HEI_KS14_TMEM")) c->ks14_tmem = std::atoi(v) != 0;
-    if (const char* v = std::getenv("HEI_KS14_HALF")) c->ks14_half = std::atoi(v);
-    if (const char* v = std::getenv("HEI_HALF13")) c->half13 = std::atoi(v) != 0;
-    if (const char* v = std::getenv("HEI_DIG14_HALF")) c->dig14_half = std::atoi(v);
     if (const char* v = std::getenv("HEI_DOT_ROWS")) c->dot_rows = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_CACHE")) c->mask_cache = std::atoi(v) != 0;
-    if (const char* v = std::getenv("HEI_FUSE_BIG")) c->fuse_big = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_OVERLAP")) c->e2e_overlap = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MASK_GROUP")) c->mask_group = std::max(1, std::atoi(v));
-    if (const char* v = std::getenv("HEI_DIG_TMA")) c->dig_tma = std::atoi(v);
-    if (const char* v = std::getenv("HEI_LAT_TMA")) c->lat_tma = std::atoi(v) != 0;
     c->n = n;
     c->logn = 31 - __builtin_clz(n);
     c->s_x = d->s_x;
@@ -2002,7 +1712,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     }
     // pass-C twiddles for the register-blocked transforms (ntt_fast.cuh)
     std::vector<uint4> twc, itwc;
-    if (c->logn >= 12 && c->logn <= 14) {
+    if (c->logn == 13 || c->logn == 14) {
       const uint32_t T = n / 16, XST = c->logn - 12, PAD = XST % 2 == 0 ? 1 : 0, KC = (PAD + XST + 16) / 2;
       g.twc_stride = KC * T;
       twc.resize((size_t)(P + 2) * KC * T);
@@ -2027,7 +1737,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     // N = 16384 half-ring tables (ks_half.cuh): half h's stage s' block i'
     // uses zetas[2^(s'+1) + h 2^s' + i'], stored at local index 2^s' + i'
     std::vector<uint4> twch, itwch;
-    if (c->logn == 14 || c->logn == 13) {
+    if (c->logn == 14) {
       const uint32_t hl = c->logn - 1, nh = n / 2, T = nh / 16, XST = hl - 12, PAD = XST % 2 == 0 ? 1 : 0,
                      KC = (PAD + XST + 16) / 2;  // Ntt<hl>'s pass-C layout
       g.twch_stride = KC * T;
@@ -2061,40 +1771,8 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
           }
         }
     }
-    // pass-C twiddles of the 32-residue transforms (ntt32.cuh)
-    std::vector<uint4> twc32, itwc32;
-    if (c->logn == 13 || c->logn == 14) {
-      const uint32_t T = n / 32, NC = c->logn - 10, EC = c->logn == 14 ? 30 : 28, KC = EC / 2;
-      g.twc32_stride = KC * T;
-      twc32.resize((size_t)(P + 2) * KC * T);
-      itwc32.resize(twc32.size());
-      std::vector<uint32_t> idx(EC);
-      for (uint32_t row = 0; row < P + 2; ++row)
-        for (uint32_t j = 0; j < T; ++j) {
-          uint32_t e = 0;
-          for (uint32_t st = 10; st < 10 + NC; ++st) {
-            const uint32_t gsh = c->logn - st;  // log2 of the twiddle group size
-            for (uint32_t b = 0; b < (32u >> gsh); ++b) idx[e++] = (1u << st) + ((32u * j) >> gsh) + b;
-          }
-          for (uint32_t k = 0; k < KC; ++k) {
-            const uint2 a = fwd[(size_t)row * n + idx[2 * k]], b = fwd[(size_t)row * n + idx[2 * k + 1]];
-            const uint2 ia = inv[(size_t)row * n + idx[2 * k]], ib = inv[(size_t)row * n + idx[2 * k + 1]];
-            twc32[((size_t)row * KC + k) * T + j] = make_uint4(a.x, a.y, b.x, b.y);
-            itwc32[((size_t)row * KC + k) * T + j] = make_uint4(ia.x, ia.y, ib.x, ib.y);
-          }
-        }
-    }
     set_device(c.get());
     CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    if (!twc32.empty()) {
-      CU(cudaMalloc(&c->d_twc32, twc32.size() * sizeof(uint4)));
-      CU(cudaMalloc(&c->d_itwc32, itwc32.size() * sizeof(uint4)));
-      CU(cudaMemcpyAsync(c->d_twc32, twc32.data(), twc32.size() * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
-      CU(cudaMemcpyAsync(c->d_itwc32, itwc32.data(), itwc32.size() * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
-      CU(cudaStreamSynchronize(c->stream));
-      g.twc32 = c->d_twc32;
-      g.itwc32 = c->d_itwc32;
-    }
     if (!twch.empty()) {
       CU(cudaMalloc(&c->d_twch, twch.size() * sizeof(uint4)));
       CU(cudaMalloc(&c->d_fwdh, c->h_fwdh.size() * sizeof(uint2)));
@@ -2143,7 +1821,6 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     g.fwd = c->d_fwd;
     g.inv = c->d_inv;
     g.index_map = c->d_index;
-    g.prime_major = c->prime_major ? 1u : 0u;
     const size_t s3 = smem_bytes(c.get(), 3);
     set_smem_attr((const void*)k_rot_keyswitch, s3);
     set_smem_attr((const void*)k_rot_digits, smem_bytes(c.get(), 1));
@@ -2161,7 +1838,6 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     set_smem_attr((const void*)k_prepare_sk, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_kg_pk, smem_bytes(c.get(), 1));
     set_smem_attr((const void*)k_kg_gk, smem_bytes(c.get(), 1));
-    if (c->logn == 12) set_fast_attrs<12>(smem_bytes(c.get(), 1));
     if (c->logn == 13) set_fast_attrs<13>(smem_bytes(c.get(), 1));
     if (c->logn == 14) set_fast_attrs<14>(smem_bytes(c.get(), 1));
     *out = c.release();
@@ -2179,15 +1855,12 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->d_itwch);
   cudaFree(c->d_invh);
   cudaFree(c->d_itwc);
-  cudaFree(c->d_twc32);
   cudaFree(c->d_mask_table);
-  cudaFree(c->d_itwc32);
   cudaFree(c->d_index);
   cudaFree(c->d_perms);
   cudaFree(c->d_err);
   for (int b = 0; b < 2; ++b) {
     cudaFree(c->d_keys[b]);
-    cudaFree(c->d_keys32[b]);
     cudaFree(c->d_pk[b]);
   }
   cudaFree(c->d_pkp);
@@ -2196,7 +1869,6 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->pool_rows);
   cudaFree(c->pool_bias);
   cudaFree(c->pool_stage64);
-  cudaFree(c->pool_part);
   if (c->pinned_bias) cudaFreeHost(c->pinned_bias);
   if (c->pinned_out) cudaFreeHost(c->pinned_out);
   cudaFree(c->pool_in32);
@@ -2297,16 +1969,9 @@ void install_galois_keys(hei_gpu_ctx* c, uint32_t b, uint32_t count, const uint6
   if (c->d_keys[b]) cudaFree(c->d_keys[b]);
   c->d_keys[b] = nullptr;
   CU(cudaMalloc(&c->d_keys[b], words * sizeof(uint2)));
-  k_prepare_keys<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, b, count, d_raw, c->d_keys[b], c->d_err, 16);
+  k_prepare_keys<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, b, count, d_raw, c->d_keys[b], c->d_err);
   LAUNCHED();
   c->keys_words[b] = words;
-  if (c->d_keys32[b]) cudaFree(c->d_keys32[b]);
-  c->d_keys32[b] = nullptr;
-  if (c->ntt32 && (c->logn == 13 || c->logn == 14)) {
-    CU(cudaMalloc(&c->d_keys32[b], words * sizeof(uint2)));
-    k_prepare_keys<<<grid_for(words, 256), 256, 0, c->stream>>>(c->geo, b, count, d_raw, c->d_keys32[b], c->d_err, 32);
-    LAUNCHED();
-  }
   CU(cudaStreamSynchronize(c->stream));
   check_err_flag(c, HEI_CODEC_ERROR, "galois keys: coefficient not reduced");
   c->key_index[b] = idx;
@@ -3214,7 +2879,6 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
     const Geo& g = c->geo;
     const uint32_t n = c->n, P = c->P();
     const uint64_t B = (rows + n - 1) / n;
-    const bool fast = c->logn >= 12 && c->logn <= 14;
     // prepared public key [gp][part] (cached)
     if (!c->d_pkp) {
       CU(cudaMalloc(&c->d_pkp, 2ull * P * n * sizeof(uint2)));
@@ -3350,7 +3014,6 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
       cudaEventDestroy(gen[k]);
       cudaEventDestroy(used[k]);
     }
-    (void)fast;
     k_bl_finish_lin<<<(unsigned)(B * cols * P), c->threads(), 3 * n * 4, st>>>(g, d_res, c->d_pk[0], c->d_pk[1],
                                                                                 d_bias, (uint32_t)cols, d_out);
     LAUNCHED();

@@ -24,8 +24,6 @@
 // Textually included by heinfer_b200.cu after tmem_ks.cuh.
 #pragma once
 
-// LOGF = 14 (C5: 512-thread halves, 3 CTAs/SM) or 13 (256-thread halves,
-// 6 CTAs/SM; measured against the 512-thread full-ring kernel).
 // Galois gather of a thread's 16 slots: their sources form one aligned
 // 16-slot group (the automorphism maps groups onto groups), so the group is
 // read with 4 x 128-bit loads and permuted through a per-thread column of
@@ -48,39 +46,26 @@ __device__ __forceinline__ void gather_group(const uint32_t* __restrict__ src, c
   for (int r = 0; r < 16; ++r) e[r] = scr[(pm[r] & 15u) * T + j];
 }
 
-template <bool PTW, int LOGF = 14>
-__global__ void __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6) k_rot_keyswitch_h(Geo g, const uint32_t* __restrict__ dot,
+// One launch per branch: both halves of primes [gp0, gp0 + np) with
+// blockIdx = (pair * np + prime - gp0) * 2 + h, so the two halves of a
+// (pair, prime) run side by side and the second read of each digit hits L2;
+// the parameter-space twiddle rows are [prime - gp0][h].
+__global__ void __launch_bounds__(512, 3) k_rot_keyswitch_h(Geo g, const uint32_t* __restrict__ dot,
                                                            const uint32_t* __restrict__ digits,
                                                            const uint32_t* __restrict__ perm,
                                                            const uint2* __restrict__ key0,
                                                            const uint2* __restrict__ key1,
-                                                           uint32_t* __restrict__ out, int fold, uint32_t hsel,
-                                                           uint32_t gp0, uint32_t np,
-                                                           const __grid_constant__ TwArg<PTW> tab) {
+                                                           uint32_t* __restrict__ out, int fold, uint32_t gp0,
+                                                           uint32_t np, const __grid_constant__ TwAB tab) {
+  constexpr int LOGF = 14;
   using NT = Ntt<LOGF - 1>;
   constexpr uint32_t NF = 1u << LOGF, NH = NF / 2, T = NH / 16, TF = NF / 16;
   constexpr uint32_t kTmemCols = T / 4;
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
   __shared__ uint32_t tbase;
-  // hsel < 2: this launch covers half hsel of every (pair, prime), blockIdx =
-  // pair * P + prime. hsel == 2: both halves of primes [gp0, gp0 + np) with
-  // blockIdx = (pair * np + prime - gp0) * 2 + h, so the two halves of a
-  // (pair, prime) run side by side and the second digit read hits L2; the
-  // parameter rows are then [prime - gp0][h].
-  uint32_t pair, gp, h, row;
-  if (hsel < 2) {
-    pair = blockIdx.x / g.P;
-    gp = blockIdx.x % g.P;
-    h = hsel;
-    row = gp;
-  } else {
-    const uint32_t loc = blockIdx.x >> 1;
-    h = blockIdx.x & 1u;
-    pair = loc / np;
-    gp = gp0 + loc % np;
-    row = (loc % np) * 2 + h;
-  }
+  const uint32_t loc = blockIdx.x >> 1, h = blockIdx.x & 1u;
+  const uint32_t pair = loc / np, gp = gp0 + loc % np, row = (loc % np) * 2 + h;
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t q = pr.q, L = pr.L, i = pr.i;
   const uint32_t j = threadIdx.x, warp = j >> 5;
@@ -93,7 +78,6 @@ __global__ void __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6) k_rot_k
   const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * NF;
   const uint2 z1 = __ldg(g.fwd + (size_t)gp * NF + 1);  // first-stage twiddle zetas[1]
   const uint4* twc = g.twch + ((size_t)gp * 2 + h) * g.twch_stride;
-  const uint2* twn = g.fwdh + ((size_t)gp * 2 + h) * NH;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tbase)),
                  "n"(kTmemCols)
@@ -147,10 +131,7 @@ __global__ void __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6) k_rot_k
       const uint32_t t = mul_shoup(v, z1.x, z1.y, q);
       e[r] = h ? sub_mod(u, t, q) : add_mod(u, t, q);
     }
-    if constexpr (PTW)
-      NT::template fwd<true>(e, sm, ParamTw{tab.w[row]}, twc, q);
-    else
-      NT::template fwd<true>(e, sm, twn, twc, q);
+    NT::template fwd<true>(e, sm, ParamTw{tab.w[row]}, twc, q);
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * NF) + jf;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * NF) + jf;
     tm_wait_st();  // the previous digit's accumulator stores have landed
@@ -220,10 +201,10 @@ __global__ void __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6) k_rot_k
 // memory, reads its partner's through distributed shared memory, and writes
 // its own output half: (U + V) n^-1 for half 0, (U - V) inv_zetas[1] n^-1 for
 // half 1 — the digit comes out finished, exactly as k_rot_digits_f<14>'s.
-template <bool PTW, int LOGF = 14>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1u << LOGF) / 32, LOGF == 14 ? 3 : 6)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 3)
     k_rot_digits_h(Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ perm,
-                   uint32_t* __restrict__ digits, int stage, const __grid_constant__ TwArg<PTW> itab) {
+                   uint32_t* __restrict__ digits) {
+  constexpr int LOGF = 14;
   using NT = Ntt<LOGF - 1>;
   constexpr uint32_t NF = 1u << LOGF, NH = NF / 2;
   extern __shared__ uint4 smem4[];
@@ -237,35 +218,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1u << LOGF) / 32, L
   const uint32_t* c1 = dot + (uint64_t)pair * g.ct_words + (uint64_t)pr.poly1 * NF;
   const uint32_t x0 = h * NH + NT::posC0(j);
   uint32_t pm[16], e[16];
-  if (stage) {
-    // each CTA stages its half of c1 with one TMA bulk copy; the Galois
-    // gather then reads the cluster's shared memory (a thread's 16 sources
-    // lie in one aligned 16-slot group, so in one CTA's half)
-    __shared__ uint64_t bar;
-    if (threadIdx.x == 0) {
-      mbar_init(&bar, 1);
-      bulk_load(sm, c1 + h * NH, NH * 4, &bar);
-    }
-    load16_ro(perm + x0, pm);
-    __syncthreads();
-    mbar_wait(&bar, 0);
-    cl.sync();  // both halves staged
-    const uint32_t* src = cl.map_shared_rank(sm, pm[0] / NH);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) e[r] = src[pm[r] % NH];
-    cl.sync();  // every gather of this CTA's half is done before the transform reuses it
-  } else {
-    load16_ro(perm + x0, pm);
-    gather_group<NT::T>(c1, pm, sm, e);  // sm is free until the transform's first barrier
-  }
+  load16_ro(perm + x0, pm);
+  gather_group<NT::T>(c1, pm, sm, e);  // sm is free until the transform's first barrier
   const uint2* itn = g.invh + ((size_t)gp * 2 + h) * NH;
   const uint4* itc = g.itwch + ((size_t)gp * 2 + h) * g.twch_stride;
   const uint2 lastH = __ldg(itn + 1);                               // local last stage: inv_zetas[2 + h]
   const uint2 one = make_uint2(1u, (uint32_t)(0x100000000ull / q));  // Shoup constant of 1: a plain reduction
-  if constexpr (PTW)
-    NT::inv(e, sm, ParamTw{itab.w[gp]}, itc, q, lastH, one);
-  else
-    NT::inv(e, sm, itn, itc, q, lastH, one);
+  NT::inv(e, sm, itn, itc, q, lastH, one);
   __syncthreads();  // the transform's last shared reads are done
 #pragma unroll
   for (int r = 0; r < 16; ++r) sm[NT::posA(j, r)] = e[r];

@@ -38,15 +38,10 @@ __device__ __forceinline__ void tm_st(uint32_t taddr, const uint32_t (&v)[X]) {
                  : "memory");
 }
 // wait::ld, threading the loaded registers through so no use is scheduled
-// before the wait. MEM = false drops the memory clobber: ordering against the
-// other tcgen05 instructions is kept (all are volatile asm), and read-only
-// global loads (the Galois key) may be scheduled across the wait.
-template <int X, bool MEM = true>
+// before the wait.
+template <int X>
 __device__ __forceinline__ void tm_wait_ld(uint32_t (&a)[X], uint32_t (&b)[X]) {
-  if constexpr (!MEM && X == 4)
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]));
-  else if constexpr (X == 8)
+  if constexpr (X == 8)
     asm volatile("tcgen05.wait::ld.sync.aligned;"
                  : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
                    "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7])
@@ -58,66 +53,36 @@ __device__ __forceinline__ void tm_wait_ld(uint32_t (&a)[X], uint32_t (&b)[X]) {
                  :
                  : "memory");
 }
-// Galois-key read: NA = true streams it past L1 (L1::no_allocate), leaving
-// L1 to the pass-C twiddles that every digit transform of the CTA re-reads.
-template <bool NA>
-__device__ __forceinline__ uint4 ldg_key(const uint4* p) {
-  if constexpr (NA) {
-    uint4 v;
-    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-        : "l"(p));
-    return v;
-  } else {
-    return __ldg(p);
-  }
-}
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 
-// GS: accumulator slots per TMEM load/store round (8 or 4).
-// NEXT: also produce the next rotation's digit for prime i (as
-// k_rot_keyswitch_s<.., NEXT>): the new c1 lands in a second shared buffer,
-// is permuted by the next Galois element and inverse-transformed here.
-// PF: each digit arrives in a second shared buffer by a TMA bulk copy issued
-// as soon as the previous digit's transform has passed its barriers.
-// PP: consecutive digit transforms alternate between two exchange buffers
-// (sm + N first, then sm, ...), so each transform skips its leading barrier.
-// HOIST: the digit loop's TMEM wait carries no memory clobber (see tm_wait_ld).
-// NA: Galois keys read with L1::no_allocate (ldg_key).
-// L2PF: one thread prefetches the next digit (and, at the last digit, c0)
-// into L2 with a bulk prefetch, so the digit loads hit L2 instead of HBM.
-// GG: the Galois gathers of c1 (l == i term) and c0 read each thread's one
-// aligned 16-slot source group with 4 x 128-bit loads, permuted through a
-// per-thread shared-memory column, instead of TMA-staging the polynomials.
-template <int LOGN, bool PTW, int MINB, int GS = 8, bool NEXT = false, bool PF = false, bool PP = false,
-          bool HOIST = false, bool NA = false, bool L2PF = false, bool GG = false>
-__global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, const uint32_t* __restrict__ dot,
-                                                                      const uint32_t* __restrict__ digits,
-                                                                      const uint32_t* __restrict__ perm,
-                                                                      const uint2* __restrict__ key0,
-                                                                      const uint2* __restrict__ key1,
-                                                                      uint32_t* __restrict__ out, int fold,
-                                                                      const uint32_t* __restrict__ perm_next,
-                                                                      uint32_t* __restrict__ dig_next,
-                                                                      const __grid_constant__ TwArg<PTW> tab) {
-  using NT = Ntt<LOGN>;
-  static_assert(NT::T == 512 || NT::T == 1024, "TMEM layout: 4 or 8 warps per lane quarter");
-  static_assert(!(PP && (PF || NEXT)), "PP uses sm + N as its second exchange buffer");
+// N = 8192 full batches: 512 threads, 40 registers, 3 CTAs per SM (the
+// launch bound), accumulators exchanged with TMEM in rounds of GS = 4 slots
+// (tcgen05.ld/st 32x32b.x4). c1 (for the l == i term) and c0 (for the
+// epilogue) are staged in the exchange buffer by TMA bulk copies so the
+// Galois gathers read shared memory.
+__global__ void __launch_bounds__(512, 3) k_rot_keyswitch_t(Geo g, const uint32_t* __restrict__ dot,
+                                                          const uint32_t* __restrict__ digits,
+                                                          const uint32_t* __restrict__ perm,
+                                                          const uint2* __restrict__ key0,
+                                                          const uint2* __restrict__ key1,
+                                                          uint32_t* __restrict__ out, int fold,
+                                                          const __grid_constant__ TwAB tab) {
+  using NT = Ntt<13>;
+  constexpr int GS = 4;
   constexpr uint32_t kTmemCols = NT::T / 4;  // 32 columns per warp, warps of a lane quarter side by side
   constexpr uint32_t N = NT::N, T = NT::T;
   extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
-  __shared__ uint64_t gbar, dbar;
+  __shared__ uint64_t gbar;
   __shared__ uint32_t tbase;
   uint32_t pair, gp;
   block_pair_prime(g, pair, gp);
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t q = pr.q, L = pr.L, i = pr.i;
   const uint32_t j = threadIdx.x, x0 = NT::posC0(j), warp = j >> 5;
-  uint32_t* stg = sm + N;  // PF: digit staging buffer
   const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
   const uint32_t* ct = dot + (uint64_t)pair * g.ct_words;
   const uint32_t* c0 = ct + (uint64_t)pr.poly0 * N;
@@ -129,35 +94,15 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (GG) {
-    const uint4* gs = reinterpret_cast<const uint4*>(c1 + (__ldg(perm + x0) & ~15u));
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint4 v = __ldg(gs + c);
-      sm[(4 * c) * T + j] = v.x;
-      sm[(4 * c + 1) * T + j] = v.y;
-      sm[(4 * c + 2) * T + j] = v.z;
-      sm[(4 * c + 3) * T + j] = v.w;
-    }
-  }
   if (threadIdx.x == 32) {
     mbar_init(&gbar, 1);
-    if (!GG) bulk_load(sm, c1, N * 4, &gbar);
-    if constexpr (L2PF) {
-      if (L > 1) bulk_prefetch_l2(dig + (uint64_t)(i == 0 ? 1 : 0) * N, N * 4);
-    }
-    if constexpr (PF) {
-      mbar_init(&dbar, 1);
-      if (L > 1) bulk_load(stg, dig + (uint64_t)(i == 0 ? 1 : 0) * N, N * 4, &dbar);
-    }
+    bulk_load(sm, c1, N * 4, &gbar);
   }
   tm_fence_before();
   __syncthreads();
   tm_fence_after();
   const uint32_t ta = tbase + ((32u * (warp & 3u)) << 16) + 32u * (warp >> 2);  // acc0 cols; acc1 at +16
-  if (!GG) mbar_wait(&gbar, 0);
-  // source of slot s of the permuted polynomial staged in sm
-  auto src_of = [&](uint32_t s) { return GG ? (s & 15u) * T + j : s; };
+  mbar_wait(&gbar, 0);
   const uint4* pp = reinterpret_cast<const uint4*>(perm + x0);
   {
     // l == i term: NTT_i(INTT_i(x)) = x, so sigma(c1)_i multiplies the key directly
@@ -169,9 +114,9 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
 #pragma unroll
       for (int c = h * GS / 4; c < (h + 1) * GS / 4; ++c) {
         const uint4 pm = __ldg(pp + c);
-        const uint32_t d0 = sm[src_of(pm.x)], d1 = sm[src_of(pm.y)], d2 = sm[src_of(pm.z)], d3 = sm[src_of(pm.w)];
-        const uint4 a = ldg_key<NA>(k0 + (2 * c) * T), b = ldg_key<NA>(k0 + (2 * c + 1) * T);
-        const uint4 u = ldg_key<NA>(k1 + (2 * c) * T), v = ldg_key<NA>(k1 + (2 * c + 1) * T);
+        const uint32_t d0 = sm[pm.x], d1 = sm[pm.y], d2 = sm[pm.z], d3 = sm[pm.w];
+        const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
+        const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
         const int o = 4 * c - GS * h;
         A[o] = mul_shoup(d0, a.x, a.y, q);
         A[o + 1] = mul_shoup(d1, a.z, a.w, q);
@@ -188,56 +133,20 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
   }
   const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
   uint32_t e[16];
-  uint32_t dpar = 0, nt = 0;
   for (uint32_t l = 0; l < L; ++l) {
     if (l == i) continue;
-    if constexpr (PF) {
-      mbar_wait(&dbar, dpar);
-      dpar ^= 1u;
+    const uint32_t* src = dig + (uint64_t)l * N;
+    if (pr.fast_reduce) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
-        const uint32_t v = stg[NT::posA(j, r)];
-        e[r] = pr.fast_reduce ? min(v, v - q) : v % q;
+        const uint32_t v = src[NT::posA(j, r)];
+        e[r] = min(v, v - q);
       }
     } else {
-      const uint32_t* src = dig + (uint64_t)l * N;
-      if constexpr (L2PF) {
-        if (threadIdx.x == 0) {
-          uint32_t ln = l + 1;
-          if (ln == i) ++ln;
-          bulk_prefetch_l2(ln < L ? dig + (uint64_t)ln * N : c0, N * 4);
-        }
-      }
-      if (pr.fast_reduce) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const uint32_t v = src[NT::posA(j, r)];
-          e[r] = min(v, v - q);
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
-      }
+      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
     }
-    if constexpr (PP) {
-      uint32_t* xb = sm + ((nt++ & 1u) ? 0u : N);
-      if constexpr (PTW)
-        NT::template fwd<true, ParamTw, false>(e, xb, ParamTw{tab.w[gp]}, twc, q);
-      else
-        NT::template fwd<true, const uint2*, false>(e, xb, g.fwd + (size_t)gp * N, twc, q);
-    } else if constexpr (PTW)
-      NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
-    else
-      NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
-    if constexpr (PF) {
-      // every thread read the staged digit before the transform's barriers
-      uint32_t ln = l + 1;
-      if (ln == i) ++ln;
-      if (ln < L && threadIdx.x == 0) {
-        fence_proxy_async_smem();
-        bulk_load(stg, dig + (uint64_t)ln * N, N * 4, &dbar);
-      }
-    }
+    NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
     tm_wait_st();  // the previous digit's accumulator stores have landed
@@ -246,16 +155,16 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
       uint32_t A[GS], B[GS];
       tm_ld(ta + GS * h, A);
       tm_ld(ta + 16 + GS * h, B);
-      tm_wait_ld<GS, !HOIST>(A, B);
+      tm_wait_ld(A, B);
 #pragma unroll
       for (int c = h * GS / 4; c < (h + 1) * GS / 4; ++c) {
-        const uint4 a = ldg_key<NA>(k0 + (2 * c) * T), b = ldg_key<NA>(k0 + (2 * c + 1) * T);
+        const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
         const int o = 4 * c - GS * h;
         A[o] = add_mod(A[o], mul_shoup(e[4 * c], a.x, a.y, q), q);
         A[o + 1] = add_mod(A[o + 1], mul_shoup(e[4 * c + 1], a.z, a.w, q), q);
         A[o + 2] = add_mod(A[o + 2], mul_shoup(e[4 * c + 2], b.x, b.y, q), q);
         A[o + 3] = add_mod(A[o + 3], mul_shoup(e[4 * c + 3], b.z, b.w, q), q);
-        const uint4 u = ldg_key<NA>(k1 + (2 * c) * T), v = ldg_key<NA>(k1 + (2 * c + 1) * T);
+        const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
         B[o] = add_mod(B[o], mul_shoup(e[4 * c], u.x, u.y, q), q);
         B[o + 1] = add_mod(B[o + 1], mul_shoup(e[4 * c + 1], u.z, u.w, q), q);
         B[o + 2] = add_mod(B[o + 2], mul_shoup(e[4 * c + 2], v.x, v.y, q), q);
@@ -267,22 +176,12 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
   }
   uint32_t* o = out + (uint64_t)pair * g.ct_words;
   __syncthreads();  // the last NTT's exchange reads of sm are done
-  if (GG) {
-    const uint4* gs = reinterpret_cast<const uint4*>(c0 + (__ldg(perm + x0) & ~15u));
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint4 v = __ldg(gs + c);
-      sm[(4 * c) * T + j] = v.x;
-      sm[(4 * c + 1) * T + j] = v.y;
-      sm[(4 * c + 2) * T + j] = v.z;
-      sm[(4 * c + 3) * T + j] = v.w;
-    }
-  } else if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     fence_proxy_async_smem();
     bulk_load(sm, c0, N * 4, &gbar);
   }
   tm_wait_st();
-  if (!GG) mbar_wait(&gbar, 1);
+  mbar_wait(&gbar, 1);
 #pragma unroll
   for (int h = 0; h < 16 / GS; ++h) {
     uint32_t A[GS], B[GS];
@@ -293,13 +192,12 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
     for (int c = h * GS / 4; c < (h + 1) * GS / 4; ++c) {
       const uint4 pm = __ldg(pp + c);
       const int k = 4 * c - GS * h;
-      A[k] = add_mod(A[k], sm[src_of(pm.x)], q);
-      A[k + 1] = add_mod(A[k + 1], sm[src_of(pm.y)], q);
-      A[k + 2] = add_mod(A[k + 2], sm[src_of(pm.z)], q);
-      A[k + 3] = add_mod(A[k + 3], sm[src_of(pm.w)], q);
+      A[k] = add_mod(A[k], sm[pm.x], q);
+      A[k + 1] = add_mod(A[k + 1], sm[pm.y], q);
+      A[k + 2] = add_mod(A[k + 2], sm[pm.z], q);
+      A[k + 3] = add_mod(A[k + 3], sm[pm.w], q);
       if (fold) {
-        const uint4 u = GG ? __ldg(reinterpret_cast<const uint4*>(c0 + x0) + c)
-                           : *reinterpret_cast<const uint4*>(sm + x0 + 4 * c);
+        const uint4 u = *reinterpret_cast<const uint4*>(sm + x0 + 4 * c);
         const uint4 v = *reinterpret_cast<const uint4*>(c1 + x0 + 4 * c);
         A[k] = add_mod(A[k], u.x, q);
         A[k + 1] = add_mod(A[k + 1], u.y, q);
@@ -312,20 +210,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
       }
       *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly0 * N + x0 + 4 * c) = make_uint4(A[k], A[k + 1], A[k + 2], A[k + 3]);
       *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly1 * N + x0 + 4 * c) = make_uint4(B[k], B[k + 1], B[k + 2], B[k + 3]);
-      if constexpr (NEXT) *reinterpret_cast<uint4*>(sm + N + x0 + 4 * c) = make_uint4(B[k], B[k + 1], B[k + 2], B[k + 3]);
     }
-  }
-  if constexpr (NEXT) {
-    // digit_i of the next rotation: INTT_i(sigma'(c1'_i)) (context.cpp:445-470)
-    __syncthreads();
-    uint32_t pm[16];
-    load16_ro(perm_next + x0, pm);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) e[r] = sm[N + pm[r]];
-    NT::inv(e, sm, g.inv + (size_t)gp * N, g.itwc + (size_t)gp * g.twc_stride, q, pr.last, pr.ninv);
-    uint32_t* d = dig_next + ((uint64_t)pair * g.P + gp) * N;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) d[NT::posA(j, r)] = e[r];
   }
   tm_fence_before();
   __syncthreads();
@@ -334,4 +219,3 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, MINB) k_rot_keyswitch_t(Geo g, c
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols) : "memory");
   }
 }
-

@@ -313,11 +313,13 @@ def test_baseline_bit_exact_and_rng_state(n):
     assert nxt.shape[-1] == p.n
 
 
-def test_baseline_gemv_variants_bit_exact(monkeypatch):
-    """baseline_matmul's feature sums (matmul.cpp:453-459) over 600 features
-    (three batches, a ragged last one) with weights of both signs, so the
-    branch-0 residues reach ~2^30: the Shoup GEMV (HEI_BL_ACCUM_W=0), the
-    exact-product GEMV (default) and its 3-slice split give the oracle's
+def test_baseline_linear_sums_bit_exact(monkeypatch):
+    """baseline_matmul (matmul.cpp:273-344) computed by linearity (exact
+    coefficient-domain sums of every encryption's noise and encoded column,
+    three transforms per output): weights of both signs so branch-0 residues
+    reach ~2^30 (N = 8192, 600 features); a tiny ring with two row blocks and
+    1,300 features (three feature batches, the last ragged); and the
+    sequential mt19937_64 replay (HEI_MT_JUMP=0) -- all equal to the oracle's
     blocks bit for bit."""
     from paper_2204_05496_b200 import Prng, baseline_matmul
 
@@ -328,14 +330,22 @@ def test_baseline_gemv_variants_bit_exact(monkeypatch):
     w = rng.integers(-(1 << 14), 1 << 14, size=(f, cols), dtype=np.int64)
     b = rng.integers(-100, 101, size=cols)
     want, _ = o.baseline_matmul(x, w, b)
-    for env in ({"HEI_BL_ACCUM_W": "0"}, {"HEI_BL_ACCUM_W": "1", "HEI_BL_SPLIT": "1"},
-                {"HEI_BL_ACCUM_W": "1", "HEI_BL_SPLIT": "3"}):
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
+    for jump in ("1", "0"):
+        monkeypatch.setenv("HEI_MT_JUMP", jump)
         s = gpu_server_from(o, with_pk=True)
         got, _ = baseline_matmul(s, x, w, b, Prng(16), Prng(17))
-        assert np.array_equal(got, want), env
+        assert np.array_equal(got, want), jump
     assert np.array_equal(o.unpack_baseline(want, R, cols), oracle_matmul(x, w, b))
+    monkeypatch.setenv("HEI_MT_JUMP", "1")
+    p, R, f, cols = tiny_params(32), 40, 1300, 3
+    o = Oracle(p, key_seed=17, enc_seed=18)
+    x = random_mat(rng, R, f, 1)
+    w = random_mat(rng, f, cols, 3)
+    b = np.array([4, -2, 0], np.int64)
+    want, _ = o.baseline_matmul(x, w, b)
+    got, _ = baseline_matmul(gpu_server_from(o, with_pk=True), x, w, b, Prng(18), Prng(19))
+    assert np.array_equal(got, want)
+    assert np.array_equal(o.unpack_baseline(got, R, cols), oracle_matmul(x, w, b))
 
 
 def test_baseline_equals_fast_algorithm(tiny32):
@@ -894,62 +904,20 @@ def test_stream_concurrent_push_from_threads(tiny32):
     assert np.array_equal(st.finish(), want)
 
 
-def test_full_batch_key_switch_variants_bit_exact(prod, monkeypatch):
-    """sum_all_slots (backend.cpp:63-73) over 64 ciphertexts: 640 (pair, prime)
-    blocks take the full-batch key switch (not the fused latency kernels).
-    The TMEM-accumulator kernel at 3 and 2 CTAs/SM and the shared-memory
-    kernel give identical ciphertexts, equal to the oracle's; so does the TMEM
-    kernel that also produces the next rotation's digits (HEI_FUSE_BIG=1), and
-    the variants with TMA digit prefetch (5), two exchange buffers (6) and
-    key loads hoisted across the TMEM waits (7, 8), prime-major block
-    order (4p), keys read past L1 (9, 9p), and
-    L2 bulk prefetch of the next digit (10), and the 256-thread half-ring
-    key switch and 2-CTA-cluster digit INTT (4h, ks_half.cuh), and the digit
-    INTT staging c1 in its exchange buffer (4d) or gathering it by source
-    group (4g)."""
+@pytest.mark.parametrize("cts_n", [1, 20, 40, 64])
+def test_fold_paths_bit_exact(prod, cts_n):
+    """sum_all_slots (backend.cpp:63-73) at the launch sizes that select each
+    N = 8192 fold path: 1 ciphertext (10 (pair, prime) blocks: the 2-group
+    latency kernel with the next digit fused), 20 (200 blocks: shared-memory
+    accumulators, fused), 40 (400 blocks: shared-memory, parameter-space
+    twiddles, fused) and 64 (640 blocks: digit INTT kernel + TMEM-accumulator
+    key switch). Every output equals the oracle's."""
     o, _ = prod
-    rng = np.random.default_rng(64)
-    x = rng.integers(-9, 9, size=(64, o.n), dtype=np.int64)
-    cts = o.encode_inputs(x)[:, 0, :]
-    got = {}
-    for v in ("4", "3", "2", "0", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10", "4h", "4d", "4g", "11"):
-        monkeypatch.setenv("HEI_KS_TMEM", v.rstrip("fphdg"))
-        monkeypatch.setenv("HEI_DIG_TMA", {"d": "2", "g": "3"}.get(v[-1], "1"))
-        monkeypatch.setenv("HEI_HALF13", "1" if v.endswith("h") else "0")
-        monkeypatch.setenv("HEI_FUSE_BIG", "1" if v.endswith("f") else "0")
-        monkeypatch.setenv("HEI_PRIME_MAJOR", "1" if v.endswith("p") else "0")
-        got[v] = gpu_server_from(o).sum_all_slots(cts)
-    for v in ("4", "3", "2", "4f", "5", "6", "7", "8", "4p", "9", "9p", "10", "4h", "4d", "4g", "11"):
-        assert np.array_equal(got[v], got["0"]), v
-    for r in (0, 37, 63):
-        assert np.array_equal(got["3"][r], o.sum_all_slots(cts[r])), r
-
-
-@pytest.mark.parametrize("n", [8192, 16384])
-def test_ntt32_bit_exact_all_primes(n, monkeypatch):
-    """The 32-residue-per-thread transforms (ntt32.cuh, HEI_NTT32) equal the
-    oracle's NTT/INTT (ring/poly.cpp:36-50) on every prime."""
-    monkeypatch.setenv("HEI_NTT32", "1")
-    test_ntt_bit_exact_all_primes(n)
-
-
-def test_ntt32_fold_bit_exact(monkeypatch):
-    """Folds on the 32-residue transforms: every N = 16384 fold (C5's ring)
-    and, with HEI_NTT32=2, N = 8192 full batches (digit INTT + TMEM key
-    switch) give the oracle's ciphertexts."""
-    from paper_2204_05496_b200 import EncodedWeights, matmul
-
-    monkeypatch.setenv("HEI_NTT32", "2")
-    test_n16384_c5_shape_bit_exact()
-    o = Oracle(production_params(8192), key_seed=1, enc_seed=2)
-    rng = np.random.default_rng(65)
-    x = rng.integers(-9, 9, size=(64, o.n), dtype=np.int64)
+    rng = np.random.default_rng(64 + cts_n)
+    x = rng.integers(-9, 9, size=(cts_n, o.n), dtype=np.int64)
     cts = o.encode_inputs(x)[:, 0, :]
     got = gpu_server_from(o).sum_all_slots(cts)
-    monkeypatch.setenv("HEI_NTT32", "0")
-    ref = gpu_server_from(o).sum_all_slots(cts)
-    assert np.array_equal(got, ref)
-    for r in (0, 63):
+    for r in sorted({0, cts_n // 2, cts_n - 1}):
         assert np.array_equal(got[r], o.sum_all_slots(cts[r])), r
 
 
@@ -1000,11 +968,10 @@ def test_chunk_products_row_kernel(prod, monkeypatch):
     assert np.array_equal(got["1"], want)
 
 
-def test_split_key_switch_latency_path(prod, monkeypatch):
-    """Single-individual folds with the key switch split over digits
-    (HEI_SPLIT=2: one block per (pair, prime, digit l != i), the l == i term
-    and the sums in the reduce kernel) match the default latency kernel and
-    the oracle (production C1 shape)."""
+def test_latency_path_graph_replay(prod, monkeypatch):
+    """Single-individual folds replay their launches as one CUDA graph;
+    eager launches (HEI_NO_GRAPHS=1) give the same packed ciphertext, equal
+    to the oracle's (production C1 shape)."""
     from paper_2204_05496_b200 import EncodedWeights, matmul
 
     o, _ = prod
@@ -1012,33 +979,28 @@ def test_split_key_switch_latency_path(prod, monkeypatch):
     inputs = o.encode_inputs(x)
     wp = o.encode_weights(w)
     got = {}
-    for v in ("2", "0"):
-        monkeypatch.setenv("HEI_SPLIT", v)
+    for v in ("1", "0"):
+        monkeypatch.setenv("HEI_NO_GRAPHS", v)
         s = gpu_server_from(o)
-        got[v], _ = matmul(s, inputs, EncodedWeights.from_prepared(s, wp, 1000), b)
-    assert np.array_equal(got["2"], got["0"])
+        ew = EncodedWeights.from_prepared(s, wp, 1000)
+        got[v], _ = matmul(s, inputs, ew, b)
+        again, _ = matmul(s, inputs, ew, b)  # a cached graph replays
+        assert np.array_equal(again, got[v])
+    assert np.array_equal(got["1"], got["0"])
     want, _ = o.fast_matmul(inputs, 1000, wp, b)
-    assert np.array_equal(got["2"], want)
+    assert np.array_equal(got["0"], want)
 
 
-def test_n16384_full_batch_tmem_key_switch(monkeypatch):
-    """C5's ring at full-batch launch sizes (60 ciphertexts = 600 blocks, not
-    fused): the half-ring key switch (two 512-thread blocks per (pair, prime),
-    ks_half.cuh) with the 2-CTA-cluster digit INTT or the 1024-thread one,
-    the TMEM-accumulator kernel (1024 threads, 256 TMEM
-    columns) and the shared-memory kernel all equal the oracle."""
+@pytest.mark.parametrize("cts_n", [20, 60])
+def test_n16384_fold_paths(cts_n):
+    """C5's ring: 60 ciphertexts (600 (pair, prime) blocks) take the
+    half-ring key switch (two 512-thread TMEM blocks per (pair, prime),
+    ks_half.cuh) after the 2-CTA-cluster digit INTT; 20 (200 blocks) the
+    shared-memory kernel with the next digit fused. Both equal the oracle."""
     o = Oracle(production_params(16384), key_seed=5, enc_seed=6)
-    rng = np.random.default_rng(60)
-    x = rng.integers(-9, 9, size=(60, o.n), dtype=np.int64)
+    rng = np.random.default_rng(60 + cts_n)
+    x = rng.integers(-9, 9, size=(cts_n, o.n), dtype=np.int64)
     cts = o.encode_inputs(x)[:, 0, :]
-    got = {}
-    for v, env in (("half", "211"), ("half1", "111"), ("half_st", "212"), ("half_ks", "210"), ("1", "010"),
-                   ("0", "000")):
-        monkeypatch.setenv("HEI_KS14_HALF", env[0])
-        monkeypatch.setenv("HEI_KS14_TMEM", env[1])
-        monkeypatch.setenv("HEI_DIG14_HALF", env[2])
-        got[v] = gpu_server_from(o).sum_all_slots(cts)
-    for v in ("1", "half", "half1", "half_st", "half_ks"):
-        assert np.array_equal(got[v], got["0"]), v
-    for r in (0, 59):
-        assert np.array_equal(got["half"][r], o.sum_all_slots(cts[r])), r
+    got = gpu_server_from(o).sum_all_slots(cts)
+    for r in (0, cts_n - 1):
+        assert np.array_equal(got[r], o.sum_all_slots(cts[r])), r
