@@ -904,21 +904,26 @@ def test_stream_concurrent_push_from_threads(tiny32):
     assert np.array_equal(st.finish(), want)
 
 
-@pytest.mark.parametrize("cts_n", [1, 20, 40, 64])
-def test_fold_paths_bit_exact(prod, cts_n):
+@pytest.mark.parametrize("cts_n,dataflow", [(1, "0"), (1, "1"), (3, "1"), (20, "0"), (20, "1"), (40, "0"), (64, "0")])
+def test_fold_paths_bit_exact(prod, cts_n, dataflow, monkeypatch):
     """sum_all_slots (backend.cpp:63-73) at the launch sizes that select each
-    N = 8192 fold path: 1 ciphertext (10 (pair, prime) blocks: the 2-group
-    latency kernel with the next digit fused), 20 (200 blocks: shared-memory
-    accumulators, fused), 40 (400 blocks: shared-memory, parameter-space
-    twiddles, fused) and 64 (640 blocks: digit INTT kernel + TMEM-accumulator
-    key switch). Every output equals the oracle's."""
+    N = 8192 fold path. Below 296 (pair, prime) blocks the per-rotation
+    kernels (1 ciphertext: the 2-group latency kernel, 20: shared-memory
+    accumulators, both with the next digit fused), or with HEI_DATAFLOW=1 the
+    persistent dataflow kernel (fold_dataflow.cuh) for the whole fold. 40 ciphertexts (400 blocks): shared-memory kernel with
+    parameter-space twiddles, fused; 64 (640 blocks): digit INTT kernel +
+    TMEM-accumulator key switch. Every output equals the oracle's."""
+    monkeypatch.setenv("HEI_DATAFLOW", dataflow)
     o, _ = prod
     rng = np.random.default_rng(64 + cts_n)
     x = rng.integers(-9, 9, size=(cts_n, o.n), dtype=np.int64)
     cts = o.encode_inputs(x)[:, 0, :]
-    got = gpu_server_from(o).sum_all_slots(cts)
+    s = gpu_server_from(o)
+    got = s.sum_all_slots(cts)
     for r in sorted({0, cts_n // 2, cts_n - 1}):
         assert np.array_equal(got[r], o.sum_all_slots(cts[r])), r
+    again = s.sum_all_slots(cts)  # pooled buffers and counters are reused
+    assert np.array_equal(again, got)
 
 
 def test_mask_table_matches_per_pair_masks(prod, monkeypatch):
