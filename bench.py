@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--rows", type=int, default=0, help="override individuals per rank")
     ap.add_argument("--batch-pairs", type=int, default=0)
+    ap.add_argument("--shard", default="rows", choices=["rows", "features"],
+                    help="N > 1: shard individuals (weak scaling) or feature blocks (strong scaling, C5's second mode)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-wire", dest="wire", action="store_false", help="skip the HECT wire-path e2e timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -392,17 +394,19 @@ def run_ours(args, world, rank, local):
     ctw = 2 * P * n
     # seeded workload from util::Prng(7): one X of world*R rows
     # (rank r holds rows [rR, (r+1)R)), then the shared model W, bias
-    rows_all = world * R
-    x, w, b = workload(rows_all, f, cols, pf, ws, row_lo=rank * R, row_hi=(rank + 1) * R)
+    feat = args.shard == "features" and world > 1
+    rows_all = R if feat else world * R
+    x, w, b = workload(rows_all, f, cols, pf, ws, row_lo=0 if feat else rank * R, row_hi=R if feat else (rank + 1) * R)
     ew = encode_weights(srv, w)
     # device-resident inputs: the client's real encryptions of x
     # (encode_inputs, matmul.cpp:59-81; Prng seeds 2, 3 as client_backend(keys, 2))
     d_in = torch.empty((R * kc, ctw), dtype=torch.int32, device=dev)
     stream = torch.cuda.Stream(device=dev)
+    seed_r = 0 if feat else rank  # feature sharding: every rank encrypts the same rows, then keeps its block
     for _ in range(2):  # first call also builds the cached mt19937_64 jump polynomial
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        encode_inputs_device(srv, x, Prng(2 + 2 * rank), Prng(3 + 2 * rank), d_in.data_ptr(), stream.cuda_stream)
+        encode_inputs_device(srv, x, Prng(2 + 2 * seed_r), Prng(3 + 2 * seed_r), d_in.data_ptr(), stream.cuda_stream)
         enc_ms = (time.perf_counter() - t0) * 1000.0
     C_ = (R * cols + n - 1) // n
     d_out = torch.empty((C_, ctw), dtype=torch.int32, device=dev)
@@ -412,58 +416,78 @@ def run_ours(args, world, rank, local):
     if world == 1:
         def step():
             matmul_device(srv, d_in.data_ptr(), R, ew, b, d_out.data_ptr(), stream.cuda_stream)
-    else:
+    elif args.shard == "rows":
         # individual sharding: rank r holds rows [r*R, (r+1)*R) of a world*R
-        # batch; one exchange of the packed partials, then the mod-q
-        # reduction + bias add.
-        from paper_2204_05496_b200.sharding import finish_packed_device, matmul_partial_device, packed_count
+        # batch. Each rank's packed partial is reduced mod q to u32 and the
+        # partials are all-gathered with NCCL on the compute stream; rank 0
+        # sums them mod q and adds the bias (no host barrier in the step).
+        from paper_2204_05496_b200.sharding import (exchange_partials, finish_parts_device, matmul_partial_device,
+                                                    packed_count, reduce_packed_device)
 
         total_rows = world * R
         Ct = packed_count(total_rows, cols, n)
         d_out = torch.empty((Ct, ctw), dtype=torch.int32, device=dev)
-        exchange = os.environ.get("HEI_EXCHANGE", "p2p")
+        exchange = "nccl all-gather of u32 partials" if os.environ.get("HEI_DIST_BACKEND", "nccl") == "nccl" else "gloo"
         acc = torch.zeros((Ct, ctw), dtype=torch.int64, device=dev)
-        gather = None
-        if exchange == "p2p":
-            # each rank writes its packed accumulator into its slot of rank
-            # 0's receive buffer through a CUDA IPC mapping (an NVLink peer
-            # write); rank 0 sums the slots and finishes — no collective
-            from paper_2204_05496_b200.sharding import PeerGather
+        part = torch.empty((Ct, ctw), dtype=torch.int32, device=dev)
 
-            ok = 1
-            try:
-                gather = PeerGather(Ct * ctw * 8, local)
-            except Exception as e:  # no peer access on this rank
-                print(f"[bench] rank {rank}: p2p exchange unavailable ({e})", file=sys.stderr)
-                ok = 0
-            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
-            torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)  # every rank agrees
-            if int(flag.item()) == 0:
-                exchange = "nccl"
-        if exchange == "p2p":
-            def step():
+        def step():
+            with torch.cuda.stream(stream):
+                acc.zero_()
+            matmul_partial_device(srv, ew, d_in.data_ptr(), R, rank * R, total_rows, acc.data_ptr(), stream.cuda_stream)
+            reduce_packed_device(srv, acc.data_ptr(), Ct, part.data_ptr(), stream.cuda_stream)
+            with torch.cuda.stream(stream):
+                gathered = exchange_partials(part)
+            if rank == 0:
+                finish_parts_device(srv, ew, gathered.data_ptr(), world, b, total_rows, d_out.data_ptr(),
+                                    stream.cuda_stream)
+    else:
+        # feature-block sharding (C5's second mode): every rank
+        # holds chunk block shard_chunks(kc) of all rows_all rows; per row
+        # batch the chunk-product partials are reduce-scattered by rows (exact
+        # integer sums), each rank folds and masks its row block, and the
+        # packed partials are exchanged as in row sharding. Strong scaling
+        # over a fixed batch of R rows.
+        from paper_2204_05496_b200.sharding import (chunk_dot_partial_device, exchange_partials, finish_parts_device,
+                                                    fold_pack_device, packed_count, reduce_packed_device,
+                                                    reduce_scatter_dots, shard_chunks, shard_rows)
+
+        klo, kn = shard_chunks(kc, world, rank)
+        if kn == 0:
+            raise SystemExit(f"--shard features needs world <= chunks per row ({kc})")
+        total_rows = R
+        torch.cuda.synchronize()
+        d_in = d_in.view(R, kc, ctw)[:, klo:klo + kn].contiguous().view(R * kn, ctw)  # this rank's feature block only
+        Ct = packed_count(total_rows, cols, n)
+        d_out = torch.empty((Ct, ctw), dtype=torch.int32, device=dev)
+        exchange = ("nccl reduce-scatter of chunk-product partials + all-gather of u32 packed partials"
+                    if os.environ.get("HEI_DIST_BACKEND", "nccl") == "nccl" else "gloo")
+        acc = torch.zeros((Ct, ctw), dtype=torch.int64, device=dev)
+        part = torch.empty((Ct, ctw), dtype=torch.int32, device=dev)
+        RB = max(world, min(R, 4 * world))  # rows per exchange batch (bounds the u64 dot buffer)
+        dot = torch.empty((RB * cols, ctw), dtype=torch.int64, device=dev)
+
+        def step():
+            with torch.cuda.stream(stream):
+                acc.zero_()
+            for r0 in range(0, R, RB):
+                nr = min(RB, R - r0)
                 with torch.cuda.stream(stream):
-                    acc.zero_()
-                matmul_partial_device(srv, ew, d_in.data_ptr(), R, rank * R, total_rows, acc.data_ptr(),
-                                      stream.cuda_stream)
-                stream.synchronize()
-                torch.distributed.barrier()  # the owner's previous reduce/finish is done with the slots
-                gather.push(acc.data_ptr(), stream.cuda_stream)
-                stream.synchronize()
-                torch.distributed.barrier()  # every slot written
-                if rank == 0:
-                    gather.reduce(stream.cuda_stream)
-                    finish_packed_device(srv, ew, gather.total_ptr, b, total_rows, d_out.data_ptr(),
+                    dot[: nr * cols].zero_()
+                chunk_dot_partial_device(srv, ew, d_in[r0 * kn:(r0 + nr) * kn].data_ptr(), nr, klo, kn, dot.data_ptr(),
                                          stream.cuda_stream)
-        else:
-            def step():
                 with torch.cuda.stream(stream):
-                    acc.zero_()
-                matmul_partial_device(srv, ew, d_in.data_ptr(), R, rank * R, total_rows, acc.data_ptr(),
-                                      stream.cuda_stream)
-                with torch.cuda.stream(stream):
-                    torch.distributed.all_reduce(acc)
-                finish_packed_device(srv, ew, acc.data_ptr(), b, total_rows, d_out.data_ptr(), stream.cuda_stream)
+                    mine = reduce_scatter_dots(dot[: nr * cols], nr)
+                lo, cnt = shard_rows(nr, world, rank)
+                if cnt:
+                    fold_pack_device(srv, ew, mine.data_ptr(), r0 + lo, cnt, total_rows, acc.data_ptr(),
+                                     stream.cuda_stream)
+            reduce_packed_device(srv, acc.data_ptr(), Ct, part.data_ptr(), stream.cuda_stream)
+            with torch.cuda.stream(stream):
+                gathered = exchange_partials(part)
+            if rank == 0:
+                finish_parts_device(srv, ew, gathered.data_ptr(), world, b, total_rows, d_out.data_ptr(),
+                                    stream.cuda_stream)
 
     for _ in range(args.warmup):
         with torch.cuda.stream(stream):
@@ -491,7 +515,7 @@ def run_ours(args, world, rank, local):
         t = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * R / (ms / 1000.0)
+    value = rows_all / (ms / 1000.0)
 
     # bit-exactness of the timed path against the reference (single rank:
     # the golden digests cover exactly this workload, keys and encryption)
@@ -508,7 +532,7 @@ def run_ours(args, world, rank, local):
 
     # e2e: host u64 (pinned) inputs through the C ABI, copies inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not feat:
         h_in = torch.empty((R, kc, ctw), dtype=torch.int64, pin_memory=True)
         h_in.copy_(d_in.view(R, kc, ctw).to(torch.int64).cpu())
         h_np = h_in.numpy().view(np.uint64)
@@ -538,8 +562,10 @@ def run_ours(args, world, rank, local):
     peaks, peak_src = _peaks()
     hbm = float(peaks.get("hbm_gbs", 7672.0))
     bfly_peak = native.butterfly_peak(local) if rank == 0 else None
+    if feat:
+        d_in = None  # the sliced block is not a full-row input for the single-GPU legs below
     L0, L1 = len(q0), len(q1)
-    if rank == 0:
+    if rank == 0 and not feat:
         native.kernel_timing(srv.handle, True)
         # the rank's own fold work only: no collective, so rank 0 can time it alone
         matmul_device(srv, d_in.data_ptr(), R, ew, b, d_one.data_ptr(), stream.cuda_stream)
@@ -642,7 +668,7 @@ def run_ours(args, world, rank, local):
         t0 = time.perf_counter()
         got = srv.unpack_results(packed_dev, rows_all, cols)
         dec_ms = (time.perf_counter() - t0) * 1000.0
-        x_all = x if world == 1 else workload(rows_all, f, cols, pf, ws)[0]
+        x_all = x if (world == 1 or feat) else workload(rows_all, f, cols, pf, ws)[0]
         want = np.rint(x_all.astype(np.float64) @ w.astype(np.float64)).astype(np.int64) + b  # exact: |sums| < 2^53
         check = {"decrypted_equals_integer_product": bool(np.array_equal(got, want)), "client_decrypt_ms": dec_ms,
                  "keygen_ms": keygen_ms, "client_encrypt_ms": enc_ms}
@@ -667,14 +693,15 @@ def run_ours(args, world, rank, local):
     line = {
         "metric": "encrypted LR inferences/sec at 40k features",
         "value": value, "unit": "inferences/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if feat else "weak",
+        "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {R} individuals/rank x {f} features x {cols} classes, N={n}, "
                                f"twin t=({T0},{T1 if n < 16384 else T1_16K}), L=({len(q0)},{len(q1)})",
                    "inputs": "seeded util::Prng(7) workload (SURVEY 8d), real encryptions (device keygen from "
                              "Prng(1), client encryption with Prng(2),(3)), resident in HBM; inputs > L2 (no flush "
                              "needed)",
-                   "parallelism": f"dp{world} (individual sharding)" + (
+                   "parallelism": f"dp{world} ({'feature-block' if feat else 'individual'} sharding)" + (
                        f", exchange={exchange}" if world > 1 else "")},
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -168,15 +168,30 @@ int hei_gpu_matmul_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint
 /* Sharded execution (one process per GPU). Each rank adds the
  * masked class results of its rows [row_offset, row_offset + rows) of a
  * total_rows batch into d_acc, an unreduced u64 packed accumulator
- * [C][twin ct] (C = ceil(total_rows * cols / N), zeroed by the caller).
- * Partial accumulators of all ranks sum exactly (no wrap below 2^63), so the
- * exchange is one integer all-reduce; finish_packed then reduces mod q and
- * adds the bias once (MatmulStream::finish, matmul.cpp:342-374). */
+ * [C][twin ct] (C = ceil(total_rows * cols / N)): the call ACCUMULATES into
+ * the caller's buffer, which must be zeroed before the first call (it is not
+ * cleared here). Partial accumulators of all ranks sum exactly (no wrap
+ * below 2^63), so the exchange is one integer reduction; finish_packed then
+ * reduces mod q and adds the bias once (MatmulStream::finish,
+ * matmul.cpp:200-232). */
 int hei_gpu_matmul_partial_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint32_t* d_inputs,
                                   uint64_t rows, uint64_t row_offset, uint64_t total_rows, uint64_t* d_acc,
                                   void* stream);
 int hei_gpu_finish_packed_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint64_t* d_acc,
                                  const int64_t* bias, uint64_t total_rows, uint32_t* d_out, void* stream);
+
+/* Stream-ordered exchange (no host synchronisation): reduce_packed turns a
+ * rank's u64 accumulator of `count` packed twin ciphertexts into u32
+ * residues mod q (its partial: half the bytes, exact); after the ranks'
+ * partials are gathered (an NCCL all-gather of `count` x twin-ct u32 words
+ * per rank), finish_parts sums the `parts` partials [parts][count][twin ct]
+ * mod q and adds the bias plaintext once (MatmulStream::finish,
+ * matmul.cpp:200-232). Both are enqueued on `stream` and return without
+ * waiting. */
+int hei_gpu_reduce_packed_device(hei_gpu_ctx* ctx, const uint64_t* d_acc, uint64_t count, uint32_t* d_out,
+                                 void* stream);
+int hei_gpu_finish_parts_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint32_t* d_parts, uint32_t parts,
+                                const int64_t* bias, uint64_t total_rows, uint32_t* d_out, void* stream);
 
 /* Peer-memory exchange: the owner rank exports a receive buffer
  * (one slot per rank) as a 64-byte CUDA IPC handle; every rank maps it and

@@ -3193,6 +3193,68 @@ int hei_gpu_sum_slots(void* d, uint64_t words, uint32_t count, void* stream) {
   });
 }
 
+// A rank's packed u64 accumulator reduced mod q into u32 residues: the
+// partial it exchanges (half the bytes of the sums; exact, mod-q addition is
+// order-free).
+__global__ void k_reduce_packed(Geo g, const unsigned long long* __restrict__ acc, uint64_t words,
+                                uint32_t* __restrict__ out) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < words; x += (uint64_t)gridDim.x * blockDim.x) {
+    const PrimeInfo& pr = g.pr[poly_prime(g, (uint32_t)((x % g.ct_words) / g.n))];
+    const unsigned long long v = acc[x];
+    const unsigned long long r = v - __umul64hi(v, pr.mu) * pr.q;  // Barrett: at most one q too large
+    out[x] = (uint32_t)(r >= pr.q ? r - pr.q : r);
+  }
+}
+// acc[x] = sum over parts of parts[k][x] (u64, exact: < parts * 2^31)
+__global__ void k_sum_parts(const uint32_t* __restrict__ parts, uint64_t words, uint32_t count,
+                            unsigned long long* __restrict__ acc) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < words; x += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long a = 0;
+    for (uint32_t k = 0; k < count; ++k) a += parts[(uint64_t)k * words + x];
+    acc[x] = a;
+  }
+}
+
+int hei_gpu_reduce_packed_device(hei_gpu_ctx* c, const uint64_t* d_acc, uint64_t count, uint32_t* d_out,
+                                 void* stream) {
+  return guarded([&] {
+    set_device(c);
+    if (!d_acc || !d_out || count == 0) raise(HEI_PARAM_ERROR, "reduce_packed: empty argument");
+    const uint64_t words = count * c->ct_words();
+    k_reduce_packed<<<grid_for(words, 256), 256, 0, (cudaStream_t)stream>>>(
+        c->geo, reinterpret_cast<const unsigned long long*>(d_acc), words, d_out);
+    LAUNCHED();
+  });
+}
+
+int hei_gpu_finish_parts_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint32_t* d_parts, uint32_t parts,
+                                const int64_t* bias, uint64_t total_rows, uint32_t* d_out, void* stream) {
+  return guarded([&] {
+    set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!w || !d_parts || !d_out || parts == 0 || total_rows == 0) raise(HEI_PARAM_ERROR, "finish_parts: empty argument");
+    check_bias_range(c, bias, w->cols);
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    hei_gpu_stream tmp{};
+    tmp.ctx = c;
+    tmp.w = w;
+    tmp.bias.assign(bias, bias + w->cols);
+    tmp.rows = total_rows;
+    tmp.C = (total_rows * w->cols + c->n - 1) / c->n;
+    const uint64_t words = tmp.C * c->ct_words();
+    tmp.d_acc = pool_get(c->pool_acc, c->pool_acc_bytes, words * 8);
+    tmp.owns_acc = false;
+    k_sum_parts<<<grid_for(words, 256), 256, 0, st>>>(d_parts, words, parts, tmp.d_acc);
+    LAUNCHED();
+    // the bias is staged synchronously (pageable host memory), then the
+    // finish is enqueued on `st` and the call returns without waiting
+    int64_t* d_bias = pool_get(c->pool_bias, c->pool_bias_bytes, tmp.bias.size() * 8);
+    CU(cudaMemcpy(d_bias, tmp.bias.data(), tmp.bias.size() * 8, cudaMemcpyHostToDevice));
+    tmp.d_bias = d_bias;
+    finish_to(&tmp, d_out, st);
+  });
+}
+
 int hei_gpu_ipc_handle(const void* d_ptr, uint8_t* handle64) {
   return guarded([&] {
     if (!d_ptr || !handle64) raise(HEI_PARAM_ERROR, "ipc: null argument");

@@ -107,6 +107,7 @@ EXPORTED = [
     "hei_gpu_debug_rejection_plan", "hei_gpu_chunk_dot_partial_device", "hei_gpu_fold_pack_device",
     "hei_default_q_primes", "hei_gpu_ipc_handle", "hei_gpu_ipc_open", "hei_gpu_ipc_close",
     "hei_gpu_buffer_alloc", "hei_gpu_buffer_zero", "hei_gpu_buffer_free", "hei_gpu_copy_async", "hei_gpu_sum_slots",
+    "hei_gpu_reduce_packed_device", "hei_gpu_finish_parts_device",
 ]
 
 _lib = None

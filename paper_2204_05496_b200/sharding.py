@@ -4,12 +4,12 @@ Individual (row) sharding is the default:
 
 Every (individual, class) pipeline is independent; rank r takes a
 contiguous row block and accumulates the masked class results of its rows into
-an unreduced u64 packed accumulator. Accumulators of all ranks add exactly
-(each rank contributes < rows * 2^31 per slot), so the only exchange is one
-integer all-reduce of C * 2 * (L0 + L1) * N words (0.65 M words, 5.2 MB at
-C4), followed by the mod-q reduction and a single bias add_plain
-(MatmulStream::finish, matmul.cpp:342-374). Order-free, hence bit-exact for
-any rank count.
+an unreduced u64 packed accumulator, reduces it mod q to u32 residues (its
+partial: C * 2 * (L0 + L1) * N words, 0.65 MB at C4), and the ranks exchange
+the partials with one NCCL all-gather on the compute stream (no host
+barrier); rank 0 sums them mod q and adds the bias once (MatmulStream::finish,
+matmul.cpp:200-232). Mod-q addition is order-free, hence bit-exact for any
+rank count.
 
 Feature-block sharding (C5's second mode): rank r holds only chunks
 shard_chunks(kc, world, r) of every row, computes the chunk products of those
@@ -55,6 +55,44 @@ def finish_packed_device(server, w, d_acc_ptr: int, bias, total_rows: int, d_out
     bias = np.ascontiguousarray(bias, dtype=np.int64)
     check(native.lib().hei_gpu_finish_packed_device(server.handle, w._h, C.c_void_p(d_acc_ptr), i64p(bias),
                                                     C.c_uint64(total_rows), C.c_void_p(d_out_ptr), C.c_void_p(stream_ptr)))
+
+
+def reduce_packed_device(server, d_acc_ptr: int, count: int, d_out_ptr: int, stream_ptr: int = 0) -> None:
+    """A rank's u64 packed accumulator -> u32 residues mod q (its partial for
+    the exchange; stream-ordered, no host wait)."""
+    check(native.lib().hei_gpu_reduce_packed_device(server.handle, C.c_void_p(d_acc_ptr), C.c_uint64(count),
+                                                    C.c_void_p(d_out_ptr), C.c_void_p(stream_ptr)))
+
+
+def finish_parts_device(server, w, d_parts_ptr: int, parts: int, bias, total_rows: int, d_out_ptr: int,
+                        stream_ptr: int = 0) -> None:
+    """Sum `parts` gathered u32 partials mod q and add the bias once
+    (MatmulStream::finish, matmul.cpp:200-232); stream-ordered."""
+    bias = np.ascontiguousarray(bias, dtype=np.int64)
+    check(native.lib().hei_gpu_finish_parts_device(server.handle, w._h, C.c_void_p(d_parts_ptr), C.c_uint32(parts),
+                                                   i64p(bias), C.c_uint64(total_rows), C.c_void_p(d_out_ptr),
+                                                   C.c_void_p(stream_ptr)))
+
+
+def exchange_partials(part, group=None):
+    """All-gather the ranks' u32 partials (torch int32 [count][twin ct] on the
+    device) into [world][count][twin ct] on every rank: one NCCL all-gather
+    on the current stream (gloo on CPU). World 1 returns the input with a
+    leading axis."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return part.unsqueeze(0)
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "gloo":  # host-side exchange (CPU tests, single-GPU plumbing checks)
+        host = part.cpu()
+        outs = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(outs, host, group=group)
+        return torch.stack(outs).to(part.device)
+    out = torch.empty((world,) + tuple(part.shape), dtype=part.dtype, device=part.device)
+    dist.all_gather_into_tensor(out, part, group=group)
+    return out
 
 
 def combine_partials(acc, group=None):
@@ -108,10 +146,11 @@ def reduce_scatter_dots(dot, total_rows: int, group=None):
     padded = torch.zeros((block * world * per_row,) + tuple(dot.shape[1:]), dtype=dot.dtype, device=dot.device)
     padded[: dot.shape[0]] = dot
     out = torch.empty((block * per_row,) + tuple(dot.shape[1:]), dtype=dot.dtype, device=dot.device)
-    if dot.device.type == "cpu" and dist.get_backend(group) == "gloo":
-        # gloo has no reduce_scatter: all-reduce and slice
-        dist.all_reduce(padded, op=dist.ReduceOp.SUM, group=group)
-        out.copy_(padded[rank * block * per_row:(rank + 1) * block * per_row])
+    if dist.get_backend(group) == "gloo":
+        # gloo has no reduce_scatter: all-reduce on the host and slice
+        host = padded.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+        out.copy_(host[rank * block * per_row:(rank + 1) * block * per_row])
     else:
         dist.reduce_scatter_tensor(out, padded, op=dist.ReduceOp.SUM, group=group)
     lo, cnt = shard_rows(total_rows, world, rank)

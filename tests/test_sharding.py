@@ -107,3 +107,40 @@ def test_gloo_feature_block_reduce_scatter_is_exact(tmp_path, total_rows):
             lo, cnt = shard_chunks(kc, world, r)
             seen += list(range(lo, lo + cnt))
         assert seen == list(range(kc))
+
+
+def _ex_worker(rank, world, port, result_path):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_05496_b200.sharding import exchange_partials
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(300 + rank)
+    part = rng.integers(0, 2 ** 31 - 1, size=(2, 5, 16), dtype=np.int64).astype(np.int32)  # u32 residues < 2^31
+    got = exchange_partials(torch.from_numpy(part))
+    np.save(result_path % rank, got.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_exchange_of_reduced_partials(tmp_path, world):
+    """Row sharding's exchange: each rank's packed partial is
+    reduced mod q to u32 and all-gathered; every rank receives every partial in
+    rank order, and summing them mod q equals reducing the sum of the
+    unreduced u64 partials (mod-q addition is order-free)."""
+    path = str(tmp_path / "ex_%d.npy")
+    mp.spawn(_ex_worker, args=(world, _free_port(), path), nprocs=world, join=True)
+    parts = [np.random.default_rng(300 + r).integers(0, 2 ** 31 - 1, size=(2, 5, 16), dtype=np.int64) for r in range(world)]
+    for r in range(world):
+        got = np.load(path % r).astype(np.int64)
+        assert got.shape == (world, 2, 5, 16)
+        for k in range(world):
+            assert np.array_equal(got[k], parts[k])
+    q = np.array([2147352577, 2147205121, 2147074049, 2146959361, 2146713601], dtype=np.uint64)
+    total = sum(p.astype(np.uint64) for p in parts)
+    via_parts = sum(reduce_packed_mod_q(p.astype(np.uint64), q) for p in parts)
+    assert np.array_equal(reduce_packed_mod_q(total, q), reduce_packed_mod_q(via_parts, q))
