@@ -55,7 +55,7 @@ typedef struct {
   uint64_t ciphertexts_out;
 } hei_op_counters;
 
-/* fpcrt::TwinParams (twin.hpp:90-95) + the derived q chains
+/* fpcrt::TwinParams (twin.hpp:20-25) + the derived q chains
  * (bfv::default_q_primes, params.cpp:84-104). */
 typedef struct {
   uint32_t n;
@@ -74,7 +74,7 @@ int hei_default_q_primes(uint32_t n, uint64_t t, uint64_t* out, uint32_t capacit
 const char* hei_gpu_last_error(void);
 const char* hei_gpu_version(void);
 
-/* Context + keys. Replaces TwinContext / server_backend (twin.hpp:119-145).
+/* Context + keys. Replaces TwinContext / server_backend (twin.hpp:49-115).
  * Validates like EncryptionParams::validate (params.cpp:27-66). */
 int hei_gpu_ctx_create(const hei_twin_desc* desc, hei_gpu_ctx** out);
 void hei_gpu_ctx_destroy(hei_gpu_ctx* ctx);
@@ -87,7 +87,7 @@ int hei_gpu_upload_galois_keys(hei_gpu_ctx* ctx, uint32_t branch, uint32_t count
 int hei_gpu_upload_public_key(hei_gpu_ctx* ctx, uint32_t branch, const uint64_t* pk);
 
 /* Weights. hei_gpu_weights_create uploads EncodedWeights values as produced by
- * matmul::encode_weights (matmul.cpp:225-246); hei_gpu_weights_encode runs
+ * matmul::encode_weights (matmul.cpp:83-104); hei_gpu_weights_encode runs
  * encode_weights itself on the device from the scaled f x cols matrix. */
 int hei_gpu_weights_create(hei_gpu_ctx* ctx, const uint64_t* prepared, uint64_t f,
                            uint64_t cols, hei_gpu_weights** out);
@@ -95,7 +95,7 @@ int hei_gpu_weights_encode(hei_gpu_ctx* ctx, const int64_t* w, uint64_t f, uint6
                            hei_gpu_weights** out);
 void hei_gpu_weights_destroy(hei_gpu_weights* w);
 
-/* matmul::matmul (matmul.cpp:381-397). Host buffers; inputs in `form`;
+/* matmul::matmul (matmul.cpp:239-255). Host buffers; inputs in `form`;
  * bias = EncodedBias::scaled [cols]; out = PackedResult cts (eval form). */
 int hei_gpu_matmul(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint64_t* inputs,
                    int form, uint64_t rows, const int64_t* bias, uint64_t* out,
@@ -215,7 +215,7 @@ int hei_gpu_ipc_close(void* d_ptr);
  * mod q, runs sum_all_slots and the mask into the packed accumulator d_acc
  * (as matmul_partial_device does), and finish_packed_device completes it.
  * Bit-exact with the single-GPU result: the chunk sum is reduced before
- * sum_all_slots, as MatmulStream::push_row does (matmul.cpp:318-326). */
+ * sum_all_slots, as MatmulStream::push_row does (matmul.cpp:176-184). */
 int hei_gpu_chunk_dot_partial_device(hei_gpu_ctx* ctx, const hei_gpu_weights* w, const uint32_t* d_inputs,
                                      uint64_t rows, uint64_t chunk_lo, uint64_t chunk_count, uint64_t* d_dot,
                                      void* stream);
@@ -230,7 +230,7 @@ int hei_gpu_stream_push_row(hei_gpu_stream* s, uint64_t row_index, const uint64_
 int hei_gpu_stream_finish(hei_gpu_stream* s, uint64_t* out, hei_op_counters* counters);
 void hei_gpu_stream_destroy(hei_gpu_stream* s);
 
-/* matmul::baseline_matmul (matmul.cpp:415-486). Encrypts every feature column
+/* matmul::baseline_matmul (matmul.cpp:273-344). Encrypts every feature column
  * with the public key; encryption randomness is replayed from one util::Prng
  * per branch, exactly as BfvBackend::encrypt draws it (context.cpp:262-303).
  * out [ceil(rows/N)][cols][twin ct] eval form. */
@@ -244,7 +244,7 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* ctx, const int64_t* x, uint64_t rows, u
                             hei_op_counters* counters);
 
 /* Client-side encryption of inputs: matmul::encode_inputs
- * (matmul.cpp:201-223) — ceil(f/N) slot chunks per row, encode_signed +
+ * (matmul.cpp:59-81) — ceil(f/N) slot chunks per row, encode_signed +
  * encrypt in eval form, randomness replayed from the two branch Prngs exactly
  * as BfvBackend::encrypt draws it. x is rows x f (scaled, row-major);
  * out [row][k][twin ct] u64 (host) or u32 (device variant). */
@@ -254,7 +254,7 @@ int hei_gpu_encode_inputs_device(hei_gpu_ctx* ctx, const int64_t* x, uint64_t ro
                                  hei_gpu_prng* rng0, hei_gpu_prng* rng1, uint32_t* d_out,
                                  void* stream);
 
-/* Closed forms (matmul.cpp:172-199). */
+/* Closed forms (matmul.cpp:30-57). */
 int hei_proposed_counts(uint64_t rows, uint64_t cols, uint64_t f, uint32_t n, hei_op_counters* c);
 int hei_baseline_counts(uint64_t rows, uint64_t cols, uint64_t f, uint32_t n, hei_op_counters* c);
 

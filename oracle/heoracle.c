@@ -277,7 +277,7 @@ static int validate(uint32_t n, uint64_t t, const uint64_t* q, uint32_t L, int s
   return 0;
 }
 
-/* FNV-1a over (n, t, security, q...) (params.cpp:373-387) */
+/* FNV-1a over (n, t, security, q...) (params.cpp:68-82) */
 static uint64_t params_hash(uint32_t n, uint64_t t, int sec, const uint64_t* q, uint32_t L) {
   uint64_t h = 0xcbf29ce484222325ull;
   uint64_t vals[3 + MAXL];
@@ -889,7 +889,7 @@ static int64_t max_centered(uint64_t t0, uint64_t t1) { return (int64_t)(((u128)
 static size_t twin_ct_words(const ho_twin* h) { return 2ull * (h->c[0].L + h->c[1].L) * h->n; }
 static size_t twin_pt_words(const ho_twin* h) { return (size_t)(h->c[0].L + h->c[1].L) * h->n; }
 
-/* encode_signed (twin.cpp:388-404): coeff plaintexts per branch [2][n] */
+/* encode_signed (twin.cpp:95-111): coeff plaintexts per branch [2][n] */
 static int encode_signed(const ho_twin* h, const int64_t* vals, size_t cnt, uint64_t* pt2) {
   int64_t lim = max_centered(h->t[0], h->t[1]);
   uint64_t* slots = malloc((cnt ? cnt : 1) * 8);
@@ -927,7 +927,7 @@ int ho_twin_create(ho_twin** out, uint32_t n, uint64_t t0, uint64_t t1, int sec,
       free(h);
       return rc;
     }
-  /* TwinContext::keygen (twin.cpp:334-341): one rng across both branches */
+  /* TwinContext::keygen (twin.cpp:41-48): one rng across both branches */
   prng rng;
   prng_init(&rng, key_seed);
   for (int b = 0; b < 2; ++b) {
@@ -995,7 +995,7 @@ int ho_twin_export_keys(const ho_twin* h, uint64_t* gk0, uint64_t* gk1, int8_t* 
   return 0;
 }
 
-/* encode_input_row / encode_inputs (matmul.cpp:201-223), client encrypt */
+/* encode_input_row / encode_inputs (matmul.cpp:59-81), client encrypt */
 int ho_encode_inputs(ho_twin* h, const int64_t* x, uint64_t R, uint64_t f, uint64_t* out) {
   if (R == 0 || f == 0) return set_err(ERR_PARAM, "encode_inputs: empty matrix");
   const uint32_t n = h->n;
@@ -1014,7 +1014,7 @@ int ho_encode_inputs(ho_twin* h, const int64_t* x, uint64_t R, uint64_t f, uint6
   return rc;
 }
 
-/* encode_weights (matmul.cpp:225-246): out [cols][k][twin plain] values */
+/* encode_weights (matmul.cpp:83-104): out [cols][k][twin plain] values */
 int ho_encode_weights(ho_twin* h, const int64_t* w, uint64_t f, uint64_t cols, uint64_t* out) {
   if (f == 0 || cols == 0) return set_err(ERR_PARAM, "encode_weights: empty matrix");
   const uint32_t n = h->n;
@@ -1036,7 +1036,7 @@ int ho_encode_weights(ho_twin* h, const int64_t* w, uint64_t f, uint64_t cols, u
   return rc;
 }
 
-/* mask_for_slot (matmul.cpp:288-305): prepared one-hot at `slot` */
+/* mask_for_slot (matmul.cpp:146-163): prepared one-hot at `slot` */
 static int make_mask(const ho_twin* h, uint32_t slot, uint64_t* vals, uint64_t* shoup) {
   int64_t* onehot = calloc(h->n, 8);
   uint64_t* pt = malloc(2ull * h->n * 8);
@@ -1055,7 +1055,7 @@ int ho_mask(ho_twin* h, uint32_t slot, uint64_t* out) {
   return make_mask(h, slot, out, NULL);
 }
 
-/* capacity_check (fixed_point.cpp:242-264) */
+/* capacity_check (fixed_point.cpp:55-77) */
 int ho_capacity_ok(uint64_t f, uint32_t s_x, uint32_t s_w, uint32_t in_bits, uint64_t t0, uint64_t t1) {
   if (f == 0) return 0;
   int log_f = f == 1 ? 0 : 64 - __builtin_clzll(f - 1);
@@ -1079,7 +1079,7 @@ int ho_scale_value(double x, uint32_t e, int64_t* out) {
   return 0;
 }
 
-/* proposed_counts / baseline_counts (matmul.cpp:172-199) */
+/* proposed_counts / baseline_counts (matmul.cpp:30-57) */
 int ho_proposed_counts(uint64_t R, uint64_t cols, uint64_t f, uint32_t n, uint64_t* c) {
   if (!R || !cols || !f) return set_err(ERR_PARAM, "empty shape");
   if (!is_pow2(n)) return set_err(ERR_PARAM, "ring degree must be a power of two");
@@ -1103,7 +1103,7 @@ int ho_baseline_counts(uint64_t R, uint64_t cols, uint64_t f, uint32_t n, uint64
   return 0;
 }
 
-/* ---- fast matmul: MatmulStream (matmul.cpp:256-397) ---- */
+/* ---- fast matmul: MatmulStream (matmul.cpp:114-255) ---- */
 typedef struct {
   ho_twin* h;
   const uint64_t* inputs;
@@ -1209,7 +1209,7 @@ int ho_fast_matmul(ho_twin* h, const uint64_t* inputs, int form, uint64_t R, uin
   free(jobs);
   free(tid);
   free(ws);
-  /* finish (matmul.cpp:342-374): bias pattern per packed ciphertext */
+  /* finish (matmul.cpp:200-232): bias pattern per packed ciphertext */
   int64_t* pattern = malloc(n * 8);
   uint64_t* pt = malloc(2ull * n * 8);
   uint64_t* dm = malloc(n * 8);
@@ -1242,7 +1242,7 @@ int ho_fast_matmul(ho_twin* h, const uint64_t* inputs, int form, uint64_t R, uin
   return rc;
 }
 
-/* ---- baseline (matmul.cpp:415-486) ---- */
+/* ---- baseline (matmul.cpp:273-344) ---- */
 int ho_baseline_matmul(ho_twin* h, const int64_t* x, uint64_t R, uint64_t f, const int64_t* w, uint64_t cols,
                        const int64_t* bias, uint64_t* out, uint64_t* counters) {
   if (R == 0 || f == 0 || cols == 0) return set_err(ERR_PARAM, "baseline: empty input");
@@ -1267,7 +1267,7 @@ int ho_baseline_matmul(ho_twin* h, const int64_t* x, uint64_t R, uint64_t f, con
       encrypt_eval(&h->c[0], &h->k[0], &h->enc[0], pt, ck);
       encrypt_eval(&h->c[1], &h->k[1], &h->enc[1], pt + n, ck + 2ull * h->c[0].L * n);
       for (uint64_t j = 0; j < cols; ++j) {
-        /* prepare_constant_signed (twin.cpp:424-436, context.cpp:120-137) */
+        /* prepare_constant_signed (twin.cpp:131-143, context.cpp:120-137) */
         size_t o = 0;
         for (int b = 0; b < 2; ++b) {
           const ctx* c = &h->c[b];
@@ -1335,8 +1335,8 @@ int ho_baseline_noise(ho_twin* h, uint64_t encryptions, int8_t* out) {
   return 0;
 }
 
-/* decrypt_signed (twin.cpp:446-452 + decode_signed :406-414 + crt_recombine
- * fixed_point.cpp:276-291) */
+/* decrypt_signed (twin.cpp:153-159 + decode_signed :113-121 + crt_recombine
+ * fixed_point.cpp:89-104) */
 int ho_decrypt_signed(ho_twin* h, const uint64_t* ct, int form, int64_t* out, int* budget) {
   const uint32_t n = h->n;
   uint64_t *m = malloc(n * 8), *s0 = malloc(n * 8), *s1 = malloc(n * 8);

@@ -73,9 +73,9 @@ int ho_unpack_baseline(ho_twin* h, const uint64_t* blocks, uint64_t R, uint64_t 
 /* Single ops (branch b ciphertext [2][L_b][N] eval form). */
 int ho_apply_galois(ho_twin* h, int b, uint64_t elt, const uint64_t* in, uint64_t* out);
 int ho_sum_all_slots(ho_twin* h, const uint64_t* in, uint64_t* out);
-/* Slot mask for slot s, prepared values [twin plain] (matmul.cpp:288-305). */
+/* Slot mask for slot s, prepared values [twin plain] (matmul.cpp:146-163). */
 int ho_mask(ho_twin* h, uint32_t slot, uint64_t* out);
-/* Closed forms (matmul.cpp:172-199): counters[5]. */
+/* Closed forms (matmul.cpp:30-57): counters[5]. */
 int ho_proposed_counts(uint64_t R, uint64_t cols, uint64_t f, uint32_t n, uint64_t* c);
 int ho_baseline_counts(uint64_t R, uint64_t cols, uint64_t f, uint32_t n, uint64_t* c);
 /* fixed point (fixed_point.cpp:37-106) */

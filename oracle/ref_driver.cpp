@@ -9,7 +9,7 @@
 //
 // The reference's own `heinfer bench` does not compile (tools/heinfer.cpp:611-612
 // passes a 1-argument lambda to parallel_for), so this driver times
-// hei::matmul::matmul (proj/src/matmul/matmul.cpp:381-397) and
+// hei::matmul::matmul (proj/src/matmul/matmul.cpp:239-255) and
 // hei::matmul::baseline_matmul (:415-486) directly, exactly as the bench's
 // "computation" phase would (tools/heinfer.cpp:596-628).
 //
@@ -242,7 +242,7 @@ int ref_num_galois(void* h) {
   return static_cast<int>(s.keys.gks[0].keys.size());
 }
 
-// encode_inputs with the client backend (matmul.cpp:201-223); optional export.
+// encode_inputs with the client backend (matmul.cpp:59-81); optional export.
 int ref_encode_inputs(void* h, const int64_t* x, uint64_t R, uint64_t f,
                       uint64_t* out) {
   GUARD_BEGIN
@@ -284,7 +284,7 @@ int ref_load_inputs(void* h, const uint64_t* in, uint64_t R, uint64_t f, int for
   GUARD_END
 }
 
-// encode_weights (matmul.cpp:225-246): export the prepared values
+// encode_weights (matmul.cpp:83-104): export the prepared values
 // [j][k][branch][prime][N].
 int ref_encode_weights(void* h, const int64_t* w, uint64_t f, uint64_t cols,
                        uint64_t* out) {
@@ -419,7 +419,7 @@ int ref_unpack(void* h, const uint64_t* packed, uint64_t R, uint64_t cols,
   GUARD_END
 }
 
-// baseline_matmul (matmul.cpp:415-486) with the client backend (it encrypts).
+// baseline_matmul (matmul.cpp:273-344) with the client backend (it encrypts).
 int ref_baseline(void* h, const int64_t* x, uint64_t R, uint64_t f,
                  const int64_t* w, uint64_t cols, uint64_t* out_blocks,
                  uint64_t* counters, double* secs) {
@@ -453,7 +453,7 @@ int ref_baseline(void* h, const int64_t* x, uint64_t R, uint64_t f,
 }
 
 // Decrypt one twin ciphertext (form 1 = eval) to signed slot values
-// (twin.cpp:446-452) and report the min noise budget.
+// (twin.cpp:153-159) and report the min noise budget.
 int ref_decrypt_signed(void* h, const uint64_t* ct, int form, int64_t* out,
                        int* budget) {
   GUARD_BEGIN

@@ -34,7 +34,7 @@ __global__ void k_poly_ntt(Geo g, uint32_t gp, uint32_t* __restrict__ polys, int
   for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) p[x] = sm[x];
 }
 
-// dot[pair] = sum_k in[row][k] (.) W[j][k]   (push_row, matmul.cpp:318-326)
+// dot[pair] = sum_k in[row][k] (.) W[j][k]   (push_row, matmul.cpp:176-184)
 // One block per (pair, poly); pairs of the batch map to (slot s = pair / cols,
 // j = pair % cols) and input rows are stored per batch slot.
 __global__ void k_chunk_dot(Geo g, const uint32_t* __restrict__ in, const uint2* __restrict__ W, uint32_t cols,
@@ -218,7 +218,7 @@ __global__ void k_rot_keyswitch(Geo g, const uint32_t* __restrict__ dot, const u
   }
 }
 
-// packed[g / N] += mask_{g mod N} (.) dot   (matmul.cpp:329-338, mask :288-305)
+// packed[g / N] += mask_{g mod N} (.) dot   (matmul.cpp:187-196, mask :288-305)
 // mask = NTT_q(lift(INTT_t(onehot at index_map[slot]))), regenerated per pair
 // exactly as the reference does for N > 4096. u64 atomics make the packed
 // accumulation order-free (mod-q addition is exact; reduced in k_finish_add).
@@ -252,11 +252,11 @@ __global__ void k_mask_acc(Geo g, const uint32_t* __restrict__ dot, const uint64
   }
 }
 
-// finish (matmul.cpp:342-374): reduce the u64 packed sums mod q and add the
+// finish (matmul.cpp:200-232): reduce the u64 packed sums mod q and add the
 // bias pattern: part0 += NTT_q(Delta * INTT_t(scatter(pattern)))
 // (context.cpp:393-402). Block per (packed ct c, gp).
 // Bias plaintext of every packed ciphertext (MatmulStream::finish,
-// matmul.cpp:342-374): slot s of ct c carries bias[(cN + s) mod |Y|] while
+// matmul.cpp:200-232): slot s of ct c carries bias[(cN + s) mod |Y|] while
 // cN + s < R|Y|; encode_slots -> INTT_t -> Delta * lift -> NTT_q. One block
 // per (c, prime); independent of the fold, so it runs on a side stream.
 __global__ void k_bias_plain(Geo g, const int64_t* __restrict__ bias, uint32_t cols, uint64_t total,
@@ -300,7 +300,7 @@ __global__ void k_finish_add(Geo g, const unsigned long long* __restrict__ acc64
   }
 }
 
-// encode_weights on the device (matmul.cpp:225-246): block per (j, k, gp):
+// encode_weights on the device (matmul.cpp:83-104): block per (j, k, gp):
 // slots -> centered residues mod t_b -> scatter -> INTT_t -> lift -> NTT_q.
 __global__ void k_encode_weights(Geo g, const int64_t* __restrict__ w, uint64_t f, uint32_t cols, uint32_t kc,
                                  uint2* __restrict__ W) {
@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
   }
 }
 
-// Mask multiply + packed accumulation, G pairs per block (matmul.cpp:329-338).
+// Mask multiply + packed accumulation, G pairs per block (matmul.cpp:187-196).
 // The one-hot's INTT_t has a closed form: slot s sits at eval position
 // p = index_map[s], i.e. at psi^(2 brv(p) + 1), so its coefficients are
 // m_j = n^-1 * w^j (mod t) with w = psi^-(2 brv(p) + 1) — identical values to

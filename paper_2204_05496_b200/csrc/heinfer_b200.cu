@@ -2,8 +2,8 @@
 //
 // Implements the C ABI of include/heinfer_b200.h. The reference path being
 // replaced is hei::matmul::MatmulStream / matmul / baseline_matmul
-// (/root/reference/proj/src/matmul/matmul.cpp:256-486) and everything it calls
-// on the server side: TwinBackend (fpcrt/twin.cpp:462-512), HeBackend
+// (/root/reference/proj/src/matmul/matmul.cpp:114-358) and everything it calls
+// on the server side: TwinBackend (fpcrt/twin.cpp:169-219), HeBackend
 // sum_all_slots (bfv/backend.cpp:63-73), BfvContext::mul_plain_inplace /
 // add_plain_inplace / apply_galois (bfv/context.cpp:393-507) and the kernels
 // table (kernels/modops_scalar.cpp, modops_avx2.cpp).
@@ -683,7 +683,7 @@ const uint32_t* mask_table(hei_gpu_ctx* c) {
 }
 
 // dot[pair] = sum_k chunk_k (.) W[j][k] for `rows` rows (push_row,
-// matmul.cpp:318-326): row-streaming kernel for the common chunk counts at
+// matmul.cpp:176-184): row-streaming kernel for the common chunk counts at
 // N >= 4096, the per-pair kernel otherwise.
 void launch_chunk_dot(hei_gpu_ctx* c, const uint32_t* in, const hei_gpu_weights* w, uint64_t rows, uint32_t* dot,
                       cudaStream_t st) {
@@ -1086,7 +1086,7 @@ void check_bias_range(hei_gpu_ctx* c, const int64_t* bias, uint64_t cols) {
     if (bias[j] > lim || bias[j] < -lim) raise(HEI_RANGE_ERROR, "encode_signed: value outside the centered range");
 }
 
-// capacity_check (fixed_point.cpp:248-264)
+// capacity_check (fixed_point.cpp:61-77)
 void capacity_gate(hei_gpu_ctx* c, uint64_t f, const char* who) {
   int log_f = f <= 1 ? 0 : 64 - __builtin_clzll(f - 1);
   int required = (int)(c->in_bits + c->s_x + c->s_w) + log_f;
@@ -1454,7 +1454,7 @@ void mt_chunk_starts(hei_gpu_ctx* c, const uint64_t* d_state, uint64_t K, uint64
   CU(cudaGetLastError());
 }
 
-// ---- client encryption: matmul::encode_inputs (matmul.cpp:201-223) --------
+// ---- client encryption: matmul::encode_inputs (matmul.cpp:59-81) --------
 // Every row is split into ceil(f / N) slot chunks, each encode_signed + encrypt
 // (eval form) with the branch's util::Prng stream, in (row, chunk) order — the
 // same draws BfvBackend::encrypt consumes (context.cpp:262-303).
@@ -2933,7 +2933,7 @@ int hei_gpu_baseline_matmul(hei_gpu_ctx* c, const int64_t* x, uint64_t rows, uin
                             uint64_t cols, const int64_t* bias, hei_gpu_prng* rng0, hei_gpu_prng* rng1,
                             uint64_t* out, hei_op_counters* cnt) {
   return guarded([&] {
-    // matmul.cpp:418-434
+    // matmul.cpp:276-292
     if (rows == 0 || f == 0 || cols == 0) raise(HEI_PARAM_ERROR, "baseline: empty input");
     capacity_gate(c, f, "baseline");
     if (!c->d_pk[0] || !c->d_pk[1]) raise(HEI_KEY_ERROR, "encrypt: this backend holds no public key");

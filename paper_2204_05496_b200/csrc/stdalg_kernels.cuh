@@ -1,5 +1,5 @@
 // Standard-algorithm and client-encryption kernels (baseline_matmul,
-// matmul.cpp:415-486; encrypt_parts, context.cpp:262-303). The mt19937_64
+// matmul.cpp:273-344; encrypt_parts, context.cpp:262-303). The mt19937_64
 // replay and the noise sampler live in baseline.cuh. Textually included by
 // heinfer_b200.cu inside its kernel namespace.
 #pragma once
@@ -8,7 +8,7 @@
 // Standard algorithm (baseline_matmul) kernels; see baseline.cuh.
 // ---------------------------------------------------------------------------
 // m = INTT_t(scatter(centered residues of x[base + s][k])) per (encryption,
-// branch); encryption e = kk * B + blk (matmul.cpp:444-452 loop order).
+// branch); encryption e = kk * B + blk (matmul.cpp:302-310 loop order).
 template <int LOGN>
 __global__ void __launch_bounds__(Ntt<LOGN>::T) k_bl_encode(Geo g, const int64_t* __restrict__ x, uint64_t R,
                                                            uint64_t f, uint64_t k0, uint32_t B,
@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T) k_bl_encode(Geo g, const int64_t
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
   const uint32_t e = blockIdx.x, b = blockIdx.y;
   // column mode (baseline): slot s = row base + s of feature k.
-  // row mode (encode_inputs, matmul.cpp:201-211): encryption k0 + e is chunk
+  // row mode (encode_inputs, matmul.cpp:59-69): encryption k0 + e is chunk
   // (k0 + e) % B of row (k0 + e) / B (B = chunks per row), slot s = feature.
   const uint64_t eg = k0 + e;
   const uint64_t k = row_mode ? 0 : k0 + e / B;
@@ -260,7 +260,7 @@ __global__ void k_bl_fold_sums(Geo g, const long long* __restrict__ sums, uint32
 // c1 = NTT(A) NTT(pk1) + NTT(Cv), with (A, Bv, Cv) the folded residues and
 // r_j = [bias_j]_t: the bias plaintext (all slots r_j) is the constant
 // polynomial r_j, so NTT(Delta r_j) is Delta r_j in every slot
-// (add_plain_inplace, context.cpp:393-402; matmul.cpp:328-335).
+// (add_plain_inplace, context.cpp:393-402; matmul.cpp:327-334).
 // pk is the coefficient-form public key [b][part][prime][n] u64.
 __global__ void k_bl_finish_lin(Geo g, const uint32_t* __restrict__ res, const uint64_t* __restrict__ pk0,
                                 const uint64_t* __restrict__ pk1, const int64_t* __restrict__ bias, uint32_t cols,
@@ -403,7 +403,7 @@ __global__ void k_prepare_pk_g(Geo g, const uint64_t* __restrict__ pk0, const ui
     o[x] = make_uint2(sm[x], (uint32_t)(((uint64_t)sm[x] << 32) / pr.q));
 }
 
-// prepare_constant_signed (twin.cpp:424-436, context.cpp:120-137) for every
+// prepare_constant_signed (twin.cpp:131-143, context.cpp:120-137) for every
 // (feature, class): centered residue mod t_b with its Shoup constant mod q_i.
 __global__ void k_bl_weights(Geo g, const int64_t* __restrict__ w, uint64_t count, uint2* __restrict__ out) {
   const uint64_t total = count * g.P;

@@ -70,10 +70,10 @@ class MatmulStream {
   OpCounters counters_;
 };
 
-// baseline_matmul (matmul.cpp:415-486). The reference draws encryption
+// baseline_matmul (matmul.cpp:273-344). The reference draws encryption
 // randomness from BfvBackend's private rng_; the device replays the same
 // util::Prng stream from `rng_seed` (branch b uses rng_seed + b, exactly as
-// TwinContext::client_backend seeds it, twin.cpp:351). Public keys come from
+// TwinContext::client_backend seeds it, twin.cpp:58). Public keys come from
 // TwinKeys::kp[b].pub.
 BaselineResult baseline_matmul(fpcrt::TwinBackend& be, const std::vector<bfv::PublicKey>& pub, uint64_t rng_seed,
                                const util::IntMat& x, const util::IntMat& w, const EncodedBias& b,

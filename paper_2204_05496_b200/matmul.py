@@ -1,13 +1,13 @@
 """Host-side mirror of hei::matmul (proj/include/hei/matmul/matmul.hpp:16-142)
 over the C ABI. Same names, argument meaning and error types as the reference:
 
-    proposed_counts / baseline_counts      (matmul.cpp:172-199)
-    GpuTwinServer                          (TwinContext::server_backend, twin.cpp:359-368)
-    encode_weights                         (matmul.cpp:225-246, on the device)
+    proposed_counts / baseline_counts      (matmul.cpp:30-57)
+    GpuTwinServer                          (TwinContext::server_backend, twin.cpp:66-75)
+    encode_weights                         (matmul.cpp:83-104, on the device)
     EncodedWeights.from_prepared           (upload of reference EncodedWeights)
-    encode_bias                            (matmul.cpp:248-254)
-    MatmulStream(push_row, finish, counters) (matmul.cpp:256-379)
-    matmul                                 (matmul.cpp:381-397)
+    encode_bias                            (matmul.cpp:106-112)
+    MatmulStream(push_row, finish, counters) (matmul.cpp:114-237)
+    matmul                                 (matmul.cpp:239-255)
 
 All residues use the reference's flat u64 layouts (include/heinfer_b200.h).
 """
@@ -288,7 +288,7 @@ class MatmulStream:
 
 
 def matmul(server: GpuTwinServer, inputs: np.ndarray, w: EncodedWeights, bias, form: int = FORM_EVAL):
-    """matmul::matmul (matmul.cpp:381-397): inputs [R][k][twin ct] u64 on the
+    """matmul::matmul (matmul.cpp:239-255): inputs [R][k][twin ct] u64 on the
     host. Returns (packed [C][twin ct] eval form, OpCounters)."""
     inputs = np.ascontiguousarray(inputs, dtype=np.uint64)
     if inputs.ndim != 3 or inputs.shape[0] == 0:
@@ -339,7 +339,7 @@ class Prng:
 
 
 def baseline_matmul(server: GpuTwinServer, x: np.ndarray, w: np.ndarray, bias, rng0: Prng, rng1: Prng):
-    """matmul::baseline_matmul (matmul.cpp:415-486): x is R x f, w is f x cols
+    """matmul::baseline_matmul (matmul.cpp:273-344): x is R x f, w is f x cols
     (scaled integers). Encrypts each feature column on the device with the
     replayed randomness. Returns (blocks [ceil(R/N)][cols][twin ct], counters)."""
     x = np.ascontiguousarray(x, dtype=np.int64)
@@ -362,7 +362,7 @@ def baseline_matmul(server: GpuTwinServer, x: np.ndarray, w: np.ndarray, bias, r
 
 
 def encode_inputs(server: GpuTwinServer, x: np.ndarray, rng0: Prng, rng1: Prng) -> np.ndarray:
-    """matmul::encode_inputs (matmul.cpp:201-223) on the device: x is R x f
+    """matmul::encode_inputs (matmul.cpp:59-81) on the device: x is R x f
     scaled integers; returns [R][ceil(f/N)][twin ct] u64 eval-form ciphertexts
     drawn from the two branch Prng streams (needs the public keys)."""
     x = np.ascontiguousarray(x, dtype=np.int64)

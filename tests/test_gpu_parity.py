@@ -283,7 +283,7 @@ def test_stream_rejects_bad_row_and_keeps_going(tiny32):
 
 @pytest.mark.parametrize("n", [32, 8192])
 def test_baseline_bit_exact_and_rng_state(n):
-    """baseline_matmul (matmul.cpp:415-486): same keys, same replayed
+    """baseline_matmul (matmul.cpp:273-344): same keys, same replayed
     randomness -> bit-identical blocks, exact decryption, closed-form counts;
     the Prng state afterwards continues the reference stream."""
     from paper_2204_05496_b200 import Prng, baseline_counts, baseline_matmul
@@ -951,7 +951,7 @@ def test_mask_table_matches_per_pair_masks(prod, monkeypatch):
 
 
 def test_chunk_products_row_kernel(prod, monkeypatch):
-    """push_row's chunk products (matmul.cpp:318-326) for a batch of >= 8
+    """push_row's chunk products (matmul.cpp:176-184) for a batch of >= 8
     rows take the row-streaming kernel (weights held in registers); same
     packed ciphertext as the per-pair kernel and the oracle."""
     from paper_2204_05496_b200 import EncodedWeights, MatmulStream
