@@ -2,7 +2,9 @@
 //
 // One CTA of T = N/16 threads transforms one polynomial; every thread keeps
 // 16 residues in registers for the whole transform and the 13 (14) radix-2
-// stages run as three register passes with two shared-memory exchanges:
+// stages run as three register passes with two shared-memory exchanges (the
+// A <-> B exchange spans the CTA; for LOGN <= 13 the B <-> C exchange stays
+// inside each warp and needs only a warp barrier):
 //
 //   pass A  stages 0..3          thread j holds x = j + T*r          (r < 16)
 //   pass B  stages 4..7          x = blk*(N/16) + jj + (N/256)*r
@@ -49,6 +51,17 @@ struct Ntt {
       __syncthreads();
     else
       asm volatile("bar.sync %0, %1;" ::"r"(1 + threadIdx.x / T), "r"(T) : "memory");
+  }
+  // The pass-B <-> pass-C exchange: for LOGN <= 13 pass B's 512-element block
+  // (blk = j >> (LOGN - 8)) and pass C's slots (posC0) of a warp are the same
+  // 512 words, so only the warp's own lanes meet there and a warp barrier
+  // orders them (one CTA barrier fewer per transform). At LOGN = 14 two warps
+  // share a pass-B block.
+  static __device__ __forceinline__ void sync_bc() {
+    if constexpr (LOGN <= 13)
+      __syncwarp();
+    else
+      sync();
   }
   static constexpr uint32_t G = N >> 8;          // pass-C block size
   static constexpr uint32_t TPG = G / 16;        // threads per pass-C block
@@ -162,7 +175,7 @@ struct Ntt {
     }
 #pragma unroll
     for (int r = 0; r < 16; ++r) sm[swz(posB(j, r))] = e[r];
-    sync();
+    sync_bc();
     // ---- pass C: stages 8..LOGN-1
     loadC(sm, j, e);
     const uint32_t x0 = posC0(j);
@@ -278,7 +291,7 @@ struct Ntt {
     }
     sync();
     storeC(sm, j, e);
-    sync();
+    sync_bc();
     // ---- pass B: stages 7..4
 #pragma unroll
     for (int r = 0; r < 16; ++r) e[r] = sm[swz(posB(j, r))];
