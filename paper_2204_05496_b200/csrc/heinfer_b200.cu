@@ -358,6 +358,7 @@ struct hei_gpu_ctx {
   size_t pool_dftrace_bytes = 0;
   size_t pool_dfcnt_bytes = 0;
   int df_grid = 0;                  // resident CTAs of k_fold_dataflow (occupancy x SMs)
+  int df_minb = 2;                  // HEI_DF_MINB: k_fold_dataflow CTAs per SM (launch bound, 2 or 3)
   uint64_t scratch_pairs = 0;
   std::mutex mu;
   // grow-only device pools for the per-call buffers of the device-resident
@@ -753,7 +754,8 @@ void set_fast_attrs(size_t sm) {
     set_smem_attr((const void*)k_rot_keyswitch_t, sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, true>, 6 * sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, false>, 6 * sm);
-    set_smem_attr((const void*)k_fold_dataflow, 2 * sm);
+    set_smem_attr((const void*)k_fold_dataflow<2>, 3 * sm);
+    set_smem_attr((const void*)k_fold_dataflow<3>, 3 * sm);
   }
   set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
   set_smem_attr((const void*)k_mask_prep<LG>, sm);
@@ -845,15 +847,16 @@ uint32_t* fold_dataflow(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t*
   d.part[0] = part;
   d.part[1] = part + part_words;
   const uint64_t tasks = df_tasks(d.S, (uint32_t)pairs, P, d.KP);
-  const size_t cnt_words = 4 * pairs * P + tasks + 2;
+  const size_t cnt_words = 2 * pairs * P + tasks + 2;
   uint32_t* cnt = pool_get(c->pool_dfcnt, c->pool_dfcnt_bytes, cnt_words * 4);
   d.count = cnt;
-  d.queue = cnt + 4 * pairs * P;
+  d.queue = cnt + 2 * pairs * P;
   d.head = d.queue + tasks;
   d.tail = d.head + 1;
+  const void* kfn = c->df_minb == 2 ? (const void*)k_fold_dataflow<2> : (const void*)k_fold_dataflow<3>;
   if (!c->df_grid) {
     int per_sm = 0, sms = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fold_dataflow, 512, smem_bytes(c, 2)));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 512, smem_bytes(c, 3)));
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
     c->df_grid = std::max(1, per_sm) * sms;
   }
@@ -865,7 +868,10 @@ uint32_t* fold_dataflow(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t*
     d.trace = pool_get(c->pool_dftrace, c->pool_dftrace_bytes, tasks * 4 * 8);
     CU(cudaMemsetAsync(d.trace, 0, tasks * 4 * 8, st));
   }
-  k_fold_dataflow<<<grid, 512, smem_bytes(c, 2), st>>>(c->geo, d);
+  if (c->df_minb == 2)
+    k_fold_dataflow<2><<<grid, 512, smem_bytes(c, 3), st>>>(c->geo, d);
+  else
+    k_fold_dataflow<3><<<grid, 512, smem_bytes(c, 3), st>>>(c->geo, d);
   LAUNCHED();
   if (trace_path) {
     std::vector<unsigned long long> h(tasks * 4);
@@ -1625,6 +1631,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_MT_JUMP")) c->mt_jump = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_DIGITS")) c->fuse_digits = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DATAFLOW")) c->dataflow = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_DF_MINB")) c->df_minb = std::atoi(v) == 2 ? 2 : 3;
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
