@@ -358,7 +358,6 @@ struct hei_gpu_ctx {
   size_t pool_dftrace_bytes = 0;
   size_t pool_dfcnt_bytes = 0;
   int df_grid = 0;                  // resident CTAs of k_fold_dataflow (occupancy x SMs)
-  int df_minb = 2;                  // HEI_DF_MINB: k_fold_dataflow CTAs per SM (launch bound, 2 or 3)
   uint64_t scratch_pairs = 0;
   std::mutex mu;
   // grow-only device pools for the per-call buffers of the device-resident
@@ -754,8 +753,8 @@ void set_fast_attrs(size_t sm) {
     set_smem_attr((const void*)k_rot_keyswitch_t, sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, true>, 6 * sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, false>, 6 * sm);
-    set_smem_attr((const void*)k_fold_dataflow<2>, 3 * sm);
-    set_smem_attr((const void*)k_fold_dataflow<3>, 3 * sm);
+    // 48 KB dynamic + the static words: past the default limit, so always opt in
+    CU(cudaFuncSetAttribute((const void*)k_fold_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * sm / 2)));
   }
   set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
   set_smem_attr((const void*)k_mask_prep<LG>, sm);
@@ -835,29 +834,31 @@ uint32_t* fold_dataflow(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t*
   for (uint32_t s = 0; s < d.S; ++s) {
     const uint64_t elt = c->fold_elts[s];
     d.perm[s] = c->d_perms + (size_t)c->perm_index.at(elt) * n;
+    if (elt % 4 == 3) d.swapmask |= 1u << s;  // g = 3 mod 4 swaps the eval halves
     for (int b = 0; b < 2; ++b)
       d.key[b][s] = c->d_keys[b] + (size_t)c->key_index[b].at(elt) * c->L[b] * 2 * c->L[b] * n;
   }
   d.ct[0] = cur;
   d.ct[1] = other;
-  d.dig[0] = dig;
-  d.dig[1] = dig2;
+  d.hd[0] = dig;  // [pairs][P][2][N/2]: the digit buffers' size
+  d.hd[1] = dig2;
   const size_t part_words = pairs * P * (kDfLmax - 1) * 2 * n;
   uint32_t* part = pool_get(c->pool_dfpart, c->pool_dfpart_bytes, 2 * part_words * 4);
   d.part[0] = part;
   d.part[1] = part + part_words;
   const uint64_t tasks = df_tasks(d.S, (uint32_t)pairs, P, d.KP);
-  const size_t cnt_words = 2 * pairs * P + tasks + 2;
+  const size_t cnt_words = 6 * pairs * P + tasks + 2;
   uint32_t* cnt = pool_get(c->pool_dfcnt, c->pool_dfcnt_bytes, cnt_words * 4);
   d.count = cnt;
-  d.queue = cnt + 2 * pairs * P;
+  d.queue = cnt + 6 * pairs * P;
   d.head = d.queue + tasks;
   d.tail = d.head + 1;
-  const void* kfn = c->df_minb == 2 ? (const void*)k_fold_dataflow<2> : (const void*)k_fold_dataflow<3>;
+  const size_t smem = 3 * (size_t)(n / 2) * 4;
   if (!c->df_grid) {
     int per_sm = 0, sms = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 512, smem_bytes(c, 3)));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fold_dataflow, 256, smem));
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    if (const char* v = std::getenv("HEI_DF_PER_SM")) per_sm = std::min(per_sm, std::max(1, std::atoi(v)));
     c->df_grid = std::max(1, per_sm) * sms;
   }
   k_df_seed<<<grid_for(tasks, 256), 256, 0, st>>>(d, P, (uint32_t)tasks);
@@ -868,10 +869,7 @@ uint32_t* fold_dataflow(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t*
     d.trace = pool_get(c->pool_dftrace, c->pool_dftrace_bytes, tasks * 4 * 8);
     CU(cudaMemsetAsync(d.trace, 0, tasks * 4 * 8, st));
   }
-  if (c->df_minb == 2)
-    k_fold_dataflow<2><<<grid, 512, smem_bytes(c, 3), st>>>(c->geo, d);
-  else
-    k_fold_dataflow<3><<<grid, 512, smem_bytes(c, 3), st>>>(c->geo, d);
+  k_fold_dataflow<<<grid, 256, smem, st>>>(c->geo, d);
   LAUNCHED();
   if (trace_path) {
     std::vector<unsigned long long> h(tasks * 4);
@@ -1631,7 +1629,6 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_MT_JUMP")) c->mt_jump = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_DIGITS")) c->fuse_digits = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_DATAFLOW")) c->dataflow = std::atoi(v) != 0;
-    if (const char* v = std::getenv("HEI_DF_MINB")) c->df_minb = std::atoi(v) == 2 ? 2 : 3;
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
@@ -1817,10 +1814,11 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
           }
         }
     }
-    // N = 16384 half-ring tables (ks_half.cuh): half h's stage s' block i'
-    // uses zetas[2^(s'+1) + h 2^s' + i'], stored at local index 2^s' + i'
+    // half-ring tables (N = 16384: ks_half.cuh; N = 8192: the dataflow
+    // fold, fold_dataflow.cuh): half h's stage s' block i' uses
+    // zetas[2^(s'+1) + h 2^s' + i'], stored at local index 2^s' + i'
     std::vector<uint4> twch, itwch;
-    if (c->logn == 14) {
+    if (c->logn == 13 || c->logn == 14) {
       const uint32_t hl = c->logn - 1, nh = n / 2, T = nh / 16, XST = hl - 12, PAD = XST % 2 == 0 ? 1 : 0,
                      KC = (PAD + XST + 16) / 2;  // Ntt<hl>'s pass-C layout
       g.twch_stride = KC * T;
