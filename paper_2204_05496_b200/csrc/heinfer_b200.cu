@@ -275,7 +275,6 @@ __device__ __forceinline__ uint32_t poly_prime(const Geo& g, uint32_t poly) {
 
 #include "fold_kernels.cuh"
 #include "tmem_ks.cuh"
-#include "fold_dataflow.cuh"
 #include "ks_half.cuh"
 
 #include "stdalg_kernels.cuh"
@@ -349,15 +348,6 @@ struct hei_gpu_ctx {
   // scratch (grown on demand)
   uint32_t *d_dotA = nullptr, *d_dotB = nullptr, *d_dig = nullptr, *d_dig2 = nullptr;
   bool fuse_digits = true;  // HEI_FUSE_DIGITS=0: separate digit kernel every rotation (small batches)
-  bool dataflow = false;    // HEI_DATAFLOW=1: small N = 8192 batches fold in the persistent dataflow kernel
-                            // (bit-exact; measured 0.65 vs 0.61 ms at C3)
-  uint32_t* pool_dfpart = nullptr;  // dataflow fold: key-switch products by parity
-  size_t pool_dfpart_bytes = 0;
-  uint32_t* pool_dfcnt = nullptr;   // dataflow fold: dependency counters + task counter
-  unsigned long long* pool_dftrace = nullptr;  // dataflow fold: debug timeline (HEI_DF_TRACE)
-  size_t pool_dftrace_bytes = 0;
-  size_t pool_dfcnt_bytes = 0;
-  int df_grid = 0;                  // resident CTAs of k_fold_dataflow (occupancy x SMs)
   uint64_t scratch_pairs = 0;
   std::mutex mu;
   // grow-only device pools for the per-call buffers of the device-resident
@@ -753,8 +743,6 @@ void set_fast_attrs(size_t sm) {
     set_smem_attr((const void*)k_rot_keyswitch_t, sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, true>, 6 * sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, false>, 6 * sm);
-    // 48 KB dynamic + the static words: past the default limit, so always opt in
-    CU(cudaFuncSetAttribute((const void*)k_fold_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * sm / 2)));
   }
   set_smem_attr((const void*)k_mask_acc_g<LG>, 3 * sm);
   set_smem_attr((const void*)k_mask_prep<LG>, sm);
@@ -817,72 +805,6 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
   return cur;
 }
 
-// Small N = 8192 batches: the whole fold as one persistent dataflow kernel
-// (fold_dataflow.cuh), every digit transform its own task.
-bool use_dataflow(hei_gpu_ctx* c, uint64_t pairs) {
-  return c->dataflow && c->logn == 13 && pairs * c->P() < 2u * 148u && c->L[0] >= 2 && c->L[1] >= 2 &&
-         c->L[0] <= (uint32_t)kDfLmax && c->L[1] <= (uint32_t)kDfLmax &&
-         c->fold_elts.size() <= (size_t)kMaxElts;
-}
-uint32_t* fold_dataflow(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, cudaStream_t st,
-                        uint32_t* dig, uint32_t* dig2) {
-  const uint32_t P = c->P(), n = c->n;
-  DfParams d{};
-  d.pairs = (uint32_t)pairs;
-  d.S = (uint32_t)c->fold_elts.size();
-  d.KP = c->L[0] * (c->L[0] - 1) + c->L[1] * (c->L[1] - 1);
-  for (uint32_t s = 0; s < d.S; ++s) {
-    const uint64_t elt = c->fold_elts[s];
-    d.perm[s] = c->d_perms + (size_t)c->perm_index.at(elt) * n;
-    if (elt % 4 == 3) d.swapmask |= 1u << s;  // g = 3 mod 4 swaps the eval halves
-    for (int b = 0; b < 2; ++b)
-      d.key[b][s] = c->d_keys[b] + (size_t)c->key_index[b].at(elt) * c->L[b] * 2 * c->L[b] * n;
-  }
-  d.ct[0] = cur;
-  d.ct[1] = other;
-  d.hd[0] = dig;  // [pairs][P][2][N/2]: the digit buffers' size
-  d.hd[1] = dig2;
-  const size_t part_words = pairs * P * (kDfLmax - 1) * 2 * n;
-  uint32_t* part = pool_get(c->pool_dfpart, c->pool_dfpart_bytes, 2 * part_words * 4);
-  d.part[0] = part;
-  d.part[1] = part + part_words;
-  const uint64_t tasks = df_tasks(d.S, (uint32_t)pairs, P, d.KP);
-  const size_t cnt_words = 6 * pairs * P + tasks + 2;
-  uint32_t* cnt = pool_get(c->pool_dfcnt, c->pool_dfcnt_bytes, cnt_words * 4);
-  d.count = cnt;
-  d.queue = cnt + 6 * pairs * P;
-  d.head = d.queue + tasks;
-  d.tail = d.head + 1;
-  const size_t smem = 3 * (size_t)(n / 2) * 4;
-  if (!c->df_grid) {
-    int per_sm = 0, sms = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fold_dataflow, 256, smem));
-    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-    if (const char* v = std::getenv("HEI_DF_PER_SM")) per_sm = std::min(per_sm, std::max(1, std::atoi(v)));
-    c->df_grid = std::max(1, per_sm) * sms;
-  }
-  k_df_seed<<<grid_for(tasks, 256), 256, 0, st>>>(d, P, (uint32_t)tasks);
-  LAUNCHED();
-  const unsigned grid = (unsigned)std::min<uint64_t>(tasks, (uint64_t)c->df_grid);
-  const char* trace_path = std::getenv("HEI_DF_TRACE");  // debug: per-task timeline
-  if (trace_path) {
-    d.trace = pool_get(c->pool_dftrace, c->pool_dftrace_bytes, tasks * 4 * 8);
-    CU(cudaMemsetAsync(d.trace, 0, tasks * 4 * 8, st));
-  }
-  k_fold_dataflow<<<grid, 256, smem, st>>>(c->geo, d);
-  LAUNCHED();
-  if (trace_path) {
-    std::vector<unsigned long long> h(tasks * 4);
-    CU(cudaMemcpyAsync(h.data(), d.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    if (FILE* f = std::fopen(trace_path, "ab")) {
-      std::fwrite(h.data(), 8, h.size(), f);
-      std::fclose(f);
-    }
-  }
-  return (d.S % 2) ? other : cur;
-}
-
 // Small batches (the single-individual latency path) replay the 26-28 fold
 // launches as one CUDA graph captured per (pairs, buffers), removing the
 // per-launch gaps that dominate when every launch covers < 2 blocks per SM.
@@ -890,7 +812,6 @@ uint32_t* fold(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* other, c
                uint32_t* dig = nullptr) {
   if (!dig) dig = c->d_dig;
   uint32_t* dig2 = c->d_dig2 + (dig - c->d_dig);  // second digit buffer of the same region
-  if (use_dataflow(c, pairs) && !c->timing) return fold_dataflow(c, pairs, cur, other, st, dig, dig2);
   const unsigned blocks = (unsigned)(pairs * c->P());
   const bool small = blocks < 2u * 148u;
   uint32_t* result = (c->fold_elts.size() % 2) ? other : cur;
@@ -1628,7 +1549,6 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_TWO_STREAMS")) c->two_streams = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_MT_JUMP")) c->mt_jump = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_DIGITS")) c->fuse_digits = std::atoi(v) != 0;
-    if (const char* v = std::getenv("HEI_DATAFLOW")) c->dataflow = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
@@ -1814,11 +1734,10 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
           }
         }
     }
-    // half-ring tables (N = 16384: ks_half.cuh; N = 8192: the dataflow
-    // fold, fold_dataflow.cuh): half h's stage s' block i' uses
-    // zetas[2^(s'+1) + h 2^s' + i'], stored at local index 2^s' + i'
+    // N = 16384 half-ring tables (ks_half.cuh): half h's stage s' block i'
+    // uses zetas[2^(s'+1) + h 2^s' + i'], stored at local index 2^s' + i'
     std::vector<uint4> twch, itwch;
-    if (c->logn == 13 || c->logn == 14) {
+    if (c->logn == 14) {
       const uint32_t hl = c->logn - 1, nh = n / 2, T = nh / 16, XST = hl - 12, PAD = XST % 2 == 0 ? 1 : 0,
                      KC = (PAD + XST + 16) / 2;  // Ntt<hl>'s pass-C layout
       g.twch_stride = KC * T;
@@ -1950,9 +1869,6 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->pool_rows);
   cudaFree(c->pool_bias);
   cudaFree(c->pool_stage64);
-  cudaFree(c->pool_dfpart);
-  cudaFree(c->pool_dfcnt);
-  cudaFree(c->pool_dftrace);
   if (c->pinned_bias) cudaFreeHost(c->pinned_bias);
   if (c->pinned_out) cudaFreeHost(c->pinned_out);
   cudaFree(c->pool_in32);

@@ -904,16 +904,15 @@ def test_stream_concurrent_push_from_threads(tiny32):
     assert np.array_equal(st.finish(), want)
 
 
-@pytest.mark.parametrize("cts_n,dataflow", [(1, "0"), (1, "1"), (3, "1"), (20, "0"), (20, "1"), (40, "0"), (64, "0")])
-def test_fold_paths_bit_exact(prod, cts_n, dataflow, monkeypatch):
+@pytest.mark.parametrize("cts_n", [1, 3, 20, 40, 64])
+def test_fold_paths_bit_exact(prod, cts_n):
     """sum_all_slots (backend.cpp:63-73) at the launch sizes that select each
     N = 8192 fold path. Below 296 (pair, prime) blocks the per-rotation
-    kernels (1 ciphertext: the 2-group latency kernel, 20: shared-memory
-    accumulators, both with the next digit fused), or with HEI_DATAFLOW=1 the
-    persistent dataflow kernel (fold_dataflow.cuh) for the whole fold. 40 ciphertexts (400 blocks): shared-memory kernel with
-    parameter-space twiddles, fused; 64 (640 blocks): digit INTT kernel +
+    kernels (1 and 3 ciphertexts: the 2-group latency kernel, 20:
+    shared-memory accumulators, both with the next digit fused). 40
+    ciphertexts (400 blocks): shared-memory kernel with parameter-space
+    twiddles, fused; 64 (640 blocks): digit INTT kernel +
     TMEM-accumulator key switch. Every output equals the oracle's."""
-    monkeypatch.setenv("HEI_DATAFLOW", dataflow)
     o, _ = prod
     rng = np.random.default_rng(64 + cts_n)
     x = rng.integers(-9, 9, size=(cts_n, o.n), dtype=np.int64)
