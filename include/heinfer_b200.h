@@ -46,7 +46,12 @@ typedef struct hei_gpu_weights hei_gpu_weights; /* EncodedWeights resident in HB
 typedef struct hei_gpu_stream hei_gpu_stream;   /* MatmulStream */
 typedef struct hei_gpu_prng hei_gpu_prng;       /* util::Prng replay (rng.hpp:19-68) */
 
-/* matmul::OpCounters (matmul.hpp:21-27) */
+/* matmul::OpCounters (matmul.hpp:21-27). The matmul entry points report
+ * MEASURED deltas, as MatmulStream::finish does (matmul.cpp:224-229): the
+ * kernels that perform the chunk products, rotations, fold adds, mask
+ * products and packed accumulations add them to context counters (branch 0
+ * speaks for the pair, as TwinBackend::counters does), and each call
+ * reports end minus start. ciphertexts_in/out are the call's shapes. */
 typedef struct {
   uint64_t mul_plain_count;
   uint64_t rotation_count;

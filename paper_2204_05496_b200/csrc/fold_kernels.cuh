@@ -42,6 +42,7 @@ __global__ void k_chunk_dot(Geo g, const uint32_t* __restrict__ in, const uint2*
   const uint32_t n = g.n, polys = 2 * g.P;
   const uint32_t pair = blockIdx.x / polys, poly = blockIdx.x % polys;
   const uint32_t s = pair / cols, j = pair % cols;
+  if (poly == 0) count_ops(g, kc, 0, kc - 1);  // push_row: kc products, kc - 1 merges (add_many)
   const uint32_t gp = poly_prime(g, poly);
   const uint32_t q = g.pr[gp].q;
   const uint32_t* src = in + ((uint64_t)s * kc * g.ct_words) + (uint64_t)poly * n;
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(256) k_chunk_dot_rows(Geo g, const uint32_t* _
   const uint32_t gp = poly_prime(g, poly);
   const uint32_t q = g.pr[gp].q;
   const uint32_t j0 = cg * CG, nj = min((uint32_t)CG, cols - j0);
+  if (poly == 0 && tile == 0) count_ops(g, (uint64_t)rows * nj * KC, 0, (uint64_t)rows * nj * (KC - 1));
   uint2 w[CG][KC];
 #pragma unroll
   for (int jj = 0; jj < CG; ++jj)
@@ -163,6 +165,7 @@ __global__ void k_rot_keyswitch(Geo g, const uint32_t* __restrict__ dot, const u
   uint32_t* acc0 = sm + n;
   uint32_t* acc1 = sm + 2 * n;
   const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  if (gp == 0) count_ops(g, 0, 1, fold ? 1 : 0);  // one rotation (+ the fold add) per pair (backend.cpp:63-73)
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t q = pr.q, L = pr.L, i = pr.i;
   const uint32_t* ct = dot + (uint64_t)pair * g.ct_words;
@@ -227,6 +230,7 @@ __global__ void k_mask_acc(Geo g, const uint32_t* __restrict__ dot, const uint64
   extern __shared__ uint32_t sm[];
   const uint32_t n = g.n;
   const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  if (gp == 0) count_ops(g, 1, 0, 1);  // mask product + packed accumulation per pair (matmul.cpp:187-196)
   const PrimeInfo& pr = g.pr[gp];
   const BranchInfo& br = g.br[pr.b];
   const uint64_t gidx = rows[pair / cols] * cols + pair % cols;
@@ -532,6 +536,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
   uint4* a0s = smem4 + N / 4;
   uint4* a1s = a0s + 4 * T;
   const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  if (gp == 0) count_ops(g, 0, 1, fold ? 1 : 0);  // one rotation (+ the fold add) per pair (backend.cpp:63-73)
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t q = pr.q, L = pr.L, i = pr.i;
   const uint32_t j = threadIdx.x, x0 = NT::posC0(j);
@@ -682,6 +687,7 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
   uint4* o1s = o0s + 4 * T;
   uint32_t* sm1 = reinterpret_cast<uint32_t*>(smem4 + 3 * N / 4);  // group 1's buffer
   const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
+  if (gp == 0) count_ops(g, 0, 1, fold ? 1 : 0);  // one rotation (+ the fold add) per pair (backend.cpp:63-73)
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t q = pr.q, L = pr.L, i = pr.i;
   const uint32_t j = threadIdx.x % T, x0 = NT::posC0(j);
@@ -867,6 +873,10 @@ __global__ void k_mask_apply(Geo g, const uint32_t* __restrict__ dot, const uint
     const uint32_t gp = (uint32_t)((x % per) / g.n), k = (uint32_t)(x % g.n);
     const PrimeInfo& pr = g.pr[gp];
     const uint64_t gidx = rows[pair / cols] * cols + pair % cols, c = gidx / g.n;
+    if (gp == 0 && k == 0 && g.ops) {  // mask product + packed accumulation per pair
+      atomicAdd(g.ops, 1ull);
+      atomicAdd(g.ops + 2, 1ull);
+    }
     const uint32_t m = masks[x];
     const uint32_t* base = dot + pair * g.ct_words;
     const uint32_t a = mul_barrett(base[(uint64_t)pr.poly0 * g.n + k], m, pr.q, pr.mu);
@@ -889,6 +899,7 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_mask_acc
   uint4* a1s = a0s + 4 * T;
   const uint32_t gp = blockIdx.x % g.P;
   const uint32_t p0 = (blockIdx.x / g.P) * G, p1 = min(npairs, p0 + G);
+  if (gp == 0) count_ops(g, p1 - p0, 0, p1 - p0);  // mask product + packed accumulation per pair
   const PrimeInfo& pr = g.pr[gp];
   const BranchInfo& br = g.br[pr.b];
   const uint32_t q = pr.q, t = br.t, j = threadIdx.x, x0 = NT::posC0(j);
@@ -996,6 +1007,7 @@ __global__ void __launch_bounds__(256) k_mask_acc_c(Geo g, const uint32_t* __res
   const uint32_t N = g.n, slices = N / 1024;
   const uint32_t sl = blockIdx.x % slices, gp = (blockIdx.x / slices) % g.P;
   const uint32_t p0 = (blockIdx.x / (slices * g.P)) * G, p1 = min(npairs, p0 + G);
+  if (gp == 0 && sl == 0) count_ops(g, p1 - p0, 0, p1 - p0);  // mask product + packed accumulation per pair
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t q = pr.q, x0 = sl * 1024 + 4 * threadIdx.x;
   uint32_t A[4] = {0, 0, 0, 0}, B[4] = {0, 0, 0, 0};

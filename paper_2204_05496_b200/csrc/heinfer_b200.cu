@@ -222,7 +222,19 @@ struct Geo {
   uint32_t twch_stride;
   const uint2* invh;    // inverse counterparts (k_rot_digits_h)
   const uint4* itwch;
+  // measured operation counters (HeBackend counters, backend.cpp:75-85):
+  // [mul_plain, rotation, add], cumulative over the context; the kernels
+  // that perform the ops add them (branch 0 speaks for the pair, as
+  // TwinBackend::counters does), and each matmul reports the delta
+  unsigned long long* ops;
 };
+// thread 0 of a counting block
+__device__ __forceinline__ void count_ops(const Geo& g, uint64_t mul_plain, uint64_t rotation, uint64_t add) {
+  if (threadIdx.x != 0 || !g.ops) return;
+  if (mul_plain) atomicAdd(g.ops, (unsigned long long)mul_plain);
+  if (rotation) atomicAdd(g.ops + 1, (unsigned long long)rotation);
+  if (add) atomicAdd(g.ops + 2, (unsigned long long)add);
+}
 // (pair, prime) of this block, for grids of pairs * P blocks (pair-major)
 __device__ __forceinline__ void block_pair_prime(const Geo& g, uint32_t& pair, uint32_t& gp) {
   pair = blockIdx.x / g.P;
@@ -342,6 +354,9 @@ struct hei_gpu_ctx {
   CrtInfo crt{};                 // exact CRT constants per branch (decrypt_core)
   uint32_t t0inv = 0;            // t0^-1 mod t1 (crt_recombine)
   uint32_t* d_err = nullptr;
+  unsigned long long* d_ops = nullptr;      // [3] measured op counters (Geo::ops), cumulative
+  unsigned long long* d_opsnap = nullptr;   // [6] one-shot calls: counters at the call's start, then at its end
+  unsigned long long* h_opsnap = nullptr;   // [6] pinned copy of d_opsnap
   cudaStream_t stream = nullptr;
   uint64_t batch_pairs = 0;
   uint64_t keys_words[2] = {0, 0};
@@ -436,6 +451,8 @@ struct hei_gpu_stream {
   uint64_t* d_stage64 = nullptr;
   uint64_t* d_rows = nullptr;
   uint64_t cap_rows = 0;
+  unsigned long long* d_ops0 = nullptr;  // [6] op counters at creation, then at finish
+  bool owns_ops0 = true;
 };
 
 // util::Prng (rng.hpp:19-68): mt19937_64 state kept explicitly so the
@@ -1055,6 +1072,14 @@ hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64
     s->owns_rows = false;
   }
   if (!ext_acc) CU(cudaMemsetAsync(s->d_acc, 0, s->C * c->ct_words() * 8, zero_on ? zero_on : c->stream));
+  // the counters' start (MatmulStream keeps start_ = be.counters(), matmul.cpp:143)
+  if (host_staging) {
+    CU(cudaMalloc(&s->d_ops0, 6 * 8));
+  } else {
+    s->d_ops0 = c->d_opsnap;
+    s->owns_ops0 = false;
+  }
+  CU(cudaMemcpyAsync(s->d_ops0, c->d_ops, 3 * 8, cudaMemcpyDeviceToDevice, zero_on ? zero_on : c->stream));
   if (!host_staging && encode_bias) {
     // stage the bias now (pinned, async): every earlier call has synchronised
     const size_t bb = s->bias.size() * 8;
@@ -1082,6 +1107,25 @@ hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64
   return s.release();
 }
 
+// The counters at the end of the call (after every counting kernel on `st`
+// and the streams joined into it), copied with the start snapshot to pinned
+// memory; read them with ops_report after `st` is synchronised.
+void ops_end(hei_gpu_stream* s, cudaStream_t st) {
+  hei_gpu_ctx* c = s->ctx;
+  CU(cudaMemcpyAsync(s->d_ops0 + 3, c->d_ops, 3 * 8, cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemcpyAsync(c->h_opsnap, s->d_ops0, 6 * 8, cudaMemcpyDeviceToHost, st));
+}
+// MatmulStream::finish's counters (matmul.cpp:224-229): measured deltas of
+// mul_plain / rotation / add, plus the ciphertext counts.
+void ops_report(hei_gpu_stream* s, hei_op_counters* cnt) {
+  const unsigned long long* h = s->ctx->h_opsnap;
+  cnt->mul_plain_count = h[3] - h[0];
+  cnt->rotation_count = h[4] - h[1];
+  cnt->add_count = h[5] - h[2];
+  cnt->ciphertexts_in = s->rows * s->w->kc;
+  cnt->ciphertexts_out = s->C;
+}
+
 void stream_free(hei_gpu_stream* s) {
   if (!s) return;
   cudaSetDevice(s->ctx->device);
@@ -1090,6 +1134,7 @@ void stream_free(hei_gpu_stream* s) {
   if (s->d_stage64) cudaFree(s->d_stage64);
   if (s->owns_rows) cudaFree(s->d_rows);
   if (s->bias_ev) cudaEventDestroy(s->bias_ev);
+  if (s->owns_ops0 && s->d_ops0) cudaFree(s->d_ops0);
   delete s;
 }
 
@@ -1131,6 +1176,7 @@ void stream_finish(hei_gpu_stream* s, uint64_t* out, hei_op_counters* cnt) {
   CU(cudaMalloc(&d_out, words * 4));
   CU(cudaMalloc(&d_out64, words * 8));
   finish_to(s, d_out, c->stream);
+  ops_end(s, c->stream);
   k_widen<<<grid_for(words, 256), 256, 0, c->stream>>>(d_out, d_out64, words);
   LAUNCHED();
   CU(cudaMemcpyAsync(out, d_out64, words * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -1138,7 +1184,7 @@ void stream_finish(hei_gpu_stream* s, uint64_t* out, hei_op_counters* cnt) {
   cudaFree(d_out);
   cudaFree(d_out64);
   s->finished = true;
-  if (cnt) hei_proposed_counts(s->rows, s->w->cols, s->w->f, c->n, cnt);
+  if (cnt) ops_report(s, cnt);
 }
 
 hei_gpu_weights* weights_alloc(hei_gpu_ctx* c, uint64_t f, uint64_t cols) {
@@ -1817,7 +1863,12 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     CU(cudaMemcpyAsync(c->d_perms, perms.data(), perms.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     CU(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
+    CU(cudaMalloc(&c->d_ops, 9 * 8));
+    c->d_opsnap = c->d_ops + 3;
+    CU(cudaMemsetAsync(c->d_ops, 0, 9 * 8, c->stream));
+    CU(cudaMallocHost(&c->h_opsnap, 6 * 8));
     CU(cudaStreamSynchronize(c->stream));
+    g.ops = c->d_ops;
     g.fwd = c->d_fwd;
     g.inv = c->d_inv;
     g.index_map = c->d_index;
@@ -1859,6 +1910,8 @@ void hei_gpu_ctx_destroy(hei_gpu_ctx* c) {
   cudaFree(c->d_index);
   cudaFree(c->d_perms);
   cudaFree(c->d_err);
+  cudaFree(c->d_ops);
+  if (c->h_opsnap) cudaFreeHost(c->h_opsnap);
   for (int b = 0; b < 2; ++b) {
     cudaFree(c->d_keys[b]);
     cudaFree(c->d_pk[b]);
@@ -2602,6 +2655,7 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
   const size_t out_bytes = wire ? s->C * (io.wg.blob[0] + io.wg.blob[1]) : outw * 8;
   uint64_t* d_out64 = pool_get(c->pool_out64, c->pool_out64_bytes, out_bytes);
   finish_to(s.get(), d_out, st);
+  ops_end(s.get(), st);
   if (wire) {
     // save_ciphertext writes canonical coefficient form (serialize.cpp:67-71)
     launch_ct_intt(c, (unsigned)(s->C * 2 * c->P()), d_out, st);
@@ -2615,7 +2669,7 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
     d2h_result(c, io.out64, d_out64, outw * 8, st);
   }
   s->finished = true;
-  if (cnt) hei_proposed_counts(rows, w->cols, w->f, c->n, cnt);
+  if (cnt) ops_report(s.get(), cnt);
 }
 
 int hei_gpu_matmul(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint64_t* inputs, int form, uint64_t rows,
@@ -2724,9 +2778,10 @@ int hei_gpu_matmul_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint32
     }
     s->pushed = rows;
     finish_to(s.get(), d_out, st);
+    ops_end(s.get(), st);
     CU(cudaStreamSynchronize(st));
     s->finished = true;
-    if (cnt) hei_proposed_counts(rows, w->cols, w->f, c->n, cnt);
+    if (cnt) ops_report(s.get(), cnt);
   });
 }
 

@@ -99,8 +99,9 @@ def test_fast_matmul_bit_exact_vs_reference(case):
     for _ in range(2):  # second call replays cached graphs / warmed pools
         d_out.zero_()
         torch.cuda.synchronize()
-        matmul_device(srv, d_in.data_ptr(), R, ew, b, d_out.data_ptr(), st.cuda_stream)
+        dcnt = matmul_device(srv, d_in.data_ptr(), R, ew, b, d_out.data_ptr(), st.cuda_stream)
         torch.cuda.synchronize()
+        assert list(dcnt.as_tuple()) == g["counters"], "measured device-path counters differ"
         dev = d_out.cpu().numpy().view(np.uint32).astype(np.uint64)
         assert sha(dev) == g["packed_sha256"], "device-path packed result differs from the reference"
     del d_in

@@ -1008,3 +1008,35 @@ def test_n16384_fold_paths(cts_n):
     got = gpu_server_from(o).sum_all_slots(cts)
     for r in (0, cts_n - 1):
         assert np.array_equal(got[r], o.sum_all_slots(cts[r])), r
+
+
+def test_counters_are_measured(prod):
+    """OpCounters are the deltas of counters the kernels themselves add up
+    (HeBackend counters, backend.cpp:75-85; MatmulStream::finish,
+    matmul.cpp:224-229), not a closed form: two calls of different shapes on
+    one context each report their own ops, equal to the reference's closed
+    forms (test_matmul.cpp:100-105), through the host, device and stream
+    paths."""
+    import torch
+
+    from paper_2204_05496_b200 import MatmulStream, encode_weights, matmul, matmul_device, proposed_counts
+
+    o, s = prod
+    for rows, f, cols in ((2, 9000, 3), (1, 20000, 11)):
+        x, w, b = synthetic(rows, f, cols, 0.05, 0.1, seed=rows + cols)
+        inputs = o.encode_inputs(x)
+        ew = encode_weights(s, w)
+        want = proposed_counts(rows, cols, f, o.n).as_tuple()
+        _, cnt = matmul(s, inputs, ew, b)
+        assert cnt.as_tuple() == want
+        d_in = torch.from_numpy(inputs.reshape(-1, inputs.shape[-1]).astype(np.uint32).view(np.int32)).cuda()
+        Cn = (rows * cols + o.n - 1) // o.n
+        d_out = torch.empty((Cn, inputs.shape[-1]), dtype=torch.int32, device="cuda")
+        dcnt = matmul_device(s, d_in.data_ptr(), rows, ew, b, d_out.data_ptr())
+        torch.cuda.synchronize()
+        assert dcnt.as_tuple() == want
+        st = MatmulStream(s, ew, b, rows)
+        for r in reversed(range(rows)):
+            st.push_row(r, inputs[r])
+        st.finish()
+        assert st.counters().as_tuple() == want
