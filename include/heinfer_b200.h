@@ -271,6 +271,11 @@ int hei_gpu_ntt(hei_gpu_ctx* ctx, uint32_t branch, uint32_t prime, uint64_t* pol
  * (BfvContext::apply_galois, context.cpp:428-507). */
 int hei_gpu_apply_galois(hei_gpu_ctx* ctx, uint32_t branch, uint64_t elt, const uint64_t* in,
                          uint64_t* out);
+/* The same on a ciphertext in either form (HEI_FORM_EVAL / HEI_FORM_COEFF):
+ * BfvContext::apply_galois's coefficient-form path (context.cpp:460-465,
+ * 499-503; automorphism_coeff, poly.cpp:107-122) returns coefficient form. */
+int hei_gpu_apply_galois_form(hei_gpu_ctx* ctx, uint32_t branch, uint64_t elt, int form,
+                              const uint64_t* in, uint64_t* out);
 /* HeBackend::sum_all_slots on twin ciphertexts (backend.cpp:63-73). */
 int hei_gpu_sum_all_slots(hei_gpu_ctx* ctx, const uint64_t* in, uint64_t* out, uint64_t count);
 /* Kernel launches issued by this thread since the last reset. */

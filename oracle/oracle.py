@@ -279,6 +279,13 @@ class Reference(_Twin):
     def _apply_galois(self, b, elt, ct, out):
         self._check(self.lib.ref_apply_galois(self._h, C.c_int(b), C.c_uint64(elt), _u64p(ct), C.c_int(1), _u64p(out)))
 
+    def apply_galois_coeff(self, b: int, elt: int, ct: np.ndarray) -> np.ndarray:
+        """The reference's coefficient-form apply_galois (context.cpp:460-465, 499-503)."""
+        ct = np.ascontiguousarray(ct, np.uint64)
+        out = np.zeros_like(ct)
+        self._check(self.lib.ref_apply_galois(self._h, C.c_int(b), C.c_uint64(elt), _u64p(ct), C.c_int(0), _u64p(out)))
+        return out
+
     def load_inputs(self, inputs: np.ndarray, f: int, form: int = 1):
         inputs = np.ascontiguousarray(inputs, np.uint64)
         self._check(self.lib.ref_load_inputs(self._h, _u64p(inputs), C.c_uint64(inputs.shape[0]), C.c_uint64(f), C.c_int(form)))

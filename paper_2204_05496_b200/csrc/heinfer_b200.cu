@@ -2809,8 +2809,13 @@ int hei_gpu_ntt(hei_gpu_ctx* c, uint32_t b, uint32_t prime, uint64_t* polys, uin
 }
 
 int hei_gpu_apply_galois(hei_gpu_ctx* c, uint32_t b, uint64_t elt, const uint64_t* in, uint64_t* out) {
+  return hei_gpu_apply_galois_form(c, b, elt, HEI_FORM_EVAL, in, out);
+}
+
+int hei_gpu_apply_galois_form(hei_gpu_ctx* c, uint32_t b, uint64_t elt, int form, const uint64_t* in, uint64_t* out) {
   return guarded([&] {
     if (b > 1) raise(HEI_PARAM_ERROR, "branch out of range");
+    if (form != HEI_FORM_EVAL && form != HEI_FORM_COEFF) raise(HEI_PARAM_ERROR, "apply_galois: unknown form");
     if (!c->has_keys[b] || !c->key_index[b].count(elt))
       raise(HEI_KEY_ERROR, "apply_galois: no key for galois element " + std::to_string(elt));
     if (!c->perm_index.count(elt)) raise(HEI_KEY_ERROR, "apply_galois: unsupported galois element");
@@ -2857,8 +2862,26 @@ int hei_gpu_apply_galois(hei_gpu_ctx* c, uint32_t b, uint64_t elt, const uint64_
     CU(cudaStreamSynchronize(c->stream));
     const uint32_t* perm = c->d_perms + (size_t)c->perm_index.at(elt) * n;
     const uint2* key = c->d_keys[b] + (size_t)c->key_index[b].at(elt) * L * 2 * L * n;
+    const size_t sm = smem_bytes(c, 1);
+    // Coefficient-form input (context.cpp:460-465, 499-503): the reference
+    // takes sigma_coeff of c0 and c1 (automorphism_coeff, poly.cpp:107-122),
+    // switches the keys in the eval domain and inverse-transforms acc0/acc1
+    // before adding sigma_coeff(c0). Transforming in, running the eval path
+    // and transforming out computes the same residues exactly: NTT and INTT
+    // are exact inverses mod q_i, INTT(sigma_eval(NTT(x))) = sigma_coeff(x),
+    // so the digits and every sum equal the reference's.
+    if (form == HEI_FORM_COEFF) {
+      HEI_DISPATCH(c->logn, (k_ct_ntt_f<LG><<<2 * L, Ntt<LG>::T, sm, c->stream>>>(gb, d_in)),
+                   (k_ct_ntt<<<2 * L, c->threads(), sm, c->stream>>>(gb, d_in, 0)));
+      LAUNCHED();
+    }
     launch_rot_digits(c, gb, L, d_in, perm, d_dig, c->stream);
     launch_rot_keyswitch(c, gb, L, d_in, d_dig, perm, key, key, d_out, 0, c->stream);
+    if (form == HEI_FORM_COEFF) {
+      HEI_DISPATCH(c->logn, (k_ct_intt_f<LG><<<2 * L, Ntt<LG>::T, sm, c->stream>>>(gb, d_out)),
+                   (k_ct_ntt<<<2 * L, c->threads(), sm, c->stream>>>(gb, d_out, 1)));
+      LAUNCHED();
+    }
     CU(cudaMemcpyAsync(h32.data(), d_out, words * 4, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     cudaFree(d_in);

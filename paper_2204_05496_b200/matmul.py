@@ -183,10 +183,13 @@ class GpuTwinServer:
         check(native.lib().hei_gpu_ntt(self._h, C.c_uint32(branch), C.c_uint32(prime), u64p(a), C.c_uint64(count), C.c_int(int(inverse))))
         return a
 
-    def apply_galois(self, branch: int, elt: int, ct: np.ndarray) -> np.ndarray:
+    def apply_galois(self, branch: int, elt: int, ct: np.ndarray, form: int = FORM_EVAL) -> np.ndarray:
+        """BfvContext::apply_galois (context.cpp:428-507) on a single-branch
+        ciphertext [2][L][N] in `form`; the result keeps the input's form."""
         ct = np.ascontiguousarray(ct, dtype=np.uint64)
         out = np.zeros_like(ct)
-        check(native.lib().hei_gpu_apply_galois(self._h, C.c_uint32(branch), C.c_uint64(elt), u64p(ct), u64p(out)))
+        check(native.lib().hei_gpu_apply_galois_form(self._h, C.c_uint32(branch), C.c_uint64(elt), C.c_int(form), u64p(ct),
+                                                     u64p(out)))
         return out
 
     def sum_all_slots(self, cts: np.ndarray) -> np.ndarray:

@@ -98,7 +98,7 @@ EXPORTED = [
     "hei_gpu_prng_create", "hei_gpu_prng_destroy", "hei_gpu_prng_draw", "hei_gpu_baseline_matmul", "hei_proposed_counts",
     "hei_baseline_counts", "hei_gpu_ntt", "hei_gpu_apply_galois", "hei_gpu_sum_all_slots",
     "hei_gpu_launch_count", "hei_gpu_reset_launch_count", "hei_gpu_set_batch_pairs",
-    "hei_gpu_kernel_timing", "hei_gpu_kernel_stats", "hei_gpu_measure_butterfly_peak",
+    "hei_gpu_kernel_timing", "hei_gpu_apply_galois_form", "hei_gpu_kernel_stats", "hei_gpu_measure_butterfly_peak",
     "hei_gpu_matmul_partial_device", "hei_gpu_finish_packed_device",
     "hei_gpu_encode_inputs", "hei_gpu_encode_inputs_device",
     "hei_hect_ciphertext_bytes", "hei_params_hash", "hei_gpu_matmul_wire",

@@ -76,6 +76,36 @@ def test_apply_galois_every_element(which, request):
             assert np.array_equal(got, want), (b, int(elt))
 
 
+@pytest.mark.parametrize("which,case", [("tiny32", "tiny_32"), ("prod", "prod_8192")])
+def test_apply_galois_coeff_form_matches_reference(which, case, request):
+    """Coefficient-form apply_galois (context.cpp:460-465, 499-503;
+    automorphism_coeff, poly.cpp:107-122) against the reference's own outputs
+    (tests/golden/make_golden_galois.py, same keys and seeded inputs), every
+    Galois element, both branches; the result stays in coefficient form."""
+    import hashlib
+    import json
+    import os
+
+    from paper_2204_05496_b200.native import FORM_COEFF
+    from tests.golden.make_golden_galois import coeff_input
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    gold = json.load(open(os.path.join(here, "galois_coeff.json")))[case]
+    arrs = np.load(os.path.join(here, "galois_coeff.npz"))
+    o, s = request.getfixturevalue(which)
+    assert [int(e) for e in o.elts()] == gold["elts"]
+    for b in range(2):
+        g = gold["branches"][str(b)]
+        ct = coeff_input(g["q"], len(g["q"]), o.n, gold["input_seed"] + b)
+        if f"{case}_b{b}_in" in arrs:
+            assert np.array_equal(ct, arrs[f"{case}_b{b}_in"])
+        for k, elt in enumerate(gold["elts"]):
+            got = s.apply_galois(b, elt, ct.reshape(-1), form=FORM_COEFF)
+            assert hashlib.sha256(got.tobytes()).hexdigest() == g["out_sha256"][k], (b, elt)
+            if f"{case}_b{b}_out" in arrs:
+                assert np.array_equal(got, arrs[f"{case}_b{b}_out"][k].reshape(-1))
+
+
 @pytest.mark.parametrize("which", ["tiny32", "prod"])
 def test_sum_all_slots_twin(which, request):
     o, s = request.getfixturevalue(which)
