@@ -291,7 +291,14 @@ __global__ void k_bias_plain(Geo g, const int64_t* __restrict__ bias, uint32_t c
 
 // Packed accumulators mod q plus the bias plaintext on part 0.
 __global__ void k_finish_add(Geo g, const unsigned long long* __restrict__ acc64, const uint32_t* __restrict__ biasp,
-                             uint64_t C, uint32_t* __restrict__ out) {
+                             uint64_t C, uint32_t* __restrict__ out, const unsigned long long* __restrict__ ops0,
+                             unsigned long long* ops_out) {
+  // the call's op counters: start snapshot and current values (every
+  // counting kernel of the call precedes this one on the stream)
+  if (ops_out && blockIdx.x == 0 && threadIdx.x < 3) {
+    ops_out[threadIdx.x] = __ldcg(ops0 + threadIdx.x);
+    ops_out[3 + threadIdx.x] = __ldcg(g.ops + threadIdx.x);
+  }
   const uint64_t total = C * g.ct_words;
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t c = x / g.ct_words;

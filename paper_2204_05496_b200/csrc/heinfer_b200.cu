@@ -268,7 +268,11 @@ __global__ void k_narrow(Geo g, const uint64_t* __restrict__ in, uint32_t* __res
   }
 }
 
-__global__ void k_iota(uint64_t* __restrict__ out, uint64_t start, uint64_t n) {
+// Row ids; optionally (snap != nullptr) also the op counters' start snapshot
+// of the call (the first kernel of a one-shot matmul).
+__global__ void k_iota(uint64_t* __restrict__ out, uint64_t start, uint64_t n,
+                       const unsigned long long* ops = nullptr, unsigned long long* snap = nullptr) {
+  if (snap && blockIdx.x == 0 && threadIdx.x < 3) snap[threadIdx.x] = __ldcg(ops + threadIdx.x);
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n; x += (uint64_t)gridDim.x * blockDim.x)
     out[x] = start + x;
 }
@@ -355,8 +359,8 @@ struct hei_gpu_ctx {
   uint32_t t0inv = 0;            // t0^-1 mod t1 (crt_recombine)
   uint32_t* d_err = nullptr;
   unsigned long long* d_ops = nullptr;      // [3] measured op counters (Geo::ops), cumulative
-  unsigned long long* d_opsnap = nullptr;   // [6] one-shot calls: counters at the call's start, then at its end
-  unsigned long long* h_opsnap = nullptr;   // [6] pinned copy of d_opsnap
+  unsigned long long* d_opsnap = nullptr;   // [3] one-shot calls: counters at the call's start (k_iota)
+  unsigned long long* h_opsnap = nullptr;   // [6] mapped pinned: a call's start and end counters (k_finish_add)
   cudaStream_t stream = nullptr;
   uint64_t batch_pairs = 0;
   uint64_t keys_words[2] = {0, 0};
@@ -451,7 +455,7 @@ struct hei_gpu_stream {
   uint64_t* d_stage64 = nullptr;
   uint64_t* d_rows = nullptr;
   uint64_t cap_rows = 0;
-  unsigned long long* d_ops0 = nullptr;  // [6] op counters at creation, then at finish
+  unsigned long long* d_ops0 = nullptr;  // [3] op counters at the stream's start
   bool owns_ops0 = true;
 };
 
@@ -579,11 +583,9 @@ const TwAB* tabs_half_pairs(hei_gpu_ctx* c, const Geo& g, uint32_t gp0, uint32_t
 // the register kernel at 3 CTAs/SM (N = 8192) with parameter-space twiddles.
 void launch_bl_encrypt(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const int8_t* d_noise, const uint32_t* d_m,
                        uint32_t* ct, size_t sm1, cudaStream_t st) {
-  const bool ptw = blocks >= 2u * 148u;
   HEI_DISPATCH(c->logn,
-               (ptw ? k_bl_encrypt<LG, true, (LG <= 13 ? 3 : 1)><<<blocks, Ntt<LG>::T, sm1, st>>>(
-                          g, d_noise, d_m, c->d_pkp, ct, *tabs_of(c, g, 0))
-                    : k_bl_encrypt<LG, false><<<blocks, Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct, TwNone{})),
+               (k_bl_encrypt<LG, true, (LG <= 13 ? 3 : 1)><<<blocks, Ntt<LG>::T, sm1, st>>>(g, d_noise, d_m, c->d_pkp,
+                                                                                           ct, *tabs_of(c, g, 0))),
                (k_bl_encrypt_g<<<blocks, c->threads(), sm1, st>>>(g, d_noise, d_m, c->d_pkp, ct)));
 }
 
@@ -591,18 +593,14 @@ void launch_bl_encrypt(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const int8
 void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* perm,
                        uint32_t* dig, cudaStream_t st) {
   const size_t sm = smem_bytes(c, 1);
-  // big launches take the pass-A/B twiddles as parameters (constant bank);
-  // small ones keep the 25 KB parameter block off the launch path
-  const bool ptw = blocks >= 2u * 148u;
-  if (c->logn == 14 && ptw) {
+  // the pass-A/B twiddles travel as kernel parameters (constant bank)
+  if (c->logn == 14 && blocks >= 2u * 148u) {
     // N = 16384: 2-CTA clusters, one CTA per half of the eval slots (ks_half.cuh)
     k_rot_digits_h<<<2 * blocks, 512, 8192 * 4, st>>>(g, cur, perm, dig);
     LAUNCHED();
     return;
   }
-  HEI_DISPATCH(c->logn,
-               (ptw ? k_rot_digits_f<LG, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1))
-                    : k_rot_digits_f<LG, false><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig, TwNone{})),
+  HEI_DISPATCH(c->logn, (k_rot_digits_f<LG, true><<<blocks, Ntt<LG>::T, sm, st>>>(g, cur, perm, dig, *tabs_of(c, g, 1))),
                (k_rot_digits<<<blocks, c->threads(), sm, st>>>(g, cur, perm, dig)));
   LAUNCHED();
 }
@@ -633,15 +631,12 @@ bool launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const u
                                                                                nullptr, nullptr);
       } else if (big && !next) {
         k_rot_keyswitch_t<<<blocks, Ntt<13>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, *tabs_of(c, g, 0));
-      } else if (big) {
+      } else if (next) {
         k_rot_keyswitch_s<13, true, true><<<blocks, Ntt<13>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
                                                                               perm_next, dig_next, *tabs_of(c, g, 0));
-      } else if (next) {
-        k_rot_keyswitch_s<13, false, true><<<blocks, Ntt<13>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                               perm_next, dig_next, TwNone{});
       } else {
-        k_rot_keyswitch_s<13, false, false><<<blocks, Ntt<13>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                                nullptr, nullptr, TwNone{});
+        k_rot_keyswitch_s<13, true, false><<<blocks, Ntt<13>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                               nullptr, nullptr, *tabs_of(c, g, 0));
       }
       break;
     case 14:
@@ -653,15 +648,12 @@ bool launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const u
                                                                        g.L[b], *tabs_half_pairs(c, g, gp0, g.L[b]));
           if (b == 0) LAUNCHED();
         }
-      } else if (big) {
+      } else if (next) {
         k_rot_keyswitch_s<14, true, true><<<blocks, Ntt<14>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
                                                                               perm_next, dig_next, *tabs_of(c, g, 0));
-      } else if (next) {
-        k_rot_keyswitch_s<14, false, true><<<blocks, Ntt<14>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                               perm_next, dig_next, TwNone{});
       } else {
-        k_rot_keyswitch_s<14, false, false><<<blocks, Ntt<14>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                                nullptr, nullptr, TwNone{});
+        k_rot_keyswitch_s<14, true, false><<<blocks, Ntt<14>::T, 3 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
+                                                                               nullptr, nullptr, *tabs_of(c, g, 0));
       }
       break;
     default:
@@ -752,9 +744,7 @@ void launch_poly_ntt(hei_gpu_ctx* c, unsigned blocks, uint32_t gp, uint32_t* pol
 template <int LG>
 void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_digits_f<LG, true>, sm);
-  set_smem_attr((const void*)k_rot_digits_f<LG, false>, sm);
-  set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, false>, 3 * sm);
-  set_smem_attr((const void*)k_rot_keyswitch_s<LG, false, true>, 3 * sm);
+  set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, false>, 3 * sm);
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
   if constexpr (LG == 13) {
     set_smem_attr((const void*)k_rot_keyswitch_t, sm);
@@ -768,7 +758,6 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_ct_intt_f<LG>, sm);
   set_smem_attr((const void*)k_poly_ntt_f<LG>, sm);
   set_smem_attr((const void*)k_bl_encode<LG>, sm);
-  set_smem_attr((const void*)k_bl_encrypt<LG, false>, sm);
   set_smem_attr((const void*)k_bl_encrypt<LG, true, (LG <= 13 ? 3 : 1)>, sm);
   set_smem_attr((const void*)k_prepare_pk<LG>, sm);
 }
@@ -1018,7 +1007,8 @@ void finish_to(hei_gpu_stream* s, uint32_t* d_out, cudaStream_t st) {
     }
     launch_bias_plain(s, d_bias, st);
   }
-  k_finish_add<<<grid_for(s->C * c->ct_words(), 256), 256, 0, st>>>(c->geo, s->d_acc, s->d_biasp, s->C, d_out);
+  k_finish_add<<<grid_for(s->C * c->ct_words(), 256), 256, 0, st>>>(c->geo, s->d_acc, s->d_biasp, s->C, d_out, s->d_ops0,
+                                                                   c->h_opsnap);
   LAUNCHED();
 }
 
@@ -1072,14 +1062,16 @@ hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64
     s->owns_rows = false;
   }
   if (!ext_acc) CU(cudaMemsetAsync(s->d_acc, 0, s->C * c->ct_words() * 8, zero_on ? zero_on : c->stream));
-  // the counters' start (MatmulStream keeps start_ = be.counters(), matmul.cpp:143)
+  // the counters' start (MatmulStream keeps start_ = be.counters(),
+  // matmul.cpp:143): one-shot calls snapshot them in their first kernel
+  // (k_iota), host-API streams here
   if (host_staging) {
-    CU(cudaMalloc(&s->d_ops0, 6 * 8));
+    CU(cudaMalloc(&s->d_ops0, 3 * 8));
+    CU(cudaMemcpyAsync(s->d_ops0, c->d_ops, 3 * 8, cudaMemcpyDeviceToDevice, c->stream));
   } else {
     s->d_ops0 = c->d_opsnap;
     s->owns_ops0 = false;
   }
-  CU(cudaMemcpyAsync(s->d_ops0, c->d_ops, 3 * 8, cudaMemcpyDeviceToDevice, zero_on ? zero_on : c->stream));
   if (!host_staging && encode_bias) {
     // stage the bias now (pinned, async): every earlier call has synchronised
     const size_t bb = s->bias.size() * 8;
@@ -1107,16 +1099,10 @@ hei_gpu_stream* stream_new(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64
   return s.release();
 }
 
-// The counters at the end of the call (after every counting kernel on `st`
-// and the streams joined into it), copied with the start snapshot to pinned
-// memory; read them with ops_report after `st` is synchronised.
-void ops_end(hei_gpu_stream* s, cudaStream_t st) {
-  hei_gpu_ctx* c = s->ctx;
-  CU(cudaMemcpyAsync(s->d_ops0 + 3, c->d_ops, 3 * 8, cudaMemcpyDeviceToDevice, st));
-  CU(cudaMemcpyAsync(c->h_opsnap, s->d_ops0, 6 * 8, cudaMemcpyDeviceToHost, st));
-}
 // MatmulStream::finish's counters (matmul.cpp:224-229): measured deltas of
-// mul_plain / rotation / add, plus the ciphertext counts.
+// mul_plain / rotation / add (k_finish_add wrote the start and end snapshots
+// to the mapped pinned h_opsnap; read after the call's synchronisation),
+// plus the ciphertext counts.
 void ops_report(hei_gpu_stream* s, hei_op_counters* cnt) {
   const unsigned long long* h = s->ctx->h_opsnap;
   cnt->mul_plain_count = h[3] - h[0];
@@ -1176,7 +1162,6 @@ void stream_finish(hei_gpu_stream* s, uint64_t* out, hei_op_counters* cnt) {
   CU(cudaMalloc(&d_out, words * 4));
   CU(cudaMalloc(&d_out64, words * 8));
   finish_to(s, d_out, c->stream);
-  ops_end(s, c->stream);
   k_widen<<<grid_for(words, 256), 256, 0, c->stream>>>(d_out, d_out64, words);
   LAUNCHED();
   CU(cudaMemcpyAsync(out, d_out64, words * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -1863,10 +1848,10 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     CU(cudaMemcpyAsync(c->d_perms, perms.data(), perms.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     CU(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
-    CU(cudaMalloc(&c->d_ops, 9 * 8));
+    CU(cudaMalloc(&c->d_ops, 6 * 8));
     c->d_opsnap = c->d_ops + 3;
-    CU(cudaMemsetAsync(c->d_ops, 0, 9 * 8, c->stream));
-    CU(cudaMallocHost(&c->h_opsnap, 6 * 8));
+    CU(cudaMemsetAsync(c->d_ops, 0, 6 * 8, c->stream));
+    CU(cudaHostAlloc(&c->h_opsnap, 6 * 8, cudaHostAllocMapped));  // written by k_finish_add (UVA)
     CU(cudaStreamSynchronize(c->stream));
     g.ops = c->d_ops;
     g.fwd = c->d_fwd;
@@ -2570,7 +2555,7 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
       pool_get(c->pool_stage64, c->pool_stage64_bytes, 2 * slot_bytes));
   uint32_t* in32 = pool_get(c->pool_in32, c->pool_in32_bytes, 2 * slot_rows * words * 4);
   uint64_t* d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, rows * 8);
-  k_iota<<<grid_for(rows, 256), 256, 0, st>>>(d_rows, 0, rows);
+  k_iota<<<grid_for(rows, 256), 256, 0, st>>>(d_rows, 0, rows, c->d_ops, s->d_ops0);
   LAUNCHED();
   cudaEvent_t copied[2], narrowed[2];
   for (int k = 0; k < 2; ++k) {
@@ -2655,7 +2640,6 @@ void matmul_host(hei_gpu_ctx* c, const hei_gpu_weights* w, const HostIO& io, uin
   const size_t out_bytes = wire ? s->C * (io.wg.blob[0] + io.wg.blob[1]) : outw * 8;
   uint64_t* d_out64 = pool_get(c->pool_out64, c->pool_out64_bytes, out_bytes);
   finish_to(s.get(), d_out, st);
-  ops_end(s.get(), st);
   if (wire) {
     // save_ciphertext writes canonical coefficient form (serialize.cpp:67-71)
     launch_ct_intt(c, (unsigned)(s->C * 2 * c->P()), d_out, st);
@@ -2770,7 +2754,7 @@ int hei_gpu_matmul_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint32
     std::unique_ptr<hei_gpu_stream, void (*)(hei_gpu_stream*)> s(stream_new(c, w, bias, rows, false, st), stream_free);
     const size_t words = w->kc * c->ct_words();
     uint64_t* d_rows = pool_get(c->pool_rows, c->pool_rows_bytes, rows * 8);
-    k_iota<<<grid_for(rows, 256), 256, 0, st>>>(d_rows, 0, rows);
+    k_iota<<<grid_for(rows, 256), 256, 0, st>>>(d_rows, 0, rows, c->d_ops, s->d_ops0);
     LAUNCHED();
     for (uint64_t r0 = 0; r0 < rows; r0 += s->cap_rows) {
       const uint64_t nr = std::min<uint64_t>(s->cap_rows, rows - r0);
@@ -2778,8 +2762,7 @@ int hei_gpu_matmul_device(hei_gpu_ctx* c, const hei_gpu_weights* w, const uint32
     }
     s->pushed = rows;
     finish_to(s.get(), d_out, st);
-    ops_end(s.get(), st);
-    CU(cudaStreamSynchronize(st));
+      CU(cudaStreamSynchronize(st));
     s->finished = true;
     if (cnt) ops_report(s.get(), cnt);
   });

@@ -82,7 +82,6 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_t(Geo g, const uint32_
   block_pair_prime(g, pair, gp);
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t q = pr.q, L = pr.L, i = pr.i;
-  if (gp == 0) count_ops(g, 0, 1, fold ? 1 : 0);  // one rotation (+ the fold add) per pair (backend.cpp:63-73)
   const uint32_t j = threadIdx.x, x0 = NT::posC0(j), warp = j >> 5;
   const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
   const uint32_t* ct = dot + (uint64_t)pair * g.ct_words;
@@ -219,4 +218,5 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_t(Geo g, const uint32_
     tm_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols) : "memory");
   }
+  if (gp == 0) count_ops(g, 0, 1, fold ? 1 : 0);  // one rotation (+ the fold add) per pair (backend.cpp:63-73)
 }
