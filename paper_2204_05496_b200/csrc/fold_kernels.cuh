@@ -584,15 +584,17 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
     if (l == i) continue;
     {
       const uint32_t* src = dig + (uint64_t)l * N;
+      // only the first stage's u operands (r < 8) must be reduced mod q_i: the
+      // v operands feed a Shoup product, exact for any 32-bit input
       if (pr.fast_reduce) {
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
           const uint32_t v = src[NT::posA(j, r)];
-          e[r] = min(v, v - q);
+          e[r] = r < 8 ? min(v, v - q) : v;
         }
       } else {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
+        for (int r = 0; r < 16; ++r) e[r] = r < 8 ? src[NT::posA(j, r)] % q : src[NT::posA(j, r)];
       }
     }
     if constexpr (PTW)

@@ -66,7 +66,6 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_h(Geo g, const uint32_
   __shared__ uint32_t tbase;
   const uint32_t loc = blockIdx.x >> 1, h = blockIdx.x & 1u;
   const uint32_t pair = loc / np, gp = gp0 + loc % np, row = (loc % np) * 2 + h;
-  if (gp == 0 && h == 0) count_ops(g, 0, 1, fold ? 1 : 0);  // one rotation (+ the fold add) per pair
   const PrimeInfo& pr = g.pr[gp];
   const uint32_t q = pr.q, L = pr.L, i = pr.i;
   const uint32_t j = threadIdx.x, warp = j >> 5;
@@ -190,6 +189,7 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_h(Geo g, const uint32_
     tm_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols) : "memory");
   }
+  if (gp == 0 && h == 0) count_ops(g, 0, 1, fold ? 1 : 0);  // one rotation (+ the fold add) per pair
 }
 
 // N = 16384 digit INTT as a 2-CTA cluster, one CTA per half of the eval

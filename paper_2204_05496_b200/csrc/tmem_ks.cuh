@@ -136,15 +136,17 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_t(Geo g, const uint32_
   for (uint32_t l = 0; l < L; ++l) {
     if (l == i) continue;
     const uint32_t* src = dig + (uint64_t)l * N;
+    // only the first stage's u operands (r < 8) must be reduced mod q_i: the
+    // v operands feed a Shoup product, exact for any 32-bit input
     if (pr.fast_reduce) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const uint32_t v = src[NT::posA(j, r)];
-        e[r] = min(v, v - q);
+        e[r] = r < 8 ? min(v, v - q) : v;
       }
     } else {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
+      for (int r = 0; r < 16; ++r) e[r] = r < 8 ? src[NT::posA(j, r)] % q : src[NT::posA(j, r)];
     }
     NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
