@@ -637,7 +637,8 @@ def run_ours(args, world, rank, local):
 
         x3, w3, b3 = config_workload("c3")
         ew3 = encode_weights(srv, w3)
-        d1 = torch.empty((kc, ctw), dtype=torch.int32, device=dev)
+        kc3 = (x3.shape[1] + n - 1) // n  # the C3 row's chunks (not this config's)
+        d1 = torch.empty((kc3, ctw), dtype=torch.int32, device=dev)
         encode_inputs_device(srv, x3, Prng(2), Prng(3), d1.data_ptr(), stream.cuda_stream)
         o1 = torch.empty((1, ctw), dtype=torch.int32, device=dev)
         for _ in range(3):

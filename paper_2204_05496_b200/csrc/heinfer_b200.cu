@@ -1007,8 +1007,9 @@ void finish_to(hei_gpu_stream* s, uint32_t* d_out, cudaStream_t st) {
     }
     launch_bias_plain(s, d_bias, st);
   }
+  // (streams assembled in place for the sharded finishes keep no counters)
   k_finish_add<<<grid_for(s->C * c->ct_words(), 256), 256, 0, st>>>(c->geo, s->d_acc, s->d_biasp, s->C, d_out, s->d_ops0,
-                                                                   c->h_opsnap);
+                                                                   s->d_ops0 ? c->h_opsnap : nullptr);
   LAUNCHED();
 }
 
