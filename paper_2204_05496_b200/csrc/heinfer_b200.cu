@@ -405,6 +405,7 @@ struct hei_gpu_ctx {
   uint32_t* pool_masks = nullptr;  // latency path: precomputed mask plaintexts
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
+  bool ks_cluster = false;  // HEI_KS_CLUSTER=1: full batches fuse the digit INTT into a cluster key switch
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   bool dot_rows = true;    // HEI_DOT_ROWS=0: per-pair chunk-product kernel for every batch
   bool mask_cache = true;  // HEI_MASK_CACHE=0: regenerate each pair's mask (the reference's N > 4096 behaviour)
@@ -748,6 +749,8 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
   if constexpr (LG == 13) {
     set_smem_attr((const void*)k_rot_keyswitch_t, sm);
+    set_smem_attr((const void*)k_rot_keyswitch_c<6>, 2 * sm);
+    set_smem_attr((const void*)k_rot_keyswitch_c<4>, 2 * sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, true>, 6 * sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, false>, 6 * sm);
   }
@@ -796,6 +799,22 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
       CU(cudaEventCreate(&e1));
       CU(cudaEventCreate(&e2));
       CU(cudaEventRecord(e0, st));
+    }
+    if (c->ks_cluster && c->logn == 13 && blocks >= 2u * 148u && !perm_next && g.L[0] == 6 && g.L[1] == 4) {
+      // digit INTT fused into a cluster key switch per branch (digits stay on chip)
+      if (c->timing) CU(cudaEventRecord(e1, st));
+      const TwAB* tab = tabs_of(c, g, 0);
+      const uint32_t pairs = blocks / g.P;
+      k_rot_keyswitch_c<6><<<pairs * 6, Ntt<13>::T, smem_bytes(c, 2), st>>>(g, cur, perm, k0, other, 1, 0, *tab);
+      LAUNCHED();
+      k_rot_keyswitch_c<4><<<pairs * 4, Ntt<13>::T, smem_bytes(c, 2), st>>>(g, cur, perm, k1, other, 1, 6, *tab);
+      LAUNCHED();
+      if (c->timing) {
+        CU(cudaEventRecord(e2, st));
+        c->fold_ev.push_back({e0, e1, e2});
+      }
+      std::swap(cur, other);
+      continue;
     }
     if (!have_digits) launch_rot_digits(c, g, blocks, cur, perm, dig, st);
     if (c->timing) CU(cudaEventRecord(e1, st));
@@ -1582,6 +1601,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_MT_JUMP")) c->mt_jump = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_DIGITS")) c->fuse_digits = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_KS_CLUSTER")) c->ks_cluster = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_FOLD_PARTS"))

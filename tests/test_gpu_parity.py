@@ -934,15 +934,18 @@ def test_stream_concurrent_push_from_threads(tiny32):
     assert np.array_equal(st.finish(), want)
 
 
-@pytest.mark.parametrize("cts_n", [1, 3, 20, 40, 64])
-def test_fold_paths_bit_exact(prod, cts_n):
+@pytest.mark.parametrize("cts_n,cluster", [(1, "0"), (3, "0"), (20, "0"), (40, "0"), (64, "0"), (64, "1")])
+def test_fold_paths_bit_exact(prod, cts_n, cluster, monkeypatch):
     """sum_all_slots (backend.cpp:63-73) at the launch sizes that select each
     N = 8192 fold path. Below 296 (pair, prime) blocks the per-rotation
     kernels (1 and 3 ciphertexts: the 2-group latency kernel, 20:
     shared-memory accumulators, both with the next digit fused). 40
     ciphertexts (400 blocks): shared-memory kernel with parameter-space
     twiddles, fused; 64 (640 blocks): digit INTT kernel +
-    TMEM-accumulator key switch. Every output equals the oracle's."""
+    TMEM-accumulator key switch, or with HEI_KS_CLUSTER=1 the cluster key
+    switch that keeps the digits on chip (DSMEM). Every output equals the
+    oracle's."""
+    monkeypatch.setenv("HEI_KS_CLUSTER", cluster)
     o, _ = prod
     rng = np.random.default_rng(64 + cts_n)
     x = rng.integers(-9, 9, size=(cts_n, o.n), dtype=np.int64)
