@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
   const uint32_t* c0 = ct + (uint64_t)pr.poly0 * N;
   const uint32_t* c1 = ct + (uint64_t)pr.poly1 * N;
   const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * N;
-  if (grp == 0) {  // the l == i term needs no transform
+  if (grp == 1) {  // the l == i term needs no transform (group 1 has the fewer digits)
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * N) + j;
     const uint4* pp = reinterpret_cast<const uint4*>(perm + x0);
@@ -770,7 +770,26 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
       a1s[c * T + j] = B;
     }
   }
+  // sigma(c0) of thread j's slots: one aligned 16-slot source group, loaded
+  // with 4 x 128-bit loads by group 0's thread j into its column of group
+  // 0's exchange buffer (free once group 0's last transform is done); both
+  // groups' thread j read it after the CTA barrier
+  if (grp == 0) {
+    const uint4* gs4 = reinterpret_cast<const uint4*>(c0 + (__ldg(perm + x0) & ~15u));
+    uint4 g0v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) g0v[c] = __ldg(gs4 + c);
+    NT::sync();  // group 0's transforms no longer read its buffer
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      sm[(4 * c) * T + j] = g0v[c].x;
+      sm[(4 * c + 1) * T + j] = g0v[c].y;
+      sm[(4 * c + 2) * T + j] = g0v[c].z;
+      sm[(4 * c + 3) * T + j] = g0v[c].w;
+    }
+  }
   __syncthreads();  // both groups' accumulators complete; all transforms done
+  const uint32_t* col = reinterpret_cast<const uint32_t*>(smem4);  // group 0's exchange buffer
   uint32_t* o = out + (uint64_t)pair * g.ct_words;
 #pragma unroll
   for (int cc = 0; cc < 2; ++cc) {  // group r finalises chunks {2r, 2r + 1}
@@ -787,10 +806,10 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
     B.y = add_mod(B.y, RB.y, q);
     B.z = add_mod(B.z, RB.z, q);
     B.w = add_mod(B.w, RB.w, q);
-    A.x = add_mod(A.x, c0[pm.x], q);
-    A.y = add_mod(A.y, c0[pm.y], q);
-    A.z = add_mod(A.z, c0[pm.z], q);
-    A.w = add_mod(A.w, c0[pm.w], q);
+    A.x = add_mod(A.x, col[(pm.x & 15u) * T + j], q);
+    A.y = add_mod(A.y, col[(pm.y & 15u) * T + j], q);
+    A.z = add_mod(A.z, col[(pm.z & 15u) * T + j], q);
+    A.w = add_mod(A.w, col[(pm.w & 15u) * T + j], q);
     if (fold) {
       const uint4 u = *reinterpret_cast<const uint4*>(c0 + xc);
       const uint4 v = *reinterpret_cast<const uint4*>(c1 + xc);
