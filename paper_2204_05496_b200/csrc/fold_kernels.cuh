@@ -680,11 +680,27 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
 // SM instead of 16); the groups then finalise half of the slots each and
 // group 1 runs the next rotation's digit INTT. Same arithmetic as
 // k_rot_keyswitch_s.
+#ifdef HEI_W2_TRACE  // debug builds only: per-(block, group) phase timestamps of the latency kernel
+__device__ unsigned long long g_w2_trace[256][2][8];
+#define W2T(k)                                                                                       \
+  do {                                                                                               \
+    if (threadIdx.x % T == 0 && blockIdx.x < 256) {                                                  \
+      unsigned long long t_;                                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+      g_w2_trace[blockIdx.x][grp][k] = t_;                                                           \
+    }                                                                                                \
+  } while (0)
+#else
+#define W2T(k) \
+  do {         \
+  } while (0)
+#endif
 template <int LOGN, bool NEXT>
 __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
     Geo g, const uint32_t* __restrict__ dot, const uint32_t* __restrict__ digits, const uint32_t* __restrict__ perm,
     const uint2* __restrict__ key0, const uint2* __restrict__ key1, uint32_t* __restrict__ out, int fold,
-    const uint32_t* __restrict__ perm_next, uint32_t* __restrict__ dig_next) {
+    const uint32_t* __restrict__ perm_next, uint32_t* __restrict__ dig_next, const uint2* __restrict__ knext0,
+    const uint2* __restrict__ knext1) {
   using NT = Ntt<LOGN, 2>;
   constexpr uint32_t N = NT::N, T = NT::T;
   extern __shared__ uint4 smem4[];
@@ -704,6 +720,13 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
   const uint32_t* c0 = ct + (uint64_t)pr.poly0 * N;
   const uint32_t* c1 = ct + (uint64_t)pr.poly1 * N;
   const uint2* key = (pr.b ? key1 : key0) + (uint64_t)i * L * 2 * N;
+  if (knext0 && pair == 0 && threadIdx.x < 2 * L) {
+    // pull the next rotation's key rows of prime i into L2 (the pairs of an
+    // individual read them ~40 us from now; they would come from HBM)
+    const uint2* kn = (pr.b ? knext1 : knext0) + (uint64_t)i * L * 2 * N + (uint64_t)threadIdx.x * N;
+    bulk_prefetch_l2(kn, N * 8);
+  }
+  W2T(0);
   if (grp == 1) {  // the l == i term needs no transform (group 1 has the fewer digits)
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * N) + j;
@@ -726,6 +749,7 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
       a1s[c * T + j] = make_uint4(0, 0, 0, 0);
     }
   }
+  W2T(1);
   const uint32_t* dig = digits + ((uint64_t)pair * g.P + pr.first) * N;
   const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
   const uint32_t half = L / 2;  // digits (l != i) with index < half go to group 0
@@ -769,6 +793,7 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
       B.w = add_mod(B.w, mul_shoup(e[4 * c + 3], v.z, v.w, q), q);
       a1s[c * T + j] = B;
     }
+    W2T(2 + u);
   }
   // sigma(c0) of thread j's slots: one aligned 16-slot source group, loaded
   // with 4 x 128-bit loads by group 0's thread j into its column of group
@@ -788,6 +813,7 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
       sm[(4 * c + 3) * T + j] = g0v[c].w;
     }
   }
+  W2T(5);
   __syncthreads();  // both groups' accumulators complete; all transforms done
   const uint32_t* col = reinterpret_cast<const uint32_t*>(smem4);  // group 0's exchange buffer
   uint32_t* o = out + (uint64_t)pair * g.ct_words;
@@ -826,6 +852,7 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
     *reinterpret_cast<uint4*>(o + (uint64_t)pr.poly1 * N + xc) = B;
     if constexpr (NEXT) *reinterpret_cast<uint4*>(sm1 + xc) = B;
   }
+  W2T(6);
   if constexpr (NEXT) {
     __syncthreads();  // c1' complete in group 1's buffer
     if (grp == 1) {   // next rotation's digit: INTT of sigma'(c1') mod q_i
@@ -838,6 +865,7 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
       uint32_t* d = dig_next + ((uint64_t)pair * g.P + gp) * N;
 #pragma unroll
       for (int r = 0; r < 16; ++r) d[NT::posA(j, r)] = e[r];
+      W2T(7);
     }
   }
 }

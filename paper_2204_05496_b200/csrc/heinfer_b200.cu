@@ -617,7 +617,8 @@ void launch_rot_digits(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint
 //   other N:   k_rot_keyswitch (generic)
 bool launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const uint32_t* cur, const uint32_t* dig,
                           const uint32_t* perm, const uint2* k0, const uint2* k1, uint32_t* out, int fold,
-                          cudaStream_t st, const uint32_t* perm_next = nullptr, uint32_t* dig_next = nullptr) {
+                          cudaStream_t st, const uint32_t* perm_next = nullptr, uint32_t* dig_next = nullptr,
+                          const uint2* kn0 = nullptr, const uint2* kn1 = nullptr) {
   const bool big = blocks >= 2u * 148u;
   bool next = dig_next != nullptr;
   const size_t sm = smem_bytes(c, 1);
@@ -626,10 +627,10 @@ bool launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const u
       if (blocks <= 148u) {
         if (next)
           k_rot_keyswitch_w2<13, true><<<blocks, 2 * Ntt<13>::T, 6 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                              perm_next, dig_next);
+                                                                              perm_next, dig_next, kn0, kn1);
         else
           k_rot_keyswitch_w2<13, false><<<blocks, 2 * Ntt<13>::T, 6 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                               nullptr, nullptr);
+                                                                               nullptr, nullptr, kn0, kn1);
       } else if (big && !next) {
         k_rot_keyswitch_t<<<blocks, Ntt<13>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, *tabs_of(c, g, 0));
       } else if (next) {
@@ -818,8 +819,14 @@ uint32_t* fold_impl(hei_gpu_ctx* c, uint64_t pairs, uint32_t* cur, uint32_t* oth
     }
     if (!have_digits) launch_rot_digits(c, g, blocks, cur, perm, dig, st);
     if (c->timing) CU(cudaEventRecord(e1, st));
+    const uint2 *kn0 = nullptr, *kn1 = nullptr;  // the next rotation's keys (L2 prefetch on small batches)
+    if (k + 1 < S) {
+      const uint64_t en = c->fold_elts[k + 1];
+      kn0 = c->d_keys[0] + (size_t)c->key_index[0].at(en) * c->L[0] * 2 * c->L[0] * c->n;
+      kn1 = c->d_keys[1] + (size_t)c->key_index[1].at(en) * c->L[1] * 2 * c->L[1] * c->n;
+    }
     have_digits = launch_rot_keyswitch(c, g, blocks, cur, dig, perm, k0, k1, other, 1, st, perm_next,
-                                       perm_next ? dig2 : nullptr);
+                                       perm_next ? dig2 : nullptr, kn0, kn1);
     if (have_digits) std::swap(dig, dig2);
     if (c->timing) {
       CU(cudaEventRecord(e2, st));
@@ -1554,6 +1561,12 @@ extern "C" {
 
 const char* hei_gpu_last_error(void) { return g_err.c_str(); }
 const char* hei_gpu_version(void) { return "heinfer_b200 0.1 (sm_100a)"; }
+#ifdef HEI_W2_TRACE
+// debug builds only: the latency kernel's last phase timestamps [256][2][8]
+int hei_gpu_debug_w2_trace(uint64_t* out) {
+  return cudaMemcpyFromSymbol(out, g_w2_trace, sizeof(g_w2_trace)) == cudaSuccess ? 0 : 8;
+}
+#endif
 uint64_t hei_gpu_launch_count(void) { return g_launches; }
 void hei_gpu_reset_launch_count(void) { g_launches = 0; }
 
