@@ -711,6 +711,10 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
   uint4* o0s = smem4 + (grp ^ 1u) * (3 * N / 4) + N / 4;  // the other group's accumulators
   uint4* o1s = o0s + 4 * T;
   uint32_t* sm1 = reinterpret_cast<uint32_t*>(smem4 + 3 * N / 4);  // group 1's buffer
+  // programmatic dependent launch: the next rotation's grid may be scheduled
+  // now (onto the idle SMs); this grid's inputs are the previous one's outputs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t pair = blockIdx.x / g.P, gp = blockIdx.x % g.P;
   if (gp == 0) count_ops(g, 0, 1, fold ? 1 : 0);  // one rotation (+ the fold add) per pair (backend.cpp:63-73)
   const PrimeInfo& pr = g.pr[gp];

@@ -405,6 +405,7 @@ struct hei_gpu_ctx {
   uint32_t* pool_masks = nullptr;  // latency path: precomputed mask plaintexts
   size_t pool_masks_bytes = 0;
   bool premask = true;  // HEI_PREMASK=0: compute masks inside the accumulation kernel
+  bool pdl = true;      // HEI_PDL=0: latency key switches launch without programmatic dependence
   bool ks_cluster = false;  // HEI_KS_CLUSTER=1: full batches fuse the digit INTT into a cluster key switch
   uint32_t e2e_div = 4;  // HEI_E2E_DIV: host-buffer matmul copies rows in ~rows/div chunks
   bool dot_rows = true;    // HEI_DOT_ROWS=0: per-pair chunk-product kernel for every batch
@@ -625,12 +626,24 @@ bool launch_rot_keyswitch(hei_gpu_ctx* c, const Geo& g, unsigned blocks, const u
   switch (c->logn) {
     case 13:
       if (blocks <= 148u) {
+        // programmatic dependent launch (the kernel waits on its predecessor
+        // with griddepcontrol.wait): the launch overlaps the previous tail
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(blocks);
+        cfg.blockDim = dim3(2 * Ntt<13>::T);
+        cfg.dynamicSmemBytes = 6 * sm;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
         if (next)
-          k_rot_keyswitch_w2<13, true><<<blocks, 2 * Ntt<13>::T, 6 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                              perm_next, dig_next, kn0, kn1);
+          CU(cudaLaunchKernelEx(&cfg, k_rot_keyswitch_w2<13, true>, g, cur, dig, perm, k0, k1, out, fold, perm_next,
+                                dig_next, kn0, kn1));
         else
-          k_rot_keyswitch_w2<13, false><<<blocks, 2 * Ntt<13>::T, 6 * sm, st>>>(g, cur, dig, perm, k0, k1, out, fold,
-                                                                               nullptr, nullptr, kn0, kn1);
+          CU(cudaLaunchKernelEx(&cfg, k_rot_keyswitch_w2<13, false>, g, cur, dig, perm, k0, k1, out, fold,
+                                (const uint32_t*)nullptr, (uint32_t*)nullptr, kn0, kn1));
       } else if (big && !next) {
         k_rot_keyswitch_t<<<blocks, Ntt<13>::T, sm, st>>>(g, cur, dig, perm, k0, k1, out, fold, *tabs_of(c, g, 0));
       } else if (next) {
@@ -1614,6 +1627,7 @@ int hei_gpu_ctx_create(const hei_twin_desc* d, hei_gpu_ctx** out) {
     if (const char* v = std::getenv("HEI_MT_JUMP")) c->mt_jump = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_FUSE_DIGITS")) c->fuse_digits = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_PREMASK")) c->premask = std::atoi(v) != 0;
+    if (const char* v = std::getenv("HEI_PDL")) c->pdl = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_KS_CLUSTER")) c->ks_cluster = std::atoi(v) != 0;
     if (const char* v = std::getenv("HEI_E2E_DIV")) c->e2e_div = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("HEI_MT_CHUNKS")) c->mt_chunks_max = std::max(1, std::atoi(v));
