@@ -735,10 +735,24 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * i + 1) * N) + j;
     const uint4* pp = reinterpret_cast<const uint4*>(perm + x0);
+    {
+      // sigma(c1)_i of the thread's slots: its one aligned 16-slot source
+      // group, 4 x 128-bit loads into its column of the group's buffer
+      const uint4* gs4 = reinterpret_cast<const uint4*>(c1 + (__ldg(perm + x0) & ~15u));
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 v = __ldg(gs4 + c);
+        sm[(4 * c) * T + j] = v.x;
+        sm[(4 * c + 1) * T + j] = v.y;
+        sm[(4 * c + 2) * T + j] = v.z;
+        sm[(4 * c + 3) * T + j] = v.w;
+      }
+    }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const uint4 pm = __ldg(pp + c);
-      const uint32_t d0 = c1[pm.x], d1 = c1[pm.y], d2 = c1[pm.z], d3 = c1[pm.w];
+      const uint32_t d0 = sm[(pm.x & 15u) * T + j], d1 = sm[(pm.y & 15u) * T + j], d2 = sm[(pm.z & 15u) * T + j],
+                     d3 = sm[(pm.w & 15u) * T + j];
       const uint4 a = __ldg(k0 + (2 * c) * T), b = __ldg(k0 + (2 * c + 1) * T);
       const uint4 u = __ldg(k1 + (2 * c) * T), v = __ldg(k1 + (2 * c + 1) * T);
       a0s[c * T + j] = make_uint4(mul_shoup(d0, a.x, a.y, q), mul_shoup(d1, a.z, a.w, q), mul_shoup(d2, b.x, b.y, q),
@@ -817,6 +831,15 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
       sm[(4 * c + 3) * T + j] = g0v[c].w;
     }
   }
+  // the finish's independent loads, issued before the barrier
+  uint4 pmf[2], uf[2], vf[2];
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    const uint32_t xc = x0 + 4 * (2 * grp + cc);
+    pmf[cc] = __ldg(reinterpret_cast<const uint4*>(perm + xc));
+    uf[cc] = *reinterpret_cast<const uint4*>(c0 + xc);
+    vf[cc] = *reinterpret_cast<const uint4*>(c1 + xc);
+  }
   W2T(5);
   __syncthreads();  // both groups' accumulators complete; all transforms done
   const uint32_t* col = reinterpret_cast<const uint32_t*>(smem4);  // group 0's exchange buffer
@@ -825,7 +848,7 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
   for (int cc = 0; cc < 2; ++cc) {  // group r finalises chunks {2r, 2r + 1}
     const int c = 2 * (int)grp + cc;
     const uint32_t xc = x0 + 4 * c;
-    const uint4 pm = __ldg(reinterpret_cast<const uint4*>(perm + xc));
+    const uint4 pm = pmf[cc];
     uint4 A = a0s[c * T + j], B = a1s[c * T + j];
     const uint4 RA = o0s[c * T + j], RB = o1s[c * T + j];
     A.x = add_mod(A.x, RA.x, q);
@@ -841,8 +864,7 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
     A.z = add_mod(A.z, col[(pm.z & 15u) * T + j], q);
     A.w = add_mod(A.w, col[(pm.w & 15u) * T + j], q);
     if (fold) {
-      const uint4 u = *reinterpret_cast<const uint4*>(c0 + xc);
-      const uint4 v = *reinterpret_cast<const uint4*>(c1 + xc);
+      const uint4 u = uf[cc], v = vf[cc];
       A.x = add_mod(A.x, u.x, q);
       A.y = add_mod(A.y, u.y, q);
       A.z = add_mod(A.z, u.z, q);
