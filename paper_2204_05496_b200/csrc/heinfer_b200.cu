@@ -2503,6 +2503,7 @@ int hei_gpu_stream_create(hei_gpu_ctx* c, const hei_gpu_weights* w, const int64_
                           hei_gpu_stream** out) {
   return guarded([&] {
     set_device(c);
+    std::lock_guard<std::mutex> lk(c->mu);  // stream_new enqueues on the context stream
     *out = stream_new(c, w, bias, rows);
   });
 }
