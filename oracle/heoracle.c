@@ -312,7 +312,7 @@ static int ntt_tab_init(ntt_tab* T, uint32_t n, uint64_t q) {
   if (!is_pow2(n) || n < 2) return set_err(ERR_PARAM, "NTT size must be a power of two >= 2");
   if (!ho_is_prime(q)) return set_err(ERR_PARAM, "NTT modulus must be prime");
   if ((q - 1) % (2ull * n)) return set_err(ERR_PARAM, "modulus is not NTT-friendly for this n");
-  uint64_t psi = ho_primitive_root_2n(n, q), psi_inv;
+  uint64_t psi = ho_primitive_root_2n(n, q), psi_inv = 0;
   if (!psi) return set_err(ERR_PARAM, "no primitive root found");
   if (inv_mod(psi, q, &psi_inv)) return ERR_PARAM;
   T->n = n;
@@ -1348,7 +1348,7 @@ int ho_decrypt_signed(ho_twin* h, const uint64_t* ct, int form, int64_t* out, in
   int rc = 0;
   if (b0 <= 0 || b1 <= 0) rc = set_err(ERR_NOISE, "decrypt: invariant noise budget exhausted");
   const uint64_t t0 = h->t[0], t1 = h->t[1];
-  uint64_t inv;
+  uint64_t inv = 0;
   inv_mod(t0 % t1, t1, &inv);
   u128 prod = (u128)t0 * t1;
   for (uint32_t i = 0; i < n; ++i) {
