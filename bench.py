@@ -546,7 +546,8 @@ def run_ours(args, world, rank, local):
         e2e = {"value": world * R / e2e_s, "unit": "inferences/s", "h2d_bytes_per_step": int(h_np.nbytes),
                "d2h_bytes_per_step": int(out.nbytes), "ms_per_step": 1000 * e2e_s}
         if parity is not None:
-            parity["inputs_equal_reference_client"] = sha(h_np) == g.get("inputs_sha256", "")
+            if "inputs_sha256" in g:  # (the streamed C5 golden has no input digest: 32 GB of ciphertexts)
+                parity["inputs_equal_reference_client"] = sha(h_np) == g["inputs_sha256"]
             parity["e2e_packed_equals_reference"] = sha(out) == g["packed_sha256"]
         # the server's wire path (server.cpp:112-172): HECT coeff-form blobs
         # in, HECT blobs out, parse/NTT/INTT/serialize on the device
