@@ -45,6 +45,7 @@ template <int LOGN, int NG = 1>
 struct Ntt {
   static constexpr uint32_t N = 1u << LOGN;
   static constexpr uint32_t T = N / 16;          // threads per polynomial
+  static_assert(T >= 256, "pass-A addressing assumes the swizzle bits (2..7) lie inside j < T");
   static __device__ __forceinline__ uint32_t tid() { return NG == 1 ? threadIdx.x : threadIdx.x % T; }
   static __device__ __forceinline__ void sync() {
     if constexpr (NG == 1)
@@ -156,8 +157,13 @@ struct Ntt {
         if (!(r & half)) ct(e[r], e[r + half], load_tw(tw, (1 << s) + (r >> (4 - s))), q, red(r, half), red(r + half, half));
     }
     if constexpr (LEAD_SYNC) sync();
+    {
+      // swz only reads bits 5..7 and flips bits 2..4, all inside j < T, so
+      // swz(j + T*r) = swz(j) + T*r: one base register, immediate offsets
+      uint32_t* pa = sm + swz(j);
 #pragma unroll
-    for (int r = 0; r < 16; ++r) store_pos(sm, posA(j, r), e[r]);
+      for (int r = 0; r < 16; ++r) pa[T * r] = e[r];
+    }
     sync();
     // ---- pass B: stages 4..7
 #pragma unroll
@@ -309,8 +315,11 @@ struct Ntt {
     for (int r = 0; r < 16; ++r) sm[swz(posB(j, r))] = e[r];
     sync();
     // ---- pass A: stages 3..1, then stage 0 fused with the n^-1 scaling
+    {
+      const uint32_t* pa = sm + swz(j);  // swz(j + T*r) = swz(j) + T*r
 #pragma unroll
-    for (int r = 0; r < 16; ++r) e[r] = sm[swz(posA(j, r))];
+      for (int r = 0; r < 16; ++r) e[r] = pa[T * r];
+    }
 #pragma unroll
     for (int s = 3; s >= 1; --s) {
       const int half = 8 >> s;
