@@ -149,12 +149,16 @@ struct Ntt {
                                              uint32_t q) {
     const uint32_t j = tid();
     // ---- pass A: stages 0..3
+    // (the last stage's outputs stay lazy: pass B knows which of them it uses
+    // as `u` operands and reduces only those, 8 instead of 16)
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int half = 8 >> s;
 #pragma unroll
       for (int r = 0; r < 16; ++r)
-        if (!(r & half)) ct(e[r], e[r + half], load_tw(tw, (1 << s) + (r >> (4 - s))), q, red(r, half), red(r + half, half));
+        if (!(r & half))
+          ct(e[r], e[r + half], load_tw(tw, (1 << s) + (r >> (4 - s))), q, s < 3 && red(r, half),
+             s < 3 && red(r + half, half));
     }
     if constexpr (LEAD_SYNC) sync();
     {
@@ -167,7 +171,10 @@ struct Ntt {
     sync();
     // ---- pass B: stages 4..7
 #pragma unroll
-    for (int r = 0; r < 16; ++r) e[r] = sm[swz(posB(j, r))];
+    for (int r = 0; r < 16; ++r) {
+      const uint32_t v = sm[swz(posB(j, r))];
+      e[r] = r < 8 ? min(v, v - q) : v;  // lazy pass-A outputs: stage 4's u operands are r < 8
+    }
     {
       const uint32_t blk = j >> (LOGN - 8);
 #pragma unroll
@@ -193,17 +200,23 @@ struct Ntt {
       const uint32_t lanebit = t / 16;
       const bool upper = (x0 & t) != 0;
       const uint2 w = entry(tc, PAD + s);
-      // Half exchange: the lower thread keeps pairs 0..7, the upper pairs
-      // 8..15; each does its 8 butterflies locally, then the outputs that
-      // belong to the partner go back (16 shuffles, no redundant products).
+      // Half exchange: each thread of a pair does 8 of the 16 butterflies
+      // locally, then the outputs that belong to the partner go back (16
+      // shuffles, no redundant products). Butterfly k leaves a_k in the lower
+      // thread's e[k] and b_k in the upper's; the next stage pairs e[k] with
+      // e[k + 8], so only butterflies k < 8 need reduced outputs when a
+      // register stage follows. The lower thread takes k = 0..3, 8..11 and the
+      // upper k + 4, so each issues the reductions for just four butterflies.
+      const bool more = s + 1 < XST;  // another cross stage follows: reduce all
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t recv = __shfl_xor_sync(0xffffffffu, upper ? e[k] : e[k + 8], lanebit);
-        uint32_t u = upper ? recv : e[k], v = upper ? e[k + 8] : recv;
-        ct(u, v, w, q);
+      for (int p = 0; p < 8; ++p) {
+        const int kl = p < 4 ? p : p + 4, ku = kl + 4;
+        const uint32_t recv = __shfl_xor_sync(0xffffffffu, upper ? e[kl] : e[ku], lanebit);
+        uint32_t u = upper ? recv : e[kl], v = upper ? e[ku] : recv;
+        ct(u, v, w, q, more || p < 4, more || p < 4);
         const uint32_t back = __shfl_xor_sync(0xffffffffu, upper ? u : v, lanebit);
-        e[k] = upper ? back : u;
-        e[k + 8] = upper ? v : back;
+        e[kl] = upper ? back : u;
+        e[ku] = upper ? v : back;
       }
     }
     {
