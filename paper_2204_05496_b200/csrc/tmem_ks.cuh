@@ -133,6 +133,14 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_t(Geo g, const uint32_
   }
   const uint4* twc = g.twc + (size_t)gp * g.twc_stride;
   uint32_t e[16];
+  const uint32_t lastl = i == L - 1 ? L - 2 : L - 1;  // the last digit besides l == i
+  if (L == 1) {  // no other digit: stage c0 right away
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();
+      bulk_load(sm, c0, N * 4, &gbar);
+    }
+  }
   for (uint32_t l = 0; l < L; ++l) {
     if (l == i) continue;
     const uint32_t* src = dig + (uint64_t)l * N;
@@ -149,6 +157,15 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_t(Geo g, const uint32_
       for (int r = 0; r < 16; ++r) e[r] = r < 8 ? src[NT::posA(j, r)] % q : src[NT::posA(j, r)];
     }
     NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
+    if (l == lastl) {
+      // the last transform's exchange reads are done: stage c0 for the
+      // epilogue now, under this digit's key products
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        fence_proxy_async_smem();
+        bulk_load(sm, c0, N * 4, &gbar);
+      }
+    }
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
     tm_wait_st();  // the previous digit's accumulator stores have landed
@@ -177,10 +194,12 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_t(Geo g, const uint32_
     }
   }
   uint32_t* o = out + (uint64_t)pair * g.ct_words;
-  __syncthreads();  // the last NTT's exchange reads of sm are done
-  if (threadIdx.x == 0) {
-    fence_proxy_async_smem();
-    bulk_load(sm, c0, N * 4, &gbar);
+  // the fold's c1 slots (e is dead: 16 free registers), issued ahead of the
+  // waits on the accumulator stores and the c0 copy
+  uint4 fv[4];
+  if (fold) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) fv[c] = *reinterpret_cast<const uint4*>(c1 + x0 + 4 * c);
   }
   tm_wait_st();
   mbar_wait(&gbar, 1);
@@ -200,7 +219,7 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_t(Geo g, const uint32_
       A[k + 3] = add_mod(A[k + 3], sm[pm.w], q);
       if (fold) {
         const uint4 u = *reinterpret_cast<const uint4*>(sm + x0 + 4 * c);
-        const uint4 v = *reinterpret_cast<const uint4*>(c1 + x0 + 4 * c);
+        const uint4 v = fv[c];
         A[k] = add_mod(A[k], u.x, q);
         A[k + 1] = add_mod(A[k + 1], u.y, q);
         A[k + 2] = add_mod(A[k + 2], u.z, q);
