@@ -161,8 +161,14 @@ class Clocks:
                 for k, nm in enumerate(names):
                     if r[4 + k].lower() == "active":
                         reasons.add(nm)
+        pw = []
+        for r in self.rows:
+            try:
+                pw.append(float(r[2]))
+            except (IndexError, ValueError):
+                pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "power_w": statistics.median(pw) if pw else None}
 
 
 def dist_setup(args):

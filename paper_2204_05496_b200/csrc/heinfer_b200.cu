@@ -763,6 +763,14 @@ void set_fast_attrs(size_t sm) {
   set_smem_attr((const void*)k_rot_keyswitch_s<LG, true, true>, 3 * sm);
   if constexpr (LG == 13) {
     set_smem_attr((const void*)k_rot_keyswitch_t, sm);
+    {
+      // three CTAs of 33 KB fit the 100 KB shared-memory carve-out; the
+      // driver's default picks 132 KB, which leaves L1 32 KB smaller
+      int pct = 43;
+      if (const char* v = std::getenv("HEI_KS_CARVE")) pct = std::atoi(v);
+      if (pct >= 0)
+        CU(cudaFuncSetAttribute((const void*)k_rot_keyswitch_t, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    }
     set_smem_attr((const void*)k_rot_keyswitch_c<6>, 2 * sm);
     set_smem_attr((const void*)k_rot_keyswitch_c<4>, 2 * sm);
     set_smem_attr((const void*)k_rot_keyswitch_w2<LG, true>, 6 * sm);
