@@ -584,18 +584,9 @@ __global__ void __launch_bounds__(Ntt<LOGN>::T, (LOGN <= 13 ? 2 : 1)) k_rot_keys
     if (l == i) continue;
     {
       const uint32_t* src = dig + (uint64_t)l * N;
-      // only the first stage's u operands (r < 8) must be reduced mod q_i: the
-      // v operands feed a Shoup product, exact for any 32-bit input
-      if (pr.fast_reduce) {
+      // (the digit enters unreduced: see k_rot_keyswitch_t)
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const uint32_t v = src[NT::posA(j, r)];
-          e[r] = r < 8 ? min(v, v - q) : v;
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < 16; ++r) e[r] = r < 8 ? src[NT::posA(j, r)] % q : src[NT::posA(j, r)];
-      }
+      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)];
     }
     if constexpr (PTW)
       NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
@@ -781,16 +772,9 @@ __global__ void __launch_bounds__(2 * Ntt<LOGN>::T, 1) k_rot_keyswitch_w2(
   for (uint32_t u = 0; u < cnt; ++u) {
     const uint32_t l = mine[u];
     const uint32_t* src = dig + (uint64_t)l * N;
-    if (pr.fast_reduce) {
+    // (the digit enters unreduced: see k_rot_keyswitch_t)
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const uint32_t v = src[NT::posA(j, r)];
-        e[r] = min(v, v - q);
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)] % q;
-    }
+    for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)];
     NT::template fwd<true>(e, sm, g.fwd + (size_t)gp * N, twc, q);
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;

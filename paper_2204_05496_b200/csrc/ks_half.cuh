@@ -120,14 +120,9 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_h(Geo g, const uint32_
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const uint32_t x = NT::posA(j, r);
-      uint32_t u = src[x], v = src[x + NH];
-      if (pr.fast_reduce) {
-        u = min(u, u - q);
-        v = min(v, v - q);
-      } else {
-        u %= q;
-        v %= q;
-      }
+      // unreduced digit residues (< q_l < 2^31): v feeds a Shoup product, and
+      // u + t, u - t + q stay below q_l + q_i < 2^32 (see k_rot_keyswitch_t)
+      const uint32_t u = src[x], v = src[x + NH];
       const uint32_t t = mul_shoup(v, z1.x, z1.y, q);
       e[r] = h ? sub_mod(u, t, q) : add_mod(u, t, q);
     }

@@ -144,18 +144,13 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_t(Geo g, const uint32_
   for (uint32_t l = 0; l < L; ++l) {
     if (l == i) continue;
     const uint32_t* src = dig + (uint64_t)l * N;
-    // only the first stage's u operands (r < 8) must be reduced mod q_i: the
-    // v operands feed a Shoup product, exact for any 32-bit input
-    if (pr.fast_reduce) {
+    // A digit enters the transform unreduced: its residues are < q_l < 2^31, and
+    // with u < max(q_i, q_l) every butterfly sum stays below q_l + q_i < 2^32, each
+    // conditional subtraction brings it back under max(q_i, q_l), and the lazy
+    // outputs only feed Shoup products (exact for any 32-bit input): congruent
+    // throughout, so the reduced key products are the reference's values.
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const uint32_t v = src[NT::posA(j, r)];
-        e[r] = r < 8 ? min(v, v - q) : v;
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < 16; ++r) e[r] = r < 8 ? src[NT::posA(j, r)] % q : src[NT::posA(j, r)];
-    }
+    for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)];
     NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
     if (l == lastl) {
       // the last transform's exchange reads are done: stage c0 for the
@@ -343,13 +338,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 3)
       e[4 * c + 2] = v.z;
       e[4 * c + 3] = v.w;
     }
-    if (pr.fast_reduce) {
-#pragma unroll
-      for (int r = 0; r < 8; ++r) e[r] = min(e[r], e[r] - q);
-    } else {
-#pragma unroll
-      for (int r = 0; r < 8; ++r) e[r] %= q;
-    }
+    // (the digit enters unreduced, as in k_rot_keyswitch_t)
     NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * N) + j;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * N) + j;
