@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_h(Geo g, const uint32_
       const uint32_t t = mul_shoup(v, z1.x, z1.y, q);
       e[r] = h ? sub_mod(u, t, q) : add_mod(u, t, q);
     }
-    NT::template fwd<true>(e, sm, ParamTw{tab.w[row]}, twc, q);
+    NT::template fwd<true, ParamTw, true, true>(e, sm, ParamTw{tab.w[row]}, twc, q);
     const uint4* k0 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l) * NF) + jf;
     const uint4* k1 = reinterpret_cast<const uint4*>(key + (uint64_t)(2 * l + 1) * NF) + jf;
     tm_wait_st();  // the previous digit's accumulator stores have landed

@@ -137,6 +137,31 @@ struct Ntt {
     }
   }
 
+  // ---- The one cross-thread stage of LOGN = 13 (stage 8, butterflies x,
+  // x + 16 inside each 32-word group) as its own warp-local pass through
+  // shared memory instead of shuffles. A warp's pass-B block is 16 groups of
+  // 32 words; lane (quarter qd, gi, hh) takes group g = 2 gi + (qd & 1) +
+  // 8 (qd >> 1) and the 4-word chunks hh, hh + 2 of its first half (u) with
+  // their partners 16 words up (v): eight butterflies per lane, four of them
+  // (the chunk with offset bit 3 clear) feeding the next stage's `u` operands.
+  // With the swizzle (chunk ^ (g & 7)) the eight lanes of a quarter-warp hit
+  // eight distinct 16-byte bank groups in each 128-bit access.
+  static __device__ __forceinline__ uint32_t x8_base(uint32_t j) {
+    const uint32_t lane = j & 31u, qd = lane >> 3, gi = (lane >> 1) & 3u, hh = lane & 1u;
+    const uint32_t g = 2 * gi + (qd & 1u) + 8 * (qd >> 1);
+    // word offset of chunk hh of group g in the warp's block, swizzled ((x >> 5) & 7 = g & 7 for every word of the group)
+    return (j & ~31u) * 16 + 32 * g + ((4 * hh) ^ ((g & 7u) << 2));
+  }
+  static __device__ __forceinline__ uint32_t x8_group(uint32_t j) {
+    const uint32_t lane = j & 31u, qd = lane >> 3, gi = (lane >> 1) & 3u;
+    return (j >> 5) * 16 + 2 * gi + (qd & 1u) + 8 * (qd >> 1);
+  }
+  // chunk c of the lane: c = 0, 1 -> u chunks hh, hh + 2; c = 2, 3 -> their v partners (+16 words).
+  // (swizzled base ^ 8 flips chunk bit 1: chunk hh -> hh + 2; ^ 16 flips bit 2: +16 words)
+  static __device__ __forceinline__ uint4* x8_ptr(uint32_t* sm, uint32_t b, int c) {
+    return reinterpret_cast<uint4*>(sm + (b ^ ((c & 1) ? 8u : 0u) ^ ((c & 2) ? 16u : 0u)));
+  }
+
   // Forward: e in pass-A order -> e in pass-C order. Begins and ends with a
   // barrier on the shared buffer (sm: N words).
   // LAZY_OUT: leave the final stage's outputs in [0, 2q) (for consumers that
@@ -144,7 +169,14 @@ struct Ntt {
   // LEAD_SYNC = false: the caller guarantees no thread still reads `sm`
   // (e.g. consecutive transforms alternate between two buffers, so the
   // previous reader of this one has since passed two barriers).
-  template <bool LAZY_OUT = false, typename TW = const uint2*, bool LEAD_SYNC = true>
+  // X8_SMEM (LOGN = 13): the cross-thread stage runs as its own warp-local
+  // pass through shared memory (x8_base) instead of the half-exchange
+  // shuffles: ~50 fewer instructions per transform, one more shared-memory
+  // round trip. Pays in the throughput kernels (C4 key switch 3.908 -> 3.855
+  // ms); the latency kernels and the inverse keep the shuffles (the round
+  // trip is on their critical path: C3 0.550 -> 0.567 ms, digits 0.652 ->
+  // 0.666 ms when tried).
+  template <bool LAZY_OUT = false, typename TW = const uint2*, bool LEAD_SYNC = true, bool X8_SMEM = false>
   static __device__ __forceinline__ void fwd(uint32_t (&e)[16], uint32_t* sm, TW tw, const uint4* __restrict__ twc,
                                              uint32_t q) {
     const uint32_t j = tid();
@@ -189,12 +221,33 @@ struct Ntt {
 #pragma unroll
     for (int r = 0; r < 16; ++r) sm[swz(posB(j, r))] = e[r];
     sync_bc();
-    // ---- pass C: stages 8..LOGN-1
-    loadC(sm, j, e);
     const uint32_t x0 = posC0(j);
     const uint4* tc = twc + j;
+    constexpr bool X8 = X8_SMEM && XST == 1;
+    if constexpr (X8) {
+      // ---- stage 8 in its own layout (see x8_base), then back through shared memory
+      const uint32_t b8 = x8_base(j);
+      const uint2 w = lo(__ldg(twc + 2 * x8_group(j)));  // zetas[256 + group]
+      uint4 u0 = *x8_ptr(sm, b8, 0), u1 = *x8_ptr(sm, b8, 1), v0 = *x8_ptr(sm, b8, 2), v1 = *x8_ptr(sm, b8, 3);
+      // chunk hh (offset bit 3 clear): the next stage's u operands -> reduced; chunk hh + 2: its v operands -> lazy
+      ct(u0.x, v0.x, w, q, true, true);
+      ct(u0.y, v0.y, w, q, true, true);
+      ct(u0.z, v0.z, w, q, true, true);
+      ct(u0.w, v0.w, w, q, true, true);
+      ct(u1.x, v1.x, w, q, false, false);
+      ct(u1.y, v1.y, w, q, false, false);
+      ct(u1.z, v1.z, w, q, false, false);
+      ct(u1.w, v1.w, w, q, false, false);
+      *x8_ptr(sm, b8, 0) = u0;
+      *x8_ptr(sm, b8, 1) = u1;
+      *x8_ptr(sm, b8, 2) = v0;
+      *x8_ptr(sm, b8, 3) = v1;
+      __syncwarp();
+    }
+    // ---- pass C: stages 8..LOGN-1
+    loadC(sm, j, e);
 #pragma unroll
-    for (int s = 0; s < XST; ++s) {
+    for (int s = 0; s < (X8 ? 0 : XST); ++s) {
       // stage st = 8 + s, t = G >> (s + 1) >= 16: partner thread h ^ (t / 16)
       const uint32_t t = G >> (s + 1);
       const uint32_t lanebit = t / 16;

@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(512, 3) k_rot_keyswitch_t(Geo g, const uint32_
     // throughout, so the reduced key products are the reference's values.
 #pragma unroll
     for (int r = 0; r < 16; ++r) e[r] = src[NT::posA(j, r)];
-    NT::template fwd<true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
+    NT::template fwd<true, ParamTw, true, true>(e, sm, ParamTw{tab.w[gp]}, twc, q);
     if (l == lastl) {
       // the last transform's exchange reads are done: stage c0 for the
       // epilogue now, under this digit's key products
