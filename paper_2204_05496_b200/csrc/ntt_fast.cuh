@@ -21,7 +21,9 @@
 // The butterflies are the reference's (modops_scalar.cpp:45-81): forward
 // Cooley–Tukey with zetas[m + i] = psi^{bitrev(m + i)}, inverse
 // Gentleman–Sande with inv_zetas and a final n^-1 scaling folded into the
-// last stage. Values stay strictly reduced, so results are bit-identical.
+// last stage. Values stay congruent mod q throughout (lazy ones, < 2q, only
+// ever feed a Shoup product) and the outputs are strictly reduced unless the
+// caller asks for lazy ones, so results are bit-identical.
 #pragma once
 #include "modmath.cuh"
 
