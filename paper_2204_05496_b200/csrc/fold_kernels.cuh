@@ -73,8 +73,12 @@ __global__ void __launch_bounds__(256) k_chunk_dot_rows(Geo g, const uint32_t* _
                                                        const uint2* __restrict__ W, uint32_t cols, uint32_t rows,
                                                        uint32_t* __restrict__ dot) {
   const uint32_t n = g.n, polys = 2 * g.P, tiles = n / 256, groups = (cols + CG - 1) / CG;
-  const uint32_t tile = blockIdx.x % tiles, poly = (blockIdx.x / tiles) % polys, cg = blockIdx.x / (tiles * polys);
-  if (cg >= groups) return;
+  // class groups vary fastest: the blocks that stream the same input slots for
+  // different class groups run side by side, so the rows are read from HBM
+  // once and from L2 by the other groups
+  const uint32_t cg = blockIdx.x % groups, tp = blockIdx.x / groups;
+  if (tp >= tiles * polys) return;
+  const uint32_t tile = tp % tiles, poly = tp / tiles;
   const uint32_t x = tile * 256 + threadIdx.x;
   const uint32_t gp = poly_prime(g, poly);
   const uint32_t q = g.pr[gp].q;
