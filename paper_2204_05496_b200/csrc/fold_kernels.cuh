@@ -91,11 +91,21 @@ __global__ void __launch_bounds__(256) k_chunk_dot_rows(Geo g, const uint32_t* _
     for (int k = 0; k < KC; ++k)
       w[jj][k] = jj < (int)nj ? __ldg(W + ((uint64_t)(j0 + jj) * KC + k) * g.pt_words + (uint64_t)gp * n + x)
                               : make_uint2(0, 0);
-  for (uint32_t s = 0; s < rows; ++s) {
-    const uint32_t* src = in + (uint64_t)s * KC * g.ct_words + (uint64_t)poly * n + x;
-    uint32_t a[KC];
+  // the next row's chunks are in flight while this row's products are formed
+  // (the loop is bound by load latency x rows, not by bandwidth)
+  const uint32_t* src0 = in + (uint64_t)poly * n + x;
+  const uint64_t rstride = (uint64_t)KC * g.ct_words;
+  uint32_t a[KC], an[KC];
 #pragma unroll
-    for (int k = 0; k < KC; ++k) a[k] = __ldg(src + (uint64_t)k * g.ct_words);
+  for (int k = 0; k < KC; ++k) an[k] = __ldg(src0 + (uint64_t)k * g.ct_words);
+  for (uint32_t s = 0; s < rows; ++s) {
+#pragma unroll
+    for (int k = 0; k < KC; ++k) a[k] = an[k];
+    if (s + 1 < rows) {
+      const uint32_t* src = src0 + (uint64_t)(s + 1) * rstride;
+#pragma unroll
+      for (int k = 0; k < KC; ++k) an[k] = __ldg(src + (uint64_t)k * g.ct_words);
+    }
 #pragma unroll
     for (int jj = 0; jj < CG; ++jj) {
       if (jj >= (int)nj) break;
